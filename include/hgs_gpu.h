@@ -1,0 +1,190 @@
+/*
+ * hgs_gpu.h -- C ABI of the B200-native (sm_100a) hybrid 3D/4DGS hot path.
+ *
+ * This is the drop-in boundary: plain pointers, sizes and POD structs, no
+ * torch or CUDA types.  Each entry point names the reference interface it
+ * replaces (paths relative to /root/reference/proj).  INTEGRATION.md shows
+ * the C++ shim (hgs::rasterize etc. over this ABI) and the pybind / ctypes
+ * binding a maintainer of the reference would add.
+ *
+ * Conventions
+ *   - One hgs_ctx per GPU, used by one host thread.  Calls are
+ *     stream-ordered on the context's stream; the "host" entry points
+ *     (hgs_rasterize, hgs_render with host outputs) synchronise before
+ *     returning, the device-resident training entry points do not.
+ *   - Every function returns an hgs_status; on error hgs_last_error(ctx)
+ *     holds a message.  The C++ shim maps statuses back to the reference's
+ *     exception types (errors.hpp:9-33 / std::invalid_argument).
+ *   - There is no CPU fallback: without a usable CUDA device every call that
+ *     needs one returns HGS_ERR_CUDA.
+ *   - Scene buffers follow the reference's per-class layout (scene.hpp:13-59):
+ *     row-major per Gaussian, quaternions (w,x,y,z), SH as K=(deg+1)^2 RGB
+ *     triples.  dtype selects double (HGS_F64, the reference's precision) or
+ *     float (HGS_F32) host arrays.  On the device parameters are FP32 SoA.
+ */
+#ifndef HGS_GPU_H
+#define HGS_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    HGS_OK = 0,
+    HGS_ERR_INVALID_ARGUMENT = 1,    /* std::invalid_argument */
+    HGS_ERR_DEGENERATE_TEMPORAL = 2, /* DegenerateTemporalError */
+    HGS_ERR_DEGENERATE_ROTATION = 3, /* DegenerateRotationError */
+    HGS_ERR_NUMERIC_ABORT = 4,       /* NumericAbort */
+    HGS_ERR_CUDA = 5,                /* no device / launch failure */
+    HGS_ERR_STATE = 6                /* call out of order (e.g. backward before forward) */
+} hgs_status;
+
+enum { HGS_F64 = 0, HGS_F32 = 1 };
+
+typedef struct hgs_ctx hgs_ctx;
+
+/* Host view of a HybridScene (scene.hpp:49-59).  Pointers are double* or
+ * float* according to the dtype argument of the call that takes it. */
+typedef struct {
+    int64_t n4, n3;
+    int32_t sh_degree;
+    double tau, extent;
+    void *mean_x, *mean_t, *ql, *qr, *log_s4, *op4, *sh4; /* dynamics */
+    void *mean3, *quat3, *log_s3, *op3, *sh3;             /* statics  */
+} hgs_host_scene;
+
+/* Camera (camera.hpp:11-16): x_cam = rot * x + trans, rot row-major. */
+typedef struct {
+    double fx, fy, cx, cy;
+    double rot[9];
+    double trans[3];
+    int32_t width, height;
+    double near_, far_;
+} hgs_camera;
+
+/* RenderStats (raster.hpp:33-40), counts identical to the reference. */
+typedef struct {
+    int64_t culled_depth, culled_offscreen, culled_degenerate, culled_temporal,
+        degenerate_temporal, projected;
+} hgs_render_stats;
+
+/* RasterOpts (raster.hpp:42-47); num_threads is accepted and ignored (the
+ * CUDA grid replaces the tile thread pool; output is thread-count invariant
+ * exactly as in the reference). */
+typedef struct {
+    double weight_cutoff;
+    int32_t num_threads;
+    int32_t count_map;
+    int32_t transmittance_map;
+} hgs_raster_opts;
+
+/* LearningRates (train.hpp:13-21) */
+typedef struct {
+    double mean, mean_final_ratio, mean_t, quat, scales, opacity, sh;
+} hgs_lrs;
+
+/* ConversionReport (scene.hpp:38-42) */
+typedef struct {
+    int64_t count;
+    double max_leakage, mean_leakage;
+} hgs_conversion_report;
+
+/* Per-render diagnostics (not in the reference). */
+typedef struct {
+    int64_t visible, instances, fixup_pixels, fp64_splats;
+} hgs_render_info;
+
+/* ---- lifecycle -------------------------------------------------------- */
+hgs_status hgs_ctx_create(int device, hgs_ctx **out);
+void hgs_ctx_destroy(hgs_ctx *ctx);
+const char *hgs_last_error(const hgs_ctx *ctx);
+/* cudaStream_t as void*; NULL = the context's own stream */
+hgs_status hgs_ctx_set_stream(hgs_ctx *ctx, void *stream);
+void *hgs_ctx_stream(hgs_ctx *ctx);
+hgs_status hgs_synchronize(hgs_ctx *ctx);
+
+/* ---- scene (device resident) ------------------------------------------ */
+/* Upload a host scene; resets the optimizer state and gradients. */
+hgs_status hgs_scene_upload(hgs_ctx *ctx, const hgs_host_scene *scene, int dtype);
+/* Download into caller buffers sized for hgs_scene_counts(). */
+hgs_status hgs_scene_download(hgs_ctx *ctx, hgs_host_scene *out, int dtype);
+hgs_status hgs_scene_counts(hgs_ctx *ctx, int64_t *n4, int64_t *n3, int32_t *sh_degree);
+
+/* ---- rendering: rasterize (raster.hpp:79-80) --------------------------- */
+/* Literal drop-in: uploads `scene`, renders, downloads.  rgb_out is an
+ * (h, w, 3) array of dtype; counts/trans are optional (h, w) maps. */
+hgs_status hgs_rasterize(hgs_ctx *ctx, const hgs_host_scene *scene, int dtype, const hgs_camera *cam,
+                         double t, const double bg[3], const hgs_raster_opts *opts, void *rgb_out,
+                         uint32_t *count_out, void *trans_out, hgs_render_stats *stats);
+/* Render the device-resident scene.  Host outputs (any may be NULL). */
+hgs_status hgs_render(hgs_ctx *ctx, const hgs_camera *cam, double t, const double bg[3],
+                      const hgs_raster_opts *opts, float *rgb_host, uint32_t *count_host,
+                      float *trans_host, hgs_render_stats *stats);
+/* Device pointer of the last rendered image (float, h*w*3), valid until the
+ * next render on this context. */
+const float *hgs_last_image_device(hgs_ctx *ctx);
+hgs_status hgs_render_info_get(hgs_ctx *ctx, hgs_render_info *info);
+
+/* ---- differentiable forward / backward (backward.hpp:68-74) ------------ */
+/* forward_train: renders and keeps the (opaque, device) tape. */
+hgs_status hgs_forward_train(hgs_ctx *ctx, const hgs_camera *cam, double t, const double bg[3],
+                             const hgs_raster_opts *opts, float *rgb_host);
+/* backward: dL/dimage (h*w*3, host dtype or device float when on_device),
+ * accumulated as scale * grad into the context's gradient buffer; also
+ * updates the densification statistics (train.cpp:433-444) with the raw
+ * per-image screen-space norms. */
+hgs_status hgs_backward(hgs_ctx *ctx, const void *loss_grad, int dtype, int on_device, double scale);
+hgs_status hgs_zero_grads(hgs_ctx *ctx);
+/* Download gradients in the scene layout (double or float), plus the
+ * screen_norm of the LAST backward call (backward.hpp:20, 30). */
+hgs_status hgs_grads_download(hgs_ctx *ctx, hgs_host_scene *out, int dtype, void *screen_norm4,
+                              void *screen_norm3);
+/* Packed device gradient buffer (for the view-parallel allreduce). */
+hgs_status hgs_grads_device(hgs_ctx *ctx, float **ptr, int64_t *count);
+
+/* ---- loss (loss.hpp:12-13) --------------------------------------------- */
+/* (1-l)*L1 + l*(1-SSIM) of the last rendered image against gt (h*w*3, host
+ * dtype or device float); dL/dimage stays on the device for hgs_backward. */
+hgs_status hgs_loss_with_grad(hgs_ctx *ctx, const void *gt, int dtype, int on_device, double ssim_lambda,
+                              double *loss_out, void *grad_host_out);
+/* Standalone: loss and gradient of two host images. */
+hgs_status hgs_photometric_loss_with_grad(hgs_ctx *ctx, const void *rendered, const void *gt, int dtype,
+                                          int width, int height, double ssim_lambda, double *loss_out,
+                                          void *grad_out);
+
+/* ---- optimizer (train.hpp:68-69) --------------------------------------- */
+hgs_status hgs_adam_step(hgs_ctx *ctx, const hgs_lrs *lrs, double mean_lr_scale, int64_t *skipped_out);
+hgs_status hgs_adam_state_download(hgs_ctx *ctx, hgs_host_scene *m, hgs_host_scene *v, int dtype,
+                                   uint64_t *step);
+hgs_status hgs_adam_state_upload(hgs_ctx *ctx, const hgs_host_scene *m, const hgs_host_scene *v, int dtype,
+                                 uint64_t step);
+hgs_status hgs_stats_download(hgs_ctx *ctx, double *grad_norm4, uint32_t *count4, double *grad_norm3,
+                              uint32_t *count3);
+
+/* ---- conversion (scene.hpp:75 + train.cpp:305-362) --------------------- */
+/* Moves every dynamic Gaussian with exp(s_t) > tau into the static pool
+ * (stable), remaps the Adam rows and resets the densify statistics.
+ * moved_out (optional, capacity n4) receives the converted indices. */
+hgs_status hgs_sweep_convert(hgs_ctx *ctx, int64_t *moved_out, hgs_conversion_report *report);
+
+/* ---- fused training iteration (train.cpp:402-475, one view batch) ------ */
+typedef struct {
+    double ssim_lambda;
+    double weight_cutoff;
+    double mean_lr_scale;
+    hgs_lrs lrs;
+    double bg[3];
+} hgs_train_opts;
+/* B views: render, loss against gt (device float images), backward scaled
+ * by 1/batch_total, and (when apply_adam) one Adam step.  loss_out receives
+ * the summed per-view loss. */
+hgs_status hgs_train_step(hgs_ctx *ctx, int n_views, const hgs_camera *cams, const double *times,
+                          const float *const *gt_device, int batch_total, const hgs_train_opts *opts,
+                          int apply_adam, double *loss_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,335 @@
+"""Python mirror of the reference's render/train surface over the C ABI.
+
+The reference exposes its C++ library to Python as ``hybridgs._core``
+(python/bindings.cpp:35-236): ``rasterize(scene, camera, t, background,
+num_threads, weight_cutoff)`` etc.  The same names and argument meanings are
+provided here, backed by the sm_100a kernels in libhgs_gpu.so; scenes are the
+SoA :class:`~paper_2505_13215_b200.scene.HybridScene`.  Errors map to the
+reference's exception types (``ValueError`` for std::invalid_argument,
+``DegenerateTemporalError`` ...).
+
+:class:`Context` is the device-resident API (one per GPU): the scene, Adam
+state and gradients stay in HBM across calls, which is how the training loop
+uses it.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _capi
+from ._capi import (HGS_F32, HGS_F64, CudaError, DegenerateRotationError, DegenerateTemporalError,  # noqa: F401
+                    HgsError, NumericAbort, StateError, check, ptr)
+from .scene import Camera, HybridScene, sh_coeff_count
+
+DEFAULT_WEIGHT_CUTOFF = 0.05  # raster.hpp:19
+
+
+@dataclass
+class LearningRates:  # train.hpp:13-21
+    mean: float = 1.6e-4
+    mean_final_ratio: float = 0.01
+    mean_t: float = 1.6e-4
+    quat: float = 1e-3
+    scales: float = 5e-3
+    opacity: float = 5e-2
+    sh: float = 2.5e-3
+
+    def struct(self) -> _capi.Lrs:
+        k = _capi.Lrs()
+        for n, _ in _capi.Lrs._fields_:
+            setattr(k, n, getattr(self, n))
+        return k
+
+
+def _host_scene(scene: HybridScene, dtype) -> tuple[_capi.HostScene, list]:
+    hs = _capi.HostScene()
+    hs.n4, hs.n3, hs.sh_degree, hs.tau, hs.extent = scene.n4, scene.n3, scene.sh_degree, scene.tau, scene.extent
+    keep = []
+    for f in HybridScene.DYN_FIELDS + HybridScene.STA_FIELDS:
+        a = np.ascontiguousarray(getattr(scene, f), dtype=dtype)
+        keep.append(a)
+        setattr(hs, f, ptr(a))
+    return hs, keep
+
+
+def _empty_like_scene(n4: int, n3: int, deg: int, dtype) -> HybridScene:
+    K = sh_coeff_count(deg)
+    s = HybridScene(sh_degree=deg)
+    shapes = dict(mean_x=(n4, 3), mean_t=(n4,), ql=(n4, 4), qr=(n4, 4), log_s4=(n4, 4), op4=(n4,), sh4=(n4, K, 3),
+                  mean3=(n3, 3), quat3=(n3, 4), log_s3=(n3, 3), op3=(n3,), sh3=(n3, K, 3))
+    for k, shp in shapes.items():
+        setattr(s, k, np.zeros(shp, dtype=dtype))
+    return s
+
+
+def _opts(weight_cutoff, num_threads=1, count_map=False, transmittance_map=False) -> _capi.RasterOpts:
+    o = _capi.RasterOpts()
+    o.weight_cutoff, o.num_threads = weight_cutoff, num_threads
+    o.count_map, o.transmittance_map = int(bool(count_map)), int(bool(transmittance_map))
+    return o
+
+
+def _dtype_code(dtype) -> int:
+    return HGS_F64 if np.dtype(dtype) == np.float64 else HGS_F32
+
+
+class Context:
+    """One CUDA device: a device-resident scene plus its optimizer state."""
+
+    def __init__(self, device: int = 0):
+        self._lib = _capi.lib()
+        h = C.c_void_p()
+        rc = self._lib.hgs_ctx_create(device, C.byref(h))
+        if rc != 0:
+            raise CudaError(f"hgs_ctx_create(device={device}) failed with status {rc} (no usable CUDA device?)")
+        self._h = h
+        self.device = device
+        self.sh_degree = 1
+        self.n4 = self.n3 = 0
+        self._last_shape = (0, 0)
+
+    # ------------------------------------------------------------ lifecycle
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            self._lib.hgs_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def _check(self, rc: int) -> None:
+        check(self._h, rc)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def synchronize(self) -> None:
+        self._check(self._lib.hgs_synchronize(self._h))
+
+    def set_stream(self, stream_ptr: int | None) -> None:
+        self._check(self._lib.hgs_ctx_set_stream(self._h, C.c_void_p(stream_ptr) if stream_ptr else None))
+
+    # ------------------------------------------------------------ scene
+    def upload(self, scene: HybridScene, dtype=np.float64) -> None:
+        scene.validate_shapes()
+        hs, keep = _host_scene(scene, dtype)
+        self._check(self._lib.hgs_scene_upload(self._h, C.byref(hs), _dtype_code(dtype)))
+        self.sh_degree, self.n4, self.n3 = scene.sh_degree, scene.n4, scene.n3
+        self._meta = (scene.tau, scene.extent, scene.duration_seconds)
+        del keep
+
+    def counts(self) -> tuple[int, int]:
+        n4, n3, deg = C.c_int64(), C.c_int64(), C.c_int32()
+        self._check(self._lib.hgs_scene_counts(self._h, C.byref(n4), C.byref(n3), C.byref(deg)))
+        self.n4, self.n3, self.sh_degree = n4.value, n3.value, deg.value
+        return self.n4, self.n3
+
+    def download(self, dtype=np.float64) -> HybridScene:
+        n4, n3 = self.counts()
+        s = _empty_like_scene(n4, n3, self.sh_degree, dtype)
+        hs, keep = _host_scene(s, dtype)
+        for f in HybridScene.DYN_FIELDS + HybridScene.STA_FIELDS:
+            setattr(s, f, keep[(HybridScene.DYN_FIELDS + HybridScene.STA_FIELDS).index(f)])
+        self._check(self._lib.hgs_scene_download(self._h, C.byref(hs), _dtype_code(dtype)))
+        s.tau, s.extent = hs.tau, hs.extent
+        return s
+
+    # ------------------------------------------------------------ render
+    def render(self, camera: Camera, t: float, background=(0.0, 0.0, 0.0), weight_cutoff=DEFAULT_WEIGHT_CUTOFF,
+               count_map=False, transmittance_map=False) -> dict:
+        H, W = camera.height, camera.width
+        rgb = np.empty((H, W, 3), dtype=np.float32)
+        counts = np.empty((H, W), dtype=np.uint32) if count_map else None
+        trans = np.empty((H, W), dtype=np.float32) if transmittance_map else None
+        st = _capi.RenderStats()
+        bg = np.ascontiguousarray(background, dtype=np.float64)
+        o = _opts(weight_cutoff, 1, count_map, transmittance_map)
+        self._check(self._lib.hgs_render(self._h, C.byref(_capi.camera_struct(camera)), float(t),
+                                         bg.ctypes.data_as(_capi._dp), C.byref(o),
+                                         rgb.ctypes.data_as(_capi._fp),
+                                         counts.ctypes.data_as(_capi._u32p) if counts is not None else None,
+                                         trans.ctypes.data_as(_capi._fp) if trans is not None else None,
+                                         C.byref(st)))
+        self._last_shape = (H, W)
+        return {"rgb": rgb, "counts": counts, "transmittance": trans,
+                "stats": {n: int(getattr(st, n)) for n, _ in _capi.RenderStats._fields_}}
+
+    def render_info(self) -> dict:
+        info = _capi.RenderInfo()
+        self._check(self._lib.hgs_render_info_get(self._h, C.byref(info)))
+        return {n: int(getattr(info, n)) for n, _ in _capi.RenderInfo._fields_}
+
+    def last_image_device_ptr(self) -> int:
+        return int(self._lib.hgs_last_image_device(self._h) or 0)
+
+    # ------------------------------------------------------------ parity introspection
+    def debug_splats(self) -> dict:
+        n = C.c_int64()
+        self._check(self._lib.hgs_debug_splats(self._h, None, None, None, None, None, None, None, 0, C.byref(n)))
+        V = n.value
+        out = dict(gid=np.zeros(V, np.int32), depth_bits=np.zeros(V, np.uint32), box=np.zeros((V, 4), np.int32),
+                   mean=np.zeros((V, 2)), conic=np.zeros((V, 4)), alpha=np.zeros(V), rgb=np.zeros((V, 3), np.float32))
+        if V:
+            self._check(self._lib.hgs_debug_splats(
+                self._h, out["gid"].ctypes.data_as(_capi._i32p), out["depth_bits"].ctypes.data_as(_capi._u32p),
+                out["box"].ctypes.data_as(_capi._i32p), out["mean"].ctypes.data_as(_capi._dp),
+                out["conic"].ctypes.data_as(_capi._dp), out["alpha"].ctypes.data_as(_capi._dp),
+                out["rgb"].ctypes.data_as(_capi._fp), V, C.byref(n)))
+        return out
+
+    def debug_instances(self) -> tuple[np.ndarray, np.ndarray]:
+        n = C.c_int64()
+        self._check(self._lib.hgs_debug_instances(self._h, None, None, 0, C.byref(n)))
+        tile = np.zeros(n.value, np.uint32)
+        gid = np.zeros(n.value, np.uint32)
+        if n.value:
+            self._check(self._lib.hgs_debug_instances(self._h, tile.ctypes.data_as(_capi._u32p),
+                                                      gid.ctypes.data_as(_capi._u32p), n.value, C.byref(n)))
+        return tile, gid
+
+    # ------------------------------------------------------------ training
+    def forward_train(self, camera: Camera, t: float, background=(0.0, 0.0, 0.0),
+                      weight_cutoff=DEFAULT_WEIGHT_CUTOFF, want_image=True) -> np.ndarray | None:
+        H, W = camera.height, camera.width
+        rgb = np.empty((H, W, 3), dtype=np.float32) if want_image else None
+        bg = np.ascontiguousarray(background, dtype=np.float64)
+        o = _opts(weight_cutoff)
+        self._check(self._lib.hgs_forward_train(self._h, C.byref(_capi.camera_struct(camera)), float(t),
+                                                bg.ctypes.data_as(_capi._dp), C.byref(o),
+                                                rgb.ctypes.data_as(_capi._fp) if rgb is not None else None))
+        self._last_shape = (H, W)
+        return rgb
+
+    def backward(self, loss_grad: np.ndarray | None = None, scale: float = 1.0) -> None:
+        """Accumulate scale * dL/dparams; loss_grad None = use the device
+        gradient left by :meth:`loss_with_grad`."""
+        if loss_grad is None:
+            self._check(self._lib.hgs_backward(self._h, None, HGS_F32, 1, float(scale)))
+            return
+        g = np.ascontiguousarray(loss_grad)
+        code = _dtype_code(g.dtype)
+        g = g.astype(np.float64 if code == HGS_F64 else np.float32, copy=False)
+        self._check(self._lib.hgs_backward(self._h, ptr(g), code, 0, float(scale)))
+
+    def zero_grads(self) -> None:
+        self._check(self._lib.hgs_zero_grads(self._h))
+
+    def grads(self, dtype=np.float64) -> dict:
+        n4, n3 = self.counts()
+        s = _empty_like_scene(n4, n3, self.sh_degree, dtype)
+        hs, keep = _host_scene(s, dtype)
+        sn4 = np.zeros(n4, dtype=dtype)
+        sn3 = np.zeros(n3, dtype=dtype)
+        self._check(self._lib.hgs_grads_download(self._h, C.byref(hs), _dtype_code(dtype), ptr(sn4), ptr(sn3)))
+        out = {f: keep[i] for i, f in enumerate(HybridScene.DYN_FIELDS + HybridScene.STA_FIELDS)}
+        out["screen_norm4"], out["screen_norm3"] = sn4, sn3
+        return out
+
+    def grads_device(self) -> tuple[int, int]:
+        p = _capi._fp()
+        n = C.c_int64()
+        self._check(self._lib.hgs_grads_device(self._h, C.byref(p), C.byref(n)))
+        return C.cast(p, C.c_void_p).value or 0, n.value
+
+    def loss_with_grad(self, gt: np.ndarray | None = None, ssim_lambda: float = 0.2, gt_device_ptr: int | None = None,
+                       want_grad: bool = False):
+        g_out = np.empty(self._last_shape + (3,), dtype=np.float32) if want_grad else None
+        loss = C.c_double()
+        if gt_device_ptr is not None:
+            self._check(self._lib.hgs_loss_with_grad(self._h, C.c_void_p(gt_device_ptr), HGS_F32, 1,
+                                                     float(ssim_lambda), C.byref(loss), ptr(g_out)))
+        else:
+            a = np.ascontiguousarray(gt)
+            code = _dtype_code(a.dtype)
+            a = a.astype(np.float64 if code == HGS_F64 else np.float32, copy=False)
+            self._check(self._lib.hgs_loss_with_grad(self._h, ptr(a), code, 0, float(ssim_lambda), C.byref(loss),
+                                                     ptr(g_out)))
+        return (loss.value, g_out) if want_grad else loss.value
+
+    def adam_step(self, lrs: LearningRates | None = None, mean_lr_scale: float = 1.0) -> int:
+        sk = C.c_int64()
+        self._check(self._lib.hgs_adam_step(self._h, C.byref((lrs or LearningRates()).struct()),
+                                            float(mean_lr_scale), C.byref(sk)))
+        return sk.value
+
+    def adam_state(self, dtype=np.float64):
+        n4, n3 = self.counts()
+        m = _empty_like_scene(n4, n3, self.sh_degree, dtype)
+        v = _empty_like_scene(n4, n3, self.sh_degree, dtype)
+        hm, km = _host_scene(m, dtype)
+        hv, kv = _host_scene(v, dtype)
+        step = C.c_uint64()
+        self._check(self._lib.hgs_adam_state_download(self._h, C.byref(hm), C.byref(hv), _dtype_code(dtype),
+                                                      C.byref(step)))
+        F = HybridScene.DYN_FIELDS + HybridScene.STA_FIELDS
+        for i, f in enumerate(F):
+            setattr(m, f, km[i])
+            setattr(v, f, kv[i])
+        return m, v, step.value
+
+    def set_adam_state(self, m: HybridScene, v: HybridScene, step: int, dtype=np.float64) -> None:
+        hm, km = _host_scene(m, dtype)
+        hv, kv = _host_scene(v, dtype)
+        self._check(self._lib.hgs_adam_state_upload(self._h, C.byref(hm), C.byref(hv), _dtype_code(dtype), step))
+
+    def densify_stats(self):
+        n4, n3 = self.counts()
+        gn4, gn3 = np.zeros(n4), np.zeros(n3)
+        c4, c3 = np.zeros(n4, np.uint32), np.zeros(n3, np.uint32)
+        self._check(self._lib.hgs_stats_download(self._h, gn4.ctypes.data_as(_capi._dp),
+                                                 c4.ctypes.data_as(_capi._u32p), gn3.ctypes.data_as(_capi._dp),
+                                                 c3.ctypes.data_as(_capi._u32p)))
+        return gn4, c4, gn3, c3
+
+    def sweep_convert(self):
+        n4, _ = self.counts()
+        moved = np.zeros(max(n4, 1), dtype=np.int64)
+        rep = _capi.ConversionReport()
+        self._check(self._lib.hgs_sweep_convert(self._h, moved.ctypes.data_as(_capi._i64p), C.byref(rep)))
+        self.counts()
+        return moved[: rep.count].copy(), {"count": int(rep.count), "max_leakage": rep.max_leakage,
+                                           "mean_leakage": rep.mean_leakage}
+
+
+_default_ctx: Context | None = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(0)
+    return _default_ctx
+
+
+def rasterize(scene: HybridScene, camera: Camera, t: float, background=(0.0, 0.0, 0.0), num_threads: int = 1,
+              weight_cutoff: float = DEFAULT_WEIGHT_CUTOFF, count_map: bool = False,
+              transmittance_map: bool = False, full: bool = False):
+    """hybridgs.rasterize (bindings.cpp:147-155): (h, w, 3) float64 image.
+
+    Literal drop-in (host scene in, host image out) through hgs_rasterize.
+    ``full=True`` returns the RenderOutput-like dict with counts/transmittance
+    and RenderStats (raster.hpp:49-54).
+    """
+    ctx = default_context()
+    hs, keep = _host_scene(scene, np.float64)
+    H, W = camera.height, camera.width
+    rgb = np.empty((H, W, 3), dtype=np.float64)
+    counts = np.empty((H, W), dtype=np.uint32) if count_map else None
+    trans = np.empty((H, W), dtype=np.float64) if transmittance_map else None
+    st = _capi.RenderStats()
+    bg = np.ascontiguousarray(background, dtype=np.float64)
+    o = _opts(weight_cutoff, num_threads, count_map, transmittance_map)
+    ctx._check(ctx._lib.hgs_rasterize(ctx.handle, C.byref(hs), HGS_F64, C.byref(_capi.camera_struct(camera)),
+                                      float(t), bg.ctypes.data_as(_capi._dp), C.byref(o), ptr(rgb),
+                                      counts.ctypes.data_as(_capi._u32p) if counts is not None else None,
+                                      ptr(trans), C.byref(st)))
+    ctx.sh_degree, ctx.n4, ctx.n3 = scene.sh_degree, scene.n4, scene.n3
+    del keep
+    if not full:
+        return rgb
+    return {"rgb": rgb, "counts": counts, "transmittance": trans,
+            "stats": {n: int(getattr(st, n)) for n, _ in _capi.RenderStats._fields_}}

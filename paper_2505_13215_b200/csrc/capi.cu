@@ -1,0 +1,589 @@
+// capi.cu -- the C ABI (include/hgs_gpu.h): context, scene residency, and
+// the render pipeline orchestration.  Host code here is compiled with
+// -ffp-contract=off: the camera position and the conversion threshold it
+// computes must round exactly like the oracle's.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "ctx.cuh"
+#include "kernels.cuh"
+#include "primitives.cuh"
+#include "train_api.cuh"
+
+using namespace hgs;
+
+namespace {
+
+struct Counters {
+    unsigned long long stats[kNumStats];
+    uint32_t flags;
+    uint32_t V;
+    uint32_t I;
+    uint32_t fix_count;
+    uint32_t skipped;
+    uint32_t pad[3];
+};
+
+hgs_status fail(hgs_ctx* ctx, hgs_status s, const std::string& m) {
+    if (ctx) ctx->err = m;
+    return s;
+}
+
+#define CK(x)                                                                                   \
+    do {                                                                                        \
+        cudaError_t e_ = (x);                                                                   \
+        if (e_ != cudaSuccess)                                                                  \
+            return fail(ctx, HGS_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_));    \
+    } while (0)
+
+#define CKL()                                                                                   \
+    do {                                                                                        \
+        cudaError_t e_ = cudaGetLastError();                                                    \
+        if (e_ != cudaSuccess)                                                                  \
+            return fail(ctx, HGS_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e_)); \
+    } while (0)
+
+int64_t round_cap(int64_t n) { return ((n + 127) / 128) * 128 + 128; }
+
+// ---------------------------------------------------------------- layout
+struct FieldMap {
+    size_t off;  // offsetof in hgs_host_scene
+    int dim;     // components per Gaussian (-1 = 3K SH)
+    int row;     // first SoA row
+};
+const FieldMap kDyn[] = {
+    {offsetof(hgs_host_scene, mean_x), 3, R4_MEAN}, {offsetof(hgs_host_scene, mean_t), 1, R4_MT},
+    {offsetof(hgs_host_scene, ql), 4, R4_QL},       {offsetof(hgs_host_scene, qr), 4, R4_QR},
+    {offsetof(hgs_host_scene, log_s4), 4, R4_LS},   {offsetof(hgs_host_scene, op4), 1, R4_OP},
+    {offsetof(hgs_host_scene, sh4), -1, R4_SH},
+};
+const FieldMap kSta[] = {
+    {offsetof(hgs_host_scene, mean3), 3, R3_MEAN}, {offsetof(hgs_host_scene, quat3), 4, R3_Q},
+    {offsetof(hgs_host_scene, log_s3), 3, R3_LS},  {offsetof(hgs_host_scene, op3), 1, R3_OP},
+    {offsetof(hgs_host_scene, sh3), -1, R3_SH},
+};
+
+void* field_ptr(const hgs_host_scene* s, const FieldMap& f) {
+    return *reinterpret_cast<void* const*>(reinterpret_cast<const char*>(s) + f.off);
+}
+
+template <typename T>
+__global__ void aos_to_soa_kernel(const T* __restrict__ src, int64_t n, int d, float* __restrict__ dst, int64_t cap,
+                                  int row0) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n * d) return;
+    const int64_t i = e / d;
+    const int k = (int)(e - i * d);
+    dst[(int64_t)(row0 + k) * cap + i] = (float)src[e];
+}
+
+template <typename T>
+__global__ void soa_to_aos_kernel(const float* __restrict__ src, int64_t n, int d, int64_t cap, int row0,
+                                  T* __restrict__ dst) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n * d) return;
+    const int64_t i = e / d;
+    const int k = (int)(e - i * d);
+    dst[e] = (T)src[(int64_t)(row0 + k) * cap + i];
+}
+
+// Host -> device SoA rows for one pool.
+hgs_status upload_pool(hgs_ctx* ctx, const hgs_host_scene* s, const FieldMap* fm, int nf, int64_t n, int64_t cap,
+                       float* dst, int dtype) {
+    const int K3 = 3 * sh_count(ctx->deg);
+    const size_t esz = dtype == HGS_F64 ? 8 : 4;
+    for (int f = 0; f < nf; ++f) {
+        const int d = fm[f].dim < 0 ? K3 : fm[f].dim;
+        const void* src = field_ptr(s, fm[f]);
+        if (n == 0) continue;
+        if (!src) return fail(ctx, HGS_ERR_INVALID_ARGUMENT, "scene upload: null field pointer");
+        const size_t bytes = (size_t)n * d * esz;
+        CK(ctx->stage.ensure(bytes));
+        CK(cudaMemcpyAsync(ctx->stage.p, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+        const int64_t tot = n * d;
+        const int blocks = (int)((tot + 255) / 256);
+        if (dtype == HGS_F64)
+            aos_to_soa_kernel<double><<<blocks, 256, 0, ctx->stream>>>(ctx->stage.as<double>(), n, d, dst, cap,
+                                                                      fm[f].row);
+        else
+            aos_to_soa_kernel<float><<<blocks, 256, 0, ctx->stream>>>(ctx->stage.as<float>(), n, d, dst, cap,
+                                                                     fm[f].row);
+        CKL();
+    }
+    return HGS_OK;
+}
+
+hgs_status download_pool(hgs_ctx* ctx, hgs_host_scene* s, const FieldMap* fm, int nf, int64_t n, int64_t cap,
+                         const float* src, int dtype) {
+    const int K3 = 3 * sh_count(ctx->deg);
+    const size_t esz = dtype == HGS_F64 ? 8 : 4;
+    for (int f = 0; f < nf; ++f) {
+        const int d = fm[f].dim < 0 ? K3 : fm[f].dim;
+        void* dst = field_ptr(s, fm[f]);
+        if (n == 0 || !dst) continue;
+        const size_t bytes = (size_t)n * d * esz;
+        CK(ctx->stage.ensure(bytes));
+        const int64_t tot = n * d;
+        const int blocks = (int)((tot + 255) / 256);
+        if (dtype == HGS_F64)
+            soa_to_aos_kernel<double><<<blocks, 256, 0, ctx->stream>>>(src, n, d, cap, fm[f].row,
+                                                                      ctx->stage.as<double>());
+        else
+            soa_to_aos_kernel<float><<<blocks, 256, 0, ctx->stream>>>(src, n, d, cap, fm[f].row,
+                                                                     ctx->stage.as<float>());
+        CKL();
+        CK(cudaMemcpyAsync(dst, ctx->stage.p, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    }
+    return HGS_OK;
+}
+
+// camera.hpp:21-26 Camera::validate
+bool camera_valid(const hgs_camera* c, std::string& why) {
+    if (!(c->fx > 0.0 && c->fy > 0.0)) return why = "Camera: fx, fy must be positive", false;
+    if (!(0.0 < c->near_ && c->near_ < c->far_)) return why = "Camera: need 0 < near < far", false;
+    if (c->width <= 0 || c->height <= 0) return why = "Camera: bad image dimensions", false;
+    if (c->width > 32767 || c->height > 32767) return why = "Camera: image dimensions above 32767", false;
+    const double* R = c->rot;
+    double worst = 0.0;
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+            double s = R[0 * 3 + i] * R[0 * 3 + j];
+            s = s + R[1 * 3 + i] * R[1 * 3 + j];
+            s = s + R[2 * 3 + i] * R[2 * 3 + j];
+            worst = std::fmax(worst, std::fabs(s - (i == j ? 1.0 : 0.0)));
+        }
+    const double det = R[0] * (R[4] * R[8] - R[5] * R[7]) - R[1] * (R[3] * R[8] - R[5] * R[6]) +
+                       R[2] * (R[3] * R[7] - R[4] * R[6]);
+    if (!(worst <= 1e-8 && std::fabs(det - 1.0) <= 1e-8)) return why = "Camera: rotation not orthonormal", false;
+    return true;
+}
+
+DevCamera to_dev(const hgs_camera* c) {
+    DevCamera d;
+    d.fx = c->fx;
+    d.fy = c->fy;
+    d.cx = c->cx;
+    d.cy = c->cy;
+    for (int i = 0; i < 9; ++i) d.R[i] = c->rot[i];
+    for (int i = 0; i < 3; ++i) d.t[i] = c->trans[i];
+    for (int i = 0; i < 3; ++i) {  // camera.hpp:19 position() = -R^T t
+        double s = (-c->rot[0 * 3 + i]) * c->trans[0];
+        s = s + (-c->rot[1 * 3 + i]) * c->trans[1];
+        s = s + (-c->rot[2 * 3 + i]) * c->trans[2];
+        d.pos[i] = s;
+    }
+    d.width = c->width;
+    d.height = c->height;
+    d.near_ = c->near_;
+    d.far_ = c->far_;
+    return d;
+}
+
+__global__ void visflag_kernel(const uint32_t* __restrict__ ntiles, int n, uint32_t* __restrict__ flag) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) flag[i] = ntiles[i] > 0u ? 1u : 0u;
+}
+
+__global__ void compact_kernel(const uint32_t* __restrict__ ntiles, const uint32_t* __restrict__ pos,
+                               const uint32_t* __restrict__ depth_key, int n, uint32_t* __restrict__ keys,
+                               uint32_t* __restrict__ vals) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n && ntiles[i] > 0u) {
+        const uint32_t p = pos[i];
+        keys[p] = depth_key[i];
+        vals[p] = (uint32_t)i;
+    }
+}
+
+hgs_status check_flags(hgs_ctx* ctx, uint32_t flags) {
+    if (flags & FLAG_NONUNIT_QUAT) return fail(ctx, HGS_ERR_INVALID_ARGUMENT, "quat_to_rot3: non-unit quaternion");
+    if (flags & FLAG_INDEFINITE)
+        return fail(ctx, HGS_ERR_INVALID_ARGUMENT, "clamp_psd: matrix is indefinite beyond rounding tolerance");
+    if (flags & FLAG_NONUNIT_DIR) return fail(ctx, HGS_ERR_INVALID_ARGUMENT, "eval_sh: view direction must be unit");
+    if (flags & FLAG_DEGENERATE_ROT)
+        return fail(ctx, HGS_ERR_DEGENERATE_ROTATION, "extract_spatial_rot: spatial block is singular");
+    if (flags & FLAG_NOT_ROTATION)
+        return fail(ctx, HGS_ERR_INVALID_ARGUMENT, "rot3_to_quat: input is not a rotation matrix");
+    return HGS_OK;
+}
+
+}  // namespace
+
+// ====================================================================== render
+// The full K1 -> sort -> K2 -> sort -> K4 pipeline; leaves the tape in ctx.
+hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, const double bg[3],
+                               const hgs_raster_opts* opts) {
+    std::string why;
+    if (!camera_valid(cam, why)) return fail(ctx, HGS_ERR_INVALID_ARGUMENT, why);
+    const double cutoff = opts ? opts->weight_cutoff : 0.05;
+    const bool want_count = opts && opts->count_map;
+    const bool want_trans = opts && opts->transmittance_map;
+    cudaStream_t st = ctx->stream;
+    ctx->have_tape = false;
+    const int n4 = (int)ctx->n4, n3 = (int)ctx->n3, N = n4 + n3;
+    const int W = cam->width, H = cam->height;
+    const int tiles_x = (W + kTile - 1) / kTile, tiles_y = (H + kTile - 1) / kTile;
+    const int n_tiles = tiles_x * tiles_y;
+    ctx->W = W;
+    ctx->H = H;
+    ctx->tiles_x = tiles_x;
+    ctx->tiles_y = tiles_y;
+    ctx->cam = to_dev(cam);
+    ctx->t = t;
+    for (int c = 0; c < 3; ++c) ctx->bg[c] = bg[c];
+
+    const size_t npx = (size_t)W * H;
+    CK(ctx->counters.ensure(sizeof(Counters)));
+    CK(ctx->pinned.ensure(sizeof(Counters) + 64));
+    Counters* dc = ctx->counters.as<Counters>();
+    Counters* hc = static_cast<Counters*>(ctx->pinned.p);
+    CK(cudaMemsetAsync(dc, 0, sizeof(Counters), st));
+    CK(ctx->img.ensure(npx * 3 * sizeof(float)));
+    CK(ctx->last.ensure(npx * sizeof(uint32_t)));
+    CK(ctx->fix_list.ensure(npx * sizeof(uint32_t)));
+    if (want_trans) CK(ctx->trans.ensure(npx * sizeof(float)));
+    if (want_count) CK(ctx->count.ensure(npx * sizeof(uint32_t)));
+    CK(ctx->ranges.ensure((size_t)n_tiles * sizeof(uint2)));
+    CK(cudaMemsetAsync(ctx->ranges.p, 0, (size_t)n_tiles * sizeof(uint2), st));
+
+    int64_t V = 0, I = 0;
+    if (N > 0) {
+        CK(ctx->rec.ensure((size_t)N * sizeof(SplatRec)));
+        CK(ctx->depth_key.ensure((size_t)N * 4));
+        CK(ctx->ntiles.ensure((size_t)N * 4));
+        CK(ctx->visflag.ensure((size_t)N * 4));
+        CK(ctx->vispos.ensure((size_t)N * 4));
+        CK(ctx->scan_ws.ensure(scan_workspace_bytes(N) + 4096));
+        preprocess_kernel<<<div_up(N, 256), 256, 0, st>>>(
+            ctx->p4.as<float>(), ctx->cap4, n4, ctx->p3.as<float>(), ctx->cap3, n3, ctx->deg, ctx->cam, t, cutoff,
+            tiles_x, ctx->rec.as<SplatRec>(), ctx->depth_key.as<uint32_t>(), ctx->ntiles.as<uint32_t>(), dc->stats,
+            &dc->flags);
+        CKL();
+        visflag_kernel<<<div_up(N, 256), 256, 0, st>>>(ctx->ntiles.as<uint32_t>(), N, ctx->visflag.as<uint32_t>());
+        exclusive_scan_u32(ctx->visflag.as<uint32_t>(), ctx->vispos.as<uint32_t>(), N, &dc->V,
+                           ctx->scan_ws.as<uint32_t>(), st);
+        CKL();
+        CK(cudaMemcpyAsync(hc, dc, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        V = hc->V;
+    }
+    if (V > 0) {
+        CK(ctx->sort_k.ensure((size_t)V * 4));
+        CK(ctx->sort_v.ensure((size_t)V * 4));
+        CK(ctx->sort_k2.ensure((size_t)V * 4));
+        CK(ctx->sort_v2.ensure((size_t)V * 4));
+        compact_kernel<<<div_up(N, 256), 256, 0, st>>>(ctx->ntiles.as<uint32_t>(), ctx->vispos.as<uint32_t>(),
+                                                        ctx->depth_key.as<uint32_t>(), N, ctx->sort_k.as<uint32_t>(),
+                                                        ctx->sort_v.as<uint32_t>());
+        CKL();
+        CK(ctx->sort_ws.ensure(radix_workspace_bytes((int)V) + 4096));
+        // stable sort by f32 depth bits; gid (projected order) breaks ties
+        int which = radix_sort_pairs(ctx->sort_k.as<uint32_t>(), ctx->sort_v.as<uint32_t>(), ctx->sort_k2.as<uint32_t>(),
+                                     ctx->sort_v2.as<uint32_t>(), (int)V, 0, 32, ctx->sort_ws.as<uint32_t>(), st);
+        CKL();
+        uint32_t* sorted_gid = which ? ctx->sort_v2.as<uint32_t>() : ctx->sort_v.as<uint32_t>();
+        ctx->sorted_gid = sorted_gid;
+        CK(ctx->rec_sorted.ensure((size_t)V * sizeof(SplatRec)));
+        CK(ctx->fast_sorted.ensure((size_t)V * sizeof(SplatFast)));
+        CK(ctx->ntiles_sorted.ensure((size_t)V * 4));
+        CK(ctx->inst_off.ensure((size_t)V * 4));
+        gather_sorted_kernel<<<div_up((uint32_t)V, 256), 256, 0, st>>>(
+            sorted_gid, (int)V, ctx->rec.as<SplatRec>(), ctx->ntiles.as<uint32_t>(), ctx->rec_sorted.as<SplatRec>(),
+            ctx->fast_sorted.as<SplatFast>(), ctx->ntiles_sorted.as<uint32_t>());
+        CKL();
+        CK(ctx->scan_ws.ensure(scan_workspace_bytes((int)V) + 4096));
+        exclusive_scan_u32(ctx->ntiles_sorted.as<uint32_t>(), ctx->inst_off.as<uint32_t>(), (int)V, &dc->I,
+                           ctx->scan_ws.as<uint32_t>(), st);
+        CKL();
+        CK(cudaMemcpyAsync(hc, dc, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        I = hc->I;
+    }
+    ctx->V = V;
+    ctx->I = I;
+    uint32_t* inst_vals = nullptr;
+    if (I > 0) {
+        CK(ctx->inst_k.ensure((size_t)I * 4));
+        CK(ctx->inst_v.ensure((size_t)I * 4));
+        CK(ctx->inst_k2.ensure((size_t)I * 4));
+        CK(ctx->inst_v2.ensure((size_t)I * 4));
+        duplicate_kernel<<<div_up((uint32_t)V, 256), 256, 0, st>>>(ctx->fast_sorted.as<SplatFast>(), (int)V,
+                                                                    ctx->inst_off.as<uint32_t>(), tiles_x,
+                                                                    ctx->inst_k.as<uint32_t>(), ctx->inst_v.as<uint32_t>());
+        CKL();
+        int bits = 1;
+        while ((1 << bits) < n_tiles) ++bits;
+        const int end_bit = ((bits + 7) / 8) * 8;
+        CK(ctx->sort_ws.ensure(radix_workspace_bytes((int)I) + 4096));
+        int which = radix_sort_pairs(ctx->inst_k.as<uint32_t>(), ctx->inst_v.as<uint32_t>(), ctx->inst_k2.as<uint32_t>(),
+                                     ctx->inst_v2.as<uint32_t>(), (int)I, 0, end_bit, ctx->sort_ws.as<uint32_t>(), st);
+        CKL();
+        uint32_t* keys = which ? ctx->inst_k2.as<uint32_t>() : ctx->inst_k.as<uint32_t>();
+        inst_vals = which ? ctx->inst_v2.as<uint32_t>() : ctx->inst_v.as<uint32_t>();
+        tile_ranges_kernel<<<div_up((uint32_t)I, 256), 256, 0, st>>>(keys, (int)I, ctx->ranges.as<uint2>());
+        CKL();
+    }
+    ctx->inst_vals_final = inst_vals;
+    raster_fwd_kernel<<<n_tiles, 256, 0, st>>>(
+        ctx->ranges.as<uint2>(), inst_vals, ctx->fast_sorted.as<SplatFast>(), ctx->rec_sorted.as<SplatRec>(), W, H,
+        tiles_x, (float)bg[0], (float)bg[1], (float)bg[2], ctx->img.as<float>(), ctx->last.as<uint32_t>(),
+        want_trans ? ctx->trans.as<float>() : nullptr, want_count ? ctx->count.as<uint32_t>() : nullptr,
+        ctx->fix_list.as<uint32_t>(), &dc->fix_count);
+    CKL();
+    raster_fixup_kernel<<<ctx->sms * 2, 128, 0, st>>>(
+        ctx->fix_list.as<uint32_t>(), &dc->fix_count, ctx->ranges.as<uint2>(), inst_vals,
+        ctx->rec_sorted.as<SplatRec>(), W, tiles_x, bg[0], bg[1], bg[2], ctx->img.as<float>(),
+        ctx->last.as<uint32_t>(), want_trans ? ctx->trans.as<float>() : nullptr,
+        want_count ? ctx->count.as<uint32_t>() : nullptr);
+    CKL();
+    CK(cudaMemcpyAsync(hc, dc, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    ctx->stats.culled_depth = (int64_t)hc->stats[0];
+    ctx->stats.culled_offscreen = (int64_t)hc->stats[1];
+    ctx->stats.culled_degenerate = (int64_t)hc->stats[2];
+    ctx->stats.culled_temporal = (int64_t)hc->stats[3];
+    ctx->stats.degenerate_temporal = (int64_t)hc->stats[4];
+    ctx->stats.projected = (int64_t)hc->stats[5];
+    ctx->fixups = hc->fix_count;
+    hgs_status s = check_flags(ctx, hc->flags);
+    if (s != HGS_OK) return s;
+    ctx->have_tape = true;
+    return HGS_OK;
+}
+
+extern "C" {
+
+hgs_status hgs_ctx_create(int device, hgs_ctx** out) {
+    if (!out) return HGS_ERR_INVALID_ARGUMENT;
+    *out = nullptr;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n <= 0) {
+        cudaGetLastError();
+        return HGS_ERR_CUDA;
+    }
+    if (device < 0 || device >= n) return HGS_ERR_INVALID_ARGUMENT;
+    if (cudaSetDevice(device) != cudaSuccess) return HGS_ERR_CUDA;
+    hgs_ctx* ctx = new hgs_ctx();
+    ctx->device = device;
+    cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device);
+    if (cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking) != cudaSuccess) {
+        delete ctx;
+        return HGS_ERR_CUDA;
+    }
+    ctx->stream = ctx->own_stream;
+    *out = ctx;
+    return HGS_OK;
+}
+
+void hgs_ctx_destroy(hgs_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    DBuf* bufs[] = {&ctx->p4, &ctx->p3, &ctx->g4, &ctx->g3, &ctx->m4, &ctx->v4, &ctx->m3, &ctx->v3, &ctx->gn4,
+                    &ctx->gn3, &ctx->cnt4, &ctx->cnt3, &ctx->sn4, &ctx->sn3, &ctx->rec, &ctx->depth_key,
+                    &ctx->ntiles, &ctx->visflag, &ctx->vispos, &ctx->sort_k, &ctx->sort_v, &ctx->sort_k2,
+                    &ctx->sort_v2, &ctx->rec_sorted, &ctx->fast_sorted, &ctx->ntiles_sorted, &ctx->inst_off,
+                    &ctx->inst_k, &ctx->inst_v, &ctx->inst_k2, &ctx->inst_v2, &ctx->ranges, &ctx->scan_ws,
+                    &ctx->sort_ws, &ctx->counters, &ctx->img, &ctx->last, &ctx->trans, &ctx->count,
+                    &ctx->fix_list, &ctx->accum, &ctx->lgrad, &ctx->gt_stage, &ctx->loss_ws, &ctx->stage};
+    for (DBuf* b : bufs) b->release();
+    ctx->pinned.release();
+    if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+    delete ctx;
+}
+
+const char* hgs_last_error(const hgs_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+hgs_status hgs_ctx_set_stream(hgs_ctx* ctx, void* stream) {
+    if (!ctx) return HGS_ERR_INVALID_ARGUMENT;
+    ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+    return HGS_OK;
+}
+
+void* hgs_ctx_stream(hgs_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+hgs_status hgs_synchronize(hgs_ctx* ctx) {
+    if (!ctx) return HGS_ERR_INVALID_ARGUMENT;
+    CK(cudaStreamSynchronize(ctx->stream));
+    return HGS_OK;
+}
+
+hgs_status hgs_scene_upload(hgs_ctx* ctx, const hgs_host_scene* s, int dtype) {
+    if (!ctx || !s) return HGS_ERR_INVALID_ARGUMENT;
+    if (s->n4 < 0 || s->n3 < 0 || s->sh_degree < 0 || s->sh_degree > 3)
+        return fail(ctx, HGS_ERR_INVALID_ARGUMENT, "scene upload: bad sizes or sh_degree (0..3)");
+    if (s->n4 + s->n3 > (int64_t)INT32_MAX / 2) return fail(ctx, HGS_ERR_INVALID_ARGUMENT, "scene too large");
+    CK(cudaSetDevice(ctx->device));
+    ctx->n4 = s->n4;
+    ctx->n3 = s->n3;
+    ctx->deg = s->sh_degree;
+    ctx->tau = s->tau;
+    ctx->extent = s->extent;
+    ctx->cap4 = round_cap(s->n4);
+    ctx->cap3 = round_cap(s->n3 + s->n4);  // room for every 4D Gaussian to convert
+    const size_t b4 = (size_t)rows4(ctx->deg) * ctx->cap4 * sizeof(float);
+    const size_t b3 = (size_t)rows3(ctx->deg) * ctx->cap3 * sizeof(float);
+    for (DBuf* b : {&ctx->p4, &ctx->g4, &ctx->m4, &ctx->v4}) CK(b->ensure(b4));
+    for (DBuf* b : {&ctx->p3, &ctx->g3, &ctx->m3, &ctx->v3}) CK(b->ensure(b3));
+    for (DBuf* b : {&ctx->g4, &ctx->m4, &ctx->v4}) CK(cudaMemsetAsync(b->p, 0, b4, ctx->stream));
+    for (DBuf* b : {&ctx->g3, &ctx->m3, &ctx->v3}) CK(cudaMemsetAsync(b->p, 0, b3, ctx->stream));
+    for (DBuf* b : {&ctx->gn4, &ctx->cnt4, &ctx->sn4}) {
+        CK(b->ensure((size_t)ctx->cap4 * 4));
+        CK(cudaMemsetAsync(b->p, 0, (size_t)ctx->cap4 * 4, ctx->stream));
+    }
+    for (DBuf* b : {&ctx->gn3, &ctx->cnt3, &ctx->sn3}) {
+        CK(b->ensure((size_t)ctx->cap3 * 4));
+        CK(cudaMemsetAsync(b->p, 0, (size_t)ctx->cap3 * 4, ctx->stream));
+    }
+    ctx->step = 0;
+    ctx->have_tape = false;
+    hgs_status r = upload_pool(ctx, s, kDyn, 7, ctx->n4, ctx->cap4, ctx->p4.as<float>(), dtype);
+    if (r != HGS_OK) return r;
+    r = upload_pool(ctx, s, kSta, 5, ctx->n3, ctx->cap3, ctx->p3.as<float>(), dtype);
+    if (r != HGS_OK) return r;
+    CK(cudaStreamSynchronize(ctx->stream));
+    return HGS_OK;
+}
+
+hgs_status hgs_scene_download(hgs_ctx* ctx, hgs_host_scene* out, int dtype) {
+    if (!ctx || !out) return HGS_ERR_INVALID_ARGUMENT;
+    CK(cudaSetDevice(ctx->device));
+    hgs_status r = download_pool(ctx, out, kDyn, 7, ctx->n4, ctx->cap4, ctx->p4.as<float>(), dtype);
+    if (r != HGS_OK) return r;
+    r = download_pool(ctx, out, kSta, 5, ctx->n3, ctx->cap3, ctx->p3.as<float>(), dtype);
+    if (r != HGS_OK) return r;
+    out->n4 = ctx->n4;
+    out->n3 = ctx->n3;
+    out->sh_degree = ctx->deg;
+    out->tau = ctx->tau;
+    out->extent = ctx->extent;
+    return HGS_OK;
+}
+
+hgs_status hgs_scene_counts(hgs_ctx* ctx, int64_t* n4, int64_t* n3, int32_t* deg) {
+    if (!ctx) return HGS_ERR_INVALID_ARGUMENT;
+    if (n4) *n4 = ctx->n4;
+    if (n3) *n3 = ctx->n3;
+    if (deg) *deg = ctx->deg;
+    return HGS_OK;
+}
+
+hgs_status hgs_render(hgs_ctx* ctx, const hgs_camera* cam, double t, const double bg[3], const hgs_raster_opts* opts,
+                      float* rgb_host, uint32_t* count_host, float* trans_host, hgs_render_stats* stats) {
+    if (!ctx || !cam || !bg) return HGS_ERR_INVALID_ARGUMENT;
+    CK(cudaSetDevice(ctx->device));
+    hgs_status r = hgs_render_pipeline(ctx, cam, t, bg, opts);
+    if (r != HGS_OK) return r;
+    const size_t npx = (size_t)ctx->W * ctx->H;
+    if (rgb_host) CK(cudaMemcpyAsync(rgb_host, ctx->img.p, npx * 3 * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    if (count_host && opts && opts->count_map)
+        CK(cudaMemcpyAsync(count_host, ctx->count.p, npx * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    if (trans_host && opts && opts->transmittance_map)
+        CK(cudaMemcpyAsync(trans_host, ctx->trans.p, npx * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (stats) *stats = ctx->stats;
+    return HGS_OK;
+}
+
+hgs_status hgs_rasterize(hgs_ctx* ctx, const hgs_host_scene* scene, int dtype, const hgs_camera* cam, double t,
+                         const double bg[3], const hgs_raster_opts* opts, void* rgb_out, uint32_t* count_out,
+                         void* trans_out, hgs_render_stats* stats) {
+    if (!ctx || !scene || !cam || !bg) return HGS_ERR_INVALID_ARGUMENT;
+    hgs_status r = hgs_scene_upload(ctx, scene, dtype);
+    if (r != HGS_OK) return r;
+    const size_t npx = (size_t)cam->width * cam->height;
+    std::vector<float> rgb(rgb_out ? npx * 3 : 0), trans(trans_out ? npx : 0);
+    r = hgs_render(ctx, cam, t, bg, opts, rgb_out ? rgb.data() : nullptr, count_out,
+                   trans_out ? trans.data() : nullptr, stats);
+    if (r != HGS_OK) return r;
+    if (rgb_out) {
+        if (dtype == HGS_F64)
+            for (size_t i = 0; i < rgb.size(); ++i) static_cast<double*>(rgb_out)[i] = rgb[i];
+        else
+            std::memcpy(rgb_out, rgb.data(), rgb.size() * 4);
+    }
+    if (trans_out) {
+        if (dtype == HGS_F64)
+            for (size_t i = 0; i < trans.size(); ++i) static_cast<double*>(trans_out)[i] = trans[i];
+        else
+            std::memcpy(trans_out, trans.data(), trans.size() * 4);
+    }
+    return HGS_OK;
+}
+
+const float* hgs_last_image_device(hgs_ctx* ctx) { return ctx ? ctx->img.as<float>() : nullptr; }
+
+hgs_status hgs_render_info_get(hgs_ctx* ctx, hgs_render_info* info) {
+    if (!ctx || !info) return HGS_ERR_INVALID_ARGUMENT;
+    info->visible = ctx->V;
+    info->instances = ctx->I;
+    info->fixup_pixels = ctx->fixups;
+    info->fp64_splats = ctx->fp64_splats;
+    return HGS_OK;
+}
+
+// ---- parity introspection (used by tests/, not part of the reference API)
+// Projected splats in projected-index order: gid, f32 depth bits, box, mean,
+// conic, alpha, rgb.
+hgs_status hgs_debug_splats(hgs_ctx* ctx, int32_t* gid, uint32_t* depth_bits, int32_t* box4, double* mean2,
+                            double* conic4, double* alpha, float* rgb, int64_t cap, int64_t* n_out) {
+    if (!ctx || !ctx->have_tape) return fail(ctx, HGS_ERR_STATE, "no render to inspect");
+    const int64_t V = ctx->V;
+    *n_out = V;
+    if (V > cap || V == 0) return HGS_OK;
+    std::vector<uint32_t> sg(V);
+    std::vector<SplatRec> rs(V);
+    CK(cudaMemcpy(sg.data(), ctx->sorted_gid, V * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(rs.data(), ctx->rec_sorted.p, V * sizeof(SplatRec), cudaMemcpyDeviceToHost));
+    std::vector<uint32_t> dk(ctx->n4 + ctx->n3);
+    CK(cudaMemcpy(dk.data(), ctx->depth_key.p, dk.size() * 4, cudaMemcpyDeviceToHost));
+    // projected order = increasing gid
+    std::vector<int64_t> order(V);
+    for (int64_t j = 0; j < V; ++j) order[j] = j;
+    std::sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return sg[a] < sg[b]; });
+    for (int64_t q = 0; q < V; ++q) {
+        const int64_t j = order[q];
+        const SplatRec& e = rs[j];
+        gid[q] = (int32_t)sg[j];
+        depth_bits[q] = dk[sg[j]];
+        box4[q * 4 + 0] = e.x0;
+        box4[q * 4 + 1] = e.x1;
+        box4[q * 4 + 2] = e.y0;
+        box4[q * 4 + 3] = e.y1;
+        mean2[q * 2 + 0] = e.sx;
+        mean2[q * 2 + 1] = e.sy;
+        conic4[q * 4 + 0] = e.c00;
+        conic4[q * 4 + 1] = e.c01;
+        conic4[q * 4 + 2] = e.c10;
+        conic4[q * 4 + 3] = e.c11;
+        alpha[q] = e.alpha;
+        rgb[q * 3 + 0] = e.r;
+        rgb[q * 3 + 1] = e.g;
+        rgb[q * 3 + 2] = e.b;
+    }
+    return HGS_OK;
+}
+
+// Tile-sorted instances: tile id and gid of each, in render order.
+hgs_status hgs_debug_instances(hgs_ctx* ctx, uint32_t* tile, uint32_t* gid, int64_t cap, int64_t* n_out) {
+    if (!ctx || !ctx->have_tape) return fail(ctx, HGS_ERR_STATE, "no render to inspect");
+    const int64_t I = ctx->I, V = ctx->V;
+    *n_out = I;
+    if (I > cap || I == 0) return HGS_OK;
+    std::vector<uint32_t> vals(I), sg(V);
+    std::vector<uint2> rg((size_t)ctx->tiles_x * ctx->tiles_y);
+    CK(cudaMemcpy(vals.data(), ctx->inst_vals_final, I * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(sg.data(), ctx->sorted_gid, V * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(rg.data(), ctx->ranges.p, rg.size() * sizeof(uint2), cudaMemcpyDeviceToHost));
+    for (size_t tl = 0; tl < rg.size(); ++tl)
+        for (uint32_t i = rg[tl].x; i < rg[tl].y; ++i) tile[i] = (uint32_t)tl;
+    for (int64_t i = 0; i < I; ++i) gid[i] = sg[vals[i]];
+    return HGS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,106 @@
+// ctx.cuh -- host-side context of the C ABI (one per GPU).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/hgs_gpu.h"
+#include "hgs_common.cuh"
+
+namespace hgs {
+
+struct DBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaError_t ensure(size_t bytes) {
+        if (bytes <= cap) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        size_t want = bytes + bytes / 4 + 256;
+        cudaError_t e = cudaMalloc(&p, want);
+        if (e == cudaSuccess) cap = want;
+        return e;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+    template <typename T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+struct HostPinned {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaError_t ensure(size_t bytes) {
+        if (bytes <= cap) return cudaSuccess;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+        size_t want = bytes + bytes / 4 + 256;
+        cudaError_t e = cudaMallocHost(&p, want);
+        if (e == cudaSuccess) cap = want;
+        return e;
+    }
+    void release() {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+}  // namespace hgs
+
+struct hgs_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaStream_t own_stream = nullptr;
+    std::string err;
+    int sms = 148;
+
+    // ---- device-resident scene (component-major SoA, see hgs_common.cuh)
+    int64_t n4 = 0, n3 = 0, cap4 = 0, cap3 = 0;
+    int deg = 1;
+    double tau = 0.5, extent = 1.0;
+    hgs::DBuf p4, p3;      // params
+    hgs::DBuf g4, g3;      // gradients (same layout)
+    hgs::DBuf m4, v4, m3, v3;  // Adam moments
+    hgs::DBuf gn4, gn3;    // densify grad_norm (float)
+    hgs::DBuf cnt4, cnt3;  // densify counts (u32)
+    hgs::DBuf sn4, sn3;    // screen_norm of the last backward (float)
+    uint64_t step = 0;
+
+    // ---- per-render workspace
+    hgs::DBuf rec, depth_key, ntiles, visflag, vispos;
+    hgs::DBuf sort_k, sort_v, sort_k2, sort_v2;       // depth sort (V)
+    hgs::DBuf rec_sorted, fast_sorted, ntiles_sorted, inst_off;
+    hgs::DBuf inst_k, inst_v, inst_k2, inst_v2;       // tile sort (I)
+    hgs::DBuf ranges, scan_ws, sort_ws;
+    hgs::DBuf counters;  // [0..5] stats u64, [6] flags, fix_count, totals...
+    hgs::DBuf img, last, trans, count, fix_list;
+    hgs::DBuf accum;     // backward per-sorted-splat accumulators
+    hgs::DBuf lgrad;     // dL/dimage (device float)
+    hgs::DBuf gt_stage;  // staged ground truth
+    hgs::DBuf loss_ws;   // loss scratch
+    hgs::DBuf stage;     // upload / download staging
+    hgs::HostPinned pinned;
+
+    // ---- state of the last render (the "tape")
+    bool have_tape = false;
+    int W = 0, H = 0, tiles_x = 0, tiles_y = 0;
+    int64_t V = 0, I = 0;
+    uint32_t* inst_vals_final = nullptr;  // tile-sorted instance values
+    hgs::DevCamera cam{};
+    double t = 0.0;
+    double bg[3] = {0, 0, 0};
+    int64_t fixups = 0, fp64_splats = 0;
+    hgs_render_stats stats{};
+    uint32_t* sorted_gid = nullptr;       // V sorted gids
+};

@@ -1,0 +1,363 @@
+// gaussian_bwd.cu -- K7: per-Gaussian backward (backward.cpp:224-354).
+//
+// One thread per visible (depth-sorted) splat.  Reads the 9 compositing
+// accumulators of K6, re-derives the forward intermediates of its Gaussian in
+// FP64 from the FP32 parameters (slice, projection Jacobian, view direction,
+// raw SH colour) and chains conic -> 2D covariance -> 3D covariance / camera
+// mean -> parameters.  4D Gaussians additionally go through the Schur
+// complement backward and the isoclinic rotation factors.  Writes
+// grad += scale * d, the per-image screen-space norm, and the densification
+// statistics (train.cpp:433-444).  Coalesced SoA reads/writes; HBM bound.
+#include "hgs_common.cuh"
+
+namespace hgs {
+
+namespace {
+
+__device__ inline void isoL(const double q[4], double L[4][4]) {
+    const double a = q[0], b = q[1], c = q[2], d = q[3];
+    const double m[4][4] = {{a, -b, -c, -d}, {b, a, -d, c}, {c, d, a, -b}, {d, -c, b, a}};
+    for (int i = 0; i < 4; ++i)
+        for (int j = 0; j < 4; ++j) L[i][j] = m[i][j];
+}
+__device__ inline void isoR(const double q[4], double R[4][4]) {
+    const double p = q[0], x = q[1], r = q[2], s = q[3];
+    const double m[4][4] = {{p, -x, -r, -s}, {x, p, s, -r}, {r, -s, p, x}, {s, r, -x, p}};
+    for (int i = 0; i < 4; ++i)
+        for (int j = 0; j < 4; ++j) R[i][j] = m[i][j];
+}
+
+__device__ inline void sh_basis_d(const double d[3], int deg, double out[16]) {
+    const double x = d[0], y = d[1], z = d[2];
+    out[0] = 0.28209479177387814;
+    if (deg < 1) return;
+    out[1] = -0.4886025119029199 * y;
+    out[2] = 0.4886025119029199 * z;
+    out[3] = -0.4886025119029199 * x;
+    if (deg < 2) return;
+    const double xx = x * x, yy = y * y, zz = z * z;
+    out[4] = 1.0925484305920792 * x * y;
+    out[5] = -1.0925484305920792 * y * z;
+    out[6] = 0.31539156525252005 * (2.0 * zz - xx - yy);
+    out[7] = -1.0925484305920792 * x * z;
+    out[8] = 0.5462742152960396 * (xx - yy);
+    if (deg < 3) return;
+    out[9] = -0.5900435899266435 * y * (3.0 * xx - yy);
+    out[10] = 2.890611442640554 * x * y * z;
+    out[11] = -0.4570457994644658 * y * (4.0 * zz - xx - yy);
+    out[12] = 0.3731763325901154 * z * (2.0 * zz - 3.0 * xx - 3.0 * yy);
+    out[13] = -0.4570457994644658 * x * (4.0 * zz - xx - yy);
+    out[14] = 1.445305721320277 * z * (xx - yy);
+    out[15] = -0.5900435899266435 * x * (xx - 3.0 * yy);
+}
+
+// sh.cpp:49-71: d Y_k / d dir
+__device__ inline void sh_basis_grad_d(const double d[3], int deg, double g[16][3]) {
+    const double x = d[0], y = d[1], z = d[2];
+    for (int k = 0; k < 16; ++k) g[k][0] = g[k][1] = g[k][2] = 0.0;
+    if (deg < 1) return;
+    const double C1 = 0.4886025119029199;
+    g[1][1] = -C1;
+    g[2][2] = C1;
+    g[3][0] = -C1;
+    if (deg < 2) return;
+    const double xx = x * x, yy = y * y, zz = z * z;
+    const double A = 1.0925484305920792, B = 0.31539156525252005, Cc = 0.5462742152960396;
+    g[4][0] = A * y; g[4][1] = A * x;
+    g[5][1] = -A * z; g[5][2] = -A * y;
+    g[6][0] = B * (-2.0 * x); g[6][1] = B * (-2.0 * y); g[6][2] = B * (4.0 * z);
+    g[7][0] = -A * z; g[7][2] = -A * x;
+    g[8][0] = Cc * (2.0 * x); g[8][1] = Cc * (-2.0 * y);
+    if (deg < 3) return;
+    const double D0 = -0.5900435899266435, D1 = 2.890611442640554, D2 = -0.4570457994644658,
+                 D3 = 0.3731763325901154, D5 = 1.445305721320277;
+    g[9][0] = D0 * (6.0 * x * y); g[9][1] = D0 * (3.0 * xx - 3.0 * yy);
+    g[10][0] = D1 * (y * z); g[10][1] = D1 * (x * z); g[10][2] = D1 * (x * y);
+    g[11][0] = D2 * (-2.0 * x * y); g[11][1] = D2 * (4.0 * zz - xx - 3.0 * yy); g[11][2] = D2 * (8.0 * y * z);
+    g[12][0] = D3 * (-6.0 * x * z); g[12][1] = D3 * (-6.0 * y * z); g[12][2] = D3 * (6.0 * zz - 3.0 * xx - 3.0 * yy);
+    g[13][0] = D2 * (4.0 * zz - 3.0 * xx - yy); g[13][1] = D2 * (-2.0 * x * y); g[13][2] = D2 * (8.0 * x * z);
+    g[14][0] = D5 * (2.0 * x * z); g[14][1] = D5 * (-2.0 * y * z); g[14][2] = D5 * (xx - yy);
+    g[15][0] = D0 * (3.0 * xx - 3.0 * yy); g[15][1] = D0 * (-6.0 * x * y);
+}
+
+__device__ inline double sigmoid(double x) { return 1.0 / (1.0 + exp(-x)); }
+
+}  // namespace
+
+__global__ void __launch_bounds__(128) gaussian_bwd_kernel(
+    int V, const uint32_t* __restrict__ sorted_gid, const float* __restrict__ accum, int acc_stride, int n4,
+    const float* __restrict__ p4, int64_t cap4, const float* __restrict__ p3, int64_t cap3, int deg, DevCamera cam,
+    double t, double scale, float* __restrict__ g4, float* __restrict__ g3, float* __restrict__ sn4,
+    float* __restrict__ sn3, float* __restrict__ gn4, float* __restrict__ gn3, uint32_t* __restrict__ cnt4,
+    uint32_t* __restrict__ cnt3, const double* __restrict__ conic_src, int conic_stride) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= V) return;
+    const float* acc = accum + (size_t)j * acc_stride;
+    const double d_rgb[3] = {acc[0], acc[1], acc[2]};
+    const double d_alpha = acc[3];
+    const double d_screen[2] = {acc[4], acc[5]};
+    const double dC[2][2] = {{acc[6], acc[7]}, {acc[7], acc[8]}};
+    if (d_rgb[0] == 0.0 && d_rgb[1] == 0.0 && d_rgb[2] == 0.0 && d_alpha == 0.0 && d_screen[0] == 0.0 &&
+        d_screen[1] == 0.0 && dC[0][0] == 0.0 && dC[0][1] == 0.0 && dC[1][1] == 0.0)
+        return;  // untouched (backward.cpp:226)
+    const uint32_t gid = sorted_gid[j];
+    const bool dyn = (int)gid < n4;
+    const int i = dyn ? (int)gid : (int)gid - n4;
+    const float* P = dyn ? p4 : p3;
+    const int64_t cap = dyn ? cap4 : cap3;
+    auto prm = [&](int row) { return (double)P[(int64_t)row * cap + i]; };
+    const double* cn = conic_src + (size_t)j * conic_stride;
+    const double C[2][2] = {{cn[0], cn[1]}, {cn[2], cn[3]}};
+
+    // ---- forward intermediates
+    double mean3[3], cov3[3][3], weight = 1.0, opl, R4[4][4], es[4], ql[4], qr[4], q3[4], cross[3], s44 = 1.0, dt = 0.0;
+    bool clamped;
+    if (dyn) {
+        for (int k = 0; k < 4; ++k) {
+            ql[k] = prm(R4_QL + k);
+            qr[k] = prm(R4_QR + k);
+            es[k] = exp(prm(R4_LS + k));
+        }
+        double L[4][4], R[4][4];
+        isoL(ql, L);
+        isoR(qr, R);
+        for (int a = 0; a < 4; ++a)
+            for (int b = 0; b < 4; ++b) {
+                double s = 0.0;
+                for (int k = 0; k < 4; ++k) s += L[a][k] * R[k][b];
+                R4[a][b] = s;
+            }
+        double M[4][4], S4[4][4];
+        for (int a = 0; a < 4; ++a)
+            for (int b = 0; b < 4; ++b) M[a][b] = R4[a][b] * es[b];
+        for (int a = 0; a < 4; ++a)
+            for (int b = 0; b < 4; ++b) {
+                double s = 0.0;
+                for (int k = 0; k < 4; ++k) s += M[a][k] * M[b][k];
+                S4[a][b] = s;
+            }
+        s44 = S4[3][3];
+        for (int k = 0; k < 3; ++k) cross[k] = S4[k][3];
+        dt = t - prm(R4_MT);
+        for (int k = 0; k < 3; ++k) mean3[k] = prm(R4_MEAN + k) + cross[k] * (dt / s44);
+        for (int a = 0; a < 3; ++a)
+            for (int b = 0; b < 3; ++b) cov3[a][b] = S4[a][b] - cross[a] * cross[b] / s44;
+        weight = exp(-0.5 * dt * dt / s44);
+        opl = prm(R4_OP);
+        clamped = sigmoid(opl) * weight >= kAlphaClamp;
+    } else {
+        for (int k = 0; k < 4; ++k) q3[k] = prm(R3_Q + k);
+        for (int k = 0; k < 3; ++k) {
+            es[k] = exp(prm(R3_LS + k));
+            mean3[k] = prm(R3_MEAN + k);
+        }
+        const double w = q3[0], x = q3[1], y = q3[2], z = q3[3];
+        const double Rm[3][3] = {{1 - 2 * (y * y + z * z), 2 * (x * y - z * w), 2 * (x * z + y * w)},
+                                 {2 * (x * y + z * w), 1 - 2 * (x * x + z * z), 2 * (y * z - x * w)},
+                                 {2 * (x * z - y * w), 2 * (y * z + x * w), 1 - 2 * (x * x + y * y)}};
+        for (int a = 0; a < 3; ++a)
+            for (int b = 0; b < 3; ++b) {
+                double s = 0.0;
+                for (int k = 0; k < 3; ++k) s += Rm[a][k] * es[k] * Rm[b][k] * es[k];
+                cov3[a][b] = s;
+            }
+        for (int a = 0; a < 3; ++a)
+            for (int b = 0; b < 3; ++b) R4[a][b] = Rm[a][b];  // reuse storage for the 3x3 rotation
+        opl = prm(R3_OP);
+        clamped = sigmoid(opl) >= kAlphaClamp;
+    }
+    double cp[3];
+    for (int a = 0; a < 3; ++a) cp[a] = cam.R[a * 3] * mean3[0] + cam.R[a * 3 + 1] * mean3[1] + cam.R[a * 3 + 2] * mean3[2] + cam.t[a];
+    const double z = cp[2], xq = cp[0], yq = cp[1];
+    const double J[2][3] = {{cam.fx / z, 0.0, -cam.fx * xq / (z * z)}, {0.0, cam.fy / z, -cam.fy * yq / (z * z)}};
+    double Tm[2][3];
+    for (int a = 0; a < 2; ++a)
+        for (int k = 0; k < 3; ++k) Tm[a][k] = J[a][0] * cam.R[k] + J[a][1] * cam.R[3 + k] + J[a][2] * cam.R[6 + k];
+
+    // ---- conic -> cov2 -> cov3 / camera mean (backward.cpp:231-250)
+    double CdC[2][2], d_cov2[2][2];
+    for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 2; ++b) CdC[a][b] = C[a][0] * dC[0][b] + C[a][1] * dC[1][b];
+    for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 2; ++b) d_cov2[a][b] = -(CdC[a][0] * C[0][b] + CdC[a][1] * C[1][b]);
+    double dT[2][3];  // d_cov2 * T
+    for (int a = 0; a < 2; ++a)
+        for (int k = 0; k < 3; ++k) dT[a][k] = d_cov2[a][0] * Tm[0][k] + d_cov2[a][1] * Tm[1][k];
+    double d_cov3[3][3];
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) d_cov3[a][b] = Tm[0][a] * dT[0][b] + Tm[1][a] * dT[1][b];
+    double d_tmat[2][3];
+    for (int a = 0; a < 2; ++a)
+        for (int k = 0; k < 3; ++k) d_tmat[a][k] = 2.0 * (dT[a][0] * cov3[0][k] + dT[a][1] * cov3[1][k] + dT[a][2] * cov3[2][k]);
+    double d_jac[2][3];
+    for (int a = 0; a < 2; ++a)
+        for (int k = 0; k < 3; ++k)
+            d_jac[a][k] = d_tmat[a][0] * cam.R[k * 3] + d_tmat[a][1] * cam.R[k * 3 + 1] + d_tmat[a][2] * cam.R[k * 3 + 2];
+    double d_cp[3];
+    for (int k = 0; k < 3; ++k) d_cp[k] = J[0][k] * d_screen[0] + J[1][k] * d_screen[1];
+    const double fx = cam.fx, fy = cam.fy;
+    d_cp[0] += d_jac[0][2] * (-fx / (z * z));
+    d_cp[1] += d_jac[1][2] * (-fy / (z * z));
+    d_cp[2] += d_jac[0][0] * (-fx / (z * z)) + d_jac[1][1] * (-fy / (z * z)) + d_jac[0][2] * (2.0 * fx * xq / (z * z * z)) +
+               d_jac[1][2] * (2.0 * fy * yq / (z * z * z));
+    double d_mean3[3];
+    for (int k = 0; k < 3; ++k) d_mean3[k] = cam.R[k] * d_cp[0] + cam.R[3 + k] * d_cp[1] + cam.R[6 + k] * d_cp[2];
+
+    // ---- colour path (backward.cpp:252-273)
+    double v[3] = {mean3[0] - cam.pos[0], mean3[1] - cam.pos[1], mean3[2] - cam.pos[2]};
+    const double vd = sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+    double dir[3] = {0.0, 0.0, 1.0};
+    if (vd > 0.0)
+        for (int k = 0; k < 3; ++k) dir[k] = v[k] / vd;
+    double basis[16];
+    sh_basis_d(dir, deg, basis);
+    const int K = sh_count(deg);
+    const int shrow = dyn ? R4_SH : R3_SH;
+    double raw[3] = {0.0, 0.0, 0.0};
+    for (int k = 0; k < K; ++k)
+        for (int c = 0; c < 3; ++c) raw[c] += basis[k] * prm(shrow + 3 * k + c);
+    double drr[3];
+    for (int c = 0; c < 3; ++c) {
+        raw[c] += 0.5;
+        drr[c] = (raw[c] < 0.0 || raw[c] > 1.0) ? 0.0 : d_rgb[c];
+    }
+    double bgrad[16][3];
+    sh_basis_grad_d(dir, deg, bgrad);
+    double d_dir[3] = {0.0, 0.0, 0.0};
+    float* G = dyn ? g4 : g3;
+    auto gadd = [&](int row, double val) {
+        float* p = &G[(int64_t)row * cap + i];
+        *p = *p + (float)(scale * val);
+    };
+    for (int k = 0; k < K; ++k) {
+        double dotc = 0.0;
+        for (int c = 0; c < 3; ++c) {
+            gadd(shrow + 3 * k + c, basis[k] * drr[c]);
+            dotc += drr[c] * prm(shrow + 3 * k + c);
+        }
+        for (int c = 0; c < 3; ++c) d_dir[c] += bgrad[k][c] * dotc;
+    }
+    if (vd > 0.0)
+        for (int a = 0; a < 3; ++a) {
+            double s = 0.0;
+            for (int b = 0; b < 3; ++b) s += ((a == b ? 1.0 : 0.0) - dir[a] * dir[b]) / vd * d_dir[b];
+            d_mean3[a] += s;
+        }
+    const double screen_norm = sqrt(d_screen[0] * d_screen[0] + d_screen[1] * d_screen[1]);
+    double dS[3][3];
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) dS[a][b] = 0.5 * (d_cov3[a][b] + d_cov3[b][a]);
+    const double sg = sigmoid(opl);
+
+    if (!dyn) {
+        for (int k = 0; k < 3; ++k) gadd(R3_MEAN + k, d_mean3[k]);
+        if (!clamped) gadd(R3_OP, d_alpha * sg * (1.0 - sg));
+        double m[3][3], dm[3][3];
+        for (int a = 0; a < 3; ++a)
+            for (int b = 0; b < 3; ++b) m[a][b] = R4[a][b] * es[b];
+        for (int a = 0; a < 3; ++a)
+            for (int b = 0; b < 3; ++b) dm[a][b] = 2.0 * (dS[a][0] * m[0][b] + dS[a][1] * m[1][b] + dS[a][2] * m[2][b]);
+        for (int k = 0; k < 3; ++k) gadd(R3_LS + k, dm[0][k] * m[0][k] + dm[1][k] * m[1][k] + dm[2][k] * m[2][k]);
+        double dR[3][3];
+        for (int a = 0; a < 3; ++a)
+            for (int b = 0; b < 3; ++b) dR[a][b] = dm[a][b] * es[b];
+        const double w = q3[0], x = q3[1], y = q3[2], zz = q3[3];
+        // drot3_dq (backward.cpp:54-72), contracted with dR
+        const double D[4][3][3] = {{{0, -zz, y}, {zz, 0, -x}, {-y, x, 0}},
+                                   {{0, y, zz}, {y, -2 * x, -w}, {zz, w, -2 * x}},
+                                   {{-2 * y, x, w}, {x, 0, zz}, {-w, zz, -2 * y}},
+                                   {{-2 * zz, -w, x}, {w, -2 * zz, y}, {x, y, 0}}};
+        double dq[4];
+        for (int k = 0; k < 4; ++k) {
+            double s = 0.0;
+            for (int a = 0; a < 3; ++a)
+                for (int b = 0; b < 3; ++b) s += dR[a][b] * 2.0 * D[k][a][b];
+            dq[k] = s;
+        }
+        const double qd = q3[0] * dq[0] + q3[1] * dq[1] + q3[2] * dq[2] + q3[3] * dq[3];
+        for (int k = 0; k < 4; ++k) gadd(R3_Q + k, dq[k] - qd * q3[k]);
+        sn3[i] = (float)screen_norm;
+        if (screen_norm > 0.0) {
+            gn3[i] += (float)screen_norm;
+            cnt3[i] += 1u;
+        }
+    } else {
+        double d_weight = 0.0;
+        if (!clamped) {
+            gadd(R4_OP, d_alpha * weight * sg * (1.0 - sg));
+            d_weight += d_alpha * sg;
+        }
+        for (int k = 0; k < 3; ++k) gadd(R4_MEAN + k, d_mean3[k]);
+        const double dmc = d_mean3[0] * cross[0] + d_mean3[1] * cross[1] + d_mean3[2] * cross[2];
+        gadd(R4_MT, -dmc / s44 + d_weight * weight * dt / s44);
+        double sc[3];
+        for (int a = 0; a < 3; ++a) sc[a] = dS[a][0] * cross[0] + dS[a][1] * cross[1] + dS[a][2] * cross[2];
+        double d_cross[3];
+        for (int a = 0; a < 3; ++a) d_cross[a] = d_mean3[a] * (dt / s44) - 2.0 * sc[a] / s44;
+        const double csc = cross[0] * sc[0] + cross[1] * sc[1] + cross[2] * sc[2];
+        const double d_s44 = -dmc * dt / (s44 * s44) + csc / (s44 * s44) + d_weight * weight * 0.5 * dt * dt / (s44 * s44);
+        double d4[4][4];
+        for (int a = 0; a < 4; ++a)
+            for (int b = 0; b < 4; ++b) d4[a][b] = 0.0;
+        for (int a = 0; a < 3; ++a)
+            for (int b = 0; b < 3; ++b) d4[a][b] = dS[a][b];
+        for (int a = 0; a < 3; ++a) d4[a][3] = d_cross[a];
+        d4[3][3] = d_s44;
+        double m4[4][4], dm4[4][4];
+        for (int a = 0; a < 4; ++a)
+            for (int b = 0; b < 4; ++b) m4[a][b] = R4[a][b] * es[b];
+        for (int a = 0; a < 4; ++a)
+            for (int b = 0; b < 4; ++b) {
+                double s = 0.0;
+                for (int k = 0; k < 4; ++k) s += (d4[a][k] + d4[k][a]) * m4[k][b];
+                dm4[a][b] = s;
+            }
+        for (int k = 0; k < 4; ++k)
+            gadd(R4_LS + k, dm4[0][k] * m4[0][k] + dm4[1][k] * m4[1][k] + dm4[2][k] * m4[2][k] + dm4[3][k] * m4[3][k]);
+        double dR4[4][4];
+        for (int a = 0; a < 4; ++a)
+            for (int b = 0; b < 4; ++b) dR4[a][b] = dm4[a][b] * es[b];
+        double L[4][4], R[4][4];
+        isoL(ql, L);
+        isoR(qr, R);
+        double dL[4][4], dR[4][4];
+        for (int a = 0; a < 4; ++a)
+            for (int b = 0; b < 4; ++b) {
+                double x = 0.0, y = 0.0;
+                for (int k = 0; k < 4; ++k) {
+                    x += dR4[a][k] * R[b][k];
+                    y += L[k][a] * dR4[k][b];
+                }
+                dL[a][b] = x;
+                dR[a][b] = y;
+            }
+        double dql[4], dqr[4];
+        for (int k = 0; k < 4; ++k) {
+            double ek[4] = {k == 0 ? 1.0 : 0.0, k == 1 ? 1.0 : 0.0, k == 2 ? 1.0 : 0.0, k == 3 ? 1.0 : 0.0};
+            double le[4][4], re[4][4];
+            isoL(ek, le);
+            isoR(ek, re);
+            double x = 0.0, y = 0.0;
+            for (int a = 0; a < 4; ++a)
+                for (int b = 0; b < 4; ++b) {
+                    x += dL[a][b] * le[a][b];
+                    y += dR[a][b] * re[a][b];
+                }
+            dql[k] = x;
+            dqr[k] = y;
+        }
+        const double dl = ql[0] * dql[0] + ql[1] * dql[1] + ql[2] * dql[2] + ql[3] * dql[3];
+        const double dr = qr[0] * dqr[0] + qr[1] * dqr[1] + qr[2] * dqr[2] + qr[3] * dqr[3];
+        for (int k = 0; k < 4; ++k) {
+            gadd(R4_QL + k, dql[k] - dl * ql[k]);
+            gadd(R4_QR + k, dqr[k] - dr * qr[k]);
+        }
+        sn4[i] = (float)screen_norm;
+        if (screen_norm > 0.0) {
+            gn4[i] += (float)screen_norm;
+            cnt4[i] += 1u;
+        }
+    }
+}
+
+}  // namespace hgs

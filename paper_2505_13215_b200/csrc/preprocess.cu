@@ -1,0 +1,428 @@
+// preprocess.cu -- K1: fused 4D->3D conditional slice + EWA projection + SH.
+//
+// One thread per Gaussian (4D pool first, then 3D: gid = i / n4 + i), the
+// reference's project_scene order (raster.cpp:90-116).  Geometry is FP64 and
+// this translation unit is compiled with -fmad=false, so every product/sum
+// below rounds exactly like the oracle's -ffp-contract=off code: the depth
+// f32 bits, the pixel box and therefore the tile assignment and sort keys are
+// bit-identical to the CPU reference path.  SH colour is FP32 (it only feeds
+// the toleranced image).
+//
+// Reads 68 B (4D) / 44 B (3D) of geometry + 4*3K B of SH per Gaussian, all
+// coalesced from the component-major SoA pools; writes an 80 B SplatRec, a
+// depth key and a tile count.  Bound: HBM.
+#include "hgs_common.cuh"
+
+namespace hgs {
+
+namespace {
+
+struct M3 {
+    double a[3][3];
+};
+struct M4 {
+    double a[4][4];
+};
+
+// gauss_math.cpp:99-121
+__device__ inline M4 rot4_from_pair(const double ql[4], const double qr[4]) {
+    const double a = ql[0], b = ql[1], c = ql[2], d = ql[3];
+    const double L[4][4] = {{a, -b, -c, -d}, {b, a, -d, c}, {c, d, a, -b}, {d, -c, b, a}};
+    const double p = qr[0], q = qr[1], r = qr[2], s = qr[3];
+    const double R[4][4] = {{p, -q, -r, -s}, {q, p, s, -r}, {r, -s, p, q}, {s, r, -q, p}};
+    M4 out;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            double acc = L[i][0] * R[0][j];
+            acc = acc + L[i][1] * R[1][j];
+            acc = acc + L[i][2] * R[2][j];
+            acc = acc + L[i][3] * R[3][j];
+            out.a[i][j] = acc;
+        }
+    return out;
+}
+
+// gauss_math.cpp:159-162
+__device__ inline M4 build_cov4(const M4& rot, const double ls[4]) {
+    double e[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) e[j] = exp(ls[j]);
+    double m[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) m[i][j] = rot.a[i][j] * e[j];
+    M4 r;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            double s = m[i][0] * m[j][0];
+            s = s + m[i][1] * m[j][1];
+            s = s + m[i][2] * m[j][2];
+            s = s + m[i][3] * m[j][3];
+            r.a[i][j] = s;
+        }
+    return r;
+}
+
+// gauss_math.cpp:48-58
+__device__ inline bool quat_to_rot3(const double q[4], M3& r) {
+    double n = sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+    double w = q[0], x = q[1], y = q[2], z = q[3];
+    r.a[0][0] = 1 - 2 * (y * y + z * z);
+    r.a[0][1] = 2 * (x * y - z * w);
+    r.a[0][2] = 2 * (x * z + y * w);
+    r.a[1][0] = 2 * (x * y + z * w);
+    r.a[1][1] = 1 - 2 * (x * x + z * z);
+    r.a[1][2] = 2 * (y * z - x * w);
+    r.a[2][0] = 2 * (x * z - y * w);
+    r.a[2][1] = 2 * (y * z + x * w);
+    r.a[2][2] = 1 - 2 * (x * x + y * y);
+    return fabs(n - 1.0) <= 1e-6;
+}
+
+// gauss_math.cpp:154-157
+__device__ inline M3 build_cov3(const M3& rot, const double ls[3]) {
+    double e[3] = {exp(ls[0]), exp(ls[1]), exp(ls[2])};
+    double m[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) m[i][j] = rot.a[i][j] * e[j];
+    M3 r;
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            double s = m[i][0] * m[j][0];
+            s = s + m[i][1] * m[j][1];
+            s = s + m[i][2] * m[j][2];
+            r.a[i][j] = s;
+        }
+    return r;
+}
+
+// Cyclic Jacobi for the rare clamp_psd eigen path (gauss_math.cpp:164-173);
+// same algorithm and operation order as the oracle's jacobi_eig3.
+__device__ __noinline__ void jacobi_eig3(const M3& in, double ev[3], M3& v) {
+    M3 a = in;
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) v.a[i][j] = i == j ? 1.0 : 0.0;
+    for (int sweep = 0; sweep < 64; ++sweep) {
+        double off = fabs(a.a[0][1]) + fabs(a.a[0][2]) + fabs(a.a[1][2]);
+        double diag = fabs(a.a[0][0]) + fabs(a.a[1][1]) + fabs(a.a[2][2]);
+        if (off <= 1e-300 || off <= 1e-18 * diag) break;
+        for (int p = 0; p < 2; ++p)
+            for (int q = p + 1; q < 3; ++q) {
+                double apq = a.a[p][q];
+                if (apq == 0.0) continue;
+                double theta = (a.a[q][q] - a.a[p][p]) / (2.0 * apq);
+                double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+                double c = 1.0 / sqrt(t * t + 1.0), s = t * c;
+                for (int k = 0; k < 3; ++k) {
+                    double akp = a.a[k][p], akq = a.a[k][q];
+                    a.a[k][p] = c * akp - s * akq;
+                    a.a[k][q] = s * akp + c * akq;
+                }
+                for (int k = 0; k < 3; ++k) {
+                    double apk = a.a[p][k], aqk = a.a[q][k];
+                    a.a[p][k] = c * apk - s * aqk;
+                    a.a[q][k] = s * apk + c * aqk;
+                }
+                for (int k = 0; k < 3; ++k) {
+                    double vkp = v.a[k][p], vkq = v.a[k][q];
+                    v.a[k][p] = c * vkp - s * vkq;
+                    v.a[k][q] = s * vkp + c * vkq;
+                }
+            }
+    }
+    int idx[3] = {0, 1, 2};
+    // insertion sort ascending by eigenvalue (std::sort on 3 keys in the oracle)
+    for (int i = 1; i < 3; ++i)
+        for (int j = i; j > 0 && a.a[idx[j]][idx[j]] < a.a[idx[j - 1]][idx[j - 1]]; --j) {
+            int tmp = idx[j];
+            idx[j] = idx[j - 1];
+            idx[j - 1] = tmp;
+        }
+    M3 vs;
+    for (int c = 0; c < 3; ++c) {
+        ev[c] = a.a[idx[c]][idx[c]];
+        for (int r = 0; r < 3; ++r) vs.a[r][c] = v.a[r][idx[c]];
+    }
+    v = vs;
+}
+
+// clamp_psd's slow path: returns false if the matrix is indefinite.
+__device__ __noinline__ bool clamp_psd_slow(M3& m) {
+    M3 sym;
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) sym.a[i][j] = 0.5 * (m.a[i][j] + m.a[j][i]);
+    double ev[3];
+    M3 v;
+    jacobi_eig3(sym, ev, v);
+    double min_ev = fmin(ev[0], fmin(ev[1], ev[2]));
+    if (min_ev >= 1e-12) {
+        m = sym;
+        return true;
+    }
+    if (min_ev < -1e-8) return false;
+    M3 vd;
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) vd.a[i][j] = v.a[i][j] * fmax(ev[j], 1e-12);
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+            double s = vd.a[i][0] * v.a[j][0];
+            s = s + vd.a[i][1] * v.a[j][1];
+            s = s + vd.a[i][2] * v.a[j][2];
+            m.a[i][j] = s;
+        }
+    return true;
+}
+
+// SH colour in FP32 (sh.cpp:25-47, 73-83); coefficient k channel c at row
+// base + 3k + c.
+__device__ inline void eval_sh_f32(const float* __restrict__ p, int64_t cap, int i, int base, int deg,
+                                   float dx, float dy, float dz, float rgb[3]) {
+    float basis[16];
+    basis[0] = 0.28209479177387814f;
+    if (deg >= 1) {
+        basis[1] = -0.4886025119029199f * dy;
+        basis[2] = 0.4886025119029199f * dz;
+        basis[3] = -0.4886025119029199f * dx;
+    }
+    if (deg >= 2) {
+        float xx = dx * dx, yy = dy * dy, zz = dz * dz;
+        basis[4] = 1.0925484305920792f * dx * dy;
+        basis[5] = -1.0925484305920792f * dy * dz;
+        basis[6] = 0.31539156525252005f * (2.0f * zz - xx - yy);
+        basis[7] = -1.0925484305920792f * dx * dz;
+        basis[8] = 0.5462742152960396f * (xx - yy);
+        if (deg >= 3) {
+            basis[9] = -0.5900435899266435f * dy * (3.0f * xx - yy);
+            basis[10] = 2.890611442640554f * dx * dy * dz;
+            basis[11] = -0.4570457994644658f * dy * (4.0f * zz - xx - yy);
+            basis[12] = 0.3731763325901154f * dz * (2.0f * zz - 3.0f * xx - 3.0f * yy);
+            basis[13] = -0.4570457994644658f * dx * (4.0f * zz - xx - yy);
+            basis[14] = 1.445305721320277f * dz * (xx - yy);
+            basis[15] = -0.5900435899266435f * dx * (xx - 3.0f * yy);
+        }
+    }
+    const int K = sh_count(deg);
+    float acc[3] = {0.f, 0.f, 0.f};
+    for (int k = 0; k < K; ++k) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) acc[c] = fmaf(basis[k], __ldg(&p[(int64_t)(base + 3 * k + c) * cap + i]), acc[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) rgb[c] = fminf(fmaxf(acc[c] + 0.5f, 0.0f), 1.0f);
+}
+
+__device__ inline uint32_t f32_bits(double d) { return __float_as_uint(__double2float_rn(d)); }
+
+// project_3d (raster.cpp:26-64).  Returns the cull reason (CULL_NONE when
+// projected) and fills the geometric part of the record.
+__device__ inline uint32_t project_3d(const double m[3], const M3& cov, const DevCamera& cam, SplatRec& s,
+                                      double& depth, int& ntiles, int tiles_x) {
+    double p[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        double a = cam.R[i * 3 + 0] * m[0];
+        a = a + cam.R[i * 3 + 1] * m[1];
+        a = a + cam.R[i * 3 + 2] * m[2];
+        p[i] = a + cam.t[i];
+    }
+    const double z = p[2];
+    if (z < cam.near_ || z > cam.far_) return CULL_DEPTH;
+    depth = z;
+    const double sx = cam.fx * p[0] / z + cam.cx;
+    const double sy = cam.fy * p[1] / z + cam.cy;
+    double J[2][3];
+    J[0][0] = cam.fx / z;
+    J[0][1] = 0.0;
+    J[0][2] = -cam.fx * p[0] / (z * z);
+    J[1][0] = 0.0;
+    J[1][1] = cam.fy / z;
+    J[1][2] = -cam.fy * p[1] / (z * z);
+    double T[2][3];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            double a = J[i][0] * cam.R[0 * 3 + k];
+            a = a + J[i][1] * cam.R[1 * 3 + k];
+            a = a + J[i][2] * cam.R[2 * 3 + k];
+            T[i][k] = a;
+        }
+    double tc[2][3];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            double a = T[i][0] * cov.a[0][k];
+            a = a + T[i][1] * cov.a[1][k];
+            a = a + T[i][2] * cov.a[2][k];
+            tc[i][k] = a;
+        }
+    double c2[2][2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            double a = tc[i][0] * T[j][0];
+            a = a + tc[i][1] * T[j][1];
+            a = a + tc[i][2] * T[j][2];
+            c2[i][j] = a;
+        }
+    c2[0][0] += kLowPass;
+    c2[1][1] += kLowPass;
+    const double det = c2[0][0] * c2[1][1] - c2[0][1] * c2[1][0];
+    if (det <= 1e-12) return CULL_DEGENERATE;
+    s.c00 = c2[1][1] / det;
+    s.c01 = -c2[0][1] / det;
+    s.c10 = -c2[1][0] / det;
+    s.c11 = c2[0][0] / det;
+    const double mid = 0.5 * (c2[0][0] + c2[1][1]);
+    const double max_ev = mid + sqrt(fmax(0.0, mid * mid - det));
+    const int radius = (int)ceil(3.0 * sqrt(max_ev));
+    const int mx = (int)floor(sx), my = (int)floor(sy);
+    const int x0 = max(0, mx - radius), x1 = min(cam.width - 1, mx + radius);
+    const int y0 = max(0, my - radius), y1 = min(cam.height - 1, my + radius);
+    if (x0 > x1 || y0 > y1) return CULL_OFFSCREEN;
+    s.sx = sx;
+    s.sy = sy;
+    s.x0 = (int16_t)x0;
+    s.x1 = (int16_t)x1;
+    s.y0 = (int16_t)y0;
+    s.y1 = (int16_t)y1;
+    ntiles = (x1 / kTile - x0 / kTile + 1) * (y1 / kTile - y0 / kTile + 1);
+    (void)tiles_x;
+    return CULL_NONE;
+}
+
+__device__ inline double sigmoid(double x) { return 1.0 / (1.0 + exp(-x)); }
+
+}  // namespace
+
+// K1.  stats[0..5] = culled_depth, culled_offscreen, culled_degenerate,
+// culled_temporal, degenerate_temporal, projected.
+__global__ void __launch_bounds__(256) preprocess_kernel(
+    const float* __restrict__ p4, int64_t cap4, int n4, const float* __restrict__ p3, int64_t cap3,
+    int n3, int deg, DevCamera cam, double t, double cutoff, int tiles_x, SplatRec* __restrict__ rec,
+    uint32_t* __restrict__ depth_key, uint32_t* __restrict__ ntiles_out,
+    unsigned long long* __restrict__ stats, uint32_t* __restrict__ flags) {
+    const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+    const int n = n4 + n3;
+    uint32_t reason = CULL_DEPTH + 100;  // sentinel: inactive lane
+    uint32_t flag = 0;
+    if (gid < n) {
+        SplatRec s;
+        double mean3[3];
+        double depth = 0.0;
+        int ntiles = 0;
+        double alpha = 0.0;
+        bool ok = true;
+        if (gid < n4) {
+            const int i = gid;
+            double ql[4], qr[4], ls[4], mean4[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                ql[k] = __ldg(&p4[(int64_t)(R4_QL + k) * cap4 + i]);
+                qr[k] = __ldg(&p4[(int64_t)(R4_QR + k) * cap4 + i]);
+                ls[k] = __ldg(&p4[(int64_t)(R4_LS + k) * cap4 + i]);
+            }
+#pragma unroll
+            for (int k = 0; k < 3; ++k) mean4[k] = __ldg(&p4[(int64_t)(R4_MEAN + k) * cap4 + i]);
+            mean4[3] = __ldg(&p4[(int64_t)R4_MT * cap4 + i]);
+            const M4 cov4 = build_cov4(rot4_from_pair(ql, qr), ls);
+            // condition_at_time (gauss_math.cpp:175-186)
+            const double s44 = cov4.a[3][3];
+            if (s44 < 1e-12) {
+                reason = CULL_DEGEN_TEMPORAL;
+            } else {
+                const double cross[3] = {cov4.a[0][3], cov4.a[1][3], cov4.a[2][3]};
+                const double dt = t - mean4[3];
+                const double f = dt / s44;
+#pragma unroll
+                for (int k = 0; k < 3; ++k) mean3[k] = mean4[k] + cross[k] * f;
+                M3 c;
+#pragma unroll
+                for (int a = 0; a < 3; ++a)
+#pragma unroll
+                    for (int b = 0; b < 3; ++b) c.a[a][b] = cov4.a[a][b] - (cross[a] * cross[b]) / s44;
+                // clamp_psd: lambda_min(Schur complement) >= lambda_min(cov4) = exp(2 min s);
+                // the eigen-solve can only change the result when that bound is near 1e-12.
+                double smin = fmin(fmin(ls[0], ls[1]), fmin(ls[2], ls[3]));
+                double smax = fmax(fmax(ls[0], ls[1]), fmax(ls[2], ls[3]));
+                double lam_lo = exp(2.0 * smin), scale = exp(2.0 * smax);
+                if (!(lam_lo - 1e-13 * scale >= 1e-12)) ok = clamp_psd_slow(c);
+                if (!ok) flag |= FLAG_INDEFINITE;
+                const double w = exp(-0.5 * dt * dt / s44);
+                if (w < cutoff) {
+                    reason = CULL_TEMPORAL;
+                } else {
+                    reason = project_3d(mean3, c, cam, s, depth, ntiles, tiles_x);
+                    if (reason == CULL_NONE)
+                        alpha = fmin(sigmoid((double)__ldg(&p4[(int64_t)R4_OP * cap4 + i])) * w, kAlphaClamp);
+                }
+            }
+        } else {
+            const int i = gid - n4;
+            double q[4], ls[3];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) q[k] = __ldg(&p3[(int64_t)(R3_Q + k) * cap3 + i]);
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                ls[k] = __ldg(&p3[(int64_t)(R3_LS + k) * cap3 + i]);
+                mean3[k] = __ldg(&p3[(int64_t)(R3_MEAN + k) * cap3 + i]);
+            }
+            M3 rot;
+            if (!quat_to_rot3(q, rot)) flag |= FLAG_NONUNIT_QUAT;
+            const M3 cov3 = build_cov3(rot, ls);
+            reason = project_3d(mean3, cov3, cam, s, depth, ntiles, tiles_x);
+            if (reason == CULL_NONE)
+                alpha = fmin(sigmoid((double)__ldg(&p3[(int64_t)R3_OP * cap3 + i])), kAlphaClamp);
+        }
+        if (reason == CULL_NONE) {
+            // view direction (raster.cpp:83-85) and SH colour
+            double v[3] = {mean3[0] - cam.pos[0], mean3[1] - cam.pos[1], mean3[2] - cam.pos[2]};
+            double nrm = sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+            double d[3] = {0.0, 0.0, 1.0};
+            if (nrm > 0.0) {
+                d[0] = v[0] / nrm;
+                d[1] = v[1] / nrm;
+                d[2] = v[2] / nrm;
+            }
+            float rgb[3];
+            if (gid < n4)
+                eval_sh_f32(p4, cap4, gid, R4_SH, deg, (float)d[0], (float)d[1], (float)d[2], rgb);
+            else
+                eval_sh_f32(p3, cap3, gid - n4, R3_SH, deg, (float)d[0], (float)d[1], (float)d[2], rgb);
+            s.alpha = alpha;
+            s.alpha_f = (float)alpha;
+            s.r = rgb[0];
+            s.g = rgb[1];
+            s.b = rgb[2];
+            rec[gid] = s;
+            depth_key[gid] = f32_bits(depth);
+            ntiles_out[gid] = (uint32_t)ntiles;
+        } else {
+            ntiles_out[gid] = 0u;
+        }
+    }
+    // warp-aggregated RenderStats counters
+    const unsigned full = 0xffffffffu;
+#pragma unroll
+    for (int k = 0; k < kNumStats; ++k) {
+        const uint32_t want = k == 0 ? CULL_DEPTH : k == 1 ? CULL_OFFSCREEN : k == 2 ? CULL_DEGENERATE
+                             : k == 3 ? CULL_TEMPORAL : k == 4 ? CULL_DEGEN_TEMPORAL : CULL_NONE;
+        const unsigned b = __ballot_sync(full, reason == want);
+        if ((threadIdx.x & 31) == 0 && b) atomicAdd(&stats[k], (unsigned long long)__popc(b));
+    }
+    const unsigned fb = __reduce_or_sync(full, flag);
+    if ((threadIdx.x & 31) == 0 && fb) atomicOr(flags, fb);
+}
+
+}  // namespace hgs

@@ -1,0 +1,20 @@
+// primitives.cuh -- device-wide scan / radix sort (see primitives.cu)
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "hgs_common.cuh"
+
+namespace hgs {
+
+size_t scan_workspace_bytes(int n);
+// out[i] = sum(in[0..i)); *total (device, optional) = sum(in)
+void exclusive_scan_u32(const uint32_t* in, uint32_t* out, int n, uint32_t* total, uint32_t* ws,
+                        cudaStream_t st);
+
+size_t radix_workspace_bytes(int n);
+int radix_sort_pairs(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt, int n,
+                     int begin_bit, int end_bit, uint32_t* ws, cudaStream_t st);
+
+}  // namespace hgs

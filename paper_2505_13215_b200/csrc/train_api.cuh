@@ -1,0 +1,6 @@
+// train_api.cuh -- host-side entry points shared between capi.cu and train.cu
+#pragma once
+#include "ctx.cuh"
+
+hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, const double bg[3],
+                               const hgs_raster_opts* opts);

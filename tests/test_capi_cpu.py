@@ -1,0 +1,52 @@
+"""CPU-side checks of the C ABI: the library builds, loads without a GPU,
+exports every symbol include/hgs_gpu.h declares, and fails loudly (no CPU
+fallback) when no CUDA device is present."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "hgs_gpu.h")).read()
+    return sorted(set(re.findall(r"\b(hgs_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_header_symbols_exported():
+    from paper_2505_13215_b200 import _capi
+
+    L = _capi.lib()
+    missing = [s for s in declared_symbols() if not hasattr(L, s)]
+    assert not missing, missing
+
+
+def test_python_binding_covers_header():
+    from paper_2505_13215_b200 import _capi
+
+    assert set(declared_symbols()) <= set(_capi.EXPORTED)
+
+
+def test_no_cpu_fallback_without_device():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    from paper_2505_13215_b200 import _capi
+    from paper_2505_13215_b200.api import Context
+
+    with pytest.raises(_capi.CudaError):
+        Context(0)
+
+
+def test_product_does_not_reference_oracle():
+    """The product package never imports / links the oracle."""
+    pkg = os.path.join(ROOT, "paper_2505_13215_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".cpp", ".h")) or f == "Makefile":
+                txt = open(os.path.join(dirpath, f), errors="ignore").read()
+                assert "import oracle" not in txt and "from oracle" not in txt, f
+                assert "hgs_oracle" not in txt and "libhgs_oracle" not in txt, f

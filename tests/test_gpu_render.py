@@ -1,0 +1,162 @@
+"""GPU render parity: the sm_100a path against the FP64 oracle, through the C ABI.
+
+Gates (BASELINE.json north_star / SURVEY.md 8d):
+  * bit-exact: projected set, f32 depth bits, pixel boxes (hence tile
+    assignment), the full tile-sorted instance order, RenderStats;
+  * image: max |delta| <= 1e-4 and PSNR > 60 dB against the oracle.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2505_13215_b200.scene import HybridScene, ring_camera, synthetic_scene
+
+pytestmark = pytest.mark.gpu
+
+IMG_TOL = 1e-4  # max abs error vs the FP64 oracle (north_star)
+PSNR_MIN = 60.0
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    from paper_2505_13215_b200.api import Context
+
+    c = Context(0)
+    yield c
+    c.close()
+
+
+def psnr(a, b):
+    mse = float(np.mean((a.astype(np.float64) - b) ** 2))
+    return math.inf if mse == 0 else 10 * math.log10(1.0 / mse)
+
+
+def check_render(ctx, scene, cam, t, bg=(0.2, 0.2, 0.2), cutoff=0.05, threads=8):
+    scene = scene.as_float32_exact()
+    ctx.upload(scene)
+    out = ctx.render(cam, t, bg, weight_cutoff=cutoff, count_map=True, transmittance_map=True)
+    ref = O.rasterize(scene, cam, t, bg, num_threads=threads, weight_cutoff=cutoff, count_map=True,
+                      transmittance_map=True)
+    assert out["stats"] == ref["stats"]
+    # bit-exact projection: set, depth key, box
+    sp = ctx.debug_splats()
+    rs, _ = O.project_scene(scene, cam, t, cutoff)
+    assert (sp["gid"] == rs["gid"]).all()
+    assert (sp["depth_bits"] == rs["depth_bits"]).all()
+    assert (sp["box"] == np.stack([rs["x0"], rs["x1"], rs["y0"], rs["y1"]], 1)).all()
+    # bit-exact tile-sorted instance order
+    tiles, gids = ctx.debug_instances()
+    rt, rp = O.sorted_instances(scene, cam, t, cutoff)
+    assert len(tiles) == len(rt)
+    assert (tiles == rt).all()
+    assert (gids == rs["gid"][rp]).all()
+    # conic / alpha within FP64 rounding of the oracle
+    assert np.abs(sp["mean"] - np.stack([rs["sx"], rs["sy"]], 1)).max(initial=0) < 1e-9
+    assert np.abs(sp["alpha"] - rs["alpha"]).max(initial=0) < 1e-12
+    # image
+    err = np.abs(out["rgb"].astype(np.float64) - ref["rgb"]).max()
+    assert err <= IMG_TOL, err
+    assert psnr(out["rgb"], ref["rgb"]) > PSNR_MIN
+    assert (out["counts"] == ref["counts"]).all()
+    assert np.abs(out["transmittance"] - ref["transmittance"]).max() <= 1e-4
+    return out, ref
+
+
+def test_empty_scene_is_background(ctx):
+    cam = O.look_at([0, 0, -3], [0, 0, 0], [0, -1, 0], 50.0, 32, 32)
+    ctx.upload(HybridScene())
+    out = ctx.render(cam, 0.3, (0.1, 0.5, 0.9))
+    assert np.allclose(out["rgb"], np.array([0.1, 0.5, 0.9], dtype=np.float32))
+
+
+@pytest.mark.parametrize("seed", [43, 44, 45, 46])
+def test_random_mixed_scenes_match_oracle(ctx, seed):
+    rng = O.Rng(seed)
+    for _ in range(3):
+        scene = rng.random_scene(15, 15)
+        cam = rng.random_camera()
+        check_render(ctx, scene, cam, rng.uniform())
+
+
+@pytest.mark.parametrize("deg", [0, 1, 2, 3])
+def test_sh_degrees(ctx, deg):
+    rng = O.Rng(100 + deg)
+    scene = rng.random_scene(60, 60, deg)
+    cam = rng.random_camera(96, 72)
+    check_render(ctx, scene, cam, 0.5)
+
+
+def test_statics_only_and_dynamics_only(ctx):
+    rng = O.Rng(7)
+    check_render(ctx, rng.random_scene(80, 0, 1), rng.random_camera(80, 64), 0.2)
+    check_render(ctx, rng.random_scene(0, 80, 1), rng.random_camera(80, 64), 0.9)
+
+
+def test_edge_sizes_and_tile_boundaries(ctx):
+    """Images that are not a multiple of the 16-px tile, 1-px images."""
+    rng = O.Rng(8)
+    scene = rng.random_scene(40, 40, 2)
+    for w, h in [(1, 1), (17, 33), (33, 17), (129, 5)]:
+        cam = rng.random_camera(w, h)
+        check_render(ctx, scene, cam, 0.4)
+
+
+def test_culling_paths(ctx):
+    """Depth, temporal and degenerate-temporal culls counted like the reference."""
+    rng = O.Rng(9)
+    scene = rng.random_scene(20, 40, 1)
+    scene.log_s4[:5, :] = math.log(1e-7)  # Sigma_tt ~ 1e-14 -> degenerate_temporal
+    scene.mean_x[5:8] = [[0.0, 0.0, -40.0]] * 3  # behind / far
+    cam = rng.random_camera(64, 64)
+    out, ref = check_render(ctx, scene, cam, 0.5)
+    assert ref["stats"]["degenerate_temporal"] >= 1
+
+
+def test_invalid_camera_raises(ctx):
+    from paper_2505_13215_b200.api import Context  # noqa: F401
+
+    cam = O.look_at([0, 0, -3], [0, 0, 0], [0, -1, 0], 50.0, 32, 32)
+    cam.fx = -1.0
+    ctx.upload(HybridScene())
+    with pytest.raises(ValueError):
+        ctx.render(cam, 0.0)
+
+
+def test_dense_scene_many_instances(ctx):
+    """Crowded tiles (hundreds of splats per tile, early termination, fix-ups)."""
+    scene = synthetic_scene(3000, 1000, 3, seed=11, density_n=100)
+    cam = ring_camera(11, 160, 120)
+    check_render(ctx, scene, cam, 0.5)
+
+
+def test_c1_config_parity(ctx):
+    """configs[0]: 100k 4D Gaussians, 640x480, t = 0.5 (BASELINE.json)."""
+    scene = synthetic_scene(100_000, 0, 3, seed=1)
+    cam = ring_camera(1, 640, 480)
+    out, ref = check_render(ctx, scene, cam, 0.5)
+    info = ctx.render_info()
+    assert info["instances"] > 0
+
+
+def test_drop_in_rasterize_float64(ctx):
+    """hgs_rasterize: host double scene in, host double image out."""
+    from paper_2505_13215_b200.api import rasterize
+
+    rng = O.Rng(12)
+    scene = rng.random_scene(30, 30, 1).as_float32_exact()
+    cam = rng.random_camera(64, 48)
+    img = rasterize(scene, cam, 0.3, (0.1, 0.2, 0.3))
+    ref = O.rasterize(scene, cam, 0.3, (0.1, 0.2, 0.3))["rgb"]
+    assert img.dtype == np.float64 and img.shape == (48, 64, 3)
+    assert np.abs(img - ref).max() <= IMG_TOL
+
+
+def test_render_deterministic(ctx):
+    scene = synthetic_scene(20000, 5000, 3, seed=3)
+    cam = ring_camera(3, 320, 240)
+    ctx.upload(scene)
+    a = ctx.render(cam, 0.5)["rgb"]
+    b = ctx.render(cam, 0.5)["rgb"]
+    assert (a == b).all()
