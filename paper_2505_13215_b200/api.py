@@ -237,15 +237,19 @@ class Context:
 
     def loss_with_grad(self, gt: np.ndarray | None = None, ssim_lambda: float = 0.2, gt_device_ptr: int | None = None,
                        want_grad: bool = False):
-        g_out = np.empty(self._last_shape + (3,), dtype=np.float32) if want_grad else None
         loss = C.c_double()
+        g_out = None
         if gt_device_ptr is not None:
+            g_out = np.empty(self._last_shape + (3,), dtype=np.float32) if want_grad else None
             self._check(self._lib.hgs_loss_with_grad(self._h, C.c_void_p(gt_device_ptr), HGS_F32, 1,
                                                      float(ssim_lambda), C.byref(loss), ptr(g_out)))
         else:
             a = np.ascontiguousarray(gt)
             code = _dtype_code(a.dtype)
             a = a.astype(np.float64 if code == HGS_F64 else np.float32, copy=False)
+            if a.shape != self._last_shape + (3,):
+                raise ValueError("photometric_loss: image dimensions differ")
+            g_out = np.empty(a.shape, dtype=a.dtype) if want_grad else None  # same dtype as gt (C ABI)
             self._check(self._lib.hgs_loss_with_grad(self._h, ptr(a), code, 0, float(ssim_lambda), C.byref(loss),
                                                      ptr(g_out)))
         return (loss.value, g_out) if want_grad else loss.value

@@ -18,16 +18,6 @@ using namespace hgs;
 
 namespace {
 
-struct Counters {
-    unsigned long long stats[kNumStats];
-    uint32_t flags;
-    uint32_t V;
-    uint32_t I;
-    uint32_t fix_count;
-    uint32_t skipped;
-    uint32_t pad[3];
-};
-
 hgs_status fail(hgs_ctx* ctx, hgs_status s, const std::string& m) {
     if (ctx) ctx->err = m;
     return s;
@@ -214,6 +204,16 @@ hgs_status check_flags(hgs_ctx* ctx, uint32_t flags) {
 
 }  // namespace
 
+// Row-major host rows -> given SoA destinations (used for Adam state upload).
+hgs_status hgs_upload_rows(hgs_ctx* ctx, const hgs_host_scene* s, int dtype, float* dst4, float* dst3) {
+    hgs_status r = upload_pool(ctx, s, kDyn, 7, ctx->n4, ctx->cap4, dst4, dtype);
+    if (r != HGS_OK) return r;
+    r = upload_pool(ctx, s, kSta, 5, ctx->n3, ctx->cap3, dst3, dtype);
+    if (r != HGS_OK) return r;
+    CK(cudaStreamSynchronize(ctx->stream));
+    return HGS_OK;
+}
+
 // ====================================================================== render
 // The full K1 -> sort -> K2 -> sort -> K4 pipeline; leaves the tape in ctx.
 hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, const double bg[3],
@@ -245,6 +245,7 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
     CK(cudaMemsetAsync(dc, 0, sizeof(Counters), st));
     CK(ctx->img.ensure(npx * 3 * sizeof(float)));
     CK(ctx->last.ensure(npx * sizeof(uint32_t)));
+    CK(ctx->tfinal.ensure(npx * sizeof(float)));
     CK(ctx->fix_list.ensure(npx * sizeof(uint32_t)));
     if (want_trans) CK(ctx->trans.ensure(npx * sizeof(float)));
     if (want_count) CK(ctx->count.ensure(npx * sizeof(uint32_t)));
@@ -332,13 +333,13 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
     raster_fwd_kernel<<<n_tiles, 256, 0, st>>>(
         ctx->ranges.as<uint2>(), inst_vals, ctx->fast_sorted.as<SplatFast>(), ctx->rec_sorted.as<SplatRec>(), W, H,
         tiles_x, (float)bg[0], (float)bg[1], (float)bg[2], ctx->img.as<float>(), ctx->last.as<uint32_t>(),
-        want_trans ? ctx->trans.as<float>() : nullptr, want_count ? ctx->count.as<uint32_t>() : nullptr,
+        ctx->tfinal.as<float>(), want_trans ? ctx->trans.as<float>() : nullptr, want_count ? ctx->count.as<uint32_t>() : nullptr,
         ctx->fix_list.as<uint32_t>(), &dc->fix_count);
     CKL();
     raster_fixup_kernel<<<ctx->sms * 2, 128, 0, st>>>(
         ctx->fix_list.as<uint32_t>(), &dc->fix_count, ctx->ranges.as<uint2>(), inst_vals,
         ctx->rec_sorted.as<SplatRec>(), W, tiles_x, bg[0], bg[1], bg[2], ctx->img.as<float>(),
-        ctx->last.as<uint32_t>(), want_trans ? ctx->trans.as<float>() : nullptr,
+        ctx->last.as<uint32_t>(), ctx->tfinal.as<float>(), want_trans ? ctx->trans.as<float>() : nullptr,
         want_count ? ctx->count.as<uint32_t>() : nullptr);
     CKL();
     CK(cudaMemcpyAsync(hc, dc, sizeof(Counters), cudaMemcpyDeviceToHost, st));
@@ -384,12 +385,12 @@ void hgs_ctx_destroy(hgs_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
-    DBuf* bufs[] = {&ctx->p4, &ctx->p3, &ctx->g4, &ctx->g3, &ctx->m4, &ctx->v4, &ctx->m3, &ctx->v3, &ctx->gn4,
+    DBuf* bufs[] = {&ctx->p4, &ctx->p3, &ctx->p4_alt, &ctx->m4_alt, &ctx->v4_alt, &ctx->gbuf, &ctx->scratch, &ctx->m4, &ctx->v4, &ctx->m3, &ctx->v3, &ctx->gn4,
                     &ctx->gn3, &ctx->cnt4, &ctx->cnt3, &ctx->sn4, &ctx->sn3, &ctx->rec, &ctx->depth_key,
                     &ctx->ntiles, &ctx->visflag, &ctx->vispos, &ctx->sort_k, &ctx->sort_v, &ctx->sort_k2,
                     &ctx->sort_v2, &ctx->rec_sorted, &ctx->fast_sorted, &ctx->ntiles_sorted, &ctx->inst_off,
                     &ctx->inst_k, &ctx->inst_v, &ctx->inst_k2, &ctx->inst_v2, &ctx->ranges, &ctx->scan_ws,
-                    &ctx->sort_ws, &ctx->counters, &ctx->img, &ctx->last, &ctx->trans, &ctx->count,
+                    &ctx->sort_ws, &ctx->counters, &ctx->img, &ctx->last, &ctx->tfinal, &ctx->trans, &ctx->count,
                     &ctx->fix_list, &ctx->accum, &ctx->lgrad, &ctx->gt_stage, &ctx->loss_ws, &ctx->stage};
     for (DBuf* b : bufs) b->release();
     ctx->pinned.release();
@@ -428,10 +429,23 @@ hgs_status hgs_scene_upload(hgs_ctx* ctx, const hgs_host_scene* s, int dtype) {
     ctx->cap3 = round_cap(s->n3 + s->n4);  // room for every 4D Gaussian to convert
     const size_t b4 = (size_t)rows4(ctx->deg) * ctx->cap4 * sizeof(float);
     const size_t b3 = (size_t)rows3(ctx->deg) * ctx->cap3 * sizeof(float);
-    for (DBuf* b : {&ctx->p4, &ctx->g4, &ctx->m4, &ctx->v4}) CK(b->ensure(b4));
-    for (DBuf* b : {&ctx->p3, &ctx->g3, &ctx->m3, &ctx->v3}) CK(b->ensure(b3));
-    for (DBuf* b : {&ctx->g4, &ctx->m4, &ctx->v4}) CK(cudaMemsetAsync(b->p, 0, b4, ctx->stream));
-    for (DBuf* b : {&ctx->g3, &ctx->m3, &ctx->v3}) CK(cudaMemsetAsync(b->p, 0, b3, ctx->stream));
+    for (DBuf* b : {&ctx->p4, &ctx->m4, &ctx->v4, &ctx->p4_alt, &ctx->m4_alt, &ctx->v4_alt}) CK(b->ensure(b4));
+    for (DBuf* b : {&ctx->p3, &ctx->m3, &ctx->v3}) CK(b->ensure(b3));
+    for (DBuf* b : {&ctx->m4, &ctx->v4}) CK(cudaMemsetAsync(b->p, 0, b4, ctx->stream));
+    for (DBuf* b : {&ctx->m3, &ctx->v3}) CK(cudaMemsetAsync(b->p, 0, b3, ctx->stream));
+    {
+        const int64_t f4 = (int64_t)rows4(ctx->deg) * ctx->cap4, f3 = (int64_t)rows3(ctx->deg) * ctx->cap3;
+        ctx->gbuf_floats = f4 + f3 + 2 * ctx->cap4 + 2 * ctx->cap3;
+        CK(ctx->gbuf.ensure((size_t)ctx->gbuf_floats * 4));
+        CK(cudaMemsetAsync(ctx->gbuf.p, 0, (size_t)ctx->gbuf_floats * 4, ctx->stream));
+        float* g = ctx->gbuf.as<float>();
+        ctx->g4 = g;
+        ctx->g3 = g + f4;
+        ctx->dgn4 = ctx->g3 + f3;
+        ctx->dgn3 = ctx->dgn4 + ctx->cap4;
+        ctx->dcnt4 = ctx->dgn3 + ctx->cap3;
+        ctx->dcnt3 = ctx->dcnt4 + ctx->cap4;
+    }
     for (DBuf* b : {&ctx->gn4, &ctx->cnt4, &ctx->sn4}) {
         CK(b->ensure((size_t)ctx->cap4 * 4));
         CK(cudaMemsetAsync(b->p, 0, (size_t)ctx->cap4 * 4, ctx->stream));

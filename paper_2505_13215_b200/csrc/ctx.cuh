@@ -56,6 +56,17 @@ struct HostPinned {
     }
 };
 
+// Per-render device counters (RenderStats, flags, totals).
+struct Counters {
+    unsigned long long stats[kNumStats];
+    uint32_t flags;
+    uint32_t V;
+    uint32_t I;
+    uint32_t fix_count;
+    uint32_t skipped;
+    uint32_t pad[3];
+};
+
 }  // namespace hgs
 
 struct hgs_ctx {
@@ -70,10 +81,19 @@ struct hgs_ctx {
     int deg = 1;
     double tau = 0.5, extent = 1.0;
     hgs::DBuf p4, p3;      // params
-    hgs::DBuf g4, g3;      // gradients (same layout)
+    hgs::DBuf p4_alt;      // compaction target of the 4D sweep
+    hgs::DBuf m4_alt, v4_alt;
+    // Packed gradient buffer (one contiguous allreduce payload):
+    //   [g4: rows4*cap4 | g3: rows3*cap3 | dgn4: cap4 | dgn3: cap3 | dcnt4: cap4 | dcnt3: cap3]
+    // g* share the parameter layout; d* are this step's densify-statistic
+    // deltas (raw per-image screen norms and observation counts), folded into
+    // gn/cnt by the Adam kernel.
+    hgs::DBuf gbuf;
+    float *g4 = nullptr, *g3 = nullptr, *dgn4 = nullptr, *dgn3 = nullptr, *dcnt4 = nullptr, *dcnt3 = nullptr;
+    int64_t gbuf_floats = 0;
     hgs::DBuf m4, v4, m3, v3;  // Adam moments
     hgs::DBuf gn4, gn3;    // densify grad_norm (float)
-    hgs::DBuf cnt4, cnt3;  // densify counts (u32)
+    hgs::DBuf cnt4, cnt3;  // densify counts (float, exact below 2^24)
     hgs::DBuf sn4, sn3;    // screen_norm of the last backward (float)
     uint64_t step = 0;
 
@@ -84,11 +104,12 @@ struct hgs_ctx {
     hgs::DBuf inst_k, inst_v, inst_k2, inst_v2;       // tile sort (I)
     hgs::DBuf ranges, scan_ws, sort_ws;
     hgs::DBuf counters;  // [0..5] stats u64, [6] flags, fix_count, totals...
-    hgs::DBuf img, last, trans, count, fix_list;
+    hgs::DBuf img, last, tfinal, trans, count, fix_list;
     hgs::DBuf accum;     // backward per-sorted-splat accumulators
     hgs::DBuf lgrad;     // dL/dimage (device float)
     hgs::DBuf gt_stage;  // staged ground truth
-    hgs::DBuf loss_ws;   // loss scratch
+    hgs::DBuf loss_ws;   // loss scratch (SSIM maps)
+    hgs::DBuf scratch;   // small device scalars (loss sums, skip counts, leakage)
     hgs::DBuf stage;     // upload / download staging
     hgs::HostPinned pinned;
 

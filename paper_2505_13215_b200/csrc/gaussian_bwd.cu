@@ -8,7 +8,7 @@
 // complement backward and the isoclinic rotation factors.  Writes
 // grad += scale * d, the per-image screen-space norm, and the densification
 // statistics (train.cpp:433-444).  Coalesced SoA reads/writes; HBM bound.
-#include "hgs_common.cuh"
+#include "kernels.cuh"
 
 namespace hgs {
 
@@ -88,8 +88,8 @@ __global__ void __launch_bounds__(128) gaussian_bwd_kernel(
     int V, const uint32_t* __restrict__ sorted_gid, const float* __restrict__ accum, int acc_stride, int n4,
     const float* __restrict__ p4, int64_t cap4, const float* __restrict__ p3, int64_t cap3, int deg, DevCamera cam,
     double t, double scale, float* __restrict__ g4, float* __restrict__ g3, float* __restrict__ sn4,
-    float* __restrict__ sn3, float* __restrict__ gn4, float* __restrict__ gn3, uint32_t* __restrict__ cnt4,
-    uint32_t* __restrict__ cnt3, const double* __restrict__ conic_src, int conic_stride) {
+    float* __restrict__ sn3, float* __restrict__ gn4, float* __restrict__ gn3, float* __restrict__ cnt4,
+    float* __restrict__ cnt3, const double* __restrict__ conic_src, int conic_stride) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= V) return;
     const float* acc = accum + (size_t)j * acc_stride;
@@ -279,7 +279,7 @@ __global__ void __launch_bounds__(128) gaussian_bwd_kernel(
         sn3[i] = (float)screen_norm;
         if (screen_norm > 0.0) {
             gn3[i] += (float)screen_norm;
-            cnt3[i] += 1u;
+            cnt3[i] += 1.0f;
         }
     } else {
         double d_weight = 0.0;
@@ -355,7 +355,7 @@ __global__ void __launch_bounds__(128) gaussian_bwd_kernel(
         sn4[i] = (float)screen_norm;
         if (screen_norm > 0.0) {
             gn4[i] += (float)screen_norm;
-            cnt4[i] += 1u;
+            cnt4[i] += 1.0f;
         }
     }
 }

@@ -22,13 +22,73 @@ __global__ void tile_ranges_kernel(const uint32_t* __restrict__ keys, int n, uin
 __global__ void raster_fwd_kernel(const uint2* __restrict__ ranges, const uint32_t* __restrict__ inst_val,
                                   const SplatFast* __restrict__ fast, const SplatRec* __restrict__ exact, int W, int H,
                                   int tiles_x, float bg_r, float bg_g, float bg_b, float* __restrict__ out_rgb,
-                                  uint32_t* __restrict__ out_last, float* __restrict__ out_trans,
-                                  uint32_t* __restrict__ out_count, uint32_t* __restrict__ fix_list,
+                                  uint32_t* __restrict__ out_last, float* __restrict__ out_tfinal,
+                                  float* __restrict__ out_trans, uint32_t* __restrict__ out_count,
+                                  uint32_t* __restrict__ fix_list,
                                   uint32_t* __restrict__ fix_count);
 __global__ void raster_fixup_kernel(const uint32_t* __restrict__ fix_list, const uint32_t* __restrict__ fix_count,
                                     const uint2* __restrict__ ranges, const uint32_t* __restrict__ inst_val,
                                     const SplatRec* __restrict__ exact, int W, int tiles_x, double bg_r, double bg_g,
                                     double bg_b, float* __restrict__ out_rgb, uint32_t* __restrict__ out_last,
-                                    float* __restrict__ out_trans, uint32_t* __restrict__ out_count);
+                                    float* __restrict__ out_tfinal, float* __restrict__ out_trans,
+                                    uint32_t* __restrict__ out_count);
+
+}  // namespace hgs
+
+namespace hgs {
+
+// raster_bwd.cu (K6)
+constexpr int kAccStrideHost = 12;
+__global__ void raster_bwd_kernel(const uint2* __restrict__ ranges, const uint32_t* __restrict__ inst_val,
+                                  const SplatFast* __restrict__ fast, const SplatRec* __restrict__ exact, int W, int H,
+                                  int tiles_x, const float* __restrict__ tfinal, const uint32_t* __restrict__ last_arr,
+                                  const float* __restrict__ dL_dimg, float bg_r, float bg_g, float bg_b,
+                                  float* __restrict__ accum);
+__global__ void raster_bwd_exact_kernel(const uint32_t* __restrict__ fix_list, const uint32_t* __restrict__ fix_count,
+                                        const uint2* __restrict__ ranges, const uint32_t* __restrict__ inst_val,
+                                        const SplatRec* __restrict__ exact, int W, int tiles_x, double bg_r,
+                                        double bg_g, double bg_b, const uint32_t* __restrict__ last_arr,
+                                        const float* __restrict__ dL_dimg, float* __restrict__ accum);
+// gaussian_bwd.cu (K7)
+__global__ void gaussian_bwd_kernel(int V, const uint32_t* __restrict__ sorted_gid, const float* __restrict__ accum,
+                                    int acc_stride, int n4, const float* __restrict__ p4, int64_t cap4,
+                                    const float* __restrict__ p3, int64_t cap3, int deg, DevCamera cam, double t,
+                                    double scale, float* __restrict__ g4, float* __restrict__ g3,
+                                    float* __restrict__ sn4, float* __restrict__ sn3, float* __restrict__ gn4,
+                                    float* __restrict__ gn3, float* __restrict__ cnt4, float* __restrict__ cnt3,
+                                    const double* __restrict__ conic_src, int conic_stride);
+// loss.cu (K5)
+void set_ssim_window();
+__global__ void ssim_fwd_kernel(const float* __restrict__ a, const float* __restrict__ b, int W, int H,
+                                float* __restrict__ maps, double* __restrict__ ssim_sum);
+__global__ void ssim_bwd_kernel(const float* __restrict__ a, const float* __restrict__ b, int W, int H,
+                                const float* __restrict__ maps, float lambda, int with_ssim, float* __restrict__ grad,
+                                double* __restrict__ l1_sum);
+// adam.cu (K8)
+struct AdamArgs {
+    float b1, b2, one_m_b1, one_m_b2;
+    float inv_bc1, inv_bc2;
+    float lr_mean, lr_mean_t, lr_quat, lr_scales, lr_opacity, lr_sh;
+};
+__global__ void adam_kernel(float* __restrict__ p4, float* __restrict__ g4, float* __restrict__ m4,
+                            float* __restrict__ v4, int64_t cap4, int n4, float* __restrict__ p3,
+                            float* __restrict__ g3, float* __restrict__ m3, float* __restrict__ v3, int64_t cap3,
+                            int n3, int deg, AdamArgs A, unsigned long long* __restrict__ skipped_total,
+                            uint32_t* __restrict__ flags);
+__global__ void fold_stats_kernel(float* __restrict__ gn, float* __restrict__ cnt, float* __restrict__ dgn,
+                                  float* __restrict__ dcnt, int n);
+// convert.cu (K9)
+__global__ void convert_mask_kernel(const float* __restrict__ p4, int64_t cap4, int n4, double s_star,
+                                    uint32_t* __restrict__ mask);
+__global__ void convert_rows_kernel(const float* __restrict__ p4, const float* __restrict__ m4,
+                                    const float* __restrict__ v4, int64_t cap4, int n4,
+                                    const uint32_t* __restrict__ mask, const uint32_t* __restrict__ pos,
+                                    float* __restrict__ p3, float* __restrict__ m3, float* __restrict__ v3,
+                                    int64_t cap3, int n3, int deg, long long* __restrict__ moved,
+                                    unsigned long long* __restrict__ max_leak_bits, double* __restrict__ leak_sum,
+                                    uint32_t* __restrict__ flags);
+__global__ void compact_survivors_kernel(const float* __restrict__ src, float* __restrict__ dst, int rows,
+                                         int64_t cap4, int n4, const uint32_t* __restrict__ mask,
+                                         const uint32_t* __restrict__ pos);
 
 }  // namespace hgs

@@ -1,19 +1,20 @@
 // raster_bwd.cu -- K6: tile rasterizer backward (backward.cpp:178-222).
 //
-// One CTA per tile, one thread per pixel, walking the tile list FRONT TO BACK
-// (the same order and the same per-pair arithmetic as K4, so every
-// contribute/skip decision is reproduced; the loop stops at the forward's
-// recorded last contributor).  The reference's reverse sweep needs the suffix
-// colour S_i = sum_{j>i} c_j a_j T_j + T_final*bg; front to back it is
-// S_i = C_out - P_i with P_i the inclusive prefix, so no division by (1 - a)
-// is needed to recover T.
+// One CTA per tile, one thread per pixel, re-evaluating every pair with the
+// same arithmetic as K4 (so every contribute/skip decision is reproduced; the
+// walk is bounded by the forward's
+// recorded last contributor).  Like the reference it walks each pixel's list
+// BACK TO FRONT from the forward's last contributor, accumulating the suffix
+// colour S_i = sum_{j>i} c_j a_j T_j + T_final*bg by addition (accurate for
+// deep, nearly occluded splats, unlike C_out - prefix) and recovering
+// T_i = T_{i+1} / (1 - a_i) from the stored final transmittance.
 //
 // Per splat and warp the 9 accumulators are reduced with a transposing
 // butterfly (14 shuffles instead of 45), summed across warps with shared
 // atomics, and flushed once per tile batch with vector red.global.add.
 // Pixels the forward handed to the FP64 fix-up are back-propagated by
 // raster_bwd_exact_kernel with the oracle's own reverse sweep.
-#include "raster_common.cuh"
+#include "kernels.cuh"
 
 namespace hgs {
 
@@ -71,11 +72,12 @@ constexpr int kAccStride = 12;
 
 __global__ void __launch_bounds__(256) raster_bwd_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ inst_val, const SplatFast* __restrict__ fast,
-    const SplatRec* __restrict__ exact, int W, int H, int tiles_x, const float* __restrict__ img,
-    const uint32_t* __restrict__ last_arr, const float* __restrict__ dL_dimg, float* __restrict__ accum) {
+    const SplatRec* __restrict__ exact, int W, int H, int tiles_x, const float* __restrict__ tfinal,
+    const uint32_t* __restrict__ last_arr, const float* __restrict__ dL_dimg, float bg_r, float bg_g, float bg_b,
+    float* __restrict__ accum) {
     __shared__ SplatFast s_fast[kBatchB];
-    __shared__ SplatRec s_exact[kBatchB];
-    __shared__ float4 s_conic[kBatchB];          // float conic (c00, c01, c10, c11)
+    __shared__ uint32_t s_j[kBatchB];
+    __shared__ float4 s_conic[kBatchB];  // float conic (c00, c01, c10, c11)
     __shared__ float s_acc[kBatchB][kAccStride - 3];
     __shared__ uint32_t s_maxlast;
     const int tile = blockIdx.x;
@@ -88,16 +90,14 @@ __global__ void __launch_bounds__(256) raster_bwd_kernel(
     const double pcx = (double)px + 0.5, pcy = (double)py + 0.5;
 
     uint32_t last = rg.x;
-    float gr = 0.f, gg = 0.f, gb = 0.f, Cr = 0.f, Cg = 0.f, Cb = 0.f;
+    float gr = 0.f, gg = 0.f, gb = 0.f, T = 1.f;
     if (inside) {
         const int pix = py * W + px;
         const uint32_t l = last_arr[pix];
         gr = dL_dimg[pix * 3 + 0];
         gg = dL_dimg[pix * 3 + 1];
         gb = dL_dimg[pix * 3 + 2];
-        Cr = img[pix * 3 + 0];
-        Cg = img[pix * 3 + 1];
-        Cb = img[pix * 3 + 2];
+        T = tfinal[pix];
         // flagged pixels go through the exact kernel; zero gradient = untouched (backward.cpp:188)
         if (!(l & 0x80000000u) && (gr != 0.f || gg != 0.f || gb != 0.f)) last = l;
     }
@@ -107,21 +107,25 @@ __global__ void __launch_bounds__(256) raster_bwd_kernel(
     __syncthreads();
     const uint32_t end = s_maxlast;
 
-    float T = 1.0f, Pr = 0.f, Pg = 0.f, Pb = 0.f;
-    for (uint32_t base = rg.x; base < end; base += kBatchB) {
-        const uint32_t idx = base + threadIdx.x;
-        if (idx < end) {
-            const uint32_t j = inst_val[idx];
+    // Reverse sweep (backward.cpp:204-221): suffix S starts at T_final * bg and
+    // accumulates c_j a_j T_j from the back, so it stays accurate relative to
+    // its own (possibly tiny) magnitude; T_i = T_{i+1} / (1 - a_i).
+    float Sr = T * bg_r, Sg = T * bg_g, Sb = T * bg_b;
+    const int nbatch = (int)((end - rg.x + kBatchB - 1) / kBatchB);
+    for (int bi = nbatch - 1; bi >= 0; --bi) {
+        const uint32_t base = rg.x + (uint32_t)bi * kBatchB;
+        const int nb = (int)min((uint32_t)kBatchB, end - base);
+        if ((int)threadIdx.x < nb) {
+            const uint32_t j = inst_val[base + threadIdx.x];
             s_fast[threadIdx.x] = fast[j];
-            const SplatRec e = exact[j];
-            s_exact[threadIdx.x] = e;
+            const SplatRec& e = exact[j];
+            s_j[threadIdx.x] = j;
             s_conic[threadIdx.x] = make_float4((float)e.c00, (float)e.c01, (float)e.c10, (float)e.c11);
         }
 #pragma unroll
         for (int q = 0; q < kAccStride - 3; ++q) s_acc[threadIdx.x][q] = 0.f;
         __syncthreads();
-        const int nb = min((uint32_t)kBatchB, end - base);
-        for (int k = 0; k < nb; ++k) {
+        for (int k = nb - 1; k >= 0; --k) {
             const uint32_t gidx = base + k;
             float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
             float v8 = 0.f;
@@ -129,19 +133,21 @@ __global__ void __launch_bounds__(256) raster_bwd_kernel(
             if (gidx < last) {
                 const SplatFast& f = s_fast[k];
                 if (!(px < f.x0 || px > f.x1 || py < f.y0 || py > f.y1)) {
-                    const float x = pair_x(f, s_exact[k], pxc, pyc, pcx, pcy);
+                    const float x = pair_x(f, exact[s_j[k]], pxc, pyc, pcx, pcy);
                     float g;
-                    const float a = pair_alpha(f, s_exact[k], x, pcx, pcy, g);
+                    const float a = pair_alpha(f, exact[s_j[k]], x, pcx, pcy, g);
                     if (a >= 0.0f) {
                         contrib = true;
-                        const float w = a * T;
-                        Pr = fmaf(f.r, w, Pr);
-                        Pg = fmaf(f.g, w, Pg);
-                        Pb = fmaf(f.b, w, Pb);
                         const float inv = __frcp_rn(1.0f - a);
-                        // d_a = g_pix . (rgb * T_i - S_i / (1 - a)), S_i = C_out - P_i
-                        const float d_a = gr * (f.r * T - (Cr - Pr) * inv) + gg * (f.g * T - (Cg - Pg) * inv) +
-                                          gb * (f.b * T - (Cb - Pb) * inv);
+                        const float Ti = T * inv;  // transmittance before this splat
+                        const float w = a * Ti;
+                        // d_a = g_pix . (rgb * T_i - S / (1 - a))
+                        const float d_a = gr * fmaf(f.r, Ti, -Sr * inv) + gg * fmaf(f.g, Ti, -Sg * inv) +
+                                          gb * fmaf(f.b, Ti, -Sb * inv);
+                        Sr = fmaf(f.r, w, Sr);
+                        Sg = fmaf(f.g, w, Sg);
+                        Sb = fmaf(f.b, w, Sb);
+                        T = Ti;
                         v[0] = w * gr;
                         v[1] = w * gg;
                         v[2] = w * gb;
@@ -149,8 +155,8 @@ __global__ void __launch_bounds__(256) raster_bwd_kernel(
                         const float d_g = f.alpha_f * d_a;
                         float dx, dy;
                         if (f.fp64) {
-                            dx = (float)__dsub_rn(pcx, s_exact[k].sx);
-                            dy = (float)__dsub_rn(pcy, s_exact[k].sy);
+                            dx = (float)__dsub_rn(pcx, exact[s_j[k]].sx);
+                            dy = (float)__dsub_rn(pcy, exact[s_j[k]].sy);
                         } else {
                             dx = __fsub_rn(__fsub_rn(pxc, f.sx_hi), f.sx_lo);
                             dy = __fsub_rn(__fsub_rn(pyc, f.sy_hi), f.sy_lo);
@@ -163,7 +169,6 @@ __global__ void __launch_bounds__(256) raster_bwd_kernel(
                         v[6] = hc * dx * dx;
                         v[7] = hc * dx * dy;
                         v8 = hc * dy * dy;
-                        T *= 1.0f - a;
                     }
                 }
             }
@@ -182,7 +187,7 @@ __global__ void __launch_bounds__(256) raster_bwd_kernel(
 #pragma unroll
             for (int q = 0; q < 9; ++q) nz |= a[q] != 0.f;
             if (nz) {
-                float* dst = accum + (size_t)inst_val[base + threadIdx.x] * kAccStride;
+                float* dst = accum + (size_t)s_j[threadIdx.x] * kAccStride;
                 red_add_v4(dst, a[0], a[1], a[2], a[3]);
                 red_add_v4(dst + 4, a[4], a[5], a[6], a[7]);
                 atomicAdd(dst + 8, a[8]);

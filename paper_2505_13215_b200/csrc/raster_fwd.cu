@@ -103,10 +103,11 @@ constexpr int kBatch = 256;
 __global__ void __launch_bounds__(256) raster_fwd_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ inst_val, const SplatFast* __restrict__ fast,
     const SplatRec* __restrict__ exact, int W, int H, int tiles_x, float bg_r, float bg_g, float bg_b,
-    float* __restrict__ out_rgb, uint32_t* __restrict__ out_last, float* __restrict__ out_trans,
-    uint32_t* __restrict__ out_count, uint32_t* __restrict__ fix_list, uint32_t* __restrict__ fix_count) {
+    float* __restrict__ out_rgb, uint32_t* __restrict__ out_last, float* __restrict__ out_tfinal,
+    float* __restrict__ out_trans, uint32_t* __restrict__ out_count, uint32_t* __restrict__ fix_list,
+    uint32_t* __restrict__ fix_count) {
     __shared__ SplatFast s_fast[kBatch];
-    __shared__ SplatRec s_exact[kBatch];
+    __shared__ uint32_t s_j[kBatch];
     const int tile = blockIdx.x;
     const int tx = tile % tiles_x, ty = tile / tiles_x;
     const int px = tx * kTile + (threadIdx.x & 15);
@@ -127,7 +128,7 @@ __global__ void __launch_bounds__(256) raster_fwd_kernel(
         if (idx < rg.y) {
             const uint32_t j = inst_val[idx];
             s_fast[threadIdx.x] = fast[j];
-            s_exact[threadIdx.x] = exact[j];
+            s_j[threadIdx.x] = j;
         }
         __syncthreads();
         const int nb = min((uint32_t)kBatch, rg.y - base);
@@ -135,9 +136,9 @@ __global__ void __launch_bounds__(256) raster_fwd_kernel(
             const SplatFast& f = s_fast[k];
             if (px < f.x0 || px > f.x1 || py < f.y0 || py > f.y1) continue;
             ++count;
-            const float x = pair_x(f, s_exact[k], pxc, pyc, pcx, pcy);
+            const float x = pair_x(f, exact[s_j[k]], pxc, pyc, pcx, pcy);
             float g;
-            const float a = pair_alpha(f, s_exact[k], x, pcx, pcy, g);
+            const float a = pair_alpha(f, exact[s_j[k]], x, pcx, pcy, g);
             if (a < 0.0f) continue;
             const float w = a * T;
             cr = fmaf(f.r, w, cr);
@@ -160,6 +161,7 @@ __global__ void __launch_bounds__(256) raster_fwd_kernel(
     out_rgb[pix * 3 + 1] = fmaf(T, bg_g, cg);
     out_rgb[pix * 3 + 2] = fmaf(T, bg_b, cb);
     out_last[pix] = last | (flagged ? 0x80000000u : 0u);
+    out_tfinal[pix] = T;
     if (out_trans) out_trans[pix] = T;
     if (out_count) out_count[pix] = count;
     if (flagged) fix_list[atomicAdd(fix_count, 1u)] = (uint32_t)pix;
@@ -171,7 +173,7 @@ __global__ void __launch_bounds__(128) raster_fixup_kernel(
     const uint32_t* __restrict__ fix_list, const uint32_t* __restrict__ fix_count, const uint2* __restrict__ ranges,
     const uint32_t* __restrict__ inst_val, const SplatRec* __restrict__ exact, int W, int tiles_x, double bg_r,
     double bg_g, double bg_b, float* __restrict__ out_rgb, uint32_t* __restrict__ out_last,
-    float* __restrict__ out_trans, uint32_t* __restrict__ out_count) {
+    float* __restrict__ out_tfinal, float* __restrict__ out_trans, uint32_t* __restrict__ out_count) {
     const uint32_t n = *fix_count;
     for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
         const int pix = (int)fix_list[q];
@@ -199,6 +201,7 @@ __global__ void __launch_bounds__(128) raster_fixup_kernel(
         out_rgb[pix * 3 + 1] = (float)__dadd_rn(ag, __dmul_rn(T, bg_g));
         out_rgb[pix * 3 + 2] = (float)__dadd_rn(ab, __dmul_rn(T, bg_b));
         out_last[pix] = last | 0x80000000u;
+        out_tfinal[pix] = (float)T;
         if (out_trans) out_trans[pix] = (float)T;
         if (out_count) out_count[pix] = count;
     }

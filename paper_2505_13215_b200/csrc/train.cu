@@ -1,2 +1,525 @@
-// train.cu -- training entry points of the C ABI (filled in next).
+// train.cu -- training entry points of the C ABI: forward_train / backward
+// (backward.hpp:68-74), loss (loss.hpp:12-13), Adam (train.hpp:68-69),
+// conversion sweep (scene.hpp:75 + train.cpp:305-362) and the fused
+// per-iteration step (train.cpp:402-475).  Host code: -ffp-contract=off.
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+#include "primitives.cuh"
 #include "train_api.cuh"
+
+using namespace hgs;
+
+namespace {
+
+struct Scratch {
+    double ssim_sum;
+    double l1_sum;
+    unsigned long long skipped;
+    uint32_t flags;
+    uint32_t count;
+    unsigned long long max_leak_bits;
+    double leak_sum;
+    double loss_acc;
+    double pad[2];
+};
+
+hgs_status fail(hgs_ctx* ctx, hgs_status s, const std::string& m) {
+    if (ctx) ctx->err = m;
+    return s;
+}
+
+#define CK(x)                                                                                \
+    do {                                                                                     \
+        cudaError_t e_ = (x);                                                                \
+        if (e_ != cudaSuccess)                                                               \
+            return fail(ctx, HGS_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+#define CKL()                                                                                         \
+    do {                                                                                              \
+        cudaError_t e_ = cudaGetLastError();                                                          \
+        if (e_ != cudaSuccess)                                                                        \
+            return fail(ctx, HGS_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e_)); \
+    } while (0)
+
+__global__ void f64_to_f32_kernel(const double* __restrict__ src, float* __restrict__ dst, int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = (float)src[i];
+}
+
+// Host image (double or float) -> device float buffer.
+hgs_status upload_image(hgs_ctx* ctx, const void* src, int dtype, int64_t n, DBuf& dst) {
+    CK(dst.ensure((size_t)n * 4));
+    if (dtype == HGS_F32) {
+        CK(cudaMemcpyAsync(dst.p, src, (size_t)n * 4, cudaMemcpyHostToDevice, ctx->stream));
+    } else {
+        CK(ctx->stage.ensure((size_t)n * 8));
+        CK(cudaMemcpyAsync(ctx->stage.p, src, (size_t)n * 8, cudaMemcpyHostToDevice, ctx->stream));
+        f64_to_f32_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(ctx->stage.as<double>(),
+                                                                               dst.as<float>(), n);
+        CKL();
+    }
+    return HGS_OK;
+}
+
+hgs_status download_floats(hgs_ctx* ctx, const float* dev, int64_t n, void* host, int dtype) {
+    if (dtype == HGS_F32) {
+        CK(cudaMemcpyAsync(host, dev, (size_t)n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    } else {
+        std::vector<float> tmp((size_t)n);
+        CK(cudaMemcpyAsync(tmp.data(), dev, (size_t)n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        for (int64_t i = 0; i < n; ++i) static_cast<double*>(host)[i] = tmp[(size_t)i];
+    }
+    return HGS_OK;
+}
+
+Scratch* scratch(hgs_ctx* ctx) { return ctx->scratch.as<Scratch>(); }
+
+hgs_status ensure_scratch(hgs_ctx* ctx) {
+    if (!ctx->scratch.p) {
+        CK(ctx->scratch.ensure(sizeof(Scratch)));
+        CK(cudaMemset(ctx->scratch.p, 0, sizeof(Scratch)));
+    }
+    CK(ctx->pinned.ensure(256 + sizeof(Scratch)));
+    return HGS_OK;
+}
+
+// K6 + exact pixels + K7 for the current tape; dL/dimage in device `lg`.
+hgs_status run_backward(hgs_ctx* ctx, const float* lg, double scale) {
+    cudaStream_t st = ctx->stream;
+    const int64_t V = ctx->V;
+    CK(cudaMemsetAsync(ctx->sn4.p, 0, (size_t)ctx->cap4 * 4, st));
+    CK(cudaMemsetAsync(ctx->sn3.p, 0, (size_t)ctx->cap3 * 4, st));
+    if (V == 0 || ctx->I == 0) return HGS_OK;
+    CK(ctx->accum.ensure((size_t)V * kAccStrideHost * 4));
+    CK(cudaMemsetAsync(ctx->accum.p, 0, (size_t)V * kAccStrideHost * 4, st));
+    const int n_tiles = ctx->tiles_x * ctx->tiles_y;
+    const uint32_t* fix_count = &ctx->counters.as<Counters>()->fix_count;
+    raster_bwd_kernel<<<n_tiles, 256, 0, st>>>(ctx->ranges.as<uint2>(), ctx->inst_vals_final,
+                                               ctx->fast_sorted.as<SplatFast>(), ctx->rec_sorted.as<SplatRec>(),
+                                               ctx->W, ctx->H, ctx->tiles_x, ctx->tfinal.as<float>(),
+                                               ctx->last.as<uint32_t>(), lg, (float)ctx->bg[0], (float)ctx->bg[1],
+                                               (float)ctx->bg[2], ctx->accum.as<float>());
+    CKL();
+    raster_bwd_exact_kernel<<<ctx->sms * 2, 128, 0, st>>>(
+        ctx->fix_list.as<uint32_t>(), fix_count, ctx->ranges.as<uint2>(), ctx->inst_vals_final,
+        ctx->rec_sorted.as<SplatRec>(), ctx->W, ctx->tiles_x, ctx->bg[0], ctx->bg[1], ctx->bg[2],
+        ctx->last.as<uint32_t>(), lg, ctx->accum.as<float>());
+    CKL();
+    gaussian_bwd_kernel<<<div_up((uint32_t)V, 128), 128, 0, st>>>(
+        (int)V, ctx->sorted_gid, ctx->accum.as<float>(), kAccStrideHost, (int)ctx->n4, ctx->p4.as<float>(), ctx->cap4,
+        ctx->p3.as<float>(), ctx->cap3, ctx->deg, ctx->cam, ctx->t, scale, ctx->g4, ctx->g3, ctx->sn4.as<float>(),
+        ctx->sn3.as<float>(), ctx->dgn4, ctx->dgn3, ctx->dcnt4, ctx->dcnt3, &ctx->rec_sorted.as<SplatRec>()->c00,
+        (int)(sizeof(SplatRec) / sizeof(double)));
+    CKL();
+    return HGS_OK;
+}
+
+// K5 on the last rendered image against device gt; writes ctx->lgrad and
+// accumulates the loss into scratch->loss_acc (device) -- no host sync.
+hgs_status run_loss(hgs_ctx* ctx, const float* gt, double lambda) {
+    cudaStream_t st = ctx->stream;
+    const int W = ctx->W, H = ctx->H;
+    const bool with_ssim = lambda != 0.0;
+    if (with_ssim && (W < 11 || H < 11))
+        return fail(ctx, HGS_ERR_INVALID_ARGUMENT, "ssim: images smaller than the 11x11 window");
+    static bool window_set = false;
+    if (!window_set) {
+        set_ssim_window();
+        window_set = true;
+    }
+    const size_t npx = (size_t)W * H;
+    CK(ctx->lgrad.ensure(npx * 3 * 4));
+    Scratch* sc = scratch(ctx);
+    CK(cudaMemsetAsync(sc, 0, offsetof(Scratch, skipped), st));  // ssim_sum, l1_sum
+    const int vw = W - 10, vh = H - 10;
+    if (with_ssim) {
+        CK(ctx->loss_ws.ensure((size_t)vw * vh * 9 * 4));
+        dim3 g((vw + 31) / 32, (vh + 15) / 16, 3);
+        ssim_fwd_kernel<<<g, 256, 0, st>>>(ctx->img.as<float>(), gt, W, H, ctx->loss_ws.as<float>(), &sc->ssim_sum);
+        CKL();
+    }
+    dim3 gb((W + 31) / 32, (H + 15) / 16, 3);
+    ssim_bwd_kernel<<<gb, 256, 0, st>>>(ctx->img.as<float>(), gt, W, H, ctx->loss_ws.as<float>(), (float)lambda,
+                                        with_ssim ? 1 : 0, ctx->lgrad.as<float>(), &sc->l1_sum);
+    CKL();
+    return HGS_OK;
+}
+
+double loss_from_sums(const Scratch& h, int W, int H, double lambda) {
+    // loss.cpp:26-32: (1-l) * L1 + l * (1 - SSIM)
+    const double n = (double)W * H * 3;
+    double loss = (1.0 - lambda) * (h.l1_sum / n);
+    if (lambda != 0.0) loss += lambda * (1.0 - h.ssim_sum / ((double)(W - 10) * (H - 10) * 3));
+    return loss;
+}
+
+hgs_status run_adam(hgs_ctx* ctx, const hgs_lrs* lrs, double mean_lr_scale) {
+    cudaStream_t st = ctx->stream;
+    ctx->step++;
+    const double bc1 = 1.0 - std::pow(0.9, (double)ctx->step);
+    const double bc2 = 1.0 - std::pow(0.999, (double)ctx->step);
+    AdamArgs A;
+    A.b1 = 0.9f;
+    A.b2 = 0.999f;
+    A.one_m_b1 = (float)(1.0 - 0.9);
+    A.one_m_b2 = (float)(1.0 - 0.999);
+    A.inv_bc1 = (float)(1.0 / bc1);
+    A.inv_bc2 = (float)(1.0 / bc2);
+    A.lr_mean = (float)(lrs->mean * ctx->extent * mean_lr_scale);  // train.cpp:137
+    A.lr_mean_t = (float)(lrs->mean_t * mean_lr_scale);           // train.cpp:138
+    A.lr_quat = (float)lrs->quat;
+    A.lr_scales = (float)lrs->scales;
+    A.lr_opacity = (float)lrs->opacity;
+    A.lr_sh = (float)lrs->sh;
+    const int n = (int)(ctx->n4 + ctx->n3);
+    Scratch* sc = scratch(ctx);
+    if (n > 0) {
+        adam_kernel<<<div_up(n, 256), 256, 0, st>>>(ctx->p4.as<float>(), ctx->g4, ctx->m4.as<float>(),
+                                                    ctx->v4.as<float>(), ctx->cap4, (int)ctx->n4, ctx->p3.as<float>(),
+                                                    ctx->g3, ctx->m3.as<float>(), ctx->v3.as<float>(), ctx->cap3,
+                                                    (int)ctx->n3, ctx->deg, A, &sc->skipped, &sc->flags);
+        CKL();
+    }
+    if (ctx->n4 > 0) {
+        fold_stats_kernel<<<div_up((uint32_t)ctx->n4, 256), 256, 0, st>>>(ctx->gn4.as<float>(), ctx->cnt4.as<float>(),
+                                                                          ctx->dgn4, ctx->dcnt4, (int)ctx->n4);
+        CKL();
+    }
+    if (ctx->n3 > 0) {
+        fold_stats_kernel<<<div_up((uint32_t)ctx->n3, 256), 256, 0, st>>>(ctx->gn3.as<float>(), ctx->cnt3.as<float>(),
+                                                                          ctx->dgn3, ctx->dcnt3, (int)ctx->n3);
+        CKL();
+    }
+    return HGS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+hgs_status hgs_forward_train(hgs_ctx* ctx, const hgs_camera* cam, double t, const double bg[3],
+                             const hgs_raster_opts* opts, float* rgb_host) {
+    if (!ctx || !cam || !bg) return HGS_ERR_INVALID_ARGUMENT;
+    CK(cudaSetDevice(ctx->device));
+    hgs_status r = hgs_render_pipeline(ctx, cam, t, bg, opts);
+    if (r != HGS_OK) return r;
+    if (rgb_host) {
+        CK(cudaMemcpyAsync(rgb_host, ctx->img.p, (size_t)ctx->W * ctx->H * 12, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    }
+    return HGS_OK;
+}
+
+hgs_status hgs_backward(hgs_ctx* ctx, const void* loss_grad, int dtype, int on_device, double scale) {
+    if (!ctx) return HGS_ERR_INVALID_ARGUMENT;
+    if (!ctx->have_tape) return fail(ctx, HGS_ERR_STATE, "backward: no forward_train tape on this context");
+    CK(cudaSetDevice(ctx->device));
+    const float* lg;
+    const int64_t n = (int64_t)ctx->W * ctx->H * 3;
+    if (on_device) {
+        lg = loss_grad ? static_cast<const float*>(loss_grad) : ctx->lgrad.as<float>();
+        if (!lg) return fail(ctx, HGS_ERR_STATE, "backward: no device loss gradient");
+    } else {
+        if (!loss_grad) return HGS_ERR_INVALID_ARGUMENT;
+        hgs_status r = upload_image(ctx, loss_grad, dtype, n, ctx->lgrad);
+        if (r != HGS_OK) return r;
+        lg = ctx->lgrad.as<float>();
+    }
+    hgs_status r = run_backward(ctx, lg, scale);
+    if (r != HGS_OK) return r;
+    CK(cudaStreamSynchronize(ctx->stream));
+    return HGS_OK;
+}
+
+hgs_status hgs_zero_grads(hgs_ctx* ctx) {
+    if (!ctx) return HGS_ERR_INVALID_ARGUMENT;
+    if (ctx->gbuf.p) CK(cudaMemsetAsync(ctx->gbuf.p, 0, (size_t)ctx->gbuf_floats * 4, ctx->stream));
+    return HGS_OK;
+}
+
+hgs_status hgs_grads_download(hgs_ctx* ctx, hgs_host_scene* out, int dtype, void* sn4, void* sn3) {
+    if (!ctx || !out) return HGS_ERR_INVALID_ARGUMENT;
+    CK(cudaSetDevice(ctx->device));
+    // reuse the scene download path on the gradient rows
+    DBuf p4 = ctx->p4, p3 = ctx->p3;
+    ctx->p4.p = ctx->g4;
+    ctx->p3.p = ctx->g3;
+    hgs_status r = hgs_scene_download(ctx, out, dtype);
+    ctx->p4 = p4;
+    ctx->p3 = p3;
+    if (r != HGS_OK) return r;
+    if (sn4 && ctx->n4) {
+        r = download_floats(ctx, ctx->sn4.as<float>(), ctx->n4, sn4, dtype);
+        if (r != HGS_OK) return r;
+    }
+    if (sn3 && ctx->n3) {
+        r = download_floats(ctx, ctx->sn3.as<float>(), ctx->n3, sn3, dtype);
+        if (r != HGS_OK) return r;
+    }
+    return HGS_OK;
+}
+
+hgs_status hgs_grads_device(hgs_ctx* ctx, float** ptr, int64_t* count) {
+    if (!ctx || !ptr || !count) return HGS_ERR_INVALID_ARGUMENT;
+    *ptr = ctx->gbuf.as<float>();
+    *count = ctx->gbuf_floats;
+    return HGS_OK;
+}
+
+hgs_status hgs_loss_with_grad(hgs_ctx* ctx, const void* gt, int dtype, int on_device, double lambda, double* loss_out,
+                              void* grad_host_out) {
+    if (!ctx || !gt) return HGS_ERR_INVALID_ARGUMENT;
+    if (!ctx->have_tape) return fail(ctx, HGS_ERR_STATE, "loss: render an image first");
+    CK(cudaSetDevice(ctx->device));
+    hgs_status r = ensure_scratch(ctx);
+    if (r != HGS_OK) return r;
+    const int64_t n = (int64_t)ctx->W * ctx->H * 3;
+    const float* g;
+    if (on_device) {
+        g = static_cast<const float*>(gt);
+    } else {
+        r = upload_image(ctx, gt, dtype, n, ctx->gt_stage);
+        if (r != HGS_OK) return r;
+        g = ctx->gt_stage.as<float>();
+    }
+    r = run_loss(ctx, g, lambda);
+    if (r != HGS_OK) return r;
+    Scratch* h = static_cast<Scratch*>(ctx->pinned.p);
+    CK(cudaMemcpyAsync(h, ctx->scratch.p, sizeof(Scratch), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (loss_out) *loss_out = loss_from_sums(*h, ctx->W, ctx->H, lambda);
+    if (grad_host_out) return download_floats(ctx, ctx->lgrad.as<float>(), n, grad_host_out, dtype);
+    return HGS_OK;
+}
+
+hgs_status hgs_photometric_loss_with_grad(hgs_ctx* ctx, const void* rendered, const void* gt, int dtype, int width,
+                                          int height, double lambda, double* loss_out, void* grad_out) {
+    if (!ctx || !rendered || !gt || width <= 0 || height <= 0) return HGS_ERR_INVALID_ARGUMENT;
+    CK(cudaSetDevice(ctx->device));
+    hgs_status r = ensure_scratch(ctx);
+    if (r != HGS_OK) return r;
+    const int64_t n = (int64_t)width * height * 3;
+    r = upload_image(ctx, rendered, dtype, n, ctx->img);
+    if (r != HGS_OK) return r;
+    r = upload_image(ctx, gt, dtype, n, ctx->gt_stage);
+    if (r != HGS_OK) return r;
+    ctx->W = width;
+    ctx->H = height;
+    ctx->have_tape = false;  // img no longer belongs to a render
+    r = run_loss(ctx, ctx->gt_stage.as<float>(), lambda);
+    if (r != HGS_OK) return r;
+    Scratch* h = static_cast<Scratch*>(ctx->pinned.p);
+    CK(cudaMemcpyAsync(h, ctx->scratch.p, sizeof(Scratch), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (loss_out) *loss_out = loss_from_sums(*h, width, height, lambda);
+    if (grad_out) return download_floats(ctx, ctx->lgrad.as<float>(), n, grad_out, dtype);
+    return HGS_OK;
+}
+
+hgs_status hgs_adam_step(hgs_ctx* ctx, const hgs_lrs* lrs, double mean_lr_scale, int64_t* skipped_out) {
+    if (!ctx || !lrs) return HGS_ERR_INVALID_ARGUMENT;
+    CK(cudaSetDevice(ctx->device));
+    hgs_status r = ensure_scratch(ctx);
+    if (r != HGS_OK) return r;
+    Scratch* sc = scratch(ctx);
+    CK(cudaMemsetAsync(&sc->skipped, 0, sizeof(unsigned long long) + 8, ctx->stream));
+    r = run_adam(ctx, lrs, mean_lr_scale);
+    if (r != HGS_OK) return r;
+    Scratch* h = static_cast<Scratch*>(ctx->pinned.p);
+    CK(cudaMemcpyAsync(h, ctx->scratch.p, sizeof(Scratch), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (skipped_out) *skipped_out = (int64_t)h->skipped;
+    if (h->flags & FLAG_NONUNIT_QUAT)
+        return fail(ctx, HGS_ERR_INVALID_ARGUMENT, "UnitQuat: cannot normalize zero/non-finite quaternion");
+    return HGS_OK;
+}
+
+hgs_status hgs_adam_state_download(hgs_ctx* ctx, hgs_host_scene* m, hgs_host_scene* v, int dtype, uint64_t* step) {
+    if (!ctx) return HGS_ERR_INVALID_ARGUMENT;
+    DBuf p4 = ctx->p4, p3 = ctx->p3;
+    hgs_status r = HGS_OK;
+    if (m) {
+        ctx->p4 = ctx->m4;
+        ctx->p3 = ctx->m3;
+        r = hgs_scene_download(ctx, m, dtype);
+        ctx->p4 = p4;
+        ctx->p3 = p3;
+        if (r != HGS_OK) return r;
+    }
+    if (v) {
+        ctx->p4 = ctx->v4;
+        ctx->p3 = ctx->v3;
+        r = hgs_scene_download(ctx, v, dtype);
+        ctx->p4 = p4;
+        ctx->p3 = p3;
+        if (r != HGS_OK) return r;
+    }
+    if (step) *step = ctx->step;
+    return HGS_OK;
+}
+
+hgs_status hgs_adam_state_upload(hgs_ctx* ctx, const hgs_host_scene* m, const hgs_host_scene* v, int dtype,
+                                 uint64_t step) {
+    if (!ctx || !m || !v) return HGS_ERR_INVALID_ARGUMENT;
+    if (m->n4 != ctx->n4 || m->n3 != ctx->n3 || v->n4 != ctx->n4 || v->n3 != ctx->n3)
+        return fail(ctx, HGS_ERR_INVALID_ARGUMENT, "adam state: pool sizes differ from the scene");
+    hgs_status r = hgs_upload_rows(ctx, m, dtype, ctx->m4.as<float>(), ctx->m3.as<float>());
+    if (r != HGS_OK) return r;
+    r = hgs_upload_rows(ctx, v, dtype, ctx->v4.as<float>(), ctx->v3.as<float>());
+    if (r != HGS_OK) return r;
+    ctx->step = step;
+    return HGS_OK;
+}
+
+hgs_status hgs_stats_download(hgs_ctx* ctx, double* gn4, uint32_t* c4, double* gn3, uint32_t* c3) {
+    if (!ctx) return HGS_ERR_INVALID_ARGUMENT;
+    CK(cudaSetDevice(ctx->device));
+    const int64_t n4 = ctx->n4, n3 = ctx->n3;
+    std::vector<float> a(n4), b(n4), da(n4), db(n4), c(n3), d(n3), dc(n3), dd(n3);
+    if (n4) {
+        CK(cudaMemcpy(a.data(), ctx->gn4.p, n4 * 4, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(b.data(), ctx->cnt4.p, n4 * 4, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(da.data(), ctx->dgn4, n4 * 4, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(db.data(), ctx->dcnt4, n4 * 4, cudaMemcpyDeviceToHost));
+    }
+    if (n3) {
+        CK(cudaMemcpy(c.data(), ctx->gn3.p, n3 * 4, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(d.data(), ctx->cnt3.p, n3 * 4, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(dc.data(), ctx->dgn3, n3 * 4, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(dd.data(), ctx->dcnt3, n3 * 4, cudaMemcpyDeviceToHost));
+    }
+    for (int64_t i = 0; i < n4; ++i) {
+        if (gn4) gn4[i] = (double)a[i] + (double)da[i];
+        if (c4) c4[i] = (uint32_t)(b[i] + db[i]);
+    }
+    for (int64_t i = 0; i < n3; ++i) {
+        if (gn3) gn3[i] = (double)c[i] + (double)dc[i];
+        if (c3) c3[i] = (uint32_t)(d[i] + dd[i]);
+    }
+    return HGS_OK;
+}
+
+hgs_status hgs_sweep_convert(hgs_ctx* ctx, int64_t* moved_out, hgs_conversion_report* report) {
+    if (!ctx) return HGS_ERR_INVALID_ARGUMENT;
+    if (!(ctx->tau > 0.0)) return fail(ctx, HGS_ERR_INVALID_ARGUMENT, "is_static: tau must be positive");
+    CK(cudaSetDevice(ctx->device));
+    hgs_status r = ensure_scratch(ctx);
+    if (r != HGS_OK) return r;
+    cudaStream_t st = ctx->stream;
+    const int n4 = (int)ctx->n4, n3 = (int)ctx->n3;
+    hgs_conversion_report rep{0, 0.0, 0.0};
+    if (n4 == 0) {
+        if (report) *report = rep;
+        return HGS_OK;
+    }
+    // s_star: smallest double with exp(s_star) > tau under the host libm
+    // (scene.cpp:12 evaluates std::exp(s_t) > tau); the device then compares
+    // s_t >= s_star, exact for every float s_t.
+    const double tau = ctx->tau;
+    double s = std::log(tau);
+    while (!(std::exp(s) > tau)) s = std::nextafter(s, INFINITY);
+    for (;;) {
+        const double p = std::nextafter(s, -INFINITY);
+        if (std::exp(p) > tau) s = p;
+        else break;
+    }
+    CK(ctx->visflag.ensure((size_t)n4 * 4));
+    CK(ctx->vispos.ensure((size_t)n4 * 4));
+    CK(ctx->scan_ws.ensure(scan_workspace_bytes(n4) + 4096));
+    Scratch* sc = scratch(ctx);
+    CK(cudaMemsetAsync(sc, 0, sizeof(Scratch), st));
+    uint32_t* mask = ctx->visflag.as<uint32_t>();
+    uint32_t* pos = ctx->vispos.as<uint32_t>();
+    convert_mask_kernel<<<div_up(n4, 256), 256, 0, st>>>(ctx->p4.as<float>(), ctx->cap4, n4, s, mask);
+    CKL();
+    exclusive_scan_u32(mask, pos, n4, &sc->count, ctx->scan_ws.as<uint32_t>(), st);
+    CKL();
+    CK(ctx->stage.ensure((size_t)n4 * 8 + 64));
+    convert_rows_kernel<<<div_up(n4, 128), 128, 0, st>>>(
+        ctx->p4.as<float>(), ctx->m4.as<float>(), ctx->v4.as<float>(), ctx->cap4, n4, mask, pos, ctx->p3.as<float>(),
+        ctx->m3.as<float>(), ctx->v3.as<float>(), ctx->cap3, n3, ctx->deg, ctx->stage.as<long long>(),
+        &sc->max_leak_bits, &sc->leak_sum, &sc->flags);
+    CKL();
+    // survivors: stable compaction of params and both moments
+    const int R4 = rows4(ctx->deg);
+    compact_survivors_kernel<<<div_up(n4, 256), 256, 0, st>>>(ctx->p4.as<float>(), ctx->p4_alt.as<float>(), R4,
+                                                              ctx->cap4, n4, mask, pos);
+    compact_survivors_kernel<<<div_up(n4, 256), 256, 0, st>>>(ctx->m4.as<float>(), ctx->m4_alt.as<float>(), R4,
+                                                              ctx->cap4, n4, mask, pos);
+    compact_survivors_kernel<<<div_up(n4, 256), 256, 0, st>>>(ctx->v4.as<float>(), ctx->v4_alt.as<float>(), R4,
+                                                              ctx->cap4, n4, mask, pos);
+    CKL();
+    Scratch* h = static_cast<Scratch*>(ctx->pinned.p);
+    CK(cudaMemcpyAsync(h, sc, sizeof(Scratch), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const uint32_t cnt = h->count;
+    if (h->flags & FLAG_DEGENERATE_ROT)
+        return fail(ctx, HGS_ERR_DEGENERATE_ROTATION, "extract_spatial_rot: spatial block is singular");
+    if (h->flags & FLAG_NOT_ROTATION)
+        return fail(ctx, HGS_ERR_INVALID_ARGUMENT, "rot3_to_quat: input is not a rotation matrix");
+    if (moved_out && cnt) CK(cudaMemcpy(moved_out, ctx->stage.p, (size_t)cnt * 8, cudaMemcpyDeviceToHost));
+    std::swap(ctx->p4, ctx->p4_alt);
+    std::swap(ctx->m4, ctx->m4_alt);
+    std::swap(ctx->v4, ctx->v4_alt);
+    ctx->n4 = n4 - (int64_t)cnt;
+    ctx->n3 = n3 + (int64_t)cnt;
+    // train.cpp:357-361: every densify statistic is reset; gradients are
+    // already zero after the Adam step, cleared here for the new row map.
+    CK(cudaMemsetAsync(ctx->gn4.p, 0, (size_t)ctx->cap4 * 4, st));
+    CK(cudaMemsetAsync(ctx->cnt4.p, 0, (size_t)ctx->cap4 * 4, st));
+    CK(cudaMemsetAsync(ctx->gn3.p, 0, (size_t)ctx->cap3 * 4, st));
+    CK(cudaMemsetAsync(ctx->cnt3.p, 0, (size_t)ctx->cap3 * 4, st));
+    CK(cudaMemsetAsync(ctx->gbuf.p, 0, (size_t)ctx->gbuf_floats * 4, st));
+    CK(cudaStreamSynchronize(st));
+    ctx->have_tape = false;
+    rep.count = cnt;
+    double mx;
+    std::memcpy(&mx, &h->max_leak_bits, 8);
+    rep.max_leakage = cnt ? mx : 0.0;
+    rep.mean_leakage = cnt ? h->leak_sum / (double)cnt : 0.0;
+    if (report) *report = rep;
+    return HGS_OK;
+}
+
+hgs_status hgs_train_step(hgs_ctx* ctx, int n_views, const hgs_camera* cams, const double* times,
+                          const float* const* gt_device, int batch_total, const hgs_train_opts* o, int apply_adam,
+                          double* loss_out) {
+    if (!ctx || n_views < 0 || (n_views && (!cams || !times || !gt_device)) || !o || batch_total <= 0)
+        return HGS_ERR_INVALID_ARGUMENT;
+    CK(cudaSetDevice(ctx->device));
+    hgs_status r = ensure_scratch(ctx);
+    if (r != HGS_OK) return r;
+    hgs_raster_opts ro{o->weight_cutoff, 1, 0, 0};
+    double loss = 0.0;
+    for (int v = 0; v < n_views; ++v) {
+        r = hgs_render_pipeline(ctx, &cams[v], times[v], o->bg, &ro);
+        if (r != HGS_OK) return r;
+        r = run_loss(ctx, gt_device[v], o->ssim_lambda);
+        if (r != HGS_OK) return r;
+        r = run_backward(ctx, ctx->lgrad.as<float>(), 1.0 / (double)batch_total);  // train.cpp:430-432
+        if (r != HGS_OK) return r;
+        Scratch* h = static_cast<Scratch*>(ctx->pinned.p);
+        CK(cudaMemcpyAsync(h, ctx->scratch.p, sizeof(Scratch), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        loss += loss_from_sums(*h, ctx->W, ctx->H, o->ssim_lambda);
+    }
+    if (loss_out) *loss_out = loss;
+    if (!std::isfinite(loss))
+        return fail(ctx, HGS_ERR_NUMERIC_ABORT, "train: non-finite loss");  // train.cpp:445-447
+    if (apply_adam) {
+        Scratch* sc = scratch(ctx);
+        CK(cudaMemsetAsync(&sc->skipped, 0, sizeof(unsigned long long) + 8, ctx->stream));
+        r = run_adam(ctx, &o->lrs, o->mean_lr_scale);
+        if (r != HGS_OK) return r;
+        CK(cudaStreamSynchronize(ctx->stream));
+    }
+    return HGS_OK;
+}
+
+}  // extern "C"
