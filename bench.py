@@ -1,0 +1,385 @@
+#!/usr/bin/env python
+"""bench.py -- throughput of the hybrid 3D/4DGS training hot path on B200.
+
+Default workload (BASELINE.json configs[1], "c2"): 240k 4D + 60k 3D Gaussians,
+SH degree 3, 1352x1014, one training view per GPU per iteration (slice +
+projection + SH, sorts, tile rasterizer forward, L1 + D-SSIM loss, rasterizer
+backward, per-Gaussian backward, fused Adam).  Synthetic data: the scene and
+the ground-truth scene (seed + 1000, rendered once on the GPU and 8-bit
+quantised like the reference's generate_synthetic) follow SURVEY.md 8d.
+
+  python bench.py [--gpus N --steps K --warmup W]            # this repo (CUDA)
+  python bench.py --impl reference [...]                      # CPU reference path
+
+One JSON line on rank 0.  value = views/s over all ranks (one view = one
+training iteration of one 1352x1014 camera; weak scaling: N GPUs -> N views
+per iteration + one NCCL all-reduce of the packed gradients).  The working
+set (params + Adam moments + grads ~ 0.3 GB) exceeds the 126 MB L2, so no
+explicit flush is needed between iterations.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
+UNIT = "views/s"
+HBM_FALLBACK_GBS = 6650.0
+
+
+def peaks() -> tuple[float, str]:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        return float(json.load(open(p))["hbm_gbs"]), "measured"
+    except Exception:
+        return HBM_FALLBACK_GBS, "fallback"
+
+
+# ------------------------------------------------------------------ workload
+def workload(cfg_name: str):
+    from paper_2505_13215_b200.scene import CONFIGS, ring_camera, synthetic_scene
+
+    c = CONFIGS[cfg_name]
+    n4, n3, W, H, seed = c["n4"], c["n3"], c["width"], c["height"], c["seed"]
+    scene = synthetic_scene(n4, n3, 3, seed=seed, tau=0.5)
+    target = synthetic_scene(n4, n3, 3, seed=seed + 1000, tau=0.5)
+    cams = [ring_camera(seed, W, H, index=i, n_ring=16) for i in range(16)]
+    times = [i / 15.0 for i in range(16)]
+    desc = {"workload": f"{cfg_name}: {n4 // 1000}k 4D + {n3 // 1000}k 3D Gaussians, SH deg 3, {W}x{H}, "
+                        "1 view/GPU/iteration: slice+EWA+SH, depth+tile radix sorts, tile raster fwd, "
+                        "L1+D-SSIM, raster bwd, per-Gaussian bwd, fused Adam",
+            "gaussians": n4 + n3, "width": W, "height": H, "sh_degree": 3, "views_in_ring": 16,
+            "l2": "working set > 126 MB L2 (no flush needed)"}
+    return scene, target, cams, times, desc
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu, self.rows, self.proc = gpu, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[3 + k].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------ roofline
+def algorithmic_bytes(phase: str, n: dict) -> float | None:
+    """Per-step algorithmic bytes of each kernel phase (SURVEY.md 8d table,
+    adapted to this implementation's passes)."""
+    N4, N3, V, I, px, P = n["n4"], n["n3"], n["V"], n["I"], n["px"], n["rows_avg"]
+    if phase == "preprocess":   # params in (68/44 B geometry + 192 B SH of visible) + 80 B record out + flags
+        return 68 * N4 + 44 * N3 + (192 + 80) * V + 4 * (N4 + N3) * 3
+    if phase == "depth_sort":   # global LSD over V keys+values: (8 + 24*passes) * n
+        return (8 + 24 * 4) * V
+    if phase == "duplicate":    # gather (80 B in, 80+64 B out) + scan + 8 B per instance out
+        return (80 + 144 + 12) * V + 8 * I
+    if phase == "tile_sort":
+        return (8 + 24 * 2) * I
+    if phase == "raster_fwd":   # K4: 4 B value + 64 B splat per instance, 24 B per pixel out
+        return 68 * I + 24 * px
+    if phase == "loss":
+        return 44 * px * 3
+    if phase == "raster_bwd":   # 68 B per instance + 36 B accumulators, 32 B per pixel in
+        return 104 * I + 32 * px
+    if phase == "gaussian_bwd":  # read params + write grads (2 * 4 * P) + 36 B accumulators
+        return V * (2 * 4 * P + 48)
+    if phase == "adam":          # 32 B per element (param, m, v rw; grad read + zero)
+        return 32 * (N4 * n["rows4"] + N3 * n["rows3"])
+    return None
+
+
+def roofline(phase_ms: dict, counts: dict, steps: int, peak: float, peak_kind: str) -> dict:
+    kernels = []
+    for ph, ms in phase_ms.items():
+        if ms <= 0:
+            continue
+        b = algorithmic_bytes(ph, counts)
+        per = ms / steps
+        gbs = (b / (per * 1e-3) / 1e9) if b else None
+        kernels.append({"phase": ph, "ms_per_step": round(per, 4), "alg_bytes": b,
+                        "GB/s": round(gbs, 1) if gbs else None, "frac": round(gbs / peak, 4) if gbs else None})
+    kernels.sort(key=lambda k: -k["ms_per_step"])
+    top = kernels[0]
+    return {"bound": "hbm", "kernel": top["phase"], "achieved": top["GB/s"], "peak": peak, "unit": "GB/s",
+            "frac": top["frac"], "traffic": None, "peak_source": peak_kind, "kernels": kernels}
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args) -> None:
+    import torch
+
+    from paper_2505_13215_b200 import _capi
+    from paper_2505_13215_b200.api import Context
+    from paper_2505_13215_b200.train import DeviceTrainer, ViewParallelTrainer, quantize_8bit
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    scene, target, cams, times, desc = workload(args.config)
+    ctx = Context(local)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
+    kw = dict(target=target, bg=(0.2, 0.2, 0.2), iterations=max(1000, args.steps * 10))
+    tr = ViewParallelTrainer(ctx, scene, cams, times, **kw) if world > 1 else DeviceTrainer(ctx, scene, cams, times,
+                                                                                             **kw)
+
+    def batch(step):
+        return [(step * world + r) % len(cams) for r in range(world)]
+
+    def barrier():
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def timed(fn, k):
+        barrier()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for i in range(k):
+            fn(i)
+        t1.record(stream)
+        torch.cuda.synchronize()
+        ms = t0.elapsed_time(t1)
+        if dist:
+            tt = torch.tensor([ms], device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ms = float(tt.item())
+        barrier()
+        return ms
+
+    step_fn = (lambda i: tr.step(batch(i))) if world > 1 else (lambda i: tr.step([batch(i)[0]]))
+    for i in range(args.warmup):
+        step_fn(i)
+    # ---- device-resident timed region (profiled per phase with CUDA events)
+    _capi.lib().hgs_profile(ctx.handle, 1)
+    _capi.lib().hgs_profile_read(ctx.handle, None, None, 1)
+    l0 = _capi.lib().hgs_launch_count()
+    with ClockSampler(local) as clk:
+        ms = timed(lambda i: step_fn(args.warmup + i), args.steps)
+    launches = _capi.lib().hgs_launch_count() - l0
+    import ctypes as C
+
+    ph = (C.c_double * 16)()
+    _capi.lib().hgs_profile_read(ctx.handle, ph, None, 1)
+    _capi.lib().hgs_profile(ctx.handle, 0)
+    phase_ms = {name: float(ph[i]) for i, name in enumerate(_capi.PHASES)}
+    info = ctx.render_info()
+    value = world * args.steps / (ms / 1e3)
+
+    # ---- end to end through the C ABI with HOST ground truth (pinned)
+    H, W = cams[0].height, cams[0].width
+    gts_host = [torch.empty((H, W, 3), dtype=torch.float32).pin_memory() for _ in range(len(cams))]
+    for i, g in enumerate(gts_host):
+        g.copy_(tr.gt[i].cpu())
+    lib = _capi.lib()
+
+    def e2e_step(i):
+        views = batch(args.warmup + args.steps + i)
+        mine = [views[rank]] if world > 1 else [views[0]]
+        n = len(mine)
+        karr = (_capi.Camera_ * n)(*[tr._cams[v] for v in mine])
+        tarr = (C.c_double * n)(*[times[v] for v in mine])
+        garr = (C.c_void_p * n)(*[C.c_void_p(gts_host[v].data_ptr()) for v in mine])
+        loss = C.c_double()
+        tr.iter += 1
+        ctx._check(lib.hgs_train_step_host(ctx.handle, n, karr, tarr, garr, _capi.HGS_F32, world,
+                                           C.byref(tr._opts(tr.decay())), 0 if world > 1 else 1, C.byref(loss)))
+        if world > 1:
+            g = tr.grads_tensor()
+            dist.all_reduce(g)
+            ctx.adam_step(tr.lrs, tr.decay())
+
+    e2e_ms = timed(e2e_step, args.steps)
+    e2e_value = world * args.steps / (e2e_ms / 1e3)
+
+    # ---- forward-only render throughput (Mpix/s), device resident
+    def render_step(i):
+        v = (i * world + rank) % len(cams)
+        ctx._check(lib.hgs_render(ctx.handle, C.byref(tr._cams[v]), times[v],
+                                  (C.c_double * 3)(0.2, 0.2, 0.2), None, None, None, None, None))
+
+    r_ms = timed(render_step, args.steps)
+    render_mpix = world * args.steps * W * H / (r_ms / 1e3) / 1e6
+
+    peak, peak_kind = peaks()
+    rows4 = 17 + 48
+    rows3 = 11 + 48
+    counts = {"n4": scene.n4, "n3": scene.n3, "V": info["visible"], "I": info["instances"], "px": W * H,
+              "rows4": rows4, "rows3": rows3,
+              "rows_avg": (rows4 * scene.n4 + rows3 * scene.n3) / max(1, scene.n4 + scene.n3)}
+    rl = roofline(phase_ms, counts, args.steps, peak, peak_kind)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(scene, cams[0], times[0], quantize_8bit(tr.gt[0].cpu().numpy().astype(np.float64)))
+
+    if rank == 0:
+        out = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
+               "scaling": "weak", "vs_baseline": None, "dtype": "f32 (geometry, keys and guard-band decisions f64)",
+               "data": "synthetic (SURVEY.md 8d generator; random init, GT = 8-bit render of a second scene)",
+               "config": dict(desc, parallelism=f"view-parallel dp{world}", views_per_iteration=world),
+               "e2e": {"value": round(e2e_value, 3), "unit": UNIT,
+                       "h2d_bytes_per_step": int(W * H * 3 * 4),
+                       "d2h_bytes_per_step": 80,
+                       "path": "hgs_train_step_host (pinned host GT frame in, loss out)"},
+               "render": {"value": round(render_mpix, 2), "unit": "Mpix/s",
+                          "what": "forward render of the device-resident c2 scene, 1352x1014"},
+               "gpu_launches": int(launches), "launches_per_step": round(launches / args.steps, 1),
+               "roofline": rl, "clocks": clk.summary(), "cpu_baseline": cpu,
+               "render_info": info}
+        print(json.dumps(out), flush=True)
+    ctx.close()
+    if dist:
+        dist.destroy_process_group()
+
+
+def cpu_baseline(scene, cam, t, gt) -> dict:
+    """The oracle (FP64 CPU restatement of the reference) on one full c2 view:
+    tiled taped forward on all cores, L1+SSIM, backward (single-threaded, as
+    the reference), Adam.  Bounded sample: one iteration (~10-30 s)."""
+    import oracle as O
+
+    s = scene.copy()
+    st = O.AdamState(s)
+    cores = O.hardware_threads()
+    t0 = time.perf_counter()
+    O.train_step(s, st, [cam], [t], [gt], (0.2, 0.2, 0.2), num_threads=1, tile_threads=cores)
+    dt = time.perf_counter() - t0
+    return {"value": round(1.0 / dt, 5), "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"one full {cam.width}x{cam.height} training iteration of the c2 scene "
+                      f"({dt:.2f} s): tiled forward w/ tape on {cores} threads, L1+SSIM, backward 1 thread, Adam"}
+
+
+# ------------------------------------------------------------------ reference arm
+def run_reference(args) -> None:
+    """The reference's own CPU path (FP64 oracle port of proj/src; the C++
+    reference needs Eigen3 and cannot be compiled in this image).  Batch-image
+    parallel like train_scene (one std::thread per view, train.cpp:419-422),
+    all host threads used; each step is a bounded sample: B views cropped to a
+    horizontal band so the whole --steps/--warmup run stays within minutes."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle as O
+    from paper_2505_13215_b200.scene import Camera
+    from paper_2505_13215_b200.train import quantize_8bit
+
+    scene, target, cams, times, desc = workload(args.config)
+    cores = O.hardware_threads()
+    B = max(1, min(cores, 8))
+    full_step_s = 14.0  # measured order of one full-view iteration per thread
+    frac = float(np.clip(150.0 / ((args.steps + args.warmup) * full_step_s), 0.1, 1.0))
+    H, W = cams[0].height, cams[0].width
+    hb = max(16, int(round(H * frac)))
+    y0 = (H - hb) // 2
+
+    def band(c: Camera) -> Camera:
+        return Camera(fx=c.fx, fy=c.fy, cx=c.cx, cy=c.cy - y0, rot=c.rot, trans=c.trans, width=W, height=hb,
+                      near=c.near, far=c.far)
+
+    bcams = [band(c) for c in cams]
+    gts = []
+    for i in range(len(cams)):
+        img = O.rasterize(target, bcams[i], times[i], (0.2, 0.2, 0.2), num_threads=cores)["rgb"]
+        gts.append(quantize_8bit(img))
+    s = scene.copy()
+    st = O.AdamState(s)
+
+    def step(i):
+        vs = [(i * B + b) % len(cams) for b in range(B)]
+        O.train_step(s, st, [bcams[v] for v in vs], [times[v] for v in vs], [gts[v] for v in vs],
+                     (0.2, 0.2, 0.2), num_threads=B, tile_threads=1)
+
+    for i in range(args.warmup):
+        step(i)
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        step(args.warmup + i)
+    dt = time.perf_counter() - t0
+    views = B * args.steps * hb / H
+    value = views / dt
+    sample = (f"each step: {B} views x {W}x{hb} band ({hb / H:.2f} of a view), one thread per view "
+              f"(train.cpp:419-422), FP64 oracle port of the reference")
+    out = {"impl": "reference", "metric": METRIC, "value": round(value, 5), "unit": UNIT, "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 2),
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": dict(desc, parallelism=f"batch-image threads x{B}"),
+           "cpu_baseline": {"value": round(value, 5), "unit": UNIT, "cores": B, "kind": "port", "sample": sample},
+           "e2e": {"value": round(value, 5), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

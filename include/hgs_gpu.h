@@ -184,6 +184,28 @@ hgs_status hgs_train_step(hgs_ctx *ctx, int n_views, const hgs_camera *cams, con
                           const float *const *gt_device, int batch_total, const hgs_train_opts *opts,
                           int apply_adam, double *loss_out);
 
+/* Same iteration with the ground-truth frames in HOST memory (dtype
+ * HGS_F32/HGS_F64); the host->device copies run on the context stream
+ * inside the call (the reference-facing end-to-end path). */
+hgs_status hgs_train_step_host(hgs_ctx *ctx, int n_views, const hgs_camera *cams, const double *times,
+                               const void *const *gt_host, int dtype, int batch_total, const hgs_train_opts *opts,
+                               int apply_adam, double *loss_out);
+
+/* ---- instrumentation (not in the reference) ---------------------------- */
+/* Per-phase CUDA-event timing on the context stream:
+ * 0 preprocess, 1 depth sort, 2 duplicate, 3 tile sort, 4 raster fwd,
+ * 5 loss, 6 raster bwd, 7 per-Gaussian bwd, 8 Adam, 9 sweep, 10 uploads. */
+hgs_status hgs_profile(hgs_ctx *ctx, int enable);
+hgs_status hgs_profile_read(hgs_ctx *ctx, double *ms16, long long *calls16, int reset);
+/* Kernels launched by this library since load (process-wide). */
+long long hgs_launch_count(void);
+/* Parity introspection used by the tests: projected splats in projected
+ * order (gid, f32 depth bits, box x0,x1,y0,y1, mean, conic, alpha, rgb) and
+ * the tile-sorted instance list (tile id, gid) of the last render. */
+hgs_status hgs_debug_splats(hgs_ctx *ctx, int32_t *gid, uint32_t *depth_bits, int32_t *box4, double *mean2,
+                            double *conic4, double *alpha, float *rgb, int64_t cap, int64_t *n_out);
+hgs_status hgs_debug_instances(hgs_ctx *ctx, uint32_t *tile, uint32_t *gid, int64_t cap, int64_t *n_out);
+
 #ifdef __cplusplus
 }
 #endif

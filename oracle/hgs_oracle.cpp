@@ -17,6 +17,7 @@
 #include <cstring>
 #include <functional>
 #include <limits>
+#include <memory>
 #include <random>
 #include <stdexcept>
 #include <string>
@@ -2001,5 +2002,78 @@ int hgso_convert_4d_to_3d(const double mean_x[3], double mean_t, const double ql
 }
 
 int hgso_hardware_threads(void) { return int(std::thread::hardware_concurrency()); }
+
+// One training iteration (train.cpp:402-450): per batch image forward_train
+// + photometric_loss_with_grad + backward (one std::thread per image when
+// num_threads > 1, as the reference does), grads averaged with add_scaled(1/B)
+// in index order, raw densify statistics, NumericAbort on a non-finite loss,
+// optimizer_step.  The forward uses the tiled tape (bitwise equal to the
+// literal forward_train, test_backward.cpp:98-100) with tile_threads.
+int hgso_train_step(hgso_scene* s, hgso_state* st, const hgso_camera* cams, const double* times,
+                    const double* const* gts, int n_views, const double bg[3], double cutoff, double lambda,
+                    const hgso_lrs* lrs, double mean_lr_scale, int num_threads, int tile_threads, double* loss_out) {
+    return guard([&] {
+        View v{s, sh_count(s->sh_degree)};
+        const int K3 = sh_count(s->sh_degree) * 3;
+        const int64_t n4 = s->n4, n3 = s->n3;
+        struct Buf {
+            std::vector<double> d[14];
+            hgso_grads g;
+        };
+        auto alloc = [&](Buf& b) {
+            const size_t sz[14] = {size_t(n4 * 3), size_t(n4), size_t(n4 * 4), size_t(n4 * 4), size_t(n4 * 4),
+                                   size_t(n4), size_t(n4 * K3), size_t(n4), size_t(n3 * 3), size_t(n3 * 4),
+                                   size_t(n3 * 3), size_t(n3), size_t(n3 * K3), size_t(n3)};
+            for (int k = 0; k < 14; ++k) b.d[k].assign(sz[k], 0.0);
+            double** p = &b.g.mean_x;
+            for (int k = 0; k < 14; ++k) p[k] = b.d[k].data();
+        };
+        std::vector<Buf> per(static_cast<size_t>(n_views));
+        std::vector<double> losses(size_t(n_views), 0.0);
+        std::vector<std::string> errs(static_cast<size_t>(n_views));
+        auto run_one = [&](int bi) {
+            try {
+                Cam cam = to_cam(cams[bi]);
+                const size_t npx = size_t(cam.width) * cam.height;
+                std::vector<double> img(npx * 3), lg(npx * 3);
+                std::unique_ptr<Tape> tape(forward_train_tiled(v, cam, times[bi], bg, cutoff, tile_threads, img.data()));
+                double loss = (1.0 - lambda) * l1(img.data(), gts[bi], npx * 3, lg.data());
+                for (double& x : lg) x *= (1.0 - lambda);
+                if (lambda != 0.0) {
+                    std::vector<double> sg(npx * 3, 0.0);
+                    double ss = ssim_impl(img.data(), gts[bi], cam.width, cam.height, sg.data());
+                    loss += lambda * (1.0 - ss);
+                    for (size_t i = 0; i < lg.size(); ++i) lg[i] -= lambda * sg[i];
+                }
+                losses[size_t(bi)] = loss;
+                alloc(per[size_t(bi)]);
+                backward(v, cam, *tape, lg.data(), per[size_t(bi)].g);
+            } catch (const std::exception& e) {
+                errs[size_t(bi)] = e.what();
+            }
+        };
+        if (num_threads > 1 && n_views > 1) {
+            std::vector<std::thread> pool;
+            for (int bi = 0; bi < n_views; ++bi) pool.emplace_back(run_one, bi);
+            for (auto& th : pool) th.join();
+        } else {
+            for (int bi = 0; bi < n_views; ++bi) run_one(bi);
+        }
+        for (const auto& e : errs)
+            if (!e.empty()) throw std::invalid_argument(e);
+        Buf acc;
+        alloc(acc);
+        double loss = 0.0;
+        for (int bi = 0; bi < n_views; ++bi) {
+            loss += losses[size_t(bi)];
+            grads_add_scaled(*s, acc.g, per[size_t(bi)].g, 1.0 / double(n_views));
+            hgso_accumulate_stats(s, st, &per[size_t(bi)].g);
+        }
+        loss /= double(n_views);
+        if (loss_out) *loss_out = loss;
+        if (!std::isfinite(loss)) throw NumericAbort("train: non-finite loss");
+        optimizer_step(*s, acc.g, *st, *lrs, mean_lr_scale);
+    });
+}
 
 }  // extern "C"

@@ -196,7 +196,12 @@ int hgso_convert_4d_to_3d(const double mean_x[3], double mean_t, const double ql
                           const double qr[4], const double log_s4[4], double op,
                           double mean3[3], double quat3[4], double log_s3[3], double *op3);
 
-/* --- fixtures for the configs in SURVEY.md 8d ---------------------------- */
+/* --- one training iteration (train.cpp:402-450) -------------------------- */
+int hgso_train_step(hgso_scene *s, hgso_state *st, const hgso_camera *cams, const double *times,
+                    const double *const *gts, int n_views, const double bg[3], double weight_cutoff,
+                    double ssim_lambda, const hgso_lrs *lrs, double mean_lr_scale, int num_threads,
+                    int tile_threads, double *loss_out);
+
 int hgso_hardware_threads(void);
 
 #ifdef __cplusplus

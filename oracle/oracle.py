@@ -648,3 +648,29 @@ def sweep_convert(scene: HybridScene, state: AdamState | None = None):
 
 def hardware_threads() -> int:
     return int(lib().hgso_hardware_threads())
+
+
+def train_step(scene: HybridScene, state: AdamState, cams, times, gts, background=(0.0, 0.0, 0.0),
+               weight_cutoff: float = 0.05, ssim_lambda: float = 0.2, lrs: LearningRates | None = None,
+               mean_lr_scale: float = 1.0, num_threads: int = 1, tile_threads: int = 1) -> float:
+    """One iteration of train_scene's loop body (train.cpp:402-450); mutates
+    scene and state, returns the mean batch loss."""
+    L = lib()
+    if not hasattr(L, "_ts_bound"):
+        L.hgso_train_step.argtypes = [C.POINTER(_Scene), C.POINTER(_State), C.POINTER(_Camera), _dp,
+                                      C.POINTER(_dp), C.c_int, _dp, C.c_double, C.c_double, C.POINTER(_Lrs),
+                                      C.c_double, C.c_int, C.c_int, _dp]
+        L._ts_bound = True
+    n = len(cams)
+    karr = (_Camera * n)(*[_cam_struct(c) for c in cams])
+    tarr = (C.c_double * n)(*times)
+    g = [_arr(x) for x in gts]
+    garr = (_dp * n)(*[_p(x) for x in g])
+    st = state._struct()
+    loss = C.c_double()
+    _check(L.hgso_train_step(C.byref(_scene_struct(scene)), C.byref(st), karr, tarr, garr, n,
+                             _p(_arr(background, 3)), weight_cutoff, ssim_lambda,
+                             C.byref(_lrs_struct(lrs or LearningRates())), mean_lr_scale, num_threads,
+                             tile_threads, C.byref(loss)))
+    state.step, state.skipped_nonfinite = st.step, st.skipped_nonfinite
+    return loss.value

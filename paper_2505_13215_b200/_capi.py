@@ -123,7 +123,15 @@ _SIGS = {
     "hgs_sweep_convert": ([_vp, _i64p, C.POINTER(ConversionReport)], C.c_int),
     "hgs_train_step": ([_vp, C.c_int, C.POINTER(Camera_), _dp, C.POINTER(_fp), C.c_int, C.POINTER(TrainOpts),
                         C.c_int, _dp], C.c_int),
+    "hgs_train_step_host": ([_vp, C.c_int, C.POINTER(Camera_), _dp, C.POINTER(_vp), C.c_int, C.c_int,
+                             C.POINTER(TrainOpts), C.c_int, _dp], C.c_int),
+    "hgs_profile": ([_vp, C.c_int], C.c_int),
+    "hgs_profile_read": ([_vp, _dp, C.POINTER(C.c_longlong), C.c_int], C.c_int),
+    "hgs_launch_count": ([], C.c_longlong),
 }
+
+PHASES = ("preprocess", "depth_sort", "duplicate", "tile_sort", "raster_fwd", "loss", "raster_bwd",
+          "gaussian_bwd", "adam", "sweep", "upload")
 
 # symbols every build must export (checked by the CPU test suite)
 EXPORTED = tuple(_SIGS)

@@ -102,6 +102,7 @@ hgs_status upload_pool(hgs_ctx* ctx, const hgs_host_scene* s, const FieldMap* fm
         else
             aos_to_soa_kernel<float><<<blocks, 256, 0, ctx->stream>>>(ctx->stage.as<float>(), n, d, dst, cap,
                                                                      fm[f].row);
+        count_launch();
         CKL();
     }
     return HGS_OK;
@@ -125,6 +126,7 @@ hgs_status download_pool(hgs_ctx* ctx, hgs_host_scene* s, const FieldMap* fm, in
         else
             soa_to_aos_kernel<float><<<blocks, 256, 0, ctx->stream>>>(src, n, d, cap, fm[f].row,
                                                                      ctx->stage.as<float>());
+        count_launch();
         CKL();
         CK(cudaMemcpyAsync(dst, ctx->stage.p, bytes, cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
@@ -214,6 +216,46 @@ hgs_status hgs_upload_rows(hgs_ctx* ctx, const hgs_host_scene* s, int dtype, flo
     return HGS_OK;
 }
 
+// ---------------------------------------------------------------- profiler
+void prof_begin(hgs_ctx* ctx, int phase) {
+    if (!ctx->profile) return;
+    cudaEvent_t a;
+    if (ctx->ev_pool.empty()) cudaEventCreate(&a);
+    else {
+        a = ctx->ev_pool.back();
+        ctx->ev_pool.pop_back();
+    }
+    cudaEventRecord(a, ctx->stream);
+    ctx->ev_pending.push_back({phase, a, nullptr});
+}
+
+void prof_end(hgs_ctx* ctx) {
+    if (!ctx->profile || ctx->ev_pending.empty() || ctx->ev_pending.back().b) return;
+    cudaEvent_t b;
+    if (ctx->ev_pool.empty()) cudaEventCreate(&b);
+    else {
+        b = ctx->ev_pool.back();
+        ctx->ev_pool.pop_back();
+    }
+    cudaEventRecord(b, ctx->stream);
+    ctx->ev_pending.back().b = b;
+}
+
+void prof_collect(hgs_ctx* ctx) {
+    for (auto& e : ctx->ev_pending) {
+        if (e.b) {
+            cudaEventSynchronize(e.b);
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, e.a, e.b);
+            ctx->phase_ms[e.phase] += ms;
+            ctx->phase_calls[e.phase] += 1;
+            ctx->ev_pool.push_back(e.b);
+        }
+        ctx->ev_pool.push_back(e.a);
+    }
+    ctx->ev_pending.clear();
+}
+
 // ====================================================================== render
 // The full K1 -> sort -> K2 -> sort -> K4 pipeline; leaves the tape in ctx.
 hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, const double bg[3],
@@ -260,15 +302,19 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
         CK(ctx->visflag.ensure((size_t)N * 4));
         CK(ctx->vispos.ensure((size_t)N * 4));
         CK(ctx->scan_ws.ensure(scan_workspace_bytes(N) + 4096));
+        prof_begin(ctx, PH_PREPROCESS);
         preprocess_kernel<<<div_up(N, 256), 256, 0, st>>>(
             ctx->p4.as<float>(), ctx->cap4, n4, ctx->p3.as<float>(), ctx->cap3, n3, ctx->deg, ctx->cam, t, cutoff,
             tiles_x, ctx->rec.as<SplatRec>(), ctx->depth_key.as<uint32_t>(), ctx->ntiles.as<uint32_t>(), dc->stats,
             &dc->flags);
+        count_launch();
         CKL();
         visflag_kernel<<<div_up(N, 256), 256, 0, st>>>(ctx->ntiles.as<uint32_t>(), N, ctx->visflag.as<uint32_t>());
+        count_launch();
         exclusive_scan_u32(ctx->visflag.as<uint32_t>(), ctx->vispos.as<uint32_t>(), N, &dc->V,
                            ctx->scan_ws.as<uint32_t>(), st);
         CKL();
+        prof_end(ctx);
         CK(cudaMemcpyAsync(hc, dc, sizeof(Counters), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         V = hc->V;
@@ -278,29 +324,35 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
         CK(ctx->sort_v.ensure((size_t)V * 4));
         CK(ctx->sort_k2.ensure((size_t)V * 4));
         CK(ctx->sort_v2.ensure((size_t)V * 4));
+        prof_begin(ctx, PH_DEPTH_SORT);
         compact_kernel<<<div_up(N, 256), 256, 0, st>>>(ctx->ntiles.as<uint32_t>(), ctx->vispos.as<uint32_t>(),
                                                         ctx->depth_key.as<uint32_t>(), N, ctx->sort_k.as<uint32_t>(),
                                                         ctx->sort_v.as<uint32_t>());
+        count_launch();
         CKL();
         CK(ctx->sort_ws.ensure(radix_workspace_bytes((int)V) + 4096));
         // stable sort by f32 depth bits; gid (projected order) breaks ties
         int which = radix_sort_pairs(ctx->sort_k.as<uint32_t>(), ctx->sort_v.as<uint32_t>(), ctx->sort_k2.as<uint32_t>(),
                                      ctx->sort_v2.as<uint32_t>(), (int)V, 0, 32, ctx->sort_ws.as<uint32_t>(), st);
         CKL();
+        prof_end(ctx);
         uint32_t* sorted_gid = which ? ctx->sort_v2.as<uint32_t>() : ctx->sort_v.as<uint32_t>();
         ctx->sorted_gid = sorted_gid;
         CK(ctx->rec_sorted.ensure((size_t)V * sizeof(SplatRec)));
         CK(ctx->fast_sorted.ensure((size_t)V * sizeof(SplatFast)));
         CK(ctx->ntiles_sorted.ensure((size_t)V * 4));
         CK(ctx->inst_off.ensure((size_t)V * 4));
+        prof_begin(ctx, PH_DUPLICATE);
         gather_sorted_kernel<<<div_up((uint32_t)V, 256), 256, 0, st>>>(
             sorted_gid, (int)V, ctx->rec.as<SplatRec>(), ctx->ntiles.as<uint32_t>(), ctx->rec_sorted.as<SplatRec>(),
             ctx->fast_sorted.as<SplatFast>(), ctx->ntiles_sorted.as<uint32_t>());
+        count_launch();
         CKL();
         CK(ctx->scan_ws.ensure(scan_workspace_bytes((int)V) + 4096));
         exclusive_scan_u32(ctx->ntiles_sorted.as<uint32_t>(), ctx->inst_off.as<uint32_t>(), (int)V, &dc->I,
                            ctx->scan_ws.as<uint32_t>(), st);
         CKL();
+        prof_end(ctx);
         CK(cudaMemcpyAsync(hc, dc, sizeof(Counters), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         I = hc->I;
@@ -313,10 +365,14 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
         CK(ctx->inst_v.ensure((size_t)I * 4));
         CK(ctx->inst_k2.ensure((size_t)I * 4));
         CK(ctx->inst_v2.ensure((size_t)I * 4));
+        prof_begin(ctx, PH_DUPLICATE);
         duplicate_kernel<<<div_up((uint32_t)V, 256), 256, 0, st>>>(ctx->fast_sorted.as<SplatFast>(), (int)V,
                                                                     ctx->inst_off.as<uint32_t>(), tiles_x,
                                                                     ctx->inst_k.as<uint32_t>(), ctx->inst_v.as<uint32_t>());
+        count_launch();
         CKL();
+        prof_end(ctx);
+        prof_begin(ctx, PH_TILE_SORT);
         int bits = 1;
         while ((1 << bits) < n_tiles) ++bits;
         const int end_bit = ((bits + 7) / 8) * 8;
@@ -327,21 +383,27 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
         uint32_t* keys = which ? ctx->inst_k2.as<uint32_t>() : ctx->inst_k.as<uint32_t>();
         inst_vals = which ? ctx->inst_v2.as<uint32_t>() : ctx->inst_v.as<uint32_t>();
         tile_ranges_kernel<<<div_up((uint32_t)I, 256), 256, 0, st>>>(keys, (int)I, ctx->ranges.as<uint2>());
+        count_launch();
         CKL();
+        prof_end(ctx);
     }
     ctx->inst_vals_final = inst_vals;
+    prof_begin(ctx, PH_RASTER_FWD);
     raster_fwd_kernel<<<n_tiles, 256, 0, st>>>(
         ctx->ranges.as<uint2>(), inst_vals, ctx->fast_sorted.as<SplatFast>(), ctx->rec_sorted.as<SplatRec>(), W, H,
         tiles_x, (float)bg[0], (float)bg[1], (float)bg[2], ctx->img.as<float>(), ctx->last.as<uint32_t>(),
         ctx->tfinal.as<float>(), want_trans ? ctx->trans.as<float>() : nullptr, want_count ? ctx->count.as<uint32_t>() : nullptr,
         ctx->fix_list.as<uint32_t>(), &dc->fix_count);
+    count_launch();
     CKL();
     raster_fixup_kernel<<<ctx->sms * 2, 128, 0, st>>>(
         ctx->fix_list.as<uint32_t>(), &dc->fix_count, ctx->ranges.as<uint2>(), inst_vals,
         ctx->rec_sorted.as<SplatRec>(), W, tiles_x, bg[0], bg[1], bg[2], ctx->img.as<float>(),
         ctx->last.as<uint32_t>(), ctx->tfinal.as<float>(), want_trans ? ctx->trans.as<float>() : nullptr,
         want_count ? ctx->count.as<uint32_t>() : nullptr);
+    count_launch();
     CKL();
+    prof_end(ctx);
     CK(cudaMemcpyAsync(hc, dc, sizeof(Counters), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     ctx->stats.culled_depth = (int64_t)hc->stats[0];
@@ -358,6 +420,30 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
 }
 
 extern "C" {
+
+hgs_status hgs_profile(hgs_ctx* ctx, int enable) {
+    if (!ctx) return HGS_ERR_INVALID_ARGUMENT;
+    prof_collect(ctx);
+    ctx->profile = enable != 0;
+    return HGS_OK;
+}
+
+hgs_status hgs_profile_read(hgs_ctx* ctx, double* ms16, long long* calls16, int reset) {
+    if (!ctx) return HGS_ERR_INVALID_ARGUMENT;
+    CK(cudaStreamSynchronize(ctx->stream));
+    prof_collect(ctx);
+    for (int i = 0; i < 16; ++i) {
+        if (ms16) ms16[i] = ctx->phase_ms[i];
+        if (calls16) calls16[i] = ctx->phase_calls[i];
+        if (reset) {
+            ctx->phase_ms[i] = 0.0;
+            ctx->phase_calls[i] = 0;
+        }
+    }
+    return HGS_OK;
+}
+
+long long hgs_launch_count(void) { return launch_count(); }
 
 hgs_status hgs_ctx_create(int device, hgs_ctx** out) {
     if (!out) return HGS_ERR_INVALID_ARGUMENT;
@@ -500,6 +586,7 @@ hgs_status hgs_render(hgs_ctx* ctx, const hgs_camera* cam, double t, const doubl
     if (trans_host && opts && opts->transmittance_map)
         CK(cudaMemcpyAsync(trans_host, ctx->trans.p, npx * 4, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
+    prof_collect(ctx);
     if (stats) *stats = ctx->stats;
     return HGS_OK;
 }

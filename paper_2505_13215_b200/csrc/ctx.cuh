@@ -124,4 +124,34 @@ struct hgs_ctx {
     int64_t fixups = 0, fp64_splats = 0;
     hgs_render_stats stats{};
     uint32_t* sorted_gid = nullptr;       // V sorted gids
+
+    // ---- optional per-phase CUDA-event timing (bench.py roofline)
+    bool profile = false;
+    struct ProfEvent {
+        int phase;
+        cudaEvent_t a, b;
+    };
+    std::vector<cudaEvent_t> ev_pool;
+    std::vector<ProfEvent> ev_pending;
+    double phase_ms[16] = {0};
+    long long phase_calls[16] = {0};
 };
+
+// Phases timed by the profiler (hgs_profile_read order).
+enum HgsPhase {
+    PH_PREPROCESS = 0,  // K1 + visibility compaction
+    PH_DEPTH_SORT = 1,  // stable radix sort by f32 depth
+    PH_DUPLICATE = 2,   // gather + tile-count scan + K2 duplication
+    PH_TILE_SORT = 3,   // stable radix sort by tile + ranges
+    PH_RASTER_FWD = 4,  // K4 + FP64 fix-up
+    PH_LOSS = 5,        // K5
+    PH_RASTER_BWD = 6,  // K6 + exact pixels
+    PH_GAUSS_BWD = 7,   // K7
+    PH_ADAM = 8,        // K8 + statistic fold
+    PH_SWEEP = 9,       // K9
+    PH_UPLOAD = 10,     // host->device copies of the e2e path
+};
+
+void prof_begin(hgs_ctx* ctx, int phase);
+void prof_end(hgs_ctx* ctx);
+void prof_collect(hgs_ctx* ctx);

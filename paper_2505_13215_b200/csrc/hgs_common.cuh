@@ -79,3 +79,10 @@ enum : uint32_t {
 inline __host__ __device__ uint32_t div_up(uint32_t a, uint32_t b) { return (a + b - 1) / b; }
 
 }  // namespace hgs
+
+namespace hgs {
+// Process-wide count of kernels launched by this library (bench.py reports
+// the launches inside its timed region as gpu_launches).
+void count_launch(int n = 1);
+long long launch_count();
+}  // namespace hgs

@@ -200,8 +200,11 @@ void exclusive_scan_u32(const uint32_t* in, uint32_t* out, int n, uint32_t* tota
         return;
     }
     scan_reduce_kernel<<<nb, kScanThreads, 0, st>>>(in, n, ws);
+    count_launch();
     scan_single_kernel<<<1, 1024, 0, st>>>(ws, nb, total);
+    count_launch();
     scan_downsweep_kernel<<<nb, kScanThreads, 0, st>>>(in, n, ws, out);
+    count_launch();
 }
 
 size_t radix_workspace_bytes(int n) {
@@ -228,8 +231,10 @@ int radix_sort_pairs(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_
     uint32_t* vout = vals_alt;
     for (int shift = begin_bit; shift < end_bit; shift += 8) {
         radix_hist_kernel<<<nb, kSortThreads, 0, st>>>(kin, n, shift, nb, hist);
+        count_launch();
         exclusive_scan_u32(hist, offs, hist_n, nullptr, scan_ws, st);
         radix_scatter_kernel<<<nb, kSortThreads, 0, st>>>(kin, vin, kout, vout, n, shift, nb, offs);
+        count_launch();
         uint32_t* t = kin;
         kin = kout;
         kout = t;
@@ -241,4 +246,11 @@ int radix_sort_pairs(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_
     return cur;
 }
 
+}  // namespace hgs
+
+#include <atomic>
+namespace hgs {
+static std::atomic<long long> g_launches{0};
+void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
 }  // namespace hgs

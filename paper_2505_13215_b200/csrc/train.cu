@@ -60,6 +60,7 @@ hgs_status upload_image(hgs_ctx* ctx, const void* src, int dtype, int64_t n, DBu
         CK(cudaMemcpyAsync(ctx->stage.p, src, (size_t)n * 8, cudaMemcpyHostToDevice, ctx->stream));
         f64_to_f32_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(ctx->stage.as<double>(),
                                                                                dst.as<float>(), n);
+        count_launch();
         CKL();
     }
     return HGS_OK;
@@ -100,23 +101,30 @@ hgs_status run_backward(hgs_ctx* ctx, const float* lg, double scale) {
     CK(cudaMemsetAsync(ctx->accum.p, 0, (size_t)V * kAccStrideHost * 4, st));
     const int n_tiles = ctx->tiles_x * ctx->tiles_y;
     const uint32_t* fix_count = &ctx->counters.as<Counters>()->fix_count;
+    prof_begin(ctx, PH_RASTER_BWD);
     raster_bwd_kernel<<<n_tiles, 256, 0, st>>>(ctx->ranges.as<uint2>(), ctx->inst_vals_final,
                                                ctx->fast_sorted.as<SplatFast>(), ctx->rec_sorted.as<SplatRec>(),
                                                ctx->W, ctx->H, ctx->tiles_x, ctx->tfinal.as<float>(),
                                                ctx->last.as<uint32_t>(), lg, (float)ctx->bg[0], (float)ctx->bg[1],
                                                (float)ctx->bg[2], ctx->accum.as<float>());
+    count_launch();
     CKL();
     raster_bwd_exact_kernel<<<ctx->sms * 2, 128, 0, st>>>(
         ctx->fix_list.as<uint32_t>(), fix_count, ctx->ranges.as<uint2>(), ctx->inst_vals_final,
         ctx->rec_sorted.as<SplatRec>(), ctx->W, ctx->tiles_x, ctx->bg[0], ctx->bg[1], ctx->bg[2],
         ctx->last.as<uint32_t>(), lg, ctx->accum.as<float>());
+    count_launch();
     CKL();
+    prof_end(ctx);
+    prof_begin(ctx, PH_GAUSS_BWD);
     gaussian_bwd_kernel<<<div_up((uint32_t)V, 128), 128, 0, st>>>(
         (int)V, ctx->sorted_gid, ctx->accum.as<float>(), kAccStrideHost, (int)ctx->n4, ctx->p4.as<float>(), ctx->cap4,
         ctx->p3.as<float>(), ctx->cap3, ctx->deg, ctx->cam, ctx->t, scale, ctx->g4, ctx->g3, ctx->sn4.as<float>(),
         ctx->sn3.as<float>(), ctx->dgn4, ctx->dgn3, ctx->dcnt4, ctx->dcnt3, &ctx->rec_sorted.as<SplatRec>()->c00,
         (int)(sizeof(SplatRec) / sizeof(double)));
+    count_launch();
     CKL();
+    prof_end(ctx);
     return HGS_OK;
 }
 
@@ -138,16 +146,20 @@ hgs_status run_loss(hgs_ctx* ctx, const float* gt, double lambda) {
     Scratch* sc = scratch(ctx);
     CK(cudaMemsetAsync(sc, 0, offsetof(Scratch, skipped), st));  // ssim_sum, l1_sum
     const int vw = W - 10, vh = H - 10;
+    prof_begin(ctx, PH_LOSS);
     if (with_ssim) {
         CK(ctx->loss_ws.ensure((size_t)vw * vh * 9 * 4));
         dim3 g((vw + 31) / 32, (vh + 15) / 16, 3);
         ssim_fwd_kernel<<<g, 256, 0, st>>>(ctx->img.as<float>(), gt, W, H, ctx->loss_ws.as<float>(), &sc->ssim_sum);
+        count_launch();
         CKL();
     }
     dim3 gb((W + 31) / 32, (H + 15) / 16, 3);
     ssim_bwd_kernel<<<gb, 256, 0, st>>>(ctx->img.as<float>(), gt, W, H, ctx->loss_ws.as<float>(), (float)lambda,
                                         with_ssim ? 1 : 0, ctx->lgrad.as<float>(), &sc->l1_sum);
+    count_launch();
     CKL();
+    prof_end(ctx);
     return HGS_OK;
 }
 
@@ -179,23 +191,28 @@ hgs_status run_adam(hgs_ctx* ctx, const hgs_lrs* lrs, double mean_lr_scale) {
     A.lr_sh = (float)lrs->sh;
     const int n = (int)(ctx->n4 + ctx->n3);
     Scratch* sc = scratch(ctx);
+    prof_begin(ctx, PH_ADAM);
     if (n > 0) {
         adam_kernel<<<div_up(n, 256), 256, 0, st>>>(ctx->p4.as<float>(), ctx->g4, ctx->m4.as<float>(),
                                                     ctx->v4.as<float>(), ctx->cap4, (int)ctx->n4, ctx->p3.as<float>(),
                                                     ctx->g3, ctx->m3.as<float>(), ctx->v3.as<float>(), ctx->cap3,
                                                     (int)ctx->n3, ctx->deg, A, &sc->skipped, &sc->flags);
+        count_launch();
         CKL();
     }
     if (ctx->n4 > 0) {
         fold_stats_kernel<<<div_up((uint32_t)ctx->n4, 256), 256, 0, st>>>(ctx->gn4.as<float>(), ctx->cnt4.as<float>(),
                                                                           ctx->dgn4, ctx->dcnt4, (int)ctx->n4);
+        count_launch();
         CKL();
     }
     if (ctx->n3 > 0) {
         fold_stats_kernel<<<div_up((uint32_t)ctx->n3, 256), 256, 0, st>>>(ctx->gn3.as<float>(), ctx->cnt3.as<float>(),
                                                                           ctx->dgn3, ctx->dcnt3, (int)ctx->n3);
+        count_launch();
         CKL();
     }
+    prof_end(ctx);
     return HGS_OK;
 }
 
@@ -437,6 +454,7 @@ hgs_status hgs_sweep_convert(hgs_ctx* ctx, int64_t* moved_out, hgs_conversion_re
     uint32_t* mask = ctx->visflag.as<uint32_t>();
     uint32_t* pos = ctx->vispos.as<uint32_t>();
     convert_mask_kernel<<<div_up(n4, 256), 256, 0, st>>>(ctx->p4.as<float>(), ctx->cap4, n4, s, mask);
+    count_launch();
     CKL();
     exclusive_scan_u32(mask, pos, n4, &sc->count, ctx->scan_ws.as<uint32_t>(), st);
     CKL();
@@ -445,15 +463,19 @@ hgs_status hgs_sweep_convert(hgs_ctx* ctx, int64_t* moved_out, hgs_conversion_re
         ctx->p4.as<float>(), ctx->m4.as<float>(), ctx->v4.as<float>(), ctx->cap4, n4, mask, pos, ctx->p3.as<float>(),
         ctx->m3.as<float>(), ctx->v3.as<float>(), ctx->cap3, n3, ctx->deg, ctx->stage.as<long long>(),
         &sc->max_leak_bits, &sc->leak_sum, &sc->flags);
+    count_launch();
     CKL();
     // survivors: stable compaction of params and both moments
     const int R4 = rows4(ctx->deg);
     compact_survivors_kernel<<<div_up(n4, 256), 256, 0, st>>>(ctx->p4.as<float>(), ctx->p4_alt.as<float>(), R4,
                                                               ctx->cap4, n4, mask, pos);
+    count_launch();
     compact_survivors_kernel<<<div_up(n4, 256), 256, 0, st>>>(ctx->m4.as<float>(), ctx->m4_alt.as<float>(), R4,
                                                               ctx->cap4, n4, mask, pos);
+    count_launch();
     compact_survivors_kernel<<<div_up(n4, 256), 256, 0, st>>>(ctx->v4.as<float>(), ctx->v4_alt.as<float>(), R4,
                                                               ctx->cap4, n4, mask, pos);
+    count_launch();
     CKL();
     Scratch* h = static_cast<Scratch*>(ctx->pinned.p);
     CK(cudaMemcpyAsync(h, sc, sizeof(Scratch), cudaMemcpyDeviceToHost, st));
@@ -487,10 +509,10 @@ hgs_status hgs_sweep_convert(hgs_ctx* ctx, int64_t* moved_out, hgs_conversion_re
     return HGS_OK;
 }
 
-hgs_status hgs_train_step(hgs_ctx* ctx, int n_views, const hgs_camera* cams, const double* times,
-                          const float* const* gt_device, int batch_total, const hgs_train_opts* o, int apply_adam,
-                          double* loss_out) {
-    if (!ctx || n_views < 0 || (n_views && (!cams || !times || !gt_device)) || !o || batch_total <= 0)
+hgs_status train_step_impl(hgs_ctx* ctx, int n_views, const hgs_camera* cams, const double* times,
+                           const void* const* gt, int gt_dtype, int gt_on_device, int batch_total,
+                           const hgs_train_opts* o, int apply_adam, double* loss_out) {
+    if (!ctx || n_views < 0 || (n_views && (!cams || !times || !gt)) || !o || batch_total <= 0)
         return HGS_ERR_INVALID_ARGUMENT;
     CK(cudaSetDevice(ctx->device));
     hgs_status r = ensure_scratch(ctx);
@@ -498,9 +520,20 @@ hgs_status hgs_train_step(hgs_ctx* ctx, int n_views, const hgs_camera* cams, con
     hgs_raster_opts ro{o->weight_cutoff, 1, 0, 0};
     double loss = 0.0;
     for (int v = 0; v < n_views; ++v) {
+        const float* g = nullptr;
+        if (!gt_on_device) {
+            // e2e path: the view's ground truth comes from host memory
+            prof_begin(ctx, PH_UPLOAD);
+            r = upload_image(ctx, gt[v], gt_dtype, (int64_t)cams[v].width * cams[v].height * 3, ctx->gt_stage);
+            prof_end(ctx);
+            if (r != HGS_OK) return r;
+            g = ctx->gt_stage.as<float>();
+        } else {
+            g = static_cast<const float*>(gt[v]);
+        }
         r = hgs_render_pipeline(ctx, &cams[v], times[v], o->bg, &ro);
         if (r != HGS_OK) return r;
-        r = run_loss(ctx, gt_device[v], o->ssim_lambda);
+        r = run_loss(ctx, g, o->ssim_lambda);
         if (r != HGS_OK) return r;
         r = run_backward(ctx, ctx->lgrad.as<float>(), 1.0 / (double)batch_total);  // train.cpp:430-432
         if (r != HGS_OK) return r;
@@ -519,7 +552,21 @@ hgs_status hgs_train_step(hgs_ctx* ctx, int n_views, const hgs_camera* cams, con
         if (r != HGS_OK) return r;
         CK(cudaStreamSynchronize(ctx->stream));
     }
+    prof_collect(ctx);
     return HGS_OK;
+}
+
+hgs_status hgs_train_step(hgs_ctx* ctx, int n_views, const hgs_camera* cams, const double* times,
+                          const float* const* gt_device, int batch_total, const hgs_train_opts* o, int apply_adam,
+                          double* loss_out) {
+    return train_step_impl(ctx, n_views, cams, times, reinterpret_cast<const void* const*>(gt_device), HGS_F32, 1,
+                           batch_total, o, apply_adam, loss_out);
+}
+
+hgs_status hgs_train_step_host(hgs_ctx* ctx, int n_views, const hgs_camera* cams, const double* times,
+                               const void* const* gt_host, int dtype, int batch_total, const hgs_train_opts* o,
+                               int apply_adam, double* loss_out) {
+    return train_step_impl(ctx, n_views, cams, times, gt_host, dtype, 0, batch_total, o, apply_adam, loss_out);
 }
 
 }  // extern "C"
