@@ -91,9 +91,11 @@ typedef struct {
     double max_leakage, mean_leakage;
 } hgs_conversion_report;
 
-/* Per-render diagnostics (not in the reference). */
+/* Per-render diagnostics (not in the reference): visible splats, tile
+ * instances (the reference's list), instances the rasterizers walk after the
+ * exact tile-ellipse culling, and pixels recomposited by the FP64 fix-up. */
 typedef struct {
-    int64_t visible, instances, fixup_pixels, fp64_splats;
+    int64_t visible, instances, fixup_pixels, kept_instances;
 } hgs_render_info;
 
 /* ---- lifecycle -------------------------------------------------------- */

@@ -55,7 +55,7 @@ class ConversionReport(C.Structure):
 
 
 class RenderInfo(C.Structure):
-    _fields_ = [(n, C.c_int64) for n in ("visible", "instances", "fixup_pixels", "fp64_splats")]
+    _fields_ = [(n, C.c_int64) for n in ("visible", "instances", "fixup_pixels", "kept_instances")]
 
 
 class TrainOpts(C.Structure):

@@ -366,9 +366,10 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
         CK(ctx->inst_k2.ensure((size_t)I * 4));
         CK(ctx->inst_v2.ensure((size_t)I * 4));
         prof_begin(ctx, PH_DUPLICATE);
-        duplicate_kernel<<<div_up((uint32_t)V, 256), 256, 0, st>>>(ctx->fast_sorted.as<SplatFast>(), (int)V,
-                                                                    ctx->inst_off.as<uint32_t>(), tiles_x,
-                                                                    ctx->inst_k.as<uint32_t>(), ctx->inst_v.as<uint32_t>());
+        const int cull = want_count ? 0 : 1;  // count_map counts every box-covered splat
+        duplicate_kernel<<<div_up((uint32_t)I, 256), 256, 0, st>>>(
+            ctx->fast_sorted.as<SplatFast>(), ctx->rec_sorted.as<SplatRec>(), (int)V, ctx->inst_off.as<uint32_t>(),
+            tiles_x, cull, ctx->inst_k.as<uint32_t>(), ctx->inst_v.as<uint32_t>(), (int)I);
         count_launch();
         CKL();
         prof_end(ctx);
@@ -382,8 +383,31 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
         CKL();
         uint32_t* keys = which ? ctx->inst_k2.as<uint32_t>() : ctx->inst_k.as<uint32_t>();
         inst_vals = which ? ctx->inst_v2.as<uint32_t>() : ctx->inst_v.as<uint32_t>();
-        tile_ranges_kernel<<<div_up((uint32_t)I, 256), 256, 0, st>>>(keys, (int)I, ctx->ranges.as<uint2>());
-        count_launch();
+        ctx->inst_keys_all = keys;
+        ctx->inst_vals_all = inst_vals;
+        if (cull) {
+            // stable compaction of the instances that can reach the alpha cutoff in their tile
+            uint32_t* kk = which ? ctx->inst_k.as<uint32_t>() : ctx->inst_k2.as<uint32_t>();
+            uint32_t* vv = which ? ctx->inst_v.as<uint32_t>() : ctx->inst_v2.as<uint32_t>();
+            CK(ctx->inst_flag.ensure((size_t)I * 4));
+            CK(ctx->inst_pos.ensure((size_t)I * 4));
+            CK(ctx->scan_ws.ensure(scan_workspace_bytes((int)I) + 4096));
+            keep_flag_kernel<<<div_up((uint32_t)I, 256), 256, 0, st>>>(inst_vals, (int)I, ctx->inst_flag.as<uint32_t>());
+            count_launch();
+            exclusive_scan_u32(ctx->inst_flag.as<uint32_t>(), ctx->inst_pos.as<uint32_t>(), (int)I, &dc->I_kept,
+                               ctx->scan_ws.as<uint32_t>(), st);
+            compact_instances_kernel<<<div_up((uint32_t)I, 256), 256, 0, st>>>(keys, inst_vals, (int)I,
+                                                                            ctx->inst_pos.as<uint32_t>(), kk, vv);
+            count_launch();
+            CKL();
+            keys = kk;
+            inst_vals = vv;
+            tile_ranges_dev_kernel<<<div_up((uint32_t)I, 256), 256, 0, st>>>(keys, &dc->I_kept, ctx->ranges.as<uint2>());
+            count_launch();
+        } else {
+            tile_ranges_kernel<<<div_up((uint32_t)I, 256), 256, 0, st>>>(keys, (int)I, ctx->ranges.as<uint2>());
+            count_launch();
+        }
         CKL();
         prof_end(ctx);
     }
@@ -413,6 +437,7 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
     ctx->stats.degenerate_temporal = (int64_t)hc->stats[4];
     ctx->stats.projected = (int64_t)hc->stats[5];
     ctx->fixups = hc->fix_count;
+    ctx->kept = ctx->I ? (int64_t)hc->I_kept : 0;
     hgs_status s = check_flags(ctx, hc->flags);
     if (s != HGS_OK) return s;
     ctx->have_tape = true;
@@ -475,7 +500,7 @@ void hgs_ctx_destroy(hgs_ctx* ctx) {
                     &ctx->gn3, &ctx->cnt4, &ctx->cnt3, &ctx->sn4, &ctx->sn3, &ctx->rec, &ctx->depth_key,
                     &ctx->ntiles, &ctx->visflag, &ctx->vispos, &ctx->sort_k, &ctx->sort_v, &ctx->sort_k2,
                     &ctx->sort_v2, &ctx->rec_sorted, &ctx->fast_sorted, &ctx->ntiles_sorted, &ctx->inst_off,
-                    &ctx->inst_k, &ctx->inst_v, &ctx->inst_k2, &ctx->inst_v2, &ctx->ranges, &ctx->scan_ws,
+                    &ctx->inst_k, &ctx->inst_v, &ctx->inst_k2, &ctx->inst_v2, &ctx->ranges, &ctx->inst_flag, &ctx->inst_pos, &ctx->scan_ws,
                     &ctx->sort_ws, &ctx->counters, &ctx->img, &ctx->last, &ctx->tfinal, &ctx->trans, &ctx->count,
                     &ctx->fix_list, &ctx->accum, &ctx->lgrad, &ctx->gt_stage, &ctx->loss_ws, &ctx->stage};
     for (DBuf* b : bufs) b->release();
@@ -624,7 +649,7 @@ hgs_status hgs_render_info_get(hgs_ctx* ctx, hgs_render_info* info) {
     info->visible = ctx->V;
     info->instances = ctx->I;
     info->fixup_pixels = ctx->fixups;
-    info->fp64_splats = ctx->fp64_splats;
+    info->kept_instances = ctx->kept;
     return HGS_OK;
 }
 
@@ -677,13 +702,10 @@ hgs_status hgs_debug_instances(hgs_ctx* ctx, uint32_t* tile, uint32_t* gid, int6
     *n_out = I;
     if (I > cap || I == 0) return HGS_OK;
     std::vector<uint32_t> vals(I), sg(V);
-    std::vector<uint2> rg((size_t)ctx->tiles_x * ctx->tiles_y);
-    CK(cudaMemcpy(vals.data(), ctx->inst_vals_final, I * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(vals.data(), ctx->inst_vals_all, I * 4, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(sg.data(), ctx->sorted_gid, V * 4, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(rg.data(), ctx->ranges.p, rg.size() * sizeof(uint2), cudaMemcpyDeviceToHost));
-    for (size_t tl = 0; tl < rg.size(); ++tl)
-        for (uint32_t i = rg[tl].x; i < rg[tl].y; ++i) tile[i] = (uint32_t)tl;
-    for (int64_t i = 0; i < I; ++i) gid[i] = sg[vals[i]];
+    CK(cudaMemcpy(tile, ctx->inst_keys_all, I * 4, cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < I; ++i) gid[i] = sg[vals[i] & 0x7fffffffu];
     return HGS_OK;
 }
 

@@ -20,7 +20,7 @@ struct DBuf {
         if (p) cudaFree(p);
         p = nullptr;
         cap = 0;
-        size_t want = bytes + bytes / 4 + 256;
+        size_t want = bytes + bytes / 2 + 4096;  // grow by 1.5x: steady state never reallocates
         cudaError_t e = cudaMalloc(&p, want);
         if (e == cudaSuccess) cap = want;
         return e;
@@ -64,7 +64,8 @@ struct Counters {
     uint32_t I;
     uint32_t fix_count;
     uint32_t skipped;
-    uint32_t pad[3];
+    uint32_t I_kept;
+    uint32_t pad[2];
 };
 
 }  // namespace hgs
@@ -102,7 +103,7 @@ struct hgs_ctx {
     hgs::DBuf sort_k, sort_v, sort_k2, sort_v2;       // depth sort (V)
     hgs::DBuf rec_sorted, fast_sorted, ntiles_sorted, inst_off;
     hgs::DBuf inst_k, inst_v, inst_k2, inst_v2;       // tile sort (I)
-    hgs::DBuf ranges, scan_ws, sort_ws;
+    hgs::DBuf ranges, scan_ws, sort_ws, inst_flag, inst_pos;
     hgs::DBuf counters;  // [0..5] stats u64, [6] flags, fix_count, totals...
     hgs::DBuf img, last, tfinal, trans, count, fix_list;
     hgs::DBuf accum;     // backward per-sorted-splat accumulators
@@ -117,7 +118,10 @@ struct hgs_ctx {
     bool have_tape = false;
     int W = 0, H = 0, tiles_x = 0, tiles_y = 0;
     int64_t V = 0, I = 0;
-    uint32_t* inst_vals_final = nullptr;  // tile-sorted instance values
+    uint32_t* inst_vals_final = nullptr;  // tile-sorted instance values the rasterizers walk (culled)
+    uint32_t* inst_keys_all = nullptr;    // full tile-sorted instance list (reference semantics)
+    uint32_t* inst_vals_all = nullptr;
+    int64_t kept = 0;
     hgs::DevCamera cam{};
     double t = 0.0;
     double bg[3] = {0, 0, 0};

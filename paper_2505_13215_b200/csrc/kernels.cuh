@@ -16,9 +16,16 @@ __global__ void preprocess_kernel(const float* __restrict__ p4, int64_t cap4, in
 __global__ void gather_sorted_kernel(const uint32_t* __restrict__ sorted_gid, int V, const SplatRec* __restrict__ rec,
                                      const uint32_t* __restrict__ ntiles, SplatRec* __restrict__ rec_sorted,
                                      SplatFast* __restrict__ fast_sorted, uint32_t* __restrict__ ntiles_sorted);
-__global__ void duplicate_kernel(const SplatFast* __restrict__ fast, int V, const uint32_t* __restrict__ offsets,
-                                 int tiles_x, uint32_t* __restrict__ keys, uint32_t* __restrict__ vals);
+__global__ void duplicate_kernel(const SplatFast* __restrict__ fast, const SplatRec* __restrict__ exact, int V,
+                                 const uint32_t* __restrict__ offsets, int tiles_x, int cull,
+                                 uint32_t* __restrict__ keys, uint32_t* __restrict__ vals, int I);
+__global__ void keep_flag_kernel(const uint32_t* __restrict__ vals, int n, uint32_t* __restrict__ flag);
+__global__ void compact_instances_kernel(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals, int n,
+                                         const uint32_t* __restrict__ pos, uint32_t* __restrict__ keys_out,
+                                         uint32_t* __restrict__ vals_out);
 __global__ void tile_ranges_kernel(const uint32_t* __restrict__ keys, int n, uint2* __restrict__ ranges);
+__global__ void tile_ranges_dev_kernel(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ n_dev,
+                                       uint2* __restrict__ ranges);
 __global__ void raster_fwd_kernel(const uint2* __restrict__ ranges, const uint32_t* __restrict__ inst_val,
                                   const SplatFast* __restrict__ fast, const SplatRec* __restrict__ exact, int W, int H,
                                   int tiles_x, float bg_r, float bg_g, float bg_b, float* __restrict__ out_rgb,

@@ -10,10 +10,11 @@
 //     in FP64 with the oracle's operation order (power bit-identical);
 //   * transmittance floor (T < 1e-4): pixels whose T lands inside the
 //     accumulated error band are flagged and recomposited entirely in FP64
-//     by the fix-up kernel.
+//     by the (warp-per-pixel) fix-up kernels.
 // Splats whose conic is too anisotropic for the FP32 bound are flagged to
-// evaluate the exponent in FP64 (warp-uniform branch: every lane of a tile
-// walks the same splat at the same time).
+// evaluate the exponent in FP64.  Both rare paths are out-of-line calls so
+// the hot loop is never if-converted into predicated FP64 code; every lane of
+// a tile walks the same splat at the same time, so the branches are uniform.
 #pragma once
 
 #include "hgs_common.cuh"
@@ -23,18 +24,25 @@ namespace hgs {
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr double kLog2eD = 1.4426950408889634;
 
-// 64-byte FP32 view of a sorted splat.
+// 64-byte FP32 view of a sorted splat, stored as four 16-byte vectors so the
+// rasterizers stage it in shared memory as SoA and read it with LDS.128.
 struct __align__(16) SplatFast {
-    float sx_hi, sx_lo, sy_hi, sy_lo;  // screen mean as double-float
+    int32_t xr;      // x0 | (x1 - x0) << 16   (inclusive clamped pixel box)
+    int32_t yr;      // y0 | (y1 - y0) << 16
+    uint32_t fp64;   // 1: evaluate the exponent in FP64
+    float eps;       // certified relative error bound of the fast alpha
+    float sx_hi, sy_hi, sx_lo, sy_lo;  // screen mean as double-float
     float l00, l01, l11;               // Cholesky of 0.5*log2(e)*conic: x = |L d|^2 = power*log2(e)
     float alpha_f;
-    float r, g, b;
-    float eps;                         // certified relative error bound of the fast alpha
-    int16_t x0, x1, y0, y1;
-    uint32_t fp64;                     // 1: evaluate the exponent in FP64
-    uint32_t pad_;
+    float r, g, b, pcut;  // pcut: power above which alpha < 1/255 (tile culling)
 };
 static_assert(sizeof(SplatFast) == 64, "SplatFast layout");
+
+__device__ __forceinline__ int box_x0(int32_t r) { return r & 0xffff; }
+__device__ __forceinline__ int box_w(int32_t r) { return r >> 16; }
+__device__ __forceinline__ bool in_box(int32_t xr, int32_t yr, int px, int py) {
+    return (unsigned)(px - box_x0(xr)) <= (unsigned)box_w(xr) && (unsigned)(py - box_x0(yr)) <= (unsigned)box_w(yr);
+}
 
 __device__ __forceinline__ double exact_power(const SplatRec& e, double pcx, double pcy) {
     // backward.cpp:163-164 / raster.cpp:136-137, same rounding sequence (no FMA)
@@ -44,15 +52,20 @@ __device__ __forceinline__ double exact_power(const SplatRec& e, double pcx, dou
     return __dmul_rn(0.5, __dadd_rn(__dmul_rn(d0, q0), __dmul_rn(d1, q1)));
 }
 
-// FP32 exponent argument x = power*log2(e) (>= 0), fast or FP64 path.
-__device__ __forceinline__ float pair_x(const SplatFast& f, const SplatRec& e, float pxc, float pyc,
-                                        double pcx, double pcy) {
-    if (f.fp64) return __double2float_rn(__dmul_rn(exact_power(e, pcx, pcy), kLog2eD));
-    const float dx = __fsub_rn(__fsub_rn(pxc, f.sx_hi), f.sx_lo);
-    const float dy = __fsub_rn(__fsub_rn(pyc, f.sy_hi), f.sy_lo);
-    const float u1 = fmaf(f.l00, dx, f.l01 * dy);
-    const float u2 = f.l11 * dy;
-    return fmaf(u1, u1, u2 * u2);
+// The oracle's alpha, bit-for-bit up to the libm exp: a = alpha * exp(-power).
+__device__ __forceinline__ double exact_alpha(const SplatRec& e, double pcx, double pcy) {
+    return __dmul_rn(e.alpha, exp(-exact_power(e, pcx, pcy)));
+}
+
+// Out-of-line rare paths (keep the FP32 hot loop free of predicated FP64).
+static __device__ __noinline__ float exact_x(const SplatRec* e, double pcx, double pcy) {
+    return __double2float_rn(__dmul_rn(exact_power(*e, pcx, pcy), kLog2eD));
+}
+static __device__ __noinline__ bool exact_alpha_passes(const SplatRec* e, double pcx, double pcy) {
+    return !(exact_alpha(*e, pcx, pcy) < kAlphaCutoff);
+}
+static __device__ __noinline__ float2 exact_delta(const SplatRec* e, double pcx, double pcy) {
+    return make_float2((float)__dsub_rn(pcx, e->sx), (float)__dsub_rn(pcy, e->sy));
 }
 
 __device__ __forceinline__ float fast_exp2_neg(float x) {
@@ -61,20 +74,47 @@ __device__ __forceinline__ float fast_exp2_neg(float x) {
     return y;
 }
 
-// Decide whether a pair passes the alpha cutoff exactly as the FP64 oracle
-// would; returns alpha (fast) or a negative value when skipped.
-__device__ __forceinline__ float pair_alpha(const SplatFast& f, const SplatRec& e, float x, double pcx, double pcy,
-                                            float& g_out) {
+// Shared-memory SoA batch of splats.
+template <int B>
+struct SplatBatch {
+    int4 hdr[B];     // xr, yr, fp64, eps bits
+    float4 mean[B];  // sx_hi, sy_hi, sx_lo, sy_lo
+    float4 chol[B];  // l00, l01, l11, alpha_f
+    float4 col[B];   // r, g, b, -
+    uint32_t j[B];   // sorted splat index (for the exact record)
+
+    __device__ __forceinline__ void load(int t, const SplatFast* __restrict__ fast, uint32_t jj) {
+        const float4* src = reinterpret_cast<const float4*>(fast + jj);
+        const float4 a = __ldg(src + 0), b = __ldg(src + 1), c = __ldg(src + 2), d = __ldg(src + 3);
+        hdr[t] = make_int4(__float_as_int(a.x), __float_as_int(a.y), __float_as_int(a.z), __float_as_int(a.w));
+        mean[t] = b;
+        chol[t] = c;
+        col[t] = d;
+        j[t] = jj;
+    }
+};
+
+// FP32 exponent argument x = power*log2(e) (>= 0) on the fast path.
+__device__ __forceinline__ float fast_x(const float4 m, const float4 L, float pxc, float pyc, float& dx, float& dy) {
+    dx = __fsub_rn(__fsub_rn(pxc, m.x), m.z);
+    dy = __fsub_rn(__fsub_rn(pyc, m.y), m.w);
+    const float u1 = fmaf(L.x, dx, L.y * dy);
+    const float u2 = L.z * dy;
+    return fmaf(u1, u1, u2 * u2);
+}
+
+// Alpha of a pair, or a negative value when the oracle skips it (a < 1/255);
+// decisions inside the certified guard band are taken in FP64.
+__device__ __forceinline__ float pair_alpha(float alpha_f, float eps, float x, const SplatRec* e, double pcx,
+                                            double pcy, float& g_out) {
     const float g = fast_exp2_neg(x);
-    const float a = f.alpha_f * g;
+    const float a = alpha_f * g;
     g_out = g;
     constexpr float kCut = 1.0f / 255.0f;
-    const float band = 1.5f * f.eps * kCut;
+    const float band = 1.5f * eps * kCut;
     if (a < kCut - band) return -1.0f;
-    if (a >= kCut + band) return a;
-    // guard band: the oracle's own test, a = alpha * exp(-power) < 1/255 in FP64
-    const double ad = __dmul_rn(e.alpha, exp(-exact_power(e, pcx, pcy)));
-    return (ad < kAlphaCutoff) ? -1.0f : a;
+    if (a < kCut + band && !exact_alpha_passes(e, pcx, pcy)) return -1.0f;
+    return a;
 }
 
 }  // namespace hgs
