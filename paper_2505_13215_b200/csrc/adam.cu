@@ -18,6 +18,7 @@ namespace {
 
 __device__ __forceinline__ bool row_finite(const float* g, int64_t cap, int i, int r0, int d) {
     bool ok = true;
+#pragma unroll 8
     for (int k = 0; k < d; ++k) ok &= isfinite(g[(int64_t)(r0 + k) * cap + i]);
     return ok;
 }
@@ -29,16 +30,34 @@ __device__ __forceinline__ void adam_class(float* p, float* g, float* m, float* 
         for (int k = 0; k < d; ++k) g[(int64_t)(r0 + k) * cap + i] = 0.f;
         return;
     }
-    for (int k = 0; k < d; ++k) {
-        const int64_t o = (int64_t)(r0 + k) * cap + i;
-        const float gr = g[o];
-        const float mk = A.b1 * m[o] + A.one_m_b1 * gr;
-        const float vk = A.b2 * v[o] + A.one_m_b2 * gr * gr;
-        m[o] = mk;
-        v[o] = vk;
-        const float mhat = mk * A.inv_bc1, vhat = vk * A.inv_bc2;
-        p[o] = p[o] - lr * mhat / (sqrtf(vhat) + 1e-15f);
-        g[o] = 0.f;
+    // chunks of 8 rows: all 32 loads of a chunk are issued before any store
+    // (memory-level parallelism; the four arrays never alias)
+    constexpr int C = 8;
+    for (int k0 = 0; k0 < d; k0 += C) {
+        float gr[C], mm[C], vv[C], pp[C];
+#pragma unroll
+        for (int u = 0; u < C; ++u) {
+            if (k0 + u < d) {
+                const int64_t o = (int64_t)(r0 + k0 + u) * cap + i;
+                gr[u] = __ldcs(&g[o]);
+                mm[u] = __ldcs(&m[o]);
+                vv[u] = __ldcs(&v[o]);
+                pp[u] = __ldcs(&p[o]);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < C; ++u) {
+            if (k0 + u < d) {
+                const int64_t o = (int64_t)(r0 + k0 + u) * cap + i;
+                const float mk = A.b1 * mm[u] + A.one_m_b1 * gr[u];
+                const float vk = A.b2 * vv[u] + A.one_m_b2 * gr[u] * gr[u];
+                const float mhat = mk * A.inv_bc1, vhat = vk * A.inv_bc2;
+                __stcs(&m[o], mk);
+                __stcs(&v[o], vk);
+                __stcs(&p[o], pp[u] - lr * mhat / (sqrtf(vhat) + 1e-15f));
+                __stcs(&g[o], 0.f);
+            }
+        }
     }
 }
 

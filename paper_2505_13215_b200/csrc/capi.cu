@@ -342,10 +342,12 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
         CK(ctx->fast_sorted.ensure((size_t)V * sizeof(SplatFast)));
         CK(ctx->ntiles_sorted.ensure((size_t)V * 4));
         CK(ctx->inst_off.ensure((size_t)V * 4));
+        CK(ctx->sorted_of_gid.ensure((size_t)N * 4));
         prof_begin(ctx, PH_DUPLICATE);
+        CK(cudaMemsetAsync(ctx->sorted_of_gid.p, 0xff, (size_t)N * 4, st));
         gather_sorted_kernel<<<div_up((uint32_t)V, 256), 256, 0, st>>>(
             sorted_gid, (int)V, ctx->rec.as<SplatRec>(), ctx->ntiles.as<uint32_t>(), ctx->rec_sorted.as<SplatRec>(),
-            ctx->fast_sorted.as<SplatFast>(), ctx->ntiles_sorted.as<uint32_t>());
+            ctx->fast_sorted.as<SplatFast>(), ctx->ntiles_sorted.as<uint32_t>(), ctx->sorted_of_gid.as<uint32_t>());
         count_launch();
         CKL();
         CK(ctx->scan_ws.ensure(scan_workspace_bytes((int)V) + 4096));
@@ -413,7 +415,7 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
     }
     ctx->inst_vals_final = inst_vals;
     prof_begin(ctx, PH_RASTER_FWD);
-    raster_fwd_kernel<<<n_tiles, 256, 0, st>>>(
+    raster_fwd_kernel<<<n_tiles, 128, 0, st>>>(
         ctx->ranges.as<uint2>(), inst_vals, ctx->fast_sorted.as<SplatFast>(), ctx->rec_sorted.as<SplatRec>(), W, H,
         tiles_x, (float)bg[0], (float)bg[1], (float)bg[2], ctx->img.as<float>(), ctx->last.as<uint32_t>(),
         ctx->tfinal.as<float>(), want_trans ? ctx->trans.as<float>() : nullptr, want_count ? ctx->count.as<uint32_t>() : nullptr,
@@ -500,7 +502,7 @@ void hgs_ctx_destroy(hgs_ctx* ctx) {
                     &ctx->gn3, &ctx->cnt4, &ctx->cnt3, &ctx->sn4, &ctx->sn3, &ctx->rec, &ctx->depth_key,
                     &ctx->ntiles, &ctx->visflag, &ctx->vispos, &ctx->sort_k, &ctx->sort_v, &ctx->sort_k2,
                     &ctx->sort_v2, &ctx->rec_sorted, &ctx->fast_sorted, &ctx->ntiles_sorted, &ctx->inst_off,
-                    &ctx->inst_k, &ctx->inst_v, &ctx->inst_k2, &ctx->inst_v2, &ctx->ranges, &ctx->inst_flag, &ctx->inst_pos, &ctx->scan_ws,
+                    &ctx->inst_k, &ctx->inst_v, &ctx->inst_k2, &ctx->inst_v2, &ctx->ranges, &ctx->sorted_of_gid, &ctx->inst_flag, &ctx->inst_pos, &ctx->scan_ws,
                     &ctx->sort_ws, &ctx->counters, &ctx->img, &ctx->last, &ctx->tfinal, &ctx->trans, &ctx->count,
                     &ctx->fix_list, &ctx->accum, &ctx->lgrad, &ctx->gt_stage, &ctx->loss_ws, &ctx->stage};
     for (DBuf* b : bufs) b->release();

@@ -82,16 +82,93 @@ __device__ inline void sh_basis_grad_d(const double d[3], int deg, double g[16][
 
 __device__ inline double sigmoid(double x) { return 1.0 / (1.0 + exp(-x)); }
 
+// sh.cpp:25-47 in FP32
+__device__ inline void sh_basis_f(const float d[3], int deg, float out[16]) {
+    const float x = d[0], y = d[1], z = d[2];
+    out[0] = 0.28209479177387814f;
+    if (deg < 1) return;
+    out[1] = -0.4886025119029199f * y;
+    out[2] = 0.4886025119029199f * z;
+    out[3] = -0.4886025119029199f * x;
+    if (deg < 2) return;
+    const float xx = x * x, yy = y * y, zz = z * z;
+    out[4] = 1.0925484305920792f * x * y;
+    out[5] = -1.0925484305920792f * y * z;
+    out[6] = 0.31539156525252005f * (2.0f * zz - xx - yy);
+    out[7] = -1.0925484305920792f * x * z;
+    out[8] = 0.5462742152960396f * (xx - yy);
+    if (deg < 3) return;
+    out[9] = -0.5900435899266435f * y * (3.0f * xx - yy);
+    out[10] = 2.890611442640554f * x * y * z;
+    out[11] = -0.4570457994644658f * y * (4.0f * zz - xx - yy);
+    out[12] = 0.3731763325901154f * z * (2.0f * zz - 3.0f * xx - 3.0f * yy);
+    out[13] = -0.4570457994644658f * x * (4.0f * zz - xx - yy);
+    out[14] = 1.445305721320277f * z * (xx - yy);
+    out[15] = -0.5900435899266435f * x * (xx - 3.0f * yy);
+}
+
+// sum_k w_k * dY_k/d(dir) (sh.cpp:49-71) without materialising the 16x3 Jacobian
+__device__ inline void sh_dir_grad_f(const float d[3], int deg, const float w[16], float g[3]) {
+    const float x = d[0], y = d[1], z = d[2];
+    g[0] = g[1] = g[2] = 0.0f;
+    if (deg < 1) return;
+    const float C1 = 0.4886025119029199f;
+    g[1] -= C1 * w[1];
+    g[2] += C1 * w[2];
+    g[0] -= C1 * w[3];
+    if (deg < 2) return;
+    const float A = 1.0925484305920792f, B = 0.31539156525252005f, Cc = 0.5462742152960396f;
+    g[0] += A * y * w[4];
+    g[1] += A * x * w[4];
+    g[1] -= A * z * w[5];
+    g[2] -= A * y * w[5];
+    g[0] += B * (-2.0f * x) * w[6];
+    g[1] += B * (-2.0f * y) * w[6];
+    g[2] += B * (4.0f * z) * w[6];
+    g[0] -= A * z * w[7];
+    g[2] -= A * x * w[7];
+    g[0] += Cc * (2.0f * x) * w[8];
+    g[1] += Cc * (-2.0f * y) * w[8];
+    if (deg < 3) return;
+    const float xx = x * x, yy = y * y, zz = z * z;
+    const float D0 = -0.5900435899266435f, D1 = 2.890611442640554f, D2 = -0.4570457994644658f,
+                D3 = 0.3731763325901154f, D5 = 1.445305721320277f;
+    g[0] += D0 * (6.0f * x * y) * w[9];
+    g[1] += D0 * (3.0f * xx - 3.0f * yy) * w[9];
+    g[0] += D1 * (y * z) * w[10];
+    g[1] += D1 * (x * z) * w[10];
+    g[2] += D1 * (x * y) * w[10];
+    g[0] += D2 * (-2.0f * x * y) * w[11];
+    g[1] += D2 * (4.0f * zz - xx - 3.0f * yy) * w[11];
+    g[2] += D2 * (8.0f * y * z) * w[11];
+    g[0] += D3 * (-6.0f * x * z) * w[12];
+    g[1] += D3 * (-6.0f * y * z) * w[12];
+    g[2] += D3 * (6.0f * zz - 3.0f * xx - 3.0f * yy) * w[12];
+    g[0] += D2 * (4.0f * zz - 3.0f * xx - yy) * w[13];
+    g[1] += D2 * (-2.0f * x * y) * w[13];
+    g[2] += D2 * (8.0f * x * z) * w[13];
+    g[0] += D5 * (2.0f * x * z) * w[14];
+    g[1] += D5 * (-2.0f * y * z) * w[14];
+    g[2] += D5 * (xx - yy) * w[14];
+    g[0] += D0 * (3.0f * xx - 3.0f * yy) * w[15];
+    g[1] += D0 * (-6.0f * x * y) * w[15];
+}
+
 }  // namespace
 
-__global__ void __launch_bounds__(128) gaussian_bwd_kernel(
-    int V, const uint32_t* __restrict__ sorted_gid, const float* __restrict__ accum, int acc_stride, int n4,
+__global__ void __launch_bounds__(128, 4) gaussian_bwd_kernel(
+    int N, const uint32_t* __restrict__ sorted_of_gid, const float* __restrict__ accum, int acc_stride, int n4,
     const float* __restrict__ p4, int64_t cap4, const float* __restrict__ p3, int64_t cap3, int deg, DevCamera cam,
     double t, double scale, float* __restrict__ g4, float* __restrict__ g3, float* __restrict__ sn4,
     float* __restrict__ sn3, float* __restrict__ gn4, float* __restrict__ gn3, float* __restrict__ cnt4,
     float* __restrict__ cnt3, const double* __restrict__ conic_src, int conic_stride) {
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= V) return;
+    // one thread per Gaussian in pool order (coalesced SoA parameter and
+    // gradient rows); the splat's accumulators are found through the
+    // gid -> depth-sorted index map written by the gather kernel
+    const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid >= N) return;
+    const uint32_t j = sorted_of_gid[gid];
+    if (j == 0xffffffffu) return;  // not visible in this view
     const float* acc = accum + (size_t)j * acc_stride;
     const double d_rgb[3] = {acc[0], acc[1], acc[2]};
     const double d_alpha = acc[3];
@@ -100,9 +177,8 @@ __global__ void __launch_bounds__(128) gaussian_bwd_kernel(
     if (d_rgb[0] == 0.0 && d_rgb[1] == 0.0 && d_rgb[2] == 0.0 && d_alpha == 0.0 && d_screen[0] == 0.0 &&
         d_screen[1] == 0.0 && dC[0][0] == 0.0 && dC[0][1] == 0.0 && dC[1][1] == 0.0)
         return;  // untouched (backward.cpp:226)
-    const uint32_t gid = sorted_gid[j];
-    const bool dyn = (int)gid < n4;
-    const int i = dyn ? (int)gid : (int)gid - n4;
+    const bool dyn = gid < n4;
+    const int i = dyn ? gid : gid - n4;
     const float* P = dyn ? p4 : p3;
     const int64_t cap = dyn ? cap4 : cap3;
     auto prm = [&](int row) { return (double)P[(int64_t)row * cap + i]; };
@@ -209,33 +285,42 @@ __global__ void __launch_bounds__(128) gaussian_bwd_kernel(
     double dir[3] = {0.0, 0.0, 1.0};
     if (vd > 0.0)
         for (int k = 0; k < 3; ++k) dir[k] = v[k] / vd;
-    double basis[16];
-    sh_basis_d(dir, deg, basis);
+    // SH part in FP32 (tolerance-level quantities; keeps the kernel's register
+    // footprint small enough for useful occupancy)
+    const float df[3] = {(float)dir[0], (float)dir[1], (float)dir[2]};
+    float basis[16];
+    sh_basis_f(df, deg, basis);
     const int K = sh_count(deg);
     const int shrow = dyn ? R4_SH : R3_SH;
-    double raw[3] = {0.0, 0.0, 0.0};
+    const float* Pf = P + i;
+    float raw[3] = {0.5f, 0.5f, 0.5f};
     for (int k = 0; k < K; ++k)
-        for (int c = 0; c < 3; ++c) raw[c] += basis[k] * prm(shrow + 3 * k + c);
-    double drr[3];
-    for (int c = 0; c < 3; ++c) {
-        raw[c] += 0.5;
-        drr[c] = (raw[c] < 0.0 || raw[c] > 1.0) ? 0.0 : d_rgb[c];
-    }
-    double bgrad[16][3];
-    sh_basis_grad_d(dir, deg, bgrad);
-    double d_dir[3] = {0.0, 0.0, 0.0};
+        for (int c = 0; c < 3; ++c) raw[c] = fmaf(basis[k], Pf[(int64_t)(shrow + 3 * k + c) * cap], raw[c]);
+    float drr[3];
+    for (int c = 0; c < 3; ++c) drr[c] = (raw[c] < 0.0f || raw[c] > 1.0f) ? 0.0f : (float)d_rgb[c];
     float* G = dyn ? g4 : g3;
     auto gadd = [&](int row, double val) {
         float* p = &G[(int64_t)row * cap + i];
         *p = *p + (float)(scale * val);
     };
+    float dotc[16];
+    const float fs = (float)scale;
     for (int k = 0; k < K; ++k) {
-        double dotc = 0.0;
+        float dc = 0.0f;
         for (int c = 0; c < 3; ++c) {
-            gadd(shrow + 3 * k + c, basis[k] * drr[c]);
-            dotc += drr[c] * prm(shrow + 3 * k + c);
+            float* p = &G[(int64_t)(shrow + 3 * k + c) * cap + i];
+            *p = fmaf(fs, basis[k] * drr[c], *p);
+            dc = fmaf(drr[c], Pf[(int64_t)(shrow + 3 * k + c) * cap], dc);
         }
-        for (int c = 0; c < 3; ++c) d_dir[c] += bgrad[k][c] * dotc;
+        dotc[k] = dc;
+    }
+    double d_dir[3];
+    {
+        float dd[3];
+        sh_dir_grad_f(df, deg, dotc, dd);
+        d_dir[0] = dd[0];
+        d_dir[1] = dd[1];
+        d_dir[2] = dd[2];
     }
     if (vd > 0.0)
         for (int a = 0; a < 3; ++a) {

@@ -15,7 +15,8 @@ __global__ void preprocess_kernel(const float* __restrict__ p4, int64_t cap4, in
 // raster_fwd.cu (K2 + K4)
 __global__ void gather_sorted_kernel(const uint32_t* __restrict__ sorted_gid, int V, const SplatRec* __restrict__ rec,
                                      const uint32_t* __restrict__ ntiles, SplatRec* __restrict__ rec_sorted,
-                                     SplatFast* __restrict__ fast_sorted, uint32_t* __restrict__ ntiles_sorted);
+                                     SplatFast* __restrict__ fast_sorted, uint32_t* __restrict__ ntiles_sorted,
+                                     uint32_t* __restrict__ sorted_of_gid);
 __global__ void duplicate_kernel(const SplatFast* __restrict__ fast, const SplatRec* __restrict__ exact, int V,
                                  const uint32_t* __restrict__ offsets, int tiles_x, int cull,
                                  uint32_t* __restrict__ keys, uint32_t* __restrict__ vals, int I);
@@ -57,7 +58,7 @@ __global__ void raster_bwd_exact_kernel(const uint32_t* __restrict__ fix_list, c
                                         double bg_g, double bg_b, const uint32_t* __restrict__ last_arr,
                                         const float* __restrict__ dL_dimg, float* __restrict__ accum);
 // gaussian_bwd.cu (K7)
-__global__ void gaussian_bwd_kernel(int V, const uint32_t* __restrict__ sorted_gid, const float* __restrict__ accum,
+__global__ void gaussian_bwd_kernel(int N, const uint32_t* __restrict__ sorted_of_gid, const float* __restrict__ accum,
                                     int acc_stride, int n4, const float* __restrict__ p4, int64_t cap4,
                                     const float* __restrict__ p3, int64_t cap3, int deg, DevCamera cam, double t,
                                     double scale, float* __restrict__ g4, float* __restrict__ g3,

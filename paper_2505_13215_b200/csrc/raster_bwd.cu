@@ -8,9 +8,10 @@
 // nearly occluded splats, unlike C_out - prefix) and recovering
 // T_i = T_{i+1} / (1 - a_i) from the stored final transmittance.
 //
-// Per splat and warp the 9 accumulators are reduced with a transposing
-// butterfly (14 shuffles instead of 45), summed across warps with shared
-// atomics, and flushed once per tile batch with vector red.global.add.
+// Two pixels per thread (rows y and y+8 of the tile) share every staged splat;
+// per splat and warp their 9 accumulators are summed in registers, reduced
+// with a transposing butterfly (14 shuffles instead of 45) and added with one
+// red.global.add.f32 instruction (9 lanes, one per accumulator).
 // Pixels the forward handed to the FP64 fix-up are back-propagated by
 // raster_bwd_exact_kernel (one warp per pixel, FP64).
 #include "kernels.cuh"
@@ -57,137 +58,150 @@ __device__ __forceinline__ float warp_sum(float v) {
     return v;
 }
 
-__device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d) {
-    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
-                 : "memory");
-}
 
 }  // namespace
 
-// accum layout: 12 floats per sorted splat (16-byte aligned for v4 reds):
+// accum layout: 12 floats per sorted splat (16-byte aligned):
 //   [0..2] d_rgb, [3] d_alpha (w.r.t. the base alpha), [4..5] d_screen,
 //   [6] d_conic00, [7] d_conic01 (= d_conic10), [8] d_conic11, [9..11] pad
 constexpr int kAccStride = 12;
+constexpr int kThreadsB = 128;  // two pixels (rows y and y+8) per thread
 
-__global__ void __launch_bounds__(256) raster_bwd_kernel(
+__device__ __forceinline__ void red_add(float* addr, float v) {
+    asm volatile("red.global.add.f32 [%0], %1;" ::"l"(addr), "f"(v) : "memory");
+}
+
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// Reverse-sweep state of one pixel.
+struct PixBwd {
+    float gr, gg, gb;  // dL/dC
+    float T;           // transmittance after the current splat
+    float Sr, Sg, Sb;  // suffix colour (incl. T_final * bg)
+    uint32_t last;
+};
+
+// One pair of backward.cpp:204-221, accumulated into v[0..8].
+__device__ __forceinline__ bool backprop_pair(PixBwd& s, const int4 hdr, const float4 m, const float4 L, const float4 col,
+                                              const float4 cn, const SplatRec* e, float pxc, float pyc, double pcx,
+                                              double pcy, float v[9]) {
+    float x, dx, dy;
+    if (__int_as_float(hdr.w) < 0.0f) {  // FP64 exponent path
+        x = exact_x(e, pcx, pcy);
+        const float2 d = exact_delta(e, pcx, pcy);
+        dx = d.x;
+        dy = d.y;
+    } else {
+        x = fast_x(m, L, pxc, pyc, dx, dy);
+    }
+    float g;
+    const float a = pair_alpha(L.w, __int_as_float(hdr.z), col.w, x, e, pcx, pcy, g);
+    if (a < 0.0f) return false;
+    const float inv = rcp_approx(1.0f - a);
+    const float Ti = s.T * inv;  // transmittance before this splat
+    const float w = a * Ti;
+    // d_a = g_pix . (rgb * T_i - S / (1 - a))
+    const float d_a =
+        s.gr * fmaf(col.x, Ti, -s.Sr * inv) + s.gg * fmaf(col.y, Ti, -s.Sg * inv) + s.gb * fmaf(col.z, Ti, -s.Sb * inv);
+    s.Sr = fmaf(col.x, w, s.Sr);
+    s.Sg = fmaf(col.y, w, s.Sg);
+    s.Sb = fmaf(col.z, w, s.Sb);
+    s.T = Ti;
+    v[0] = fmaf(w, s.gr, v[0]);
+    v[1] = fmaf(w, s.gg, v[1]);
+    v[2] = fmaf(w, s.gb, v[2]);
+    v[3] = fmaf(g, d_a, v[3]);
+    const float gdg = g * (L.w * d_a);  // g * d_g, d_g = alpha * d_a
+    v[4] = fmaf(gdg, fmaf(cn.x, dx, cn.y * dy), v[4]);
+    v[5] = fmaf(gdg, fmaf(cn.z, dx, cn.w * dy), v[5]);
+    const float hc = -0.5f * gdg;
+    v[6] = fmaf(hc * dx, dx, v[6]);
+    v[7] = fmaf(hc * dx, dy, v[7]);
+    v[8] = fmaf(hc * dy, dy, v[8]);
+    return true;
+}
+
+__global__ void __launch_bounds__(kThreadsB) raster_bwd_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ inst_val, const SplatFast* __restrict__ fast,
     const SplatRec* __restrict__ exact, int W, int H, int tiles_x, const float* __restrict__ tfinal,
     const uint32_t* __restrict__ last_arr, const float* __restrict__ dL_dimg, float bg_r, float bg_g, float bg_b,
     float* __restrict__ accum) {
     __shared__ SplatBatch<kBatchB> sb;
     __shared__ float4 s_conic[kBatchB];  // float conic (c00, c01, c10, c11)
-    __shared__ float s_acc[kBatchB][kAccStride - 3];
     __shared__ uint32_t s_maxlast;
     const int tile = blockIdx.x;
     const int tx = tile % tiles_x, ty = tile / tiles_x;
     const int px = tx * kTile + (threadIdx.x & 15);
-    const int py = ty * kTile + (threadIdx.x >> 4);
-    const bool inside = px < W && py < H;
+    const int py0 = ty * kTile + (threadIdx.x >> 4), py1 = py0 + 8;
     const uint2 rg = ranges[tile];
-    const float pxc = (float)px + 0.5f, pyc = (float)py + 0.5f;
-    const double pcx = (double)px + 0.5, pcy = (double)py + 0.5;
+    const float pxc = (float)px + 0.5f, pyc0 = (float)py0 + 0.5f, pyc1 = (float)py1 + 0.5f;
+    const double pcx = (double)px + 0.5, pcy0 = (double)py0 + 0.5, pcy1 = (double)py1 + 0.5;
 
-    uint32_t last = rg.x;
-    float gr = 0.f, gg = 0.f, gb = 0.f, T = 1.f;
-    if (inside) {
+    auto init = [&](int py, PixBwd& s) {
+        s = PixBwd{0.f, 0.f, 0.f, 1.f, 0.f, 0.f, 0.f, rg.x};
+        if (px >= W || py >= H) return;
         const int pix = py * W + px;
         const uint32_t l = last_arr[pix];
-        gr = dL_dimg[pix * 3 + 0];
-        gg = dL_dimg[pix * 3 + 1];
-        gb = dL_dimg[pix * 3 + 2];
-        T = tfinal[pix];
+        s.gr = dL_dimg[pix * 3 + 0];
+        s.gg = dL_dimg[pix * 3 + 1];
+        s.gb = dL_dimg[pix * 3 + 2];
+        s.T = tfinal[pix];
+        s.Sr = s.T * bg_r;
+        s.Sg = s.T * bg_g;
+        s.Sb = s.T * bg_b;
         // flagged pixels go through the exact kernel; zero gradient = untouched (backward.cpp:188)
-        if (!(l & 0x80000000u) && (gr != 0.f || gg != 0.f || gb != 0.f)) last = l;
-    }
+        if (!(l & 0x80000000u) && (s.gr != 0.f || s.gg != 0.f || s.gb != 0.f)) s.last = l;
+    };
+    PixBwd s0, s1;
+    init(py0, s0);
+    init(py1, s1);
     if (threadIdx.x == 0) s_maxlast = rg.x;
     __syncthreads();
-    if (last > rg.x) atomicMax(&s_maxlast, last);
+    const uint32_t ml = max(s0.last, s1.last);
+    if (ml > rg.x) atomicMax(&s_maxlast, ml);
     __syncthreads();
     const uint32_t end = s_maxlast;
+    const int lane = threadIdx.x & 31;
 
-    // Reverse sweep (backward.cpp:204-221): suffix S starts at T_final * bg and
-    // accumulates c_j a_j T_j from the back; T_i = T_{i+1} / (1 - a_i).
-    float Sr = T * bg_r, Sg = T * bg_g, Sb = T * bg_b;
     const int nbatch = (int)((end - rg.x + kBatchB - 1) / kBatchB);
     for (int bi = nbatch - 1; bi >= 0; --bi) {
         const uint32_t base = rg.x + (uint32_t)bi * kBatchB;
         const int nb = (int)min((uint32_t)kBatchB, end - base);
-        if ((int)threadIdx.x < nb) {
-            const uint32_t j = inst_val[base + threadIdx.x];
-            sb.load(threadIdx.x, fast, j);
+        __syncthreads();
+        for (int t = threadIdx.x; t < nb; t += kThreadsB) {
+            const uint32_t j = inst_val[base + t];
+            sb.load(t, fast, j);
             const SplatRec& e = exact[j];
-            s_conic[threadIdx.x] = make_float4((float)e.c00, (float)e.c01, (float)e.c10, (float)e.c11);
+            s_conic[t] = make_float4((float)e.c00, (float)e.c01, (float)e.c10, (float)e.c11);
         }
-#pragma unroll
-        for (int q = 0; q < kAccStride - 3; ++q) s_acc[threadIdx.x][q] = 0.f;
         __syncthreads();
         for (int k = nb - 1; k >= 0; --k) {
-            float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-            float v8 = 0.f;
-            bool contrib = false;
             const int4 hdr = sb.hdr[k];
-            if (base + k < last && in_box(hdr.x, hdr.y, px, py)) {
-                float x, dx, dy;
-                if (hdr.z) {
-                    x = exact_x(exact + sb.j[k], pcx, pcy);
-                    const float2 d = exact_delta(exact + sb.j[k], pcx, pcy);
-                    dx = d.x;
-                    dy = d.y;
-                } else {
-                    x = fast_x(sb.mean[k], sb.chol[k], pxc, pyc, dx, dy);
-                }
-                const float4 L = sb.chol[k];
-                float g;
-                const float a = pair_alpha(L.w, __int_as_float(hdr.w), x, exact + sb.j[k], pcx, pcy, g);
-                if (a >= 0.0f) {
-                    contrib = true;
-                    const float4 col = sb.col[k];
-                    const float inv = __frcp_rn(1.0f - a);
-                    const float Ti = T * inv;  // transmittance before this splat
-                    const float w = a * Ti;
-                    // d_a = g_pix . (rgb * T_i - S / (1 - a))
-                    const float d_a = gr * fmaf(col.x, Ti, -Sr * inv) + gg * fmaf(col.y, Ti, -Sg * inv) +
-                                      gb * fmaf(col.z, Ti, -Sb * inv);
-                    Sr = fmaf(col.x, w, Sr);
-                    Sg = fmaf(col.y, w, Sg);
-                    Sb = fmaf(col.z, w, Sb);
-                    T = Ti;
-                    v[0] = w * gr;
-                    v[1] = w * gg;
-                    v[2] = w * gb;
-                    v[3] = g * d_a;
-                    const float gdg = g * (L.w * d_a);  // g * d_g, d_g = alpha * d_a
-                    const float4 c = s_conic[k];
-                    v[4] = gdg * fmaf(c.x, dx, c.y * dy);
-                    v[5] = gdg * fmaf(c.z, dx, c.w * dy);
-                    const float hc = -0.5f * gdg;
-                    v[6] = hc * dx * dx;
-                    v[7] = hc * dx * dy;
-                    v8 = hc * dy * dy;
-                }
+            const uint32_t idx = base + k;
+            const bool b0 = idx < s0.last && in_box(hdr.x, hdr.y, px, py0);
+            const bool b1 = idx < s1.last && in_box(hdr.x, hdr.y, px, py1);
+            if (!__any_sync(0xffffffffu, b0 || b1)) continue;
+            float v[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            bool any = false;
+            if (b0 || b1) {
+                const float4 m = sb.mean[k], L = sb.chol[k], col = sb.col[k], cn = s_conic[k];
+                const SplatRec* e = exact + sb.j[k];
+                if (b0) any |= backprop_pair(s0, hdr, m, L, col, cn, e, pxc, pyc0, pcx, pcy0, v);
+                if (b1) any |= backprop_pair(s1, hdr, m, L, col, cn, e, pxc, pyc1, pcx, pcy1, v);
             }
-            if (__any_sync(0xffffffffu, contrib)) {
-                const float r8 = transpose_reduce8(v);
-                const float r9 = warp_sum(v8);
-                const int lane = threadIdx.x & 31;
-                if ((lane & 3) == 0) atomicAdd(&s_acc[k][lane >> 2], r8);
-                if (lane == 1) atomicAdd(&s_acc[k][8], r9);
-            }
+            // lanes without a contributing pixel hold zeros; skip the
+            // reduction when the whole warp is empty
+            if (!__any_sync(0xffffffffu, any)) continue;
+            const float r8 = transpose_reduce8(v);
+            const float r9 = warp_sum(v[8]);
+            float* dst = accum + (size_t)sb.j[k] * kAccStride;
+            if ((lane & 3) == 0) red_add(dst + (lane >> 2), r8);
+            else if (lane == 1) red_add(dst + 8, r9);
         }
-        __syncthreads();
-        if ((int)threadIdx.x < nb) {
-            const float* a = s_acc[threadIdx.x];
-            bool nz = false;
-#pragma unroll
-            for (int q = 0; q < 9; ++q) nz |= a[q] != 0.f;
-            if (nz) {
-                float* dst = accum + (size_t)sb.j[threadIdx.x] * kAccStride;
-                red_add_v4(dst, a[0], a[1], a[2], a[3]);
-                red_add_v4(dst + 4, a[4], a[5], a[6], a[7]);
-                atomicAdd(dst + 8, a[8]);
-            }
-        }
-        __syncthreads();
     }
 }
 

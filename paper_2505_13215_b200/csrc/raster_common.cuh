@@ -29,12 +29,13 @@ constexpr double kLog2eD = 1.4426950408889634;
 struct __align__(16) SplatFast {
     int32_t xr;      // x0 | (x1 - x0) << 16   (inclusive clamped pixel box)
     int32_t yr;      // y0 | (y1 - y0) << 16
-    uint32_t fp64;   // 1: evaluate the exponent in FP64
-    float eps;       // certified relative error bound of the fast alpha
+    float x_skip;    // x >= x_skip: alpha certainly below 1/255 (no exp needed)
+    float eps;       // certified relative error bound of the fast alpha; < 0: FP64 path
     float sx_hi, sy_hi, sx_lo, sy_lo;  // screen mean as double-float
     float l00, l01, l11;               // Cholesky of 0.5*log2(e)*conic: x = |L d|^2 = power*log2(e)
     float alpha_f;
-    float r, g, b, pcut;  // pcut: power above which alpha < 1/255 (tile culling)
+    float r, g, b;
+    float x_keep;    // x < x_keep: alpha certainly >= 1/255; in between: FP64 decision
 };
 static_assert(sizeof(SplatFast) == 64, "SplatFast layout");
 
@@ -77,10 +78,10 @@ __device__ __forceinline__ float fast_exp2_neg(float x) {
 // Shared-memory SoA batch of splats.
 template <int B>
 struct SplatBatch {
-    int4 hdr[B];     // xr, yr, fp64, eps bits
+    int4 hdr[B];     // xr, yr, x_skip bits, eps bits (negative: FP64 path)
     float4 mean[B];  // sx_hi, sy_hi, sx_lo, sy_lo
     float4 chol[B];  // l00, l01, l11, alpha_f
-    float4 col[B];   // r, g, b, -
+    float4 col[B];   // r, g, b, x_keep
     uint32_t j[B];   // sorted splat index (for the exact record)
 
     __device__ __forceinline__ void load(int t, const SplatFast* __restrict__ fast, uint32_t jj) {
@@ -103,18 +104,26 @@ __device__ __forceinline__ float fast_x(const float4 m, const float4 L, float px
     return fmaf(u1, u1, u2 * u2);
 }
 
-// Alpha of a pair, or a negative value when the oracle skips it (a < 1/255);
-// decisions inside the certified guard band are taken in FP64.
-__device__ __forceinline__ float pair_alpha(float alpha_f, float eps, float x, const SplatRec* e, double pcx,
-                                            double pcy, float& g_out) {
+// Alpha of a pair, or a negative value when the oracle skips it (a < 1/255).
+// The cutoff is tested on the exponent argument before any exp: x >= x_skip
+// means a < 1/255 even with the certified error, x < x_keep means a >= 1/255;
+// inside the guard band the decision is taken in FP64 by the oracle's own test.
+__device__ __forceinline__ float pair_alpha(float alpha_f, float x_skip, float x_keep, float x, const SplatRec* e,
+                                            double pcx, double pcy, float& g_out) {
+    if (x >= x_skip) return -1.0f;
+    if (x >= x_keep && !exact_alpha_passes(e, pcx, pcy)) return -1.0f;
     const float g = fast_exp2_neg(x);
-    const float a = alpha_f * g;
     g_out = g;
-    constexpr float kCut = 1.0f / 255.0f;
-    const float band = 1.5f * eps * kCut;
-    if (a < kCut - band) return -1.0f;
-    if (a < kCut + band && !exact_alpha_passes(e, pcx, pcy)) return -1.0f;
-    return a;
+    return alpha_f * g;
+}
+
+// Per-splat thresholds of pair_alpha (computed once in FP64 at gather time):
+// a_f = alpha_f * 2^-x has relative error <= eps against the oracle's alpha;
+// a margin of 2*eps around 1/255 defines the guard band.
+__host__ __device__ inline void cutoff_thresholds(double alpha_f, double eps, float& x_skip, float& x_keep) {
+    const double cut = 1.0 / 255.0;
+    x_skip = (float)(log2(alpha_f / (cut * (1.0 - 2.0 * eps))));
+    x_keep = (float)(log2(alpha_f / (cut * (1.0 + 2.0 * eps))));
 }
 
 }  // namespace hgs

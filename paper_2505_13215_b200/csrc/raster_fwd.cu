@@ -15,10 +15,12 @@ __global__ void __launch_bounds__(256) gather_sorted_kernel(const uint32_t* __re
                                                             const uint32_t* __restrict__ ntiles,
                                                             SplatRec* __restrict__ rec_sorted,
                                                             SplatFast* __restrict__ fast_sorted,
-                                                            uint32_t* __restrict__ ntiles_sorted) {
+                                                            uint32_t* __restrict__ ntiles_sorted,
+                                                            uint32_t* __restrict__ sorted_of_gid) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= V) return;
     const uint32_t gid = sorted_gid[j];
+    sorted_of_gid[gid] = (uint32_t)j;
     const SplatRec e = rec[gid];
     rec_sorted[j] = e;
     ntiles_sorted[j] = ntiles[gid];
@@ -50,15 +52,14 @@ __global__ void __launch_bounds__(256) gather_sorted_kernel(const uint32_t* __re
     f.r = e.r;
     f.g = e.g;
     f.b = e.b;
-    // culling threshold on the power: alpha * exp(-p) >= 1/255  <=>  p <= ln(255 alpha)
-    f.pcut = (float)(log(e.alpha * 255.0) + 1e-5);
     // FP32 path: |x_f - x| <= u*X*(17 + 16r) over the relevant region x <= 8,
     // u = 2^-24 (two extra roundings for the double-float mean); relative
     // alpha error = ln2*|dx| + 2^-22 (ex2.approx) + 2 roundings.
-    f.eps = fp64 ? 1.0e-6f : (float)(8.0e-6 * (1.0 + r) + 4.0e-7);
+    const double eps = fp64 ? 1.0e-6 : 8.0e-6 * (1.0 + r) + 4.0e-7;
+    cutoff_thresholds((double)e.alpha_f, eps, f.x_skip, f.x_keep);
+    f.eps = fp64 ? -(float)eps : (float)eps;  // sign bit selects the FP64 exponent path
     f.xr = (int32_t)e.x0 | ((int32_t)(e.x1 - e.x0) << 16);
     f.yr = (int32_t)e.y0 | ((int32_t)(e.y1 - e.y0) << 16);
-    f.fp64 = fp64 ? 1u : 0u;
     fast_sorted[j] = f;
 }
 
@@ -112,8 +113,10 @@ __global__ void __launch_bounds__(256) duplicate_kernel(const SplatFast* __restr
     const int ty = ty0 + local / w, tx = tx0 + local % w;
     uint32_t v = (uint32_t)j;
     if (cull && !(tx0 == tx1 && ty0 == y1 / kTile)) {
-        const double pcut = (double)__ldg(&fast[j].pcut);
-        if (!tile_may_contribute(exact[j], pcut, max(x0, tx * kTile), min(x1, tx * kTile + kTile - 1),
+        // culling threshold on the power: alpha * exp(-p) >= 1/255  <=>  p <= ln(255 alpha)
+        const SplatRec& e = exact[j];
+        const double pcut = log(e.alpha * 255.0) + 1e-5;
+        if (!tile_may_contribute(e, pcut, max(x0, tx * kTile), min(x1, tx * kTile + kTile - 1),
                                  max(y0, ty * kTile), min(y1, ty * kTile + kTile - 1)))
             v |= 0x80000000u;
     }
@@ -164,17 +167,75 @@ __global__ void __launch_bounds__(256) tile_ranges_dev_kernel(const uint32_t* __
 }
 
 constexpr int kBatch = 256;
+constexpr int kThreads = 128;  // 16x16 tile, two pixels (rows y and y+8) per thread
 
-// K4: one CTA per 16x16 tile, one thread per pixel, front-to-back alpha
-// blending over the tile's depth-ordered list staged through shared memory
-// (SoA, LDS.128 broadcasts) in batches of 256 splats; CTA-wide early exit once
-// every pixel saturated.
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// Per-pixel compositing state of K4.
+struct PixFwd {
+    float T, r, g, b, err;
+    uint32_t last, count;
+    bool done, flagged;
+};
+
+// One pair of raster.cpp:132-143 on the fast path (bounded relative error).
+__device__ __forceinline__ void composite_pair(PixFwd& s, const int4 hdr, const float4 m, const float4 L, const float4 c,
+                                               const SplatRec* e, float pxc, float pyc, double pcx, double pcy,
+                                               uint32_t idx) {
+    ++s.count;
+    float x, dx, dy;
+    const float eps_s = __int_as_float(hdr.w);
+    if (eps_s < 0.0f) x = exact_x(e, pcx, pcy);
+    else x = fast_x(m, L, pxc, pyc, dx, dy);
+    const float eps = fabsf(eps_s);
+    float g;
+    const float a = pair_alpha(L.w, __int_as_float(hdr.z), c.w, x, e, pcx, pcy, g);
+    if (a < 0.0f) return;
+    const float w = a * s.T;
+    s.r = fmaf(c.x, w, s.r);
+    s.g = fmaf(c.y, w, s.g);
+    s.b = fmaf(c.z, w, s.b);
+    const float om = 1.0f - a;
+    s.err = fmaf(a * eps, rcp_approx(om), s.err + 2.5e-7f);
+    s.T *= om;
+    s.last = idx + 1;
+    if (s.T < 1.0e-4f * (1.0f + 2.0f * s.err)) {
+        // inside the certified error band of the oracle's T < 1e-4 decision?
+        if (s.T > 1.0e-4f * (1.0f - 2.0f * s.err)) s.flagged = true;
+        s.done = true;
+    }
+}
+
+__device__ __forceinline__ void write_pixel(const PixFwd& s, int pix, float bg_r, float bg_g, float bg_b,
+                                            float* __restrict__ out_rgb, uint32_t* __restrict__ out_last,
+                                            float* __restrict__ out_tfinal, float* __restrict__ out_trans,
+                                            uint32_t* __restrict__ out_count, uint32_t* __restrict__ fix_list,
+                                            uint32_t* __restrict__ fix_count) {
+    out_rgb[pix * 3 + 0] = fmaf(s.T, bg_r, s.r);
+    out_rgb[pix * 3 + 1] = fmaf(s.T, bg_g, s.g);
+    out_rgb[pix * 3 + 2] = fmaf(s.T, bg_b, s.b);
+    out_last[pix] = s.last | (s.flagged ? 0x80000000u : 0u);
+    out_tfinal[pix] = s.T;
+    if (out_trans) out_trans[pix] = s.T;
+    if (out_count) out_count[pix] = s.count;
+    if (s.flagged) fix_list[atomicAdd(fix_count, 1u)] = (uint32_t)pix;
+}
+
+// K4: one CTA (128 threads) per 16x16 tile, two pixels per thread, front-to-
+// back alpha blending over the tile's depth-ordered list staged through shared
+// memory (SoA, LDS.128 broadcasts) in batches of 256 splats; CTA-wide early
+// exit once every pixel saturated.  Each staged splat is read once for both
+// pixels of a thread.
 //
 // Outputs per pixel: rgb (HWC float), last[pix] = one past the instance index
 // of the last contributor (bit 31 = pixel handed to the FP64 fix-up), the
 // final transmittance (read by the backward) and the optional count /
 // transmittance maps.
-__global__ void __launch_bounds__(256) raster_fwd_kernel(
+__global__ void __launch_bounds__(kThreads) raster_fwd_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ inst_val, const SplatFast* __restrict__ fast,
     const SplatRec* __restrict__ exact, int W, int H, int tiles_x, float bg_r, float bg_g, float bg_b,
     float* __restrict__ out_rgb, uint32_t* __restrict__ out_last, float* __restrict__ out_tfinal,
@@ -184,61 +245,41 @@ __global__ void __launch_bounds__(256) raster_fwd_kernel(
     const int tile = blockIdx.x;
     const int tx = tile % tiles_x, ty = tile / tiles_x;
     const int px = tx * kTile + (threadIdx.x & 15);
-    const int py = ty * kTile + (threadIdx.x >> 4);
-    const bool inside = px < W && py < H;
+    const int py0 = ty * kTile + (threadIdx.x >> 4), py1 = py0 + 8;
+    const bool in0 = px < W && py0 < H, in1 = px < W && py1 < H;
     const uint2 rg = ranges[tile];
-    const float pxc = (float)px + 0.5f, pyc = (float)py + 0.5f;
-    const double pcx = (double)px + 0.5, pcy = (double)py + 0.5;
+    const float pxc = (float)px + 0.5f, pyc0 = (float)py0 + 0.5f, pyc1 = (float)py1 + 0.5f;
+    const double pcx = (double)px + 0.5, pcy0 = (double)py0 + 0.5, pcy1 = (double)py1 + 0.5;
 
-    float T = 1.0f, cr = 0.0f, cg = 0.0f, cb = 0.0f;
-    float err = 0.0f;  // certified relative error bound of T
-    uint32_t last = rg.x, count = 0;
-    bool done = !inside, flagged = false;
+    PixFwd s0{1.0f, 0.f, 0.f, 0.f, 0.f, rg.x, 0u, !in0, false};
+    PixFwd s1{1.0f, 0.f, 0.f, 0.f, 0.f, rg.x, 0u, !in1, false};
 
     for (uint32_t base = rg.x; base < rg.y; base += kBatch) {
-        if (__syncthreads_count(!done) == 0) break;
-        const uint32_t idx = base + threadIdx.x;
-        if (idx < rg.y) sb.load(threadIdx.x, fast, inst_val[idx]);
+        if (__syncthreads_count(!(s0.done && s1.done)) == 0) break;
+        for (int t = threadIdx.x; t < kBatch; t += kThreads) {
+            const uint32_t idx = base + t;
+            if (idx < rg.y) sb.load(t, fast, inst_val[idx]);
+        }
         __syncthreads();
         const int nb = min((uint32_t)kBatch, rg.y - base);
-        for (int k = 0; k < nb && !done; ++k) {
+        for (int k = 0; k < nb; ++k) {
+            if (s0.done && s1.done) break;
             const int4 hdr = sb.hdr[k];
-            if (!in_box(hdr.x, hdr.y, px, py)) continue;
-            ++count;
-            float x, dx, dy;
-            if (hdr.z) x = exact_x(exact + sb.j[k], pcx, pcy);
-            else x = fast_x(sb.mean[k], sb.chol[k], pxc, pyc, dx, dy);
-            const float4 L = sb.chol[k];
-            const float eps = __int_as_float(hdr.w);
-            float g;
-            const float a = pair_alpha(L.w, eps, x, exact + sb.j[k], pcx, pcy, g);
-            if (a < 0.0f) continue;
-            const float4 c = sb.col[k];
-            const float w = a * T;
-            cr = fmaf(c.x, w, cr);
-            cg = fmaf(c.y, w, cg);
-            cb = fmaf(c.z, w, cb);
-            const float om = 1.0f - a;
-            err += __fdividef(a * eps, om) + 2.5e-7f;
-            T *= om;
-            last = base + k + 1;
-            if (T < 1.0e-4f * (1.0f + 2.0f * err)) {
-                // inside the error band of the oracle's T < 1e-4 decision?
-                if (T > 1.0e-4f * (1.0f - 2.0f * err)) flagged = true;
-                done = true;
-            }
+            const bool b0 = !s0.done && in_box(hdr.x, hdr.y, px, py0);
+            const bool b1 = !s1.done && in_box(hdr.x, hdr.y, px, py1);
+            if (!(b0 || b1)) continue;
+            const float4 m = sb.mean[k], L = sb.chol[k], c = sb.col[k];
+            const SplatRec* e = exact + sb.j[k];
+            if (b0) composite_pair(s0, hdr, m, L, c, e, pxc, pyc0, pcx, pcy0, base + k);
+            if (b1) composite_pair(s1, hdr, m, L, c, e, pxc, pyc1, pcx, pcy1, base + k);
         }
     }
-    if (!inside) return;
-    const int pix = py * W + px;
-    out_rgb[pix * 3 + 0] = fmaf(T, bg_r, cr);
-    out_rgb[pix * 3 + 1] = fmaf(T, bg_g, cg);
-    out_rgb[pix * 3 + 2] = fmaf(T, bg_b, cb);
-    out_last[pix] = last | (flagged ? 0x80000000u : 0u);
-    out_tfinal[pix] = T;
-    if (out_trans) out_trans[pix] = T;
-    if (out_count) out_count[pix] = count;
-    if (flagged) fix_list[atomicAdd(fix_count, 1u)] = (uint32_t)pix;
+    if (in0)
+        write_pixel(s0, py0 * W + px, bg_r, bg_g, bg_b, out_rgb, out_last, out_tfinal, out_trans, out_count, fix_list,
+                    fix_count);
+    if (in1)
+        write_pixel(s1, py1 * W + px, bg_r, bg_g, bg_b, out_rgb, out_last, out_tfinal, out_trans, out_count, fix_list,
+                    fix_count);
 }
 
 // Exact FP64 recomposite of the flagged pixels (raster.cpp:123-148), one warp

@@ -102,7 +102,7 @@ hgs_status run_backward(hgs_ctx* ctx, const float* lg, double scale) {
     const int n_tiles = ctx->tiles_x * ctx->tiles_y;
     const uint32_t* fix_count = &ctx->counters.as<Counters>()->fix_count;
     prof_begin(ctx, PH_RASTER_BWD);
-    raster_bwd_kernel<<<n_tiles, 256, 0, st>>>(ctx->ranges.as<uint2>(), ctx->inst_vals_final,
+    raster_bwd_kernel<<<n_tiles, 128, 0, st>>>(ctx->ranges.as<uint2>(), ctx->inst_vals_final,
                                                ctx->fast_sorted.as<SplatFast>(), ctx->rec_sorted.as<SplatRec>(),
                                                ctx->W, ctx->H, ctx->tiles_x, ctx->tfinal.as<float>(),
                                                ctx->last.as<uint32_t>(), lg, (float)ctx->bg[0], (float)ctx->bg[1],
@@ -117,8 +117,9 @@ hgs_status run_backward(hgs_ctx* ctx, const float* lg, double scale) {
     CKL();
     prof_end(ctx);
     prof_begin(ctx, PH_GAUSS_BWD);
-    gaussian_bwd_kernel<<<div_up((uint32_t)V, 128), 128, 0, st>>>(
-        (int)V, ctx->sorted_gid, ctx->accum.as<float>(), kAccStrideHost, (int)ctx->n4, ctx->p4.as<float>(), ctx->cap4,
+    const int N = (int)(ctx->n4 + ctx->n3);
+    gaussian_bwd_kernel<<<div_up((uint32_t)N, 128), 128, 0, st>>>(
+        N, ctx->sorted_of_gid.as<uint32_t>(), ctx->accum.as<float>(), kAccStrideHost, (int)ctx->n4, ctx->p4.as<float>(), ctx->cap4,
         ctx->p3.as<float>(), ctx->cap3, ctx->deg, ctx->cam, ctx->t, scale, ctx->g4, ctx->g3, ctx->sn4.as<float>(),
         ctx->sn3.as<float>(), ctx->dgn4, ctx->dgn3, ctx->dcnt4, ctx->dcnt3, &ctx->rec_sorted.as<SplatRec>()->c00,
         (int)(sizeof(SplatRec) / sizeof(double)));
