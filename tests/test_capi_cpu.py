@@ -50,3 +50,26 @@ def test_product_does_not_reference_oracle():
                 txt = open(os.path.join(dirpath, f), errors="ignore").read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
                 assert "hgs_oracle" not in txt and "libhgs_oracle" not in txt, f
+
+
+def _build_demo(tmp_path):
+    import subprocess
+
+    exe = str(tmp_path / "render_demo")
+    lib = os.path.join(ROOT, "paper_2505_13215_b200")
+    subprocess.check_call(["g++", "-std=c++17", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+                           os.path.join(ROOT, "examples", "render_demo.cpp"), "-L", lib, "-lhgs_gpu",
+                           f"-Wl,-rpath,{lib}", "-o", exe])
+    return exe
+
+
+def test_cpp_consumer_compiles_and_fails_loudly(tmp_path):
+    """A plain C++ program links against the C ABI; without a device it exits 2."""
+    import subprocess
+
+    import torch
+
+    exe = _build_demo(tmp_path)
+    if torch.cuda.is_available():
+        pytest.skip("GPU present: covered by tests/test_gpu_render.py::test_cpp_consumer_runs")
+    assert subprocess.run([exe], capture_output=True).returncode == 2

@@ -160,3 +160,21 @@ def test_render_deterministic(ctx):
     a = ctx.render(cam, 0.5)["rgb"]
     b = ctx.render(cam, 0.5)["rgb"]
     assert (a == b).all()
+
+
+def test_cpp_consumer_runs(tmp_path):
+    """examples/render_demo.cpp through the C ABI: the single-splat closed form."""
+    import subprocess
+
+    from tests.test_capi_cpu import _build_demo
+
+    out = subprocess.run([_build_demo(tmp_path)], capture_output=True, text=True, check=True).stdout
+    assert "projected=1" in out
+    vals = [float(v) for v in out.split("centre=(")[1].rstrip(")\n").split(",")]
+    cov = O.build_cov3(np.eye(3), [math.log(0.3)] * 3)
+    cam = O.look_at([0, 0, -3], [0, 0, 0], [0, -1, 0], 40.0, 33, 33)
+    s = O.project_3d([0, 0, 0], cov, cam)
+    d = np.array([16.5, 16.5]) - np.array([s["sx"], s["sy"]])
+    alpha = 0.7 * math.exp(-0.5 * d @ (np.array(s["conic"]).reshape(2, 2) @ d))
+    for c, (rgb, bgc) in enumerate(zip((0.9, 0.1, 0.3), (0.0, 0.0, 1.0))):
+        assert vals[c] == pytest.approx(rgb * alpha + bgc * (1 - alpha), abs=1e-6)
