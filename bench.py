@@ -328,7 +328,7 @@ def run_reference(args) -> None:
     scene, target, cams, times, desc = workload(args.config)
     cores = O.hardware_threads()
     B = max(1, min(cores, 8))
-    full_step_s = 14.0  # measured order of one full-view iteration per thread
+    full_step_s = 30.0  # measured: B=8 concurrent full-view iterations, one thread each (8-core host)
     frac = float(np.clip(150.0 / ((args.steps + args.warmup) * full_step_s), 0.1, 1.0))
     H, W = cams[0].height, cams[0].width
     hb = max(16, int(round(H * frac)))

@@ -181,6 +181,9 @@ class Context:
                 out["rgb"].ctypes.data_as(_capi._fp), V, C.byref(n)))
         return out
 
+    def debug_keep_instances(self, enable: bool = True) -> None:
+        self._check(self._lib.hgs_debug_keep_instances(self._h, int(enable)))
+
     def debug_instances(self) -> tuple[np.ndarray, np.ndarray]:
         n = C.c_int64()
         self._check(self._lib.hgs_debug_instances(self._h, None, None, 0, C.byref(n)))

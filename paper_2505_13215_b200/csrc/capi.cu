@@ -380,33 +380,54 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
         while ((1 << bits) < n_tiles) ++bits;
         const int end_bit = ((bits + 7) / 8) * 8;
         CK(ctx->sort_ws.ensure(radix_workspace_bytes((int)I) + 4096));
-        int which = radix_sort_pairs(ctx->inst_k.as<uint32_t>(), ctx->inst_v.as<uint32_t>(), ctx->inst_k2.as<uint32_t>(),
+        ctx->inst_keys_all = ctx->inst_vals_all = nullptr;
+        if (ctx->debug_full_list || !cull) {
+            // the reference's complete instance list (raster.cpp:180-212): kept for
+            // count_map and for the bit-exact parity check (hgs_debug_instances)
+            CK(ctx->dbg_k.ensure((size_t)I * 4));
+            CK(ctx->dbg_v.ensure((size_t)I * 4));
+            CK(cudaMemcpyAsync(ctx->dbg_k.p, ctx->inst_k.p, (size_t)I * 4, cudaMemcpyDeviceToDevice, st));
+            CK(cudaMemcpyAsync(ctx->dbg_v.p, ctx->inst_v.p, (size_t)I * 4, cudaMemcpyDeviceToDevice, st));
+            int w = radix_sort_pairs(ctx->dbg_k.as<uint32_t>(), ctx->dbg_v.as<uint32_t>(), ctx->inst_k2.as<uint32_t>(),
                                      ctx->inst_v2.as<uint32_t>(), (int)I, 0, end_bit, ctx->sort_ws.as<uint32_t>(), st);
-        CKL();
-        uint32_t* keys = which ? ctx->inst_k2.as<uint32_t>() : ctx->inst_k.as<uint32_t>();
-        inst_vals = which ? ctx->inst_v2.as<uint32_t>() : ctx->inst_v.as<uint32_t>();
-        ctx->inst_keys_all = keys;
-        ctx->inst_vals_all = inst_vals;
+            CKL();
+            if (w) {
+                CK(cudaMemcpyAsync(ctx->dbg_k.p, ctx->inst_k2.p, (size_t)I * 4, cudaMemcpyDeviceToDevice, st));
+                CK(cudaMemcpyAsync(ctx->dbg_v.p, ctx->inst_v2.p, (size_t)I * 4, cudaMemcpyDeviceToDevice, st));
+            }
+            ctx->inst_keys_all = ctx->dbg_k.as<uint32_t>();
+            ctx->inst_vals_all = ctx->dbg_v.as<uint32_t>();
+        }
+        uint32_t* keys;
         if (cull) {
-            // stable compaction of the instances that can reach the alpha cutoff in their tile
-            uint32_t* kk = which ? ctx->inst_k.as<uint32_t>() : ctx->inst_k2.as<uint32_t>();
-            uint32_t* vv = which ? ctx->inst_v.as<uint32_t>() : ctx->inst_v2.as<uint32_t>();
+            // Exact culling first (order-preserving compaction of the depth-ordered
+            // instances that can reach the alpha cutoff in their tile), then the
+            // stable tile sort of the kept instances only: same relative order as
+            // filtering the reference's sorted list, at a third of the sort cost.
             CK(ctx->inst_flag.ensure((size_t)I * 4));
             CK(ctx->inst_pos.ensure((size_t)I * 4));
             CK(ctx->scan_ws.ensure(scan_workspace_bytes((int)I) + 4096));
-            keep_flag_kernel<<<div_up((uint32_t)I, 256), 256, 0, st>>>(inst_vals, (int)I, ctx->inst_flag.as<uint32_t>());
+            keep_flag_kernel<<<div_up((uint32_t)I, 256), 256, 0, st>>>(ctx->inst_v.as<uint32_t>(), (int)I,
+                                                                      ctx->inst_flag.as<uint32_t>());
             count_launch();
             exclusive_scan_u32(ctx->inst_flag.as<uint32_t>(), ctx->inst_pos.as<uint32_t>(), (int)I, &dc->I_kept,
                                ctx->scan_ws.as<uint32_t>(), st);
-            compact_instances_kernel<<<div_up((uint32_t)I, 256), 256, 0, st>>>(keys, inst_vals, (int)I,
-                                                                            ctx->inst_pos.as<uint32_t>(), kk, vv);
+            compact_instances_kernel<<<div_up((uint32_t)I, 256), 256, 0, st>>>(
+                ctx->inst_k.as<uint32_t>(), ctx->inst_v.as<uint32_t>(), (int)I, ctx->inst_pos.as<uint32_t>(),
+                ctx->inst_k2.as<uint32_t>(), ctx->inst_v2.as<uint32_t>());
             count_launch();
             CKL();
-            keys = kk;
-            inst_vals = vv;
+            int which = radix_sort_pairs(ctx->inst_k2.as<uint32_t>(), ctx->inst_v2.as<uint32_t>(),
+                                         ctx->inst_k.as<uint32_t>(), ctx->inst_v.as<uint32_t>(), (int)I, 0, end_bit,
+                                         ctx->sort_ws.as<uint32_t>(), st, &dc->I_kept);
+            CKL();
+            keys = which ? ctx->inst_k.as<uint32_t>() : ctx->inst_k2.as<uint32_t>();
+            inst_vals = which ? ctx->inst_v.as<uint32_t>() : ctx->inst_v2.as<uint32_t>();
             tile_ranges_dev_kernel<<<div_up((uint32_t)I, 256), 256, 0, st>>>(keys, &dc->I_kept, ctx->ranges.as<uint2>());
             count_launch();
         } else {
+            keys = ctx->inst_keys_all;
+            inst_vals = ctx->inst_vals_all;
             tile_ranges_kernel<<<div_up((uint32_t)I, 256), 256, 0, st>>>(keys, (int)I, ctx->ranges.as<uint2>());
             count_launch();
         }
@@ -502,7 +523,7 @@ void hgs_ctx_destroy(hgs_ctx* ctx) {
                     &ctx->gn3, &ctx->cnt4, &ctx->cnt3, &ctx->sn4, &ctx->sn3, &ctx->rec, &ctx->depth_key,
                     &ctx->ntiles, &ctx->visflag, &ctx->vispos, &ctx->sort_k, &ctx->sort_v, &ctx->sort_k2,
                     &ctx->sort_v2, &ctx->rec_sorted, &ctx->fast_sorted, &ctx->ntiles_sorted, &ctx->inst_off,
-                    &ctx->inst_k, &ctx->inst_v, &ctx->inst_k2, &ctx->inst_v2, &ctx->ranges, &ctx->sorted_of_gid, &ctx->inst_flag, &ctx->inst_pos, &ctx->scan_ws,
+                    &ctx->inst_k, &ctx->inst_v, &ctx->inst_k2, &ctx->inst_v2, &ctx->ranges, &ctx->sorted_of_gid, &ctx->inst_flag, &ctx->inst_pos, &ctx->dbg_k, &ctx->dbg_v, &ctx->scan_ws,
                     &ctx->sort_ws, &ctx->counters, &ctx->img, &ctx->last, &ctx->tfinal, &ctx->trans, &ctx->count,
                     &ctx->fix_list, &ctx->accum, &ctx->lgrad, &ctx->gt_stage, &ctx->loss_ws, &ctx->stage};
     for (DBuf* b : bufs) b->release();
@@ -697,12 +718,22 @@ hgs_status hgs_debug_splats(hgs_ctx* ctx, int32_t* gid, uint32_t* depth_bits, in
     return HGS_OK;
 }
 
-// Tile-sorted instances: tile id and gid of each, in render order.
+// Keep the reference's complete tile-sorted instance list on subsequent
+// renders (an extra sort of every instance; parity tests only).
+hgs_status hgs_debug_keep_instances(hgs_ctx* ctx, int enable) {
+    if (!ctx) return HGS_ERR_INVALID_ARGUMENT;
+    ctx->debug_full_list = enable != 0;
+    return HGS_OK;
+}
+
+// Tile-sorted instances: tile id and gid of each, in reference order.
 hgs_status hgs_debug_instances(hgs_ctx* ctx, uint32_t* tile, uint32_t* gid, int64_t cap, int64_t* n_out) {
     if (!ctx || !ctx->have_tape) return fail(ctx, HGS_ERR_STATE, "no render to inspect");
     const int64_t I = ctx->I, V = ctx->V;
     *n_out = I;
     if (I > cap || I == 0) return HGS_OK;
+    if (!ctx->inst_vals_all)
+        return fail(ctx, HGS_ERR_STATE, "full instance list not kept: call hgs_debug_keep_instances(ctx, 1) first");
     std::vector<uint32_t> vals(I), sg(V);
     CK(cudaMemcpy(vals.data(), ctx->inst_vals_all, I * 4, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(sg.data(), ctx->sorted_gid, V * 4, cudaMemcpyDeviceToHost));

@@ -104,6 +104,8 @@ struct hgs_ctx {
     hgs::DBuf rec_sorted, fast_sorted, ntiles_sorted, inst_off, sorted_of_gid;
     hgs::DBuf inst_k, inst_v, inst_k2, inst_v2;       // tile sort (I)
     hgs::DBuf ranges, scan_ws, sort_ws, inst_flag, inst_pos;
+    hgs::DBuf dbg_k, dbg_v;         // the reference's full sorted instance list (debug / count_map)
+    bool debug_full_list = false;   // hgs_debug_keep_instances
     hgs::DBuf counters;  // [0..5] stats u64, [6] flags, fix_count, totals...
     hgs::DBuf img, last, tfinal, trans, count, fix_list;
     hgs::DBuf accum;     // backward per-sorted-splat accumulators

@@ -18,7 +18,7 @@ namespace hgs {
 namespace {
 
 constexpr int kScanThreads = 256;
-constexpr int kScanItems = 8;
+constexpr int kScanItems = 16;
 constexpr int kScanTile = kScanThreads * kScanItems;  // 2048
 
 __device__ inline uint32_t warp_incl_scan(uint32_t v) {
@@ -118,10 +118,12 @@ constexpr int kSortWarps = kSortThreads / 32;
 
 __global__ void __launch_bounds__(kSortThreads) radix_hist_kernel(const uint32_t* __restrict__ keys, int n,
                                                                   int shift, int nblocks,
-                                                                  uint32_t* __restrict__ hist) {
+                                                                  uint32_t* __restrict__ hist,
+                                                                  const uint32_t* __restrict__ n_dev) {
     __shared__ uint32_t h[256];
     h[threadIdx.x] = 0;
     __syncthreads();
+    if (n_dev) n = (int)*n_dev;
     const int base = blockIdx.x * kSortTile;
 #pragma unroll 4
     for (int k = 0; k < kSortItems; ++k) {
@@ -134,10 +136,13 @@ __global__ void __launch_bounds__(kSortThreads) radix_hist_kernel(const uint32_t
 
 __global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(
     const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals, uint32_t* __restrict__ keys_out,
-    uint32_t* __restrict__ vals_out, int n, int shift, int nblocks, const uint32_t* __restrict__ offsets) {
+    uint32_t* __restrict__ vals_out, int n, int shift, int nblocks, const uint32_t* __restrict__ offsets,
+    const uint32_t* __restrict__ n_dev) {
     __shared__ uint32_t cnt[kSortWarps][256];
     __shared__ uint32_t goff[256];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (n_dev) n = (int)*n_dev;
+    if ((int)(blockIdx.x * kSortTile) >= n) return;  // whole block beyond the device-side count
     for (int i = threadIdx.x; i < kSortWarps * 256; i += kSortThreads) (&cnt[0][0])[i] = 0u;
     goff[threadIdx.x] = offsets[threadIdx.x * nblocks + blockIdx.x];
     __syncthreads();
@@ -194,6 +199,12 @@ void exclusive_scan_u32(const uint32_t* in, uint32_t* out, int n, uint32_t* tota
         if (total) cudaMemsetAsync(total, 0, sizeof(uint32_t), st);
         return;
     }
+    if (n <= 1024 * kScanItems) {  // one CTA: a single launch
+        if (in != out) cudaMemcpyAsync(out, in, (size_t)n * 4, cudaMemcpyDeviceToDevice, st);
+        scan_single_kernel<<<1, 1024, 0, st>>>(out, n, total);
+        count_launch();
+        return;
+    }
     const int nb = (int)div_up((uint32_t)n, kScanTile);
     if (nb > 1024 * kScanItems) {
         fprintf(stderr, "exclusive_scan_u32: n=%d exceeds the single-level capacity\n", n);
@@ -217,8 +228,9 @@ size_t radix_workspace_bytes(int n) {
 // lands in (keys, vals) when the pass count is even, else in (keys_alt,
 // vals_alt); the return value says which (0 = original buffers).
 int radix_sort_pairs(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt, int n,
-                     int begin_bit, int end_bit, uint32_t* ws, cudaStream_t st) {
-    if (n <= 1) return 0;
+                     int begin_bit, int end_bit, uint32_t* ws, cudaStream_t st, const uint32_t* n_dev) {
+    if (n <= 1 && !n_dev) return 0;
+    if (n < 1) return 0;
     const int nb = (int)div_up((uint32_t)n, kSortTile);
     const int hist_n = 256 * nb;
     uint32_t* hist = ws;
@@ -230,10 +242,10 @@ int radix_sort_pairs(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_
     uint32_t* kout = keys_alt;
     uint32_t* vout = vals_alt;
     for (int shift = begin_bit; shift < end_bit; shift += 8) {
-        radix_hist_kernel<<<nb, kSortThreads, 0, st>>>(kin, n, shift, nb, hist);
+        radix_hist_kernel<<<nb, kSortThreads, 0, st>>>(kin, n, shift, nb, hist, n_dev);
         count_launch();
         exclusive_scan_u32(hist, offs, hist_n, nullptr, scan_ws, st);
-        radix_scatter_kernel<<<nb, kSortThreads, 0, st>>>(kin, vin, kout, vout, n, shift, nb, offs);
+        radix_scatter_kernel<<<nb, kSortThreads, 0, st>>>(kin, vin, kout, vout, n, shift, nb, offs, n_dev);
         count_launch();
         uint32_t* t = kin;
         kin = kout;

@@ -24,6 +24,7 @@ def ctx():
     from paper_2505_13215_b200.api import Context
 
     c = Context(0)
+    c.debug_keep_instances(True)  # keep the reference's full instance list for the parity check
     yield c
     c.close()
 
