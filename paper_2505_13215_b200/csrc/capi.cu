@@ -738,7 +738,7 @@ hgs_status hgs_debug_instances(hgs_ctx* ctx, uint32_t* tile, uint32_t* gid, int6
     CK(cudaMemcpy(vals.data(), ctx->inst_vals_all, I * 4, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(sg.data(), ctx->sorted_gid, V * 4, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(tile, ctx->inst_keys_all, I * 4, cudaMemcpyDeviceToHost));
-    for (int64_t i = 0; i < I; ++i) gid[i] = sg[vals[i] & 0x7fffffffu];
+    for (int64_t i = 0; i < I; ++i) gid[i] = sg[vals[i] & hgs::kInstIndexMask];
     return HGS_OK;
 }
 

@@ -27,59 +27,6 @@ __device__ inline void isoR(const double q[4], double R[4][4]) {
         for (int j = 0; j < 4; ++j) R[i][j] = m[i][j];
 }
 
-__device__ inline void sh_basis_d(const double d[3], int deg, double out[16]) {
-    const double x = d[0], y = d[1], z = d[2];
-    out[0] = 0.28209479177387814;
-    if (deg < 1) return;
-    out[1] = -0.4886025119029199 * y;
-    out[2] = 0.4886025119029199 * z;
-    out[3] = -0.4886025119029199 * x;
-    if (deg < 2) return;
-    const double xx = x * x, yy = y * y, zz = z * z;
-    out[4] = 1.0925484305920792 * x * y;
-    out[5] = -1.0925484305920792 * y * z;
-    out[6] = 0.31539156525252005 * (2.0 * zz - xx - yy);
-    out[7] = -1.0925484305920792 * x * z;
-    out[8] = 0.5462742152960396 * (xx - yy);
-    if (deg < 3) return;
-    out[9] = -0.5900435899266435 * y * (3.0 * xx - yy);
-    out[10] = 2.890611442640554 * x * y * z;
-    out[11] = -0.4570457994644658 * y * (4.0 * zz - xx - yy);
-    out[12] = 0.3731763325901154 * z * (2.0 * zz - 3.0 * xx - 3.0 * yy);
-    out[13] = -0.4570457994644658 * x * (4.0 * zz - xx - yy);
-    out[14] = 1.445305721320277 * z * (xx - yy);
-    out[15] = -0.5900435899266435 * x * (xx - 3.0 * yy);
-}
-
-// sh.cpp:49-71: d Y_k / d dir
-__device__ inline void sh_basis_grad_d(const double d[3], int deg, double g[16][3]) {
-    const double x = d[0], y = d[1], z = d[2];
-    for (int k = 0; k < 16; ++k) g[k][0] = g[k][1] = g[k][2] = 0.0;
-    if (deg < 1) return;
-    const double C1 = 0.4886025119029199;
-    g[1][1] = -C1;
-    g[2][2] = C1;
-    g[3][0] = -C1;
-    if (deg < 2) return;
-    const double xx = x * x, yy = y * y, zz = z * z;
-    const double A = 1.0925484305920792, B = 0.31539156525252005, Cc = 0.5462742152960396;
-    g[4][0] = A * y; g[4][1] = A * x;
-    g[5][1] = -A * z; g[5][2] = -A * y;
-    g[6][0] = B * (-2.0 * x); g[6][1] = B * (-2.0 * y); g[6][2] = B * (4.0 * z);
-    g[7][0] = -A * z; g[7][2] = -A * x;
-    g[8][0] = Cc * (2.0 * x); g[8][1] = Cc * (-2.0 * y);
-    if (deg < 3) return;
-    const double D0 = -0.5900435899266435, D1 = 2.890611442640554, D2 = -0.4570457994644658,
-                 D3 = 0.3731763325901154, D5 = 1.445305721320277;
-    g[9][0] = D0 * (6.0 * x * y); g[9][1] = D0 * (3.0 * xx - 3.0 * yy);
-    g[10][0] = D1 * (y * z); g[10][1] = D1 * (x * z); g[10][2] = D1 * (x * y);
-    g[11][0] = D2 * (-2.0 * x * y); g[11][1] = D2 * (4.0 * zz - xx - 3.0 * yy); g[11][2] = D2 * (8.0 * y * z);
-    g[12][0] = D3 * (-6.0 * x * z); g[12][1] = D3 * (-6.0 * y * z); g[12][2] = D3 * (6.0 * zz - 3.0 * xx - 3.0 * yy);
-    g[13][0] = D2 * (4.0 * zz - 3.0 * xx - yy); g[13][1] = D2 * (-2.0 * x * y); g[13][2] = D2 * (8.0 * x * z);
-    g[14][0] = D5 * (2.0 * x * z); g[14][1] = D5 * (-2.0 * y * z); g[14][2] = D5 * (xx - yy);
-    g[15][0] = D0 * (3.0 * xx - 3.0 * yy); g[15][1] = D0 * (-6.0 * x * y);
-}
-
 __device__ inline double sigmoid(double x) { return 1.0 / (1.0 + exp(-x)); }
 
 // sh.cpp:25-47 in FP32

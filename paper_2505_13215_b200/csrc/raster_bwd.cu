@@ -135,8 +135,10 @@ __global__ void __launch_bounds__(kThreadsB) raster_bwd_kernel(
     __shared__ uint32_t s_maxlast;
     const int tile = blockIdx.x;
     const int tx = tile % tiles_x, ty = tile / tiles_x;
-    const int px = tx * kTile + (threadIdx.x & 15);
-    const int py0 = ty * kTile + (threadIdx.x >> 4), py1 = py0 + 8;
+    // warp w owns the 8x8 quadrant (w & 1, w >> 1); a lane owns rows y, y+4
+    const int warp = threadIdx.x >> 5;
+    const int px = tx * kTile + (warp & 1) * 8 + (threadIdx.x & 7);
+    const int py0 = ty * kTile + (warp >> 1) * 8 + ((threadIdx.x & 31) >> 3), py1 = py0 + 4;
     const uint2 rg = ranges[tile];
     const float pxc = (float)px + 0.5f, pyc0 = (float)py0 + 0.5f, pyc1 = (float)py1 + 0.5f;
     const double pcx = (double)px + 0.5, pcy0 = (double)py0 + 0.5, pcy1 = (double)py1 + 0.5;
@@ -166,6 +168,7 @@ __global__ void __launch_bounds__(kThreadsB) raster_bwd_kernel(
     __syncthreads();
     const uint32_t end = s_maxlast;
     const int lane = threadIdx.x & 31;
+    const uint32_t warp_end = __reduce_max_sync(0xffffffffu, ml);  // nothing past it in this warp
 
     const int nbatch = (int)((end - rg.x + kBatchB - 1) / kBatchB);
     for (int bi = nbatch - 1; bi >= 0; --bi) {
@@ -173,13 +176,15 @@ __global__ void __launch_bounds__(kThreadsB) raster_bwd_kernel(
         const int nb = (int)min((uint32_t)kBatchB, end - base);
         __syncthreads();
         for (int t = threadIdx.x; t < nb; t += kThreadsB) {
-            const uint32_t j = inst_val[base + t];
-            sb.load(t, fast, j);
-            const SplatRec& e = exact[j];
+            const uint32_t v = inst_val[base + t];
+            sb.load(t, fast, v);
+            const SplatRec& e = exact[v & kInstIndexMask];
             s_conic[t] = make_float4((float)e.c00, (float)e.c01, (float)e.c10, (float)e.c11);
         }
         __syncthreads();
-        for (int k = nb - 1; k >= 0; --k) {
+        const int kmax = (int)min((uint32_t)nb, warp_end > base ? warp_end - base : 0u);
+        for (int k = kmax - 1; k >= 0; --k) {
+            if (!((sb.qm[k] >> warp) & 1u)) continue;  // exact: no pixel of this quadrant reaches 1/255
             const int4 hdr = sb.hdr[k];
             const uint32_t idx = base + k;
             const bool b0 = idx < s0.last && in_box(hdr.x, hdr.y, px, py0);
@@ -237,7 +242,7 @@ __global__ void __launch_bounds__(128) raster_bwd_exact_kernel(
                 double rgb[3] = {0.0, 0.0, 0.0};
                 const SplatRec* e = nullptr;
                 if (i < last) {
-                    e = &exact[inst_val[i]];
+                    e = &exact[inst_val[i] & kInstIndexMask];
                     if (px >= e->x0 && px <= e->x1 && py >= e->y0 && py <= e->y1) {
                         g = exp(-exact_power(*e, pcx, pcy));
                         a = __dmul_rn(e->alpha, g);
@@ -265,7 +270,7 @@ __global__ void __launch_bounds__(128) raster_bwd_exact_kernel(
                 if (pass == 1 && mine) {
                     double d_a = 0.0;
                     for (int c = 0; c < 3; ++c) d_a += gp[c] * (rgb[c] * myT - (Cout[c] - myP[c]) / (1.0 - a));
-                    float* dst = accum + (size_t)inst_val[i] * kAccStride;
+                    float* dst = accum + (size_t)(inst_val[i] & kInstIndexMask) * kAccStride;
                     const double w = a * myT;
                     for (int c = 0; c < 3; ++c) atomicAdd(dst + c, (float)(w * gp[c]));
                     atomicAdd(dst + 3, (float)(g * d_a));

@@ -39,6 +39,10 @@ struct __align__(16) SplatFast {
 };
 static_assert(sizeof(SplatFast) == 64, "SplatFast layout");
 
+// Instance value = sorted splat index | (8x8-quadrant contribution mask << 28).
+constexpr int kInstMaskShift = 28;
+constexpr uint32_t kInstIndexMask = (1u << kInstMaskShift) - 1u;
+
 __device__ __forceinline__ int box_x0(int32_t r) { return r & 0xffff; }
 __device__ __forceinline__ int box_w(int32_t r) { return r >> 16; }
 __device__ __forceinline__ bool in_box(int32_t xr, int32_t yr, int px, int py) {
@@ -83,8 +87,11 @@ struct SplatBatch {
     float4 chol[B];  // l00, l01, l11, alpha_f
     float4 col[B];   // r, g, b, x_keep
     uint32_t j[B];   // sorted splat index (for the exact record)
+    uint32_t qm[B];  // 8x8-quadrant contribution mask of this tile instance
 
-    __device__ __forceinline__ void load(int t, const SplatFast* __restrict__ fast, uint32_t jj) {
+    __device__ __forceinline__ void load(int t, const SplatFast* __restrict__ fast, uint32_t v) {
+        const uint32_t jj = v & kInstIndexMask;
+        qm[t] = v >> kInstMaskShift;
         const float4* src = reinterpret_cast<const float4*>(fast + jj);
         const float4 a = __ldg(src + 0), b = __ldg(src + 1), c = __ldg(src + 2), d = __ldg(src + 3);
         hdr[t] = make_int4(__float_as_int(a.x), __float_as_int(a.y), __float_as_int(a.z), __float_as_int(a.w));

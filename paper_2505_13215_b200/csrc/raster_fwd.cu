@@ -111,23 +111,30 @@ __global__ void __launch_bounds__(256) duplicate_kernel(const SplatFast* __restr
     const int local = i - (int)__ldg(&offsets[j]);
     const int w = tx1 - tx0 + 1;
     const int ty = ty0 + local / w, tx = tx0 + local % w;
-    uint32_t v = (uint32_t)j;
-    if (cull && !(tx0 == tx1 && ty0 == y1 / kTile)) {
+    // one bit per 8x8 quadrant of the tile (bit q = qy*2 + qx): can the splat
+    // reach the cutoff at a pixel of quadrant q inside its box?  Each quadrant
+    // is one warp of the rasterizers, so the test is warp-uniform there.
+    uint32_t mask = 0xfu;
+    if (cull) {
         // culling threshold on the power: alpha * exp(-p) >= 1/255  <=>  p <= ln(255 alpha)
         const SplatRec& e = exact[j];
         const double pcut = log(e.alpha * 255.0) + 1e-5;
-        if (!tile_may_contribute(e, pcut, max(x0, tx * kTile), min(x1, tx * kTile + kTile - 1),
-                                 max(y0, ty * kTile), min(y1, ty * kTile + kTile - 1)))
-            v |= 0x80000000u;
+        mask = 0u;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int qx0 = tx * kTile + (q & 1) * 8, qy0 = ty * kTile + (q >> 1) * 8;
+            const int xa = max(x0, qx0), xb = min(x1, qx0 + 7), ya = max(y0, qy0), yb = min(y1, qy0 + 7);
+            if (xa <= xb && ya <= yb && tile_may_contribute(e, pcut, xa, xb, ya, yb)) mask |= 1u << q;
+        }
     }
     keys[i] = (uint32_t)(ty * tiles_x + tx);
-    vals[i] = v;
+    vals[i] = (uint32_t)j | (mask << kInstMaskShift);
 }
 
 __global__ void __launch_bounds__(256) keep_flag_kernel(const uint32_t* __restrict__ vals, int n,
                                                         uint32_t* __restrict__ flag) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) flag[i] = (vals[i] >> 31) ? 0u : 1u;
+    if (i < n) flag[i] = (vals[i] >> kInstMaskShift) ? 1u : 0u;
 }
 
 // Stable compaction of the tile-sorted instances that can contribute.
@@ -139,7 +146,7 @@ __global__ void __launch_bounds__(256) compact_instances_kernel(const uint32_t* 
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint32_t v = vals[i];
-    if (v >> 31) return;
+    if (!(v >> kInstMaskShift)) return;
     const uint32_t p = pos[i];
     keys_out[p] = keys[i];
     vals_out[p] = v;
@@ -244,8 +251,10 @@ __global__ void __launch_bounds__(kThreads) raster_fwd_kernel(
     __shared__ SplatBatch<kBatch> sb;
     const int tile = blockIdx.x;
     const int tx = tile % tiles_x, ty = tile / tiles_x;
-    const int px = tx * kTile + (threadIdx.x & 15);
-    const int py0 = ty * kTile + (threadIdx.x >> 4), py1 = py0 + 8;
+    // warp w owns the 8x8 quadrant (w & 1, w >> 1); a lane owns rows y, y+4
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int px = tx * kTile + (warp & 1) * 8 + (lane & 7);
+    const int py0 = ty * kTile + (warp >> 1) * 8 + (lane >> 3), py1 = py0 + 4;
     const bool in0 = px < W && py0 < H, in1 = px < W && py1 < H;
     const uint2 rg = ranges[tile];
     const float pxc = (float)px + 0.5f, pyc0 = (float)py0 + 0.5f, pyc1 = (float)py1 + 0.5f;
@@ -264,6 +273,7 @@ __global__ void __launch_bounds__(kThreads) raster_fwd_kernel(
         const int nb = min((uint32_t)kBatch, rg.y - base);
         for (int k = 0; k < nb; ++k) {
             if (s0.done && s1.done) break;
+            if (!((sb.qm[k] >> warp) & 1u)) continue;  // exact: no pixel of this quadrant reaches 1/255
             const int4 hdr = sb.hdr[k];
             const bool b0 = !s0.done && in_box(hdr.x, hdr.y, px, py0);
             const bool b1 = !s1.done && in_box(hdr.x, hdr.y, px, py1);
@@ -307,7 +317,7 @@ __global__ void __launch_bounds__(128) raster_fixup_kernel(
             bool inb = false;
             double a = -1.0, r = 0.0, g = 0.0, b = 0.0;
             if (i < rg.y) {
-                const SplatRec& e = exact[inst_val[i]];
+                const SplatRec& e = exact[inst_val[i] & kInstIndexMask];
                 inb = px >= e.x0 && px <= e.x1 && py >= e.y0 && py <= e.y1;
                 if (inb) {
                     a = exact_alpha(e, pcx, pcy);
