@@ -119,10 +119,8 @@ __global__ void __launch_bounds__(128, 4) gaussian_bwd_kernel(
     const float* acc = accum + (size_t)j * acc_stride;
     const double d_rgb[3] = {acc[0], acc[1], acc[2]};
     const double d_alpha = acc[3];
-    const double d_screen[2] = {acc[4], acc[5]};
-    const double dC[2][2] = {{acc[6], acc[7]}, {acc[7], acc[8]}};
-    if (d_rgb[0] == 0.0 && d_rgb[1] == 0.0 && d_rgb[2] == 0.0 && d_alpha == 0.0 && d_screen[0] == 0.0 &&
-        d_screen[1] == 0.0 && dC[0][0] == 0.0 && dC[0][1] == 0.0 && dC[1][1] == 0.0)
+    if (d_rgb[0] == 0.0 && d_rgb[1] == 0.0 && d_rgb[2] == 0.0 && d_alpha == 0.0 && acc[4] == 0.0f &&
+        acc[5] == 0.0f && acc[6] == 0.0f && acc[7] == 0.0f && acc[8] == 0.0f)
         return;  // untouched (backward.cpp:226)
     const bool dyn = gid < n4;
     const int i = dyn ? gid : gid - n4;
@@ -131,6 +129,12 @@ __global__ void __launch_bounds__(128, 4) gaussian_bwd_kernel(
     auto prm = [&](int row) { return (double)P[(int64_t)row * cap + i]; };
     const double* cn = conic_src + (size_t)j * conic_stride;
     const double C[2][2] = {{cn[0], cn[1]}, {cn[2], cn[3]}};
+    // K6's conic-free sums -> d_screen = alpha * C . (sum h dx, sum h dy) and
+    // d_conic = -alpha/2 * sum h d d^T (backward.cpp:212-221)
+    const double ag = cn[4];  // SplatRec::alpha follows c11
+    const double d_screen[2] = {ag * (C[0][0] * acc[4] + C[0][1] * acc[5]), ag * (C[1][0] * acc[4] + C[1][1] * acc[5])};
+    const double hc = -0.5 * ag;
+    const double dC[2][2] = {{hc * acc[6], hc * acc[7]}, {hc * acc[7], hc * acc[8]}};
 
     // ---- forward intermediates
     double mean3[3], cov3[3][3], weight = 1.0, opl, R4[4][4], es[4], ql[4], qr[4], q3[4], cross[3], s44 = 1.0, dt = 0.0;

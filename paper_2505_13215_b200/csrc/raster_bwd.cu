@@ -1,17 +1,20 @@
 // raster_bwd.cu -- K6: tile rasterizer backward (backward.cpp:178-222).
 //
-// One CTA per tile, one thread per pixel, re-evaluating every pair with the
-// same arithmetic as K4 (so every contribute/skip decision is reproduced).
-// Like the reference it walks each pixel's list BACK TO FRONT from the
-// forward's recorded last contributor, accumulating the suffix colour
-// S_i = sum_{j>i} c_j a_j T_j + T_final*bg by addition (accurate for deep,
-// nearly occluded splats, unlike C_out - prefix) and recovering
-// T_i = T_{i+1} / (1 - a_i) from the stored final transmittance.
+// One CTA per tile, re-evaluating every pair with the same arithmetic as K4
+// (so every contribute/skip decision is reproduced).  Like the reference it
+// walks each pixel's list BACK TO FRONT from the forward's recorded last
+// contributor, accumulating the suffix colour already dotted with the pixel
+// gradient, GS_i = g . (sum_{j>i} c_j a_j T_j + T_final*bg), by addition
+// (accurate for deep, nearly occluded splats, unlike C_out - prefix) and
+// recovering T_i = T_{i+1} / (1 - a_i) from the stored final transmittance.
 //
-// Two pixels per thread (rows y and y+8 of the tile) share every staged splat;
-// per splat and warp their 9 accumulators are summed in registers, reduced
-// with a transposing butterfly (14 shuffles instead of 45) and added with one
-// red.global.add.f32 instruction (9 lanes, one per accumulator).
+// Warp w owns the 8x8 quadrant w of the tile, two pixels (rows y, y+4) per
+// lane; splats whose quadrant mask bit is clear are skipped warp-uniformly.
+// Per splat and warp the pixels' contributions are summed in registers,
+// reduced with a transposing butterfly (14 shuffles instead of 45) and added
+// with one red.global.add.f32 instruction per accumulator.  The accumulators
+// are conic-free (h = g * dL/da, h*dx, h*dy, h*dx^2, h*dx*dy, h*dy^2): K7
+// applies alpha and the FP64 conic once per splat.
 // Pixels the forward handed to the FP64 fix-up are back-propagated by
 // raster_bwd_exact_kernel (one warp per pixel, FP64).
 #include "kernels.cuh"
@@ -61,11 +64,14 @@ __device__ __forceinline__ float warp_sum(float v) {
 
 }  // namespace
 
-// accum layout: 12 floats per sorted splat (16-byte aligned):
-//   [0..2] d_rgb, [3] d_alpha (w.r.t. the base alpha), [4..5] d_screen,
-//   [6] d_conic00, [7] d_conic01 (= d_conic10), [8] d_conic11, [9..11] pad
+// accum layout: 12 floats per sorted splat (16-byte aligned), with
+// h = g * dL/da (g = exp(-power), a = alpha * g) and d = pixel - mean:
+//   [0..2] sum w * dL/dC (d_rgb), [3] sum h (= d_alpha), [4] sum h dx,
+//   [5] sum h dy, [6] sum h dx^2, [7] sum h dx dy, [8] sum h dy^2, [9..11] pad
+// K7 turns [4..8] into d_screen = alpha * conic . ([4],[5]) and
+// d_conic = -alpha/2 * ([6] [7]; [7] [8]) (backward.cpp:212-221).
 constexpr int kAccStride = 12;
-constexpr int kThreadsB = 128;  // two pixels (rows y and y+8) per thread
+constexpr int kThreadsB = 128;  // two pixels per thread
 
 __device__ __forceinline__ void red_add(float* addr, float v) {
     asm volatile("red.global.add.f32 [%0], %1;" ::"l"(addr), "f"(v) : "memory");
@@ -81,70 +87,47 @@ __device__ __forceinline__ float rcp_approx(float x) {
 struct PixBwd {
     float gr, gg, gb;  // dL/dC
     float T;           // transmittance after the current splat
-    float Sr, Sg, Sb;  // suffix colour (incl. T_final * bg)
+    float GS;          // g . suffix colour (incl. T_final * bg)
     uint32_t last;
 };
 
-// One pair of backward.cpp:204-221, accumulated into v[0..8].
-__device__ __forceinline__ bool backprop_pair(PixBwd& s, const int4 hdr, const float4 m, const float4 L, const float4 col,
-                                              const float4 cn, const SplatRec* e, float pxc, float pyc, double pcx,
-                                              double pcy, float v[9]) {
-    float x, dx, dy;
-    if (__int_as_float(hdr.w) < 0.0f) {  // FP64 exponent path
-        x = exact_x(e, pcx, pcy);
-        const float2 d = exact_delta(e, pcx, pcy);
-        dx = d.x;
-        dy = d.y;
-    } else {
-        x = fast_x(m, L, pxc, pyc, dx, dy);
-    }
-    float g;
-    const float a = pair_alpha(L.w, __int_as_float(hdr.z), col.w, x, e, pcx, pcy, g);
-    if (a < 0.0f) return false;
+// One pair of backward.cpp:204-221 given its alpha (p = the pair
+// contributes): returns w = a T_i and h = g dL/da (both 0 when !p) and steps
+// the pixel's state to the front of the splat.
+__device__ __forceinline__ void backprop_pair(PixBwd& s, bool p, float g, float alpha_f, const float4 col,
+                                              float& w_out, float& h_out) {
+    const float a = alpha_f * g;
     const float inv = rcp_approx(1.0f - a);
     const float Ti = s.T * inv;  // transmittance before this splat
-    const float w = a * Ti;
-    // d_a = g_pix . (rgb * T_i - S / (1 - a))
-    const float d_a =
-        s.gr * fmaf(col.x, Ti, -s.Sr * inv) + s.gg * fmaf(col.y, Ti, -s.Sg * inv) + s.gb * fmaf(col.z, Ti, -s.Sb * inv);
-    s.Sr = fmaf(col.x, w, s.Sr);
-    s.Sg = fmaf(col.y, w, s.Sg);
-    s.Sb = fmaf(col.z, w, s.Sb);
-    s.T = Ti;
-    v[0] = fmaf(w, s.gr, v[0]);
-    v[1] = fmaf(w, s.gg, v[1]);
-    v[2] = fmaf(w, s.gb, v[2]);
-    v[3] = fmaf(g, d_a, v[3]);
-    const float gdg = g * (L.w * d_a);  // g * d_g, d_g = alpha * d_a
-    v[4] = fmaf(gdg, fmaf(cn.x, dx, cn.y * dy), v[4]);
-    v[5] = fmaf(gdg, fmaf(cn.z, dx, cn.w * dy), v[5]);
-    const float hc = -0.5f * gdg;
-    v[6] = fmaf(hc * dx, dx, v[6]);
-    v[7] = fmaf(hc * dx, dy, v[7]);
-    v[8] = fmaf(hc * dy, dy, v[8]);
-    return true;
+    const float gc = fmaf(s.gr, col.x, fmaf(s.gg, col.y, s.gb * col.z));
+    // dL/da = g . (rgb * T_i - S / (1 - a))
+    const float d_a = fmaf(Ti, gc, -inv * s.GS);
+    const float w = p ? a * Ti : 0.0f;
+    h_out = p ? g * d_a : 0.0f;
+    w_out = w;
+    s.GS = fmaf(w, gc, s.GS);
+    s.T = p ? Ti : s.T;
 }
 
-__global__ void __launch_bounds__(kThreadsB) raster_bwd_kernel(
+__global__ void __launch_bounds__(kThreadsB, 8) raster_bwd_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ inst_val, const SplatFast* __restrict__ fast,
     const SplatRec* __restrict__ exact, int W, int H, int tiles_x, const float* __restrict__ tfinal,
     const uint32_t* __restrict__ last_arr, const float* __restrict__ dL_dimg, float bg_r, float bg_g, float bg_b,
     float* __restrict__ accum) {
     __shared__ SplatBatch<kBatchB> sb;
-    __shared__ float4 s_conic[kBatchB];  // float conic (c00, c01, c10, c11)
     __shared__ uint32_t s_maxlast;
     const int tile = blockIdx.x;
     const int tx = tile % tiles_x, ty = tile / tiles_x;
     // warp w owns the 8x8 quadrant (w & 1, w >> 1); a lane owns rows y, y+4
-    const int warp = threadIdx.x >> 5;
-    const int px = tx * kTile + (warp & 1) * 8 + (threadIdx.x & 7);
-    const int py0 = ty * kTile + (warp >> 1) * 8 + ((threadIdx.x & 31) >> 3), py1 = py0 + 4;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int px = tx * kTile + (warp & 1) * 8 + (lane & 7);
+    const int py0 = ty * kTile + (warp >> 1) * 8 + (lane >> 3), py1 = py0 + 4;
     const uint2 rg = ranges[tile];
     const float pxc = (float)px + 0.5f, pyc0 = (float)py0 + 0.5f, pyc1 = (float)py1 + 0.5f;
     const double pcx = (double)px + 0.5, pcy0 = (double)py0 + 0.5, pcy1 = (double)py1 + 0.5;
 
     auto init = [&](int py, PixBwd& s) {
-        s = PixBwd{0.f, 0.f, 0.f, 1.f, 0.f, 0.f, 0.f, rg.x};
+        s = PixBwd{0.f, 0.f, 0.f, 1.f, 0.f, rg.x};
         if (px >= W || py >= H) return;
         const int pix = py * W + px;
         const uint32_t l = last_arr[pix];
@@ -152,9 +135,7 @@ __global__ void __launch_bounds__(kThreadsB) raster_bwd_kernel(
         s.gg = dL_dimg[pix * 3 + 1];
         s.gb = dL_dimg[pix * 3 + 2];
         s.T = tfinal[pix];
-        s.Sr = s.T * bg_r;
-        s.Sg = s.T * bg_g;
-        s.Sb = s.T * bg_b;
+        s.GS = s.T * fmaf(s.gr, bg_r, fmaf(s.gg, bg_g, s.gb * bg_b));
         // flagged pixels go through the exact kernel; zero gradient = untouched (backward.cpp:188)
         if (!(l & 0x80000000u) && (s.gr != 0.f || s.gg != 0.f || s.gb != 0.f)) s.last = l;
     };
@@ -167,7 +148,6 @@ __global__ void __launch_bounds__(kThreadsB) raster_bwd_kernel(
     if (ml > rg.x) atomicMax(&s_maxlast, ml);
     __syncthreads();
     const uint32_t end = s_maxlast;
-    const int lane = threadIdx.x & 31;
     const uint32_t warp_end = __reduce_max_sync(0xffffffffu, ml);  // nothing past it in this warp
 
     const int nbatch = (int)((end - rg.x + kBatchB - 1) / kBatchB);
@@ -175,12 +155,7 @@ __global__ void __launch_bounds__(kThreadsB) raster_bwd_kernel(
         const uint32_t base = rg.x + (uint32_t)bi * kBatchB;
         const int nb = (int)min((uint32_t)kBatchB, end - base);
         __syncthreads();
-        for (int t = threadIdx.x; t < nb; t += kThreadsB) {
-            const uint32_t v = inst_val[base + t];
-            sb.load(t, fast, v);
-            const SplatRec& e = exact[v & kInstIndexMask];
-            s_conic[t] = make_float4((float)e.c00, (float)e.c01, (float)e.c10, (float)e.c11);
-        }
+        for (int t = threadIdx.x; t < nb; t += kThreadsB) sb.load(t, fast, inst_val[base + t]);
         __syncthreads();
         const int kmax = (int)min((uint32_t)nb, warp_end > base ? warp_end - base : 0u);
         for (int k = kmax - 1; k >= 0; --k) {
@@ -190,17 +165,55 @@ __global__ void __launch_bounds__(kThreadsB) raster_bwd_kernel(
             const bool b0 = idx < s0.last && in_box(hdr.x, hdr.y, px, py0);
             const bool b1 = idx < s1.last && in_box(hdr.x, hdr.y, px, py1);
             if (!__any_sync(0xffffffffu, b0 || b1)) continue;
-            float v[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-            bool any = false;
-            if (b0 || b1) {
-                const float4 m = sb.mean[k], L = sb.chol[k], col = sb.col[k], cn = s_conic[k];
-                const SplatRec* e = exact + sb.j[k];
-                if (b0) any |= backprop_pair(s0, hdr, m, L, col, cn, e, pxc, pyc0, pcx, pcy0, v);
-                if (b1) any |= backprop_pair(s1, hdr, m, L, col, cn, e, pxc, pyc1, pcx, pcy1, v);
+            const float4 L = sb.chol[k], col = sb.col[k];
+            const SplatRec* e = exact + sb.j[k];
+            // exponent argument and offset of both pixels (same column: one dx
+            // on the fast path, the same rounding sequence as K4's fast_x)
+            float x0 = INFINITY, x1 = INFINITY, dx0 = 0.f, dx1 = 0.f, dy0 = 0.f, dy1 = 0.f;
+            if (__int_as_float(hdr.w) < 0.0f) {  // FP64 exponent path (uniform per splat)
+                if (b0) {
+                    x0 = exact_x(e, pcx, pcy0);
+                    const float2 d = exact_delta(e, pcx, pcy0);
+                    dx0 = d.x;
+                    dy0 = d.y;
+                }
+                if (b1) {
+                    x1 = exact_x(e, pcx, pcy1);
+                    const float2 d = exact_delta(e, pcx, pcy1);
+                    dx1 = d.x;
+                    dy1 = d.y;
+                }
+            } else {
+                const float4 m = sb.mean[k];
+                x0 = fast_x(m, L, pxc, pyc0, dx0, dy0);
+                dx1 = dx0;
+                dy1 = __fsub_rn(__fsub_rn(pyc1, m.y), m.w);
+                const float u1 = fmaf(L.x, dx1, L.y * dy1), u2 = L.z * dy1;
+                x1 = fmaf(u1, u1, u2 * u2);
             }
+            // the oracle's a >= 1/255 test (exact: FP64 inside the guard band)
+            const float x_skip = __int_as_float(hdr.z), x_keep = col.w;
+            bool p0 = b0 && x0 < x_skip, p1 = b1 && x1 < x_skip;
+            if (p0 && x0 >= x_keep) p0 = exact_alpha_passes(e, pcx, pcy0);
+            if (p1 && x1 >= x_keep) p1 = exact_alpha_passes(e, pcx, pcy1);
             // lanes without a contributing pixel hold zeros; skip the
             // reduction when the whole warp is empty
-            if (!__any_sync(0xffffffffu, any)) continue;
+            if (!__any_sync(0xffffffffu, p0 || p1)) continue;
+            const float g0 = fast_exp2_neg(p0 ? x0 : 128.0f), g1 = fast_exp2_neg(p1 ? x1 : 128.0f);
+            float w0, h0, w1, h1;
+            backprop_pair(s0, p0, g0, L.w, col, w0, h0);
+            backprop_pair(s1, p1, g1, L.w, col, w1, h1);
+            const float hx0 = h0 * dx0, hx1 = h1 * dx1, hy0 = h0 * dy0, hy1 = h1 * dy1;
+            float v[9];
+            v[0] = fmaf(w0, s0.gr, w1 * s1.gr);
+            v[1] = fmaf(w0, s0.gg, w1 * s1.gg);
+            v[2] = fmaf(w0, s0.gb, w1 * s1.gb);
+            v[3] = h0 + h1;
+            v[4] = hx0 + hx1;
+            v[5] = hy0 + hy1;
+            v[6] = fmaf(hx0, dx0, hx1 * dx1);
+            v[7] = fmaf(hx0, dy0, hx1 * dy1);
+            v[8] = fmaf(hy0, dy0, hy1 * dy1);
             const float r8 = transpose_reduce8(v);
             const float r9 = warp_sum(v[8]);
             float* dst = accum + (size_t)sb.j[k] * kAccStride;
@@ -273,16 +286,14 @@ __global__ void __launch_bounds__(128) raster_bwd_exact_kernel(
                     float* dst = accum + (size_t)(inst_val[i] & kInstIndexMask) * kAccStride;
                     const double w = a * myT;
                     for (int c = 0; c < 3; ++c) atomicAdd(dst + c, (float)(w * gp[c]));
-                    atomicAdd(dst + 3, (float)(g * d_a));
-                    const double d_g = e->alpha * d_a;
+                    const double h = g * d_a;
                     const double dx = pcx - e->sx, dy = pcy - e->sy;
-                    const double q0 = e->c00 * dx + e->c01 * dy, q1 = e->c10 * dx + e->c11 * dy;
-                    atomicAdd(dst + 4, (float)(g * d_g * q0));
-                    atomicAdd(dst + 5, (float)(g * d_g * q1));
-                    const double f = -0.5 * g * d_g;
-                    atomicAdd(dst + 6, (float)(f * dx * dx));
-                    atomicAdd(dst + 7, (float)(f * dx * dy));
-                    atomicAdd(dst + 8, (float)(f * dy * dy));
+                    atomicAdd(dst + 3, (float)h);
+                    atomicAdd(dst + 4, (float)(h * dx));
+                    atomicAdd(dst + 5, (float)(h * dy));
+                    atomicAdd(dst + 6, (float)(h * dx * dx));
+                    atomicAdd(dst + 7, (float)(h * dx * dy));
+                    atomicAdd(dst + 8, (float)(h * dy * dy));
                 }
             }
             if (pass == 0) {
