@@ -22,6 +22,7 @@
 namespace hgs {
 
 constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kAlphaErr0 = 4.0e-7f;  // ex2.approx (2^-22) + alpha_f and product roundings
 constexpr double kLog2eD = 1.4426950408889634;
 
 // 64-byte FP32 view of a sorted splat, stored as four 16-byte vectors so the
@@ -30,7 +31,7 @@ struct __align__(16) SplatFast {
     int32_t xr;      // x0 | (x1 - x0) << 16   (inclusive clamped pixel box)
     int32_t yr;      // y0 | (y1 - y0) << 16
     float x_skip;    // x >= x_skip: alpha certainly below 1/255 (no exp needed)
-    float eps;       // certified relative error bound of the fast alpha; < 0: FP64 path
+    float eps;       // e1: the fast alpha's relative error is <= e1*x + kAlphaErr0; < 0: FP64 path
     float sx_hi, sy_hi, sx_lo, sy_lo;  // screen mean as double-float
     float l00, l01, l11;               // Cholesky of 0.5*log2(e)*conic: x = |L d|^2 = power*log2(e)
     float alpha_f;

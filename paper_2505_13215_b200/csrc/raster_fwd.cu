@@ -55,9 +55,15 @@ __global__ void __launch_bounds__(256) gather_sorted_kernel(const uint32_t* __re
     // FP32 path: |x_f - x| <= u*X*(17 + 16r) over the relevant region x <= 8,
     // u = 2^-24 (two extra roundings for the double-float mean); relative
     // alpha error = ln2*|dx| + 2^-22 (ex2.approx) + 2 roundings.
-    const double eps = fp64 ? 1.0e-6 : 8.0e-6 * (1.0 + r) + 4.0e-7;
+    // The error of x grows with x itself: |x_f - x| <= u*x*(17 + 16r), i.e. a
+    // relative alpha error <= e1*x + e0 with e1 = ln2*u*(17 + 16r) <=
+    // 1e-6*(1 + r) and e0 = 4e-7 (FP64 path: x only rounded, e1 = 1e-7).
+    // The cutoff guard band uses the bound at x <= 8; the transmittance
+    // error (K4) uses the per-pair bound, tight for the opaque core.
+    const double e1 = fp64 ? 1.0e-7 : 1.0e-6 * (1.0 + r);
+    const double eps = 8.0 * e1 + 4.0e-7;
     cutoff_thresholds((double)e.alpha_f, eps, f.x_skip, f.x_keep);
-    f.eps = fp64 ? -(float)eps : (float)eps;  // sign bit selects the FP64 exponent path
+    f.eps = fp64 ? -(float)e1 : (float)e1;  // sign bit selects the FP64 exponent path
     f.xr = (int32_t)e.x0 | ((int32_t)(e.x1 - e.x0) << 16);
     f.yr = (int32_t)e.y0 | ((int32_t)(e.y1 - e.y0) << 16);
     fast_sorted[j] = f;
@@ -189,27 +195,20 @@ struct PixFwd {
     bool done, flagged;
 };
 
-// One pair of raster.cpp:132-143 on the fast path (bounded relative error).
-__device__ __forceinline__ void composite_pair(PixFwd& s, const int4 hdr, const float4 m, const float4 L, const float4 c,
-                                               const SplatRec* e, float pxc, float pyc, double pcx, double pcy,
-                                               uint32_t idx) {
-    ++s.count;
-    float x, dx, dy;
-    const float eps_s = __int_as_float(hdr.w);
-    if (eps_s < 0.0f) x = exact_x(e, pcx, pcy);
-    else x = fast_x(m, L, pxc, pyc, dx, dy);
-    const float eps = fabsf(eps_s);
-    float g;
-    const float a = pair_alpha(L.w, __int_as_float(hdr.z), c.w, x, e, pcx, pcy, g);
-    if (a < 0.0f) return;
-    const float w = a * s.T;
+// One pair of raster.cpp:132-143 given its alpha (p = the pair passes the
+// 1/255 test; a no-op otherwise).  err tracks the certified relative error
+// bound of T; a pixel whose T lands inside the band around the oracle's
+// T < 1e-4 decision is flagged for the FP64 fix-up.
+__device__ __forceinline__ void composite_pair(PixFwd& s, bool p, float a, float eps, const float4 c, uint32_t idx) {
+    const float w = p ? a * s.T : 0.0f;
     s.r = fmaf(c.x, w, s.r);
     s.g = fmaf(c.y, w, s.g);
     s.b = fmaf(c.z, w, s.b);
     const float om = 1.0f - a;
-    s.err = fmaf(a * eps, rcp_approx(om), s.err + 2.5e-7f);
-    s.T *= om;
-    s.last = idx + 1;
+    s.err = p ? fmaf(a * eps, rcp_approx(om), s.err + 2.5e-7f) : s.err;
+    s.T = p ? s.T * om : s.T;
+    s.last = p ? idx + 1 : s.last;
+    // T and err only change with p, so re-testing an unchanged pixel is a no-op
     if (s.T < 1.0e-4f * (1.0f + 2.0f * s.err)) {
         // inside the certified error band of the oracle's T < 1e-4 decision?
         if (s.T > 1.0e-4f * (1.0f - 2.0f * s.err)) s.flagged = true;
@@ -278,10 +277,33 @@ __global__ void __launch_bounds__(kThreads, 8) raster_fwd_kernel(
             const bool b0 = !s0.done && in_box(hdr.x, hdr.y, px, py0);
             const bool b1 = !s1.done && in_box(hdr.x, hdr.y, px, py1);
             if (!(b0 || b1)) continue;
-            const float4 m = sb.mean[k], L = sb.chol[k], c = sb.col[k];
+            s0.count += b0;
+            s1.count += b1;
+            const float4 L = sb.chol[k], c = sb.col[k];
             const SplatRec* e = exact + sb.j[k];
-            if (b0) composite_pair(s0, hdr, m, L, c, e, pxc, pyc0, pcx, pcy0, base + k);
-            if (b1) composite_pair(s1, hdr, m, L, c, e, pxc, pyc1, pcx, pcy1, base + k);
+            const float eps_s = __int_as_float(hdr.w);
+            float x0 = INFINITY, x1 = INFINITY;
+            if (eps_s < 0.0f) {  // FP64 exponent path (uniform per splat)
+                if (b0) x0 = exact_x(e, pcx, pcy0);
+                if (b1) x1 = exact_x(e, pcx, pcy1);
+            } else {  // both pixels share the column: one dx (same rounding as fast_x)
+                const float4 m = sb.mean[k];
+                float dx, dy0;
+                x0 = fast_x(m, L, pxc, pyc0, dx, dy0);
+                const float dy1 = __fsub_rn(__fsub_rn(pyc1, m.y), m.w);
+                const float u1 = fmaf(L.x, dx, L.y * dy1), u2 = L.z * dy1;
+                x1 = fmaf(u1, u1, u2 * u2);
+            }
+            // the oracle's a >= 1/255 test (exact: FP64 inside the guard band)
+            const float x_skip = __int_as_float(hdr.z), x_keep = c.w;
+            bool p0 = b0 && x0 < x_skip, p1 = b1 && x1 < x_skip;
+            if (p0 && x0 >= x_keep) p0 = exact_alpha_passes(e, pcx, pcy0);
+            if (p1 && x1 >= x_keep) p1 = exact_alpha_passes(e, pcx, pcy1);
+            if (!(p0 || p1)) continue;
+            const float a0 = L.w * fast_exp2_neg(p0 ? x0 : 128.0f), a1 = L.w * fast_exp2_neg(p1 ? x1 : 128.0f);
+            const float e1 = fabsf(eps_s);
+            composite_pair(s0, p0, a0, fmaf(e1, x0, kAlphaErr0), c, base + k);
+            composite_pair(s1, p1, a1, fmaf(e1, x1, kAlphaErr0), c, base + k);
         }
     }
     if (in0)
