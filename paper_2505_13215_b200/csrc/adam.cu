@@ -1,125 +1,191 @@
 // adam.cu -- K8: fused Adam step + gradient zeroing (train.cpp:18-180).
 //
-// One thread per Gaussian row, looping over the parameter classes in the
-// reference's order (3D: mean, quat, scales, opacity, SH; 4D: mean_x, mean_t,
-// q_left, q_right, scales, opacity, SH).  Per row and class: skip the whole
-// class if any gradient is non-finite (counted), else the bias-corrected
-// update with eps = 1e-15; quaternions are renormalised every step with the
-// canonical sign and the first moment flipped with it (train.cpp:46-53,
-// applied even when the update was skipped).  Every component access is a
-// coalesced SoA row; the gradient is zeroed in the same pass.
-// Bytes per element: param, m, v read+write, grad read+zero = 32 B.  HBM bound.
+// Reference semantics per Gaussian, parameter classes in the reference's
+// order (3D: mean, quat, scales, opacity, SH; 4D: mean_x, mean_t, q_left,
+// q_right, scales, opacity, SH): skip a whole class if any of its gradients
+// is non-finite (counted), else the bias-corrected update with eps = 1e-15;
+// quaternions are renormalised every step with the canonical sign and the
+// first moment flipped with it (train.cpp:46-53, applied even when the update
+// was skipped).
+//
+// Two passes, both over coalesced SoA rows with float4 (four Gaussians per
+// thread; capacities are multiples of 128):
+//   adam_classes_kernel  one thread per 4 Gaussians: reads every gradient
+//                        row once, writes a per-Gaussian bitmask of finite
+//                        classes, fully updates + renormalises the quaternion
+//                        classes (their 4 rows belong together), folds the
+//                        densification-statistic deltas;
+//   adam_rows_kernel     one thread per (row, 4 Gaussians) of every other
+//                        row: p, m, v read+write, grad read+zero = 32 B per
+//                        element at full memory-level parallelism.  HBM bound.
 #include "kernels.cuh"
 
 namespace hgs {
 
-
 namespace {
 
-__device__ __forceinline__ bool row_finite(const float* g, int64_t cap, int i, int r0, int d) {
-    bool ok = true;
-#pragma unroll 8
-    for (int k = 0; k < d; ++k) ok &= isfinite(g[(int64_t)(r0 + k) * cap + i]);
-    return ok;
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float y;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float rcp_approx_a(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
 }
 
-__device__ __forceinline__ void adam_class(float* p, float* g, float* m, float* v, int64_t cap, int i, int r0, int d,
-                                           float lr, const AdamArgs& A, uint32_t& skipped) {
-    if (!row_finite(g, cap, i, r0, d)) {
-        ++skipped;
-        for (int k = 0; k < d; ++k) g[(int64_t)(r0 + k) * cap + i] = 0.f;
-        return;
+__device__ __forceinline__ float4 ld4(const float* p) { return __ldcs(reinterpret_cast<const float4*>(p)); }
+__device__ __forceinline__ void st4(float* p, float4 v) { __stcs(reinterpret_cast<float4*>(p), v); }
+__device__ __forceinline__ float comp(const float4& v, int k) { return k == 0 ? v.x : k == 1 ? v.y : k == 2 ? v.z : v.w; }
+__device__ __forceinline__ bool fin(float x) { return isfinite(x); }
+
+// One Adam element (train.cpp:155-170); ok = the class is finite.
+__device__ __forceinline__ void adam1(float& p, float& m, float& v, float g, bool ok, float lr, const AdamArgs& A) {
+    if (!ok) return;
+    m = fmaf(A.b1, m, A.one_m_b1 * g);
+    v = fmaf(A.b2, v, A.one_m_b2 * g * g);
+    const float mhat = m * A.inv_bc1, vhat = v * A.inv_bc2;
+    p -= lr * mhat * rcp_approx_a(sqrt_approx(vhat) + 1e-15f);
+}
+
+// Parameter classes of a pool: first row, row count, bit in the class mask.
+struct PoolLayout {
+    int n_cls;
+    int r0[7], d[7];
+    bool quat[7];
+};
+__device__ __forceinline__ PoolLayout layout(bool dyn, int K3) {
+    PoolLayout L;
+    if (dyn) {
+        L.n_cls = 7;
+        const int r0[7] = {R4_MEAN, R4_MT, R4_QL, R4_QR, R4_LS, R4_OP, R4_SH};
+        const int d[7] = {3, 1, 4, 4, 4, 1, K3};
+        for (int c = 0; c < 7; ++c) L.r0[c] = r0[c], L.d[c] = d[c], L.quat[c] = (c == 2 || c == 3);
+    } else {
+        L.n_cls = 5;
+        const int r0[5] = {R3_MEAN, R3_Q, R3_LS, R3_OP, R3_SH};
+        const int d[5] = {3, 4, 3, 1, K3};
+        for (int c = 0; c < 5; ++c) L.r0[c] = r0[c], L.d[c] = d[c], L.quat[c] = (c == 1);
+        L.r0[5] = L.r0[6] = 0;
+        L.d[5] = L.d[6] = 0;
+        L.quat[5] = L.quat[6] = false;
     }
-    // chunks of 8 rows: all 32 loads of a chunk are issued before any store
-    // (memory-level parallelism; the four arrays never alias)
-    constexpr int C = 8;
-    for (int k0 = 0; k0 < d; k0 += C) {
-        float gr[C], mm[C], vv[C], pp[C];
-#pragma unroll
-        for (int u = 0; u < C; ++u) {
-            if (k0 + u < d) {
-                const int64_t o = (int64_t)(r0 + k0 + u) * cap + i;
-                gr[u] = __ldcs(&g[o]);
-                mm[u] = __ldcs(&m[o]);
-                vv[u] = __ldcs(&v[o]);
-                pp[u] = __ldcs(&p[o]);
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < C; ++u) {
-            if (k0 + u < d) {
-                const int64_t o = (int64_t)(r0 + k0 + u) * cap + i;
-                const float mk = A.b1 * mm[u] + A.one_m_b1 * gr[u];
-                const float vk = A.b2 * vv[u] + A.one_m_b2 * gr[u] * gr[u];
-                const float mhat = mk * A.inv_bc1, vhat = vk * A.inv_bc2;
-                __stcs(&m[o], mk);
-                __stcs(&v[o], vk);
-                __stcs(&p[o], pp[u] - lr * mhat / (sqrtf(vhat) + 1e-15f));
-                __stcs(&g[o], 0.f);
-            }
-        }
-    }
+    return L;
 }
 
 // train.cpp:46-53 followed by UnitQuat::normalized (gauss_math.cpp:35-44)
-__device__ __forceinline__ bool renorm_quat(float* p, float* m, int64_t cap, int i, int r0) {
-    float q[4];
-    for (int k = 0; k < 4; ++k) q[k] = p[(int64_t)(r0 + k) * cap + i];
+__device__ __forceinline__ bool renorm_quat(float q[4], float mq[4]) {
     float n = sqrtf(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
     float w = q[0] / n, x = q[1] / n, y = q[2] / n, z = q[3] / n;
     const bool flip = w < 0.f || (w == 0.f && (x < 0.f || (x == 0.f && (y < 0.f || (y == 0.f && z < 0.f)))));
     if (flip)
-        for (int k = 0; k < 4; ++k) m[(int64_t)(r0 + k) * cap + i] = -m[(int64_t)(r0 + k) * cap + i];
+        for (int k = 0; k < 4; ++k) mq[k] = -mq[k];
     n = sqrtf(w * w + x * x + y * y + z * z);
     if (!(n > 0.f) || !isfinite(n)) return false;
     w /= n;
     x /= n;
     y /= n;
     z /= n;
-    if (flip) {
-        w = -w;
-        x = -x;
-        y = -y;
-        z = -z;
-    }
-    p[(int64_t)(r0 + 0) * cap + i] = w;
-    p[(int64_t)(r0 + 1) * cap + i] = x;
-    p[(int64_t)(r0 + 2) * cap + i] = y;
-    p[(int64_t)(r0 + 3) * cap + i] = z;
+    const float s = flip ? -1.f : 1.f;
+    q[0] = s * w;
+    q[1] = s * x;
+    q[2] = s * y;
+    q[3] = s * z;
     return true;
 }
 
 }  // namespace
 
-__global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ p4, float* __restrict__ g4, float* __restrict__ m4,
-                                                   float* __restrict__ v4, int64_t cap4, int n4, float* __restrict__ p3,
-                                                   float* __restrict__ g3, float* __restrict__ m3, float* __restrict__ v3,
-                                                   int64_t cap3, int n3, int deg, AdamArgs A,
-                                                   unsigned long long* __restrict__ skipped_total,
-                                                   uint32_t* __restrict__ flags) {
+__global__ void __launch_bounds__(128) adam_classes_kernel(AdamPools P, AdamArgs A, uint8_t* __restrict__ cls_ok3,
+                                                           uint8_t* __restrict__ cls_ok4,
+                                                           unsigned long long* __restrict__ skipped_total,
+                                                           uint32_t* __restrict__ flags) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int q3 = (P.n3 + 3) >> 2, q4 = (P.n4 + 3) >> 2;
     uint32_t skipped = 0;
     bool ok = true;
-    const int K3 = 3 * sh_count(deg);
-    if (t < n3) {
-        const int i = t;
-        adam_class(p3, g3, m3, v3, cap3, i, R3_MEAN, 3, A.lr_mean, A, skipped);
-        adam_class(p3, g3, m3, v3, cap3, i, R3_Q, 4, A.lr_quat, A, skipped);
-        ok &= renorm_quat(p3, m3, cap3, i, R3_Q);
-        adam_class(p3, g3, m3, v3, cap3, i, R3_LS, 3, A.lr_scales, A, skipped);
-        adam_class(p3, g3, m3, v3, cap3, i, R3_OP, 1, A.lr_opacity, A, skipped);
-        adam_class(p3, g3, m3, v3, cap3, i, R3_SH, K3, A.lr_sh, A, skipped);
-    } else if (t < n3 + n4) {
-        const int i = t - n3;
-        adam_class(p4, g4, m4, v4, cap4, i, R4_MEAN, 3, A.lr_mean, A, skipped);
-        adam_class(p4, g4, m4, v4, cap4, i, R4_MT, 1, A.lr_mean_t, A, skipped);
-        adam_class(p4, g4, m4, v4, cap4, i, R4_QL, 4, A.lr_quat, A, skipped);
-        ok &= renorm_quat(p4, m4, cap4, i, R4_QL);
-        adam_class(p4, g4, m4, v4, cap4, i, R4_QR, 4, A.lr_quat, A, skipped);
-        ok &= renorm_quat(p4, m4, cap4, i, R4_QR);
-        adam_class(p4, g4, m4, v4, cap4, i, R4_LS, 4, A.lr_scales, A, skipped);
-        adam_class(p4, g4, m4, v4, cap4, i, R4_OP, 1, A.lr_opacity, A, skipped);
-        adam_class(p4, g4, m4, v4, cap4, i, R4_SH, K3, A.lr_sh, A, skipped);
+    if (t < q3 + q4) {
+        const bool dyn = t >= q3;
+        const int i0 = (dyn ? t - q3 : t) * 4;
+        const int n = dyn ? P.n4 : P.n3;
+        const int64_t cap = dyn ? P.cap4 : P.cap3;
+        float* p = dyn ? P.p4 : P.p3;
+        float* g = dyn ? P.g4 : P.g3;
+        float* m = dyn ? P.m4 : P.m3;
+        float* v = dyn ? P.v4 : P.v3;
+        const PoolLayout L = layout(dyn, P.K3);
+        const int nvalid = min(4, n - i0);
+        uint32_t okm[4] = {0u, 0u, 0u, 0u};
+        for (int c = 0; c < L.n_cls; ++c) {
+            bool f[4] = {true, true, true, true};
+#pragma unroll 4
+            for (int k = 0; k < L.d[c]; ++k) {
+                const float4 gv = __ldg(reinterpret_cast<const float4*>(g + (int64_t)(L.r0[c] + k) * cap + i0));
+                f[0] &= fin(gv.x);
+                f[1] &= fin(gv.y);
+                f[2] &= fin(gv.z);
+                f[3] &= fin(gv.w);
+            }
+            for (int u = 0; u < 4; ++u) {
+                okm[u] |= (f[u] ? 1u : 0u) << c;
+                if (u < nvalid && !f[u]) ++skipped;
+            }
+            if (!L.quat[c]) continue;
+            // quaternion class: update, renormalise (even if skipped), zero its gradient
+            float4 pr[4], mr[4], vr[4], gr[4];
+            for (int k = 0; k < 4; ++k) {
+                const int64_t o = (int64_t)(L.r0[c] + k) * cap + i0;
+                pr[k] = ld4(p + o);
+                mr[k] = ld4(m + o);
+                vr[k] = ld4(v + o);
+                gr[k] = ld4(g + o);
+            }
+            float lr = A.lr_quat;
+            for (int u = 0; u < nvalid; ++u) {
+                float q[4], mq[4], vq[4];
+                for (int k = 0; k < 4; ++k) {
+                    q[k] = comp(pr[k], u);
+                    mq[k] = comp(mr[k], u);
+                    vq[k] = comp(vr[k], u);
+                    adam1(q[k], mq[k], vq[k], comp(gr[k], u), f[u], lr, A);
+                }
+                ok &= renorm_quat(q, mq);
+                for (int k = 0; k < 4; ++k) {
+                    float* pp = &pr[k].x;
+                    float* mm = &mr[k].x;
+                    float* vv = &vr[k].x;
+                    pp[u] = q[k];
+                    mm[u] = mq[k];
+                    vv[u] = vq[k];
+                }
+            }
+            for (int k = 0; k < 4; ++k) {
+                const int64_t o = (int64_t)(L.r0[c] + k) * cap + i0;
+                st4(p + o, pr[k]);
+                st4(m + o, mr[k]);
+                st4(v + o, vr[k]);
+                st4(g + o, make_float4(0.f, 0.f, 0.f, 0.f));
+            }
+        }
+        uint8_t* out = dyn ? cls_ok4 : cls_ok3;
+        *reinterpret_cast<uchar4*>(out + i0) = make_uchar4(okm[0], okm[1], okm[2], okm[3]);
+        // fold this step's densification-statistic deltas (train.cpp:433-444)
+        float* gn = dyn ? P.gn4 : P.gn3;
+        float* cnt = dyn ? P.cnt4 : P.cnt3;
+        float* dgn = dyn ? P.dgn4 : P.dgn3;
+        float* dcnt = dyn ? P.dcnt4 : P.dcnt3;
+        const float4 d = *reinterpret_cast<const float4*>(dgn + i0), dc = *reinterpret_cast<const float4*>(dcnt + i0);
+        if (d.x != 0.f || d.y != 0.f || d.z != 0.f || d.w != 0.f || dc.x != 0.f || dc.y != 0.f || dc.z != 0.f ||
+            dc.w != 0.f) {
+            float4 a = *reinterpret_cast<float4*>(gn + i0), b = *reinterpret_cast<float4*>(cnt + i0);
+            a.x += d.x, a.y += d.y, a.z += d.z, a.w += d.w;
+            b.x += dc.x, b.y += dc.y, b.z += dc.z, b.w += dc.w;
+            *reinterpret_cast<float4*>(gn + i0) = a;
+            *reinterpret_cast<float4*>(cnt + i0) = b;
+            *reinterpret_cast<float4*>(dgn + i0) = make_float4(0.f, 0.f, 0.f, 0.f);
+            *reinterpret_cast<float4*>(dcnt + i0) = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
     }
     const unsigned full = 0xffffffffu;
     const uint32_t s = __reduce_add_sync(full, skipped);
@@ -128,19 +194,53 @@ __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ p4, float
     if ((threadIdx.x & 31) == 0 && bad) atomicOr(flags, FLAG_NONUNIT_QUAT);
 }
 
-// Fold this step's densify-statistic deltas into the running sums
-// (train.cpp:433-444) and clear them.
-__global__ void __launch_bounds__(256) fold_stats_kernel(float* __restrict__ gn, float* __restrict__ cnt,
-                                                         float* __restrict__ dgn, float* __restrict__ dcnt, int n) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const float d = dgn[i], c = dcnt[i];
-    if (c != 0.f || d != 0.f) {
-        gn[i] += d;
-        cnt[i] += c;
-        dgn[i] = 0.f;
-        dcnt[i] = 0.f;
+// Every non-quaternion row: block b covers 4*blockDim Gaussians of one row.
+__global__ void __launch_bounds__(256) adam_rows_kernel(AdamPools P, AdamArgs A, const uint8_t* __restrict__ cls_ok3,
+                                                        const uint8_t* __restrict__ cls_ok4, int blocks_per_row3,
+                                                        int blocks_per_row4) {
+    const int R3 = R3_SH + P.K3 - 4, R4 = R4_SH + P.K3 - 8;  // rows without the quaternions
+    int b = blockIdx.x;
+    const bool dyn = b >= R3 * blocks_per_row3;
+    if (dyn) b -= R3 * blocks_per_row3;
+    const int bpr = dyn ? blocks_per_row4 : blocks_per_row3;
+    const int rr = b / bpr;  // compacted row index
+    if (rr >= (dyn ? R4 : R3)) return;
+    const int i0 = ((b % bpr) * blockDim.x + threadIdx.x) * 4;
+    const int n = dyn ? P.n4 : P.n3;
+    if (i0 >= n) return;
+    // compacted row -> pool row, class bit, learning rate (warp-uniform)
+    int row, c;
+    float lr;
+    if (dyn) {
+        row = rr < 4 ? rr : rr + 8;  // skip q_left, q_right (rows 4..11)
+        if (row < R4_MT) c = 0, lr = A.lr_mean;
+        else if (row == R4_MT) c = 1, lr = A.lr_mean_t;
+        else if (row < R4_OP) c = 4, lr = A.lr_scales;
+        else if (row == R4_OP) c = 5, lr = A.lr_opacity;
+        else c = 6, lr = A.lr_sh;
+    } else {
+        row = rr < 3 ? rr : rr + 4;  // skip the quaternion (rows 3..6)
+        if (row < R3_Q) c = 0, lr = A.lr_mean;
+        else if (row < R3_OP) c = 2, lr = A.lr_scales;
+        else if (row == R3_OP) c = 3, lr = A.lr_opacity;
+        else c = 4, lr = A.lr_sh;
     }
+    const int64_t o = (int64_t)row * (dyn ? P.cap4 : P.cap3) + i0;
+    float* p = (dyn ? P.p4 : P.p3) + o;
+    float* g = (dyn ? P.g4 : P.g3) + o;
+    float* m = (dyn ? P.m4 : P.m3) + o;
+    float* v = (dyn ? P.v4 : P.v3) + o;
+    const uchar4 okb = *reinterpret_cast<const uchar4*>((dyn ? cls_ok4 : cls_ok3) + i0);
+    float4 pv = ld4(p), gv = ld4(g), mv = ld4(m), vv = ld4(v);
+    const int nvalid = min(4, n - i0);
+    adam1(pv.x, mv.x, vv.x, gv.x, (okb.x >> c) & 1u, lr, A);
+    if (nvalid > 1) adam1(pv.y, mv.y, vv.y, gv.y, (okb.y >> c) & 1u, lr, A);
+    if (nvalid > 2) adam1(pv.z, mv.z, vv.z, gv.z, (okb.z >> c) & 1u, lr, A);
+    if (nvalid > 3) adam1(pv.w, mv.w, vv.w, gv.w, (okb.w >> c) & 1u, lr, A);
+    st4(p, pv);
+    st4(m, mv);
+    st4(v, vv);
+    st4(g, make_float4(0.f, 0.f, 0.f, 0.f));
 }
 
 }  // namespace hgs

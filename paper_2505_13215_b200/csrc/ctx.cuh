@@ -93,6 +93,7 @@ struct hgs_ctx {
     float *g4 = nullptr, *g3 = nullptr, *dgn4 = nullptr, *dgn3 = nullptr, *dcnt4 = nullptr, *dcnt3 = nullptr;
     int64_t gbuf_floats = 0;
     hgs::DBuf m4, v4, m3, v3;  // Adam moments
+    hgs::DBuf adam_ok;         // per-Gaussian finite-class bitmask (K8, cap3 + cap4 bytes)
     hgs::DBuf gn4, gn3;    // densify grad_norm (float)
     hgs::DBuf cnt4, cnt3;  // densify counts (float, exact below 2^24)
     hgs::DBuf sn4, sn3;    // screen_norm of the last backward (float)

@@ -78,13 +78,17 @@ struct AdamArgs {
     float inv_bc1, inv_bc2;
     float lr_mean, lr_mean_t, lr_quat, lr_scales, lr_opacity, lr_sh;
 };
-__global__ void adam_kernel(float* __restrict__ p4, float* __restrict__ g4, float* __restrict__ m4,
-                            float* __restrict__ v4, int64_t cap4, int n4, float* __restrict__ p3,
-                            float* __restrict__ g3, float* __restrict__ m3, float* __restrict__ v3, int64_t cap3,
-                            int n3, int deg, AdamArgs A, unsigned long long* __restrict__ skipped_total,
-                            uint32_t* __restrict__ flags);
-__global__ void fold_stats_kernel(float* __restrict__ gn, float* __restrict__ cnt, float* __restrict__ dgn,
-                                  float* __restrict__ dcnt, int n);
+struct AdamPools {
+    float *p4, *g4, *m4, *v4, *p3, *g3, *m3, *v3;
+    float *gn4, *cnt4, *dgn4, *dcnt4, *gn3, *cnt3, *dgn3, *dcnt3;
+    int64_t cap4, cap3;
+    int n4, n3, K3;  // K3 = 3 * sh_count(deg)
+};
+__global__ void adam_classes_kernel(AdamPools P, AdamArgs A, uint8_t* __restrict__ cls_ok3,
+                                    uint8_t* __restrict__ cls_ok4, unsigned long long* __restrict__ skipped_total,
+                                    uint32_t* __restrict__ flags);
+__global__ void adam_rows_kernel(AdamPools P, AdamArgs A, const uint8_t* __restrict__ cls_ok3,
+                                 const uint8_t* __restrict__ cls_ok4, int blocks_per_row3, int blocks_per_row4);
 // convert.cu (K9)
 __global__ void convert_mask_kernel(const float* __restrict__ p4, int64_t cap4, int n4, double s_star,
                                     uint32_t* __restrict__ mask);

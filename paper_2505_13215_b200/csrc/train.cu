@@ -192,26 +192,29 @@ hgs_status run_adam(hgs_ctx* ctx, const hgs_lrs* lrs, double mean_lr_scale) {
     A.lr_sh = (float)lrs->sh;
     const int n = (int)(ctx->n4 + ctx->n3);
     Scratch* sc = scratch(ctx);
+    AdamPools P;
+    P.p4 = ctx->p4.as<float>(), P.g4 = ctx->g4, P.m4 = ctx->m4.as<float>(), P.v4 = ctx->v4.as<float>();
+    P.p3 = ctx->p3.as<float>(), P.g3 = ctx->g3, P.m3 = ctx->m3.as<float>(), P.v3 = ctx->v3.as<float>();
+    P.gn4 = ctx->gn4.as<float>(), P.cnt4 = ctx->cnt4.as<float>(), P.dgn4 = ctx->dgn4, P.dcnt4 = ctx->dcnt4;
+    P.gn3 = ctx->gn3.as<float>(), P.cnt3 = ctx->cnt3.as<float>(), P.dgn3 = ctx->dgn3, P.dcnt3 = ctx->dcnt3;
+    P.cap4 = ctx->cap4, P.cap3 = ctx->cap3, P.n4 = (int)ctx->n4, P.n3 = (int)ctx->n3, P.K3 = 3 * sh_count(ctx->deg);
     prof_begin(ctx, PH_ADAM);
     if (n > 0) {
-        adam_kernel<<<div_up(n, 256), 256, 0, st>>>(ctx->p4.as<float>(), ctx->g4, ctx->m4.as<float>(),
-                                                    ctx->v4.as<float>(), ctx->cap4, (int)ctx->n4, ctx->p3.as<float>(),
-                                                    ctx->g3, ctx->m3.as<float>(), ctx->v3.as<float>(), ctx->cap3,
-                                                    (int)ctx->n3, ctx->deg, A, &sc->skipped, &sc->flags);
+        CK(ctx->adam_ok.ensure((size_t)(ctx->cap3 + ctx->cap4)));
+        uint8_t* ok3 = ctx->adam_ok.as<uint8_t>();
+        uint8_t* ok4 = ok3 + ctx->cap3;
+        const uint32_t groups = div_up((uint32_t)ctx->n3, 4) + div_up((uint32_t)ctx->n4, 4);
+        adam_classes_kernel<<<div_up(groups, 128), 128, 0, st>>>(P, A, ok3, ok4, &sc->skipped, &sc->flags);
         count_launch();
         CKL();
-    }
-    if (ctx->n4 > 0) {
-        fold_stats_kernel<<<div_up((uint32_t)ctx->n4, 256), 256, 0, st>>>(ctx->gn4.as<float>(), ctx->cnt4.as<float>(),
-                                                                          ctx->dgn4, ctx->dcnt4, (int)ctx->n4);
-        count_launch();
-        CKL();
-    }
-    if (ctx->n3 > 0) {
-        fold_stats_kernel<<<div_up((uint32_t)ctx->n3, 256), 256, 0, st>>>(ctx->gn3.as<float>(), ctx->cnt3.as<float>(),
-                                                                          ctx->dgn3, ctx->dcnt3, (int)ctx->n3);
-        count_launch();
-        CKL();
+        const int bpr3 = (int)div_up(div_up((uint32_t)ctx->n3, 4), 256), bpr4 = (int)div_up(div_up((uint32_t)ctx->n4, 4), 256);
+        const int R3 = R3_SH + P.K3 - 4, R4 = R4_SH + P.K3 - 8;
+        const int blocks = R3 * bpr3 + R4 * bpr4;
+        if (blocks > 0) {
+            adam_rows_kernel<<<blocks, 256, 0, st>>>(P, A, ok3, ok4, bpr3, bpr4);
+            count_launch();
+            CKL();
+        }
     }
     prof_end(ctx);
     return HGS_OK;
