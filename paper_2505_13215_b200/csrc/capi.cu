@@ -343,11 +343,13 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
         CK(ctx->ntiles_sorted.ensure((size_t)V * 4));
         CK(ctx->inst_off.ensure((size_t)V * 4));
         CK(ctx->sorted_of_gid.ensure((size_t)N * 4));
+        CK(ctx->pcut.ensure((size_t)V * 8));
         prof_begin(ctx, PH_DUPLICATE);
         CK(cudaMemsetAsync(ctx->sorted_of_gid.p, 0xff, (size_t)N * 4, st));
         gather_sorted_kernel<<<div_up((uint32_t)V, 256), 256, 0, st>>>(
             sorted_gid, (int)V, ctx->rec.as<SplatRec>(), ctx->ntiles.as<uint32_t>(), ctx->rec_sorted.as<SplatRec>(),
-            ctx->fast_sorted.as<SplatFast>(), ctx->ntiles_sorted.as<uint32_t>(), ctx->sorted_of_gid.as<uint32_t>());
+            ctx->fast_sorted.as<SplatFast>(), ctx->ntiles_sorted.as<uint32_t>(), ctx->sorted_of_gid.as<uint32_t>(),
+            ctx->pcut.as<double>());
         count_launch();
         CKL();
         CK(ctx->scan_ws.ensure(scan_workspace_bytes((int)V) + 4096));
@@ -369,9 +371,14 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
         CK(ctx->inst_v2.ensure((size_t)I * 4));
         prof_begin(ctx, PH_DUPLICATE);
         const int cull = want_count ? 0 : 1;  // count_map counts every box-covered splat
-        duplicate_kernel<<<div_up((uint32_t)I, 256), 256, 0, st>>>(
+        if (cull) {
+            CK(ctx->inst_flag.ensure((size_t)I * 4));
+            CK(ctx->inst_pos.ensure((size_t)I * 4));
+        }
+        duplicate_kernel<<<div_up((uint32_t)I, kDupPerCtaHost), 256, 0, st>>>(
             ctx->fast_sorted.as<SplatFast>(), ctx->rec_sorted.as<SplatRec>(), (int)V, ctx->inst_off.as<uint32_t>(),
-            tiles_x, cull, ctx->inst_k.as<uint32_t>(), ctx->inst_v.as<uint32_t>(), (int)I);
+            tiles_x, cull, ctx->pcut.as<double>(), ctx->inst_k.as<uint32_t>(), ctx->inst_v.as<uint32_t>(),
+            cull ? ctx->inst_flag.as<uint32_t>() : nullptr, (int)I);
         count_launch();
         CKL();
         prof_end(ctx);
@@ -404,12 +411,7 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
             // instances that can reach the alpha cutoff in their tile), then the
             // stable tile sort of the kept instances only: same relative order as
             // filtering the reference's sorted list, at a third of the sort cost.
-            CK(ctx->inst_flag.ensure((size_t)I * 4));
-            CK(ctx->inst_pos.ensure((size_t)I * 4));
             CK(ctx->scan_ws.ensure(scan_workspace_bytes((int)I) + 4096));
-            keep_flag_kernel<<<div_up((uint32_t)I, 256), 256, 0, st>>>(ctx->inst_v.as<uint32_t>(), (int)I,
-                                                                      ctx->inst_flag.as<uint32_t>());
-            count_launch();
             exclusive_scan_u32(ctx->inst_flag.as<uint32_t>(), ctx->inst_pos.as<uint32_t>(), (int)I, &dc->I_kept,
                                ctx->scan_ws.as<uint32_t>(), st);
             compact_instances_kernel<<<div_up((uint32_t)I, 256), 256, 0, st>>>(
@@ -525,7 +527,7 @@ void hgs_ctx_destroy(hgs_ctx* ctx) {
                     &ctx->sort_v2, &ctx->rec_sorted, &ctx->fast_sorted, &ctx->ntiles_sorted, &ctx->inst_off,
                     &ctx->inst_k, &ctx->inst_v, &ctx->inst_k2, &ctx->inst_v2, &ctx->ranges, &ctx->sorted_of_gid, &ctx->inst_flag, &ctx->inst_pos, &ctx->dbg_k, &ctx->dbg_v, &ctx->scan_ws,
                     &ctx->sort_ws, &ctx->counters, &ctx->img, &ctx->last, &ctx->tfinal, &ctx->trans, &ctx->count,
-                    &ctx->fix_list, &ctx->accum, &ctx->lgrad, &ctx->gt_stage, &ctx->loss_ws, &ctx->stage, &ctx->adam_ok};
+                    &ctx->fix_list, &ctx->accum, &ctx->lgrad, &ctx->gt_stage, &ctx->loss_ws, &ctx->stage, &ctx->adam_ok, &ctx->pcut};
     for (DBuf* b : bufs) b->release();
     ctx->pinned.release();
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);

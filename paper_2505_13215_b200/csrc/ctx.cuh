@@ -102,7 +102,7 @@ struct hgs_ctx {
     // ---- per-render workspace
     hgs::DBuf rec, depth_key, ntiles, visflag, vispos;
     hgs::DBuf sort_k, sort_v, sort_k2, sort_v2;       // depth sort (V)
-    hgs::DBuf rec_sorted, fast_sorted, ntiles_sorted, inst_off, sorted_of_gid;
+    hgs::DBuf rec_sorted, fast_sorted, ntiles_sorted, inst_off, sorted_of_gid, pcut;
     hgs::DBuf inst_k, inst_v, inst_k2, inst_v2;       // tile sort (I)
     hgs::DBuf ranges, scan_ws, sort_ws, inst_flag, inst_pos;
     hgs::DBuf dbg_k, dbg_v;         // the reference's full sorted instance list (debug / count_map)

@@ -103,7 +103,7 @@ __device__ inline void sh_dir_grad_f(const float d[3], int deg, const float w[16
 
 }  // namespace
 
-__global__ void __launch_bounds__(128, 4) gaussian_bwd_kernel(
+__global__ void __launch_bounds__(128, 3) gaussian_bwd_kernel(
     int N, const uint32_t* __restrict__ sorted_of_gid, const float* __restrict__ accum, int acc_stride, int n4,
     const float* __restrict__ p4, int64_t cap4, const float* __restrict__ p3, int64_t cap3, int deg, DevCamera cam,
     double t, double scale, float* __restrict__ g4, float* __restrict__ g3, float* __restrict__ sn4,
@@ -250,20 +250,36 @@ __global__ void __launch_bounds__(128, 4) gaussian_bwd_kernel(
     float drr[3];
     for (int c = 0; c < 3; ++c) drr[c] = (raw[c] < 0.0f || raw[c] > 1.0f) ? 0.0f : (float)d_rgb[c];
     float* G = dyn ? g4 : g3;
-    auto gadd = [&](int row, double val) {
-        float* p = &G[(int64_t)row * cap + i];
-        *p = *p + (float)(scale * val);
-    };
+    // Gradient rows are read-modify-written in batches (all loads of a batch
+    // issued before its stores): the row pointers alias as far as the
+    // compiler knows, so one-at-a-time RMW would serialise ~65 memory
+    // latencies per thread.  Non-SH rows are collected here and flushed last.
+    float gacc[R4_SH];
+#pragma unroll
+    for (int r = 0; r < R4_SH; ++r) gacc[r] = 0.0f;
+    auto gadd = [&](int row, double val) { gacc[row] = (float)(scale * val); };
     float dotc[16];
     const float fs = (float)scale;
-    for (int k = 0; k < K; ++k) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
         float dc = 0.0f;
-        for (int c = 0; c < 3; ++c) {
-            float* p = &G[(int64_t)(shrow + 3 * k + c) * cap + i];
-            *p = fmaf(fs, basis[k] * drr[c], *p);
-            dc = fmaf(drr[c], Pf[(int64_t)(shrow + 3 * k + c) * cap], dc);
-        }
+        if (k < K)
+            for (int c = 0; c < 3; ++c) dc = fmaf(drr[c], Pf[(int64_t)(shrow + 3 * k + c) * cap], dc);
         dotc[k] = dc;
+    }
+    {
+        float* Gs = G + (int64_t)shrow * cap + i;
+#pragma unroll
+        for (int k0 = 0; k0 < 16; k0 += 4) {
+            if (k0 >= K) break;
+            float gv[12];
+#pragma unroll
+            for (int u = 0; u < 12; ++u)
+                if (k0 + u / 3 < K) gv[u] = Gs[(int64_t)(3 * k0 + u) * cap];
+#pragma unroll
+            for (int u = 0; u < 12; ++u)
+                if (k0 + u / 3 < K) Gs[(int64_t)(3 * k0 + u) * cap] = fmaf(fs, basis[k0 + u / 3] * drr[u % 3], gv[u]);
+        }
     }
     double d_dir[3];
     {
@@ -317,6 +333,11 @@ __global__ void __launch_bounds__(128, 4) gaussian_bwd_kernel(
             gn3[i] += (float)screen_norm;
             cnt3[i] += 1.0f;
         }
+        float old[R3_SH];
+#pragma unroll
+        for (int r = 0; r < R3_SH; ++r) old[r] = G[(int64_t)r * cap + i];
+#pragma unroll
+        for (int r = 0; r < R3_SH; ++r) G[(int64_t)r * cap + i] = old[r] + gacc[r];
     } else {
         double d_weight = 0.0;
         if (!clamped) {
@@ -393,6 +414,11 @@ __global__ void __launch_bounds__(128, 4) gaussian_bwd_kernel(
             gn4[i] += (float)screen_norm;
             cnt4[i] += 1.0f;
         }
+        float old[R4_SH];
+#pragma unroll
+        for (int r = 0; r < R4_SH; ++r) old[r] = G[(int64_t)r * cap + i];
+#pragma unroll
+        for (int r = 0; r < R4_SH; ++r) G[(int64_t)r * cap + i] = old[r] + gacc[r];
     }
 }
 

@@ -16,11 +16,12 @@ __global__ void preprocess_kernel(const float* __restrict__ p4, int64_t cap4, in
 __global__ void gather_sorted_kernel(const uint32_t* __restrict__ sorted_gid, int V, const SplatRec* __restrict__ rec,
                                      const uint32_t* __restrict__ ntiles, SplatRec* __restrict__ rec_sorted,
                                      SplatFast* __restrict__ fast_sorted, uint32_t* __restrict__ ntiles_sorted,
-                                     uint32_t* __restrict__ sorted_of_gid);
+                                     uint32_t* __restrict__ sorted_of_gid, double* __restrict__ pcut);
+constexpr int kDupPerCtaHost = 1024;  // instances per duplicate_kernel CTA
 __global__ void duplicate_kernel(const SplatFast* __restrict__ fast, const SplatRec* __restrict__ exact, int V,
                                  const uint32_t* __restrict__ offsets, int tiles_x, int cull,
-                                 uint32_t* __restrict__ keys, uint32_t* __restrict__ vals, int I);
-__global__ void keep_flag_kernel(const uint32_t* __restrict__ vals, int n, uint32_t* __restrict__ flag);
+                                 const double* __restrict__ pcut, uint32_t* __restrict__ keys,
+                                 uint32_t* __restrict__ vals, uint32_t* __restrict__ keep, int I);
 __global__ void compact_instances_kernel(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals, int n,
                                          const uint32_t* __restrict__ pos, uint32_t* __restrict__ keys_out,
                                          uint32_t* __restrict__ vals_out);

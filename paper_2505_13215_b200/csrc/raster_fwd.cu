@@ -16,13 +16,17 @@ __global__ void __launch_bounds__(256) gather_sorted_kernel(const uint32_t* __re
                                                             SplatRec* __restrict__ rec_sorted,
                                                             SplatFast* __restrict__ fast_sorted,
                                                             uint32_t* __restrict__ ntiles_sorted,
-                                                            uint32_t* __restrict__ sorted_of_gid) {
+                                                            uint32_t* __restrict__ sorted_of_gid,
+                                                            double* __restrict__ pcut) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= V) return;
     const uint32_t gid = sorted_gid[j];
     sorted_of_gid[gid] = (uint32_t)j;
     const SplatRec e = rec[gid];
     rec_sorted[j] = e;
+    // tile-culling threshold on the power: alpha * exp(-p) >= 1/255 <=> p <= ln(255 alpha)
+    // (+1e-5 margin, see tile_may_contribute)
+    pcut[j] = log(e.alpha * 255.0) + 1e-5;
     ntiles_sorted[j] = ntiles[gid];
     SplatFast f;
     f.sx_hi = __double2float_rn(e.sx);
@@ -93,54 +97,68 @@ __device__ inline bool tile_may_contribute(const SplatRec& e, double pcut, int x
 }
 
 // Duplicate each sorted splat into every tile its box overlaps
-// (raster.cpp:182-201), one thread per INSTANCE (binary search of the splat
-// in the exclusive tile-count scan) so splats covering hundreds of tiles do
-// not serialise; key = tile id, value = sorted splat index with bit 31 set
-// when the splat cannot reach the alpha cutoff anywhere in that tile.
-__global__ void __launch_bounds__(256) duplicate_kernel(const SplatFast* __restrict__ fast,
-                                                        const SplatRec* __restrict__ exact, int V,
-                                                        const uint32_t* __restrict__ offsets, int tiles_x, int cull,
-                                                        uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
-                                                        int I) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= I) return;
-    int lo = 0, hi = V - 1;  // last j with offsets[j] <= i
-    while (lo < hi) {
+// (raster.cpp:182-201), one thread per INSTANCE so splats covering hundreds of
+// tiles do not serialise.  A CTA covers kDupPerCta consecutive instances: two
+// global binary searches bound its splat range [j_lo, j_hi] (at most
+// kDupPerCta splats, every visible splat owns >= 1 instance), whose offsets
+// are staged in shared memory for the per-instance searches.
+// key = tile id, value = sorted splat index | 4-bit quadrant mask << 28.
+constexpr int kDupThreads = 256, kDupPerCta = kDupPerCtaHost;
+
+__device__ __forceinline__ int last_le(const uint32_t* __restrict__ off, int lo, int hi, uint32_t i) {
+    while (lo < hi) {  // last j in [lo, hi] with off[j] <= i (off[lo] <= i)
         const int mid = (lo + hi + 1) >> 1;
-        if (__ldg(&offsets[mid]) <= (uint32_t)i) lo = mid;
+        if (off[mid] <= i) lo = mid;
         else hi = mid - 1;
     }
-    const int j = lo;
-    const int32_t xr = __ldg(&fast[j].xr), yr = __ldg(&fast[j].yr);
-    const int x0 = box_x0(xr), x1 = x0 + box_w(xr), y0 = box_x0(yr), y1 = y0 + box_w(yr);
-    const int tx0 = x0 / kTile, tx1 = x1 / kTile, ty0 = y0 / kTile;
-    const int local = i - (int)__ldg(&offsets[j]);
-    const int w = tx1 - tx0 + 1;
-    const int ty = ty0 + local / w, tx = tx0 + local % w;
-    // one bit per 8x8 quadrant of the tile (bit q = qy*2 + qx): can the splat
-    // reach the cutoff at a pixel of quadrant q inside its box?  Each quadrant
-    // is one warp of the rasterizers, so the test is warp-uniform there.
-    uint32_t mask = 0xfu;
-    if (cull) {
-        // culling threshold on the power: alpha * exp(-p) >= 1/255  <=>  p <= ln(255 alpha)
-        const SplatRec& e = exact[j];
-        const double pcut = log(e.alpha * 255.0) + 1e-5;
-        mask = 0u;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int qx0 = tx * kTile + (q & 1) * 8, qy0 = ty * kTile + (q >> 1) * 8;
-            const int xa = max(x0, qx0), xb = min(x1, qx0 + 7), ya = max(y0, qy0), yb = min(y1, qy0 + 7);
-            if (xa <= xb && ya <= yb && tile_may_contribute(e, pcut, xa, xb, ya, yb)) mask |= 1u << q;
-        }
-    }
-    keys[i] = (uint32_t)(ty * tiles_x + tx);
-    vals[i] = (uint32_t)j | (mask << kInstMaskShift);
+    return lo;
 }
 
-__global__ void __launch_bounds__(256) keep_flag_kernel(const uint32_t* __restrict__ vals, int n,
-                                                        uint32_t* __restrict__ flag) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) flag[i] = (vals[i] >> kInstMaskShift) ? 1u : 0u;
+__global__ void __launch_bounds__(kDupThreads) duplicate_kernel(const SplatFast* __restrict__ fast,
+                                                                const SplatRec* __restrict__ exact, int V,
+                                                                const uint32_t* __restrict__ offsets, int tiles_x,
+                                                                int cull, const double* __restrict__ pcut_arr,
+                                                                uint32_t* __restrict__ keys,
+                                                                uint32_t* __restrict__ vals,
+                                                                uint32_t* __restrict__ keep, int I) {
+    __shared__ uint32_t s_off[kDupPerCta];
+    __shared__ int s_j[2];
+    const int i0 = blockIdx.x * kDupPerCta;
+    const int i_last = min(i0 + kDupPerCta, I) - 1;
+    if (threadIdx.x < 2) s_j[threadIdx.x] = last_le(offsets, 0, V - 1, (uint32_t)(threadIdx.x ? i_last : i0));
+    __syncthreads();
+    const int j_lo = s_j[0], cnt = s_j[1] - j_lo + 1;
+    for (int k = threadIdx.x; k < cnt; k += kDupThreads) s_off[k] = __ldg(&offsets[j_lo + k]);
+    __syncthreads();
+    for (int i = i0 + threadIdx.x; i <= i_last; i += kDupThreads) {
+        const int jl = last_le(s_off, 0, cnt - 1, (uint32_t)i);
+        const int j = j_lo + jl;
+        const int32_t xr = __ldg(&fast[j].xr), yr = __ldg(&fast[j].yr);
+        const int x0 = box_x0(xr), x1 = x0 + box_w(xr), y0 = box_x0(yr), y1 = y0 + box_w(yr);
+        const int tx0 = x0 / kTile, tx1 = x1 / kTile, ty0 = y0 / kTile;
+        const int local = i - (int)s_off[jl];
+        const int w = tx1 - tx0 + 1;
+        const int ty = ty0 + local / w, tx = tx0 + local % w;
+        // one bit per 8x8 quadrant of the tile (bit q = qy*2 + qx): can the splat
+        // reach the cutoff at a pixel of quadrant q inside its box?  Each quadrant
+        // is one warp of the rasterizers, so the test is warp-uniform there.
+        uint32_t mask = 0xfu;
+        if (cull) {
+            // culling threshold on the power: alpha * exp(-p) >= 1/255  <=>  p <= ln(255 alpha)
+            const SplatRec& e = exact[j];
+            const double pcut = log(e.alpha * 255.0) + 1e-5;
+            mask = 0u;
+    #pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int qx0 = tx * kTile + (q & 1) * 8, qy0 = ty * kTile + (q >> 1) * 8;
+                const int xa = max(x0, qx0), xb = min(x1, qx0 + 7), ya = max(y0, qy0), yb = min(y1, qy0 + 7);
+                if (xa <= xb && ya <= yb && tile_may_contribute(e, pcut, xa, xb, ya, yb)) mask |= 1u << q;
+            }
+        }
+        keys[i] = (uint32_t)(ty * tiles_x + tx);
+        vals[i] = (uint32_t)j | (mask << kInstMaskShift);
+        if (keep) keep[i] = mask ? 1u : 0u;
+    }
 }
 
 // Stable compaction of the tile-sorted instances that can contribute.
