@@ -10,11 +10,11 @@
 //
 // Two passes, both over coalesced SoA rows with float4 (four Gaussians per
 // thread; capacities are multiples of 128):
-//   adam_classes_kernel  one thread per 4 Gaussians: reads every gradient
-//                        row once, writes a per-Gaussian bitmask of finite
-//                        classes, fully updates + renormalises the quaternion
-//                        classes (their 4 rows belong together), folds the
-//                        densification-statistic deltas;
+//   adam_classes_kernel  one thread per (class, 4 Gaussians): reads the
+//                        class's gradient rows once, writes a finite flag per
+//                        (class, Gaussian), fully updates + renormalises the
+//                        quaternion classes (their 4 rows belong together),
+//                        folds the densification-statistic deltas;
 //   adam_rows_kernel     one thread per (row, 4 Gaussians) of every other
 //                        row: p, m, v read+write, grad read+zero = 32 B per
 //                        element at full memory-level parallelism.  HBM bound.
@@ -101,13 +101,16 @@ __global__ void __launch_bounds__(128) adam_classes_kernel(AdamPools P, AdamArgs
                                                            uint8_t* __restrict__ cls_ok4,
                                                            unsigned long long* __restrict__ skipped_total,
                                                            uint32_t* __restrict__ flags) {
+    // one thread per (parameter class, 4 consecutive Gaussians); 3D units first
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     const int q3 = (P.n3 + 3) >> 2, q4 = (P.n4 + 3) >> 2;
     uint32_t skipped = 0;
     bool ok = true;
-    if (t < q3 + q4) {
-        const bool dyn = t >= q3;
-        const int i0 = (dyn ? t - q3 : t) * 4;
+    if (t < 5 * q3 + 7 * q4) {
+        const bool dyn = t >= 5 * q3;
+        const int u = dyn ? t - 5 * q3 : t;
+        const int q = dyn ? q4 : q3;
+        const int c = u / q, i0 = (u % q) * 4;
         const int n = dyn ? P.n4 : P.n3;
         const int64_t cap = dyn ? P.cap4 : P.cap3;
         float* p = dyn ? P.p4 : P.p3;
@@ -116,75 +119,71 @@ __global__ void __launch_bounds__(128) adam_classes_kernel(AdamPools P, AdamArgs
         float* v = dyn ? P.v4 : P.v3;
         const PoolLayout L = layout(dyn, P.K3);
         const int nvalid = min(4, n - i0);
-        uint32_t okm[4] = {0u, 0u, 0u, 0u};
-        for (int c = 0; c < L.n_cls; ++c) {
-            bool f[4] = {true, true, true, true};
-#pragma unroll 4
-            for (int k = 0; k < L.d[c]; ++k) {
-                const float4 gv = __ldg(reinterpret_cast<const float4*>(g + (int64_t)(L.r0[c] + k) * cap + i0));
-                f[0] &= fin(gv.x);
-                f[1] &= fin(gv.y);
-                f[2] &= fin(gv.z);
-                f[3] &= fin(gv.w);
-            }
-            for (int u = 0; u < 4; ++u) {
-                okm[u] |= (f[u] ? 1u : 0u) << c;
-                if (u < nvalid && !f[u]) ++skipped;
-            }
-            if (!L.quat[c]) continue;
+        const int r0 = L.r0[c], d = L.d[c];
+        bool f[4] = {true, true, true, true};
+#pragma unroll 16
+        for (int k = 0; k < d; ++k) {
+            const float4 gv = __ldg(reinterpret_cast<const float4*>(g + (int64_t)(r0 + k) * cap + i0));
+            f[0] &= fin(gv.x);
+            f[1] &= fin(gv.y);
+            f[2] &= fin(gv.z);
+            f[3] &= fin(gv.w);
+        }
+        for (int w = 0; w < nvalid; ++w)
+            if (!f[w]) ++skipped;
+        uint8_t* out = (dyn ? cls_ok4 : cls_ok3) + (int64_t)c * cap + i0;
+        *reinterpret_cast<uchar4*>(out) = make_uchar4(f[0], f[1], f[2], f[3]);
+        if (L.quat[c]) {
             // quaternion class: update, renormalise (even if skipped), zero its gradient
             float4 pr[4], mr[4], vr[4], gr[4];
             for (int k = 0; k < 4; ++k) {
-                const int64_t o = (int64_t)(L.r0[c] + k) * cap + i0;
+                const int64_t o = (int64_t)(r0 + k) * cap + i0;
                 pr[k] = ld4(p + o);
                 mr[k] = ld4(m + o);
                 vr[k] = ld4(v + o);
                 gr[k] = ld4(g + o);
             }
-            float lr = A.lr_quat;
-            for (int u = 0; u < nvalid; ++u) {
-                float q[4], mq[4], vq[4];
+            for (int w = 0; w < nvalid; ++w) {
+                float qv[4], mq[4], vq[4];
                 for (int k = 0; k < 4; ++k) {
-                    q[k] = comp(pr[k], u);
-                    mq[k] = comp(mr[k], u);
-                    vq[k] = comp(vr[k], u);
-                    adam1(q[k], mq[k], vq[k], comp(gr[k], u), f[u], lr, A);
+                    qv[k] = comp(pr[k], w);
+                    mq[k] = comp(mr[k], w);
+                    vq[k] = comp(vr[k], w);
+                    adam1(qv[k], mq[k], vq[k], comp(gr[k], w), f[w], A.lr_quat, A);
                 }
-                ok &= renorm_quat(q, mq);
+                ok &= renorm_quat(qv, mq);
                 for (int k = 0; k < 4; ++k) {
-                    float* pp = &pr[k].x;
-                    float* mm = &mr[k].x;
-                    float* vv = &vr[k].x;
-                    pp[u] = q[k];
-                    mm[u] = mq[k];
-                    vv[u] = vq[k];
+                    (&pr[k].x)[w] = qv[k];
+                    (&mr[k].x)[w] = mq[k];
+                    (&vr[k].x)[w] = vq[k];
                 }
             }
             for (int k = 0; k < 4; ++k) {
-                const int64_t o = (int64_t)(L.r0[c] + k) * cap + i0;
+                const int64_t o = (int64_t)(r0 + k) * cap + i0;
                 st4(p + o, pr[k]);
                 st4(m + o, mr[k]);
                 st4(v + o, vr[k]);
                 st4(g + o, make_float4(0.f, 0.f, 0.f, 0.f));
             }
         }
-        uint8_t* out = dyn ? cls_ok4 : cls_ok3;
-        *reinterpret_cast<uchar4*>(out + i0) = make_uchar4(okm[0], okm[1], okm[2], okm[3]);
-        // fold this step's densification-statistic deltas (train.cpp:433-444)
-        float* gn = dyn ? P.gn4 : P.gn3;
-        float* cnt = dyn ? P.cnt4 : P.cnt3;
-        float* dgn = dyn ? P.dgn4 : P.dgn3;
-        float* dcnt = dyn ? P.dcnt4 : P.dcnt3;
-        const float4 d = *reinterpret_cast<const float4*>(dgn + i0), dc = *reinterpret_cast<const float4*>(dcnt + i0);
-        if (d.x != 0.f || d.y != 0.f || d.z != 0.f || d.w != 0.f || dc.x != 0.f || dc.y != 0.f || dc.z != 0.f ||
-            dc.w != 0.f) {
-            float4 a = *reinterpret_cast<float4*>(gn + i0), b = *reinterpret_cast<float4*>(cnt + i0);
-            a.x += d.x, a.y += d.y, a.z += d.z, a.w += d.w;
-            b.x += dc.x, b.y += dc.y, b.z += dc.z, b.w += dc.w;
-            *reinterpret_cast<float4*>(gn + i0) = a;
-            *reinterpret_cast<float4*>(cnt + i0) = b;
-            *reinterpret_cast<float4*>(dgn + i0) = make_float4(0.f, 0.f, 0.f, 0.f);
-            *reinterpret_cast<float4*>(dcnt + i0) = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (c == 0) {
+            // fold this step's densification-statistic deltas (train.cpp:433-444)
+            float* gn = dyn ? P.gn4 : P.gn3;
+            float* cnt = dyn ? P.cnt4 : P.cnt3;
+            float* dgn = dyn ? P.dgn4 : P.dgn3;
+            float* dcnt = dyn ? P.dcnt4 : P.dcnt3;
+            const float4 dg = *reinterpret_cast<const float4*>(dgn + i0);
+            const float4 dc = *reinterpret_cast<const float4*>(dcnt + i0);
+            if (dg.x != 0.f || dg.y != 0.f || dg.z != 0.f || dg.w != 0.f || dc.x != 0.f || dc.y != 0.f ||
+                dc.z != 0.f || dc.w != 0.f) {
+                float4 a = *reinterpret_cast<float4*>(gn + i0), b = *reinterpret_cast<float4*>(cnt + i0);
+                a.x += dg.x, a.y += dg.y, a.z += dg.z, a.w += dg.w;
+                b.x += dc.x, b.y += dc.y, b.z += dc.z, b.w += dc.w;
+                *reinterpret_cast<float4*>(gn + i0) = a;
+                *reinterpret_cast<float4*>(cnt + i0) = b;
+                *reinterpret_cast<float4*>(dgn + i0) = make_float4(0.f, 0.f, 0.f, 0.f);
+                *reinterpret_cast<float4*>(dcnt + i0) = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
         }
     }
     const unsigned full = 0xffffffffu;
@@ -230,13 +229,14 @@ __global__ void __launch_bounds__(256) adam_rows_kernel(AdamPools P, AdamArgs A,
     float* g = (dyn ? P.g4 : P.g3) + o;
     float* m = (dyn ? P.m4 : P.m3) + o;
     float* v = (dyn ? P.v4 : P.v3) + o;
-    const uchar4 okb = *reinterpret_cast<const uchar4*>((dyn ? cls_ok4 : cls_ok3) + i0);
+    const uchar4 okb =
+        *reinterpret_cast<const uchar4*>((dyn ? cls_ok4 : cls_ok3) + (int64_t)c * (dyn ? P.cap4 : P.cap3) + i0);
     float4 pv = ld4(p), gv = ld4(g), mv = ld4(m), vv = ld4(v);
     const int nvalid = min(4, n - i0);
-    adam1(pv.x, mv.x, vv.x, gv.x, (okb.x >> c) & 1u, lr, A);
-    if (nvalid > 1) adam1(pv.y, mv.y, vv.y, gv.y, (okb.y >> c) & 1u, lr, A);
-    if (nvalid > 2) adam1(pv.z, mv.z, vv.z, gv.z, (okb.z >> c) & 1u, lr, A);
-    if (nvalid > 3) adam1(pv.w, mv.w, vv.w, gv.w, (okb.w >> c) & 1u, lr, A);
+    adam1(pv.x, mv.x, vv.x, gv.x, okb.x, lr, A);
+    if (nvalid > 1) adam1(pv.y, mv.y, vv.y, gv.y, okb.y, lr, A);
+    if (nvalid > 2) adam1(pv.z, mv.z, vv.z, gv.z, okb.z, lr, A);
+    if (nvalid > 3) adam1(pv.w, mv.w, vv.w, gv.w, okb.w, lr, A);
     st4(p, pv);
     st4(m, mv);
     st4(v, vv);

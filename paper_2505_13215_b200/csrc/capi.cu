@@ -375,10 +375,15 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
             CK(ctx->inst_flag.ensure((size_t)I * 4));
             CK(ctx->inst_pos.ensure((size_t)I * 4));
         }
-        duplicate_kernel<<<div_up((uint32_t)I, kDupPerCtaHost), 256, 0, st>>>(
+        const uint32_t dup_blocks = div_up((uint32_t)I, kDupPerCtaHost);
+        CK(ctx->dup_first.ensure((size_t)dup_blocks * 4));
+        dup_bounds_kernel<<<div_up((uint32_t)V, 256), 256, 0, st>>>(
+            ctx->inst_off.as<uint32_t>(), ctx->ntiles_sorted.as<uint32_t>(), (int)V, ctx->dup_first.as<uint32_t>());
+        count_launch();
+        duplicate_kernel<<<dup_blocks, 256, 0, st>>>(
             ctx->fast_sorted.as<SplatFast>(), ctx->rec_sorted.as<SplatRec>(), (int)V, ctx->inst_off.as<uint32_t>(),
             tiles_x, cull, ctx->pcut.as<double>(), ctx->inst_k.as<uint32_t>(), ctx->inst_v.as<uint32_t>(),
-            cull ? ctx->inst_flag.as<uint32_t>() : nullptr, (int)I);
+            cull ? ctx->inst_flag.as<uint32_t>() : nullptr, ctx->dup_first.as<uint32_t>(), (int)I);
         count_launch();
         CKL();
         prof_end(ctx);
@@ -527,7 +532,7 @@ void hgs_ctx_destroy(hgs_ctx* ctx) {
                     &ctx->sort_v2, &ctx->rec_sorted, &ctx->fast_sorted, &ctx->ntiles_sorted, &ctx->inst_off,
                     &ctx->inst_k, &ctx->inst_v, &ctx->inst_k2, &ctx->inst_v2, &ctx->ranges, &ctx->sorted_of_gid, &ctx->inst_flag, &ctx->inst_pos, &ctx->dbg_k, &ctx->dbg_v, &ctx->scan_ws,
                     &ctx->sort_ws, &ctx->counters, &ctx->img, &ctx->last, &ctx->tfinal, &ctx->trans, &ctx->count,
-                    &ctx->fix_list, &ctx->accum, &ctx->lgrad, &ctx->gt_stage, &ctx->loss_ws, &ctx->stage, &ctx->adam_ok, &ctx->pcut};
+                    &ctx->fix_list, &ctx->accum, &ctx->lgrad, &ctx->gt_stage, &ctx->loss_ws, &ctx->stage, &ctx->adam_ok, &ctx->pcut, &ctx->dup_first};
     for (DBuf* b : bufs) b->release();
     ctx->pinned.release();
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);

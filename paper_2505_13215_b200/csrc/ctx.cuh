@@ -93,7 +93,7 @@ struct hgs_ctx {
     float *g4 = nullptr, *g3 = nullptr, *dgn4 = nullptr, *dgn3 = nullptr, *dcnt4 = nullptr, *dcnt3 = nullptr;
     int64_t gbuf_floats = 0;
     hgs::DBuf m4, v4, m3, v3;  // Adam moments
-    hgs::DBuf adam_ok;         // per-Gaussian finite-class bitmask (K8, cap3 + cap4 bytes)
+    hgs::DBuf adam_ok;         // per-(class, Gaussian) finite flags (K8, 5 cap3 + 7 cap4 bytes)
     hgs::DBuf gn4, gn3;    // densify grad_norm (float)
     hgs::DBuf cnt4, cnt3;  // densify counts (float, exact below 2^24)
     hgs::DBuf sn4, sn3;    // screen_norm of the last backward (float)
@@ -102,7 +102,7 @@ struct hgs_ctx {
     // ---- per-render workspace
     hgs::DBuf rec, depth_key, ntiles, visflag, vispos;
     hgs::DBuf sort_k, sort_v, sort_k2, sort_v2;       // depth sort (V)
-    hgs::DBuf rec_sorted, fast_sorted, ntiles_sorted, inst_off, sorted_of_gid, pcut;
+    hgs::DBuf rec_sorted, fast_sorted, ntiles_sorted, inst_off, sorted_of_gid, pcut, dup_first;
     hgs::DBuf inst_k, inst_v, inst_k2, inst_v2;       // tile sort (I)
     hgs::DBuf ranges, scan_ws, sort_ws, inst_flag, inst_pos;
     hgs::DBuf dbg_k, dbg_v;         // the reference's full sorted instance list (debug / count_map)

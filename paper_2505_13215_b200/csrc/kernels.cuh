@@ -21,7 +21,10 @@ constexpr int kDupPerCtaHost = 1024;  // instances per duplicate_kernel CTA
 __global__ void duplicate_kernel(const SplatFast* __restrict__ fast, const SplatRec* __restrict__ exact, int V,
                                  const uint32_t* __restrict__ offsets, int tiles_x, int cull,
                                  const double* __restrict__ pcut, uint32_t* __restrict__ keys,
-                                 uint32_t* __restrict__ vals, uint32_t* __restrict__ keep, int I);
+                                 uint32_t* __restrict__ vals, uint32_t* __restrict__ keep,
+                                 const uint32_t* __restrict__ cta_first, int I);
+__global__ void dup_bounds_kernel(const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ ntiles_sorted,
+                                  int V, uint32_t* __restrict__ cta_first);
 __global__ void compact_instances_kernel(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals, int n,
                                          const uint32_t* __restrict__ pos, uint32_t* __restrict__ keys_out,
                                          uint32_t* __restrict__ vals_out);

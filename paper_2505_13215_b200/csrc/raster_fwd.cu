@@ -114,20 +114,32 @@ __device__ __forceinline__ int last_le(const uint32_t* __restrict__ off, int lo,
     return lo;
 }
 
+// cta_first[b] = the sorted splat owning instance b * kDupPerCta (each CTA
+// boundary lies in exactly one splat's [offset, offset + ntiles) range).
+__global__ void __launch_bounds__(256) dup_bounds_kernel(const uint32_t* __restrict__ offsets,
+                                                         const uint32_t* __restrict__ ntiles_sorted, int V,
+                                                         uint32_t* __restrict__ cta_first) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= V) return;
+    const uint32_t o = offsets[j], n = ntiles_sorted[j];
+    for (uint32_t b = (o + kDupPerCta - 1) / kDupPerCta; b * kDupPerCta < o + n; ++b) cta_first[b] = (uint32_t)j;
+}
+
 __global__ void __launch_bounds__(kDupThreads) duplicate_kernel(const SplatFast* __restrict__ fast,
                                                                 const SplatRec* __restrict__ exact, int V,
                                                                 const uint32_t* __restrict__ offsets, int tiles_x,
                                                                 int cull, const double* __restrict__ pcut_arr,
                                                                 uint32_t* __restrict__ keys,
                                                                 uint32_t* __restrict__ vals,
-                                                                uint32_t* __restrict__ keep, int I) {
-    __shared__ uint32_t s_off[kDupPerCta];
-    __shared__ int s_j[2];
+                                                                uint32_t* __restrict__ keep,
+                                                                const uint32_t* __restrict__ cta_first, int I) {
+    __shared__ uint32_t s_off[kDupPerCta + 1];
     const int i0 = blockIdx.x * kDupPerCta;
     const int i_last = min(i0 + kDupPerCta, I) - 1;
-    if (threadIdx.x < 2) s_j[threadIdx.x] = last_le(offsets, 0, V - 1, (uint32_t)(threadIdx.x ? i_last : i0));
-    __syncthreads();
-    const int j_lo = s_j[0], cnt = s_j[1] - j_lo + 1;
+    // splats [j_lo, j_hi] cover this CTA's instances (j_hi may own none of them)
+    const int j_lo = (int)cta_first[blockIdx.x];
+    const int j_hi = blockIdx.x + 1 < gridDim.x ? (int)cta_first[blockIdx.x + 1] : V - 1;
+    const int cnt = j_hi - j_lo + 1;
     for (int k = threadIdx.x; k < cnt; k += kDupThreads) s_off[k] = __ldg(&offsets[j_lo + k]);
     __syncthreads();
     for (int i = i0 + threadIdx.x; i <= i_last; i += kDupThreads) {
@@ -146,9 +158,9 @@ __global__ void __launch_bounds__(kDupThreads) duplicate_kernel(const SplatFast*
         if (cull) {
             // culling threshold on the power: alpha * exp(-p) >= 1/255  <=>  p <= ln(255 alpha)
             const SplatRec& e = exact[j];
-            const double pcut = log(e.alpha * 255.0) + 1e-5;
+            const double pcut = pcut_arr[j];
             mask = 0u;
-    #pragma unroll
+#pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const int qx0 = tx * kTile + (q & 1) * 8, qy0 = ty * kTile + (q >> 1) * 8;
                 const int xa = max(x0, qx0), xb = min(x1, qx0 + 7), ya = max(y0, qy0), yb = min(y1, qy0 + 7);

@@ -200,11 +200,11 @@ hgs_status run_adam(hgs_ctx* ctx, const hgs_lrs* lrs, double mean_lr_scale) {
     P.cap4 = ctx->cap4, P.cap3 = ctx->cap3, P.n4 = (int)ctx->n4, P.n3 = (int)ctx->n3, P.K3 = 3 * sh_count(ctx->deg);
     prof_begin(ctx, PH_ADAM);
     if (n > 0) {
-        CK(ctx->adam_ok.ensure((size_t)(ctx->cap3 + ctx->cap4)));
+        CK(ctx->adam_ok.ensure((size_t)(5 * ctx->cap3 + 7 * ctx->cap4)));
         uint8_t* ok3 = ctx->adam_ok.as<uint8_t>();
-        uint8_t* ok4 = ok3 + ctx->cap3;
-        const uint32_t groups = div_up((uint32_t)ctx->n3, 4) + div_up((uint32_t)ctx->n4, 4);
-        adam_classes_kernel<<<div_up(groups, 128), 128, 0, st>>>(P, A, ok3, ok4, &sc->skipped, &sc->flags);
+        uint8_t* ok4 = ok3 + 5 * ctx->cap3;
+        const uint32_t units = 5 * div_up((uint32_t)ctx->n3, 4) + 7 * div_up((uint32_t)ctx->n4, 4);
+        adam_classes_kernel<<<div_up(units, 128), 128, 0, st>>>(P, A, ok3, ok4, &sc->skipped, &sc->flags);
         count_launch();
         CKL();
         const int bpr3 = (int)div_up(div_up((uint32_t)ctx->n3, 4), 256), bpr4 = (int)div_up(div_up((uint32_t)ctx->n4, 4), 256);
