@@ -224,21 +224,21 @@ __global__ void __launch_bounds__(kThreadsB, 8) raster_bwd_kernel(
 }
 
 // FP64 backward of the fix-up pixels (backward.cpp:182-221), one warp per
-// pixel.  Pass 1 recomposites the pixel exactly like raster_fixup_kernel to
-// get C_out; pass 2 walks the same list again: lanes evaluate 32 splats in
-// parallel, the uniform sequential walk hands every contributing lane its
-// T_i and inclusive prefix P_i, and the lanes then emit their gradient
-// contributions with d_a = g.(c T_i - (C_out - P_i)/(1 - a)) (in FP64 the
-// subtraction is exact enough) via global atomics.
+// pixel over 32-splat chunks (exact_chunk).  Pass 0 recomposites the pixel to
+// get C_out; pass 1 walks the list again, forms the inclusive colour prefix
+// P_i with a warp scan, and every contributing lane emits its gradient with
+// d_a = g.(c T_i - (C_out - P_i)/(1 - a)) (in FP64 the subtraction is exact
+// enough) via global atomics, in the accumulator layout of raster_bwd_kernel.
 __global__ void __launch_bounds__(128) raster_bwd_exact_kernel(
     const uint32_t* __restrict__ fix_list, const uint32_t* __restrict__ fix_count, const uint2* __restrict__ ranges,
     const uint32_t* __restrict__ inst_val, const SplatRec* __restrict__ exact, int W, int tiles_x, double bg_r,
     double bg_g, double bg_b, const uint32_t* __restrict__ last_arr, const float* __restrict__ dL_dimg,
     float* __restrict__ accum) {
+    __shared__ double s_om[4][32 * kExactSub];
     const uint32_t n = *fix_count;
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const uint32_t warps = gridDim.x * (blockDim.x >> 5);
-    for (uint32_t q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); q < n; q += warps) {
+    for (uint32_t q = blockIdx.x * (blockDim.x >> 5) + wib; q < n; q += warps) {
         const int pix = (int)fix_list[q];
         const double gp[3] = {dL_dimg[pix * 3], dL_dimg[pix * 3 + 1], dL_dimg[pix * 3 + 2]};
         if (gp[0] == 0.0 && gp[1] == 0.0 && gp[2] == 0.0) continue;
@@ -249,52 +249,51 @@ __global__ void __launch_bounds__(128) raster_bwd_exact_kernel(
         double Cout[3];
         for (int pass = 0; pass < 2; ++pass) {
             double T = 1.0, P[3] = {0.0, 0.0, 0.0};
-            for (uint32_t base = rg.x; base < last; base += 32) {
-                const uint32_t i = base + lane;
-                double a = -1.0, g = 0.0;
-                double rgb[3] = {0.0, 0.0, 0.0};
-                const SplatRec* e = nullptr;
-                if (i < last) {
-                    e = &exact[inst_val[i] & kInstIndexMask];
-                    if (px >= e->x0 && px <= e->x1 && py >= e->y0 && py <= e->y1) {
-                        g = exp(-exact_power(*e, pcx, pcy));
-                        a = __dmul_rn(e->alpha, g);
-                        rgb[0] = e->r;
-                        rgb[1] = e->g;
-                        rgb[2] = e->b;
+            constexpr int S = kExactSub;
+            for (uint32_t base = rg.x; base < last; base += 32 * S) {
+                ExactChunk<S> c;
+                exact_chunk<S>(inst_val, exact, base, last, px, py, pcx, pcy, T, s_om[wib], c);
+#pragma unroll
+                for (int s = 0; s < S; ++s) {
+                    double wc[3] = {0.0, 0.0, 0.0}, w = 0.0;
+                    if (c.contrib[s]) {
+                        w = __dmul_rn(c.a[s], c.Ti[s]);
+                        wc[0] = c.e[s]->r * w;
+                        wc[1] = c.e[s]->g * w;
+                        wc[2] = c.e[s]->b * w;
                     }
-                }
-                const bool mine = a >= kAlphaCutoff;
-                const unsigned cm = __ballot_sync(0xffffffffu, mine);
-                double myT = 0.0, myP[3] = {0.0, 0.0, 0.0};
-                for (int jj = 0; jj < 32; ++jj) {
-                    if (!((cm >> jj) & 1u)) continue;
-                    const double aj = __shfl_sync(0xffffffffu, a, jj);
-                    const double w = aj * T;
-                    for (int c = 0; c < 3; ++c) P[c] += __shfl_sync(0xffffffffu, rgb[c], jj) * w;
-                    if (lane == jj) {
-                        myT = T;
-                        myP[0] = P[0];
-                        myP[1] = P[1];
-                        myP[2] = P[2];
+                    if (pass == 0) {
+                        for (int k = 0; k < 3; ++k) P[k] += warp_sum_d(wc[k]);
+                        continue;
                     }
-                    T *= 1.0 - aj;
+                    // inclusive prefix of this 32-splat slice (list order) on top of the running P
+                    double inc[3] = {wc[0], wc[1], wc[2]};
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1)
+                        for (int k = 0; k < 3; ++k) {
+                            const double u = __shfl_up_sync(0xffffffffu, inc[k], o);
+                            if (lane >= o) inc[k] += u;
+                        }
+                    if (c.contrib[s]) {
+                        const SplatRec* e = c.e[s];
+                        const double rgb[3] = {e->r, e->g, e->b};
+                        double d_a = 0.0;
+                        for (int k = 0; k < 3; ++k)
+                            d_a += gp[k] * (rgb[k] * c.Ti[s] - (Cout[k] - (P[k] + inc[k])) / (1.0 - c.a[s]));
+                        float* dst = accum + (size_t)(e - exact) * kAccStride;
+                        for (int k = 0; k < 3; ++k) atomicAdd(dst + k, (float)(w * gp[k]));
+                        const double h = c.g[s] * d_a;
+                        const double dx = pcx - e->sx, dy = pcy - e->sy;
+                        atomicAdd(dst + 3, (float)h);
+                        atomicAdd(dst + 4, (float)(h * dx));
+                        atomicAdd(dst + 5, (float)(h * dy));
+                        atomicAdd(dst + 6, (float)(h * dx * dx));
+                        atomicAdd(dst + 7, (float)(h * dx * dy));
+                        atomicAdd(dst + 8, (float)(h * dy * dy));
+                    }
+                    for (int k = 0; k < 3; ++k) P[k] += __shfl_sync(0xffffffffu, inc[k], 31);
                 }
-                if (pass == 1 && mine) {
-                    double d_a = 0.0;
-                    for (int c = 0; c < 3; ++c) d_a += gp[c] * (rgb[c] * myT - (Cout[c] - myP[c]) / (1.0 - a));
-                    float* dst = accum + (size_t)(inst_val[i] & kInstIndexMask) * kAccStride;
-                    const double w = a * myT;
-                    for (int c = 0; c < 3; ++c) atomicAdd(dst + c, (float)(w * gp[c]));
-                    const double h = g * d_a;
-                    const double dx = pcx - e->sx, dy = pcy - e->sy;
-                    atomicAdd(dst + 3, (float)h);
-                    atomicAdd(dst + 4, (float)(h * dx));
-                    atomicAdd(dst + 5, (float)(h * dy));
-                    atomicAdd(dst + 6, (float)(h * dx * dx));
-                    atomicAdd(dst + 7, (float)(h * dx * dy));
-                    atomicAdd(dst + 8, (float)(h * dy * dy));
-                }
+                if (c.term >= 0) break;
             }
             if (pass == 0) {
                 Cout[0] = P[0] + T * bg_r;

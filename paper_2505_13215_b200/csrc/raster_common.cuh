@@ -22,7 +22,8 @@
 namespace hgs {
 
 constexpr float kLog2e = 1.4426950408889634f;
-constexpr float kAlphaErr0 = 4.0e-7f;  // ex2.approx (2^-22) + alpha_f and product roundings
+constexpr float kAlphaErr0 = 4.0e-7f;
+constexpr int kExactSub = 4;  // 32-splat slices per fix-up chunk  // ex2.approx (2^-22) + alpha_f and product roundings
 constexpr double kLog2eD = 1.4426950408889634;
 
 // 64-byte FP32 view of a sorted splat, stored as four 16-byte vectors so the
@@ -132,6 +133,91 @@ __host__ __device__ inline void cutoff_thresholds(double alpha_f, double eps, fl
     const double cut = 1.0 / 255.0;
     x_skip = (float)(log2(alpha_f / (cut * (1.0 - 2.0 * eps))));
     x_keep = (float)(log2(alpha_f / (cut * (1.0 + 2.0 * eps))));
+}
+
+// ---- exact (FP64) per-pixel walk: one warp per pixel (fix-up kernels)
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// One chunk [base, base + 32*S) of the oracle's per-pixel loop
+// (raster.cpp:130-147, backward.cpp:182-203); lane l owns the splats
+// base + 32 s + l (s < S), whose records it loads together (memory-level
+// parallelism: the fix-up pixels are few, so their walk is latency bound).
+// Every lane evaluates its splats (box test + FP64 alpha, bit-identical to
+// the oracle); the transmittance chain T <- T * (1 - a) then runs in list
+// order as a branch-free run of dependent DMULs over factors staged in shared
+// memory (factor 1.0 -- exact -- for the splats the oracle skips), and the
+// walk stops after the first contributing splat that takes T below 1e-4,
+// exactly where the oracle breaks.  Each contributing lane receives the
+// transmittance in front of its splat; colours and gradients are then formed
+// lane-parallel.
+template <int S>
+struct ExactChunk {
+    const SplatRec* e[S];  // the lane's splats (valid when inb)
+    double a[S], g[S];     // alpha and exp(-power) (a < 0: outside the box)
+    double Ti[S];          // transmittance in front of the splat (when contrib)
+    bool inb[S], contrib[S];
+    uint32_t inmask[S];    // ballots of inb
+    int term;              // chunk index (32 s + lane) of the terminating splat, -1 if none
+};
+
+template <int S>
+__device__ __forceinline__ void exact_chunk(const uint32_t* __restrict__ inst_val, const SplatRec* __restrict__ exact,
+                                            uint32_t base, uint32_t end, int px, int py, double pcx, double pcy,
+                                            double& T, double* s_om, ExactChunk<S>& c) {
+    const int lane = threadIdx.x & 31;
+    uint32_t v[S];
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        const uint32_t i = base + 32 * s + lane;
+        v[s] = i < end ? inst_val[i] : 0xffffffffu;
+    }
+    double om[S];
+    bool ok[S];
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        c.e[s] = v[s] != 0xffffffffu ? exact + (v[s] & kInstIndexMask) : nullptr;
+        c.a[s] = -1.0;
+        c.g[s] = 0.0;
+        c.Ti[s] = 0.0;
+        c.inb[s] = c.e[s] && px >= c.e[s]->x0 && px <= c.e[s]->x1 && py >= c.e[s]->y0 && py <= c.e[s]->y1;
+        if (c.inb[s]) {
+            c.g[s] = exp(-exact_power(*c.e[s], pcx, pcy));
+            c.a[s] = __dmul_rn(c.e[s]->alpha, c.g[s]);
+        }
+        ok[s] = c.a[s] >= kAlphaCutoff;
+        c.inmask[s] = __ballot_sync(0xffffffffu, c.inb[s]);
+        om[s] = ok[s] ? __dsub_rn(1.0, c.a[s]) : 1.0;
+        s_om[32 * s + lane] = om[s];
+    }
+    __syncwarp();
+    double Tl = T;
+#pragma unroll
+    for (int s = 0; s < S; ++s)
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            if (lane == j) c.Ti[s] = Tl;
+            Tl = __dmul_rn(Tl, s_om[32 * s + j]);
+        }
+    __syncwarp();  // s_om is rewritten by the next chunk
+    c.term = -1;
+    double Tt = Tl;
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        const double Tafter = __dmul_rn(c.Ti[s], om[s]);
+        const uint32_t tm = __ballot_sync(0xffffffffu, ok[s] && Tafter < kTransFloor);
+        if (tm && c.term < 0) {
+            c.term = 32 * s + __ffs(tm) - 1;
+            Tt = __shfl_sync(0xffffffffu, Tafter, __ffs(tm) - 1);
+        }
+    }
+    T = Tt;
+#pragma unroll
+    for (int s = 0; s < S; ++s) c.contrib[s] = ok[s] && (c.term < 0 || 32 * s + lane <= c.term);
 }
 
 }  // namespace hgs

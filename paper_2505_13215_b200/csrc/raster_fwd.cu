@@ -345,59 +345,48 @@ __global__ void __launch_bounds__(kThreads, 8) raster_fwd_kernel(
 }
 
 // Exact FP64 recomposite of the flagged pixels (raster.cpp:123-148), one warp
-// per pixel: the 32 lanes evaluate 32 consecutive splats' box test and FP64
-// alpha in parallel, then every lane walks them in order (uniform loop) to
-// apply the oracle's sequential transmittance update and break.
+// per pixel over 32-splat chunks (exact_chunk: lane-parallel FP64 alphas, the
+// transmittance chain in list order, colours summed lane-parallel in FP64).
 __global__ void __launch_bounds__(128) raster_fixup_kernel(
     const uint32_t* __restrict__ fix_list, const uint32_t* __restrict__ fix_count, const uint2* __restrict__ ranges,
     const uint32_t* __restrict__ inst_val, const SplatRec* __restrict__ exact, int W, int tiles_x, double bg_r,
     double bg_g, double bg_b, float* __restrict__ out_rgb, uint32_t* __restrict__ out_last,
     float* __restrict__ out_tfinal, float* __restrict__ out_trans, uint32_t* __restrict__ out_count) {
+    __shared__ double s_om[4][32 * kExactSub];
     const uint32_t n = *fix_count;
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const uint32_t warps = gridDim.x * (blockDim.x >> 5);
-    for (uint32_t q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); q < n; q += warps) {
+    for (uint32_t q = blockIdx.x * (blockDim.x >> 5) + wib; q < n; q += warps) {
         const int pix = (int)fix_list[q];
         const int px = pix % W, py = pix / W;
         const uint2 rg = ranges[(py / kTile) * tiles_x + px / kTile];
         const double pcx = px + 0.5, pcy = py + 0.5;
         double T = 1.0, ar = 0.0, ag = 0.0, ab = 0.0;
         uint32_t count = 0, last = rg.x;
-        bool done = false;
-        for (uint32_t base = rg.x; base < rg.y && !done; base += 32) {
-            const uint32_t i = base + lane;
-            bool inb = false;
-            double a = -1.0, r = 0.0, g = 0.0, b = 0.0;
-            if (i < rg.y) {
-                const SplatRec& e = exact[inst_val[i] & kInstIndexMask];
-                inb = px >= e.x0 && px <= e.x1 && py >= e.y0 && py <= e.y1;
-                if (inb) {
-                    a = exact_alpha(e, pcx, pcy);
-                    r = e.r;
-                    g = e.g;
-                    b = e.b;
+        constexpr int S = kExactSub;
+        for (uint32_t base = rg.x; base < rg.y; base += 32 * S) {
+            ExactChunk<S> c;
+            exact_chunk<S>(inst_val, exact, base, rg.y, px, py, pcx, pcy, T, s_om[wib], c);
+            double wr = 0.0, wg = 0.0, wb = 0.0;
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                // in-box splats up to (and including) the terminating one
+                const int tl = c.term - 32 * s;
+                const uint32_t upto = (c.term < 0 || tl >= 31) ? 0xffffffffu : tl < 0 ? 0u : ((2u << tl) - 1u);
+                count += __popc(c.inmask[s] & upto);
+                if (c.contrib[s]) {
+                    const double w = __dmul_rn(c.a[s], c.Ti[s]);
+                    wr += c.e[s]->r * w;
+                    wg += c.e[s]->g * w;
+                    wb += c.e[s]->b * w;
                 }
+                const uint32_t cb = __ballot_sync(0xffffffffu, c.contrib[s]);
+                if (cb) last = base + 32 * s + (31 - __clz(cb)) + 1;
             }
-            const unsigned inmask = __ballot_sync(0xffffffffu, inb);
-            const int cnt = (int)min(32u, rg.y - base);
-            for (int jj = 0; jj < cnt; ++jj) {
-                if (!((inmask >> jj) & 1u)) continue;
-                ++count;
-                const double aj = __shfl_sync(0xffffffffu, a, jj);
-                if (aj < kAlphaCutoff) continue;
-                const double rj = __shfl_sync(0xffffffffu, r, jj), gj = __shfl_sync(0xffffffffu, g, jj),
-                             bj = __shfl_sync(0xffffffffu, b, jj);
-                const double w = __dmul_rn(aj, T);
-                ar = __dadd_rn(ar, __dmul_rn(rj, w));
-                ag = __dadd_rn(ag, __dmul_rn(gj, w));
-                ab = __dadd_rn(ab, __dmul_rn(bj, w));
-                T = __dmul_rn(T, __dsub_rn(1.0, aj));
-                last = base + jj + 1;
-                if (T < kTransFloor) {
-                    done = true;
-                    break;
-                }
-            }
+            ar += warp_sum_d(wr);
+            ag += warp_sum_d(wg);
+            ab += warp_sum_d(wb);
+            if (c.term >= 0) break;
         }
         if (lane == 0) {
             out_rgb[pix * 3 + 0] = (float)__dadd_rn(ar, __dmul_rn(T, bg_r));
