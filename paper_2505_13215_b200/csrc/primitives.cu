@@ -6,256 +6,270 @@
 // sorted once by f32 depth bits (4 x 8-bit passes) and then by tile id
 // (ceil(bits/8) passes); stability carries the index tie-break through both.
 //
-// Each pass = per-block digit histogram (shared-memory atomics), one
-// exclusive scan of the digit-major histogram, and a scatter that ranks
-// items stably inside each warp with __match_any_sync + per-warp counters.
+// Both are ONE cooperative launch (persistent grid, co-resident by
+// construction, grid-wide barriers between phases) so a whole sort or scan
+// costs one launch instead of 3-5 per pass: every block owns one contiguous,
+// ordered chunk of the items.
+//   scan:  block sums | barrier | prefix of the preceding block sums + block
+//          scans of the chunk in 4096-item tiles.
+//   sort pass: chunk digit histogram -> [digit][block] | barrier | exclusive
+//          scan of each digit row over the blocks (one block per digit) |
+//          barrier | digit bases + stable scatter of the chunk in 4096-item
+//          tiles (in-warp ranks via __match_any_sync, per-warp counters) |
+//          barrier.
+// The item count may come from device memory (n_dev) so the pipeline needs
+// no host round trip to size a sort.
+#include <cooperative_groups.h>
+#include <algorithm>
 #include <cstdio>
 
 #include "primitives.cuh"
 
 namespace hgs {
 
+namespace cg = cooperative_groups;
+
 namespace {
 
-constexpr int kScanThreads = 256;
-constexpr int kScanItems = 16;
-constexpr int kScanTile = kScanThreads * kScanItems;  // 2048
+constexpr int kCoopThreads = 256;
+constexpr int kItems = 16;
+constexpr int kTileItems = kCoopThreads * kItems;  // 4096
+constexpr int kWarps = kCoopThreads / 32;
 
-__device__ inline uint32_t warp_incl_scan(uint32_t v) {
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
     const int lane = threadIdx.x & 31;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-        uint32_t n = __shfl_up_sync(0xffffffffu, v, o);
-        if (lane >= o) v += n;
+        const uint32_t t = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += t;
     }
     return v;
 }
 
-// Block-wide exclusive scan of one value per thread.
-template <int NT>
-__device__ inline void block_excl_scan(uint32_t v, uint32_t& excl) {
-    __shared__ uint32_t warp_tot[NT / 32];
+// Exclusive scan of one value per thread over a 256-thread block; also
+// returns the block total.  Ends with a barrier (shared scratch reusable).
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t& total) {
+    __shared__ uint32_t wt[kWarps + 1];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t incl = warp_incl_scan(v);
-    if (lane == 31) warp_tot[warp] = incl;
+    const uint32_t incl = warp_incl_scan(v);
+    if (lane == 31) wt[warp] = incl;
     __syncthreads();
     if (warp == 0) {
-        uint32_t w = lane < NT / 32 ? warp_tot[lane] : 0u;
-        uint32_t wi = warp_incl_scan(w);
-        if (lane < NT / 32) warp_tot[lane] = wi - w;
+        const uint32_t w = lane < kWarps ? wt[lane] : 0u;
+        const uint32_t wi = warp_incl_scan(w);
+        if (lane < kWarps) wt[lane] = wi - w;
+        if (lane == kWarps - 1) wt[kWarps] = wi;
     }
     __syncthreads();
-    excl = incl - v + warp_tot[warp];
+    const uint32_t ex = incl - v + wt[warp];
+    total = wt[kWarps];
     __syncthreads();
+    return ex;
 }
 
-__global__ void __launch_bounds__(kScanThreads) scan_reduce_kernel(const uint32_t* __restrict__ in, int n,
-                                                                   uint32_t* __restrict__ block_sums) {
-    const int base = blockIdx.x * kScanTile + threadIdx.x * kScanItems;
+__device__ __forceinline__ uint32_t block_sum(uint32_t v) {
+    uint32_t t;
+    block_excl_scan(v, t);
+    return t;
+}
+
+__global__ void __launch_bounds__(kCoopThreads) scan_coop_kernel(const uint32_t* in, uint32_t* out, int n,
+                                                                 const uint32_t* __restrict__ n_dev,
+                                                                 uint32_t* __restrict__ total,
+                                                                 uint32_t* __restrict__ bsum) {
+    cg::grid_group grid = cg::this_grid();
+    const int G = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
+    if (n_dev) n = (int)*n_dev;
+    const int C = ((n + G - 1) / G + 3) & ~3;
+    const int lo = min(b * C, n), hi = min(lo + C, n);
     uint32_t s = 0;
+    for (int i = lo + tid; i < hi; i += kCoopThreads) s += in[i];
+    s = block_sum(s);
+    if (tid == 0) bsum[b] = s;
+    grid.sync();
+    uint32_t part = 0;
+    for (int c = tid; c < b; c += kCoopThreads) part += bsum[c];
+    uint32_t run = block_sum(part);
+    if (b == G - 1 && tid == 0 && total) *total = run + bsum[b];
+    for (int t0 = lo; t0 < hi; t0 += kTileItems) {
+        const int base = t0 + tid * kItems;
+        uint32_t v[kItems], sum = 0;
 #pragma unroll
-    for (int k = 0; k < kScanItems; ++k) s += (base + k < n) ? in[base + k] : 0u;
-    __shared__ uint32_t red[kScanThreads / 32];
+        for (int k = 0; k < kItems; ++k) {
+            v[k] = base + k < hi ? in[base + k] : 0u;
+            sum += v[k];
+        }
+        uint32_t tot;
+        uint32_t r = run + block_excl_scan(sum, tot);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        uint32_t t = 0;
-        for (int w = 0; w < kScanThreads / 32; ++w) t += red[w];
-        block_sums[blockIdx.x] = t;
+        for (int k = 0; k < kItems; ++k) {
+            if (base + k < hi) out[base + k] = r;
+            r += v[k];
+        }
+        run += tot;
     }
 }
 
-// Single-block exclusive scan of up to 1024*kScanItems values, in place.
-__global__ void __launch_bounds__(1024) scan_single_kernel(uint32_t* __restrict__ data, int n,
-                                                           uint32_t* __restrict__ total) {
-    const int base = threadIdx.x * kScanItems;
-    uint32_t v[kScanItems];
-    uint32_t s = 0;
-#pragma unroll
-    for (int k = 0; k < kScanItems; ++k) {
-        v[k] = (base + k < n) ? data[base + k] : 0u;
-        s += v[k];
-    }
-    uint32_t excl;
-    block_excl_scan<1024>(s, excl);
-    uint32_t run = excl;
-#pragma unroll
-    for (int k = 0; k < kScanItems; ++k) {
-        if (base + k < n) data[base + k] = run;
-        run += v[k];
-    }
-    if (threadIdx.x == 1023 && total) *total = excl + s;
-}
+struct CoopSort {
+    uint32_t *k0, *v0, *k1, *v1;
+    const uint32_t* n_dev;
+    int n, shift0, npasses;
+    uint32_t* hist;    // [256][G]
+    uint32_t* rowsum;  // [256]
+};
 
-__global__ void __launch_bounds__(kScanThreads) scan_downsweep_kernel(const uint32_t* __restrict__ in, int n,
-                                                                      const uint32_t* __restrict__ block_off,
-                                                                      uint32_t* __restrict__ out) {
-    const int base = blockIdx.x * kScanTile + threadIdx.x * kScanItems;
-    uint32_t v[kScanItems];
-    uint32_t s = 0;
-#pragma unroll
-    for (int k = 0; k < kScanItems; ++k) {
-        v[k] = (base + k < n) ? in[base + k] : 0u;
-        s += v[k];
-    }
-    uint32_t excl;
-    block_excl_scan<kScanThreads>(s, excl);
-    uint32_t run = excl + block_off[blockIdx.x];
-#pragma unroll
-    for (int k = 0; k < kScanItems; ++k) {
-        if (base + k < n) out[base + k] = run;
-        run += v[k];
-    }
-}
-
-// ---------------------------------------------------------------- radix sort
-constexpr int kSortThreads = 256;
-constexpr int kSortItems = 16;
-constexpr int kSortTile = kSortThreads * kSortItems;  // 4096
-constexpr int kSortWarps = kSortThreads / 32;
-
-__global__ void __launch_bounds__(kSortThreads) radix_hist_kernel(const uint32_t* __restrict__ keys, int n,
-                                                                  int shift, int nblocks,
-                                                                  uint32_t* __restrict__ hist,
-                                                                  const uint32_t* __restrict__ n_dev) {
+__global__ void __launch_bounds__(kCoopThreads) radix_sort_coop_kernel(CoopSort a) {
+    cg::grid_group grid = cg::this_grid();
     __shared__ uint32_t h[256];
-    h[threadIdx.x] = 0;
-    __syncthreads();
-    if (n_dev) n = (int)*n_dev;
-    const int base = blockIdx.x * kSortTile;
-#pragma unroll 4
-    for (int k = 0; k < kSortItems; ++k) {
-        const int idx = base + k * kSortThreads + threadIdx.x;
-        if (idx < n) atomicAdd(&h[(keys[idx] >> shift) & 255u], 1u);
+    __shared__ uint32_t cnt[kWarps][256];
+    __shared__ uint32_t goff[256];
+    const int G = gridDim.x, b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int n = a.n_dev ? (int)*a.n_dev : a.n;
+    const int C = ((n + G - 1) / G + 31) & ~31;
+    const int lo = min(b * C, n), hi = min(lo + C, n);
+    const unsigned lt_mask = (1u << lane) - 1u;
+    uint32_t *ki = a.k0, *vi = a.v0, *ko = a.k1, *vo = a.v1;
+    for (int p = 0; p < a.npasses; ++p) {
+        const int shift = a.shift0 + 8 * p;
+        // 1. digit histogram of this block's chunk
+        h[tid] = 0u;
+        __syncthreads();
+        for (int i = lo + tid; i < hi; i += kCoopThreads) atomicAdd(&h[(ki[i] >> shift) & 255u], 1u);
+        __syncthreads();
+        a.hist[tid * G + b] = h[tid];
+        grid.sync();
+        // 2. exclusive scan of each digit row over the blocks
+        for (int d = b; d < 256; d += G) {
+            uint32_t* row = a.hist + (size_t)d * G;
+            uint32_t run = 0;
+            for (int c0 = 0; c0 < G; c0 += kCoopThreads) {
+                const int c = c0 + tid;
+                const uint32_t x = c < G ? row[c] : 0u;
+                uint32_t tot;
+                const uint32_t ex = block_excl_scan(x, tot);
+                if (c < G) row[c] = run + ex;
+                run += tot;
+            }
+            if (tid == 0) a.rowsum[d] = run;
+        }
+        grid.sync();
+        // 3. global digit bases, then the stable scatter of the chunk
+        {
+            uint32_t tot;
+            const uint32_t base = block_excl_scan(a.rowsum[tid], tot);
+            goff[tid] = base + a.hist[tid * G + b];
+        }
+        for (int t0 = lo; t0 < hi; t0 += kTileItems) {
+            for (int i = tid; i < kWarps * 256; i += kCoopThreads) (&cnt[0][0])[i] = 0u;
+            __syncthreads();
+            const int wbase = t0 + warp * (kItems * 32);
+            uint32_t k[kItems], v[kItems], rank[kItems];
+#pragma unroll
+            for (int r = 0; r < kItems; ++r) {
+                const int idx = wbase + r * 32 + lane;
+                const bool valid = idx < hi;
+                k[r] = valid ? ki[idx] : 0u;
+                v[r] = valid ? vi[idx] : 0u;
+                const uint32_t d = valid ? ((k[r] >> shift) & 255u) : 256u;
+                const unsigned peers = __match_any_sync(0xffffffffu, d);
+                const uint32_t before = valid ? cnt[warp][d] : 0u;
+                __syncwarp();
+                if (valid && lane == __ffs(peers) - 1) cnt[warp][d] = before + __popc(peers);
+                __syncwarp();
+                rank[r] = before + __popc(peers & lt_mask);
+            }
+            __syncthreads();
+            uint32_t tile_tot = 0;
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) {
+                const uint32_t t = cnt[w][tid];
+                cnt[w][tid] = tile_tot;
+                tile_tot += t;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int r = 0; r < kItems; ++r) {
+                const int idx = wbase + r * 32 + lane;
+                if (idx < hi) {
+                    const uint32_t d = (k[r] >> shift) & 255u;
+                    const uint32_t pos = goff[d] + cnt[warp][d] + rank[r];
+                    ko[pos] = k[r];
+                    vo[pos] = v[r];
+                }
+            }
+            __syncthreads();
+            goff[tid] += tile_tot;
+        }
+        grid.sync();
+        uint32_t* t = ki;
+        ki = ko;
+        ko = t;
+        t = vi;
+        vi = vo;
+        vo = t;
     }
-    __syncthreads();
-    hist[threadIdx.x * nblocks + blockIdx.x] = h[threadIdx.x];
 }
 
-__global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(
-    const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals, uint32_t* __restrict__ keys_out,
-    uint32_t* __restrict__ vals_out, int n, int shift, int nblocks, const uint32_t* __restrict__ offsets,
-    const uint32_t* __restrict__ n_dev) {
-    __shared__ uint32_t cnt[kSortWarps][256];
-    __shared__ uint32_t goff[256];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (n_dev) n = (int)*n_dev;
-    if ((int)(blockIdx.x * kSortTile) >= n) return;  // whole block beyond the device-side count
-    for (int i = threadIdx.x; i < kSortWarps * 256; i += kSortThreads) (&cnt[0][0])[i] = 0u;
-    goff[threadIdx.x] = offsets[threadIdx.x * nblocks + blockIdx.x];
-    __syncthreads();
-    const unsigned lt_mask = (1u << lane) - 1u;
-    const int base = blockIdx.x * kSortTile + warp * (kSortItems * 32);
-    uint32_t k[kSortItems], v[kSortItems], rank[kSortItems];
-#pragma unroll
-    for (int r = 0; r < kSortItems; ++r) {
-        const int idx = base + r * 32 + lane;
-        const bool valid = idx < n;
-        k[r] = valid ? keys[idx] : 0u;
-        v[r] = valid ? vals[idx] : 0u;
-        const uint32_t d = valid ? ((k[r] >> shift) & 255u) : 256u;
-        const unsigned peers = __match_any_sync(0xffffffffu, d);
-        const uint32_t before = valid ? cnt[warp][d] : 0u;
-        __syncwarp();
-        if (valid && lane == __ffs(peers) - 1) cnt[warp][d] = before + __popc(peers);
-        __syncwarp();
-        rank[r] = before + __popc(peers & lt_mask);
+// Co-resident grid size of a cooperative kernel on the current device.
+template <typename K>
+int coop_grid(K kernel) {
+    static int cached[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (!cached[dev]) {
+        int per_sm = 0, sms = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kCoopThreads, 0);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cached[dev] = std::max(1, std::min(per_sm, 4)) * sms;
     }
-    __syncthreads();
-    {
-        uint32_t run = 0;
-#pragma unroll
-        for (int w = 0; w < kSortWarps; ++w) {
-            const uint32_t t = cnt[w][threadIdx.x];
-            cnt[w][threadIdx.x] = run;
-            run += t;
-        }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int r = 0; r < kSortItems; ++r) {
-        const int idx = base + r * 32 + lane;
-        if (idx < n) {
-            const uint32_t d = (k[r] >> shift) & 255u;
-            const uint32_t pos = goff[d] + cnt[warp][d] + rank[r];
-            keys_out[pos] = k[r];
-            vals_out[pos] = v[r];
-        }
-    }
+    return cached[dev];
 }
+
+constexpr int kMaxCoopGrid = 4 * 256;  // workspace bound (<= 4 blocks/SM on <= 256 SMs)
 
 }  // namespace
 
-size_t scan_workspace_bytes(int n) {
-    const int nb = (int)div_up((uint32_t)n, kScanTile);
-    return (size_t)(nb + 32) * sizeof(uint32_t);
-}
+size_t scan_workspace_bytes(int) { return (size_t)(kMaxCoopGrid + 32) * sizeof(uint32_t); }
 
-void exclusive_scan_u32(const uint32_t* in, uint32_t* out, int n, uint32_t* total, uint32_t* ws,
-                        cudaStream_t st) {
-    if (n <= 0) {
+void exclusive_scan_u32(const uint32_t* in, uint32_t* out, int n, uint32_t* total, uint32_t* ws, cudaStream_t st,
+                        const uint32_t* n_dev) {
+    if (n <= 0 && !n_dev) {
         if (total) cudaMemsetAsync(total, 0, sizeof(uint32_t), st);
         return;
     }
-    if (n <= 1024 * kScanItems) {  // one CTA: a single launch
-        if (in != out) cudaMemcpyAsync(out, in, (size_t)n * 4, cudaMemcpyDeviceToDevice, st);
-        scan_single_kernel<<<1, 1024, 0, st>>>(out, n, total);
-        count_launch();
-        return;
-    }
-    const int nb = (int)div_up((uint32_t)n, kScanTile);
-    if (nb > 1024 * kScanItems) {
-        fprintf(stderr, "exclusive_scan_u32: n=%d exceeds the single-level capacity\n", n);
-        return;
-    }
-    scan_reduce_kernel<<<nb, kScanThreads, 0, st>>>(in, n, ws);
-    count_launch();
-    scan_single_kernel<<<1, 1024, 0, st>>>(ws, nb, total);
-    count_launch();
-    scan_downsweep_kernel<<<nb, kScanThreads, 0, st>>>(in, n, ws, out);
+    const int G = std::min(coop_grid(scan_coop_kernel), kMaxCoopGrid);
+    void* args[] = {(void*)&in, (void*)&out, (void*)&n, (void*)&n_dev, (void*)&total, (void*)&ws};
+    cudaLaunchCooperativeKernel((void*)scan_coop_kernel, G, kCoopThreads, args, 0, st);
     count_launch();
 }
 
-size_t radix_workspace_bytes(int n) {
-    const int nb = (int)div_up((uint32_t)n, kSortTile);
-    const size_t hist = (size_t)256 * nb;
-    return (hist * 2 + 64) * sizeof(uint32_t) + scan_workspace_bytes((int)hist);
-}
+size_t radix_workspace_bytes(int) { return (size_t)(256 * kMaxCoopGrid + 256 + 64) * sizeof(uint32_t); }
 
 // Stable LSD sort of (keys, vals) on bits [begin_bit, end_bit).  The result
 // lands in (keys, vals) when the pass count is even, else in (keys_alt,
 // vals_alt); the return value says which (0 = original buffers).
 int radix_sort_pairs(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt, int n,
                      int begin_bit, int end_bit, uint32_t* ws, cudaStream_t st, const uint32_t* n_dev) {
-    if (n <= 1 && !n_dev) return 0;
-    if (n < 1) return 0;
-    const int nb = (int)div_up((uint32_t)n, kSortTile);
-    const int hist_n = 256 * nb;
-    uint32_t* hist = ws;
-    uint32_t* offs = ws + hist_n;
-    uint32_t* scan_ws = offs + hist_n + 64;
-    int cur = 0;
-    uint32_t* kin = keys;
-    uint32_t* vin = vals;
-    uint32_t* kout = keys_alt;
-    uint32_t* vout = vals_alt;
-    for (int shift = begin_bit; shift < end_bit; shift += 8) {
-        radix_hist_kernel<<<nb, kSortThreads, 0, st>>>(kin, n, shift, nb, hist, n_dev);
-        count_launch();
-        exclusive_scan_u32(hist, offs, hist_n, nullptr, scan_ws, st);
-        radix_scatter_kernel<<<nb, kSortThreads, 0, st>>>(kin, vin, kout, vout, n, shift, nb, offs, n_dev);
-        count_launch();
-        uint32_t* t = kin;
-        kin = kout;
-        kout = t;
-        t = vin;
-        vin = vout;
-        vout = t;
-        cur ^= 1;
-    }
-    return cur;
+    if (!n_dev && n <= 1) return 0;
+    const int npasses = (end_bit - begin_bit + 7) / 8;
+    if (npasses <= 0) return 0;
+    CoopSort a;
+    a.k0 = keys;
+    a.v0 = vals;
+    a.k1 = keys_alt;
+    a.v1 = vals_alt;
+    a.n_dev = n_dev;
+    a.n = n;
+    a.shift0 = begin_bit;
+    a.npasses = npasses;
+    a.hist = ws;
+    a.rowsum = ws + 256 * kMaxCoopGrid;
+    const int G = std::min(coop_grid(radix_sort_coop_kernel), kMaxCoopGrid);
+    void* args[] = {(void*)&a};
+    cudaLaunchCooperativeKernel((void*)radix_sort_coop_kernel, G, kCoopThreads, args, 0, st);
+    count_launch();
+    return npasses & 1;
 }
 
 }  // namespace hgs

@@ -10,11 +10,12 @@ namespace hgs {
 
 size_t scan_workspace_bytes(int n);
 // out[i] = sum(in[0..i)); *total (device, optional) = sum(in)
+// n_dev (optional): device-side item count (then n is ignored).  in may equal out.
 void exclusive_scan_u32(const uint32_t* in, uint32_t* out, int n, uint32_t* total, uint32_t* ws,
-                        cudaStream_t st);
+                        cudaStream_t st, const uint32_t* n_dev = nullptr);
 
 size_t radix_workspace_bytes(int n);
-// n_dev (optional): device-side item count <= n; n then only sizes the grid.
+// n_dev (optional): device-side item count (then n is ignored).
 int radix_sort_pairs(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt, int n,
                      int begin_bit, int end_bit, uint32_t* ws, cudaStream_t st, const uint32_t* n_dev = nullptr);
 
