@@ -139,21 +139,21 @@ class ClockSampler:
 def algorithmic_bytes(phase: str, n: dict) -> float | None:
     """Per-step algorithmic bytes of each kernel phase (SURVEY.md 8d table,
     adapted to this implementation's passes)."""
-    N4, N3, V, I, px, P = n["n4"], n["n3"], n["V"], n["I"], n["px"], n["rows_avg"]
+    N4, N3, V, I, K, px, P = n["n4"], n["n3"], n["V"], n["I"], n["K"], n["px"], n["rows_avg"]
     if phase == "preprocess":   # params in (68/44 B geometry + 192 B SH of visible) + 80 B record out + flags
         return 68 * N4 + 44 * N3 + (192 + 80) * V + 4 * (N4 + N3) * 3
     if phase == "depth_sort":   # global LSD over V keys+values: (8 + 24*passes) * n
         return (8 + 24 * 4) * V
-    if phase == "duplicate":    # gather (80 B in, 80+64 B out) + scan + 8 B per instance out
-        return (80 + 144 + 12) * V + 8 * I
-    if phase == "tile_sort":
-        return (8 + 24 * 2) * I
-    if phase == "raster_fwd":   # K4: 4 B value + 64 B splat per instance, 24 B per pixel out
-        return 68 * I + 24 * px
+    if phase == "duplicate":    # gather (80 B in, 80+64+8 B out) + offsets scan; 12 B per instance out
+        return (80 + 152 + 12) * V + 12 * I
+    if phase == "tile_sort":    # keep-flag scan (8 B per instance), compaction (8 B in per instance,
+        return 16 * I + 8 * K + (8 + 16 * 2) * K  # 8 B out per kept one), 2 passes over the kept pairs
+    if phase == "raster_fwd":   # K4: 4 B value + 64 B splat per kept instance, 24 B per pixel out
+        return 68 * K + 24 * px
     if phase == "loss":
         return 44 * px * 3
-    if phase == "raster_bwd":   # 68 B per instance + 36 B accumulators, 32 B per pixel in
-        return 104 * I + 32 * px
+    if phase == "raster_bwd":   # 68 B per kept instance + 36 B accumulators, 32 B per pixel in
+        return 104 * K + 32 * px
     if phase == "gaussian_bwd":  # read params + write grads (2 * 4 * P) + 36 B accumulators
         return V * (2 * 4 * P + 48)
     if phase == "adam":          # 32 B per element (param, m, v rw; grad read + zero)
@@ -277,6 +277,8 @@ def run_ours(args) -> None:
             dist.all_reduce(g)
             ctx.adam_step(tr.lrs, tr.decay())
 
+    for i in range(args.warmup):  # untimed: the copy stream and GT buffers are created on first use
+        e2e_step(-1 - i)
     e2e_ms = timed(e2e_step, args.steps)
     e2e_value = world * args.steps / (e2e_ms / 1e3)
 
@@ -292,7 +294,8 @@ def run_ours(args) -> None:
     peak, peak_kind = peaks()
     rows4 = 17 + 48
     rows3 = 11 + 48
-    counts = {"n4": scene.n4, "n3": scene.n3, "V": info["visible"], "I": info["instances"], "px": W * H,
+    counts = {"n4": scene.n4, "n3": scene.n3, "V": info["visible"], "I": info["instances"],
+              "K": info["kept_instances"], "px": W * H,
               "rows4": rows4, "rows3": rows3,
               "rows_avg": (rows4 * scene.n4 + rows3 * scene.n3) / max(1, scene.n4 + scene.n3)}
     rl = roofline(phase_ms, counts, args.steps, peak, peak_kind)

@@ -259,7 +259,7 @@ void prof_collect(hgs_ctx* ctx) {
 // ====================================================================== render
 // The full K1 -> sort -> K2 -> sort -> K4 pipeline; leaves the tape in ctx.
 hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, const double bg[3],
-                               const hgs_raster_opts* opts) {
+                               const hgs_raster_opts* opts, int deferred) {
     std::string why;
     if (!camera_valid(cam, why)) return fail(ctx, HGS_ERR_INVALID_ARGUMENT, why);
     const double cutoff = opts ? opts->weight_cutoff : 0.05;
@@ -267,6 +267,7 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
     const bool want_trans = opts && opts->transmittance_map;
     cudaStream_t st = ctx->stream;
     ctx->have_tape = false;
+    ctx->stats_pending = false;
     const int n4 = (int)ctx->n4, n3 = (int)ctx->n3, N = n4 + n3;
     const int W = cam->width, H = cam->height;
     const int tiles_x = (W + kTile - 1) / kTile, tiles_y = (H + kTile - 1) / kTile;
@@ -281,9 +282,9 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
 
     const size_t npx = (size_t)W * H;
     CK(ctx->counters.ensure(sizeof(Counters)));
-    CK(ctx->pinned.ensure(sizeof(Counters) + 64));
+    CK(ctx->pinned_ctr.ensure(sizeof(Counters) + 64));
     Counters* dc = ctx->counters.as<Counters>();
-    Counters* hc = static_cast<Counters*>(ctx->pinned.p);
+    Counters* hc = static_cast<Counters*>(ctx->pinned_ctr.p);
     CK(cudaMemsetAsync(dc, 0, sizeof(Counters), st));
     CK(ctx->img.ensure(npx * 3 * sizeof(float)));
     CK(ctx->last.ensure(npx * sizeof(uint32_t)));
@@ -315,51 +316,53 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
                            ctx->scan_ws.as<uint32_t>(), st);
         CKL();
         prof_end(ctx);
-        CK(cudaMemcpyAsync(hc, dc, sizeof(Counters), cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-        V = hc->V;
-    }
-    if (V > 0) {
-        CK(ctx->sort_k.ensure((size_t)V * 4));
-        CK(ctx->sort_v.ensure((size_t)V * 4));
-        CK(ctx->sort_k2.ensure((size_t)V * 4));
-        CK(ctx->sort_v2.ensure((size_t)V * 4));
+        // the visible count V stays on the device: buffers are sized for N,
+        // the sort, gather and offset scan read V from device memory
+        CK(ctx->sort_k.ensure((size_t)N * 4));
+        CK(ctx->sort_v.ensure((size_t)N * 4));
+        CK(ctx->sort_k2.ensure((size_t)N * 4));
+        CK(ctx->sort_v2.ensure((size_t)N * 4));
         prof_begin(ctx, PH_DEPTH_SORT);
         compact_kernel<<<div_up(N, 256), 256, 0, st>>>(ctx->ntiles.as<uint32_t>(), ctx->vispos.as<uint32_t>(),
                                                         ctx->depth_key.as<uint32_t>(), N, ctx->sort_k.as<uint32_t>(),
                                                         ctx->sort_v.as<uint32_t>());
         count_launch();
         CKL();
-        CK(ctx->sort_ws.ensure(radix_workspace_bytes((int)V) + 4096));
+        CK(ctx->sort_ws.ensure(radix_workspace_bytes(N) + 4096));
         // stable sort by f32 depth bits; gid (projected order) breaks ties
         int which = radix_sort_pairs(ctx->sort_k.as<uint32_t>(), ctx->sort_v.as<uint32_t>(), ctx->sort_k2.as<uint32_t>(),
-                                     ctx->sort_v2.as<uint32_t>(), (int)V, 0, 32, ctx->sort_ws.as<uint32_t>(), st);
+                                     ctx->sort_v2.as<uint32_t>(), N, 0, 32, ctx->sort_ws.as<uint32_t>(), st, &dc->V);
         CKL();
         prof_end(ctx);
         uint32_t* sorted_gid = which ? ctx->sort_v2.as<uint32_t>() : ctx->sort_v.as<uint32_t>();
         ctx->sorted_gid = sorted_gid;
-        CK(ctx->rec_sorted.ensure((size_t)V * sizeof(SplatRec)));
-        CK(ctx->fast_sorted.ensure((size_t)V * sizeof(SplatFast)));
-        CK(ctx->ntiles_sorted.ensure((size_t)V * 4));
-        CK(ctx->inst_off.ensure((size_t)V * 4));
+        CK(ctx->rec_sorted.ensure((size_t)N * sizeof(SplatRec)));
+        CK(ctx->fast_sorted.ensure((size_t)N * sizeof(SplatFast)));
+        CK(ctx->ntiles_sorted.ensure((size_t)N * 4));
+        CK(ctx->inst_off.ensure((size_t)N * 4));
         CK(ctx->sorted_of_gid.ensure((size_t)N * 4));
-        CK(ctx->pcut.ensure((size_t)V * 8));
+        CK(ctx->pcut.ensure((size_t)N * 8));
         prof_begin(ctx, PH_DUPLICATE);
         CK(cudaMemsetAsync(ctx->sorted_of_gid.p, 0xff, (size_t)N * 4, st));
-        gather_sorted_kernel<<<div_up((uint32_t)V, 256), 256, 0, st>>>(
-            sorted_gid, (int)V, ctx->rec.as<SplatRec>(), ctx->ntiles.as<uint32_t>(), ctx->rec_sorted.as<SplatRec>(),
+        gather_sorted_kernel<<<div_up((uint32_t)N, 256), 256, 0, st>>>(
+            sorted_gid, &dc->V, ctx->rec.as<SplatRec>(), ctx->ntiles.as<uint32_t>(), ctx->rec_sorted.as<SplatRec>(),
             ctx->fast_sorted.as<SplatFast>(), ctx->ntiles_sorted.as<uint32_t>(), ctx->sorted_of_gid.as<uint32_t>(),
             ctx->pcut.as<double>());
         count_launch();
         CKL();
-        CK(ctx->scan_ws.ensure(scan_workspace_bytes((int)V) + 4096));
-        exclusive_scan_u32(ctx->ntiles_sorted.as<uint32_t>(), ctx->inst_off.as<uint32_t>(), (int)V, &dc->I,
-                           ctx->scan_ws.as<uint32_t>(), st);
+        exclusive_scan_u32(ctx->ntiles_sorted.as<uint32_t>(), ctx->inst_off.as<uint32_t>(), N, &dc->I,
+                           ctx->scan_ws.as<uint32_t>(), st, &dc->V);
         CKL();
         prof_end(ctx);
+        // the one host round trip of a render: the instance count sizes the
+        // duplication buffers; the preprocess error flags are reported here,
+        // before anything downstream runs (the reference throws in K1)
         CK(cudaMemcpyAsync(hc, dc, sizeof(Counters), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
-        I = hc->I;
+        V = hc->V;
+        I = V ? hc->I : 0;
+        hgs_status fs = check_flags(ctx, hc->flags);
+        if (fs != HGS_OK) return fs;
     }
     ctx->V = V;
     ctx->I = I;
@@ -458,8 +461,22 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
     count_launch();
     CKL();
     prof_end(ctx);
-    CK(cudaMemcpyAsync(hc, dc, sizeof(Counters), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    ctx->have_tape = true;
+    ctx->stats_pending = true;
+    if (deferred) return HGS_OK;
+    return hgs_render_finish(ctx);
+}
+
+// Reads the counters of the last render (RenderStats, fix-up and kept
+// counts, error flags): one stream synchronisation, skipped by the training
+// step until its end.
+hgs_status hgs_render_finish(hgs_ctx* ctx) {
+    if (!ctx->stats_pending) return HGS_OK;
+    ctx->stats_pending = false;
+    Counters* dc = ctx->counters.as<Counters>();
+    Counters* hc = static_cast<Counters*>(ctx->pinned_ctr.p);
+    CK(cudaMemcpyAsync(hc, dc, sizeof(Counters), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
     ctx->stats.culled_depth = (int64_t)hc->stats[0];
     ctx->stats.culled_offscreen = (int64_t)hc->stats[1];
     ctx->stats.culled_degenerate = (int64_t)hc->stats[2];
@@ -469,8 +486,10 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
     ctx->fixups = hc->fix_count;
     ctx->kept = ctx->I ? (int64_t)hc->I_kept : 0;
     hgs_status s = check_flags(ctx, hc->flags);
-    if (s != HGS_OK) return s;
-    ctx->have_tape = true;
+    if (s != HGS_OK) {
+        ctx->have_tape = false;
+        return s;
+    }
     return HGS_OK;
 }
 
@@ -535,6 +554,14 @@ void hgs_ctx_destroy(hgs_ctx* ctx) {
                     &ctx->fix_list, &ctx->accum, &ctx->lgrad, &ctx->gt_stage, &ctx->loss_ws, &ctx->stage, &ctx->adam_ok, &ctx->pcut, &ctx->dup_first};
     for (DBuf* b : bufs) b->release();
     ctx->pinned.release();
+    ctx->pinned_ctr.release();
+    for (int b = 0; b < 2; ++b) {
+        ctx->gt_buf[b].release();
+        ctx->gt_stage64[b].release();
+        if (ctx->gt_ready[b]) cudaEventDestroy(ctx->gt_ready[b]);
+        if (ctx->gt_free[b]) cudaEventDestroy(ctx->gt_free[b]);
+    }
+    if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;
 }
@@ -676,6 +703,8 @@ const float* hgs_last_image_device(hgs_ctx* ctx) { return ctx ? ctx->img.as<floa
 
 hgs_status hgs_render_info_get(hgs_ctx* ctx, hgs_render_info* info) {
     if (!ctx || !info) return HGS_ERR_INVALID_ARGUMENT;
+    hgs_status r = hgs_render_finish(ctx);
+    if (r != HGS_OK) return r;
     info->visible = ctx->V;
     info->instances = ctx->I;
     info->fixup_pixels = ctx->fixups;

@@ -71,6 +71,7 @@ struct Counters {
 }  // namespace hgs
 
 struct hgs_ctx {
+    bool stats_pending = false;  // counters of the last render not read back yet
     int device = 0;
     cudaStream_t stream = nullptr;
     cudaStream_t own_stream = nullptr;
@@ -112,10 +113,14 @@ struct hgs_ctx {
     hgs::DBuf accum;     // backward per-sorted-splat accumulators
     hgs::DBuf lgrad;     // dL/dimage (device float)
     hgs::DBuf gt_stage;  // staged ground truth
+    hgs::DBuf gt_buf[2], gt_stage64[2];  // double-buffered host GT of the training step
+    cudaStream_t copy_stream = nullptr;  // host -> device GT copies, overlapped with the render
+    cudaEvent_t gt_ready[2] = {nullptr, nullptr}, gt_free[2] = {nullptr, nullptr};
     hgs::DBuf loss_ws;   // loss scratch (SSIM maps)
     hgs::DBuf scratch;   // small device scalars (loss sums, skip counts, leakage)
     hgs::DBuf stage;     // upload / download staging
-    hgs::HostPinned pinned;
+    hgs::HostPinned pinned;      // Scratch read-back (training / loss)
+    hgs::HostPinned pinned_ctr;  // Counters read-back (render)
 
     // ---- state of the last render (the "tape")
     bool have_tape = false;

@@ -13,7 +13,8 @@ __global__ void preprocess_kernel(const float* __restrict__ p4, int64_t cap4, in
                                   uint32_t* __restrict__ flags);
 
 // raster_fwd.cu (K2 + K4)
-__global__ void gather_sorted_kernel(const uint32_t* __restrict__ sorted_gid, int V, const SplatRec* __restrict__ rec,
+__global__ void gather_sorted_kernel(const uint32_t* __restrict__ sorted_gid, const uint32_t* __restrict__ V_dev,
+                                     const SplatRec* __restrict__ rec,
                                      const uint32_t* __restrict__ ntiles, SplatRec* __restrict__ rec_sorted,
                                      SplatFast* __restrict__ fast_sorted, uint32_t* __restrict__ ntiles_sorted,
                                      uint32_t* __restrict__ sorted_of_gid, double* __restrict__ pcut);
@@ -81,6 +82,8 @@ struct AdamArgs {
     float b1, b2, one_m_b1, one_m_b2;
     float inv_bc1, inv_bc2;
     float lr_mean, lr_mean_t, lr_quat, lr_scales, lr_opacity, lr_sh;
+    const double* view_sums = nullptr;  // the step's (ssim, l1) loss sums per view
+    int n_views = 0;                    // > 0: skip the whole update if one is non-finite
 };
 struct AdamPools {
     float *p4, *g4, *m4, *v4, *p3, *g3, *m3, *v3;

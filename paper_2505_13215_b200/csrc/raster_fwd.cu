@@ -10,7 +10,8 @@ namespace hgs {
 // After the depth sort: gather the exact record into depth order, derive the
 // FP32 fast view (Cholesky of the scaled conic + certified error bound), and
 // emit the tile count of each sorted splat.
-__global__ void __launch_bounds__(256) gather_sorted_kernel(const uint32_t* __restrict__ sorted_gid, int V,
+__global__ void __launch_bounds__(256) gather_sorted_kernel(const uint32_t* __restrict__ sorted_gid,
+                                                            const uint32_t* __restrict__ V_dev,
                                                             const SplatRec* __restrict__ rec,
                                                             const uint32_t* __restrict__ ntiles,
                                                             SplatRec* __restrict__ rec_sorted,
@@ -19,7 +20,7 @@ __global__ void __launch_bounds__(256) gather_sorted_kernel(const uint32_t* __re
                                                             uint32_t* __restrict__ sorted_of_gid,
                                                             double* __restrict__ pcut) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= V) return;
+    if (j >= (int)*V_dev) return;
     const uint32_t gid = sorted_gid[j];
     sorted_of_gid[gid] = (uint32_t)j;
     const SplatRec e = rec[gid];

@@ -15,6 +15,8 @@ using namespace hgs;
 
 namespace {
 
+constexpr int kMaxStepViews = 32;  // views per step between loss read-backs
+
 struct Scratch {
     double ssim_sum;
     double l1_sum;
@@ -25,6 +27,7 @@ struct Scratch {
     double leak_sum;
     double loss_acc;
     double pad[2];
+    double view_sums[kMaxStepViews][2];  // per-view (ssim_sum, l1_sum) of a training step
 };
 
 hgs_status fail(hgs_ctx* ctx, hgs_status s, const std::string& m) {
@@ -50,18 +53,32 @@ __global__ void f64_to_f32_kernel(const double* __restrict__ src, float* __restr
     if (i < n) dst[i] = (float)src[i];
 }
 
-// Host image (double or float) -> device float buffer.
-hgs_status upload_image(hgs_ctx* ctx, const void* src, int dtype, int64_t n, DBuf& dst) {
+// Host image (double or float) -> device float buffer, on stream s (default
+// the context stream) with `stage` as the FP64 staging buffer.
+hgs_status upload_image(hgs_ctx* ctx, const void* src, int dtype, int64_t n, DBuf& dst, cudaStream_t s = nullptr,
+                        DBuf* stage = nullptr) {
+    if (!s) s = ctx->stream;
+    if (!stage) stage = &ctx->stage;
     CK(dst.ensure((size_t)n * 4));
     if (dtype == HGS_F32) {
-        CK(cudaMemcpyAsync(dst.p, src, (size_t)n * 4, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(dst.p, src, (size_t)n * 4, cudaMemcpyHostToDevice, s));
     } else {
-        CK(ctx->stage.ensure((size_t)n * 8));
-        CK(cudaMemcpyAsync(ctx->stage.p, src, (size_t)n * 8, cudaMemcpyHostToDevice, ctx->stream));
-        f64_to_f32_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(ctx->stage.as<double>(),
-                                                                               dst.as<float>(), n);
+        CK(stage->ensure((size_t)n * 8));
+        CK(cudaMemcpyAsync(stage->p, src, (size_t)n * 8, cudaMemcpyHostToDevice, s));
+        f64_to_f32_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(stage->as<double>(), dst.as<float>(), n);
         count_launch();
         CKL();
+    }
+    return HGS_OK;
+}
+
+// The copy stream and the double-buffer events of the host-GT path.
+hgs_status ensure_copy_stream(hgs_ctx* ctx) {
+    if (ctx->copy_stream) return HGS_OK;
+    CK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; ++b) {
+        CK(cudaEventCreateWithFlags(&ctx->gt_ready[b], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ctx->gt_free[b], cudaEventDisableTiming));
     }
     return HGS_OK;
 }
@@ -131,7 +148,9 @@ hgs_status run_backward(hgs_ctx* ctx, const float* lg, double scale) {
 
 // K5 on the last rendered image against device gt; writes ctx->lgrad and
 // accumulates the loss into scratch->loss_acc (device) -- no host sync.
-hgs_status run_loss(hgs_ctx* ctx, const float* gt, double lambda) {
+// sums (device, optional): where to accumulate (ssim_sum, l1_sum); default
+// the scratch pair read by the loss API
+hgs_status run_loss(hgs_ctx* ctx, const float* gt, double lambda, double* sums = nullptr) {
     cudaStream_t st = ctx->stream;
     const int W = ctx->W, H = ctx->H;
     const bool with_ssim = lambda != 0.0;
@@ -145,34 +164,43 @@ hgs_status run_loss(hgs_ctx* ctx, const float* gt, double lambda) {
     const size_t npx = (size_t)W * H;
     CK(ctx->lgrad.ensure(npx * 3 * 4));
     Scratch* sc = scratch(ctx);
-    CK(cudaMemsetAsync(sc, 0, offsetof(Scratch, skipped), st));  // ssim_sum, l1_sum
+    if (!sums) sums = &sc->ssim_sum;
+    CK(cudaMemsetAsync(sums, 0, 2 * sizeof(double), st));  // ssim_sum, l1_sum
     const int vw = W - 10, vh = H - 10;
     prof_begin(ctx, PH_LOSS);
     if (with_ssim) {
         CK(ctx->loss_ws.ensure((size_t)vw * vh * 9 * 4));
         dim3 g((vw + 31) / 32, (vh + 15) / 16, 3);
-        ssim_fwd_kernel<<<g, 256, 0, st>>>(ctx->img.as<float>(), gt, W, H, ctx->loss_ws.as<float>(), &sc->ssim_sum);
+        ssim_fwd_kernel<<<g, 256, 0, st>>>(ctx->img.as<float>(), gt, W, H, ctx->loss_ws.as<float>(), &sums[0]);
         count_launch();
         CKL();
     }
     dim3 gb((W + 31) / 32, (H + 15) / 16, 3);
     ssim_bwd_kernel<<<gb, 256, 0, st>>>(ctx->img.as<float>(), gt, W, H, ctx->loss_ws.as<float>(), (float)lambda,
-                                        with_ssim ? 1 : 0, ctx->lgrad.as<float>(), &sc->l1_sum);
+                                        with_ssim ? 1 : 0, ctx->lgrad.as<float>(), &sums[1]);
     count_launch();
     CKL();
     prof_end(ctx);
     return HGS_OK;
 }
 
-double loss_from_sums(const Scratch& h, int W, int H, double lambda) {
+double loss_from_sums(double ssim_sum, double l1_sum, int W, int H, double lambda) {
     // loss.cpp:26-32: (1-l) * L1 + l * (1 - SSIM)
     const double n = (double)W * H * 3;
-    double loss = (1.0 - lambda) * (h.l1_sum / n);
-    if (lambda != 0.0) loss += lambda * (1.0 - h.ssim_sum / ((double)(W - 10) * (H - 10) * 3));
+    double loss = (1.0 - lambda) * (l1_sum / n);
+    if (lambda != 0.0) loss += lambda * (1.0 - ssim_sum / ((double)(W - 10) * (H - 10) * 3));
     return loss;
 }
+double loss_from_sums(const Scratch& h, int W, int H, double lambda) {
+    return loss_from_sums(h.ssim_sum, h.l1_sum, W, H, lambda);
+}
 
-hgs_status run_adam(hgs_ctx* ctx, const hgs_lrs* lrs, double mean_lr_scale) {
+// view_sums/n_views (device, optional): the step's per-view loss sums; the
+// kernels leave every parameter untouched when one is non-finite (the step
+// then fails with NumericAbort, train.cpp:445-447, without a host round trip
+// before the update).
+hgs_status run_adam(hgs_ctx* ctx, const hgs_lrs* lrs, double mean_lr_scale, const double* view_sums = nullptr,
+                    int n_views = 0) {
     cudaStream_t st = ctx->stream;
     ctx->step++;
     const double bc1 = 1.0 - std::pow(0.9, (double)ctx->step);
@@ -190,6 +218,8 @@ hgs_status run_adam(hgs_ctx* ctx, const hgs_lrs* lrs, double mean_lr_scale) {
     A.lr_scales = (float)lrs->scales;
     A.lr_opacity = (float)lrs->opacity;
     A.lr_sh = (float)lrs->sh;
+    A.view_sums = view_sums;
+    A.n_views = n_views;
     const int n = (int)(ctx->n4 + ctx->n3);
     Scratch* sc = scratch(ctx);
     AdamPools P;
@@ -522,39 +552,75 @@ hgs_status train_step_impl(hgs_ctx* ctx, int n_views, const hgs_camera* cams, co
     hgs_status r = ensure_scratch(ctx);
     if (r != HGS_OK) return r;
     hgs_raster_opts ro{o->weight_cutoff, 1, 0, 0};
+    // No host round trip per view beyond the render's instance count: the
+    // per-view loss sums stay on the device (read every kMaxStepViews views
+    // and at the end), Adam checks their finiteness itself.
     double loss = 0.0;
+    Scratch* sc = scratch(ctx);
+    Scratch* h = static_cast<Scratch*>(ctx->pinned.p);
+    int pending = 0;  // views whose loss sums are still on the device
+    auto flush = [&]() -> hgs_status {
+        CK(cudaMemcpyAsync(h->view_sums, sc->view_sums, sizeof(double) * 2 * pending, cudaMemcpyDeviceToHost,
+                           ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        for (int k = 0; k < pending; ++k)
+            loss += loss_from_sums(h->view_sums[k][0], h->view_sums[k][1], ctx->W, ctx->H, o->ssim_lambda);
+        pending = 0;
+        return HGS_OK;
+    };
+    if (!gt_on_device) {
+        r = ensure_copy_stream(ctx);
+        if (r != HGS_OK) return r;
+    }
     for (int v = 0; v < n_views; ++v) {
         const float* g = nullptr;
+        const int b = v & 1;
         if (!gt_on_device) {
-            // e2e path: the view's ground truth comes from host memory
-            prof_begin(ctx, PH_UPLOAD);
-            r = upload_image(ctx, gt[v], gt_dtype, (int64_t)cams[v].width * cams[v].height * 3, ctx->gt_stage);
-            prof_end(ctx);
+            // e2e path: the view's ground truth comes from host memory.  It is
+            // copied on the copy stream into one of two buffers while the view
+            // renders; the loss waits for it, the copy into the same buffer
+            // two views later waits for that loss.
+            CK(cudaStreamWaitEvent(ctx->copy_stream, ctx->gt_free[b], 0));
+            r = upload_image(ctx, gt[v], gt_dtype, (int64_t)cams[v].width * cams[v].height * 3, ctx->gt_buf[b],
+                             ctx->copy_stream, &ctx->gt_stage64[b]);
             if (r != HGS_OK) return r;
-            g = ctx->gt_stage.as<float>();
+            CK(cudaEventRecord(ctx->gt_ready[b], ctx->copy_stream));
+            g = ctx->gt_buf[b].as<float>();
         } else {
             g = static_cast<const float*>(gt[v]);
         }
-        r = hgs_render_pipeline(ctx, &cams[v], times[v], o->bg, &ro);
+        r = hgs_render_pipeline(ctx, &cams[v], times[v], o->bg, &ro, 1);
         if (r != HGS_OK) return r;
-        r = run_loss(ctx, g, o->ssim_lambda);
+        if (!gt_on_device) CK(cudaStreamWaitEvent(ctx->stream, ctx->gt_ready[b], 0));
+        r = run_loss(ctx, g, o->ssim_lambda, sc->view_sums[pending]);
         if (r != HGS_OK) return r;
+        if (!gt_on_device) CK(cudaEventRecord(ctx->gt_free[b], ctx->stream));
+        ++pending;
         r = run_backward(ctx, ctx->lgrad.as<float>(), 1.0 / (double)batch_total);  // train.cpp:430-432
         if (r != HGS_OK) return r;
-        Scratch* h = static_cast<Scratch*>(ctx->pinned.p);
-        CK(cudaMemcpyAsync(h, ctx->scratch.p, sizeof(Scratch), cudaMemcpyDeviceToHost, ctx->stream));
-        CK(cudaStreamSynchronize(ctx->stream));
-        loss += loss_from_sums(*h, ctx->W, ctx->H, o->ssim_lambda);
+        if (pending == kMaxStepViews && v + 1 < n_views) {
+            r = flush();
+            if (r != HGS_OK) return r;
+        }
     }
-    if (loss_out) *loss_out = loss;
-    if (!std::isfinite(loss))
+    if (!std::isfinite(loss)) {  // an earlier group of views already failed
+        if (loss_out) *loss_out = loss;
         return fail(ctx, HGS_ERR_NUMERIC_ABORT, "train: non-finite loss");  // train.cpp:445-447
+    }
+    const int gate = pending;
     if (apply_adam) {
-        Scratch* sc = scratch(ctx);
         CK(cudaMemsetAsync(&sc->skipped, 0, sizeof(unsigned long long) + 8, ctx->stream));
-        r = run_adam(ctx, &o->lrs, o->mean_lr_scale);
+        r = run_adam(ctx, &o->lrs, o->mean_lr_scale, &sc->view_sums[0][0], gate);
         if (r != HGS_OK) return r;
-        CK(cudaStreamSynchronize(ctx->stream));
+    }
+    r = flush();
+    if (r != HGS_OK) return r;
+    r = hgs_render_finish(ctx);
+    if (r != HGS_OK) return r;
+    if (loss_out) *loss_out = loss;
+    if (!std::isfinite(loss)) {
+        if (apply_adam) --ctx->step;  // the kernels skipped the update
+        return fail(ctx, HGS_ERR_NUMERIC_ABORT, "train: non-finite loss");  // train.cpp:445-447
     }
     prof_collect(ctx);
     return HGS_OK;

@@ -240,3 +240,26 @@ def test_train_step_reduces_loss(ctx):
     losses = [tr.step([i % 8, (i + 3) % 8]) for i in range(40)]
     assert np.isfinite(losses).all()
     assert np.mean(losses[-5:]) < np.mean(losses[:5])
+
+
+def test_train_step_nonfinite_loss_aborts_before_update(ctx):
+    """train.cpp:445-447: a non-finite loss aborts the step before Adam.  The
+    device step has no host round trip between the loss and the update, so
+    the Adam kernels gate themselves on the per-view loss sums."""
+    from paper_2505_13215_b200._capi import NumericAbort
+    from paper_2505_13215_b200.train import DeviceTrainer
+
+    scene = synthetic_scene(1500, 500, 1, seed=31, density_n=2000)
+    cams = [ring_camera(31, 80, 64, index=i, n_ring=4) for i in range(4)]
+    tr = DeviceTrainer(ctx, scene, cams, [0.5] * 4, target=synthetic_scene(1500, 500, 1, seed=32, density_n=2000),
+                       bg=(0.2, 0.2, 0.2))
+    tr.step([0, 1])  # one healthy step (Adam state exists)
+    before = ctx.download()
+    tr.gt[2][5, 5, 1] = float("nan")
+    with pytest.raises(NumericAbort):
+        tr.step([1, 2])
+    after = ctx.download()
+    for f in ("mean_x", "ql", "sh4", "mean3", "op3", "sh3"):
+        assert np.array_equal(getattr(before, f), getattr(after, f), equal_nan=True), f
+    tr.gt[2][5, 5, 1] = 0.5
+    assert np.isfinite(tr.step([2, 3]))  # the context keeps working
