@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhgs_gpu.so")
+LIB_PATH = os.environ.get("HGS_LIB") or os.path.join(_HERE, "libhgs_gpu.so")  # HGS_LIB: A/B builds
 
 HGS_F64, HGS_F32 = 0, 1
 

@@ -109,7 +109,7 @@ __device__ __forceinline__ void backprop_pair(PixBwd& s, bool p, float g, float 
     s.T = p ? Ti : s.T;
 }
 
-__global__ void __launch_bounds__(kThreadsB, 8) raster_bwd_kernel(
+__global__ void __launch_bounds__(kThreadsB, 7) raster_bwd_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ inst_val, const SplatFast* __restrict__ fast,
     const SplatRec* __restrict__ exact, int W, int H, int tiles_x, const float* __restrict__ tfinal,
     const uint32_t* __restrict__ last_arr, const float* __restrict__ dL_dimg, float bg_r, float bg_g, float bg_b,
@@ -162,8 +162,12 @@ __global__ void __launch_bounds__(kThreadsB, 8) raster_bwd_kernel(
             if (!((sb.qm[k] >> warp) & 1u)) continue;  // exact: no pixel of this quadrant reaches 1/255
             const int4 hdr = sb.hdr[k];
             const uint32_t idx = base + k;
-            const bool b0 = idx < s0.last && in_box(hdr.x, hdr.y, px, py0);
-            const bool b1 = idx < s1.last && in_box(hdr.x, hdr.y, px, py1);
+            // box test without short-circuit branches (the column is shared)
+            const bool colin = (unsigned)(px - box_x0(hdr.x)) <= (unsigned)box_w(hdr.x);
+            const int y0 = box_x0(hdr.y);
+            const unsigned wy = (unsigned)box_w(hdr.y);
+            const bool b0 = colin & (idx < s0.last) & ((unsigned)(py0 - y0) <= wy);
+            const bool b1 = colin & (idx < s1.last) & ((unsigned)(py1 - y0) <= wy);
             if (!__any_sync(0xffffffffu, b0 || b1)) continue;
             const float4 L = sb.chol[k], col = sb.col[k];
             const SplatRec* e = exact + sb.j[k];

@@ -272,7 +272,7 @@ __device__ __forceinline__ void write_pixel(const PixFwd& s, int pix, float bg_r
 // of the last contributor (bit 31 = pixel handed to the FP64 fix-up), the
 // final transmittance (read by the backward) and the optional count /
 // transmittance maps.
-__global__ void __launch_bounds__(kThreads, 8) raster_fwd_kernel(
+__global__ void __launch_bounds__(kThreads, 6) raster_fwd_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ inst_val, const SplatFast* __restrict__ fast,
     const SplatRec* __restrict__ exact, int W, int H, int tiles_x, float bg_r, float bg_g, float bg_b,
     float* __restrict__ out_rgb, uint32_t* __restrict__ out_last, float* __restrict__ out_tfinal,
@@ -305,8 +305,12 @@ __global__ void __launch_bounds__(kThreads, 8) raster_fwd_kernel(
             if (s0.done && s1.done) break;
             if (!((sb.qm[k] >> warp) & 1u)) continue;  // exact: no pixel of this quadrant reaches 1/255
             const int4 hdr = sb.hdr[k];
-            const bool b0 = !s0.done && in_box(hdr.x, hdr.y, px, py0);
-            const bool b1 = !s1.done && in_box(hdr.x, hdr.y, px, py1);
+            // box test without short-circuit branches (the column is shared)
+            const bool colin = (unsigned)(px - box_x0(hdr.x)) <= (unsigned)box_w(hdr.x);
+            const int y0 = box_x0(hdr.y);
+            const unsigned wy = (unsigned)box_w(hdr.y);
+            const bool b0 = colin & !s0.done & ((unsigned)(py0 - y0) <= wy);
+            const bool b1 = colin & !s1.done & ((unsigned)(py1 - y0) <= wy);
             if (!(b0 || b1)) continue;
             s0.count += b0;
             s1.count += b1;
