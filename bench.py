@@ -173,8 +173,27 @@ def roofline(phase_ms: dict, counts: dict, steps: int, peak: float, peak_kind: s
                         "GB/s": round(gbs, 1) if gbs else None, "frac": round(gbs / peak, 4) if gbs else None})
     kernels.sort(key=lambda k: -k["ms_per_step"])
     top = kernels[0]
+    # DRAM traffic per launch of the phase's main kernel from the committed
+    # `ncu --set full` capture (profiles/ncu_summary.json, tools/make_profiles.py)
+    ncu = {}
+    try:
+        ncu = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
+    except Exception:
+        pass
+    main_kernel = {"raster_bwd": "raster_bwd_kernel", "raster_fwd": "raster_fwd_kernel",
+                   "duplicate": "duplicate_kernel", "gaussian_bwd": "gaussian_bwd_kernel",
+                   "adam": "adam_rows_kernel", "tile_sort": "radix_sort_coop_kernel",
+                   "depth_sort": "radix_sort_coop_kernel"}
+    for k in kernels:
+        prof = ncu.get(main_kernel.get(k["phase"], ""), {})
+        k["ncu"] = {key: prof.get(key) for key in ("kernel", "duration_us", "dram_bytes_per_launch",
+                                                   "issue_slots_busy_pct", "ipc_active")} if prof else None
+    tp = (top.get("ncu") or {})
     return {"bound": "hbm", "kernel": top["phase"], "achieved": top["GB/s"], "peak": peak, "unit": "GB/s",
-            "frac": top["frac"], "traffic": None, "peak_source": peak_kind, "kernels": kernels}
+            "frac": top["frac"], "traffic": tp.get("dram_bytes_per_launch"), "peak_source": peak_kind,
+            "note": "the tile rasterizers are issue-bound (see issue_slots_busy_pct), not HBM-bound: "
+                    "their splat reads hit L2",
+            "kernels": kernels}
 
 
 # ------------------------------------------------------------------ our arm
