@@ -341,13 +341,13 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
         CK(ctx->ntiles_sorted.ensure((size_t)N * 4));
         CK(ctx->inst_off.ensure((size_t)N * 4));
         CK(ctx->sorted_of_gid.ensure((size_t)N * 4));
-        CK(ctx->pcut.ensure((size_t)N * 8));
+        CK(ctx->pcut.ensure((size_t)N * sizeof(CullRec)));
         prof_begin(ctx, PH_DUPLICATE);
         CK(cudaMemsetAsync(ctx->sorted_of_gid.p, 0xff, (size_t)N * 4, st));
         gather_sorted_kernel<<<div_up((uint32_t)N, 256), 256, 0, st>>>(
             sorted_gid, &dc->V, ctx->rec.as<SplatRec>(), ctx->ntiles.as<uint32_t>(), ctx->rec_sorted.as<SplatRec>(),
             ctx->fast_sorted.as<SplatFast>(), ctx->ntiles_sorted.as<uint32_t>(), ctx->sorted_of_gid.as<uint32_t>(),
-            ctx->pcut.as<double>());
+            ctx->pcut.as<CullRec>());
         count_launch();
         CKL();
         exclusive_scan_u32(ctx->ntiles_sorted.as<uint32_t>(), ctx->inst_off.as<uint32_t>(), N, &dc->I,
@@ -385,7 +385,7 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
         count_launch();
         duplicate_kernel<<<dup_blocks, 256, 0, st>>>(
             ctx->fast_sorted.as<SplatFast>(), ctx->rec_sorted.as<SplatRec>(), (int)V, ctx->inst_off.as<uint32_t>(),
-            tiles_x, cull, ctx->pcut.as<double>(), ctx->inst_k.as<uint32_t>(), ctx->inst_v.as<uint32_t>(),
+            tiles_x, cull, ctx->pcut.as<CullRec>(), ctx->inst_k.as<uint32_t>(), ctx->inst_v.as<uint32_t>(),
             cull ? ctx->inst_flag.as<uint32_t>() : nullptr, ctx->dup_first.as<uint32_t>(), (int)I);
         count_launch();
         CKL();

@@ -17,11 +17,11 @@ __global__ void gather_sorted_kernel(const uint32_t* __restrict__ sorted_gid, co
                                      const SplatRec* __restrict__ rec,
                                      const uint32_t* __restrict__ ntiles, SplatRec* __restrict__ rec_sorted,
                                      SplatFast* __restrict__ fast_sorted, uint32_t* __restrict__ ntiles_sorted,
-                                     uint32_t* __restrict__ sorted_of_gid, double* __restrict__ pcut);
+                                     uint32_t* __restrict__ sorted_of_gid, CullRec* __restrict__ cull_rec);
 constexpr int kDupPerCtaHost = 1024;  // instances per duplicate_kernel CTA
 __global__ void duplicate_kernel(const SplatFast* __restrict__ fast, const SplatRec* __restrict__ exact, int V,
                                  const uint32_t* __restrict__ offsets, int tiles_x, int cull,
-                                 const double* __restrict__ pcut, uint32_t* __restrict__ keys,
+                                 const CullRec* __restrict__ cull_rec, uint32_t* __restrict__ keys,
                                  uint32_t* __restrict__ vals, uint32_t* __restrict__ keep,
                                  const uint32_t* __restrict__ cta_first, int I);
 __global__ void dup_bounds_kernel(const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ ntiles_sorted,

@@ -41,6 +41,13 @@ struct __align__(16) SplatFast {
 };
 static_assert(sizeof(SplatFast) == 64, "SplatFast layout");
 
+// FP32 view of a sorted splat for the conservative tile / quadrant culling of
+// the duplication pass: double-float mean, symmetric conic, power threshold.
+struct __align__(16) CullRec {
+    float sx_hi, sy_hi, sx_lo, sy_lo;
+    float a, b, c, pcut;
+};
+
 // Instance value = sorted splat index | (8x8-quadrant contribution mask << 28).
 constexpr int kInstMaskShift = 28;
 constexpr uint32_t kInstIndexMask = (1u << kInstMaskShift) - 1u;
@@ -103,6 +110,8 @@ struct SplatBatch {
         j[t] = jj;
     }
 };
+
+__device__ __forceinline__ float fast_dx(float pc, float hi, float lo) { return __fsub_rn(__fsub_rn(pc, hi), lo); }
 
 // FP32 exponent argument x = power*log2(e) (>= 0) on the fast path.
 __device__ __forceinline__ float fast_x(const float4 m, const float4 L, float pxc, float pyc, float& dx, float& dy) {

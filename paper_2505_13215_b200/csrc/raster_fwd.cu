@@ -18,16 +18,27 @@ __global__ void __launch_bounds__(256) gather_sorted_kernel(const uint32_t* __re
                                                             SplatFast* __restrict__ fast_sorted,
                                                             uint32_t* __restrict__ ntiles_sorted,
                                                             uint32_t* __restrict__ sorted_of_gid,
-                                                            double* __restrict__ pcut) {
+                                                            CullRec* __restrict__ cull_rec) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= (int)*V_dev) return;
     const uint32_t gid = sorted_gid[j];
     sorted_of_gid[gid] = (uint32_t)j;
     const SplatRec e = rec[gid];
     rec_sorted[j] = e;
-    // tile-culling threshold on the power: alpha * exp(-p) >= 1/255 <=> p <= ln(255 alpha)
-    // (+1e-5 margin, see tile_may_contribute)
-    pcut[j] = log(e.alpha * 255.0) + 1e-5;
+    // tile culling (FP32, conservative): threshold on the power, alpha * exp(-p)
+    // >= 1/255 <=> p <= ln(255 alpha) (+1e-5 margin, see tile_may_contribute)
+    {
+        CullRec cr;
+        cr.sx_hi = __double2float_rn(e.sx);
+        cr.sx_lo = __double2float_rn(e.sx - (double)cr.sx_hi);
+        cr.sy_hi = __double2float_rn(e.sy);
+        cr.sy_lo = __double2float_rn(e.sy - (double)cr.sy_hi);
+        cr.a = (float)e.c00;
+        cr.b = (float)(0.5 * (e.c01 + e.c10));
+        cr.c = (float)e.c11;
+        cr.pcut = (float)(log(e.alpha * 255.0) + 1e-5);
+        cull_rec[j] = cr;
+    }
     ntiles_sorted[j] = ntiles[gid];
     SplatFast f;
     f.sx_hi = __double2float_rn(e.sx);
@@ -77,24 +88,35 @@ __global__ void __launch_bounds__(256) gather_sorted_kernel(const uint32_t* __re
 // Can splat e reach alpha >= 1/255 at any pixel centre of [xa,xb]x[ya,yb]?
 // Minimum of the (convex) power over the rectangle: 0 if the mean is inside,
 // else on one of the four edges at the clamped 1D minimiser, compared with
-// pcut = ln(alpha * 255) + 1e-5 (a 1e-5 margin on the power, i.e. ~1e-5
-// relative on alpha).  A pair skipped here is one the reference skips too
-// (raster.cpp:139-140), so the output is unchanged.
-__device__ inline bool tile_may_contribute(const SplatRec& e, double pcut, int xa, int xb, int ya, int yb) {
-    const double lx = xa + 0.5 - e.sx, hx = xb + 0.5 - e.sx, ly = ya + 0.5 - e.sy, hy = yb + 0.5 - e.sy;
-    if (lx <= 0.0 && 0.0 <= hx && ly <= 0.0 && 0.0 <= hy) return true;
-    const double a = e.c00, b = 0.5 * (e.c01 + e.c10), c = e.c11;
-    auto q = [&](double dx, double dy) { return 0.5 * (a * dx * dx + 2.0 * b * dx * dy + c * dy * dy); };
-    double pmin = INFINITY;
-    const double xs[2] = {lx, hx}, ys[2] = {ly, hy};
+// pcut = ln(alpha * 255) + 1e-5.  Evaluated in FP32 and CONSERVATIVE: the
+// rectangle is declared unreachable only when the FP32 minimum exceeds pcut
+// by more than its error bound (1e-5 of the summed magnitudes S of the
+// quadratic's terms, >> the ~10 ulp actual error, plus 1e-5 absolute), so a
+// pair skipped here is one the reference skips too (raster.cpp:139-140) and
+// the output is unchanged; doubtful rectangles are simply kept.
+__device__ inline bool tile_may_contribute(const CullRec& e, int xa, int xb, int ya, int yb) {
+    const float lx = fast_dx((float)xa + 0.5f, e.sx_hi, e.sx_lo), hx = fast_dx((float)xb + 0.5f, e.sx_hi, e.sx_lo);
+    const float ly = fast_dx((float)ya + 0.5f, e.sy_hi, e.sy_lo), hy = fast_dx((float)yb + 0.5f, e.sy_hi, e.sy_lo);
+    if (lx <= 0.0f && 0.0f <= hx && ly <= 0.0f && 0.0f <= hy) return true;
+    const float a = e.a, b = e.b, c = e.c;
+    if (!(a > 0.0f && c > 0.0f)) return true;  // not positive definite in FP32: keep
+    const float ia = __fdividef(1.0f, a), ic = __fdividef(1.0f, c);  // minimiser only: approximate is fine
+    float pmin = INFINITY, smag = 0.0f;
+    auto eval = [&](float dx, float dy) {
+        const float bxy = b * dx * dy;
+        const float q = 0.5f * fmaf(a * dx, dx, fmaf(c * dy, dy, 2.0f * bxy));
+        if (q < pmin) {
+            pmin = q;
+            smag = 0.5f * fmaf(a * dx, dx, fmaf(c * dy, dy, 2.0f * fabsf(bxy)));
+        }
+    };
+    const float xs[2] = {lx, hx}, ys[2] = {ly, hy};
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
-        const double dy = fmin(fmax(-b * xs[k] / c, ly), hy);
-        pmin = fmin(pmin, q(xs[k], dy));
-        const double dx = fmin(fmax(-b * ys[k] / a, lx), hx);
-        pmin = fmin(pmin, q(dx, ys[k]));
+        eval(xs[k], fminf(fmaxf(-b * xs[k] * ic, ly), hy));
+        eval(fminf(fmaxf(-b * ys[k] * ia, lx), hx), ys[k]);
     }
-    return pmin <= pcut;
+    return pmin <= e.pcut + 1e-5f * (1.0f + smag);
 }
 
 // Duplicate each sorted splat into every tile its box overlaps
@@ -129,7 +151,7 @@ __global__ void __launch_bounds__(256) dup_bounds_kernel(const uint32_t* __restr
 __global__ void __launch_bounds__(kDupThreads) duplicate_kernel(const SplatFast* __restrict__ fast,
                                                                 const SplatRec* __restrict__ exact, int V,
                                                                 const uint32_t* __restrict__ offsets, int tiles_x,
-                                                                int cull, const double* __restrict__ pcut_arr,
+                                                                int cull, const CullRec* __restrict__ cull_rec,
                                                                 uint32_t* __restrict__ keys,
                                                                 uint32_t* __restrict__ vals,
                                                                 uint32_t* __restrict__ keep,
@@ -158,14 +180,13 @@ __global__ void __launch_bounds__(kDupThreads) duplicate_kernel(const SplatFast*
         uint32_t mask = 0xfu;
         if (cull) {
             // culling threshold on the power: alpha * exp(-p) >= 1/255  <=>  p <= ln(255 alpha)
-            const SplatRec& e = exact[j];
-            const double pcut = pcut_arr[j];
+            const CullRec e = cull_rec[j];
             mask = 0u;
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const int qx0 = tx * kTile + (q & 1) * 8, qy0 = ty * kTile + (q >> 1) * 8;
                 const int xa = max(x0, qx0), xb = min(x1, qx0 + 7), ya = max(y0, qy0), yb = min(y1, qy0 + 7);
-                if (xa <= xb && ya <= yb && tile_may_contribute(e, pcut, xa, xb, ya, yb)) mask |= 1u << q;
+                if (xa <= xb && ya <= yb && tile_may_contribute(e, xa, xb, ya, yb)) mask |= 1u << q;
             }
         }
         keys[i] = (uint32_t)(ty * tiles_x + tx);
