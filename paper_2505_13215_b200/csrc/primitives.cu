@@ -210,20 +210,24 @@ __global__ void __launch_bounds__(kCoopThreads) radix_sort_coop_kernel(CoopSort 
     }
 }
 
-// Co-resident grid size of a cooperative kernel on the current device.
+// Grid of a cooperative kernel for n items: co-resident (<= 4 blocks per SM
+// and the occupancy limit), at least one block per SM, about 2048 items per
+// block -- small sorts pay for fewer blocks at every grid barrier.
 template <typename K>
-int coop_grid(K kernel) {
-    static int cached[64] = {0};
+int coop_grid(K kernel, int n) {
+    static int cached[64][2] = {};
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev < 0 || dev >= 64) dev = 0;
-    if (!cached[dev]) {
+    if (!cached[dev][0]) {
         int per_sm = 0, sms = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kCoopThreads, 0);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cached[dev] = std::max(1, std::min(per_sm, 4)) * sms;
+        cached[dev][0] = std::max(1, std::min(per_sm, 4)) * sms;
+        cached[dev][1] = sms;
     }
-    return cached[dev];
+    const int want = std::max(cached[dev][1], (int)div_up((uint32_t)std::max(n, 1), 2048u));
+    return std::min(cached[dev][0], want);
 }
 
 constexpr int kMaxCoopGrid = 4 * 256;  // workspace bound (<= 4 blocks/SM on <= 256 SMs)
@@ -238,7 +242,7 @@ void exclusive_scan_u32(const uint32_t* in, uint32_t* out, int n, uint32_t* tota
         if (total) cudaMemsetAsync(total, 0, sizeof(uint32_t), st);
         return;
     }
-    const int G = std::min(coop_grid(scan_coop_kernel), kMaxCoopGrid);
+    const int G = std::min(coop_grid(scan_coop_kernel, n), kMaxCoopGrid);
     void* args[] = {(void*)&in, (void*)&out, (void*)&n, (void*)&n_dev, (void*)&total, (void*)&ws};
     cudaLaunchCooperativeKernel((void*)scan_coop_kernel, G, kCoopThreads, args, 0, st);
     count_launch();
@@ -265,7 +269,7 @@ int radix_sort_pairs(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_
     a.npasses = npasses;
     a.hist = ws;
     a.rowsum = ws + 256 * kMaxCoopGrid;
-    const int G = std::min(coop_grid(radix_sort_coop_kernel), kMaxCoopGrid);
+    const int G = std::min(coop_grid(radix_sort_coop_kernel, n), kMaxCoopGrid);
     void* args[] = {(void*)&a};
     cudaLaunchCooperativeKernel((void*)radix_sort_coop_kernel, G, kCoopThreads, args, 0, st);
     count_launch();
