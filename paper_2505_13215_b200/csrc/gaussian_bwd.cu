@@ -126,7 +126,11 @@ __global__ void __launch_bounds__(128, 3) gaussian_bwd_kernel(
     const int i = dyn ? gid : gid - n4;
     const float* P = dyn ? p4 : p3;
     const int64_t cap = dyn ? cap4 : cap3;
-    auto prm = [&](int row) { return (double)P[(int64_t)row * cap + i]; };
+    // all geometry rows loaded up front (independent loads in flight together)
+    float pg[R4_SH];
+#pragma unroll
+    for (int r = 0; r < R4_SH; ++r) pg[r] = (dyn || r < R3_SH) ? P[(int64_t)r * cap + i] : 0.0f;
+    auto prm = [&](int row) { return (double)pg[row]; };
     const double* cn = conic_src + (size_t)j * conic_stride;
     const double C[2][2] = {{cn[0], cn[1]}, {cn[2], cn[3]}};
     // K6's conic-free sums -> d_screen = alpha * C . (sum h dx, sum h dy) and
