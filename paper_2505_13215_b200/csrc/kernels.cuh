@@ -32,6 +32,7 @@ __global__ void compact_instances_kernel(const uint32_t* __restrict__ keys, cons
 __global__ void tile_ranges_kernel(const uint32_t* __restrict__ keys, int n, uint2* __restrict__ ranges);
 __global__ void tile_ranges_dev_kernel(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ n_dev,
                                        uint2* __restrict__ ranges);
+template <bool kCount>
 __global__ void raster_fwd_kernel(const uint2* __restrict__ ranges, const uint32_t* __restrict__ inst_val,
                                   const SplatFast* __restrict__ fast, const SplatRec* __restrict__ exact, int W, int H,
                                   int tiles_x, float bg_r, float bg_g, float bg_b, float* __restrict__ out_rgb,

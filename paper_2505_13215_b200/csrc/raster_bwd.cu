@@ -198,8 +198,11 @@ __global__ void __launch_bounds__(kThreadsB, 7) raster_bwd_kernel(
             // the oracle's a >= 1/255 test (exact: FP64 inside the guard band)
             const float x_skip = __int_as_float(hdr.z), x_keep = col.w;
             bool p0 = b0 && x0 < x_skip, p1 = b1 && x1 < x_skip;
-            if (p0 && x0 >= x_keep) p0 = exact_alpha_passes(e, pcx, pcy0);
-            if (p1 && x1 >= x_keep) p1 = exact_alpha_passes(e, pcx, pcy1);
+            const bool band0 = p0 && x0 >= x_keep, band1 = p1 && x1 >= x_keep;
+            if (band0 || band1) {  // rare
+                if (band0) p0 = exact_alpha_passes(e, pcx, pcy0);
+                if (band1) p1 = exact_alpha_passes(e, pcx, pcy1);
+            }
             // lanes without a contributing pixel hold zeros; skip the
             // reduction when the whole warp is empty
             if (!__any_sync(0xffffffffu, p0 || p1)) continue;

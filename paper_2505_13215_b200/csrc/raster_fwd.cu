@@ -261,9 +261,9 @@ __device__ __forceinline__ void composite_pair(PixFwd& s, bool p, float a, float
     s.T = p ? s.T * om : s.T;
     s.last = p ? idx + 1 : s.last;
     // T and err only change with p, so re-testing an unchanged pixel is a no-op
-    if (s.T < 1.0e-4f * (1.0f + 2.0f * s.err)) {
+    if (s.T < fmaf(2.0e-4f, s.err, 1.0e-4f)) {
         // inside the certified error band of the oracle's T < 1e-4 decision?
-        if (s.T > 1.0e-4f * (1.0f - 2.0f * s.err)) s.flagged = true;
+        if (s.T > fmaf(-2.0e-4f, s.err, 1.0e-4f)) s.flagged = true;
         s.done = true;
     }
 }
@@ -293,6 +293,7 @@ __device__ __forceinline__ void write_pixel(const PixFwd& s, int pix, float bg_r
 // of the last contributor (bit 31 = pixel handed to the FP64 fix-up), the
 // final transmittance (read by the backward) and the optional count /
 // transmittance maps.
+template <bool kCount>  // kCount: per-pixel count of box-covered splats (count_map)
 __global__ void __launch_bounds__(kThreads, 6) raster_fwd_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ inst_val, const SplatFast* __restrict__ fast,
     const SplatRec* __restrict__ exact, int W, int H, int tiles_x, float bg_r, float bg_g, float bg_b,
@@ -333,8 +334,10 @@ __global__ void __launch_bounds__(kThreads, 6) raster_fwd_kernel(
             const bool b0 = colin & !s0.done & ((unsigned)(py0 - y0) <= wy);
             const bool b1 = colin & !s1.done & ((unsigned)(py1 - y0) <= wy);
             if (!(b0 || b1)) continue;
-            s0.count += b0;
-            s1.count += b1;
+            if (kCount) {
+                s0.count += b0;
+                s1.count += b1;
+            }
             const float4 L = sb.chol[k], c = sb.col[k];
             const SplatRec* e = exact + sb.j[k];
             const float eps_s = __int_as_float(hdr.w);
@@ -353,8 +356,11 @@ __global__ void __launch_bounds__(kThreads, 6) raster_fwd_kernel(
             // the oracle's a >= 1/255 test (exact: FP64 inside the guard band)
             const float x_skip = __int_as_float(hdr.z), x_keep = c.w;
             bool p0 = b0 && x0 < x_skip, p1 = b1 && x1 < x_skip;
-            if (p0 && x0 >= x_keep) p0 = exact_alpha_passes(e, pcx, pcy0);
-            if (p1 && x1 >= x_keep) p1 = exact_alpha_passes(e, pcx, pcy1);
+            const bool band0 = p0 && x0 >= x_keep, band1 = p1 && x1 >= x_keep;
+            if (band0 || band1) {  // rare
+                if (band0) p0 = exact_alpha_passes(e, pcx, pcy0);
+                if (band1) p1 = exact_alpha_passes(e, pcx, pcy1);
+            }
             if (!(p0 || p1)) continue;
             const float a0 = L.w * fast_exp2_neg(p0 ? x0 : 128.0f), a1 = L.w * fast_exp2_neg(p1 ? x1 : 128.0f);
             const float e1 = fabsf(eps_s);
@@ -369,6 +375,13 @@ __global__ void __launch_bounds__(kThreads, 6) raster_fwd_kernel(
         write_pixel(s1, py1 * W + px, bg_r, bg_g, bg_b, out_rgb, out_last, out_tfinal, out_trans, out_count, fix_list,
                     fix_count);
 }
+
+template __global__ void raster_fwd_kernel<false>(const uint2*, const uint32_t*, const SplatFast*, const SplatRec*,
+                                                   int, int, int, float, float, float, float*, uint32_t*, float*,
+                                                   float*, uint32_t*, uint32_t*, uint32_t*);
+template __global__ void raster_fwd_kernel<true>(const uint2*, const uint32_t*, const SplatFast*, const SplatRec*,
+                                                  int, int, int, float, float, float, float*, uint32_t*, float*,
+                                                  float*, uint32_t*, uint32_t*, uint32_t*);
 
 // Exact FP64 recomposite of the flagged pixels (raster.cpp:123-148), one warp
 // per pixel over 32-splat chunks (exact_chunk: lane-parallel FP64 alphas, the
