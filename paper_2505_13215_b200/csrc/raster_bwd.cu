@@ -71,6 +71,10 @@ __device__ __forceinline__ float warp_sum(float v) {
 // K7 turns [4..8] into d_screen = alpha * conic . ([4],[5]) and
 // d_conic = -alpha/2 * ([6] [7]; [7] [8]) (backward.cpp:212-221).
 constexpr int kAccStride = 12;
+#ifndef HGS_DIRECT_LANES
+#define HGS_DIRECT_LANES 4
+#endif
+constexpr int kDirectLanes = HGS_DIRECT_LANES;  // contributing lanes up to which atomics replace the reduction
 constexpr int kThreadsB = 128;  // two pixels per thread
 
 __device__ __forceinline__ void red_add(float* addr, float v) {
@@ -221,11 +225,19 @@ __global__ void __launch_bounds__(kThreadsB, 7) raster_bwd_kernel(
             v[6] = fmaf(hx0, dx0, hx1 * dx1);
             v[7] = fmaf(hx0, dy0, hx1 * dy1);
             v[8] = fmaf(hy0, dy0, hy1 * dy1);
-            const float r8 = transpose_reduce8(v);
-            const float r9 = warp_sum(v[8]);
             float* dst = accum + (size_t)sb.j[k] * kAccStride;
-            if ((lane & 3) == 0) red_add(dst + (lane >> 2), r8);
-            else if (lane == 1) red_add(dst + 8, r9);
+            const unsigned am = __ballot_sync(0xffffffffu, p0 || p1);
+            if (__popc(am) <= kDirectLanes) {
+                // few contributing lanes: their own atomics are cheaper than the butterfly
+                if (p0 || p1)
+#pragma unroll
+                    for (int q = 0; q < 9; ++q) red_add(dst + q, v[q]);
+            } else {
+                const float r8 = transpose_reduce8(v);
+                const float r9 = warp_sum(v[8]);
+                if ((lane & 3) == 0) red_add(dst + (lane >> 2), r8);
+                else if (lane == 1) red_add(dst + 8, r9);
+            }
         }
     }
 }
