@@ -20,8 +20,6 @@ namespace hgs {
 namespace {
 
 constexpr int kWin = 11, kHalf = 5;
-constexpr int kTX = 32, kTY = 16;  // outputs per CTA
-constexpr int kSX = kTX + 2 * kHalf, kSY = kTY + 2 * kHalf;
 
 __constant__ float c_win[kWin];
 
@@ -57,19 +55,29 @@ void set_ssim_window() {
     cudaMemcpyToSymbol(c_win, g, sizeof(g));
 }
 
-// grid: (ceil(vw/32), ceil(vh/16), 3 channels); block 256.
-// a, b: HWC float images.  Writes maps (3 x planes of vw*vh per channel) and
-// the per-block SSIM sums.
+// Both passes are register-blocked: a thread produces 4 consecutive outputs
+// of a 1D pass from 14 staged inputs (sliding window), so each shared-memory
+// value is read once per 4 outputs instead of once per tap.  CTA tile: 32x32
+// outputs, 256 threads (8 column groups x 32 rows horizontally, 32 columns x
+// 8 row groups vertically).
+constexpr int kB = 4;                 // outputs per thread and pass
+constexpr int kT = 32;                // CTA tile (outputs) per side
+constexpr int kS = kT + 2 * kHalf;    // staged rows / columns (42)
+constexpr int kSpan = kB + kWin - 1;  // inputs per blocked output group (14)
+
+// grid: (ceil(vw/32), ceil(vh/32), 3 channels); block 256.
+// a, b: HWC float images.  Writes maps (3 planes of vw*vh per channel) and
+// the SSIM sum.
 __global__ void __launch_bounds__(256) ssim_fwd_kernel(const float* __restrict__ a, const float* __restrict__ b, int W,
                                                        int H, float* __restrict__ maps, double* __restrict__ ssim_sum) {
-    __shared__ float sa[kSY][kSX], sb[kSY][kSX];
-    __shared__ float h[5][kSY][kTX];
+    __shared__ float sa[kS][kS + 1], sb[kS][kS + 1];
+    __shared__ float h[5][kS][kT + 1];
     __shared__ float red[8];
     const int c = blockIdx.z;
     const int vw = W - kWin + 1, vh = H - kWin + 1;
-    const int ox = blockIdx.x * kTX, oy = blockIdx.y * kTY;
-    for (int e = threadIdx.x; e < kSX * kSY; e += blockDim.x) {
-        const int lx = e % kSX, ly = e / kSX;
+    const int ox = blockIdx.x * kT, oy = blockIdx.y * kT;
+    for (int e = threadIdx.x; e < kS * kS; e += blockDim.x) {
+        const int lx = e % kS, ly = e / kS;
         const int x = ox + lx, y = oy + ly;
         float va = 0.f, vb = 0.f;
         if (x < W && y < H) {
@@ -80,78 +88,103 @@ __global__ void __launch_bounds__(256) ssim_fwd_kernel(const float* __restrict__
         sb[ly][lx] = vb;
     }
     __syncthreads();
-    // horizontal pass: for each of the kSY rows and kTX output columns
-    for (int e = threadIdx.x; e < kSY * kTX; e += blockDim.x) {
-        const int lx = e % kTX, ly = e / kTX;
-        float m0 = 0.f, m1 = 0.f, m2 = 0.f, m3 = 0.f, m4 = 0.f;
+    // horizontal: (row, group of 4 output columns)
+    for (int e = threadIdx.x; e < kS * (kT / kB); e += blockDim.x) {
+        const int g = e % (kT / kB), ly = e / (kT / kB);
+        const int x0 = g * kB;
+        float m[kB][5];
 #pragma unroll
-        for (int j = 0; j < kWin; ++j) {
-            const float w = c_win[j];
-            const float va = sa[ly][lx + j], vb = sb[ly][lx + j];
-            m0 = fmaf(w, va, m0);
-            m1 = fmaf(w, vb, m1);
-            m2 = fmaf(w * va, va, m2);
-            m3 = fmaf(w * vb, vb, m3);
-            m4 = fmaf(w * va, vb, m4);
+        for (int o = 0; o < kB; ++o)
+#pragma unroll
+            for (int q = 0; q < 5; ++q) m[o][q] = 0.f;
+#pragma unroll
+        for (int j = 0; j < kSpan; ++j) {
+            const float va = sa[ly][x0 + j], vb = sb[ly][x0 + j];
+            const float aa = va * va, bb = vb * vb, ab = va * vb;
+#pragma unroll
+            for (int o = 0; o < kB; ++o) {
+                const int t = j - o;
+                if (t < 0 || t >= kWin) continue;
+                const float w = c_win[t];
+                m[o][0] = fmaf(w, va, m[o][0]);
+                m[o][1] = fmaf(w, vb, m[o][1]);
+                m[o][2] = fmaf(w, aa, m[o][2]);
+                m[o][3] = fmaf(w, bb, m[o][3]);
+                m[o][4] = fmaf(w, ab, m[o][4]);
+            }
         }
-        h[0][ly][lx] = m0;
-        h[1][ly][lx] = m1;
-        h[2][ly][lx] = m2;
-        h[3][ly][lx] = m3;
-        h[4][ly][lx] = m4;
+#pragma unroll
+        for (int o = 0; o < kB; ++o)
+#pragma unroll
+            for (int q = 0; q < 5; ++q) h[q][ly][x0 + o] = m[o][q];
     }
     __syncthreads();
+    // vertical: (column, group of 4 output rows) -> SSIM and its gradient maps
     float local = 0.f;
-    for (int e = threadIdx.x; e < kTX * kTY; e += blockDim.x) {
-        const int lx = e % kTX, ly = e / kTX;
-        const int vx = ox + lx, vy = oy + ly;
-        if (vx >= vw || vy >= vh) continue;
-        float mu_a = 0.f, mu_b = 0.f, aa = 0.f, bb = 0.f, ab = 0.f;
+    {
+        const int lx = threadIdx.x % kT, y0 = (threadIdx.x / kT) * kB;
+        float m[kB][5];
 #pragma unroll
-        for (int i = 0; i < kWin; ++i) {
-            const float w = c_win[i];
-            mu_a = fmaf(w, h[0][ly + i][lx], mu_a);
-            mu_b = fmaf(w, h[1][ly + i][lx], mu_b);
-            aa = fmaf(w, h[2][ly + i][lx], aa);
-            bb = fmaf(w, h[3][ly + i][lx], bb);
-            ab = fmaf(w, h[4][ly + i][lx], ab);
+        for (int o = 0; o < kB; ++o)
+#pragma unroll
+            for (int q = 0; q < 5; ++q) m[o][q] = 0.f;
+#pragma unroll
+        for (int i = 0; i < kSpan; ++i) {
+            float v[5];
+#pragma unroll
+            for (int q = 0; q < 5; ++q) v[q] = h[q][y0 + i][lx];
+#pragma unroll
+            for (int o = 0; o < kB; ++o) {
+                const int t = i - o;
+                if (t < 0 || t >= kWin) continue;
+                const float w = c_win[t];
+#pragma unroll
+                for (int q = 0; q < 5; ++q) m[o][q] = fmaf(w, v[q], m[o][q]);
+            }
         }
-        const float C1 = 1e-4f, C2 = 9e-4f;
-        const float var_a = aa - mu_a * mu_a, var_b = bb - mu_b * mu_b, cov = ab - mu_a * mu_b;
-        const float a1 = 2.f * mu_a * mu_b + C1, a2 = 2.f * cov + C2;
-        const float b1 = mu_a * mu_a + mu_b * mu_b + C1, b2 = var_a + var_b + C2;
-        const float denom = b1 * b2;
-        const float s = a1 * a2 / denom;
-        local += s;
-        const float d_mu = (a2 / denom) * 2.f * mu_b - (s / b1) * 2.f * mu_a;
-        const float d_var = -s / b2;
-        const float d_cov = 2.f * a1 / denom;
+        const int vx = ox + lx;
         const size_t plane = (size_t)vw * vh;
-        const size_t o = (size_t)c * 3 * plane + (size_t)vy * vw + vx;
-        maps[o] = d_mu - 2.f * d_var * mu_a - d_cov * mu_b;
-        maps[o + plane] = d_var;
-        maps[o + 2 * plane] = d_cov;
+#pragma unroll
+        for (int o = 0; o < kB; ++o) {
+            const int vy = oy + y0 + o;
+            if (vx >= vw || vy >= vh) continue;
+            const float mu_a = m[o][0], mu_b = m[o][1];
+            const float C1 = 1e-4f, C2 = 9e-4f;
+            const float var_a = m[o][2] - mu_a * mu_a, var_b = m[o][3] - mu_b * mu_b, cov = m[o][4] - mu_a * mu_b;
+            const float a1 = 2.f * mu_a * mu_b + C1, a2 = 2.f * cov + C2;
+            const float b1 = mu_a * mu_a + mu_b * mu_b + C1, b2 = var_a + var_b + C2;
+            const float denom = b1 * b2;
+            const float sv = a1 * a2 / denom;
+            local += sv;
+            const float d_mu = (a2 / denom) * 2.f * mu_b - (sv / b1) * 2.f * mu_a;
+            const float d_var = -sv / b2;
+            const float d_cov = 2.f * a1 / denom;
+            const size_t off = (size_t)c * 3 * plane + (size_t)vy * vw + vx;
+            maps[off] = d_mu - 2.f * d_var * mu_a - d_cov * mu_b;
+            maps[off + plane] = d_var;
+            maps[off + 2 * plane] = d_cov;
+        }
     }
     const float tot = block_sum(local, red);
     if (threadIdx.x == 0) atomicAdd(ssim_sum, (double)tot);
 }
 
-// grid: (ceil(W/32), ceil(H/16), 3); dL/dimage = (1-l) sign(a-b)/n - l dSSIM/da.
+// grid: (ceil(W/32), ceil(H/32), 3); dL/dimage = (1-l) sign(a-b)/n - l dSSIM/da.
 __global__ void __launch_bounds__(256) ssim_bwd_kernel(const float* __restrict__ a, const float* __restrict__ b, int W,
                                                        int H, const float* __restrict__ maps, float lambda,
                                                        int with_ssim, float* __restrict__ grad,
                                                        double* __restrict__ l1_sum) {
-    __shared__ float sm[3][kSY][kSX];
-    __shared__ float h[3][kSY][kTX];
+    __shared__ float sm[3][kS][kS + 1];
+    __shared__ float h[3][kS][kT + 1];
     __shared__ float red[8];
     const int c = blockIdx.z;
     const int vw = W - kWin + 1, vh = H - kWin + 1;
-    const int ox = blockIdx.x * kTX, oy = blockIdx.y * kTY;
+    const int ox = blockIdx.x * kT, oy = blockIdx.y * kT;
     const size_t plane = with_ssim ? (size_t)vw * vh : 0;
     if (with_ssim) {
         // maps at valid positions (x - 10 .. x) contribute to pixel x
-        for (int e = threadIdx.x; e < kSX * kSY; e += blockDim.x) {
-            const int lx = e % kSX, ly = e / kSX;
+        for (int e = threadIdx.x; e < kS * kS; e += blockDim.x) {
+            const int lx = e % kS, ly = e / kS;
             const int vx = ox + lx - 2 * kHalf, vy = oy + ly - 2 * kHalf;
             float m0 = 0.f, m1 = 0.f, m2 = 0.f;
             if (vx >= 0 && vy >= 0 && vx < vw && vy < vh) {
@@ -165,47 +198,68 @@ __global__ void __launch_bounds__(256) ssim_bwd_kernel(const float* __restrict__
             sm[2][ly][lx] = m2;
         }
         __syncthreads();
-        for (int e = threadIdx.x; e < kSY * kTX; e += blockDim.x) {
-            const int lx = e % kTX, ly = e / kTX;
-            float s0 = 0.f, s1 = 0.f, s2 = 0.f;
+        for (int e = threadIdx.x; e < kS * (kT / kB); e += blockDim.x) {
+            const int g = e % (kT / kB), ly = e / (kT / kB);
+            const int x0 = g * kB;
+            float s3[kB][3];
 #pragma unroll
-            for (int j = 0; j < kWin; ++j) {
-                // pixel x gets window weight w[x - vx] from the map at vx
-                const float w = c_win[kWin - 1 - j];
-                s0 = fmaf(w, sm[0][ly][lx + j], s0);
-                s1 = fmaf(w, sm[1][ly][lx + j], s1);
-                s2 = fmaf(w, sm[2][ly][lx + j], s2);
+            for (int o = 0; o < kB; ++o) s3[o][0] = s3[o][1] = s3[o][2] = 0.f;
+#pragma unroll
+            for (int j = 0; j < kSpan; ++j) {
+                const float v0 = sm[0][ly][x0 + j], v1 = sm[1][ly][x0 + j], v2 = sm[2][ly][x0 + j];
+#pragma unroll
+                for (int o = 0; o < kB; ++o) {
+                    const int t = j - o;
+                    if (t < 0 || t >= kWin) continue;
+                    // pixel x gets window weight w[x - vx] from the map at vx
+                    const float w = c_win[kWin - 1 - t];
+                    s3[o][0] = fmaf(w, v0, s3[o][0]);
+                    s3[o][1] = fmaf(w, v1, s3[o][1]);
+                    s3[o][2] = fmaf(w, v2, s3[o][2]);
+                }
             }
-            h[0][ly][lx] = s0;
-            h[1][ly][lx] = s1;
-            h[2][ly][lx] = s2;
+#pragma unroll
+            for (int o = 0; o < kB; ++o) {
+                h[0][ly][x0 + o] = s3[o][0];
+                h[1][ly][x0 + o] = s3[o][1];
+                h[2][ly][x0 + o] = s3[o][2];
+            }
         }
         __syncthreads();
     }
     const float inv_n = 1.0f / (float)((size_t)W * H * 3);
     const float inv_nv = with_ssim ? 1.0f / (float)((size_t)vw * vh * 3) : 0.f;
     float local = 0.f;
-    for (int e = threadIdx.x; e < kTX * kTY; e += blockDim.x) {
-        const int lx = e % kTX, ly = e / kTX;
-        const int x = ox + lx, y = oy + ly;
+    const int lx = threadIdx.x % kT, y0 = (threadIdx.x / kT) * kB;
+    float g3[kB][3];
+#pragma unroll
+    for (int o = 0; o < kB; ++o) g3[o][0] = g3[o][1] = g3[o][2] = 0.f;
+    if (with_ssim) {
+#pragma unroll
+        for (int i = 0; i < kSpan; ++i) {
+            const float v0 = h[0][y0 + i][lx], v1 = h[1][y0 + i][lx], v2 = h[2][y0 + i][lx];
+#pragma unroll
+            for (int o = 0; o < kB; ++o) {
+                const int t = i - o;
+                if (t < 0 || t >= kWin) continue;
+                const float w = c_win[kWin - 1 - t];
+                g3[o][0] = fmaf(w, v0, g3[o][0]);
+                g3[o][1] = fmaf(w, v1, g3[o][1]);
+                g3[o][2] = fmaf(w, v2, g3[o][2]);
+            }
+        }
+    }
+    const int x = ox + lx;
+#pragma unroll
+    for (int o = 0; o < kB; ++o) {
+        const int y = oy + y0 + o;
         if (x >= W || y >= H) continue;
         const size_t p = ((size_t)y * W + x) * 3 + c;
         const float va = a[p], vb = b[p];
         const float d = va - vb;
         local += fabsf(d);
         float gsum = (1.0f - lambda) * ((d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f)) * inv_n);
-        if (with_ssim) {
-            float g0 = 0.f, g1 = 0.f, g2 = 0.f;
-#pragma unroll
-            for (int i = 0; i < kWin; ++i) {
-                const float w = c_win[kWin - 1 - i];
-                g0 = fmaf(w, h[0][ly + i][lx], g0);
-                g1 = fmaf(w, h[1][ly + i][lx], g1);
-                g2 = fmaf(w, h[2][ly + i][lx], g2);
-            }
-            const float dssim = (g0 + 2.f * va * g1 + vb * g2) * inv_nv;
-            gsum -= lambda * dssim;
-        }
+        if (with_ssim) gsum -= lambda * ((g3[o][0] + 2.f * va * g3[o][1] + vb * g3[o][2]) * inv_nv);
         grad[p] = gsum;
     }
     const float tot = block_sum(local, red);

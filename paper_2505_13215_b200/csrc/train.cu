@@ -170,12 +170,12 @@ hgs_status run_loss(hgs_ctx* ctx, const float* gt, double lambda, double* sums =
     prof_begin(ctx, PH_LOSS);
     if (with_ssim) {
         CK(ctx->loss_ws.ensure((size_t)vw * vh * 9 * 4));
-        dim3 g((vw + 31) / 32, (vh + 15) / 16, 3);
+        dim3 g((vw + 31) / 32, (vh + 31) / 32, 3);
         ssim_fwd_kernel<<<g, 256, 0, st>>>(ctx->img.as<float>(), gt, W, H, ctx->loss_ws.as<float>(), &sums[0]);
         count_launch();
         CKL();
     }
-    dim3 gb((W + 31) / 32, (H + 15) / 16, 3);
+    dim3 gb((W + 31) / 32, (H + 31) / 32, 3);
     ssim_bwd_kernel<<<gb, 256, 0, st>>>(ctx->img.as<float>(), gt, W, H, ctx->loss_ws.as<float>(), (float)lambda,
                                         with_ssim ? 1 : 0, ctx->lgrad.as<float>(), &sums[1]);
     count_launch();
