@@ -1664,6 +1664,12 @@ double hgso_rng_normal(void* rng) {
     std::normal_distribution<double> nd(0.0, 1.0);
     return nd(*static_cast<std::mt19937_64*>(rng));
 }
+// train.cpp:392 `std::uniform_int_distribution<std::size_t> pick(0, n - 1)`
+uint64_t hgso_rng_index(void* rng, uint64_t lo, uint64_t hi) {
+    std::uniform_int_distribution<std::size_t> pick(lo, hi);
+    return pick(*static_cast<std::mt19937_64*>(rng));
+}
+uint64_t hgso_rng_raw(void* rng) { return (*static_cast<std::mt19937_64*>(rng))(); }
 
 // tests/oracles.hpp:26-29
 void hgso_random_quat(void* rngp, double q[4]) {

@@ -117,6 +117,8 @@ void *hgso_rng_new(uint64_t seed);
 void hgso_rng_free(void *rng);
 double hgso_rng_uniform(void *rng);  /* uniform_real_distribution(0,1) */
 double hgso_rng_normal(void *rng);   /* a fresh normal_distribution(0,1) draw */
+uint64_t hgso_rng_index(void *rng, uint64_t lo, uint64_t hi); /* uniform_int_distribution<size_t>(lo, hi) */
+uint64_t hgso_rng_raw(void *rng);    /* one raw mt19937_64 output */
 /* random_scene: caller passes buffers sized for (n_static, n_dynamic, degree) */
 void hgso_random_scene(void *rng, int n_static, int n_dynamic, int sh_degree, hgso_scene *out);
 void hgso_random_quat(void *rng, double q[4]);

@@ -120,6 +120,10 @@ def lib():
         for f in ("hgso_rng_uniform", "hgso_rng_normal"):
             getattr(L, f).restype = C.c_double
             getattr(L, f).argtypes = [C.c_void_p]
+        L.hgso_rng_index.restype = C.c_uint64
+        L.hgso_rng_index.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64]
+        L.hgso_rng_raw.restype = C.c_uint64
+        L.hgso_rng_raw.argtypes = [C.c_void_p]
         L.hgso_random_scene.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(_Scene)]
         L.hgso_random_quat.argtypes = [C.c_void_p, _dp]
         L.hgso_random_camera.argtypes = [C.c_void_p, C.c_int, C.c_int, C.POINTER(_Camera)]
@@ -248,6 +252,13 @@ class Rng:
 
     def normal(self) -> float:
         return lib().hgso_rng_normal(self._h)
+
+    def index(self, lo: int, hi: int) -> int:
+        """std::uniform_int_distribution<size_t>(lo, hi) (train.cpp:392)."""
+        return lib().hgso_rng_index(self._h, lo, hi)
+
+    def raw(self) -> int:
+        return lib().hgso_rng_raw(self._h)
 
     def random_quat(self) -> np.ndarray:
         q = np.zeros(4)

@@ -155,3 +155,165 @@ def sample_batches(n_samples: int, batch_size: int, iterations: int, seed: int) 
     samples (camera, frame) pairs uniformly; every rank draws the same list)."""
     rng = np.random.default_rng(seed)
     return [list(rng.integers(0, n_samples, batch_size)) for _ in range(iterations)]
+
+
+# --------------------------------------------------------------------------
+# train_scene: the reference's training loop (train.cpp:382-494), device
+# resident.  Same configuration, same batch schedule (std::mt19937_64 +
+# uniform_int_distribution restated bit-exactly in rng.py), same cadence of
+# Adam / decay / sweep / probe; densification is not on this tier's path
+# (SURVEY.md 8f-1) and is rejected explicitly when the config asks for it.
+
+from dataclasses import dataclass, field  # noqa: E402
+
+from .rng import MT19937_64, uniform_index  # noqa: E402
+
+
+@dataclass
+class TrainConfig:  # train.hpp:23-49
+    iterations: int = 2000
+    batch_size: int = 2
+    warmup_iters: int = 500
+    densify_interval: int = 100
+    densify_stop_iter: int = 1500
+    grad_threshold: float = 0.02
+    opacity_prune_eps: float = 0.005
+    tau: float = 0.5
+    conversion_enabled: bool = True
+    ssim_lambda: float = 0.2
+    lrs: LearningRates = field(default_factory=LearningRates)
+    opacity_reset_enabled: bool = False
+    opacity_reset_interval: int = 600
+    seed: int = 0
+    sh_degree: int = 1
+    weight_cutoff: float = 0.05
+    max_gaussians: int = 20000
+    clone_size_frac: float = 0.01
+    split_factor: float = 1.6
+    num_threads: int = 1
+    probe_interval: int = 100
+    init_temporal_scale: float = 0.1
+    init_opacity: float = 0.1
+
+    def validate(self) -> None:  # train.cpp:76-85 (TrainConfig::validate)
+        if self.warmup_iters > self.iterations and self.iterations > 0:
+            raise ValueError("TrainConfig: warmup_iters must be <= iterations")
+        if self.densify_interval < 1:
+            raise ValueError("TrainConfig: densify_interval must be >= 1")
+        if self.ssim_lambda < 0.0 or self.ssim_lambda > 1.0:
+            raise ValueError("TrainConfig: ssim_lambda must be in [0,1]")
+        if self.batch_size < 1:
+            raise ValueError("TrainConfig: batch_size must be >= 1")
+        if not self.tau > 0.0:
+            raise ValueError("TrainConfig: tau must be positive")
+
+    def densifies(self) -> bool:
+        """Would train.cpp:456-458 call densify_and_prune at some iteration?"""
+        first = max(self.warmup_iters, 1)
+        first += (-first) % self.densify_interval
+        return first <= min(self.iterations, self.densify_stop_iter)
+
+
+@dataclass
+class Frame:  # data_io.hpp Frame: one image of one camera at one time
+    time: float
+    image: np.ndarray  # (H, W, 3) linear RGB
+
+
+@dataclass
+class MultiViewDataset:  # data_io.hpp MultiViewDataset (the fields the loop reads)
+    cameras: list
+    frames: list  # frames[camera][frame] -> Frame
+    background: tuple = (0.0, 0.0, 0.0)
+    duration_seconds: float = 1.0
+
+    def total_frames(self) -> int:
+        return sum(len(f) for f in self.frames)
+
+
+@dataclass
+class TrainLogRow:  # train.hpp:51-58
+    iter: int = 0
+    loss: float = 0.0
+    probe_psnr: float = -1.0
+    n_static: int = 0
+    n_dynamic: int = 0
+    conversions: int = 0
+    wall_seconds: float = 0.0
+
+
+@dataclass
+class TrainResult:  # train.hpp:80-84 (state = Adam moments m, v and the step)
+    scene: HybridScene
+    log: list
+    state: tuple
+
+
+def psnr(a: np.ndarray, b: np.ndarray) -> float:
+    """metrics.cpp:91-101: 10 log10(1 / MSE) over all channels (inf if equal)."""
+    mse = float(np.mean((np.asarray(a, np.float64) - np.asarray(b, np.float64)) ** 2))
+    return math.inf if mse == 0.0 else 10.0 * math.log10(1.0 / mse)
+
+
+def train_scene(scene: HybridScene, dataset: MultiViewDataset, cfg: TrainConfig, ctx: Context | None = None,
+                state: tuple | None = None, on_row=None) -> TrainResult:
+    """train.cpp:382-494 on the device: ``state`` = (m, v, step) to continue
+    from (checkpoints), ``on_row`` is called with each TrainLogRow."""
+    import time as _time
+
+    import torch
+
+    if not dataset.cameras or dataset.total_frames() == 0:  # train.cpp:367-368
+        raise ValueError("train: dataset is empty")
+    cfg.validate()
+    if cfg.densifies():
+        raise NotImplementedError("train_scene: densification (train.cpp:182-299) is not on this tier's "
+                                  "hot path (SURVEY.md 8f-1); use a config whose densify window is empty "
+                                  "(e.g. densify_stop_iter < warmup_iters, as the c3 benchmark run)")
+    from .api import default_context
+
+    ctx = ctx or default_context()
+    scene = scene.copy()
+    scene.tau = cfg.tau
+    ctx.upload(scene)
+    if state is not None:
+        ctx.set_adam_state(*state)
+    dev = torch.device("cuda", ctx.device)
+    samples = [(c, f) for c in range(len(dataset.frames)) for f in range(len(dataset.frames[c]))]
+    gts = {(c, f): torch.as_tensor(np.ascontiguousarray(dataset.frames[c][f].image, dtype=np.float32), device=dev)
+           for c, f in samples}
+    cams = [_capi.camera_struct(c) for c in dataset.cameras]
+    rng = MT19937_64(cfg.seed)
+    probe = (0, len(dataset.frames[0]) // 2)
+    o = _capi.TrainOpts()
+    o.ssim_lambda, o.weight_cutoff = cfg.ssim_lambda, cfg.weight_cutoff
+    o.lrs = cfg.lrs.struct()
+    for i in range(3):
+        o.bg[i] = float(dataset.background[i])
+    B = cfg.batch_size
+    log = []
+    t0 = _time.perf_counter()
+    for it in range(1, cfg.iterations + 1):
+        batch = [samples[uniform_index(rng, 0, len(samples) - 1)] for _ in range(B)]
+        o.mean_lr_scale = math.pow(cfg.lrs.mean_final_ratio, it / cfg.iterations)  # train.cpp:449
+        karr = (_capi.Camera_ * B)(*[cams[c] for c, _ in batch])
+        tarr = (C.c_double * B)(*[dataset.frames[c][f].time for c, f in batch])
+        garr = (_capi._fp * B)(*[C.cast(C.c_void_p(gts[b].data_ptr()), _capi._fp) for b in batch])
+        loss = C.c_double()
+        # renders, losses, backward scaled by 1/B, densify statistics, NumericAbort, Adam
+        ctx._check(ctx._lib.hgs_train_step(ctx.handle, B, karr, tarr, garr, B, C.byref(o), 1, C.byref(loss)))
+        row = TrainLogRow(iter=it, loss=loss.value / B)
+        if it >= cfg.warmup_iters and it % cfg.densify_interval == 0 and cfg.conversion_enabled:
+            moved, _ = ctx.sweep_convert()  # train.cpp:466-472 (Adam rows remapped on the device)
+            row.conversions = len(moved)
+        if cfg.probe_interval > 0 and (it % cfg.probe_interval == 0 or it == cfg.iterations):
+            pf = dataset.frames[probe[0]][probe[1]]
+            img = ctx.render(dataset.cameras[probe[0]], pf.time, dataset.background,
+                             weight_cutoff=cfg.weight_cutoff)["rgb"]
+            row.probe_psnr = psnr(img, pf.image)
+        row.n_dynamic, row.n_static = ctx.counts()
+        row.wall_seconds = _time.perf_counter() - t0
+        log.append(row)
+        if on_row:
+            on_row(row)
+    return TrainResult(scene=ctx.download(), log=log, state=ctx.adam_state())

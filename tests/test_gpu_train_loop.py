@@ -1,0 +1,90 @@
+"""train_scene: the reference training loop (train.cpp:382-494) on the device.
+
+Pinned pieces: the batch schedule (rng.py, tests/test_rng.py), the first
+iteration's loss against the oracle on the same batch, the sweep cadence and
+pool bookkeeping, the probe PSNR and NumericAbort propagation."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2505_13215_b200.rng import MT19937_64, uniform_index
+from paper_2505_13215_b200.scene import ring_camera, synthetic_scene
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    from paper_2505_13215_b200.api import Context
+
+    c = Context(0)
+    yield c
+    c.close()
+
+
+def _dataset(ctx, n_cams=4, n_frames=3, W=64, H=48):
+    from paper_2505_13215_b200.train import Frame, MultiViewDataset, quantize_8bit
+
+    target = synthetic_scene(1200, 400, 1, seed=41, density_n=1500)
+    cams = [ring_camera(41, W, H, index=i, n_ring=n_cams) for i in range(n_cams)]
+    ctx.upload(target)
+    frames = [[Frame(time=f / max(1, n_frames - 1),
+                     image=quantize_8bit(ctx.render(c, f / max(1, n_frames - 1), (0.2, 0.2, 0.2))["rgb"]
+                                         .astype(np.float64)))
+               for f in range(n_frames)] for c in cams]
+    return MultiViewDataset(cameras=cams, frames=frames, background=(0.2, 0.2, 0.2), duration_seconds=1.0)
+
+
+def test_train_scene_loop(ctx):
+    from paper_2505_13215_b200.train import TrainConfig, train_scene
+
+    ds = _dataset(ctx)
+    init = synthetic_scene(1200, 400, 1, seed=42, density_n=1500, tau=0.3)
+    cfg = TrainConfig(iterations=40, batch_size=2, warmup_iters=10, densify_interval=10, densify_stop_iter=0,
+                      tau=0.3, seed=7, sh_degree=1, probe_interval=10)
+    res = train_scene(init, ds, cfg, ctx=ctx)
+    log = res.log
+    assert [r.iter for r in log] == list(range(1, 41))
+    assert all(math.isfinite(r.loss) for r in log)
+    assert np.mean([r.loss for r in log[-5:]]) < np.mean([r.loss for r in log[:5]])
+    # sweeps at 10, 20, 30, 40 only; the pools shrink / grow by the moved counts
+    assert all(r.conversions == 0 for r in log if r.iter % 10)
+    assert sum(r.conversions for r in log) > 0
+    n0 = init.n4 + init.n3
+    for r in log:
+        assert r.n_static + r.n_dynamic == n0
+    assert log[-1].n_static == init.n3 + sum(r.conversions for r in log)
+    # probe rows
+    assert [r.iter for r in log if r.probe_psnr >= 0] == [10, 20, 30, 40]
+    assert res.scene.n4 == log[-1].n_dynamic and res.state[2] == 40
+
+
+def test_first_iteration_loss_matches_oracle(ctx):
+    """Iteration 1 draws the reference's batch and its mean loss is the
+    oracle's photometric loss of the oracle renders of those views."""
+    from paper_2505_13215_b200.train import TrainConfig, train_scene
+
+    ds = _dataset(ctx)
+    init = synthetic_scene(1200, 400, 1, seed=43, density_n=1500).as_float32_exact()
+    cfg = TrainConfig(iterations=1, batch_size=3, warmup_iters=1, densify_stop_iter=0, seed=11, sh_degree=1,
+                      probe_interval=0, conversion_enabled=False)
+    res = train_scene(init, ds, cfg, ctx=ctx)
+    samples = [(c, f) for c in range(len(ds.frames)) for f in range(len(ds.frames[c]))]
+    g = MT19937_64(cfg.seed)
+    batch = [samples[uniform_index(g, 0, len(samples) - 1)] for _ in range(cfg.batch_size)]
+    ref = np.mean([O.photometric_loss(O.rasterize(init, ds.cameras[c], ds.frames[c][f].time, ds.background)["rgb"],
+                                      ds.frames[c][f].image, 0.2) for c, f in batch])
+    assert res.log[0].loss == pytest.approx(ref, rel=1e-5)
+
+
+def test_train_scene_rejects_densification_and_bad_config(ctx):
+    from paper_2505_13215_b200.train import TrainConfig, train_scene
+
+    ds = _dataset(ctx, n_cams=2, n_frames=1)
+    init = synthetic_scene(100, 50, 1, seed=44)
+    with pytest.raises(NotImplementedError):
+        train_scene(init, ds, TrainConfig(iterations=200, warmup_iters=100, densify_stop_iter=150), ctx=ctx)
+    with pytest.raises(ValueError):
+        train_scene(init, ds, TrainConfig(iterations=10, warmup_iters=20), ctx=ctx)
