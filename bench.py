@@ -319,6 +319,8 @@ def run_ours(args) -> None:
               "rows_avg": (rows4 * scene.n4 + rows3 * scene.n3) / max(1, scene.n4 + scene.n3)}
     rl = roofline(phase_ms, counts, args.steps, peak, peak_kind)
 
+    extra = run_extras(args, ctx, lib, timed, world, rank) if not args.no_extras else None
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(scene, cams[0], times[0], quantize_8bit(tr.gt[0].cpu().numpy().astype(np.float64)))
@@ -337,11 +339,72 @@ def run_ours(args) -> None:
                           "what": "forward render of the device-resident c2 scene, 1352x1014"},
                "gpu_launches": int(launches), "launches_per_step": round(launches / args.steps, 1),
                "roofline": rl, "clocks": clk.summary(), "cpu_baseline": cpu,
-               "render_info": info}
+               "render_info": info, "extra": extra}
         print(json.dumps(out), flush=True)
     ctx.close()
     if dist:
         dist.destroy_process_group()
+
+
+def run_extras(args, ctx, lib, timed, world, rank) -> dict:
+    """The other SURVEY.md 8d configurations, measured the same way (CUDA
+    events on the context stream, W untimed + K timed steps, max over ranks):
+      c1 / c5: forward render throughput (Mpix/s) -- c5 is the render sweep
+               (4M Gaussians, 2048x1088, t = j/49);
+      c4:      training with 8 views per GPU per step (2M Gaussians)."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2505_13215_b200 import _capi
+    from paper_2505_13215_b200.scene import CONFIGS, ring_camera, synthetic_scene
+    from paper_2505_13215_b200.train import DeviceTrainer
+
+    out = {}
+    bg = (C.c_double * 3)(0.2, 0.2, 0.2)
+    for name in ("c1", "c5"):
+        c = CONFIGS[name]
+        scene = synthetic_scene(c["n4"], c["n3"], 3, seed=c["seed"])
+        ctx.upload(scene)
+        cams = [_capi.camera_struct(ring_camera(c["seed"], c["width"], c["height"], index=0, n_ring=16))]
+        ts = [j / 49.0 for j in range(50)] if name == "c5" else [c["t"]]
+
+        def render(i, cams=cams, ts=ts):
+            ctx._check(lib.hgs_render(ctx.handle, C.byref(cams[0]), ts[(i * world + rank) % len(ts)], bg,
+                                      None, None, None, None, None))
+
+        for i in range(len(ts) if name == "c5" else args.warmup):  # also sizes the workspaces
+            render(i)
+        k = max(args.steps, 10)
+        ms = timed(render, k)
+        out[f"{name}_render"] = {"value": round(world * k * c["width"] * c["height"] / (ms / 1e3) / 1e6, 2),
+                                 "unit": "Mpix/s", "ms_per_frame": round(ms / k, 4),
+                                 "config": f"{c['n4'] // 1000}k 4D + {c['n3'] // 1000}k 3D, "
+                                           f"{c['width']}x{c['height']}" + (", t=j/49" if name == "c5" else "")}
+        del scene
+    c = CONFIGS["c4"]
+    scene = synthetic_scene(c["n4"], c["n3"], 3, seed=c["seed"], tau=0.5)
+    target = synthetic_scene(c["n4"], c["n3"], 3, seed=c["seed"] + 1000, tau=0.5)
+    cams = [ring_camera(c["seed"], c["width"], c["height"], index=i, n_ring=16) for i in range(16)]
+    times = [i / 15.0 for i in range(16)]
+    tr = DeviceTrainer(ctx, scene, cams, times, target=target, bg=(0.2, 0.2, 0.2), iterations=1000)
+    del target
+    for v in range(16):
+        ctx.render(cams[v], times[v], (0.2, 0.2, 0.2))
+    per = 8
+
+    def step(i):
+        tr.step([(i * per * world + rank * per + j) % 16 for j in range(per)])
+
+    for i in range(args.warmup):
+        step(i)
+    k = max(2, args.steps // 2)
+    ms = timed(step, k)
+    out["c4_train"] = {"value": round(world * k * per / (ms / 1e3), 3), "unit": "views/s",
+                       "ms_per_step": round(ms / k, 4), "views_per_step_per_gpu": per,
+                       "config": "1600k 4D + 400k 3D, SH 3, 1352x1014, 8 views/GPU/step"}
+    torch.cuda.synchronize()
+    return out
 
 
 def cpu_baseline(scene, cam, t, gt) -> dict:
@@ -428,6 +491,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the c1/c5 render and c4 training lines")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     if args.impl == "reference":
