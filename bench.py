@@ -234,13 +234,15 @@ def run_ours(args) -> None:
             dist.barrier()
         torch.cuda.synchronize()
 
-    def timed(fn, k):
+    def timed(fn, k, drain=None):
         barrier()
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record(stream)
         for i in range(k):
             fn(i)
+        if drain:
+            drain()
         t1.record(stream)
         torch.cuda.synchronize()
         ms = t0.elapsed_time(t1)
@@ -251,9 +253,29 @@ def run_ours(args) -> None:
         barrier()
         return ms
 
-    step_fn = (lambda i: tr.step(batch(i))) if world > 1 else (lambda i: tr.step([batch(i)[0]]))
+    # 1 GPU: pipelined iterations (hgs_train_step_async): iteration i is
+    # enqueued before iteration i-1's loss is read back (hgs_train_collect),
+    # every loss is read inside the timed region.  N GPUs: synchronous steps
+    # around the NCCL all-reduce.
+    def pending():
+        return lib.hgs_train_pending(ctx.handle)
+
+    def drain():
+        while pending():
+            tr.collect()
+
+    def step_1gpu(i, gt_host=None):
+        v = batch(i)[0]
+        tr.step_async([v], gt_host=None if gt_host is None else [gt_host[v]])
+        if pending() > 1:
+            tr.collect()
+
+    lib = _capi.lib()
+    step_fn = (lambda i: tr.step(batch(i))) if world > 1 else step_1gpu
     for i in range(args.warmup):
         step_fn(i)
+    if world == 1:
+        drain()
     # ---- device-resident timed region (profiled per phase with CUDA events)
     _capi.lib().hgs_profile(ctx.handle, 1)
     _capi.lib().hgs_profile_read(ctx.handle, None, None, 1)
@@ -261,7 +283,7 @@ def run_ours(args) -> None:
     with ClockSampler(local) as clk:
         # NVTX range "timed": `ncu --nvtx --nvtx-include timed/` lists exactly these launches
         torch.cuda.nvtx.range_push("timed")
-        ms = timed(lambda i: step_fn(args.warmup + i), args.steps)
+        ms = timed(lambda i: step_fn(args.warmup + i), args.steps, drain if world == 1 else None)
         torch.cuda.nvtx.range_pop()
     launches = _capi.lib().hgs_launch_count() - l0
     import ctypes as C
@@ -296,9 +318,14 @@ def run_ours(args) -> None:
             dist.all_reduce(g)
             ctx.adam_step(tr.lrs, tr.decay())
 
+    if world == 1:
+        def e2e_step(i):  # noqa: F811 -- pipelined like the device loop, host GT frames
+            step_1gpu(args.warmup + args.steps + i, gt_host=gts_host)
     for i in range(args.warmup):  # untimed: the copy stream and GT buffers are created on first use
         e2e_step(-1 - i)
-    e2e_ms = timed(e2e_step, args.steps)
+    if world == 1:
+        drain()
+    e2e_ms = timed(e2e_step, args.steps, drain if world == 1 else None)
     e2e_value = world * args.steps / (e2e_ms / 1e3)
 
     # ---- forward-only render throughput (Mpix/s), device resident
@@ -333,8 +360,10 @@ def run_ours(args) -> None:
                "config": dict(desc, parallelism=f"view-parallel dp{world}", views_per_iteration=world),
                "e2e": {"value": round(e2e_value, 3), "unit": UNIT,
                        "h2d_bytes_per_step": int(W * H * 3 * 4),
-                       "d2h_bytes_per_step": 80,
-                       "path": "hgs_train_step_host (pinned host GT frame in, loss out)"},
+                       "d2h_bytes_per_step": 16 if world == 1 else 96,  # loss sums (+ counters when synchronous)
+                       "path": ("hgs_train_step_async with host GT + hgs_train_collect (pinned host GT frame in, "
+                                "loss out, every iteration)") if world == 1 else
+                               "hgs_train_step_host (pinned host GT frame in, loss out)"},
                "render": {"value": round(render_mpix, 2), "unit": "Mpix/s",
                           "what": "forward render of the device-resident c2 scene, 1352x1014"},
                "gpu_launches": int(launches), "launches_per_step": round(launches / args.steps, 1),

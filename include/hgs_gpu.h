@@ -193,6 +193,25 @@ hgs_status hgs_train_step_host(hgs_ctx *ctx, int n_views, const hgs_camera *cams
                                const void *const *gt_host, int dtype, int batch_total, const hgs_train_opts *opts,
                                int apply_adam, double *loss_out);
 
+/* Pipelined form of the same iteration (gt_on_device selects device float
+ * frames or host frames of the given dtype): it is enqueued and the call
+ * returns without waiting for it, so the host prepares iteration k+1 while
+ * the device finishes iteration k.  hgs_train_collect returns the losses in
+ * enqueue order.  A non-finite loss (train.cpp:445-447) makes the device skip
+ * the Adam update of that iteration and of every later pending one; its
+ * hgs_train_collect then fails with HGS_ERR_NUMERIC_ABORT and drops the
+ * pending ones -- the parameters are those after the last finite iteration,
+ * as when the reference throws.  At most HGS_TRAIN_PIPELINE iterations may be
+ * pending (HGS_ERR_STATE otherwise); the synchronous entry points require an
+ * empty pipeline. */
+#define HGS_TRAIN_PIPELINE 4
+hgs_status hgs_train_step_async(hgs_ctx *ctx, int n_views, const hgs_camera *cams, const double *times,
+                                const void *const *gt, int dtype, int gt_on_device, int batch_total,
+                                const hgs_train_opts *opts, int apply_adam);
+hgs_status hgs_train_collect(hgs_ctx *ctx, double *loss_out);
+/* Number of enqueued iterations not collected yet. */
+int hgs_train_pending(hgs_ctx *ctx);
+
 /* ---- instrumentation (not in the reference) ---------------------------- */
 /* Per-phase CUDA-event timing on the context stream:
  * 0 preprocess, 1 depth sort, 2 duplicate, 3 tile sort, 4 raster fwd,

@@ -126,6 +126,10 @@ _SIGS = {
                         C.c_int, _dp], C.c_int),
     "hgs_train_step_host": ([_vp, C.c_int, C.POINTER(Camera_), _dp, C.POINTER(_vp), C.c_int, C.c_int,
                              C.POINTER(TrainOpts), C.c_int, _dp], C.c_int),
+    "hgs_train_step_async": ([_vp, C.c_int, C.POINTER(Camera_), _dp, C.POINTER(_vp), C.c_int, C.c_int, C.c_int,
+                              C.POINTER(TrainOpts), C.c_int], C.c_int),
+    "hgs_train_collect": ([_vp, _dp], C.c_int),
+    "hgs_train_pending": ([_vp], C.c_int),
     "hgs_profile": ([_vp, C.c_int], C.c_int),
     "hgs_profile_read": ([_vp, _dp, C.POINTER(C.c_longlong), C.c_int], C.c_int),
     "hgs_launch_count": ([], C.c_longlong),

@@ -96,9 +96,15 @@ __device__ __forceinline__ bool renorm_quat(float q[4], float mq[4]) {
 }
 
 // train.cpp:445-447: a non-finite loss aborts the step before the update.
-__device__ __forceinline__ bool loss_finite(const AdamArgs& A) {
+// With pipelined iterations the abort is sticky: every later update is
+// skipped too until the host collects the failure.
+__device__ __forceinline__ bool update_allowed(const AdamArgs& A) {
+    if (A.abort && *(volatile const uint32_t*)A.abort) return false;
     for (int v = 0; v < A.n_views; ++v)
-        if (!isfinite(A.view_sums[2 * v]) || !isfinite(A.view_sums[2 * v + 1])) return false;
+        if (!isfinite(A.view_sums[2 * v]) || !isfinite(A.view_sums[2 * v + 1])) {
+            if (A.abort && blockIdx.x == 0 && threadIdx.x == 0) atomicOr(A.abort, 1u);
+            return false;
+        }
     return true;
 }
 
@@ -109,7 +115,7 @@ __global__ void __launch_bounds__(128) adam_classes_kernel(AdamPools P, AdamArgs
                                                            unsigned long long* __restrict__ skipped_total,
                                                            uint32_t* __restrict__ flags) {
     // one thread per (parameter class, 4 consecutive Gaussians); 3D units first
-    if (!loss_finite(A)) return;
+    if (!update_allowed(A)) return;
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     const int q3 = (P.n3 + 3) >> 2, q4 = (P.n4 + 3) >> 2;
     uint32_t skipped = 0;
@@ -205,7 +211,7 @@ __global__ void __launch_bounds__(128) adam_classes_kernel(AdamPools P, AdamArgs
 __global__ void __launch_bounds__(256) adam_rows_kernel(AdamPools P, AdamArgs A, const uint8_t* __restrict__ cls_ok3,
                                                         const uint8_t* __restrict__ cls_ok4, int blocks_per_row3,
                                                         int blocks_per_row4) {
-    if (!loss_finite(A)) return;
+    if (!update_allowed(A)) return;
     const int R3 = R3_SH + P.K3 - 4, R4 = R4_SH + P.K3 - 8;  // rows without the quaternions
     int b = blockIdx.x;
     const bool dyn = b >= R3 * blocks_per_row3;

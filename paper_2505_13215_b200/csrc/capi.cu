@@ -555,6 +555,9 @@ void hgs_ctx_destroy(hgs_ctx* ctx) {
     for (DBuf* b : bufs) b->release();
     ctx->pinned.release();
     ctx->pinned_ctr.release();
+    ctx->pinned_pipe.release();
+    for (int k = 0; k < HGS_TRAIN_PIPELINE; ++k)
+        if (ctx->pipe_ev[k]) cudaEventDestroy(ctx->pipe_ev[k]);
     for (int b = 0; b < 2; ++b) {
         ctx->gt_buf[b].release();
         ctx->gt_stage64[b].release();

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <deque>
 #include <string>
 #include <vector>
 
@@ -70,8 +71,20 @@ struct Counters {
 
 }  // namespace hgs
 
+// One enqueued (pipelined) training iteration awaiting hgs_train_collect.
+struct hgs_pending_step {
+    int slot = 0, n_views = 0;
+    int dims[32][2] = {};  // per view (W, H)
+    double lambda = 0.2;
+    bool adam = false;
+    uint64_t step_before = 0;
+};
+
 struct hgs_ctx {
     bool stats_pending = false;  // counters of the last render not read back yet
+    std::deque<hgs_pending_step> pipeline;  // hgs_train_step_async iterations, oldest first
+    int pipe_next = 0;                      // next step-sum slot
+    cudaEvent_t pipe_ev[HGS_TRAIN_PIPELINE] = {};
     int device = 0;
     cudaStream_t stream = nullptr;
     cudaStream_t own_stream = nullptr;
@@ -121,6 +134,7 @@ struct hgs_ctx {
     hgs::DBuf stage;     // upload / download staging
     hgs::HostPinned pinned;      // Scratch read-back (training / loss)
     hgs::HostPinned pinned_ctr;  // Counters read-back (render)
+    hgs::HostPinned pinned_pipe; // per-slot loss sums of pipelined iterations
 
     // ---- state of the last render (the "tape")
     bool have_tape = false;

@@ -85,6 +85,7 @@ struct AdamArgs {
     float lr_mean, lr_mean_t, lr_quat, lr_scales, lr_opacity, lr_sh;
     const double* view_sums = nullptr;  // the step's (ssim, l1) loss sums per view
     int n_views = 0;                    // > 0: skip the whole update if one is non-finite
+    uint32_t* abort = nullptr;          // sticky: set by a non-finite step, blocks later updates
 };
 struct AdamPools {
     float *p4, *g4, *m4, *v4, *p3, *g3, *m3, *v3;

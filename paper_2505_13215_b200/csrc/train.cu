@@ -28,7 +28,11 @@ struct Scratch {
     double loss_acc;
     double pad[2];
     double view_sums[kMaxStepViews][2];  // per-view (ssim_sum, l1_sum) of a training step
+    uint32_t abort;                      // sticky non-finite-loss flag of pipelined iterations
+    uint32_t pad2;
+    double pipe_sums[HGS_TRAIN_PIPELINE][kMaxStepViews][2];  // loss sums of pipelined iterations
 };
+static_assert(kMaxStepViews == 32, "hgs_pending_step::dims");
 
 hgs_status fail(hgs_ctx* ctx, hgs_status s, const std::string& m) {
     if (ctx) ctx->err = m;
@@ -200,7 +204,7 @@ double loss_from_sums(const Scratch& h, int W, int H, double lambda) {
 // then fails with NumericAbort, train.cpp:445-447, without a host round trip
 // before the update).
 hgs_status run_adam(hgs_ctx* ctx, const hgs_lrs* lrs, double mean_lr_scale, const double* view_sums = nullptr,
-                    int n_views = 0) {
+                    int n_views = 0, uint32_t* abort = nullptr) {
     cudaStream_t st = ctx->stream;
     ctx->step++;
     const double bc1 = 1.0 - std::pow(0.9, (double)ctx->step);
@@ -220,6 +224,7 @@ hgs_status run_adam(hgs_ctx* ctx, const hgs_lrs* lrs, double mean_lr_scale, cons
     A.lr_sh = (float)lrs->sh;
     A.view_sums = view_sums;
     A.n_views = n_views;
+    A.abort = abort;
     const int n = (int)(ctx->n4 + ctx->n3);
     Scratch* sc = scratch(ctx);
     AdamPools P;
@@ -543,14 +548,29 @@ hgs_status hgs_sweep_convert(hgs_ctx* ctx, int64_t* moved_out, hgs_conversion_re
     return HGS_OK;
 }
 
+// pipelined != 0: enqueue only (hgs_train_step_async); the loss sums land in
+// the iteration's slot and are read by hgs_train_collect.
 hgs_status train_step_impl(hgs_ctx* ctx, int n_views, const hgs_camera* cams, const double* times,
                            const void* const* gt, int gt_dtype, int gt_on_device, int batch_total,
-                           const hgs_train_opts* o, int apply_adam, double* loss_out) {
+                           const hgs_train_opts* o, int apply_adam, double* loss_out, int pipelined = 0) {
     if (!ctx || n_views < 0 || (n_views && (!cams || !times || !gt)) || !o || batch_total <= 0)
         return HGS_ERR_INVALID_ARGUMENT;
     CK(cudaSetDevice(ctx->device));
     hgs_status r = ensure_scratch(ctx);
     if (r != HGS_OK) return r;
+    if (!pipelined && !ctx->pipeline.empty())
+        return fail(ctx, HGS_ERR_STATE, "train_step: pipelined iterations pending (hgs_train_collect first)");
+    if (pipelined) {
+        if ((int)ctx->pipeline.size() >= HGS_TRAIN_PIPELINE)
+            return fail(ctx, HGS_ERR_STATE, "train_step_async: pipeline full (hgs_train_collect first)");
+        if (n_views > kMaxStepViews)
+            return fail(ctx, HGS_ERR_INVALID_ARGUMENT, "train_step_async: at most 32 views per iteration");
+        if (!ctx->pipe_ev[0])
+            for (int k = 0; k < HGS_TRAIN_PIPELINE; ++k)
+                CK(cudaEventCreateWithFlags(&ctx->pipe_ev[k], cudaEventDisableTiming));
+        CK(ctx->pinned_pipe.ensure(sizeof(double) * 2 * kMaxStepViews * HGS_TRAIN_PIPELINE));
+    }
+    const int slot = ctx->pipe_next;
     hgs_raster_opts ro{o->weight_cutoff, 1, 0, 0};
     // No host round trip per view beyond the render's instance count: the
     // per-view loss sums stay on the device (read every kMaxStepViews views
@@ -592,13 +612,13 @@ hgs_status train_step_impl(hgs_ctx* ctx, int n_views, const hgs_camera* cams, co
         r = hgs_render_pipeline(ctx, &cams[v], times[v], o->bg, &ro, 1);
         if (r != HGS_OK) return r;
         if (!gt_on_device) CK(cudaStreamWaitEvent(ctx->stream, ctx->gt_ready[b], 0));
-        r = run_loss(ctx, g, o->ssim_lambda, sc->view_sums[pending]);
+        r = run_loss(ctx, g, o->ssim_lambda, pipelined ? sc->pipe_sums[slot][v] : sc->view_sums[pending]);
         if (r != HGS_OK) return r;
         if (!gt_on_device) CK(cudaEventRecord(ctx->gt_free[b], ctx->stream));
         ++pending;
         r = run_backward(ctx, ctx->lgrad.as<float>(), 1.0 / (double)batch_total);  // train.cpp:430-432
         if (r != HGS_OK) return r;
-        if (pending == kMaxStepViews && v + 1 < n_views) {
+        if (!pipelined && pending == kMaxStepViews && v + 1 < n_views) {
             r = flush();
             if (r != HGS_OK) return r;
         }
@@ -608,10 +628,33 @@ hgs_status train_step_impl(hgs_ctx* ctx, int n_views, const hgs_camera* cams, co
         return fail(ctx, HGS_ERR_NUMERIC_ABORT, "train: non-finite loss");  // train.cpp:445-447
     }
     const int gate = pending;
+    const uint64_t step_before = ctx->step;
     if (apply_adam) {
         CK(cudaMemsetAsync(&sc->skipped, 0, sizeof(unsigned long long) + 8, ctx->stream));
-        r = run_adam(ctx, &o->lrs, o->mean_lr_scale, &sc->view_sums[0][0], gate);
+        r = run_adam(ctx, &o->lrs, o->mean_lr_scale, pipelined ? &sc->pipe_sums[slot][0][0] : &sc->view_sums[0][0],
+                     gate, pipelined ? &sc->abort : nullptr);
         if (r != HGS_OK) return r;
+    }
+    if (pipelined) {
+        hgs_pending_step ps;
+        ps.slot = slot;
+        ps.n_views = n_views;
+        for (int v = 0; v < n_views; ++v) {
+            ps.dims[v][0] = cams[v].width;
+            ps.dims[v][1] = cams[v].height;
+        }
+        ps.lambda = o->ssim_lambda;
+        ps.adam = apply_adam != 0;
+        ps.step_before = step_before;
+        double* hp = static_cast<double*>(ctx->pinned_pipe.p) + (size_t)slot * kMaxStepViews * 2;
+        CK(cudaMemcpyAsync(hp, sc->pipe_sums[slot], sizeof(double) * 2 * n_views, cudaMemcpyDeviceToHost,
+                           ctx->stream));
+        CK(cudaEventRecord(ctx->pipe_ev[slot], ctx->stream));
+        ctx->pipeline.push_back(ps);
+        ctx->pipe_next = (slot + 1) % HGS_TRAIN_PIPELINE;
+        ctx->stats_pending = true;
+        prof_collect(ctx);
+        return HGS_OK;
     }
     r = flush();
     if (r != HGS_OK) return r;
@@ -631,6 +674,44 @@ hgs_status hgs_train_step(hgs_ctx* ctx, int n_views, const hgs_camera* cams, con
                           double* loss_out) {
     return train_step_impl(ctx, n_views, cams, times, reinterpret_cast<const void* const*>(gt_device), HGS_F32, 1,
                            batch_total, o, apply_adam, loss_out);
+}
+
+hgs_status hgs_train_step_async(hgs_ctx* ctx, int n_views, const hgs_camera* cams, const double* times,
+                                const void* const* gt, int dtype, int gt_on_device, int batch_total,
+                                const hgs_train_opts* o, int apply_adam) {
+    return train_step_impl(ctx, n_views, cams, times, gt, gt_on_device ? HGS_F32 : dtype, gt_on_device ? 1 : 0,
+                           batch_total, o, apply_adam, nullptr, 1);
+}
+
+int hgs_train_pending(hgs_ctx* ctx) { return ctx ? (int)ctx->pipeline.size() : 0; }
+
+hgs_status hgs_train_collect(hgs_ctx* ctx, double* loss_out) {
+    if (!ctx) return HGS_ERR_INVALID_ARGUMENT;
+    if (ctx->pipeline.empty()) return fail(ctx, HGS_ERR_STATE, "train_collect: no pipelined iteration pending");
+    CK(cudaSetDevice(ctx->device));
+    const hgs_pending_step p = ctx->pipeline.front();
+    ctx->pipeline.pop_front();
+    CK(cudaEventSynchronize(ctx->pipe_ev[p.slot]));
+    const double* hp = static_cast<const double*>(ctx->pinned_pipe.p) + (size_t)p.slot * kMaxStepViews * 2;
+    double loss = 0.0;
+    for (int v = 0; v < p.n_views; ++v)
+        loss += loss_from_sums(hp[2 * v], hp[2 * v + 1], p.dims[v][0], p.dims[v][1], p.lambda);
+    if (loss_out) *loss_out = loss;
+    if (!std::isfinite(loss)) {
+        // the device skipped this update and every later pending one
+        if (p.adam) ctx->step = p.step_before;
+        ctx->pipeline.clear();
+        ctx->pipe_next = 0;
+        CK(cudaStreamSynchronize(ctx->stream));
+        CK(cudaMemsetAsync(&scratch(ctx)->abort, 0, sizeof(uint32_t), ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        return fail(ctx, HGS_ERR_NUMERIC_ABORT, "train: non-finite loss");  // train.cpp:445-447
+    }
+    if (ctx->pipeline.empty()) {
+        hgs_status r = hgs_render_finish(ctx);
+        if (r != HGS_OK) return r;
+    }
+    return HGS_OK;
 }
 
 hgs_status hgs_train_step_host(hgs_ctx* ctx, int n_views, const hgs_camera* cams, const double* times,

@@ -112,6 +112,35 @@ class DeviceTrainer:
                                                      C.byref(loss)))
         return loss.value / max(1, n)
 
+    def step_async(self, views: list[int], batch_total: int | None = None, apply_adam: bool = True,
+                   gt_host: list | None = None) -> None:
+        """Enqueue one iteration (hgs_train_step_async) without waiting for it;
+        ``collect()`` returns the mean losses in order.  ``gt_host``: pinned
+        host float32 frames per view instead of the device-resident ones."""
+        if apply_adam:
+            self.iter += 1
+        n = len(views)
+        cams = (_capi.Camera_ * max(1, n))(*[self._cams[v] for v in views])
+        times = (C.c_double * max(1, n))(*[self.times[v] for v in views])
+        src = gt_host if gt_host is not None else [self.gt[v] for v in views]
+        gts = (C.c_void_p * max(1, n))(*[C.c_void_p(t.data_ptr()) for t in src])
+        self.ctx._check(self.ctx._lib.hgs_train_step_async(self.ctx.handle, n, cams, times, gts, _capi.HGS_F32,
+                                                           0 if gt_host is not None else 1, batch_total or n,
+                                                           C.byref(self._opts(self.decay())),
+                                                           1 if apply_adam else 0))
+        self._pending_n = getattr(self, "_pending_n", [])
+        self._pending_n.append(n)
+
+    def collect(self) -> float:
+        """Mean loss of the oldest enqueued iteration (raises NumericAbort)."""
+        loss = C.c_double()
+        n = self._pending_n.pop(0)
+        rc = self.ctx._lib.hgs_train_collect(self.ctx.handle, C.byref(loss))
+        if rc != 0:
+            self._pending_n.clear()
+        self.ctx._check(rc)
+        return loss.value / max(1, n)
+
     def adam(self) -> int:
         return self.ctx.adam_step(self.lrs, self.decay())
 

@@ -263,3 +263,56 @@ def test_train_step_nonfinite_loss_aborts_before_update(ctx):
         assert np.array_equal(getattr(before, f), getattr(after, f), equal_nan=True), f
     tr.gt[2][5, 5, 1] = 0.5
     assert np.isfinite(tr.step([2, 3]))  # the context keeps working
+
+
+def test_pipelined_steps_match_synchronous(ctx):
+    """hgs_train_step_async + hgs_train_collect: the same iterations as the
+    synchronous call, losses returned in order."""
+    from paper_2505_13215_b200.train import DeviceTrainer
+
+    scene = synthetic_scene(1500, 500, 1, seed=33, density_n=2000)
+    target = synthetic_scene(1500, 500, 1, seed=34, density_n=2000)
+    cams = [ring_camera(33, 80, 64, index=i, n_ring=4) for i in range(4)]
+    sched = [[i % 4, (i + 1) % 4] for i in range(8)]
+    ta = DeviceTrainer(ctx, scene, cams, [0.5] * 4, target=target, bg=(0.2, 0.2, 0.2))
+    la = [ta.step(b) for b in sched]
+    pa = ctx.download()
+    tb = DeviceTrainer(ctx, scene, cams, [0.5] * 4, target=target, bg=(0.2, 0.2, 0.2))
+    lb = []
+    for i, b in enumerate(sched):
+        tb.step_async(b)
+        if i >= 2:
+            lb.append(tb.collect())
+    while ctx._lib.hgs_train_pending(ctx.handle):
+        lb.append(tb.collect())
+    pb = ctx.download()
+    assert np.allclose(la, lb, rtol=1e-4, atol=0)
+    for f in ("mean_x", "ql", "log_s4", "op4", "mean3", "sh3"):
+        assert np.allclose(getattr(pa, f), getattr(pb, f), rtol=1e-3, atol=1e-5), f
+
+
+def test_pipelined_nonfinite_loss_keeps_last_good_state(ctx):
+    """A non-finite loss inside the pipeline: that update and every later
+    pending one are skipped on the device; collect raises NumericAbort."""
+    from paper_2505_13215_b200._capi import NumericAbort
+    from paper_2505_13215_b200.train import DeviceTrainer
+
+    scene = synthetic_scene(1500, 500, 1, seed=35, density_n=2000)
+    cams = [ring_camera(35, 80, 64, index=i, n_ring=4) for i in range(4)]
+    tr = DeviceTrainer(ctx, scene, cams, [0.5] * 4, target=synthetic_scene(1500, 500, 1, seed=36, density_n=2000),
+                       bg=(0.2, 0.2, 0.2))
+    tr.step([0, 1])
+    good = ctx.download()
+    tr.gt[2][3, 3, 0] = float("nan")
+    tr.step_async([0, 2])   # non-finite
+    tr.step_async([1, 3])   # finite, but after the failure: must not update
+    with pytest.raises(NumericAbort):
+        tr.collect()
+    assert ctx._lib.hgs_train_pending(ctx.handle) == 0
+    after = ctx.download()
+    for f in ("mean_x", "ql", "sh4", "mean3", "op3", "sh3"):
+        assert np.array_equal(getattr(good, f), getattr(after, f), equal_nan=True), f
+    tr.gt[2][3, 3, 0] = 0.5
+    tr._pending_n = []
+    assert np.isfinite(tr.step([2, 3]))  # usable again: the sticky flag was cleared
+    assert ctx.download().mean_x.tolist() != good.mean_x.tolist()
