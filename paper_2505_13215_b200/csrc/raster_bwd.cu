@@ -143,6 +143,7 @@ __global__ void __launch_bounds__(kThreadsB, 7) raster_bwd_kernel(
         // flagged pixels go through the exact kernel; zero gradient = untouched (backward.cpp:188)
         if (!(l & 0x80000000u) && (s.gr != 0.f || s.gg != 0.f || s.gb != 0.f)) s.last = l;
     };
+    const int cshift = px - tx * kTile, rshift0 = 16 + py0 - ty * kTile, rshift1 = rshift0 + 4;
     PixBwd s0, s1;
     init(py0, s0);
     init(py1, s1);
@@ -159,19 +160,18 @@ __global__ void __launch_bounds__(kThreadsB, 7) raster_bwd_kernel(
         const uint32_t base = rg.x + (uint32_t)bi * kBatchB;
         const int nb = (int)min((uint32_t)kBatchB, end - base);
         __syncthreads();
-        for (int t = threadIdx.x; t < nb; t += kThreadsB) sb.load(t, fast, inst_val[base + t]);
+        for (int t = threadIdx.x; t < nb; t += kThreadsB) sb.load(t, fast, inst_val[base + t], tx * kTile, ty * kTile);
         __syncthreads();
         const int kmax = (int)min((uint32_t)nb, warp_end > base ? warp_end - base : 0u);
         for (int k = kmax - 1; k >= 0; --k) {
             if (!((sb.qm[k] >> warp) & 1u)) continue;  // exact: no pixel of this quadrant reaches 1/255
             const int4 hdr = sb.hdr[k];
             const uint32_t idx = base + k;
-            // box test without short-circuit branches (the column is shared)
-            const bool colin = (unsigned)(px - box_x0(hdr.x)) <= (unsigned)box_w(hdr.x);
-            const int y0 = box_x0(hdr.y);
-            const unsigned wy = (unsigned)box_w(hdr.y);
-            const bool b0 = colin & (idx < s0.last) & ((unsigned)(py0 - y0) <= wy);
-            const bool b1 = colin & (idx < s1.last) & ((unsigned)(py1 - y0) <= wy);
+            // box test from the staged tile-relative column/row masks
+            const uint32_t bm = sb.bm[k];
+            const bool colin = (bm >> cshift) & 1u;
+            const bool b0 = colin & (idx < s0.last) & ((bm >> rshift0) & 1u);
+            const bool b1 = colin & (idx < s1.last) & ((bm >> rshift1) & 1u);
             if (!__any_sync(0xffffffffu, b0 || b1)) continue;
             const float4 L = sb.chol[k], col = sb.col[k];
             const SplatRec* e = exact + sb.j[k];

@@ -97,12 +97,22 @@ struct SplatBatch {
     float4 col[B];   // r, g, b, x_keep
     uint32_t j[B];   // sorted splat index (for the exact record)
     uint32_t qm[B];  // 8x8-quadrant contribution mask of this tile instance
+    uint32_t bm[B];  // pixel box inside the tile: bit c = column ox+c covered, bit 16+r = row oy+r
 
-    __device__ __forceinline__ void load(int t, const SplatFast* __restrict__ fast, uint32_t v) {
+    // (ox, oy): the tile's first pixel
+    __device__ __forceinline__ void load(int t, const SplatFast* __restrict__ fast, uint32_t v, int ox, int oy) {
         const uint32_t jj = v & kInstIndexMask;
         qm[t] = v >> kInstMaskShift;
         const float4* src = reinterpret_cast<const float4*>(fast + jj);
         const float4 a = __ldg(src + 0), b = __ldg(src + 1), c = __ldg(src + 2), d = __ldg(src + 3);
+        {
+            const int xr = __float_as_int(a.x), yr = __float_as_int(a.y);
+            const int cl = min(max(box_x0(xr) - ox, 0), 16), ch = min(max(box_x0(xr) + box_w(xr) + 1 - ox, 0), 16);
+            const int rl = min(max(box_x0(yr) - oy, 0), 16), rh = min(max(box_x0(yr) + box_w(yr) + 1 - oy, 0), 16);
+            const uint32_t cmask = ((1u << ch) - 1u) & ~((1u << cl) - 1u);
+            const uint32_t rmask = ((1u << rh) - 1u) & ~((1u << rl) - 1u);
+            bm[t] = (cmask & 0xffffu) | (rmask << 16);
+        }
         hdr[t] = make_int4(__float_as_int(a.x), __float_as_int(a.y), __float_as_int(a.z), __float_as_int(a.w));
         mean[t] = b;
         chol[t] = c;

@@ -312,6 +312,7 @@ __global__ void __launch_bounds__(kThreads, 6) raster_fwd_kernel(
     const float pxc = (float)px + 0.5f, pyc0 = (float)py0 + 0.5f, pyc1 = (float)py1 + 0.5f;
     const double pcx = (double)px + 0.5, pcy0 = (double)py0 + 0.5, pcy1 = (double)py1 + 0.5;
 
+    const int cshift = px - tx * kTile, rshift0 = 16 + py0 - ty * kTile, rshift1 = rshift0 + 4;
     PixFwd s0{1.0f, 0.f, 0.f, 0.f, 0.f, rg.x, 0u, !in0, false};
     PixFwd s1{1.0f, 0.f, 0.f, 0.f, 0.f, rg.x, 0u, !in1, false};
 
@@ -319,7 +320,7 @@ __global__ void __launch_bounds__(kThreads, 6) raster_fwd_kernel(
         if (__syncthreads_count(!(s0.done && s1.done)) == 0) break;
         for (int t = threadIdx.x; t < kBatch; t += kThreads) {
             const uint32_t idx = base + t;
-            if (idx < rg.y) sb.load(t, fast, inst_val[idx]);
+            if (idx < rg.y) sb.load(t, fast, inst_val[idx], tx * kTile, ty * kTile);
         }
         __syncthreads();
         const int nb = min((uint32_t)kBatch, rg.y - base);
@@ -327,12 +328,11 @@ __global__ void __launch_bounds__(kThreads, 6) raster_fwd_kernel(
             if (s0.done && s1.done) break;
             if (!((sb.qm[k] >> warp) & 1u)) continue;  // exact: no pixel of this quadrant reaches 1/255
             const int4 hdr = sb.hdr[k];
-            // box test without short-circuit branches (the column is shared)
-            const bool colin = (unsigned)(px - box_x0(hdr.x)) <= (unsigned)box_w(hdr.x);
-            const int y0 = box_x0(hdr.y);
-            const unsigned wy = (unsigned)box_w(hdr.y);
-            const bool b0 = colin & !s0.done & ((unsigned)(py0 - y0) <= wy);
-            const bool b1 = colin & !s1.done & ((unsigned)(py1 - y0) <= wy);
+            // box test from the staged tile-relative column/row masks
+            const uint32_t bm = sb.bm[k];
+            const bool colin = (bm >> cshift) & 1u;
+            const bool b0 = colin & !s0.done & ((bm >> rshift0) & 1u);
+            const bool b1 = colin & !s1.done & ((bm >> rshift1) & 1u);
             if (!(b0 || b1)) continue;
             if (kCount) {
                 s0.count += b0;
