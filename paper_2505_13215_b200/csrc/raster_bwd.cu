@@ -17,6 +17,8 @@
 // applies alpha and the FP64 conic once per splat.
 // Pixels the forward handed to the FP64 fix-up are back-propagated by
 // raster_bwd_exact_kernel (one warp per pixel, FP64).
+#include <cstddef>
+
 #include "kernels.cuh"
 
 namespace hgs {
@@ -155,6 +157,11 @@ __global__ void __launch_bounds__(kThreadsB, 7) raster_bwd_kernel(
     const uint32_t end = s_maxlast;
     const uint32_t warp_end = __reduce_max_sync(0xffffffffu, ml);  // nothing past it in this warp
 
+    using SB = SplatBatch<kBatchB>;
+    const uint32_t sbase = opaque_u32((uint32_t)__cvta_generic_to_shared(&sb));
+    const uint32_t a_qm = sbase + offsetof(SB, qm), a_bm = sbase + offsetof(SB, bm), a_hdr = sbase + offsetof(SB, hdr),
+                   a_chol = sbase + offsetof(SB, chol), a_col = sbase + offsetof(SB, col),
+                   a_mean = sbase + offsetof(SB, mean), a_j = sbase + offsetof(SB, j);
     const int nbatch = (int)((end - rg.x + kBatchB - 1) / kBatchB);
     for (int bi = nbatch - 1; bi >= 0; --bi) {
         const uint32_t base = rg.x + (uint32_t)bi * kBatchB;
@@ -164,17 +171,18 @@ __global__ void __launch_bounds__(kThreadsB, 7) raster_bwd_kernel(
         __syncthreads();
         const int kmax = (int)min((uint32_t)nb, warp_end > base ? warp_end - base : 0u);
         for (int k = kmax - 1; k >= 0; --k) {
-            if (!((sb.qm[k] >> warp) & 1u)) continue;  // exact: no pixel of this quadrant reaches 1/255
-            const int4 hdr = sb.hdr[k];
+            if (!((lds_u32(a_qm + 4 * k) >> warp) & 1u)) continue;  // exact: no pixel of this quadrant reaches 1/255
+            const int4 hdr = lds_i4(a_hdr + 16 * k);
             const uint32_t idx = base + k;
             // box test from the staged tile-relative column/row masks
-            const uint32_t bm = sb.bm[k];
+            const uint32_t bm = lds_u32(a_bm + 4 * k);
             const bool colin = (bm >> cshift) & 1u;
             const bool b0 = colin & (idx < s0.last) & ((bm >> rshift0) & 1u);
             const bool b1 = colin & (idx < s1.last) & ((bm >> rshift1) & 1u);
             if (!__any_sync(0xffffffffu, b0 || b1)) continue;
-            const float4 L = sb.chol[k], col = sb.col[k];
-            const SplatRec* e = exact + sb.j[k];
+            const float4 L = lds_f4(a_chol + 16 * k), col = lds_f4(a_col + 16 * k);
+            const uint32_t sj = lds_u32(a_j + 4 * k);
+            const SplatRec* e = exact + sj;
             // exponent argument and offset of both pixels (same column: one dx
             // on the fast path, the same rounding sequence as K4's fast_x)
             float x0 = INFINITY, x1 = INFINITY, dx0 = 0.f, dx1 = 0.f, dy0 = 0.f, dy1 = 0.f;
@@ -192,7 +200,7 @@ __global__ void __launch_bounds__(kThreadsB, 7) raster_bwd_kernel(
                     dy1 = d.y;
                 }
             } else {
-                const float4 m = sb.mean[k];
+                const float4 m = lds_f4(a_mean + 16 * k);
                 x0 = fast_x(m, L, pxc, pyc0, dx0, dy0);
                 dx1 = dx0;
                 dy1 = __fsub_rn(__fsub_rn(pyc1, m.y), m.w);
@@ -225,7 +233,7 @@ __global__ void __launch_bounds__(kThreadsB, 7) raster_bwd_kernel(
             v[6] = fmaf(hx0, dx0, hx1 * dx1);
             v[7] = fmaf(hx0, dy0, hx1 * dy1);
             v[8] = fmaf(hy0, dy0, hy1 * dy1);
-            float* dst = accum + (size_t)sb.j[k] * kAccStride;
+            float* dst = accum + (size_t)sj * kAccStride;
             const unsigned am = __ballot_sync(0xffffffffu, p0 || p1);
             if (__popc(am) <= kDirectLanes) {
                 // few contributing lanes: their own atomics are cheaper than the butterfly

@@ -123,6 +123,30 @@ struct SplatBatch {
 
 __device__ __forceinline__ float fast_dx(float pc, float hi, float lo) { return __fsub_rn(__fsub_rn(pc, hi), lo); }
 
+// Shared-memory loads through an explicit 32-bit shared-window address held
+// in a register: keeps the compiler from re-deriving the CTA's shared base
+// (an S2R) inside the hot loops under register pressure.
+__device__ __forceinline__ uint32_t opaque_u32(uint32_t x) {
+    uint32_t y;
+    asm volatile("mov.u32 %0, %1;" : "=r"(y) : "r"(x));
+    return y;
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ float4 lds_f4(uint32_t a) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ int4 lds_i4(uint32_t a) {
+    int4 v;
+    asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
+
 // FP32 exponent argument x = power*log2(e) (>= 0) on the fast path.
 __device__ __forceinline__ float fast_x(const float4 m, const float4 L, float pxc, float pyc, float& dx, float& dy) {
     dx = __fsub_rn(__fsub_rn(pxc, m.x), m.z);
