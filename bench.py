@@ -172,6 +172,9 @@ def roofline(phase_ms: dict, counts: dict, steps: int, peak: float, peak_kind: s
         kernels.append({"phase": ph, "ms_per_step": round(per, 4), "alg_bytes": b,
                         "GB/s": round(gbs, 1) if gbs else None, "frac": round(gbs / peak, 4) if gbs else None})
     kernels.sort(key=lambda k: -k["ms_per_step"])
+    if not kernels:
+        return {"bound": "hbm", "kernel": None, "achieved": None, "peak": peak, "unit": "GB/s", "frac": None,
+                "traffic": None, "peak_source": peak_kind, "kernels": []}
     top = kernels[0]
     # DRAM traffic per launch of the phase's main kernel from the committed
     # `ncu --set full` capture (profiles/ncu_summary.json, tools/make_profiles.py)
@@ -276,9 +279,7 @@ def run_ours(args) -> None:
         step_fn(i)
     if world == 1:
         drain()
-    # ---- device-resident timed region (profiled per phase with CUDA events)
-    _capi.lib().hgs_profile(ctx.handle, 1)
-    _capi.lib().hgs_profile_read(ctx.handle, None, None, 1)
+    # ---- device-resident timed region (the headline; no instrumentation)
     l0 = _capi.lib().hgs_launch_count()
     with ClockSampler(local) as clk:
         # NVTX range "timed": `ncu --nvtx --nvtx-include timed/` lists exactly these launches
@@ -288,10 +289,17 @@ def run_ours(args) -> None:
     launches = _capi.lib().hgs_launch_count() - l0
     import ctypes as C
 
-    ph = (C.c_double * 16)()
-    _capi.lib().hgs_profile_read(ctx.handle, ph, None, 1)
-    _capi.lib().hgs_profile(ctx.handle, 0)
-    phase_ms = {name: float(ph[i]) for i, name in enumerate(_capi.PHASES)}
+    # ---- the same steps again with per-phase CUDA events (roofline.kernels);
+    # the events cost ~4% of the step, so they are kept out of the headline
+    phase_ms = {}
+    if not args.no_phase_profile:
+        _capi.lib().hgs_profile(ctx.handle, 1)
+        _capi.lib().hgs_profile_read(ctx.handle, None, None, 1)
+        timed(lambda i: step_fn(args.warmup + args.steps + i), args.steps, drain if world == 1 else None)
+        ph = (C.c_double * 16)()
+        _capi.lib().hgs_profile_read(ctx.handle, ph, None, 1)
+        _capi.lib().hgs_profile(ctx.handle, 0)
+        phase_ms = {name: float(ph[i]) for i, name in enumerate(_capi.PHASES)}
     info = ctx.render_info()
     value = world * args.steps / (ms / 1e3)
 
@@ -521,6 +529,8 @@ def main():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip the c1/c5 render and c4 training lines")
+    ap.add_argument("--no-phase-profile", action="store_true",
+                    help="no per-phase CUDA events in the timed region (roofline.kernels then empty)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     if args.impl == "reference":
