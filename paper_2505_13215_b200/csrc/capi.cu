@@ -302,12 +302,13 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
         CK(ctx->ntiles.ensure((size_t)N * 4));
         CK(ctx->visflag.ensure((size_t)N * 4));
         CK(ctx->vispos.ensure((size_t)N * 4));
+        CK(ctx->shdir.ensure((size_t)N * sizeof(float4)));
         CK(ctx->scan_ws.ensure(scan_workspace_bytes(N) + 4096));
         prof_begin(ctx, PH_PREPROCESS);
         preprocess_kernel<<<div_up(N, 256), 256, 0, st>>>(
             ctx->p4.as<float>(), ctx->cap4, n4, ctx->p3.as<float>(), ctx->cap3, n3, ctx->deg, ctx->cam, t, cutoff,
             tiles_x, ctx->rec.as<SplatRec>(), ctx->depth_key.as<uint32_t>(), ctx->ntiles.as<uint32_t>(), dc->stats,
-            &dc->flags);
+            &dc->flags, ctx->shdir.as<float4>());
         count_launch();
         CKL();
         visflag_kernel<<<div_up(N, 256), 256, 0, st>>>(ctx->ntiles.as<uint32_t>(), N, ctx->visflag.as<uint32_t>());
@@ -551,7 +552,7 @@ void hgs_ctx_destroy(hgs_ctx* ctx) {
                     &ctx->sort_v2, &ctx->rec_sorted, &ctx->fast_sorted, &ctx->ntiles_sorted, &ctx->inst_off,
                     &ctx->inst_k, &ctx->inst_v, &ctx->inst_k2, &ctx->inst_v2, &ctx->ranges, &ctx->sorted_of_gid, &ctx->inst_flag, &ctx->inst_pos, &ctx->dbg_k, &ctx->dbg_v, &ctx->scan_ws,
                     &ctx->sort_ws, &ctx->counters, &ctx->img, &ctx->last, &ctx->tfinal, &ctx->trans, &ctx->count,
-                    &ctx->fix_list, &ctx->accum, &ctx->lgrad, &ctx->gt_stage, &ctx->loss_ws, &ctx->stage, &ctx->adam_ok, &ctx->pcut, &ctx->dup_first};
+                    &ctx->fix_list, &ctx->accum, &ctx->lgrad, &ctx->gt_stage, &ctx->loss_ws, &ctx->stage, &ctx->adam_ok, &ctx->pcut, &ctx->dup_first, &ctx->shdir, &ctx->ddir};
     for (DBuf* b : bufs) b->release();
     ctx->pinned.release();
     ctx->pinned_ctr.release();

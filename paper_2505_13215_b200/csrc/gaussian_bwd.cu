@@ -103,12 +103,13 @@ __device__ inline void sh_dir_grad_f(const float d[3], int deg, const float w[16
 
 }  // namespace
 
-__global__ void __launch_bounds__(128, 3) gaussian_bwd_kernel(
+__global__ void __launch_bounds__(128, 4) gaussian_bwd_kernel(
     int N, const uint32_t* __restrict__ sorted_of_gid, const float* __restrict__ accum, int acc_stride, int n4,
     const float* __restrict__ p4, int64_t cap4, const float* __restrict__ p3, int64_t cap3, int deg, DevCamera cam,
     double t, double scale, float* __restrict__ g4, float* __restrict__ g3, float* __restrict__ sn4,
     float* __restrict__ sn3, float* __restrict__ gn4, float* __restrict__ gn3, float* __restrict__ cnt4,
-    float* __restrict__ cnt3, const double* __restrict__ conic_src, int conic_stride) {
+    float* __restrict__ cnt3, const double* __restrict__ conic_src, int conic_stride,
+    const float4* __restrict__ ddir) {
     // one thread per Gaussian in pool order (coalesced SoA parameter and
     // gradient rows); the splat's accumulators are found through the
     // gid -> depth-sorted index map written by the gather kernel
@@ -240,59 +241,17 @@ __global__ void __launch_bounds__(128, 3) gaussian_bwd_kernel(
     double dir[3] = {0.0, 0.0, 1.0};
     if (vd > 0.0)
         for (int k = 0; k < 3; ++k) dir[k] = v[k] / vd;
-    // SH part in FP32 (tolerance-level quantities; keeps the kernel's register
-    // footprint small enough for useful occupancy)
-    const float df[3] = {(float)dir[0], (float)dir[1], (float)dir[2]};
-    float basis[16];
-    sh_basis_f(df, deg, basis);
-    const int K = sh_count(deg);
-    const int shrow = dyn ? R4_SH : R3_SH;
-    const float* Pf = P + i;
-    float raw[3] = {0.5f, 0.5f, 0.5f};
-    for (int k = 0; k < K; ++k)
-        for (int c = 0; c < 3; ++c) raw[c] = fmaf(basis[k], Pf[(int64_t)(shrow + 3 * k + c) * cap], raw[c]);
-    float drr[3];
-    for (int c = 0; c < 3; ++c) drr[c] = (raw[c] < 0.0f || raw[c] > 1.0f) ? 0.0f : (float)d_rgb[c];
     float* G = dyn ? g4 : g3;
-    // Gradient rows are read-modify-written in batches (all loads of a batch
-    // issued before its stores): the row pointers alias as far as the
-    // compiler knows, so one-at-a-time RMW would serialise ~65 memory
-    // latencies per thread.  Non-SH rows are collected here and flushed last.
+    // Gradient rows are read-modify-written in one batch at the end (all
+    // loads before the stores): the row pointers alias as far as the compiler
+    // knows, so one-at-a-time RMW would serialise the memory latencies.
     float gacc[R4_SH];
 #pragma unroll
     for (int r = 0; r < R4_SH; ++r) gacc[r] = 0.0f;
     auto gadd = [&](int row, double val) { gacc[row] = (float)(scale * val); };
-    float dotc[16];
-    const float fs = (float)scale;
-#pragma unroll
-    for (int k = 0; k < 16; ++k) {
-        float dc = 0.0f;
-        if (k < K)
-            for (int c = 0; c < 3; ++c) dc = fmaf(drr[c], Pf[(int64_t)(shrow + 3 * k + c) * cap], dc);
-        dotc[k] = dc;
-    }
-    {
-        float* Gs = G + (int64_t)shrow * cap + i;
-#pragma unroll
-        for (int k0 = 0; k0 < 16; k0 += 4) {
-            if (k0 >= K) break;
-            float gv[12];
-#pragma unroll
-            for (int u = 0; u < 12; ++u)
-                if (k0 + u / 3 < K) gv[u] = Gs[(int64_t)(3 * k0 + u) * cap];
-#pragma unroll
-            for (int u = 0; u < 12; ++u)
-                if (k0 + u / 3 < K) Gs[(int64_t)(3 * k0 + u) * cap] = fmaf(fs, basis[k0 + u / 3] * drr[u % 3], gv[u]);
-        }
-    }
-    double d_dir[3];
-    {
-        float dd[3];
-        sh_dir_grad_f(df, deg, dotc, dd);
-        d_dir[0] = dd[0];
-        d_dir[1] = dd[1];
-        d_dir[2] = dd[2];
-    }
+    // d(loss)/d(view direction) from the SH backward (K7b, sh_bwd_kernel)
+    const float4 dd = ddir[gid];
+    const double d_dir[3] = {dd.x, dd.y, dd.z};
     if (vd > 0.0)
         for (int a = 0; a < 3; ++a) {
             double s = 0.0;
@@ -424,6 +383,68 @@ __global__ void __launch_bounds__(128, 3) gaussian_bwd_kernel(
 #pragma unroll
         for (int r = 0; r < R4_SH; ++r) G[(int64_t)r * cap + i] = old[r] + gacc[r];
     }
+}
+
+// K7b: SH colour backward (backward.cpp:252-273), one thread per visible
+// Gaussian, FP32: dL/dSH_k = scale * Y_k(dir) * dL/drgb (zero on clamped
+// channels) into the SH gradient rows, and dL/d(dir) = sum_k (dL/drgb . SH_k)
+// dY_k/d(dir) for K7 (which chains it into the mean).  The view direction and
+// the clamped-channel mask were recorded by K1.  Split from K7 so the
+// FP64 geometry kernel carries no SH state (occupancy) and the 48-row
+// coefficient / gradient traffic runs at high memory-level parallelism.
+__global__ void __launch_bounds__(128) sh_bwd_kernel(int N, const uint32_t* __restrict__ sorted_of_gid,
+                                                     const float* __restrict__ accum, int acc_stride, int n4,
+                                                     const float* __restrict__ p4, int64_t cap4,
+                                                     const float* __restrict__ p3, int64_t cap3, int deg, float scale,
+                                                     float* __restrict__ g4, float* __restrict__ g3,
+                                                     const float4* __restrict__ shdir, float4* __restrict__ ddir) {
+    const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid >= N) return;
+    const uint32_t j = sorted_of_gid[gid];
+    if (j == 0xffffffffu) return;  // not visible in this view
+    const float* acc = accum + (size_t)j * acc_stride;
+    const float4 a03 = *reinterpret_cast<const float4*>(acc);
+    const float4 a47 = *reinterpret_cast<const float4*>(acc + 4);
+    if (a03.x == 0.f && a03.y == 0.f && a03.z == 0.f && a03.w == 0.f && a47.x == 0.f && a47.y == 0.f &&
+        a47.z == 0.f && a47.w == 0.f && acc[8] == 0.f)
+        return;  // untouched (backward.cpp:226): K7 skips it too
+    const bool dyn = gid < n4;
+    const int i = dyn ? gid : gid - n4;
+    const float* Pf = (dyn ? p4 : p3) + i;
+    float* Gs = (dyn ? g4 : g3) + i;
+    const int64_t cap = dyn ? cap4 : cap3;
+    const int shrow = dyn ? R4_SH : R3_SH;
+    const float4 sd = shdir[gid];
+    const float df[3] = {sd.x, sd.y, sd.z};
+    const uint32_t clamped = __float_as_uint(sd.w);
+    const float d_rgb[3] = {a03.x, a03.y, a03.z};
+    float drr[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) drr[c] = ((clamped >> c) & 1u) ? 0.0f : d_rgb[c];
+    float basis[16];
+    sh_basis_f(df, deg, basis);
+    const int K = sh_count(deg);
+    float dotc[16];
+#pragma unroll
+    for (int k0 = 0; k0 < 16; k0 += 4) {
+        // 4 coefficients (12 rows): loads of P and G first, then the G stores
+        float pv[12], gv[12];
+#pragma unroll
+        for (int u = 0; u < 12; ++u)
+            if (k0 + u / 3 < K) {
+                pv[u] = Pf[(int64_t)(shrow + 3 * k0 + u) * cap];
+                gv[u] = Gs[(int64_t)(shrow + 3 * k0 + u) * cap];
+            }
+#pragma unroll
+        for (int u = 0; u < 12; ++u)
+            if (k0 + u / 3 < K) Gs[(int64_t)(shrow + 3 * k0 + u) * cap] = fmaf(scale, basis[k0 + u / 3] * drr[u % 3], gv[u]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            dotc[k0 + q] = k0 + q < K ? fmaf(drr[0], pv[3 * q], fmaf(drr[1], pv[3 * q + 1], drr[2] * pv[3 * q + 2])) : 0.f;
+    }
+    float dd[3];
+    sh_dir_grad_f(df, deg, dotc, dd);
+    ddir[gid] = make_float4(dd[0], dd[1], dd[2], 0.f);
 }
 
 }  // namespace hgs

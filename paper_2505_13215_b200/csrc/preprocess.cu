@@ -184,8 +184,9 @@ __device__ __noinline__ bool clamp_psd_slow(M3& m) {
 
 // SH colour in FP32 (sh.cpp:25-47, 73-83); coefficient k channel c at row
 // base + 3k + c.
-__device__ inline void eval_sh_f32(const float* __restrict__ p, int64_t cap, int i, int base, int deg,
-                                   float dx, float dy, float dz, float rgb[3]) {
+// Returns the bit mask of the channels clamped to [0, 1] (raster.cpp:86 / sh.cpp:81).
+__device__ inline uint32_t eval_sh_f32(const float* __restrict__ p, int64_t cap, int i, int base, int deg,
+                                       float dx, float dy, float dz, float rgb[3]) {
     float basis[16];
     basis[0] = 0.28209479177387814f;
     if (deg >= 1) {
@@ -216,8 +217,14 @@ __device__ inline void eval_sh_f32(const float* __restrict__ p, int64_t cap, int
 #pragma unroll
         for (int c = 0; c < 3; ++c) acc[c] = fmaf(basis[k], __ldg(&p[(int64_t)(base + 3 * k + c) * cap + i]), acc[c]);
     }
+    uint32_t clamped = 0;
 #pragma unroll
-    for (int c = 0; c < 3; ++c) rgb[c] = fminf(fmaxf(acc[c] + 0.5f, 0.0f), 1.0f);
+    for (int c = 0; c < 3; ++c) {
+        const float raw = acc[c] + 0.5f;
+        clamped |= (raw < 0.0f || raw > 1.0f) ? (1u << c) : 0u;
+        rgb[c] = fminf(fmaxf(raw, 0.0f), 1.0f);
+    }
+    return clamped;
 }
 
 __device__ inline uint32_t f32_bits(double d) { return __float_as_uint(__double2float_rn(d)); }
@@ -312,7 +319,7 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
     const float* __restrict__ p4, int64_t cap4, int n4, const float* __restrict__ p3, int64_t cap3,
     int n3, int deg, DevCamera cam, double t, double cutoff, int tiles_x, SplatRec* __restrict__ rec,
     uint32_t* __restrict__ depth_key, uint32_t* __restrict__ ntiles_out,
-    unsigned long long* __restrict__ stats, uint32_t* __restrict__ flags) {
+    unsigned long long* __restrict__ stats, uint32_t* __restrict__ flags, float4* __restrict__ shdir) {
     const int gid = blockIdx.x * blockDim.x + threadIdx.x;
     const int n = n4 + n3;
     uint32_t reason = CULL_DEPTH + 100;  // sentinel: inactive lane
@@ -396,10 +403,12 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
                 d[2] = v[2] / nrm;
             }
             float rgb[3];
-            if (gid < n4)
-                eval_sh_f32(p4, cap4, gid, R4_SH, deg, (float)d[0], (float)d[1], (float)d[2], rgb);
-            else
-                eval_sh_f32(p3, cap3, gid - n4, R3_SH, deg, (float)d[0], (float)d[1], (float)d[2], rgb);
+            const float fd[3] = {(float)d[0], (float)d[1], (float)d[2]};
+            const uint32_t clamped =
+                gid < n4 ? eval_sh_f32(p4, cap4, gid, R4_SH, deg, fd[0], fd[1], fd[2], rgb)
+                         : eval_sh_f32(p3, cap3, gid - n4, R3_SH, deg, fd[0], fd[1], fd[2], rgb);
+            // view direction + clamped-channel mask for the SH backward (K7b)
+            shdir[gid] = make_float4(fd[0], fd[1], fd[2], __uint_as_float(clamped));
             s.alpha = alpha;
             s.alpha_f = (float)alpha;
             s.r = rgb[0];

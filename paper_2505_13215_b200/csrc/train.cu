@@ -139,11 +139,18 @@ hgs_status run_backward(hgs_ctx* ctx, const float* lg, double scale) {
     prof_end(ctx);
     prof_begin(ctx, PH_GAUSS_BWD);
     const int N = (int)(ctx->n4 + ctx->n3);
+    CK(ctx->ddir.ensure((size_t)N * sizeof(float4)));
+    sh_bwd_kernel<<<div_up((uint32_t)N, 128), 128, 0, st>>>(
+        N, ctx->sorted_of_gid.as<uint32_t>(), ctx->accum.as<float>(), kAccStrideHost, (int)ctx->n4,
+        ctx->p4.as<float>(), ctx->cap4, ctx->p3.as<float>(), ctx->cap3, ctx->deg, (float)scale, ctx->g4, ctx->g3,
+        ctx->shdir.as<float4>(), ctx->ddir.as<float4>());
+    count_launch();
+    CKL();
     gaussian_bwd_kernel<<<div_up((uint32_t)N, 128), 128, 0, st>>>(
         N, ctx->sorted_of_gid.as<uint32_t>(), ctx->accum.as<float>(), kAccStrideHost, (int)ctx->n4, ctx->p4.as<float>(), ctx->cap4,
         ctx->p3.as<float>(), ctx->cap3, ctx->deg, ctx->cam, ctx->t, scale, ctx->g4, ctx->g3, ctx->sn4.as<float>(),
         ctx->sn3.as<float>(), ctx->dgn4, ctx->dgn3, ctx->dcnt4, ctx->dcnt3, &ctx->rec_sorted.as<SplatRec>()->c00,
-        (int)(sizeof(SplatRec) / sizeof(double)));
+        (int)(sizeof(SplatRec) / sizeof(double)), ctx->ddir.as<float4>());
     count_launch();
     CKL();
     prof_end(ctx);
