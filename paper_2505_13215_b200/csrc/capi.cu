@@ -302,13 +302,13 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
         CK(ctx->ntiles.ensure((size_t)N * 4));
         CK(ctx->visflag.ensure((size_t)N * 4));
         CK(ctx->vispos.ensure((size_t)N * 4));
-        CK(ctx->shdir.ensure((size_t)N * sizeof(float4)));
+        CK(ctx->shdir.ensure((size_t)N * sizeof(ShRec)));
         CK(ctx->scan_ws.ensure(scan_workspace_bytes(N) + 4096));
         prof_begin(ctx, PH_PREPROCESS);
         preprocess_kernel<<<div_up(N, 256), 256, 0, st>>>(
             ctx->p4.as<float>(), ctx->cap4, n4, ctx->p3.as<float>(), ctx->cap3, n3, ctx->deg, ctx->cam, t, cutoff,
             tiles_x, ctx->rec.as<SplatRec>(), ctx->depth_key.as<uint32_t>(), ctx->ntiles.as<uint32_t>(), dc->stats,
-            &dc->flags, ctx->shdir.as<float4>());
+            &dc->flags, ctx->shdir.as<ShRec>());
         count_launch();
         CKL();
         visflag_kernel<<<div_up(N, 256), 256, 0, st>>>(ctx->ntiles.as<uint32_t>(), N, ctx->visflag.as<uint32_t>());
@@ -610,6 +610,7 @@ hgs_status hgs_scene_upload(hgs_ctx* ctx, const hgs_host_scene* s, int dtype) {
         ctx->gbuf_floats = f4 + f3 + 2 * ctx->cap4 + 2 * ctx->cap3;
         CK(ctx->gbuf.ensure((size_t)ctx->gbuf_floats * 4));
         CK(cudaMemsetAsync(ctx->gbuf.p, 0, (size_t)ctx->gbuf_floats * 4, ctx->stream));
+        ctx->grads_zero = true;
         float* g = ctx->gbuf.as<float>();
         ctx->g4 = g;
         ctx->g3 = g + f4;

@@ -82,6 +82,7 @@ struct hgs_pending_step {
 
 struct hgs_ctx {
     bool stats_pending = false;  // counters of the last render not read back yet
+    bool grads_zero = false;     // the packed gradient buffer is known to be all zero (K7/K7b store, no RMW)
     std::deque<hgs_pending_step> pipeline;  // hgs_train_step_async iterations, oldest first
     int pipe_next = 0;                      // next step-sum slot
     cudaEvent_t pipe_ev[HGS_TRAIN_PIPELINE] = {};

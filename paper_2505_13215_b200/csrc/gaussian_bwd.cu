@@ -9,6 +9,7 @@
 // grad += scale * d, the per-image screen-space norm, and the densification
 // statistics (train.cpp:433-444).  Coalesced SoA reads/writes; HBM bound.
 #include "kernels.cuh"
+#include "sh.cuh"
 
 namespace hgs {
 
@@ -29,77 +30,6 @@ __device__ inline void isoR(const double q[4], double R[4][4]) {
 
 __device__ inline double sigmoid(double x) { return 1.0 / (1.0 + exp(-x)); }
 
-// sh.cpp:25-47 in FP32
-__device__ inline void sh_basis_f(const float d[3], int deg, float out[16]) {
-    const float x = d[0], y = d[1], z = d[2];
-    out[0] = 0.28209479177387814f;
-    if (deg < 1) return;
-    out[1] = -0.4886025119029199f * y;
-    out[2] = 0.4886025119029199f * z;
-    out[3] = -0.4886025119029199f * x;
-    if (deg < 2) return;
-    const float xx = x * x, yy = y * y, zz = z * z;
-    out[4] = 1.0925484305920792f * x * y;
-    out[5] = -1.0925484305920792f * y * z;
-    out[6] = 0.31539156525252005f * (2.0f * zz - xx - yy);
-    out[7] = -1.0925484305920792f * x * z;
-    out[8] = 0.5462742152960396f * (xx - yy);
-    if (deg < 3) return;
-    out[9] = -0.5900435899266435f * y * (3.0f * xx - yy);
-    out[10] = 2.890611442640554f * x * y * z;
-    out[11] = -0.4570457994644658f * y * (4.0f * zz - xx - yy);
-    out[12] = 0.3731763325901154f * z * (2.0f * zz - 3.0f * xx - 3.0f * yy);
-    out[13] = -0.4570457994644658f * x * (4.0f * zz - xx - yy);
-    out[14] = 1.445305721320277f * z * (xx - yy);
-    out[15] = -0.5900435899266435f * x * (xx - 3.0f * yy);
-}
-
-// sum_k w_k * dY_k/d(dir) (sh.cpp:49-71) without materialising the 16x3 Jacobian
-__device__ inline void sh_dir_grad_f(const float d[3], int deg, const float w[16], float g[3]) {
-    const float x = d[0], y = d[1], z = d[2];
-    g[0] = g[1] = g[2] = 0.0f;
-    if (deg < 1) return;
-    const float C1 = 0.4886025119029199f;
-    g[1] -= C1 * w[1];
-    g[2] += C1 * w[2];
-    g[0] -= C1 * w[3];
-    if (deg < 2) return;
-    const float A = 1.0925484305920792f, B = 0.31539156525252005f, Cc = 0.5462742152960396f;
-    g[0] += A * y * w[4];
-    g[1] += A * x * w[4];
-    g[1] -= A * z * w[5];
-    g[2] -= A * y * w[5];
-    g[0] += B * (-2.0f * x) * w[6];
-    g[1] += B * (-2.0f * y) * w[6];
-    g[2] += B * (4.0f * z) * w[6];
-    g[0] -= A * z * w[7];
-    g[2] -= A * x * w[7];
-    g[0] += Cc * (2.0f * x) * w[8];
-    g[1] += Cc * (-2.0f * y) * w[8];
-    if (deg < 3) return;
-    const float xx = x * x, yy = y * y, zz = z * z;
-    const float D0 = -0.5900435899266435f, D1 = 2.890611442640554f, D2 = -0.4570457994644658f,
-                D3 = 0.3731763325901154f, D5 = 1.445305721320277f;
-    g[0] += D0 * (6.0f * x * y) * w[9];
-    g[1] += D0 * (3.0f * xx - 3.0f * yy) * w[9];
-    g[0] += D1 * (y * z) * w[10];
-    g[1] += D1 * (x * z) * w[10];
-    g[2] += D1 * (x * y) * w[10];
-    g[0] += D2 * (-2.0f * x * y) * w[11];
-    g[1] += D2 * (4.0f * zz - xx - 3.0f * yy) * w[11];
-    g[2] += D2 * (8.0f * y * z) * w[11];
-    g[0] += D3 * (-6.0f * x * z) * w[12];
-    g[1] += D3 * (-6.0f * y * z) * w[12];
-    g[2] += D3 * (6.0f * zz - 3.0f * xx - 3.0f * yy) * w[12];
-    g[0] += D2 * (4.0f * zz - 3.0f * xx - yy) * w[13];
-    g[1] += D2 * (-2.0f * x * y) * w[13];
-    g[2] += D2 * (8.0f * x * z) * w[13];
-    g[0] += D5 * (2.0f * x * z) * w[14];
-    g[1] += D5 * (-2.0f * y * z) * w[14];
-    g[2] += D5 * (xx - yy) * w[14];
-    g[0] += D0 * (3.0f * xx - 3.0f * yy) * w[15];
-    g[1] += D0 * (-6.0f * x * y) * w[15];
-}
 
 }  // namespace
 
@@ -109,7 +39,7 @@ __global__ void __launch_bounds__(128, 4) gaussian_bwd_kernel(
     double t, double scale, float* __restrict__ g4, float* __restrict__ g3, float* __restrict__ sn4,
     float* __restrict__ sn3, float* __restrict__ gn4, float* __restrict__ gn3, float* __restrict__ cnt4,
     float* __restrict__ cnt3, const double* __restrict__ conic_src, int conic_stride,
-    const float4* __restrict__ ddir) {
+    const float4* __restrict__ ddir, int first) {
     // one thread per Gaussian in pool order (coalesced SoA parameter and
     // gradient rows); the splat's accumulators are found through the
     // gid -> depth-sorted index map written by the gather kernel
@@ -298,7 +228,7 @@ __global__ void __launch_bounds__(128, 4) gaussian_bwd_kernel(
         }
         float old[R3_SH];
 #pragma unroll
-        for (int r = 0; r < R3_SH; ++r) old[r] = G[(int64_t)r * cap + i];
+        for (int r = 0; r < R3_SH; ++r) old[r] = first ? 0.0f : G[(int64_t)r * cap + i];
 #pragma unroll
         for (int r = 0; r < R3_SH; ++r) G[(int64_t)r * cap + i] = old[r] + gacc[r];
     } else {
@@ -379,7 +309,7 @@ __global__ void __launch_bounds__(128, 4) gaussian_bwd_kernel(
         }
         float old[R4_SH];
 #pragma unroll
-        for (int r = 0; r < R4_SH; ++r) old[r] = G[(int64_t)r * cap + i];
+        for (int r = 0; r < R4_SH; ++r) old[r] = first ? 0.0f : G[(int64_t)r * cap + i];
 #pragma unroll
         for (int r = 0; r < R4_SH; ++r) G[(int64_t)r * cap + i] = old[r] + gacc[r];
     }
@@ -397,7 +327,8 @@ __global__ void __launch_bounds__(128) sh_bwd_kernel(int N, const uint32_t* __re
                                                      const float* __restrict__ p4, int64_t cap4,
                                                      const float* __restrict__ p3, int64_t cap3, int deg, float scale,
                                                      float* __restrict__ g4, float* __restrict__ g3,
-                                                     const float4* __restrict__ shdir, float4* __restrict__ ddir) {
+                                                     const ShRec* __restrict__ shrec, float4* __restrict__ ddir,
+                                                     int first) {
     const int gid = blockIdx.x * blockDim.x + threadIdx.x;
     if (gid >= N) return;
     const uint32_t j = sorted_of_gid[gid];
@@ -410,41 +341,43 @@ __global__ void __launch_bounds__(128) sh_bwd_kernel(int N, const uint32_t* __re
         return;  // untouched (backward.cpp:226): K7 skips it too
     const bool dyn = gid < n4;
     const int i = dyn ? gid : gid - n4;
-    const float* Pf = (dyn ? p4 : p3) + i;
     float* Gs = (dyn ? g4 : g3) + i;
     const int64_t cap = dyn ? cap4 : cap3;
     const int shrow = dyn ? R4_SH : R3_SH;
-    const float4 sd = shdir[gid];
-    const float df[3] = {sd.x, sd.y, sd.z};
-    const uint32_t clamped = __float_as_uint(sd.w);
+    const ShRec sr = shrec[gid];
+    const float df[3] = {sr.dir.x, sr.dir.y, sr.dir.z};
+    const uint32_t clamped = __float_as_uint(sr.dir.w);
     const float d_rgb[3] = {a03.x, a03.y, a03.z};
     float drr[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) drr[c] = ((clamped >> c) & 1u) ? 0.0f : d_rgb[c];
+    // dL/d(direction) = sum_c drr_c * d rgb_c / d direction (K1's Jacobian)
+    ddir[gid] = make_float4(fmaf(drr[0], sr.j[0].x, fmaf(drr[1], sr.j[1].x, drr[2] * sr.j[2].x)),
+                            fmaf(drr[0], sr.j[0].y, fmaf(drr[1], sr.j[1].y, drr[2] * sr.j[2].y)),
+                            fmaf(drr[0], sr.j[0].z, fmaf(drr[1], sr.j[1].z, drr[2] * sr.j[2].z)), 0.f);
     float basis[16];
     sh_basis_f(df, deg, basis);
     const int K = sh_count(deg);
-    float dotc[16];
+    float* G = Gs + (int64_t)shrow * cap;
+    if (first) {  // the gradient buffer is known to be zero: plain stores
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+            if (k < K)
+#pragma unroll
+                for (int c = 0; c < 3; ++c) G[(int64_t)(3 * k + c) * cap] = scale * (basis[k] * drr[c]);
+        return;
+    }
 #pragma unroll
     for (int k0 = 0; k0 < 16; k0 += 4) {
-        // 4 coefficients (12 rows): loads of P and G first, then the G stores
-        float pv[12], gv[12];
+        // 4 coefficients (12 rows): loads first, then the stores
+        float gv[12];
 #pragma unroll
         for (int u = 0; u < 12; ++u)
-            if (k0 + u / 3 < K) {
-                pv[u] = Pf[(int64_t)(shrow + 3 * k0 + u) * cap];
-                gv[u] = Gs[(int64_t)(shrow + 3 * k0 + u) * cap];
-            }
+            if (k0 + u / 3 < K) gv[u] = G[(int64_t)(3 * k0 + u) * cap];
 #pragma unroll
         for (int u = 0; u < 12; ++u)
-            if (k0 + u / 3 < K) Gs[(int64_t)(shrow + 3 * k0 + u) * cap] = fmaf(scale, basis[k0 + u / 3] * drr[u % 3], gv[u]);
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-            dotc[k0 + q] = k0 + q < K ? fmaf(drr[0], pv[3 * q], fmaf(drr[1], pv[3 * q + 1], drr[2] * pv[3 * q + 2])) : 0.f;
+            if (k0 + u / 3 < K) G[(int64_t)(3 * k0 + u) * cap] = fmaf(scale, basis[k0 + u / 3] * drr[u % 3], gv[u]);
     }
-    float dd[3];
-    sh_dir_grad_f(df, deg, dotc, dd);
-    ddir[gid] = make_float4(dd[0], dd[1], dd[2], 0.f);
 }
 
 }  // namespace hgs

@@ -10,7 +10,7 @@ __global__ void preprocess_kernel(const float* __restrict__ p4, int64_t cap4, in
                                   int64_t cap3, int n3, int deg, DevCamera cam, double t, double cutoff, int tiles_x,
                                   SplatRec* __restrict__ rec, uint32_t* __restrict__ depth_key,
                                   uint32_t* __restrict__ ntiles_out, unsigned long long* __restrict__ stats,
-                                  uint32_t* __restrict__ flags, float4* __restrict__ shdir);
+                                  uint32_t* __restrict__ flags, ShRec* __restrict__ shrec);
 
 // raster_fwd.cu (K2 + K4)
 __global__ void gather_sorted_kernel(const uint32_t* __restrict__ sorted_gid, const uint32_t* __restrict__ V_dev,
@@ -51,8 +51,8 @@ __global__ void raster_fixup_kernel(const uint32_t* __restrict__ fix_list, const
 __global__ void sh_bwd_kernel(int N, const uint32_t* __restrict__ sorted_of_gid, const float* __restrict__ accum,
                               int acc_stride, int n4, const float* __restrict__ p4, int64_t cap4,
                               const float* __restrict__ p3, int64_t cap3, int deg, float scale,
-                              float* __restrict__ g4, float* __restrict__ g3, const float4* __restrict__ shdir,
-                              float4* __restrict__ ddir);
+                              float* __restrict__ g4, float* __restrict__ g3, const ShRec* __restrict__ shrec,
+                              float4* __restrict__ ddir, int first);
 
 }  // namespace hgs
 
@@ -77,7 +77,7 @@ __global__ void gaussian_bwd_kernel(int N, const uint32_t* __restrict__ sorted_o
                                     double scale, float* __restrict__ g4, float* __restrict__ g3,
                                     float* __restrict__ sn4, float* __restrict__ sn3, float* __restrict__ gn4,
                                     float* __restrict__ gn3, float* __restrict__ cnt4, float* __restrict__ cnt3,
-                                    const double* __restrict__ conic_src, int conic_stride, const float4* __restrict__ ddir);
+                                    const double* __restrict__ conic_src, int conic_stride, const float4* __restrict__ ddir, int first);
 // loss.cu (K5)
 void set_ssim_window();
 __global__ void ssim_fwd_kernel(const float* __restrict__ a, const float* __restrict__ b, int W, int H,
@@ -123,7 +123,7 @@ __global__ void compact_survivors_kernel(const float* __restrict__ src, float* _
 __global__ void sh_bwd_kernel(int N, const uint32_t* __restrict__ sorted_of_gid, const float* __restrict__ accum,
                               int acc_stride, int n4, const float* __restrict__ p4, int64_t cap4,
                               const float* __restrict__ p3, int64_t cap3, int deg, float scale,
-                              float* __restrict__ g4, float* __restrict__ g3, const float4* __restrict__ shdir,
-                              float4* __restrict__ ddir);
+                              float* __restrict__ g4, float* __restrict__ g3, const ShRec* __restrict__ shrec,
+                              float4* __restrict__ ddir, int first);
 
 }  // namespace hgs

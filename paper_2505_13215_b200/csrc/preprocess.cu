@@ -12,6 +12,8 @@
 // coalesced from the component-major SoA pools; writes an 80 B SplatRec, a
 // depth key and a tile count.  Bound: HBM.
 #include "hgs_common.cuh"
+#include "raster_common.cuh"
+#include "sh.cuh"
 
 namespace hgs {
 
@@ -319,7 +321,7 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
     const float* __restrict__ p4, int64_t cap4, int n4, const float* __restrict__ p3, int64_t cap3,
     int n3, int deg, DevCamera cam, double t, double cutoff, int tiles_x, SplatRec* __restrict__ rec,
     uint32_t* __restrict__ depth_key, uint32_t* __restrict__ ntiles_out,
-    unsigned long long* __restrict__ stats, uint32_t* __restrict__ flags, float4* __restrict__ shdir) {
+    unsigned long long* __restrict__ stats, uint32_t* __restrict__ flags, ShRec* __restrict__ shrec) {
     const int gid = blockIdx.x * blockDim.x + threadIdx.x;
     const int n = n4 + n3;
     uint32_t reason = CULL_DEPTH + 100;  // sentinel: inactive lane
@@ -407,8 +409,31 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
             const uint32_t clamped =
                 gid < n4 ? eval_sh_f32(p4, cap4, gid, R4_SH, deg, fd[0], fd[1], fd[2], rgb)
                          : eval_sh_f32(p3, cap3, gid - n4, R3_SH, deg, fd[0], fd[1], fd[2], rgb);
-            // view direction + clamped-channel mask for the SH backward (K7b)
-            shdir[gid] = make_float4(fd[0], fd[1], fd[2], __uint_as_float(clamped));
+            // view direction, clamped-channel mask and d rgb / d direction for
+            // the SH backward (K7b): it then needs no SH coefficient
+            {
+                const float* P = gid < n4 ? p4 : p3;
+                const int64_t cap = gid < n4 ? cap4 : cap3;
+                const int i = gid < n4 ? gid : gid - n4;
+                const int shrow = gid < n4 ? R4_SH : R3_SH;
+                const int K = sh_count(deg);
+                ShRec sr;
+                sr.dir = make_float4(fd[0], fd[1], fd[2], __uint_as_float(clamped));
+                float* jr[3] = {&sr.j[0].x, &sr.j[1].x, &sr.j[2].x};
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    float w[16];
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) w[k] = k < K ? __ldg(&P[(int64_t)(shrow + 3 * k + c) * cap + i]) : 0.f;
+                    float g[3];
+                    sh_dir_grad_f(fd, deg, w, g);
+                    jr[c][0] = g[0];
+                    jr[c][1] = g[1];
+                    jr[c][2] = g[2];
+                    jr[c][3] = 0.f;
+                }
+                shrec[gid] = sr;
+            }
             s.alpha = alpha;
             s.alpha_f = (float)alpha;
             s.r = rgb[0];

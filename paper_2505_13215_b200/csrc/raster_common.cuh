@@ -48,6 +48,14 @@ struct __align__(16) CullRec {
     float a, b, c, pcut;
 };
 
+// Per-Gaussian colour record of K1 for the SH backward (K7b): the FP32 view
+// direction, the mask of channels clamped to [0,1] and the Jacobian
+// J[c] = d rgb_c / d direction of the unclamped SH colour.
+struct __align__(16) ShRec {
+    float4 dir;   // x, y, z, clamped-channel bits
+    float4 j[3];  // J[c].xyz
+};
+
 // Instance value = sorted splat index | (8x8-quadrant contribution mask << 28).
 constexpr int kInstMaskShift = 28;
 constexpr uint32_t kInstIndexMask = (1u << kInstMaskShift) - 1u;

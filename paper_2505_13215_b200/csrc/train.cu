@@ -143,16 +143,17 @@ hgs_status run_backward(hgs_ctx* ctx, const float* lg, double scale) {
     sh_bwd_kernel<<<div_up((uint32_t)N, 128), 128, 0, st>>>(
         N, ctx->sorted_of_gid.as<uint32_t>(), ctx->accum.as<float>(), kAccStrideHost, (int)ctx->n4,
         ctx->p4.as<float>(), ctx->cap4, ctx->p3.as<float>(), ctx->cap3, ctx->deg, (float)scale, ctx->g4, ctx->g3,
-        ctx->shdir.as<float4>(), ctx->ddir.as<float4>());
+        ctx->shdir.as<ShRec>(), ctx->ddir.as<float4>(), ctx->grads_zero ? 1 : 0);
     count_launch();
     CKL();
     gaussian_bwd_kernel<<<div_up((uint32_t)N, 128), 128, 0, st>>>(
         N, ctx->sorted_of_gid.as<uint32_t>(), ctx->accum.as<float>(), kAccStrideHost, (int)ctx->n4, ctx->p4.as<float>(), ctx->cap4,
         ctx->p3.as<float>(), ctx->cap3, ctx->deg, ctx->cam, ctx->t, scale, ctx->g4, ctx->g3, ctx->sn4.as<float>(),
         ctx->sn3.as<float>(), ctx->dgn4, ctx->dgn3, ctx->dcnt4, ctx->dcnt3, &ctx->rec_sorted.as<SplatRec>()->c00,
-        (int)(sizeof(SplatRec) / sizeof(double)), ctx->ddir.as<float4>());
+        (int)(sizeof(SplatRec) / sizeof(double)), ctx->ddir.as<float4>(), ctx->grads_zero ? 1 : 0);
     count_launch();
     CKL();
+    ctx->grads_zero = false;
     prof_end(ctx);
     return HGS_OK;
 }
@@ -258,6 +259,9 @@ hgs_status run_adam(hgs_ctx* ctx, const hgs_lrs* lrs, double mean_lr_scale, cons
             CKL();
         }
     }
+    // the update zeroes every gradient row (a gated-off update does not: the
+    // NumericAbort paths clear the buffer themselves)
+    ctx->grads_zero = true;
     prof_end(ctx);
     return HGS_OK;
 }
@@ -303,6 +307,7 @@ hgs_status hgs_backward(hgs_ctx* ctx, const void* loss_grad, int dtype, int on_d
 hgs_status hgs_zero_grads(hgs_ctx* ctx) {
     if (!ctx) return HGS_ERR_INVALID_ARGUMENT;
     if (ctx->gbuf.p) CK(cudaMemsetAsync(ctx->gbuf.p, 0, (size_t)ctx->gbuf_floats * 4, ctx->stream));
+    ctx->grads_zero = ctx->gbuf.p != nullptr;
     return HGS_OK;
 }
 
@@ -332,6 +337,7 @@ hgs_status hgs_grads_device(hgs_ctx* ctx, float** ptr, int64_t* count) {
     if (!ctx || !ptr || !count) return HGS_ERR_INVALID_ARGUMENT;
     *ptr = ctx->gbuf.as<float>();
     *count = ctx->gbuf_floats;
+    ctx->grads_zero = false;  // the caller may write into it (e.g. an in-place all-reduce)
     return HGS_OK;
 }
 
@@ -544,6 +550,7 @@ hgs_status hgs_sweep_convert(hgs_ctx* ctx, int64_t* moved_out, hgs_conversion_re
     CK(cudaMemsetAsync(ctx->gn3.p, 0, (size_t)ctx->cap3 * 4, st));
     CK(cudaMemsetAsync(ctx->cnt3.p, 0, (size_t)ctx->cap3 * 4, st));
     CK(cudaMemsetAsync(ctx->gbuf.p, 0, (size_t)ctx->gbuf_floats * 4, st));
+    ctx->grads_zero = true;
     CK(cudaStreamSynchronize(st));
     ctx->have_tape = false;
     rep.count = cnt;
@@ -669,7 +676,11 @@ hgs_status train_step_impl(hgs_ctx* ctx, int n_views, const hgs_camera* cams, co
     if (r != HGS_OK) return r;
     if (loss_out) *loss_out = loss;
     if (!std::isfinite(loss)) {
-        if (apply_adam) --ctx->step;  // the kernels skipped the update
+        if (apply_adam) {
+            --ctx->step;  // the kernels skipped the update (and left the gradients)
+            CK(cudaMemsetAsync(ctx->gbuf.p, 0, (size_t)ctx->gbuf_floats * 4, ctx->stream));
+            ctx->grads_zero = true;
+        }
         return fail(ctx, HGS_ERR_NUMERIC_ABORT, "train: non-finite loss");  // train.cpp:445-447
     }
     prof_collect(ctx);
@@ -711,6 +722,9 @@ hgs_status hgs_train_collect(hgs_ctx* ctx, double* loss_out) {
         ctx->pipe_next = 0;
         CK(cudaStreamSynchronize(ctx->stream));
         CK(cudaMemsetAsync(&scratch(ctx)->abort, 0, sizeof(uint32_t), ctx->stream));
+        // the skipped updates left gradients behind: start the next iteration from zero
+        CK(cudaMemsetAsync(ctx->gbuf.p, 0, (size_t)ctx->gbuf_floats * 4, ctx->stream));
+        ctx->grads_zero = true;
         CK(cudaStreamSynchronize(ctx->stream));
         return fail(ctx, HGS_ERR_NUMERIC_ABORT, "train: non-finite loss");  // train.cpp:445-447
     }
