@@ -57,8 +57,9 @@ def summarize(rep):
     d = {}
     for r in det[1:]:
         d.setdefault(r[mi], r[vi])
+    kname = name.split("(")[0].replace("void ", "").split("::")[-1].split("<")[0].strip()
     return {
-        "kernel": name.split("(")[0],
+        "kernel": kname,
         "duration_us": round(dur_ns * scale, 2) if dur_ns else None,
         "dram_bytes_per_launch": int(rd * bscale + wr * bscale2) if rd is not None and wr is not None else None,
         "issue_slots_busy_pct": num(d.get("Issue Slots Busy")),
