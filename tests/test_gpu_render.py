@@ -179,3 +179,14 @@ def test_cpp_consumer_runs(tmp_path):
     alpha = 0.7 * math.exp(-0.5 * d @ (np.array(s["conic"]).reshape(2, 2) @ d))
     for c, (rgb, bgc) in enumerate(zip((0.9, 0.1, 0.3), (0.0, 0.0, 1.0))):
         assert vals[c] == pytest.approx(rgb * alpha + bgc * (1 - alpha), abs=1e-6)
+
+
+def test_c2_config_parity(ctx):
+    """configs[1] at full size: 240k 4D + 60k 3D Gaussians, SH 3, 1352x1014 --
+    every projected splat, the complete tile-sorted instance list (~3.8M) and
+    the image against the oracle."""
+    scene = synthetic_scene(240_000, 60_000, 3, seed=2, tau=0.5)
+    cam = ring_camera(2, 1352, 1014, index=5, n_ring=16)
+    check_render(ctx, scene, cam, 1.0 / 3.0, threads=O.hardware_threads())
+    info = ctx.render_info()
+    assert info["instances"] > 1_000_000 and info["kept_instances"] < info["instances"]

@@ -316,3 +316,32 @@ def test_pipelined_nonfinite_loss_keeps_last_good_state(ctx):
     tr._pending_n = []
     assert np.isfinite(tr.step([2, 3]))  # usable again: the sticky flag was cleared
     assert ctx.download().mean_x.tolist() != good.mean_x.tolist()
+
+
+def test_gradients_c2_full_size(ctx):
+    """configs[1] at full size (300k Gaussians, SH 3, 1352x1014, one view):
+    the real photometric-loss gradient against the 8-bit GT of another scene
+    (SURVEY.md 8d), every parameter gradient against the oracle's backward."""
+    from paper_2505_13215_b200.train import quantize_8bit
+
+    scene = synthetic_scene(240_000, 60_000, 3, seed=2, tau=0.5).as_float32_exact()
+    target = synthetic_scene(240_000, 60_000, 3, seed=1002, tau=0.5)
+    cam = ring_camera(2, 1352, 1014, index=0, n_ring=16)
+    bg = (0.2, 0.2, 0.2)
+    ctx.upload(target)
+    gt = quantize_8bit(ctx.render(cam, 0.0, bg)["rgb"].astype(np.float64))
+    ctx.upload(scene)
+    img = ctx.forward_train(cam, 0.0, bg)
+    loss, w = O.photometric_loss_with_grad(img.astype(np.float64), gt, 0.2)  # the oracle's dL/dimage
+    ref_img, tape = O.forward_train(scene, cam, 0.0, bg, num_threads=O.hardware_threads())
+    assert np.abs(img - ref_img).max() <= 1e-4
+    ctx.backward(w)
+    g = ctx.grads()
+    r = O.backward(scene, cam, tape, w)
+    rep = grad_report(g, r, scene)
+    n_el = sum(v["n"] for v in rep.values())
+    n_bad = sum(v["n_bad"] for v in rep.values())
+    print({k: (v["max_rel"], v["n_bad"], v["norm_ratio"]) for k, v in rep.items()})
+    assert n_bad <= 1e-4 * n_el, (n_bad, n_el)
+    for k, v in rep.items():
+        assert abs(v["norm_ratio"] - 1.0) < 1e-3, (k, v)
