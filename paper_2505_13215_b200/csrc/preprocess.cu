@@ -317,7 +317,7 @@ __device__ inline double sigmoid(double x) { return 1.0 / (1.0 + exp(-x)); }
 
 // K1.  stats[0..5] = culled_depth, culled_offscreen, culled_degenerate,
 // culled_temporal, degenerate_temporal, projected.
-__global__ void __launch_bounds__(256) preprocess_kernel(
+__global__ void __launch_bounds__(256, 3) preprocess_kernel(
     const float* __restrict__ p4, int64_t cap4, int n4, const float* __restrict__ p3, int64_t cap3,
     int n3, int deg, DevCamera cam, double t, double cutoff, int tiles_x, SplatRec* __restrict__ rec,
     uint32_t* __restrict__ depth_key, uint32_t* __restrict__ ntiles_out,
