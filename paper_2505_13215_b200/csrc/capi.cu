@@ -373,14 +373,49 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
         CK(ctx->inst_v.ensure((size_t)I * 4));
         CK(ctx->inst_k2.ensure((size_t)I * 4));
         CK(ctx->inst_v2.ensure((size_t)I * 4));
-        prof_begin(ctx, PH_DUPLICATE);
         const int cull = want_count ? 0 : 1;  // count_map counts every box-covered splat
+        const uint32_t dup_blocks = div_up((uint32_t)I, kDupPerCtaHost);
+        CK(ctx->dup_first.ensure((size_t)dup_blocks * 4));
+        if (cull && !ctx->debug_full_list) {
+            // production path: duplication + exact culling + order-preserving
+            // compaction in one kernel, then the stable tile sort of the kept
+            prof_begin(ctx, PH_DUPLICATE);
+            CK(ctx->dup_status.ensure((size_t)dup_blocks * 8 + 64));
+            unsigned long long* status = ctx->dup_status.as<unsigned long long>();
+            uint32_t* counter = reinterpret_cast<uint32_t*>(status + dup_blocks);
+            CK(cudaMemsetAsync(status, 0, (size_t)dup_blocks * 8 + 4, st));
+            dup_bounds_kernel<<<div_up((uint32_t)V, 256), 256, 0, st>>>(
+                ctx->inst_off.as<uint32_t>(), ctx->ntiles_sorted.as<uint32_t>(), (int)V, ctx->dup_first.as<uint32_t>());
+            count_launch();
+            duplicate_compact_kernel<<<dup_blocks, 256, 0, st>>>(
+                ctx->fast_sorted.as<SplatFast>(), (int)V, ctx->inst_off.as<uint32_t>(), tiles_x,
+                ctx->pcut.as<CullRec>(), ctx->dup_first.as<uint32_t>(), (int)I, ctx->inst_k2.as<uint32_t>(),
+                ctx->inst_v2.as<uint32_t>(), &dc->I_kept, status, counter);
+            count_launch();
+            CKL();
+            prof_end(ctx);
+            prof_begin(ctx, PH_TILE_SORT);
+            int bits = 1;
+            while ((1 << bits) < n_tiles) ++bits;
+            const int end_bit = ((bits + 7) / 8) * 8;
+            CK(ctx->sort_ws.ensure(radix_workspace_bytes((int)I) + 4096));
+            ctx->inst_keys_all = ctx->inst_vals_all = nullptr;
+            int which = radix_sort_pairs(ctx->inst_k2.as<uint32_t>(), ctx->inst_v2.as<uint32_t>(),
+                                         ctx->inst_k.as<uint32_t>(), ctx->inst_v.as<uint32_t>(), (int)I, 0, end_bit,
+                                         ctx->sort_ws.as<uint32_t>(), st, &dc->I_kept);
+            CKL();
+            uint32_t* keys = which ? ctx->inst_k.as<uint32_t>() : ctx->inst_k2.as<uint32_t>();
+            inst_vals = which ? ctx->inst_v.as<uint32_t>() : ctx->inst_v2.as<uint32_t>();
+            tile_ranges_dev_kernel<<<div_up((uint32_t)I, 256), 256, 0, st>>>(keys, &dc->I_kept, ctx->ranges.as<uint2>());
+            count_launch();
+            CKL();
+            prof_end(ctx);
+        } else {
+        prof_begin(ctx, PH_DUPLICATE);
         if (cull) {
             CK(ctx->inst_flag.ensure((size_t)I * 4));
             CK(ctx->inst_pos.ensure((size_t)I * 4));
         }
-        const uint32_t dup_blocks = div_up((uint32_t)I, kDupPerCtaHost);
-        CK(ctx->dup_first.ensure((size_t)dup_blocks * 4));
         dup_bounds_kernel<<<div_up((uint32_t)V, 256), 256, 0, st>>>(
             ctx->inst_off.as<uint32_t>(), ctx->ntiles_sorted.as<uint32_t>(), (int)V, ctx->dup_first.as<uint32_t>());
         count_launch();
@@ -444,6 +479,7 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
         }
         CKL();
         prof_end(ctx);
+        }
     }
     ctx->inst_vals_final = inst_vals;
     prof_begin(ctx, PH_RASTER_FWD);
@@ -552,7 +588,7 @@ void hgs_ctx_destroy(hgs_ctx* ctx) {
                     &ctx->sort_v2, &ctx->rec_sorted, &ctx->fast_sorted, &ctx->ntiles_sorted, &ctx->inst_off,
                     &ctx->inst_k, &ctx->inst_v, &ctx->inst_k2, &ctx->inst_v2, &ctx->ranges, &ctx->sorted_of_gid, &ctx->inst_flag, &ctx->inst_pos, &ctx->dbg_k, &ctx->dbg_v, &ctx->scan_ws,
                     &ctx->sort_ws, &ctx->counters, &ctx->img, &ctx->last, &ctx->tfinal, &ctx->trans, &ctx->count,
-                    &ctx->fix_list, &ctx->accum, &ctx->lgrad, &ctx->gt_stage, &ctx->loss_ws, &ctx->stage, &ctx->adam_ok, &ctx->pcut, &ctx->dup_first, &ctx->shdir, &ctx->ddir};
+                    &ctx->fix_list, &ctx->accum, &ctx->lgrad, &ctx->gt_stage, &ctx->loss_ws, &ctx->stage, &ctx->adam_ok, &ctx->pcut, &ctx->dup_first, &ctx->shdir, &ctx->ddir, &ctx->dup_status};
     for (DBuf* b : bufs) b->release();
     ctx->pinned.release();
     ctx->pinned_ctr.release();

@@ -24,6 +24,11 @@ __global__ void duplicate_kernel(const SplatFast* __restrict__ fast, const Splat
                                  const CullRec* __restrict__ cull_rec, uint32_t* __restrict__ keys,
                                  uint32_t* __restrict__ vals, uint32_t* __restrict__ keep,
                                  const uint32_t* __restrict__ cta_first, int I);
+__global__ void duplicate_compact_kernel(const SplatFast* __restrict__ fast, int V, const uint32_t* __restrict__ offsets,
+                                         int tiles_x, const CullRec* __restrict__ cull_rec,
+                                         const uint32_t* __restrict__ cta_first, int I, uint32_t* __restrict__ keys_out,
+                                         uint32_t* __restrict__ vals_out, uint32_t* __restrict__ kept_total,
+                                         unsigned long long* status, uint32_t* __restrict__ counter);
 __global__ void dup_bounds_kernel(const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ ntiles_sorted,
                                   int V, uint32_t* __restrict__ cta_first);
 __global__ void compact_instances_kernel(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals, int n,

@@ -148,6 +148,141 @@ __global__ void __launch_bounds__(256) dup_bounds_kernel(const uint32_t* __restr
     for (uint32_t b = (o + kDupPerCta - 1) / kDupPerCta; b * kDupPerCta < o + n; ++b) cta_first[b] = (uint32_t)j;
 }
 
+// One instance i of the CTA's range: tile key and value (sorted splat index |
+// quadrant mask << 28).  s_off: the offsets of splats [j_lo, j_lo + cnt).
+__device__ __forceinline__ void dup_instance(int i, const uint32_t* s_off, int cnt, int j_lo,
+                                             const SplatFast* __restrict__ fast, int cull,
+                                             const CullRec* __restrict__ cull_rec, int tiles_x, uint32_t& key,
+                                             uint32_t& val) {
+    const int jl = last_le(s_off, 0, cnt - 1, (uint32_t)i);
+    const int j = j_lo + jl;
+    const int32_t xr = __ldg(&fast[j].xr), yr = __ldg(&fast[j].yr);
+    const int x0 = box_x0(xr), x1 = x0 + box_w(xr), y0 = box_x0(yr), y1 = y0 + box_w(yr);
+    const int tx0 = x0 / kTile, tx1 = x1 / kTile, ty0 = y0 / kTile;
+    const int local = i - (int)s_off[jl];
+    const int w = tx1 - tx0 + 1;
+    const int ty = ty0 + local / w, tx = tx0 + local % w;
+    // one bit per 8x8 quadrant of the tile (bit q = qy*2 + qx): can the splat
+    // reach the cutoff at a pixel of quadrant q inside its box?  Each quadrant
+    // is one warp of the rasterizers, so the test is warp-uniform there.
+    uint32_t mask = 0xfu;
+    if (cull) {
+        const CullRec e = cull_rec[j];
+        mask = 0u;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int qx0 = tx * kTile + (q & 1) * 8, qy0 = ty * kTile + (q >> 1) * 8;
+            const int xa = max(x0, qx0), xb = min(x1, qx0 + 7), ya = max(y0, qy0), yb = min(y1, qy0 + 7);
+            if (xa <= xb && ya <= yb && tile_may_contribute(e, xa, xb, ya, yb)) mask |= 1u << q;
+        }
+    }
+    key = (uint32_t)(ty * tiles_x + tx);
+    val = (uint32_t)j | (mask << kInstMaskShift);
+}
+
+__device__ __forceinline__ uint32_t dup_warp_incl_scan(uint32_t v) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += t;
+    }
+    return v;
+}
+
+// Duplication fused with the exact culling compaction: each CTA claims the
+// next 1024-instance tile in order (atomic counter), evaluates its instances
+// (4 consecutive per thread), block-scans the keep flags, obtains the number
+// of kept instances before it by decoupled look-back over the earlier tiles,
+// and writes only the kept (tile key, value) pairs -- in the reference's
+// order, without materialising the full instance list.  status: one 64-bit
+// (flag << 32 | count) word per tile, zeroed before the launch.
+__global__ void __launch_bounds__(kDupThreads) duplicate_compact_kernel(
+    const SplatFast* __restrict__ fast, int V, const uint32_t* __restrict__ offsets, int tiles_x,
+    const CullRec* __restrict__ cull_rec, const uint32_t* __restrict__ cta_first, int I,
+    uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out, uint32_t* __restrict__ kept_total,
+    unsigned long long* status, uint32_t* __restrict__ counter) {
+    __shared__ uint32_t s_off[kDupPerCta + 1];
+    __shared__ uint32_t s_tile, s_excl, s_wt[kDupThreads / 32];
+    if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1u);
+    __syncthreads();
+    const int tile = (int)s_tile;
+    const int i0 = tile * kDupPerCta;
+    const int i_end = min(i0 + kDupPerCta, I);
+    const int j_lo = (int)cta_first[tile];
+    const int j_hi = i_end < I ? (int)cta_first[tile + 1] : V - 1;
+    const int cnt = j_hi - j_lo + 1;
+    for (int k = threadIdx.x; k < cnt; k += kDupThreads) s_off[k] = __ldg(&offsets[j_lo + k]);
+    __syncthreads();
+    constexpr int kPer = kDupPerCta / kDupThreads;  // 4 consecutive instances per thread
+    uint32_t key[kPer], val[kPer];
+    uint32_t nk = 0;
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+        const int i = i0 + threadIdx.x * kPer + k;
+        key[k] = 0u;
+        val[k] = 0u;
+        if (i < i_end) dup_instance(i, s_off, cnt, j_lo, fast, 1, cull_rec, tiles_x, key[k], val[k]);
+        nk += (val[k] >> kInstMaskShift) ? 1u : 0u;
+    }
+    // block exclusive scan of the kept counts
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t incl = dup_warp_incl_scan(nk);
+    if (lane == 31) s_wt[warp] = incl;
+    __syncthreads();
+    uint32_t wbase = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < kDupThreads / 32; ++w) {
+        const uint32_t x = s_wt[w];
+        wbase += w < warp ? x : 0u;
+        tot += x;
+    }
+    const uint32_t ex = wbase + incl - nk;
+    if (threadIdx.x < 32) {
+        // warp 0: publish the aggregate, look back 32 predecessors at a time
+        volatile unsigned long long* st = status;
+        uint32_t excl = 0;
+        if (tile > 0) {
+            if (lane == 0) st[tile] = (1ull << 32) | tot;
+            int hi = tile - 1;
+            while (true) {
+                const int p = hi - lane;
+                unsigned long long w = p >= 0 ? st[p] : (2ull << 32);
+                uint32_t flag = (uint32_t)(w >> 32);
+                while (__any_sync(0xffffffffu, flag == 0u)) {
+                    if (flag == 0u) {
+                        w = st[p];
+                        flag = (uint32_t)(w >> 32);
+                    }
+                }
+                const unsigned pm = __ballot_sync(0xffffffffu, flag == 2u);
+                const int stop = pm ? __ffs(pm) - 1 : 32;
+                uint32_t v = (lane <= stop && p >= 0) ? (uint32_t)w : 0u;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                excl += v;
+                if (pm) break;
+                hi -= 32;
+            }
+        }
+        if (lane == 0) {
+            __threadfence();
+            st[tile] = (2ull << 32) | (excl + tot);
+            s_excl = excl;
+            if (i_end >= I) *kept_total = excl + tot;
+        }
+    }
+    __syncthreads();
+    uint32_t pos = s_excl + ex;
+#pragma unroll
+    for (int k = 0; k < kPer; ++k)
+        if (val[k] >> kInstMaskShift) {
+            keys_out[pos] = key[k];
+            vals_out[pos] = val[k];
+            ++pos;
+        }
+}
+
 __global__ void __launch_bounds__(kDupThreads) duplicate_kernel(const SplatFast* __restrict__ fast,
                                                                 const SplatRec* __restrict__ exact, int V,
                                                                 const uint32_t* __restrict__ offsets, int tiles_x,
@@ -166,32 +301,11 @@ __global__ void __launch_bounds__(kDupThreads) duplicate_kernel(const SplatFast*
     for (int k = threadIdx.x; k < cnt; k += kDupThreads) s_off[k] = __ldg(&offsets[j_lo + k]);
     __syncthreads();
     for (int i = i0 + threadIdx.x; i <= i_last; i += kDupThreads) {
-        const int jl = last_le(s_off, 0, cnt - 1, (uint32_t)i);
-        const int j = j_lo + jl;
-        const int32_t xr = __ldg(&fast[j].xr), yr = __ldg(&fast[j].yr);
-        const int x0 = box_x0(xr), x1 = x0 + box_w(xr), y0 = box_x0(yr), y1 = y0 + box_w(yr);
-        const int tx0 = x0 / kTile, tx1 = x1 / kTile, ty0 = y0 / kTile;
-        const int local = i - (int)s_off[jl];
-        const int w = tx1 - tx0 + 1;
-        const int ty = ty0 + local / w, tx = tx0 + local % w;
-        // one bit per 8x8 quadrant of the tile (bit q = qy*2 + qx): can the splat
-        // reach the cutoff at a pixel of quadrant q inside its box?  Each quadrant
-        // is one warp of the rasterizers, so the test is warp-uniform there.
-        uint32_t mask = 0xfu;
-        if (cull) {
-            // culling threshold on the power: alpha * exp(-p) >= 1/255  <=>  p <= ln(255 alpha)
-            const CullRec e = cull_rec[j];
-            mask = 0u;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int qx0 = tx * kTile + (q & 1) * 8, qy0 = ty * kTile + (q >> 1) * 8;
-                const int xa = max(x0, qx0), xb = min(x1, qx0 + 7), ya = max(y0, qy0), yb = min(y1, qy0 + 7);
-                if (xa <= xb && ya <= yb && tile_may_contribute(e, xa, xb, ya, yb)) mask |= 1u << q;
-            }
-        }
-        keys[i] = (uint32_t)(ty * tiles_x + tx);
-        vals[i] = (uint32_t)j | (mask << kInstMaskShift);
-        if (keep) keep[i] = mask ? 1u : 0u;
+        uint32_t key, val;
+        dup_instance(i, s_off, cnt, j_lo, fast, cull, cull_rec, tiles_x, key, val);
+        keys[i] = key;
+        vals[i] = val;
+        if (keep) keep[i] = (val >> kInstMaskShift) ? 1u : 0u;
     }
 }
 

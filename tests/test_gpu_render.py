@@ -190,3 +190,26 @@ def test_c2_config_parity(ctx):
     check_render(ctx, scene, cam, 1.0 / 3.0, threads=O.hardware_threads())
     info = ctx.render_info()
     assert info["instances"] > 1_000_000 and info["kept_instances"] < info["instances"]
+
+
+@pytest.mark.parametrize("cfg", ["dense", "c2"])
+def test_fused_duplication_path_matches_debug_path(ctx, cfg):
+    """The production path (duplication + exact culling + compaction fused,
+    look-back ordered) renders bit-identically to the path that keeps the
+    reference's full instance list (used by the other parity tests)."""
+    from paper_2505_13215_b200.api import Context
+
+    if cfg == "dense":
+        scene, cam = synthetic_scene(3000, 1000, 3, seed=11, density_n=100), ring_camera(11, 160, 120)
+    else:
+        scene, cam = synthetic_scene(240_000, 60_000, 3, seed=2), ring_camera(2, 1352, 1014, index=3, n_ring=16)
+    prod = Context(0)
+    try:
+        ctx.upload(scene)
+        prod.upload(scene)
+        a = ctx.render(cam, 0.4, (0.2, 0.2, 0.2), transmittance_map=True)
+        b = prod.render(cam, 0.4, (0.2, 0.2, 0.2), transmittance_map=True)
+        assert (a["rgb"] == b["rgb"]).all() and (a["transmittance"] == b["transmittance"]).all()
+        assert ctx.render_info() == prod.render_info()
+    finally:
+        prod.close()
