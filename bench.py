@@ -322,8 +322,9 @@ def run_ours(args) -> None:
         ctx._check(lib.hgs_train_step_host(ctx.handle, n, karr, tarr, garr, _capi.HGS_F32, world,
                                            C.byref(tr._opts(tr.decay())), 0 if world > 1 else 1, C.byref(loss)))
         if world > 1:
-            g = tr.grads_tensor()
+            g = tr.packed_grads_tensor()
             dist.all_reduce(g)
+            ctx.grads_unpack()
             ctx.adam_step(tr.lrs, tr.decay())
 
     if world == 1:

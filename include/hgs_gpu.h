@@ -145,6 +145,11 @@ hgs_status hgs_grads_download(hgs_ctx *ctx, hgs_host_scene *out, int dtype, void
                               void *screen_norm3);
 /* Packed device gradient buffer (for the view-parallel allreduce). */
 hgs_status hgs_grads_device(hgs_ctx *ctx, float **ptr, int64_t *count);
+/* Packed gradient payload for a multi-GPU all-reduce: unpack = 0 fills a
+ * context-owned device buffer with the valid part of every gradient row and
+ * the densify-statistic deltas (ptr/count out); unpack = 1 scatters that
+ * buffer (reduced in place by the caller, e.g. ncclAllReduce) back. */
+hgs_status hgs_grads_packed(hgs_ctx *ctx, int unpack, float **ptr, int64_t *count);
 
 /* ---- loss (loss.hpp:12-13) --------------------------------------------- */
 /* (1-l)*L1 + l*(1-SSIM) of the last rendered image against gt (h*w*3, host

@@ -114,6 +114,7 @@ _SIGS = {
     "hgs_zero_grads": ([_vp], C.c_int),
     "hgs_grads_download": ([_vp, C.POINTER(HostScene), C.c_int, _vp, _vp], C.c_int),
     "hgs_grads_device": ([_vp, C.POINTER(_fp), _i64p], C.c_int),
+    "hgs_grads_packed": ([_vp, C.c_int, C.POINTER(_fp), _i64p], C.c_int),
     "hgs_loss_with_grad": ([_vp, _vp, C.c_int, C.c_int, C.c_double, _dp, _vp], C.c_int),
     "hgs_photometric_loss_with_grad": ([_vp, _vp, _vp, C.c_int, C.c_int, C.c_int, C.c_double, _dp, _vp], C.c_int),
     "hgs_adam_step": ([_vp, C.POINTER(Lrs), C.c_double, _i64p], C.c_int),

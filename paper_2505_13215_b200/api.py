@@ -232,6 +232,17 @@ class Context:
         out["screen_norm4"], out["screen_norm3"] = sn4, sn3
         return out
 
+    def grads_packed(self) -> tuple[int, int]:
+        """(device pointer, float count) of the packed gradient payload
+        (hgs_grads_packed): valid gradient rows + stat deltas, contiguous."""
+        p, n = _capi._fp(), C.c_int64()
+        self._check(self._lib.hgs_grads_packed(self._h, 0, C.byref(p), C.byref(n)))
+        return C.cast(p, C.c_void_p).value or 0, n.value
+
+    def grads_unpack(self) -> None:
+        """Scatter the (reduced) packed payload back into the gradient rows."""
+        self._check(self._lib.hgs_grads_packed(self._h, 1, None, None))
+
     def grads_device(self) -> tuple[int, int]:
         p = _capi._fp()
         n = C.c_int64()

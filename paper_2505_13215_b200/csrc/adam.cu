@@ -258,4 +258,41 @@ __global__ void __launch_bounds__(256) adam_rows_kernel(AdamPools P, AdamArgs A,
     st4(g, make_float4(0.f, 0.f, 0.f, 0.f));
 }
 
+// Packed gradient payload for the multi-GPU all-reduce: the valid part of
+// every gradient row ([0, n) of each [row][cap] row) and the two stat-delta
+// rows of each pool, contiguous.  Segment s covers pool rows then deltas:
+// [g4 rows | g3 rows | dgn4 | dgn3 | dcnt4 | dcnt3].
+__global__ void __launch_bounds__(256) grads_pack_kernel(const float* __restrict__ gbuf, int64_t off_g3,
+                                                         int64_t off_dgn4, int rows4, int rows3, int64_t cap4,
+                                                         int64_t cap3, int n4, int n3, float* __restrict__ packed,
+                                                         int unpack) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t a4 = (int64_t)rows4 * n4, a3 = (int64_t)rows3 * n3;
+    const int64_t total = a4 + a3 + 2 * (int64_t)n4 + 2 * (int64_t)n3;
+    if (e >= total) return;
+    int64_t src;
+    if (e < a4) {
+        src = (e / n4) * cap4 + e % n4;
+    } else if (e < a4 + a3) {
+        const int64_t k = e - a4;
+        src = off_g3 + (k / n3) * cap3 + k % n3;
+    } else {
+        // delta rows: dgn4 (cap4) | dgn3 (cap3) | dcnt4 (cap4) | dcnt3 (cap3)
+        int64_t k = e - a4 - a3;
+        int64_t base = off_dgn4;
+        if (k < n4) {
+            src = base + k;
+        } else if ((k -= n4) < n3) {
+            src = base + cap4 + k;
+        } else if ((k -= n3) < n4) {
+            src = base + cap4 + cap3 + k;
+        } else {
+            k -= n4;
+            src = base + 2 * cap4 + cap3 + k;
+        }
+    }
+    if (unpack) const_cast<float*>(gbuf)[src] = packed[e];
+    else packed[e] = gbuf[src];
+}
+
 }  // namespace hgs

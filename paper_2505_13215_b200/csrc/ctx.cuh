@@ -118,6 +118,7 @@ struct hgs_ctx {
     hgs::DBuf rec, depth_key, ntiles, visflag, vispos;
     hgs::DBuf sort_k, sort_v, sort_k2, sort_v2;       // depth sort (V)
     hgs::DBuf rec_sorted, fast_sorted, ntiles_sorted, inst_off, sorted_of_gid, pcut, dup_first;
+    hgs::DBuf gpack;        // packed gradient payload (multi-GPU all-reduce)
     hgs::DBuf dup_status;   // look-back status words of duplicate_compact_kernel
     hgs::DBuf shdir, ddir;  // K1 view direction + clamp mask; K7b dL/d(direction)
     hgs::DBuf inst_k, inst_v, inst_k2, inst_v2;       // tile sort (I)

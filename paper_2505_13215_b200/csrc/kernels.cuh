@@ -52,6 +52,9 @@ __global__ void raster_fixup_kernel(const uint32_t* __restrict__ fix_list, const
                                     float* __restrict__ out_tfinal, float* __restrict__ out_trans,
                                     uint32_t* __restrict__ out_count);
 
+__global__ void grads_pack_kernel(const float* __restrict__ gbuf, int64_t off_g3, int64_t off_dgn4, int rows4,
+                                  int rows3, int64_t cap4, int64_t cap3, int n4, int n3, float* __restrict__ packed,
+                                  int unpack);
 // K7b: SH colour backward (runs before K7)
 __global__ void sh_bwd_kernel(int N, const uint32_t* __restrict__ sorted_of_gid, const float* __restrict__ accum,
                               int acc_stride, int n4, const float* __restrict__ p4, int64_t cap4,
@@ -124,6 +127,9 @@ __global__ void compact_survivors_kernel(const float* __restrict__ src, float* _
                                          int64_t cap4, int n4, const uint32_t* __restrict__ mask,
                                          const uint32_t* __restrict__ pos);
 
+__global__ void grads_pack_kernel(const float* __restrict__ gbuf, int64_t off_g3, int64_t off_dgn4, int rows4,
+                                  int rows3, int64_t cap4, int64_t cap3, int n4, int n3, float* __restrict__ packed,
+                                  int unpack);
 // K7b: SH colour backward (runs before K7)
 __global__ void sh_bwd_kernel(int N, const uint32_t* __restrict__ sorted_of_gid, const float* __restrict__ accum,
                               int acc_stride, int n4, const float* __restrict__ p4, int64_t cap4,

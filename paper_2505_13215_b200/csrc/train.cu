@@ -333,6 +333,32 @@ hgs_status hgs_grads_download(hgs_ctx* ctx, hgs_host_scene* out, int dtype, void
     return HGS_OK;
 }
 
+// Packed payload ([0, n) of every gradient row + stat deltas) for the
+// multi-GPU all-reduce: pack = 0 -> device buffer filled from the gradient
+// buffer (ptr/count returned), pack = 1 -> the buffer scattered back.
+hgs_status hgs_grads_packed(hgs_ctx* ctx, int unpack, float** ptr, int64_t* count) {
+    if (!ctx || (!unpack && (!ptr || !count))) return HGS_ERR_INVALID_ARGUMENT;
+    if (!ctx->gbuf.p) return fail(ctx, HGS_ERR_STATE, "grads_packed: no scene uploaded");
+    CK(cudaSetDevice(ctx->device));
+    const int r4 = rows4(ctx->deg), r3 = rows3(ctx->deg);
+    const int64_t n = (int64_t)r4 * ctx->n4 + (int64_t)r3 * ctx->n3 + 2 * (ctx->n4 + ctx->n3);
+    CK(ctx->gpack.ensure((size_t)std::max<int64_t>(n, 1) * 4));
+    if (n > 0) {
+        grads_pack_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(
+            ctx->gbuf.as<float>(), ctx->g3 - ctx->g4, ctx->dgn4 - ctx->g4, r4, r3, ctx->cap4, ctx->cap3,
+            (int)ctx->n4, (int)ctx->n3, ctx->gpack.as<float>(), unpack);
+        count_launch();
+        CKL();
+    }
+    if (unpack) {
+        ctx->grads_zero = false;
+    } else {
+        *ptr = ctx->gpack.as<float>();
+        *count = n;
+    }
+    return HGS_OK;
+}
+
 hgs_status hgs_grads_device(hgs_ctx* ctx, float** ptr, int64_t* count) {
     if (!ctx || !ptr || !count) return HGS_ERR_INVALID_ARGUMENT;
     *ptr = ctx->gbuf.as<float>();

@@ -162,12 +162,18 @@ class ViewParallelTrainer(DeviceTrainer):
         ptr, n = self.ctx.grads_device()
         return self.torch.as_tensor(_CudaArray(ptr, n), device=f"cuda:{self.ctx.device}")
 
+    def packed_grads_tensor(self):
+        """The packed payload (valid gradient rows + stat deltas, no capacity padding)."""
+        ptr, n = self.ctx.grads_packed()
+        return self.torch.as_tensor(_CudaArray(ptr, n), device=f"cuda:{self.ctx.device}")
+
     def step(self, batch: list[int], batch_total: int | None = None, apply_adam: bool = True) -> float:
         mine = shard_batch(batch, self.rank, self.world)
         self.iter += 1
         loss = DeviceTrainer.step(self, mine, batch_total=len(batch), apply_adam=False) * max(1, len(mine))
-        g = self.grads_tensor()
+        g = self.packed_grads_tensor()
         self.dist.all_reduce(g, group=self.group)          # sum of dense grads + stat deltas
+        self.ctx.grads_unpack()
         lt = self.torch.tensor([loss], dtype=self.torch.float64, device=g.device)
         self.dist.all_reduce(lt, group=self.group)
         self.ctx.adam_step(self.lrs, self.decay())

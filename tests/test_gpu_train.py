@@ -345,3 +345,33 @@ def test_gradients_c2_full_size(ctx):
     assert n_bad <= 1e-4 * n_el, (n_bad, n_el)
     for k, v in rep.items():
         assert abs(v["norm_ratio"] - 1.0) < 1e-3, (k, v)
+
+
+def test_packed_gradient_payload_round_trip(ctx):
+    """hgs_grads_packed: the all-reduce payload holds exactly the valid gradient
+    rows and stat deltas; scaling it and scattering it back scales the
+    gradients (what an in-place NCCL sum over identical ranks does)."""
+    import torch
+
+    scene = synthetic_scene(700, 300, 1, seed=37, density_n=1000)
+    cam = ring_camera(37, 64, 48)
+    ctx.upload(scene)
+    ctx.zero_grads()
+    ctx.forward_train(cam, 0.5, (0.2, 0.2, 0.2))
+    ctx.backward(np.random.default_rng(3).uniform(-1, 1, (48, 64, 3)))
+    before = ctx.grads()
+    stats0 = ctx.densify_stats()
+    ptr, n = ctx.grads_packed()
+    K3 = 3 * 4
+    assert n == (17 + K3) * scene.n4 + (11 + K3) * scene.n3 + 2 * (scene.n4 + scene.n3)
+    ctx.synchronize()
+    from paper_2505_13215_b200.train import _CudaArray
+
+    t = torch.as_tensor(_CudaArray(ptr, n), device="cuda:0")
+    t.mul_(2.0)
+    torch.cuda.synchronize()
+    ctx.grads_unpack()
+    after = ctx.grads()
+    for k in CLASSES4 + CLASSES3:
+        assert np.array_equal(np.asarray(after[k]), 2 * np.asarray(before[k])), k
+    ctx.zero_grads()
