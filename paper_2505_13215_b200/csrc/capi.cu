@@ -483,8 +483,8 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
     }
     ctx->inst_vals_final = inst_vals;
     prof_begin(ctx, PH_RASTER_FWD);
-    (want_count ? raster_fwd_kernel<true> : raster_fwd_kernel<false>)<<<n_tiles, 128, 0, st>>>(
-        ctx->ranges.as<uint2>(), inst_vals, ctx->fast_sorted.as<SplatFast>(), ctx->rec_sorted.as<SplatRec>(), W, H,
+    launch_raster_fwd(
+        want_count, n_tiles, st, ctx->ranges.as<uint2>(), inst_vals, ctx->fast_sorted.as<SplatFast>(), ctx->rec_sorted.as<SplatRec>(), W, H,
         tiles_x, (float)bg[0], (float)bg[1], (float)bg[2], ctx->img.as<float>(), ctx->last.as<uint32_t>(),
         ctx->tfinal.as<float>(), want_trans ? ctx->trans.as<float>() : nullptr, want_count ? ctx->count.as<uint32_t>() : nullptr,
         ctx->fix_list.as<uint32_t>(), &dc->fix_count);

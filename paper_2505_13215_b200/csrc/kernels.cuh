@@ -37,14 +37,10 @@ __global__ void compact_instances_kernel(const uint32_t* __restrict__ keys, cons
 __global__ void tile_ranges_kernel(const uint32_t* __restrict__ keys, int n, uint2* __restrict__ ranges);
 __global__ void tile_ranges_dev_kernel(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ n_dev,
                                        uint2* __restrict__ ranges);
-template <bool kCount>
-__global__ void raster_fwd_kernel(const uint2* __restrict__ ranges, const uint32_t* __restrict__ inst_val,
-                                  const SplatFast* __restrict__ fast, const SplatRec* __restrict__ exact, int W, int H,
-                                  int tiles_x, float bg_r, float bg_g, float bg_b, float* __restrict__ out_rgb,
-                                  uint32_t* __restrict__ out_last, float* __restrict__ out_tfinal,
-                                  float* __restrict__ out_trans, uint32_t* __restrict__ out_count,
-                                  uint32_t* __restrict__ fix_list,
-                                  uint32_t* __restrict__ fix_count);
+void launch_raster_fwd(bool count_map, int n_tiles, cudaStream_t st, const uint2* ranges, const uint32_t* inst_val,
+                       const SplatFast* fast, const SplatRec* exact, int W, int H, int tiles_x, float bg_r, float bg_g,
+                       float bg_b, float* out_rgb, uint32_t* out_last, float* out_tfinal, float* out_trans,
+                       uint32_t* out_count, uint32_t* fix_list, uint32_t* fix_count);
 __global__ void raster_fixup_kernel(const uint32_t* __restrict__ fix_list, const uint32_t* __restrict__ fix_count,
                                     const uint2* __restrict__ ranges, const uint32_t* __restrict__ inst_val,
                                     const SplatRec* __restrict__ exact, int W, int tiles_x, double bg_r, double bg_g,

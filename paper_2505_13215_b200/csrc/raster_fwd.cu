@@ -490,12 +490,20 @@ __global__ void __launch_bounds__(kThreads, 6) raster_fwd_kernel(
                     fix_count);
 }
 
-template __global__ void raster_fwd_kernel<false>(const uint2*, const uint32_t*, const SplatFast*, const SplatRec*,
-                                                   int, int, int, float, float, float, float*, uint32_t*, float*,
-                                                   float*, uint32_t*, uint32_t*, uint32_t*);
-template __global__ void raster_fwd_kernel<true>(const uint2*, const uint32_t*, const SplatFast*, const SplatRec*,
-                                                  int, int, int, float, float, float, float*, uint32_t*, float*,
-                                                  float*, uint32_t*, uint32_t*, uint32_t*);
+// Host launcher (keeps the template instantiations in this translation unit).
+void launch_raster_fwd(bool count_map, int n_tiles, cudaStream_t st, const uint2* ranges, const uint32_t* inst_val,
+                       const SplatFast* fast, const SplatRec* exact, int W, int H, int tiles_x, float bg_r, float bg_g,
+                       float bg_b, float* out_rgb, uint32_t* out_last, float* out_tfinal, float* out_trans,
+                       uint32_t* out_count, uint32_t* fix_list, uint32_t* fix_count) {
+    if (count_map)
+        raster_fwd_kernel<true><<<n_tiles, kThreads, 0, st>>>(ranges, inst_val, fast, exact, W, H, tiles_x, bg_r, bg_g,
+                                                              bg_b, out_rgb, out_last, out_tfinal, out_trans,
+                                                              out_count, fix_list, fix_count);
+    else
+        raster_fwd_kernel<false><<<n_tiles, kThreads, 0, st>>>(ranges, inst_val, fast, exact, W, H, tiles_x, bg_r,
+                                                               bg_g, bg_b, out_rgb, out_last, out_tfinal, out_trans,
+                                                               out_count, fix_list, fix_count);
+}
 
 // Exact FP64 recomposite of the flagged pixels (raster.cpp:123-148), one warp
 // per pixel over 32-splat chunks (exact_chunk: lane-parallel FP64 alphas, the
