@@ -186,7 +186,10 @@ typedef struct {
 } hgs_train_opts;
 /* B views: render, loss against gt (device float images), backward scaled
  * by 1/batch_total, and (when apply_adam) one Adam step.  loss_out receives
- * the summed per-view loss. */
+ * the summed per-view loss.  A non-finite loss fails with
+ * HGS_ERR_NUMERIC_ABORT when apply_adam (no update is applied); without the
+ * update it is returned as is, for the caller to combine (e.g. the batch
+ * loss summed over ranks) and decide. */
 hgs_status hgs_train_step(hgs_ctx *ctx, int n_views, const hgs_camera *cams, const double *times,
                           const float *const *gt_device, int batch_total, const hgs_train_opts *opts,
                           int apply_adam, double *loss_out);

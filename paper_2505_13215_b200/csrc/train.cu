@@ -663,7 +663,7 @@ hgs_status train_step_impl(hgs_ctx* ctx, int n_views, const hgs_camera* cams, co
             if (r != HGS_OK) return r;
         }
     }
-    if (!std::isfinite(loss)) {  // an earlier group of views already failed
+    if (!std::isfinite(loss) && apply_adam) {  // an earlier group of views already failed
         if (loss_out) *loss_out = loss;
         return fail(ctx, HGS_ERR_NUMERIC_ABORT, "train: non-finite loss");  // train.cpp:445-447
     }
@@ -701,8 +701,10 @@ hgs_status train_step_impl(hgs_ctx* ctx, int n_views, const hgs_camera* cams, co
     r = hgs_render_finish(ctx);
     if (r != HGS_OK) return r;
     if (loss_out) *loss_out = loss;
-    if (!std::isfinite(loss)) {
-        if (apply_adam) {
+    // without the update the caller owns the decision (e.g. after summing the
+    // batch loss over ranks), so a non-finite loss is returned, not raised
+    if (!std::isfinite(loss) && apply_adam) {
+        {
             --ctx->step;  // the kernels skipped the update (and left the gradients)
             CK(cudaMemsetAsync(ctx->gbuf.p, 0, (size_t)ctx->gbuf_floats * 4, ctx->stream));
             ctx->grads_zero = true;
@@ -741,7 +743,7 @@ hgs_status hgs_train_collect(hgs_ctx* ctx, double* loss_out) {
     for (int v = 0; v < p.n_views; ++v)
         loss += loss_from_sums(hp[2 * v], hp[2 * v + 1], p.dims[v][0], p.dims[v][1], p.lambda);
     if (loss_out) *loss_out = loss;
-    if (!std::isfinite(loss)) {
+    if (!std::isfinite(loss) && p.adam) {
         // the device skipped this update and every later pending one
         if (p.adam) ctx->step = p.step_before;
         ctx->pipeline.clear();

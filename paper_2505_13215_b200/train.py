@@ -171,13 +171,19 @@ class ViewParallelTrainer(DeviceTrainer):
         mine = shard_batch(batch, self.rank, self.world)
         self.iter += 1
         loss = DeviceTrainer.step(self, mine, batch_total=len(batch), apply_adam=False) * max(1, len(mine))
+        # the batch loss first: every rank takes the same NumericAbort decision
+        # (train.cpp:445-447) before any collective on the gradients
+        lt = self.torch.tensor([loss], dtype=self.torch.float64, device=f"cuda:{self.ctx.device}")
+        self.dist.all_reduce(lt, group=self.group)
+        total = float(lt.item())
+        if not math.isfinite(total):
+            self.ctx.zero_grads()
+            raise _capi.NumericAbort("train: non-finite loss")
         g = self.packed_grads_tensor()
         self.dist.all_reduce(g, group=self.group)          # sum of dense grads + stat deltas
         self.ctx.grads_unpack()
-        lt = self.torch.tensor([loss], dtype=self.torch.float64, device=g.device)
-        self.dist.all_reduce(lt, group=self.group)
         self.ctx.adam_step(self.lrs, self.decay())
-        return float(lt.item()) / len(batch)
+        return total / len(batch)
 
 
 def shard_batch(batch: list[int], rank: int, world: int) -> list[int]:

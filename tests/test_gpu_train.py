@@ -375,3 +375,19 @@ def test_packed_gradient_payload_round_trip(ctx):
     for k in CLASSES4 + CLASSES3:
         assert np.array_equal(np.asarray(after[k]), 2 * np.asarray(before[k])), k
     ctx.zero_grads()
+
+
+def test_nonfinite_loss_without_update_is_returned(ctx):
+    """apply_adam = 0 (view-parallel ranks): the loss comes back non-finite
+    instead of raising, so all ranks can take the decision together."""
+    from paper_2505_13215_b200.train import DeviceTrainer
+
+    scene = synthetic_scene(500, 200, 1, seed=38, density_n=800)
+    cams = [ring_camera(38, 48, 40, index=i, n_ring=2) for i in range(2)]
+    tr = DeviceTrainer(ctx, scene, cams, [0.5] * 2, target=synthetic_scene(500, 200, 1, seed=39, density_n=800))
+    tr.gt[1][2, 2, 2] = float("nan")
+    loss = tr.step([0, 1], apply_adam=False)
+    assert not np.isfinite(loss)
+    ctx.zero_grads()
+    tr.gt[1][2, 2, 2] = 0.25
+    assert np.isfinite(tr.step([0, 1]))
