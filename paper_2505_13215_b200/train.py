@@ -173,17 +173,29 @@ class ViewParallelTrainer(DeviceTrainer):
         loss = DeviceTrainer.step(self, mine, batch_total=len(batch), apply_adam=False) * max(1, len(mine))
         # the batch loss first: every rank takes the same NumericAbort decision
         # (train.cpp:445-447) before any collective on the gradients
-        lt = self.torch.tensor([loss], dtype=self.torch.float64, device=f"cuda:{self.ctx.device}")
-        self.dist.all_reduce(lt, group=self.group)
-        total = float(lt.item())
-        if not math.isfinite(total):
+        try:
+            total = reduce_batch_loss(self.dist, self.group, loss, f"cuda:{self.ctx.device}")
+        except _capi.NumericAbort:
             self.ctx.zero_grads()
-            raise _capi.NumericAbort("train: non-finite loss")
+            raise
         g = self.packed_grads_tensor()
         self.dist.all_reduce(g, group=self.group)          # sum of dense grads + stat deltas
         self.ctx.grads_unpack()
         self.ctx.adam_step(self.lrs, self.decay())
         return total / len(batch)
+
+
+def reduce_batch_loss(dist, group, local_loss: float, device: str = "cpu") -> float:
+    """Sum of the ranks' view losses; every rank raises NumericAbort together
+    when it is non-finite (train.cpp:445-447), before any gradient collective."""
+    import torch
+
+    lt = torch.tensor([local_loss], dtype=torch.float64, device=device)
+    dist.all_reduce(lt, group=group)
+    total = float(lt.item())
+    if not math.isfinite(total):
+        raise _capi.NumericAbort("train: non-finite loss")
+    return total
 
 
 def shard_batch(batch: list[int], rank: int, world: int) -> list[int]:

@@ -130,3 +130,38 @@ def test_view_parallel_step_matches_single_process():
     np.testing.assert_allclose(res["gn4"], st.grad_norm4, rtol=1e-12)
     np.testing.assert_allclose(res["gn3"], st.grad_norm3, rtol=1e-12)
     assert (res["c4"] == st.count4).all() and (res["c3"] == st.count3).all()
+
+
+def _abort_worker(rank, world, port, q):
+    from paper_2505_13215_b200._capi import NumericAbort
+    from paper_2505_13215_b200.train import reduce_batch_loss
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    out = []
+    out.append(reduce_batch_loss(dist, None, 0.25 + rank))            # finite on both ranks
+    try:
+        reduce_batch_loss(dist, None, float("nan") if rank == 1 else 0.5)
+        out.append("no-abort")
+    except NumericAbort:
+        out.append("abort")
+    out.append(reduce_batch_loss(dist, None, 1.0))                     # collectives still aligned
+    dist.destroy_process_group()
+    q.put((rank, out))
+
+
+def test_numeric_abort_is_a_collective_decision():
+    """One rank's non-finite view loss makes EVERY rank raise NumericAbort at
+    the same step (the batch loss is all-reduced before the gradients)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_abort_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    for r in (0, 1):
+        assert res[r] == [1.5, "abort", 2.0], res
