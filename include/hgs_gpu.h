@@ -176,6 +176,32 @@ hgs_status hgs_stats_download(hgs_ctx *ctx, double *grad_norm4, uint32_t *count4
  * moved_out (optional, capacity n4) receives the converted indices. */
 hgs_status hgs_sweep_convert(hgs_ctx *ctx, int64_t *moved_out, hgs_conversion_report *report);
 
+/* ---- densification (train.cpp:182-299) ------------------ */
+typedef struct {
+    double grad_threshold, opacity_prune_eps, clone_size_frac, split_factor;
+    int64_t max_gaussians; /* per pool */
+} hgs_densify_cfg;
+typedef struct {
+    int64_t cloned3, split3, pruned3, cloned4, split4, pruned4; /* DensifyReport (train.hpp:73-77) */
+    int64_t new_n3, new_n4;
+} hgs_densify_report;
+/* densify_and_prune in two calls, so the caller draws the reference's normal
+ * variates (std::mt19937_64 + std::normal_distribution, in the reference's
+ * order) between them:
+ *   hgs_densify_plan: classifies on the device; kinds3/kinds4 (capacity n3 /
+ *     n4) receive, in pool order, 1 = clone / 2 = split for every densified
+ *     Gaussian; report has the counts and the new pool sizes.
+ *   hgs_densify_apply: normals3 = 6 doubles per densified static (a clone
+ *     uses the first 3 = one sample_normal3; a split two of them), normals4 =
+ *     8 per densified dynamic (the Vec4 n as the reference builds it, twice
+ *     for a split).  Rebuilds both pools (and the Adam moments: fresh rows
+ *     zero), resets the densify statistics and gradients. */
+hgs_status hgs_densify_plan(hgs_ctx *ctx, const hgs_densify_cfg *cfg, uint8_t *kinds3, uint8_t *kinds4,
+                            hgs_densify_report *report);
+hgs_status hgs_densify_apply(hgs_ctx *ctx, const double *normals3, const double *normals4, double split_factor);
+/* train.cpp:459-465: every opacity logit capped at floor_logit (logit(0.01)). */
+hgs_status hgs_opacity_reset(hgs_ctx *ctx, double floor_logit);
+
 /* ---- fused training iteration (train.cpp:402-475, one view batch) ------ */
 typedef struct {
     double ssim_lambda;

@@ -1670,6 +1670,193 @@ uint64_t hgso_rng_index(void* rng, uint64_t lo, uint64_t hi) {
     return pick(*static_cast<std::mt19937_64*>(rng));
 }
 uint64_t hgso_rng_raw(void* rng) { return (*static_cast<std::mt19937_64*>(rng))(); }
+void hgso_rng_normal_seq(void* rng, int64_t n, double* out) {
+    std::normal_distribution<double> nd(0.0, 1.0);
+    for (int64_t i = 0; i < n; ++i) out[i] = nd(*static_cast<std::mt19937_64*>(rng));
+}
+
+// train.cpp:182-299 densify_and_prune, restated on the flat pools.  Per pool,
+// in index order: prune if sigmoid(opacity) < eps; "dense" if the averaged
+// screen gradient exceeds the threshold and two more rows still fit under
+// max_gaussians; dense and small (max scale < clone_size_frac * extent) ->
+// the original + a clone jittered by 0.1 * (R diag(e^s)) n; dense and large
+// -> two parts offset by (R diag(e^s)) n with scales / split_factor.  Normal
+// draws: statics call sample_normal3 (a fresh normal_distribution per call,
+// train.cpp:68-72); dynamics share one distribution for the whole pool and
+// fill Vec4(nd, nd, nd, nd), whose arguments g++ evaluates right to left.
+// Adam rows follow their source (remap_buf, train.cpp:56-66: fresh rows 0).
+int hgso_densify_and_prune(const hgso_scene* in, const hgso_state* st_in, hgso_scene* out, hgso_state* st_out,
+                           const hgso_densify_cfg* cfg, void* rngp, hgso_densify_report* rep) {
+    return guard([&] {
+        auto& rng = *static_cast<std::mt19937_64*>(rngp);
+        *rep = hgso_densify_report{};
+        const int K3 = 3 * sh_count(in->sh_degree);
+        const double size_gate = cfg->clone_size_frac * in->extent;
+        const double log_split = std::log(cfg->split_factor);
+        const size_t maxg = size_t(cfg->max_gaussians);
+        auto sig = [](double x) { return 1.0 / (1.0 + std::exp(-x)); };
+        // ---- statics
+        {
+            size_t o = 0;
+            auto copy_row = [&](int64_t i, size_t d, bool adam) {
+                for (int k = 0; k < 3; ++k) out->mean3[d * 3 + k] = in->mean3[i * 3 + k];
+                for (int k = 0; k < 4; ++k) out->quat3[d * 4 + k] = in->quat3[i * 4 + k];
+                for (int k = 0; k < 3; ++k) out->log_s3[d * 3 + k] = in->log_s3[i * 3 + k];
+                out->op3[d] = in->op3[i];
+                for (int k = 0; k < K3; ++k) out->sh3[d * K3 + k] = in->sh3[i * K3 + k];
+                const hgso_scene* sm[2] = {&st_in->m, &st_in->v};
+                hgso_scene* dm[2] = {&st_out->m, &st_out->v};
+                for (int b = 0; b < 2; ++b) {
+                    for (int k = 0; k < 3; ++k) dm[b]->mean3[d * 3 + k] = adam ? sm[b]->mean3[i * 3 + k] : 0.0;
+                    for (int k = 0; k < 4; ++k) dm[b]->quat3[d * 4 + k] = adam ? sm[b]->quat3[i * 4 + k] : 0.0;
+                    for (int k = 0; k < 3; ++k) dm[b]->log_s3[d * 3 + k] = adam ? sm[b]->log_s3[i * 3 + k] : 0.0;
+                    dm[b]->op3[d] = adam ? sm[b]->op3[i] : 0.0;
+                    for (int k = 0; k < K3; ++k) dm[b]->sh3[d * K3 + k] = adam ? sm[b]->sh3[i * K3 + k] : 0.0;
+                }
+            };
+            auto sample_normal3 = [&](double n[3]) {
+                std::normal_distribution<double> nd(0.0, 1.0);
+                double a = nd(rng), b = nd(rng), c = nd(rng);
+                n[0] = a;
+                n[1] = b;
+                n[2] = c;
+            };
+            for (int64_t i = 0; i < in->n3; ++i) {
+                if (sig(in->op3[i]) < cfg->opacity_prune_eps) {
+                    rep->pruned3++;
+                    continue;
+                }
+                const double avg = st_in->count3[i] > 0 ? st_in->grad_norm3[i] / st_in->count3[i] : 0.0;
+                const bool dense = avg > cfg->grad_threshold && o + 2 <= maxg;
+                const double* ls = &in->log_s3[i * 3];
+                const double mx = std::max(std::max(std::exp(ls[0]), std::exp(ls[1])), std::exp(ls[2]));
+                if (dense) {
+                    const M3 r = quat_to_rot3(&in->quat3[i * 4]);
+                    double m[3][3];
+                    for (int a = 0; a < 3; ++a)
+                        for (int b = 0; b < 3; ++b) m[a][b] = r.a[a][b] * std::exp(ls[b]);
+                    auto mv = [&](const double n[3], double y[3]) {
+                        for (int a = 0; a < 3; ++a) y[a] = m[a][0] * n[0] + m[a][1] * n[1] + m[a][2] * n[2];
+                    };
+                    if (mx < size_gate) {
+                        copy_row(i, o, true);
+                        double n[3], y[3];
+                        sample_normal3(n);
+                        mv(n, y);
+                        copy_row(i, o + 1, false);
+                        for (int a = 0; a < 3; ++a) out->mean3[(o + 1) * 3 + a] = in->mean3[i * 3 + a] + 0.1 * y[a];
+                        o += 2;
+                        rep->cloned3++;
+                    } else {
+                        for (int c = 0; c < 2; ++c) {
+                            double n[3], y[3];
+                            sample_normal3(n);
+                            mv(n, y);
+                            copy_row(i, o, false);
+                            for (int a = 0; a < 3; ++a) out->mean3[o * 3 + a] = in->mean3[i * 3 + a] + y[a];
+                            for (int a = 0; a < 3; ++a) out->log_s3[o * 3 + a] = ls[a] - log_split;
+                            ++o;
+                        }
+                        rep->split3++;
+                    }
+                } else {
+                    copy_row(i, o, true);
+                    ++o;
+                }
+            }
+            out->n3 = int64_t(o);
+            for (size_t k = 0; k < o; ++k) {
+                st_out->grad_norm3[k] = 0.0;
+                st_out->count3[k] = 0;
+            }
+        }
+        // ---- dynamics
+        {
+            size_t o = 0;
+            std::normal_distribution<double> nd(0.0, 1.0);
+            auto copy_row = [&](int64_t i, size_t d, bool adam) {
+                for (int k = 0; k < 3; ++k) out->mean_x[d * 3 + k] = in->mean_x[i * 3 + k];
+                out->mean_t[d] = in->mean_t[i];
+                for (int k = 0; k < 4; ++k) out->ql[d * 4 + k] = in->ql[i * 4 + k];
+                for (int k = 0; k < 4; ++k) out->qr[d * 4 + k] = in->qr[i * 4 + k];
+                for (int k = 0; k < 4; ++k) out->log_s4[d * 4 + k] = in->log_s4[i * 4 + k];
+                out->op4[d] = in->op4[i];
+                for (int k = 0; k < K3; ++k) out->sh4[d * K3 + k] = in->sh4[i * K3 + k];
+                const hgso_scene* sm[2] = {&st_in->m, &st_in->v};
+                hgso_scene* dm[2] = {&st_out->m, &st_out->v};
+                for (int b = 0; b < 2; ++b) {
+                    for (int k = 0; k < 3; ++k) dm[b]->mean_x[d * 3 + k] = adam ? sm[b]->mean_x[i * 3 + k] : 0.0;
+                    dm[b]->mean_t[d] = adam ? sm[b]->mean_t[i] : 0.0;
+                    for (int k = 0; k < 4; ++k) dm[b]->ql[d * 4 + k] = adam ? sm[b]->ql[i * 4 + k] : 0.0;
+                    for (int k = 0; k < 4; ++k) dm[b]->qr[d * 4 + k] = adam ? sm[b]->qr[i * 4 + k] : 0.0;
+                    for (int k = 0; k < 4; ++k) dm[b]->log_s4[d * 4 + k] = adam ? sm[b]->log_s4[i * 4 + k] : 0.0;
+                    dm[b]->op4[d] = adam ? sm[b]->op4[i] : 0.0;
+                    for (int k = 0; k < K3; ++k) dm[b]->sh4[d * K3 + k] = adam ? sm[b]->sh4[i * K3 + k] : 0.0;
+                }
+            };
+            auto draw4 = [&](double n[4]) {  // Vec4 n(nd(rng), nd(rng), nd(rng), nd(rng)), g++ right-to-left
+                const double d0 = nd(rng), d1 = nd(rng), d2 = nd(rng), d3 = nd(rng);
+                n[0] = d3;
+                n[1] = d2;
+                n[2] = d1;
+                n[3] = d0;
+            };
+            for (int64_t i = 0; i < in->n4; ++i) {
+                if (sig(in->op4[i]) < cfg->opacity_prune_eps) {
+                    rep->pruned4++;
+                    continue;
+                }
+                const double avg = st_in->count4[i] > 0 ? st_in->grad_norm4[i] / st_in->count4[i] : 0.0;
+                const bool dense = avg > cfg->grad_threshold && o + 2 <= maxg;
+                const double* ls = &in->log_s4[i * 4];
+                const double mx = std::max(std::max(std::exp(ls[0]), std::exp(ls[1])), std::exp(ls[2]));
+                if (dense) {
+                    const M4 r = rot4_from_pair(&in->ql[i * 4], &in->qr[i * 4]);
+                    double m[4][4];
+                    for (int a = 0; a < 4; ++a)
+                        for (int b = 0; b < 4; ++b) m[a][b] = r.a[a][b] * std::exp(ls[b]);
+                    auto mv = [&](const double n[4], double y[4]) {
+                        for (int a = 0; a < 4; ++a)
+                            y[a] = m[a][0] * n[0] + m[a][1] * n[1] + m[a][2] * n[2] + m[a][3] * n[3];
+                    };
+                    if (mx < size_gate) {
+                        copy_row(i, o, true);
+                        double n[4], y[4];
+                        draw4(n);
+                        mv(n, y);
+                        copy_row(i, o + 1, false);
+                        for (int a = 0; a < 3; ++a) out->mean_x[(o + 1) * 3 + a] = in->mean_x[i * 3 + a] + 0.1 * y[a];
+                        o += 2;
+                        rep->cloned4++;
+                    } else {
+                        for (int c = 0; c < 2; ++c) {
+                            double n[4], y[4];
+                            draw4(n);
+                            mv(n, y);
+                            copy_row(i, o, false);
+                            for (int a = 0; a < 3; ++a) out->mean_x[o * 3 + a] = in->mean_x[i * 3 + a] + y[a];
+                            out->mean_t[o] = in->mean_t[i] + y[3];
+                            for (int a = 0; a < 4; ++a) out->log_s4[o * 4 + a] = ls[a] - log_split;
+                            ++o;
+                        }
+                        rep->split4++;
+                    }
+                } else {
+                    copy_row(i, o, true);
+                    ++o;
+                }
+            }
+            out->n4 = int64_t(o);
+            for (size_t k = 0; k < o; ++k) {
+                st_out->grad_norm4[k] = 0.0;
+                st_out->count4[k] = 0;
+            }
+        }
+        out->sh_degree = in->sh_degree;
+        out->tau = in->tau;
+        out->extent = in->extent;
+    });
+}
 
 // tests/oracles.hpp:26-29
 void hgso_random_quat(void* rngp, double q[4]) {

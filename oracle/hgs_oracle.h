@@ -101,6 +101,16 @@ typedef struct {
     double max_leakage, mean_leakage;
 } hgso_conversion;
 
+/* densify_and_prune configuration (train.hpp:23-49 fields it reads) and report */
+typedef struct {
+    double grad_threshold, opacity_prune_eps, clone_size_frac, split_factor;
+    int64_t max_gaussians;
+} hgso_densify_cfg;
+
+typedef struct {
+    int64_t cloned3, split3, pruned3, cloned4, split4, pruned4;
+} hgso_densify_report;
+
 /* status codes: 0 ok; the message is in hgso_last_error() */
 enum {
     HGSO_OK = 0,
@@ -119,6 +129,14 @@ double hgso_rng_uniform(void *rng);  /* uniform_real_distribution(0,1) */
 double hgso_rng_normal(void *rng);   /* a fresh normal_distribution(0,1) draw */
 uint64_t hgso_rng_index(void *rng, uint64_t lo, uint64_t hi); /* uniform_int_distribution<size_t>(lo, hi) */
 uint64_t hgso_rng_raw(void *rng);    /* one raw mt19937_64 output */
+/* n draws from ONE std::normal_distribution(0,1) object (its cached second
+ * polar value carries across the draws) */
+void hgso_rng_normal_seq(void *rng, int64_t n, double *out);
+/* densify_and_prune (train.cpp:182-299): in -> out (out arrays sized by the
+ * caller for the worst case, out->n3/n4 set), Adam m/v remapped (fresh rows
+ * zero), statistics reset; the rng is advanced exactly like the reference. */
+int hgso_densify_and_prune(const hgso_scene *in, const hgso_state *st_in, hgso_scene *out, hgso_state *st_out,
+                           const hgso_densify_cfg *cfg, void *rng, hgso_densify_report *rep);
 /* random_scene: caller passes buffers sized for (n_static, n_dynamic, degree) */
 void hgso_random_scene(void *rng, int n_static, int n_dynamic, int sh_degree, hgso_scene *out);
 void hgso_random_quat(void *rng, double q[4]);

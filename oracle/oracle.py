@@ -73,6 +73,15 @@ class _Lrs(C.Structure):
                                           "opacity", "sh")]
 
 
+class _DensifyCfg(C.Structure):
+    _fields_ = [("grad_threshold", C.c_double), ("opacity_prune_eps", C.c_double),
+                ("clone_size_frac", C.c_double), ("split_factor", C.c_double), ("max_gaussians", C.c_int64)]
+
+
+class _DensifyRep(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in ("cloned3", "split3", "pruned3", "cloned4", "split4", "pruned4")]
+
+
 class _Conv(C.Structure):
     _fields_ = [("count", C.c_int64), ("max_leakage", C.c_double), ("mean_leakage", C.c_double)]
 
@@ -124,6 +133,10 @@ def lib():
         L.hgso_rng_index.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64]
         L.hgso_rng_raw.restype = C.c_uint64
         L.hgso_rng_raw.argtypes = [C.c_void_p]
+        L.hgso_rng_normal_seq.argtypes = [C.c_void_p, C.c_int64, _dp]
+        L.hgso_densify_and_prune.argtypes = [C.POINTER(_Scene), C.POINTER(_State), C.POINTER(_Scene),
+                                             C.POINTER(_State), C.POINTER(_DensifyCfg), C.c_void_p,
+                                             C.POINTER(_DensifyRep)]
         L.hgso_random_scene.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(_Scene)]
         L.hgso_random_quat.argtypes = [C.c_void_p, _dp]
         L.hgso_random_camera.argtypes = [C.c_void_p, C.c_int, C.c_int, C.POINTER(_Camera)]
@@ -259,6 +272,12 @@ class Rng:
 
     def raw(self) -> int:
         return lib().hgso_rng_raw(self._h)
+
+    def normal_seq(self, n: int) -> np.ndarray:
+        """n draws from ONE std::normal_distribution object."""
+        out = np.zeros(max(n, 1))
+        lib().hgso_rng_normal_seq(self._h, n, _p(out))
+        return out[:n]
 
     def random_quat(self) -> np.ndarray:
         q = np.zeros(4)
@@ -655,6 +674,42 @@ def sweep_convert(scene: HybridScene, state: AdamState | None = None):
         state.count4 = np.zeros(new_n4, dtype=np.uint32)
     report = {"count": int(rep.count), "max_leakage": rep.max_leakage, "mean_leakage": rep.mean_leakage}
     return moved[: rep.count].copy(), report
+
+
+def densify_and_prune(scene: HybridScene, state: AdamState, rng: Rng, grad_threshold=0.02, opacity_prune_eps=0.005,
+                      clone_size_frac=0.01, split_factor=1.6, max_gaussians=20000):
+    """densify_and_prune (train.cpp:182-299): returns (new scene, new state,
+    report dict); ``rng`` is advanced exactly like the reference's."""
+    cap4, cap3 = 2 * scene.n4, 2 * scene.n3
+    out = _empty_scene_like(scene, cap4, cap3)
+    ost = AdamState(out)
+    st_in, st_out = state._struct(), ost._struct()
+    so = _scene_struct(out)
+    cfg = _DensifyCfg(grad_threshold, opacity_prune_eps, clone_size_frac, split_factor, max_gaussians)
+    rep = _DensifyRep()
+    _check(lib().hgso_densify_and_prune(C.byref(_scene_struct(scene)), C.byref(st_in), C.byref(so), C.byref(st_out),
+                                        C.byref(cfg), rng._h, C.byref(rep)))
+    n4, n3 = int(so.n4), int(so.n3)
+    for obj in (out, ost.m, ost.v):
+        for f in HybridScene.DYN_FIELDS:
+            setattr(obj, f, np.ascontiguousarray(getattr(obj, f)[:n4]))
+        for f in HybridScene.STA_FIELDS:
+            setattr(obj, f, np.ascontiguousarray(getattr(obj, f)[:n3]))
+    ost.grad_norm4, ost.count4 = np.zeros(n4), np.zeros(n4, dtype=np.uint32)
+    ost.grad_norm3, ost.count3 = np.zeros(n3), np.zeros(n3, dtype=np.uint32)
+    ost.step, ost.skipped_nonfinite = state.step, state.skipped_nonfinite
+    return out, ost, {n: int(getattr(rep, n)) for n, _ in _DensifyRep._fields_}
+
+
+def _empty_scene_like(scene: HybridScene, n4: int, n3: int) -> HybridScene:
+    K = sh_coeff_count(scene.sh_degree)
+    s = HybridScene(sh_degree=scene.sh_degree, tau=scene.tau, extent=scene.extent)
+    s.mean_x, s.mean_t = np.zeros((n4, 3)), np.zeros(n4)
+    s.ql, s.qr, s.log_s4 = np.zeros((n4, 4)), np.zeros((n4, 4)), np.zeros((n4, 4))
+    s.op4, s.sh4 = np.zeros(n4), np.zeros((n4, K, 3))
+    s.mean3, s.quat3, s.log_s3 = np.zeros((n3, 3)), np.zeros((n3, 4)), np.zeros((n3, 3))
+    s.op3, s.sh3 = np.zeros(n3), np.zeros((n3, K, 3))
+    return s
 
 
 def hardware_threads() -> int:

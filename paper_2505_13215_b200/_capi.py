@@ -63,6 +63,16 @@ class TrainOpts(C.Structure):
                 ("lrs", Lrs), ("bg", C.c_double * 3)]
 
 
+class DensifyCfg(C.Structure):
+    _fields_ = [("grad_threshold", C.c_double), ("opacity_prune_eps", C.c_double),
+                ("clone_size_frac", C.c_double), ("split_factor", C.c_double), ("max_gaussians", C.c_int64)]
+
+
+class DensifyReport(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in ("cloned3", "split3", "pruned3", "cloned4", "split4", "pruned4",
+                                         "new_n3", "new_n4")]
+
+
 class HgsError(RuntimeError):
     """Base of the errors raised from hgs_status codes."""
 
@@ -127,6 +137,9 @@ _SIGS = {
                         C.c_int, _dp], C.c_int),
     "hgs_train_step_host": ([_vp, C.c_int, C.POINTER(Camera_), _dp, C.POINTER(_vp), C.c_int, C.c_int,
                              C.POINTER(TrainOpts), C.c_int, _dp], C.c_int),
+    "hgs_densify_plan": ([_vp, C.POINTER(DensifyCfg), _vp, _vp, C.POINTER(DensifyReport)], C.c_int),
+    "hgs_densify_apply": ([_vp, _dp, _dp, C.c_double], C.c_int),
+    "hgs_opacity_reset": ([_vp, C.c_double], C.c_int),
     "hgs_train_step_async": ([_vp, C.c_int, C.POINTER(Camera_), _dp, C.POINTER(_vp), C.c_int, C.c_int, C.c_int,
                               C.POINTER(TrainOpts), C.c_int], C.c_int),
     "hgs_train_collect": ([_vp, _dp], C.c_int),

@@ -303,6 +303,34 @@ class Context:
                                                  c3.ctypes.data_as(_capi._u32p)))
         return gn4, c4, gn3, c3
 
+    def densify_and_prune(self, rng, grad_threshold: float = 0.02, opacity_prune_eps: float = 0.005,
+                          clone_size_frac: float = 0.01, split_factor: float = 1.6,
+                          max_gaussians: int = 20000) -> dict:
+        """densify_and_prune (train.cpp:182-299) on the device; ``rng`` is the
+        loop's rng.MT19937_64, advanced exactly like the reference's."""
+        from .rng import densify_normals
+
+        n4, n3 = self.counts()
+        cfg = _capi.DensifyCfg(grad_threshold, opacity_prune_eps, clone_size_frac, split_factor, max_gaussians)
+        k3, k4 = np.zeros(max(n3, 1), np.uint8), np.zeros(max(n4, 1), np.uint8)
+        rep = _capi.DensifyReport()
+        self._check(self._lib.hgs_densify_plan(self._h, C.byref(cfg), k3.ctypes.data_as(C.c_void_p),
+                                               k4.ctypes.data_as(C.c_void_p), C.byref(rep)))
+        d3 = rep.cloned3 + rep.split3
+        d4 = rep.cloned4 + rep.split4
+        nrm3, nrm4 = densify_normals(rng, k3[:d3].tolist(), k4[:d4].tolist())
+        self._check(self._lib.hgs_densify_apply(self._h, nrm3.ctypes.data_as(_capi._dp),
+                                                nrm4.ctypes.data_as(_capi._dp), float(split_factor)))
+        self.counts()
+        return {n: int(getattr(rep, n)) for n, _ in _capi.DensifyReport._fields_}
+
+    def opacity_reset(self, floor_logit: float | None = None) -> None:
+        """train.cpp:459-465: opacity logits capped at logit(0.01)."""
+        import math
+
+        f = math.log(0.01 / 0.99) if floor_logit is None else floor_logit
+        self._check(self._lib.hgs_opacity_reset(self._h, float(f)))
+
     def sweep_convert(self):
         n4, _ = self.counts()
         moved = np.zeros(max(n4, 1), dtype=np.int64)

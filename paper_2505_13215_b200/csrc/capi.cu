@@ -530,6 +530,35 @@ hgs_status hgs_render_finish(hgs_ctx* ctx) {
     return HGS_OK;
 }
 
+// (Re)lays out the packed gradient buffer and the per-Gaussian statistics
+// for the current capacities, all zero (upload, densification).
+hgs_status hgs_layout_state(hgs_ctx* ctx) {
+    {
+        const int64_t f4 = (int64_t)rows4(ctx->deg) * ctx->cap4, f3 = (int64_t)rows3(ctx->deg) * ctx->cap3;
+        ctx->gbuf_floats = f4 + f3 + 2 * ctx->cap4 + 2 * ctx->cap3;
+        CK(ctx->gbuf.ensure((size_t)ctx->gbuf_floats * 4));
+        CK(cudaMemsetAsync(ctx->gbuf.p, 0, (size_t)ctx->gbuf_floats * 4, ctx->stream));
+        ctx->grads_zero = true;
+        float* g = ctx->gbuf.as<float>();
+        ctx->g4 = g;
+        ctx->g3 = g + f4;
+        ctx->dgn4 = ctx->g3 + f3;
+        ctx->dgn3 = ctx->dgn4 + ctx->cap4;
+        ctx->dcnt4 = ctx->dgn3 + ctx->cap3;
+        ctx->dcnt3 = ctx->dcnt4 + ctx->cap4;
+    }
+    for (DBuf* b : {&ctx->gn4, &ctx->cnt4, &ctx->sn4}) {
+        CK(b->ensure((size_t)ctx->cap4 * 4));
+        CK(cudaMemsetAsync(b->p, 0, (size_t)ctx->cap4 * 4, ctx->stream));
+    }
+    for (DBuf* b : {&ctx->gn3, &ctx->cnt3, &ctx->sn3}) {
+        CK(b->ensure((size_t)ctx->cap3 * 4));
+        CK(cudaMemsetAsync(b->p, 0, (size_t)ctx->cap3 * 4, ctx->stream));
+    }
+    ctx->have_tape = false;
+    return HGS_OK;
+}
+
 extern "C" {
 
 hgs_status hgs_profile(hgs_ctx* ctx, int enable) {
@@ -588,7 +617,7 @@ void hgs_ctx_destroy(hgs_ctx* ctx) {
                     &ctx->sort_v2, &ctx->rec_sorted, &ctx->fast_sorted, &ctx->ntiles_sorted, &ctx->inst_off,
                     &ctx->inst_k, &ctx->inst_v, &ctx->inst_k2, &ctx->inst_v2, &ctx->ranges, &ctx->sorted_of_gid, &ctx->inst_flag, &ctx->inst_pos, &ctx->dbg_k, &ctx->dbg_v, &ctx->scan_ws,
                     &ctx->sort_ws, &ctx->counters, &ctx->img, &ctx->last, &ctx->tfinal, &ctx->trans, &ctx->count,
-                    &ctx->fix_list, &ctx->accum, &ctx->lgrad, &ctx->gt_stage, &ctx->loss_ws, &ctx->stage, &ctx->adam_ok, &ctx->pcut, &ctx->dup_first, &ctx->shdir, &ctx->ddir, &ctx->dup_status, &ctx->gpack};
+                    &ctx->fix_list, &ctx->accum, &ctx->lgrad, &ctx->gt_stage, &ctx->loss_ws, &ctx->stage, &ctx->adam_ok, &ctx->pcut, &ctx->dup_first, &ctx->shdir, &ctx->ddir, &ctx->dup_status, &ctx->gpack, &ctx->dens_cat, &ctx->dens_u32, &ctx->dens_misc, &ctx->dens_kinds, &ctx->dens_jit};
     for (DBuf* b : bufs) b->release();
     ctx->pinned.release();
     ctx->pinned_ctr.release();
@@ -642,26 +671,8 @@ hgs_status hgs_scene_upload(hgs_ctx* ctx, const hgs_host_scene* s, int dtype) {
     for (DBuf* b : {&ctx->m4, &ctx->v4}) CK(cudaMemsetAsync(b->p, 0, b4, ctx->stream));
     for (DBuf* b : {&ctx->m3, &ctx->v3}) CK(cudaMemsetAsync(b->p, 0, b3, ctx->stream));
     {
-        const int64_t f4 = (int64_t)rows4(ctx->deg) * ctx->cap4, f3 = (int64_t)rows3(ctx->deg) * ctx->cap3;
-        ctx->gbuf_floats = f4 + f3 + 2 * ctx->cap4 + 2 * ctx->cap3;
-        CK(ctx->gbuf.ensure((size_t)ctx->gbuf_floats * 4));
-        CK(cudaMemsetAsync(ctx->gbuf.p, 0, (size_t)ctx->gbuf_floats * 4, ctx->stream));
-        ctx->grads_zero = true;
-        float* g = ctx->gbuf.as<float>();
-        ctx->g4 = g;
-        ctx->g3 = g + f4;
-        ctx->dgn4 = ctx->g3 + f3;
-        ctx->dgn3 = ctx->dgn4 + ctx->cap4;
-        ctx->dcnt4 = ctx->dgn3 + ctx->cap3;
-        ctx->dcnt3 = ctx->dcnt4 + ctx->cap4;
-    }
-    for (DBuf* b : {&ctx->gn4, &ctx->cnt4, &ctx->sn4}) {
-        CK(b->ensure((size_t)ctx->cap4 * 4));
-        CK(cudaMemsetAsync(b->p, 0, (size_t)ctx->cap4 * 4, ctx->stream));
-    }
-    for (DBuf* b : {&ctx->gn3, &ctx->cnt3, &ctx->sn3}) {
-        CK(b->ensure((size_t)ctx->cap3 * 4));
-        CK(cudaMemsetAsync(b->p, 0, (size_t)ctx->cap3 * 4, ctx->stream));
+        hgs_status r = hgs_layout_state(ctx);
+        if (r != HGS_OK) return r;
     }
     ctx->step = 0;
     ctx->have_tape = false;

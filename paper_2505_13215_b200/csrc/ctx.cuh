@@ -119,6 +119,10 @@ struct hgs_ctx {
     hgs::DBuf sort_k, sort_v, sort_k2, sort_v2;       // depth sort (V)
     hgs::DBuf rec_sorted, fast_sorted, ntiles_sorted, inst_off, sorted_of_gid, pcut, dup_first;
     hgs::DBuf gpack;        // packed gradient payload (multi-GPU all-reduce)
+    // densify_and_prune (densify.cu): plan buffers + planned sizes
+    hgs::DBuf dens_cat, dens_u32, dens_misc, dens_kinds, dens_jit;
+    bool dens_planned = false;
+    int64_t dens_new[2] = {0, 0}, dens_count[2] = {0, 0};  // [statics, dynamics]
     hgs::DBuf dup_status;   // look-back status words of duplicate_compact_kernel
     hgs::DBuf shdir, ddir;  // K1 view direction + clamp mask; K7b dL/d(direction)
     hgs::DBuf inst_k, inst_v, inst_k2, inst_v2;       // tile sort (I)

@@ -14,37 +14,16 @@
 #include "hgs_common.cuh"
 #include "raster_common.cuh"
 #include "sh.cuh"
+#include "gauss_math.cuh"
 
 namespace hgs {
 
 namespace {
 
-struct M3 {
-    double a[3][3];
-};
-struct M4 {
-    double a[4][4];
-};
-
-// gauss_math.cpp:99-121
-__device__ inline M4 rot4_from_pair(const double ql[4], const double qr[4]) {
-    const double a = ql[0], b = ql[1], c = ql[2], d = ql[3];
-    const double L[4][4] = {{a, -b, -c, -d}, {b, a, -d, c}, {c, d, a, -b}, {d, -c, b, a}};
-    const double p = qr[0], q = qr[1], r = qr[2], s = qr[3];
-    const double R[4][4] = {{p, -q, -r, -s}, {q, p, s, -r}, {r, -s, p, q}, {s, r, -q, p}};
-    M4 out;
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            double acc = L[i][0] * R[0][j];
-            acc = acc + L[i][1] * R[1][j];
-            acc = acc + L[i][2] * R[2][j];
-            acc = acc + L[i][3] * R[3][j];
-            out.a[i][j] = acc;
-        }
-    return out;
-}
+using gm::M3;
+using gm::M4;
+using gm::rot4_from_pair;
+using gm::quat_to_rot3;
 
 // gauss_math.cpp:159-162
 __device__ inline M4 build_cov4(const M4& rot, const double ls[4]) {
@@ -68,22 +47,6 @@ __device__ inline M4 build_cov4(const M4& rot, const double ls[4]) {
             r.a[i][j] = s;
         }
     return r;
-}
-
-// gauss_math.cpp:48-58
-__device__ inline bool quat_to_rot3(const double q[4], M3& r) {
-    double n = sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
-    double w = q[0], x = q[1], y = q[2], z = q[3];
-    r.a[0][0] = 1 - 2 * (y * y + z * z);
-    r.a[0][1] = 2 * (x * y - z * w);
-    r.a[0][2] = 2 * (x * z + y * w);
-    r.a[1][0] = 2 * (x * y + z * w);
-    r.a[1][1] = 1 - 2 * (x * x + z * z);
-    r.a[1][2] = 2 * (y * z - x * w);
-    r.a[2][0] = 2 * (x * z - y * w);
-    r.a[2][1] = 2 * (y * z + x * w);
-    r.a[2][2] = 1 - 2 * (x * x + y * y);
-    return fabs(n - 1.0) <= 1e-6;
 }
 
 // gauss_math.cpp:154-157

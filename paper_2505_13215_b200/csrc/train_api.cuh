@@ -8,3 +8,4 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
                                const hgs_raster_opts* opts, int deferred = 0);
 hgs_status hgs_render_finish(hgs_ctx* ctx);
 hgs_status hgs_upload_rows(hgs_ctx* ctx, const hgs_host_scene* s, int dtype, float* dst4, float* dst3);
+hgs_status hgs_layout_state(hgs_ctx* ctx);

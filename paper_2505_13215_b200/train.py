@@ -214,8 +214,7 @@ def sample_batches(n_samples: int, batch_size: int, iterations: int, seed: int) 
 # train_scene: the reference's training loop (train.cpp:382-494), device
 # resident.  Same configuration, same batch schedule (std::mt19937_64 +
 # uniform_int_distribution restated bit-exactly in rng.py), same cadence of
-# Adam / decay / sweep / probe; densification is not on this tier's path
-# and is rejected explicitly when the config asks for it.
+# Adam / decay / densify (device) / sweep / probe.
 
 from dataclasses import dataclass, field  # noqa: E402
 
@@ -319,10 +318,6 @@ def train_scene(scene: HybridScene, dataset: MultiViewDataset, cfg: TrainConfig,
     if not dataset.cameras or dataset.total_frames() == 0:  # train.cpp:367-368
         raise ValueError("train: dataset is empty")
     cfg.validate()
-    if cfg.densifies():
-        raise NotImplementedError("train_scene: densification (train.cpp:182-299) is not on this tier's "
-                                  "hot path (SURVEY.md 8f-1); use a config whose densify window is empty "
-                                  "(e.g. densify_stop_iter < warmup_iters, as the c3 benchmark run)")
     from .api import default_context
 
     ctx = ctx or default_context()
@@ -356,9 +351,16 @@ def train_scene(scene: HybridScene, dataset: MultiViewDataset, cfg: TrainConfig,
         # renders, losses, backward scaled by 1/B, densify statistics, NumericAbort, Adam
         ctx._check(ctx._lib.hgs_train_step(ctx.handle, B, karr, tarr, garr, B, C.byref(o), 1, C.byref(loss)))
         row = TrainLogRow(iter=it, loss=loss.value / B)
-        if it >= cfg.warmup_iters and it % cfg.densify_interval == 0 and cfg.conversion_enabled:
-            moved, _ = ctx.sweep_convert()  # train.cpp:466-472 (Adam rows remapped on the device)
-            row.conversions = len(moved)
+        if it >= cfg.warmup_iters and it % cfg.densify_interval == 0:
+            if it <= cfg.densify_stop_iter:  # train.cpp:457-465, on the device
+                ctx.densify_and_prune(rng, cfg.grad_threshold, cfg.opacity_prune_eps, cfg.clone_size_frac,
+                                      cfg.split_factor, cfg.max_gaussians)
+                if cfg.opacity_reset_enabled and cfg.opacity_reset_interval > 0 and \
+                        it % cfg.opacity_reset_interval == 0:
+                    ctx.opacity_reset()
+            if cfg.conversion_enabled:
+                moved, _ = ctx.sweep_convert()  # train.cpp:466-472 (Adam rows remapped on the device)
+                row.conversions = len(moved)
         if cfg.probe_interval > 0 and (it % cfg.probe_interval == 0 or it == cfg.iterations):
             pf = dataset.frames[probe[0]][probe[1]]
             img = ctx.render(dataset.cameras[probe[0]], pf.time, dataset.background,

@@ -391,3 +391,50 @@ def test_nonfinite_loss_without_update_is_returned(ctx):
     ctx.zero_grads()
     tr.gt[1][2, 2, 2] = 0.25
     assert np.isfinite(tr.step([0, 1]))
+
+
+def _densify_case(ctx, max_gaussians):
+    from paper_2505_13215_b200.rng import MT19937_64
+    from paper_2505_13215_b200.train import DeviceTrainer
+
+    scene = synthetic_scene(1200, 800, 1, seed=41, density_n=600)
+    cams = [ring_camera(41, 96, 72, index=i, n_ring=4) for i in range(4)]
+    tr = DeviceTrainer(ctx, scene, cams, [0.5] * 4, target=synthetic_scene(1200, 800, 1, seed=42, density_n=600),
+                       bg=(0.2, 0.2, 0.2))
+    for i in range(6):
+        tr.step([i % 4, (i + 1) % 4])
+    cur = ctx.download()
+    m, v, step = ctx.adam_state()
+    gn4, c4, gn3, c3 = ctx.densify_stats()
+    st = O.AdamState(cur)
+    st.m, st.v, st.step = m, v, step
+    st.grad_norm4, st.count4, st.grad_norm3, st.count3 = gn4, c4.astype(np.uint32), gn3, c3.astype(np.uint32)
+    avg = np.concatenate([gn4 / np.maximum(c4, 1), gn3 / np.maximum(c3, 1)])
+    cfg = dict(grad_threshold=float(np.quantile(avg[avg > 0], 0.5)), opacity_prune_eps=0.3,
+               clone_size_frac=0.05, split_factor=1.6, max_gaussians=max_gaussians)
+    ref_scene, ref_st, ref_rep = O.densify_and_prune(cur, st, O.Rng(17), **cfg)
+    rep = ctx.densify_and_prune(MT19937_64(17), **cfg)
+    return cur, ref_scene, ref_st, ref_rep, rep
+
+
+@pytest.mark.parametrize("max_gaussians", [20000, 1300])
+def test_densify_matches_oracle(ctx, max_gaussians):
+    """densify_and_prune (train.cpp:182-299) on the device against the oracle
+    on the same pools, statistics, Adam state and seed: identical decisions
+    (counts, pool sizes, row order), the reference's normal variates (same
+    mt19937_64 sequence), Adam rows remapped with fresh rows zero."""
+    cur, ref, ref_st, ref_rep, rep = _densify_case(ctx, max_gaussians)
+    for k in ("cloned3", "split3", "pruned3", "cloned4", "split4", "pruned4"):
+        assert rep[k] == ref_rep[k], (k, rep, ref_rep)
+    assert rep["cloned4"] + rep["split4"] > 0 and rep["pruned4"] > 0
+    assert (rep["new_n4"], rep["new_n3"]) == (ref.n4, ref.n3)
+    out = ctx.download()
+    m, v, _ = ctx.adam_state()
+    for f in ("mean_x", "mean_t", "ql", "qr", "log_s4", "op4", "sh4", "mean3", "quat3", "log_s3", "op3", "sh3"):
+        a, b = getattr(out, f), getattr(ref, f)
+        assert a.shape == b.shape, f
+        assert np.allclose(a, b, rtol=1e-6, atol=1e-6), (f, np.abs(a - b).max())
+        assert np.allclose(getattr(m, f), getattr(ref_st.m, f), rtol=1e-6, atol=1e-12), f
+        assert np.allclose(getattr(v, f), getattr(ref_st.v, f), rtol=1e-6, atol=1e-12), f
+    gn4, c4, gn3, c3 = ctx.densify_stats()
+    assert not gn4.any() and not c4.any() and not gn3.any() and not c3.any()

@@ -79,12 +79,31 @@ def test_first_iteration_loss_matches_oracle(ctx):
     assert res.log[0].loss == pytest.approx(ref, rel=1e-5)
 
 
-def test_train_scene_rejects_densification_and_bad_config(ctx):
+def test_train_scene_with_densification(ctx):
+    """The full loop with the densify window open (train.cpp:456-465): pools
+    change size at the densify iterations only, the loss still decreases."""
+    from paper_2505_13215_b200.train import TrainConfig, train_scene
+
+    ds = _dataset(ctx)
+    init = synthetic_scene(1200, 400, 1, seed=45, density_n=1500, tau=0.3)
+    sizes = []
+    cfg = TrainConfig(iterations=40, batch_size=2, warmup_iters=10, densify_interval=10, densify_stop_iter=30,
+                      grad_threshold=1e-4, opacity_prune_eps=0.02, tau=0.3, seed=3, sh_degree=1, probe_interval=0,
+                      max_gaussians=1500, opacity_reset_enabled=True, opacity_reset_interval=20)
+    res = train_scene(init, ds, cfg, ctx=ctx, on_row=lambda r: sizes.append(r.n_static + r.n_dynamic))
+    log = res.log
+    assert all(math.isfinite(r.loss) for r in log)
+    changes = [i + 1 for i in range(1, len(sizes)) if sizes[i] != sizes[i - 1]]
+    assert changes and set(changes) <= {10, 20, 30, 40}, changes
+    assert res.scene.n4 <= 1500 and res.scene.n3 <= 1500 + 1200
+    # the opacity reset at iteration 20 (logit(0.01) cap) makes the scene translucent
+    assert max(r.loss for r in log[20:]) > min(r.loss for r in log[:20])
+
+
+def test_train_scene_rejects_bad_config(ctx):
     from paper_2505_13215_b200.train import TrainConfig, train_scene
 
     ds = _dataset(ctx, n_cams=2, n_frames=1)
     init = synthetic_scene(100, 50, 1, seed=44)
-    with pytest.raises(NotImplementedError):
-        train_scene(init, ds, TrainConfig(iterations=200, warmup_iters=100, densify_stop_iter=150), ctx=ctx)
     with pytest.raises(ValueError):
         train_scene(init, ds, TrainConfig(iterations=10, warmup_iters=20), ctx=ctx)

@@ -17,3 +17,25 @@ def test_uniform_index_matches_libstdcxx():
         ref, ours = O.Rng(seed), MT19937_64(seed)
         for _ in range(500):
             assert uniform_index(ours, 0, n - 1) == ref.index(0, n - 1)
+
+
+def test_normal_distribution_matches_libstdcxx():
+    """std::normal_distribution<double> (Marsaglia polar, cached second
+    variate) drawn from one object, as the dynamics pool of densify does."""
+    from paper_2505_13215_b200.rng import NormalDistribution
+
+    for seed in (0, 7, 123456789):
+        ref = O.Rng(seed).normal_seq(1001)
+        g, nd = MT19937_64(seed), NormalDistribution()
+        ours = [nd(g) for _ in range(1001)]
+        assert ours == ref.tolist()
+
+
+def test_fresh_distribution_per_call_matches_oracle_normal():
+    """hgso_rng_normal draws from a fresh distribution each call (like
+    sample_normal3's per-call object): the cached variate is discarded."""
+    from paper_2505_13215_b200.rng import NormalDistribution
+
+    ref, g = O.Rng(99), MT19937_64(99)
+    for _ in range(200):
+        assert NormalDistribution()(g) == ref.normal()
