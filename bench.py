@@ -303,11 +303,15 @@ def run_ours(args) -> None:
     info = ctx.render_info()
     value = world * args.steps / (ms / 1e3)
 
-    # ---- end to end through the C ABI with HOST ground truth (pinned)
+    # ---- end to end through the C ABI with HOST ground truth (pinned): the
+    # frames as the reference's dataset holds them, 8-bit sRGB (read_ppm),
+    # decoded on the device inside the loss (HGS_U8)
+    from paper_2505_13215_b200.train import linear_to_srgb8
+
     H, W = cams[0].height, cams[0].width
-    gts_host = [torch.empty((H, W, 3), dtype=torch.float32).pin_memory() for _ in range(len(cams))]
+    gts_host = [torch.empty((H, W, 3), dtype=torch.uint8).pin_memory() for _ in range(len(cams))]
     for i, g in enumerate(gts_host):
-        g.copy_(tr.gt[i].cpu())
+        g.copy_(torch.as_tensor(linear_to_srgb8(tr.gt[i].cpu().numpy().astype(np.float64))))
     lib = _capi.lib()
 
     def e2e_step(i):
@@ -319,7 +323,7 @@ def run_ours(args) -> None:
         garr = (C.c_void_p * n)(*[C.c_void_p(gts_host[v].data_ptr()) for v in mine])
         loss = C.c_double()
         tr.iter += 1
-        ctx._check(lib.hgs_train_step_host(ctx.handle, n, karr, tarr, garr, _capi.HGS_F32, world,
+        ctx._check(lib.hgs_train_step_host(ctx.handle, n, karr, tarr, garr, _capi.HGS_U8, world,
                                            C.byref(tr._opts(tr.decay())), 0 if world > 1 else 1, C.byref(loss)))
         if world > 1:
             g = tr.packed_grads_tensor()
@@ -368,11 +372,11 @@ def run_ours(args) -> None:
                "data": "synthetic (SURVEY.md 8d generator; random init, GT = 8-bit render of a second scene)",
                "config": dict(desc, parallelism=f"view-parallel dp{world}", views_per_iteration=world),
                "e2e": {"value": round(e2e_value, 3), "unit": UNIT,
-                       "h2d_bytes_per_step": int(W * H * 3 * 4),
+                       "h2d_bytes_per_step": int(W * H * 3),  # one 8-bit sRGB frame
                        "d2h_bytes_per_step": 16 if world == 1 else 96,  # loss sums (+ counters when synchronous)
-                       "path": ("hgs_train_step_async with host GT + hgs_train_collect (pinned host GT frame in, "
-                                "loss out, every iteration)") if world == 1 else
-                               "hgs_train_step_host (pinned host GT frame in, loss out)"},
+                       "path": ("hgs_train_step_async with a host 8-bit sRGB GT frame + hgs_train_collect "
+                                "(pinned host frame in, loss out, every iteration)") if world == 1 else
+                               "hgs_train_step_host (pinned host 8-bit GT frame in, loss out)"},
                "render": {"value": round(render_mpix, 2), "unit": "Mpix/s",
                           "what": "forward render of the device-resident c2 scene, 1352x1014"},
                "gpu_launches": int(launches), "launches_per_step": round(launches / args.steps, 1),

@@ -41,7 +41,11 @@ typedef enum {
     HGS_ERR_STATE = 6                /* call out of order (e.g. backward before forward) */
 } hgs_status;
 
-enum { HGS_F64 = 0, HGS_F32 = 1 };
+enum { HGS_F64 = 0, HGS_F32 = 1, HGS_U8 = 2 };
+/* HGS_U8: ground-truth frames only -- 8-bit sRGB RGB triples as the dataset
+ * stores them (read_ppm), decoded on the device with srgb8_to_linear
+ * (image.cpp:20-22, (v/255)^2.2) inside the loss: 4x less memory and
+ * host->device traffic than float frames, identical loss values. */
 
 typedef struct hgs_ctx hgs_ctx;
 

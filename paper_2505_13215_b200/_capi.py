@@ -14,7 +14,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("HGS_LIB") or os.path.join(_HERE, "libhgs_gpu.so")  # HGS_LIB: A/B builds
 
-HGS_F64, HGS_F32 = 0, 1
+HGS_F64, HGS_F32, HGS_U8 = 0, 1, 2
 
 _vp = C.c_void_p
 _dp = C.POINTER(C.c_double)

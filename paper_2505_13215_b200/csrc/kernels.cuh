@@ -84,11 +84,9 @@ __global__ void gaussian_bwd_kernel(int N, const uint32_t* __restrict__ sorted_o
                                     const double* __restrict__ conic_src, int conic_stride, const float4* __restrict__ ddir, int first);
 // loss.cu (K5)
 void set_ssim_window();
-__global__ void ssim_fwd_kernel(const float* __restrict__ a, const float* __restrict__ b, int W, int H,
-                                float* __restrict__ maps, double* __restrict__ ssim_sum);
-__global__ void ssim_bwd_kernel(const float* __restrict__ a, const float* __restrict__ b, int W, int H,
-                                const float* __restrict__ maps, float lambda, int with_ssim, float* __restrict__ grad,
-                                double* __restrict__ l1_sum);
+void set_srgb_lut();
+void launch_loss(cudaStream_t st, const float* img, const void* gt, bool gt_u8, int W, int H, float* maps,
+                 float lambda, bool with_ssim, float* grad, double* sums);
 // adam.cu (K8)
 struct AdamArgs {
     float b1, b2, one_m_b1, one_m_b2;

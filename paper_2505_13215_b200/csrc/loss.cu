@@ -22,6 +22,19 @@ namespace {
 constexpr int kWin = 11, kHalf = 5;
 
 __constant__ float c_win[kWin];
+// image.cpp:20-22 srgb8_to_linear(v) = (v / 255)^2.2, evaluated in FP64 on
+// the host and rounded to FP32 (the same value a float frame would hold)
+__constant__ float c_srgb[256];
+
+// ground-truth pixel loaders: linear float frames or 8-bit sRGB frames
+struct GtF32 {
+    const float* p;
+    __device__ __forceinline__ float operator[](size_t i) const { return p[i]; }
+};
+struct GtU8 {
+    const uint8_t* p;
+    __device__ __forceinline__ float operator[](size_t i) const { return c_srgb[p[i]]; }
+};
 
 __device__ inline float block_sum(float v, float* red) {
 #pragma unroll
@@ -40,6 +53,12 @@ __device__ inline float block_sum(float v, float* red) {
 }
 
 }  // namespace
+
+void set_srgb_lut() {
+    float lut[256];
+    for (int v = 0; v < 256; ++v) lut[v] = (float)std::pow((double)v / 255.0, 2.2);
+    cudaMemcpyToSymbol(c_srgb, lut, sizeof(lut));
+}
 
 void set_ssim_window() {
     // metrics.cpp:16-30: 2D window normalised by its sum == outer product of
@@ -68,8 +87,9 @@ constexpr int kSpan = kB + kWin - 1;  // inputs per blocked output group (14)
 // grid: (ceil(vw/32), ceil(vh/32), 3 channels); block 256.
 // a, b: HWC float images.  Writes maps (3 planes of vw*vh per channel) and
 // the SSIM sum.
-__global__ void __launch_bounds__(256) ssim_fwd_kernel(const float* __restrict__ a, const float* __restrict__ b, int W,
-                                                       int H, float* __restrict__ maps, double* __restrict__ ssim_sum) {
+template <typename Gt>
+__global__ void __launch_bounds__(256) ssim_fwd_kernel(const float* __restrict__ a, const Gt b, int W, int H,
+                                                       float* __restrict__ maps, double* __restrict__ ssim_sum) {
     __shared__ float sa[kS][kS + 1], sb[kS][kS + 1];
     __shared__ float h[5][kS][kT + 1];
     __shared__ float red[8];
@@ -170,10 +190,10 @@ __global__ void __launch_bounds__(256) ssim_fwd_kernel(const float* __restrict__
 }
 
 // grid: (ceil(W/32), ceil(H/32), 3); dL/dimage = (1-l) sign(a-b)/n - l dSSIM/da.
-__global__ void __launch_bounds__(256) ssim_bwd_kernel(const float* __restrict__ a, const float* __restrict__ b, int W,
-                                                       int H, const float* __restrict__ maps, float lambda,
-                                                       int with_ssim, float* __restrict__ grad,
-                                                       double* __restrict__ l1_sum) {
+template <typename Gt>
+__global__ void __launch_bounds__(256) ssim_bwd_kernel(const float* __restrict__ a, const Gt b, int W, int H,
+                                                       const float* __restrict__ maps, float lambda, int with_ssim,
+                                                       float* __restrict__ grad, double* __restrict__ l1_sum) {
     __shared__ float sm[3][kS][kS + 1];
     __shared__ float h[3][kS][kT + 1];
     __shared__ float red[8];
@@ -264,6 +284,23 @@ __global__ void __launch_bounds__(256) ssim_bwd_kernel(const float* __restrict__
     }
     const float tot = block_sum(local, red);
     if (threadIdx.x == 0) atomicAdd(l1_sum, (double)tot);
+}
+
+// Host launcher of the two loss passes; gt_u8: the ground truth is an 8-bit
+// sRGB frame (decoded through c_srgb), else a linear float frame.
+void launch_loss(cudaStream_t st, const float* img, const void* gt, bool gt_u8, int W, int H, float* maps,
+                 float lambda, bool with_ssim, float* grad, double* sums) {
+    const int vw = W - kWin + 1, vh = H - kWin + 1;
+    dim3 g((vw + 31) / 32, (vh + 31) / 32, 3), gb((W + 31) / 32, (H + 31) / 32, 3);
+    if (gt_u8) {
+        const GtU8 b{static_cast<const uint8_t*>(gt)};
+        if (with_ssim) ssim_fwd_kernel<GtU8><<<g, 256, 0, st>>>(img, b, W, H, maps, &sums[0]);
+        ssim_bwd_kernel<GtU8><<<gb, 256, 0, st>>>(img, b, W, H, maps, lambda, with_ssim ? 1 : 0, grad, &sums[1]);
+    } else {
+        const GtF32 b{static_cast<const float*>(gt)};
+        if (with_ssim) ssim_fwd_kernel<GtF32><<<g, 256, 0, st>>>(img, b, W, H, maps, &sums[0]);
+        ssim_bwd_kernel<GtF32><<<gb, 256, 0, st>>>(img, b, W, H, maps, lambda, with_ssim ? 1 : 0, grad, &sums[1]);
+    }
 }
 
 }  // namespace hgs

@@ -63,6 +63,11 @@ hgs_status upload_image(hgs_ctx* ctx, const void* src, int dtype, int64_t n, DBu
                         DBuf* stage = nullptr) {
     if (!s) s = ctx->stream;
     if (!stage) stage = &ctx->stage;
+    if (dtype == HGS_U8) {  // 8-bit sRGB frame: stays 8-bit, decoded by the loss
+        CK(dst.ensure((size_t)n));
+        CK(cudaMemcpyAsync(dst.p, src, (size_t)n, cudaMemcpyHostToDevice, s));
+        return HGS_OK;
+    }
     CK(dst.ensure((size_t)n * 4));
     if (dtype == HGS_F32) {
         CK(cudaMemcpyAsync(dst.p, src, (size_t)n * 4, cudaMemcpyHostToDevice, s));
@@ -162,16 +167,17 @@ hgs_status run_backward(hgs_ctx* ctx, const float* lg, double scale) {
 // accumulates the loss into scratch->loss_acc (device) -- no host sync.
 // sums (device, optional): where to accumulate (ssim_sum, l1_sum); default
 // the scratch pair read by the loss API
-hgs_status run_loss(hgs_ctx* ctx, const float* gt, double lambda, double* sums = nullptr) {
+hgs_status run_loss(hgs_ctx* ctx, const void* gt, bool gt_u8, double lambda, double* sums = nullptr) {
     cudaStream_t st = ctx->stream;
     const int W = ctx->W, H = ctx->H;
     const bool with_ssim = lambda != 0.0;
     if (with_ssim && (W < 11 || H < 11))
         return fail(ctx, HGS_ERR_INVALID_ARGUMENT, "ssim: images smaller than the 11x11 window");
-    static bool window_set = false;
-    if (!window_set) {
+    static bool tables_set = false;
+    if (!tables_set) {
         set_ssim_window();
-        window_set = true;
+        set_srgb_lut();
+        tables_set = true;
     }
     const size_t npx = (size_t)W * H;
     CK(ctx->lgrad.ensure(npx * 3 * 4));
@@ -180,17 +186,10 @@ hgs_status run_loss(hgs_ctx* ctx, const float* gt, double lambda, double* sums =
     CK(cudaMemsetAsync(sums, 0, 2 * sizeof(double), st));  // ssim_sum, l1_sum
     const int vw = W - 10, vh = H - 10;
     prof_begin(ctx, PH_LOSS);
-    if (with_ssim) {
-        CK(ctx->loss_ws.ensure((size_t)vw * vh * 9 * 4));
-        dim3 g((vw + 31) / 32, (vh + 31) / 32, 3);
-        ssim_fwd_kernel<<<g, 256, 0, st>>>(ctx->img.as<float>(), gt, W, H, ctx->loss_ws.as<float>(), &sums[0]);
-        count_launch();
-        CKL();
-    }
-    dim3 gb((W + 31) / 32, (H + 31) / 32, 3);
-    ssim_bwd_kernel<<<gb, 256, 0, st>>>(ctx->img.as<float>(), gt, W, H, ctx->loss_ws.as<float>(), (float)lambda,
-                                        with_ssim ? 1 : 0, ctx->lgrad.as<float>(), &sums[1]);
-    count_launch();
+    if (with_ssim) CK(ctx->loss_ws.ensure((size_t)vw * vh * 9 * 4));
+    launch_loss(st, ctx->img.as<float>(), gt, gt_u8, W, H, ctx->loss_ws.as<float>(), (float)lambda, with_ssim,
+                ctx->lgrad.as<float>(), sums);
+    count_launch(with_ssim ? 2 : 1);
     CKL();
     prof_end(ctx);
     return HGS_OK;
@@ -383,7 +382,7 @@ hgs_status hgs_loss_with_grad(hgs_ctx* ctx, const void* gt, int dtype, int on_de
         if (r != HGS_OK) return r;
         g = ctx->gt_stage.as<float>();
     }
-    r = run_loss(ctx, g, lambda);
+    r = run_loss(ctx, g, false, lambda);
     if (r != HGS_OK) return r;
     Scratch* h = static_cast<Scratch*>(ctx->pinned.p);
     CK(cudaMemcpyAsync(h, ctx->scratch.p, sizeof(Scratch), cudaMemcpyDeviceToHost, ctx->stream));
@@ -407,7 +406,7 @@ hgs_status hgs_photometric_loss_with_grad(hgs_ctx* ctx, const void* rendered, co
     ctx->W = width;
     ctx->H = height;
     ctx->have_tape = false;  // img no longer belongs to a render
-    r = run_loss(ctx, ctx->gt_stage.as<float>(), lambda);
+    r = run_loss(ctx, ctx->gt_stage.as<float>(), false, lambda);
     if (r != HGS_OK) return r;
     Scratch* h = static_cast<Scratch*>(ctx->pinned.p);
     CK(cudaMemcpyAsync(h, ctx->scratch.p, sizeof(Scratch), cudaMemcpyDeviceToHost, ctx->stream));
@@ -633,7 +632,7 @@ hgs_status train_step_impl(hgs_ctx* ctx, int n_views, const hgs_camera* cams, co
         if (r != HGS_OK) return r;
     }
     for (int v = 0; v < n_views; ++v) {
-        const float* g = nullptr;
+        const void* g = nullptr;
         const int b = v & 1;
         if (!gt_on_device) {
             // e2e path: the view's ground truth comes from host memory.  It is
@@ -645,14 +644,15 @@ hgs_status train_step_impl(hgs_ctx* ctx, int n_views, const hgs_camera* cams, co
                              ctx->copy_stream, &ctx->gt_stage64[b]);
             if (r != HGS_OK) return r;
             CK(cudaEventRecord(ctx->gt_ready[b], ctx->copy_stream));
-            g = ctx->gt_buf[b].as<float>();
+            g = ctx->gt_buf[b].p;
         } else {
-            g = static_cast<const float*>(gt[v]);
+            g = gt[v];
         }
         r = hgs_render_pipeline(ctx, &cams[v], times[v], o->bg, &ro, 1);
         if (r != HGS_OK) return r;
         if (!gt_on_device) CK(cudaStreamWaitEvent(ctx->stream, ctx->gt_ready[b], 0));
-        r = run_loss(ctx, g, o->ssim_lambda, pipelined ? sc->pipe_sums[slot][v] : sc->view_sums[pending]);
+        r = run_loss(ctx, g, gt_dtype == HGS_U8, o->ssim_lambda,
+                     pipelined ? sc->pipe_sums[slot][v] : sc->view_sums[pending]);
         if (r != HGS_OK) return r;
         if (!gt_on_device) CK(cudaEventRecord(ctx->gt_free[b], ctx->stream));
         ++pending;
@@ -725,8 +725,10 @@ hgs_status hgs_train_step(hgs_ctx* ctx, int n_views, const hgs_camera* cams, con
 hgs_status hgs_train_step_async(hgs_ctx* ctx, int n_views, const hgs_camera* cams, const double* times,
                                 const void* const* gt, int dtype, int gt_on_device, int batch_total,
                                 const hgs_train_opts* o, int apply_adam) {
-    return train_step_impl(ctx, n_views, cams, times, gt, gt_on_device ? HGS_F32 : dtype, gt_on_device ? 1 : 0,
-                           batch_total, o, apply_adam, nullptr, 1);
+    if (gt_on_device && dtype == HGS_F64)
+        return fail(ctx, HGS_ERR_INVALID_ARGUMENT, "train_step_async: device frames are HGS_F32 or HGS_U8");
+    return train_step_impl(ctx, n_views, cams, times, gt, dtype, gt_on_device ? 1 : 0, batch_total, o, apply_adam,
+                           nullptr, 1);
 }
 
 int hgs_train_pending(hgs_ctx* ctx) { return ctx ? (int)ctx->pipeline.size() : 0; }

@@ -24,15 +24,19 @@ from .api import Context, LearningRates
 from .scene import Camera, HybridScene
 
 
+# image.cpp:20-22 srgb8_to_linear for every code, with the C library's pow
+SRGB8_LUT = np.array([math.pow(v / 255.0, 2.2) for v in range(256)])
+
+
 def linear_to_srgb8(v: np.ndarray) -> np.ndarray:
-    """image.cpp:15-18"""
+    """image.cpp:15-18 (std::lround: halves away from zero)"""
     v = np.clip(v, 0.0, 1.0)
-    return np.rint(np.power(v, 1.0 / 2.2) * 255.0).astype(np.uint8)
+    return np.floor(np.power(v, 1.0 / 2.2) * 255.0 + 0.5).astype(np.uint8)
 
 
 def srgb8_to_linear(v: np.ndarray) -> np.ndarray:
     """image.cpp:20-22"""
-    return np.power(v.astype(np.float64) / 255.0, 2.2)
+    return SRGB8_LUT[np.asarray(v, dtype=np.uint8)]
 
 
 def quantize_8bit(img: np.ndarray) -> np.ndarray:
@@ -57,7 +61,10 @@ class DeviceTrainer:
     def __init__(self, ctx: Context, scene: HybridScene, cameras: list[Camera], times: list[float],
                  target: HybridScene | None = None, gt_images: list[np.ndarray] | None = None,
                  bg=(0.0, 0.0, 0.0), ssim_lambda: float = 0.2, lrs: LearningRates | None = None,
-                 iterations: int = 2000, weight_cutoff: float = 0.05, quantize_gt: bool = True):
+                 iterations: int = 2000, weight_cutoff: float = 0.05, quantize_gt: bool = True,
+                 gt_format: str = "f32"):
+        """gt_format: "f32" -- linear float frames on the device; "u8" -- the
+        8-bit sRGB codes (4x smaller), decoded inside the loss (HGS_U8)."""
         import torch
 
         self.torch = torch
@@ -79,7 +86,13 @@ class DeviceTrainer:
             for cam, t in zip(self.cameras, self.times):
                 img = ctx.render(cam, t, self.bg, weight_cutoff=weight_cutoff)["rgb"].astype(np.float64)
                 gt_images.append(quantize_8bit(img) if quantize_gt else img)
-        self.gt = [torch.as_tensor(np.ascontiguousarray(g, dtype=np.float32), device=dev) for g in gt_images]
+        if gt_format not in ("f32", "u8"):
+            raise ValueError("gt_format: 'f32' or 'u8'")
+        self.gt_format = gt_format
+        if gt_format == "u8":
+            self.gt = [torch.as_tensor(np.ascontiguousarray(linear_to_srgb8(g)), device=dev) for g in gt_images]
+        else:
+            self.gt = [torch.as_tensor(np.ascontiguousarray(g, dtype=np.float32), device=dev) for g in gt_images]
         ctx.upload(scene)
         self._cams = (_capi.Camera_ * max(1, len(self.cameras)))()
         for i, c in enumerate(self.cameras):
@@ -99,6 +112,9 @@ class DeviceTrainer:
 
     def step(self, views: list[int], batch_total: int | None = None, apply_adam: bool = True) -> float:
         """One iteration over ``views`` (indices into cameras); returns the mean loss."""
+        if self.gt_format == "u8":
+            self.step_async(views, batch_total, apply_adam)
+            return self.collect()
         if apply_adam:
             self.iter += 1
         n = len(views)
@@ -124,7 +140,8 @@ class DeviceTrainer:
         times = (C.c_double * max(1, n))(*[self.times[v] for v in views])
         src = gt_host if gt_host is not None else [self.gt[v] for v in views]
         gts = (C.c_void_p * max(1, n))(*[C.c_void_p(t.data_ptr()) for t in src])
-        self.ctx._check(self.ctx._lib.hgs_train_step_async(self.ctx.handle, n, cams, times, gts, _capi.HGS_F32,
+        dtype = _capi.HGS_U8 if src and src[0].dtype == self.torch.uint8 else _capi.HGS_F32
+        self.ctx._check(self.ctx._lib.hgs_train_step_async(self.ctx.handle, n, cams, times, gts, dtype,
                                                            0 if gt_host is not None else 1, batch_total or n,
                                                            C.byref(self._opts(self.decay())),
                                                            1 if apply_adam else 0))

@@ -438,3 +438,30 @@ def test_densify_matches_oracle(ctx, max_gaussians):
         assert np.allclose(getattr(v, f), getattr(ref_st.v, f), rtol=1e-6, atol=1e-12), f
     gn4, c4, gn3, c3 = ctx.densify_stats()
     assert not gn4.any() and not c4.any() and not gn3.any() and not c3.any()
+
+
+def test_u8_ground_truth_matches_float_frames(ctx):
+    """HGS_U8 frames (8-bit sRGB, decoded in the loss with srgb8_to_linear,
+    image.cpp:20-22) give the loss of the equivalent float frames."""
+    import torch
+
+    from paper_2505_13215_b200.train import DeviceTrainer, linear_to_srgb8, srgb8_to_linear
+
+    scene = synthetic_scene(900, 300, 1, seed=46, density_n=1200)
+    cams = [ring_camera(46, 80, 64, index=i, n_ring=2) for i in range(2)]
+    target = synthetic_scene(900, 300, 1, seed=47, density_n=1200)
+    a = DeviceTrainer(ctx, scene, cams, [0.5, 0.5], target=target, bg=(0.2, 0.2, 0.2), gt_format="u8")
+    la = [a.step([0, 1], apply_adam=False) for _ in range(1)]
+    ctx.zero_grads()
+    b = DeviceTrainer(ctx, scene, cams, [0.5, 0.5], target=target, bg=(0.2, 0.2, 0.2))
+    for v in range(2):  # identical values: the codes decoded in FP64, rounded to FP32
+        assert torch.equal(b.gt[v], torch.as_tensor(srgb8_to_linear(a.gt[v].cpu().numpy()).astype(np.float32),
+                                                    device=b.gt[v].device))
+        assert (linear_to_srgb8(srgb8_to_linear(a.gt[v].cpu().numpy())) == a.gt[v].cpu().numpy()).all()
+    lb = [b.step([0, 1], apply_adam=False) for _ in range(1)]
+    ctx.zero_grads()
+    assert la[0] == pytest.approx(lb[0], rel=1e-12)
+    # and training with 8-bit frames works end to end
+    c = DeviceTrainer(ctx, scene, cams, [0.5, 0.5], target=target, bg=(0.2, 0.2, 0.2), gt_format="u8")
+    losses = [c.step([i % 2]) for i in range(20)]
+    assert losses[-1] < losses[0]
