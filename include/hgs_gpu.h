@@ -165,6 +165,24 @@ hgs_status hgs_photometric_loss_with_grad(hgs_ctx *ctx, const void *rendered, co
                                           int width, int height, double ssim_lambda, double *loss_out,
                                           void *grad_out);
 
+/* ---- evaluation (eval.cpp:12-23, metrics.cpp:91-101, raster.cpp:268-287) */
+/* PSNR (peak 1) and mean SSIM (valid 11x11 windows, over channels) of the
+ * last rendered image against gt (h*w*3: host HGS_F64/HGS_F32/HGS_U8, or a
+ * device HGS_F32/HGS_U8 frame when on_device).  psnr is +inf for identical
+ * images; asking for ssim of an image smaller than the window is
+ * HGS_ERR_INVALID_ARGUMENT (metrics.cpp:38-39). */
+hgs_status hgs_image_metrics(hgs_ctx *ctx, const void *gt, int dtype, int on_device, double *psnr_out,
+                             double *ssim_out);
+/* Standalone psnr / ssim (bindings.cpp:175-180) of two host images (h*w*3,
+ * HGS_F64 or HGS_F32); NULL outputs are skipped. */
+hgs_status hgs_metrics(hgs_ctx *ctx, const void *a, const void *b, int dtype, int width, int height,
+                       double *psnr_out, double *ssim_out);
+/* density_map: counts[h*w] = number of projected splats (dynamics only when
+ * dynamics_only) whose clamped pixel box covers the pixel.  Releases the
+ * last render's tape (it reuses the projection buffers). */
+hgs_status hgs_density_map(hgs_ctx *ctx, const hgs_camera *cam, double t, int dynamics_only,
+                           double weight_cutoff, uint32_t *counts_host);
+
 /* ---- optimizer (train.hpp:68-69) --------------------------------------- */
 hgs_status hgs_adam_step(hgs_ctx *ctx, const hgs_lrs *lrs, double mean_lr_scale, int64_t *skipped_out);
 hgs_status hgs_adam_state_download(hgs_ctx *ctx, hgs_host_scene *m, hgs_host_scene *v, int dtype,

@@ -2011,6 +2011,25 @@ int hgso_eval_sh(const double* coeffs, int degree, const double dir[3], double r
 }
 double hgso_exp(double x) { return std::exp(x); }
 
+// raster.cpp:268-287 density_map: per pixel, the number of projected splats
+// whose clamped box covers it (dynamics only on request).
+int hgso_density_map(const hgso_scene* s, const hgso_camera* cam, double t, int dynamics_only, double cutoff,
+                     uint32_t* counts) {
+    return guard([&] {
+        Cam c = to_cam(*cam);
+        hgso_scene tmp = *s;
+        if (dynamics_only) tmp.n3 = 0;
+        View v{&tmp, sh_count(s->sh_degree)};
+        std::vector<Splat> prims = project_scene(v, c, t, cutoff, nullptr);
+        std::fill(counts, counts + size_t(c.width) * c.height, 0u);
+        for (const Splat& sp : prims) {
+            Bounds b = splat_bounds(sp, c.width, c.height);
+            for (int y = b.y0; y <= b.y1; ++y)
+                for (int x = b.x0; x <= b.x1; ++x) counts[size_t(y) * c.width + x]++;
+        }
+    });
+}
+
 static void fill_splat(const Splat& s, int n4, int W, int H, hgso_splat& o) {
     o.sx = s.sx; o.sy = s.sy;
     o.conic[0] = s.conic[0][0]; o.conic[1] = s.conic[0][1];

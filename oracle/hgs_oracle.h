@@ -163,6 +163,9 @@ double hgso_exp(double x);
 /* project_3d (raster.cpp:26-64): returns 1 and fills *out when projected */
 int hgso_project_3d(const double mean3[3], const double cov3[9], const hgso_camera *cam,
                     hgso_splat *out, hgso_stats *stats, int *projected);
+/* density_map (raster.cpp:268-287): counts[h*w] */
+int hgso_density_map(const hgso_scene *s, const hgso_camera *cam, double t, int dynamics_only, double weight_cutoff,
+                     uint32_t *counts);
 /* project_scene: writes up to cap splats (dynamics first, then statics) */
 int hgso_project_scene(const hgso_scene *s, const hgso_camera *cam, double t, double weight_cutoff,
                        hgso_splat *out, int64_t cap, int64_t *n_out, hgso_stats *stats);

@@ -134,6 +134,8 @@ def lib():
         L.hgso_rng_raw.restype = C.c_uint64
         L.hgso_rng_raw.argtypes = [C.c_void_p]
         L.hgso_rng_normal_seq.argtypes = [C.c_void_p, C.c_int64, _dp]
+        L.hgso_density_map.argtypes = [C.POINTER(_Scene), C.POINTER(_Camera), C.c_double, C.c_int, C.c_double,
+                                       _u32p]
         L.hgso_densify_and_prune.argtypes = [C.POINTER(_Scene), C.POINTER(_State), C.POINTER(_Scene),
                                              C.POINTER(_State), C.POINTER(_DensifyCfg), C.c_void_p,
                                              C.POINTER(_DensifyRep)]
@@ -699,6 +701,15 @@ def densify_and_prune(scene: HybridScene, state: AdamState, rng: Rng, grad_thres
     ost.grad_norm3, ost.count3 = np.zeros(n3), np.zeros(n3, dtype=np.uint32)
     ost.step, ost.skipped_nonfinite = state.step, state.skipped_nonfinite
     return out, ost, {n: int(getattr(rep, n)) for n, _ in _DensifyRep._fields_}
+
+
+def density_map(scene: HybridScene, cam: Camera, t: float, dynamics_only: bool = False,
+                weight_cutoff: float = 0.05) -> np.ndarray:
+    """raster.cpp:268-287: (h, w) uint32 box-coverage counts."""
+    out = np.zeros((cam.height, cam.width), dtype=np.uint32)
+    _check(lib().hgso_density_map(C.byref(_scene_struct(scene)), C.byref(_cam_struct(cam)), t,
+                                  1 if dynamics_only else 0, weight_cutoff, out.ctypes.data_as(_u32p)))
+    return out
 
 
 def _empty_scene_like(scene: HybridScene, n4: int, n3: int) -> HybridScene:

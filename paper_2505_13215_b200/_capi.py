@@ -140,6 +140,9 @@ _SIGS = {
     "hgs_densify_plan": ([_vp, C.POINTER(DensifyCfg), _vp, _vp, C.POINTER(DensifyReport)], C.c_int),
     "hgs_densify_apply": ([_vp, _dp, _dp, C.c_double], C.c_int),
     "hgs_opacity_reset": ([_vp, C.c_double], C.c_int),
+    "hgs_image_metrics": ([_vp, _vp, C.c_int, C.c_int, _dp, _dp], C.c_int),
+    "hgs_metrics": ([_vp, _vp, _vp, C.c_int, C.c_int, C.c_int, _dp, _dp], C.c_int),
+    "hgs_density_map": ([_vp, C.POINTER(Camera_), C.c_double, C.c_int, C.c_double, _u32p], C.c_int),
     "hgs_train_step_async": ([_vp, C.c_int, C.POINTER(Camera_), _dp, C.POINTER(_vp), C.c_int, C.c_int, C.c_int,
                               C.POINTER(TrainOpts), C.c_int], C.c_int),
     "hgs_train_collect": ([_vp, _dp], C.c_int),

@@ -20,7 +20,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _capi
-from ._capi import (HGS_F32, HGS_F64, CudaError, DegenerateRotationError, DegenerateTemporalError,  # noqa: F401
+from ._capi import (HGS_F32, HGS_F64, HGS_U8, CudaError, DegenerateRotationError, DegenerateTemporalError,  # noqa: F401
                     HgsError, NumericAbort, StateError, check, ptr)
 from .scene import Camera, HybridScene, sh_coeff_count
 
@@ -157,6 +157,48 @@ class Context:
         self._last_shape = (H, W)
         return {"rgb": rgb, "counts": counts, "transmittance": trans,
                 "stats": {n: int(getattr(st, n)) for n, _ in _capi.RenderStats._fields_}}
+
+    def render_device(self, camera: Camera, t: float, background=(0.0, 0.0, 0.0),
+                      weight_cutoff=DEFAULT_WEIGHT_CUTOFF) -> None:
+        """Render into the context's device image only (no host copy); read
+        it with last_image_device_ptr() or score it with image_metrics()."""
+        bg = np.ascontiguousarray(background, dtype=np.float64)
+        o = _opts(weight_cutoff)
+        self._check(self._lib.hgs_render(self._h, C.byref(_capi.camera_struct(camera)), float(t),
+                                         bg.ctypes.data_as(_capi._dp), C.byref(o), None, None, None, None))
+        self._last_shape = (camera.height, camera.width)
+
+    def image_metrics(self, gt: np.ndarray | None = None, gt_device_ptr: int | None = None,
+                      gt_u8: bool = False, want_ssim: bool = True) -> tuple[float, float | None]:
+        """(psnr, ssim) of the last rendered image against gt (metrics.cpp:91-101
+        and the valid-window SSIM), on the device.  gt: (h, w, 3) float64 /
+        float32 linear, or uint8 sRGB; or a device float32 / uint8 frame."""
+        p, q = C.c_double(), C.c_double()
+        qs = C.byref(q) if want_ssim else None
+        if gt_device_ptr is not None:
+            self._check(self._lib.hgs_image_metrics(self._h, C.c_void_p(gt_device_ptr), HGS_U8 if gt_u8 else HGS_F32,
+                                                    1, C.byref(p), qs))
+        else:
+            a = np.ascontiguousarray(gt)
+            if a.shape != self._last_shape + (3,):
+                raise ValueError("metrics: image dimensions differ")
+            if a.dtype == np.uint8:
+                code = HGS_U8
+            else:
+                code = _dtype_code(a.dtype)
+                a = a.astype(np.float64 if code == HGS_F64 else np.float32, copy=False)
+            self._check(self._lib.hgs_image_metrics(self._h, ptr(a), code, 0, C.byref(p), qs))
+        return p.value, (q.value if want_ssim else None)
+
+    def density_map(self, camera: Camera, t: float, dynamics_only: bool = False,
+                    weight_cutoff: float = DEFAULT_WEIGHT_CUTOFF) -> np.ndarray:
+        """raster.cpp:268-287 on the device: (h, w) uint32 splat coverage
+        counts of the resident scene.  Releases the last render's tape."""
+        out = np.empty((camera.height, camera.width), dtype=np.uint32)
+        self._check(self._lib.hgs_density_map(self._h, C.byref(_capi.camera_struct(camera)), float(t),
+                                              int(bool(dynamics_only)), float(weight_cutoff),
+                                              out.ctypes.data_as(_capi._u32p)))
+        return out
 
     def render_info(self) -> dict:
         info = _capi.RenderInfo()
@@ -379,3 +421,33 @@ def rasterize(scene: HybridScene, camera: Camera, t: float, background=(0.0, 0.0
         return rgb
     return {"rgb": rgb, "counts": counts, "transmittance": trans,
             "stats": {n: int(getattr(st, n)) for n, _ in _capi.RenderStats._fields_}}
+
+
+def density_map(scene: HybridScene, camera: Camera, t: float, dynamics_only: bool = False,
+                weight_cutoff: float = DEFAULT_WEIGHT_CUTOFF) -> np.ndarray:
+    """hybridgs.density_map (bindings.cpp:165-172): (h, w) uint32 counts."""
+    ctx = default_context()
+    ctx.upload(scene)
+    return ctx.density_map(camera, t, dynamics_only, weight_cutoff)
+
+
+def _metrics(a: np.ndarray, b: np.ndarray, want_psnr: bool, want_ssim: bool) -> tuple[float, float]:
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    if a.shape != b.shape or a.ndim != 3 or a.shape[2] != 3:
+        raise ValueError("metrics: image dimensions differ")
+    ctx = default_context()
+    p, q = C.c_double(), C.c_double()
+    ctx._check(ctx._lib.hgs_metrics(ctx.handle, ptr(a), ptr(b), HGS_F64, a.shape[1], a.shape[0],
+                                    C.byref(p) if want_psnr else None, C.byref(q) if want_ssim else None))
+    return p.value, q.value
+
+
+def psnr(a: np.ndarray, b: np.ndarray) -> float:
+    """hybridgs.psnr (metrics.cpp:91-101) on the device: 10 log10(1 / MSE)."""
+    return _metrics(a, b, True, False)[0]
+
+
+def ssim(a: np.ndarray, b: np.ndarray) -> float:
+    """hybridgs.ssim (metrics.cpp): mean SSIM over the valid 11x11 windows."""
+    return _metrics(a, b, False, True)[1]

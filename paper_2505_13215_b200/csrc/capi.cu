@@ -699,6 +699,61 @@ hgs_status hgs_scene_download(hgs_ctx* ctx, hgs_host_scene* out, int dtype) {
     return HGS_OK;
 }
 
+// density_map (raster.cpp:268-287): K1 projects the pools (statics skipped
+// when dynamics_only), every projected splat adds +1 over its clamped box
+// through a 2D difference array, row and column prefix sums finish it.
+// Reuses the render buffers, so the last render's tape is released.
+hgs_status hgs_density_map(hgs_ctx* ctx, const hgs_camera* cam, double t, int dynamics_only, double weight_cutoff,
+                           uint32_t* counts_host) {
+    if (!ctx || !cam || !counts_host) return HGS_ERR_INVALID_ARGUMENT;
+    CK(cudaSetDevice(ctx->device));
+    std::string why;
+    if (!camera_valid(cam, why)) return fail(ctx, HGS_ERR_INVALID_ARGUMENT, why);
+    hgs_status r = hgs_render_finish(ctx);
+    if (r != HGS_OK) return r;
+    ctx->have_tape = false;
+    cudaStream_t st = ctx->stream;
+    const int n4 = (int)ctx->n4, n3 = dynamics_only ? 0 : (int)ctx->n3, N = n4 + n3;
+    const int W = cam->width, H = cam->height;
+    const int tiles_x = (W + kTile - 1) / kTile;
+    const size_t npx = (size_t)W * H, ndiff = (size_t)(W + 1) * (H + 1);
+    CK(ctx->counters.ensure(sizeof(Counters)));
+    CK(ctx->pinned_ctr.ensure(sizeof(Counters) + 64));
+    Counters* dc = ctx->counters.as<Counters>();
+    Counters* hc = static_cast<Counters*>(ctx->pinned_ctr.p);
+    CK(cudaMemsetAsync(dc, 0, sizeof(Counters), st));
+    CK(ctx->dmap.ensure((ndiff + npx) * 4));
+    int* diff = ctx->dmap.as<int>();
+    uint32_t* out = reinterpret_cast<uint32_t*>(diff + ndiff);
+    CK(cudaMemsetAsync(diff, 0, ndiff * 4, st));
+    if (N > 0) {
+        CK(ctx->rec.ensure((size_t)N * sizeof(SplatRec)));
+        CK(ctx->depth_key.ensure((size_t)N * 4));
+        CK(ctx->ntiles.ensure((size_t)N * 4));
+        CK(ctx->shdir.ensure((size_t)N * sizeof(ShRec)));
+        preprocess_kernel<<<div_up(N, 256), 256, 0, st>>>(
+            ctx->p4.as<float>(), ctx->cap4, n4, ctx->p3.as<float>(), ctx->cap3, n3, ctx->deg, to_dev(cam), t,
+            weight_cutoff, tiles_x, ctx->rec.as<SplatRec>(), ctx->depth_key.as<uint32_t>(), ctx->ntiles.as<uint32_t>(),
+            dc->stats, &dc->flags, ctx->shdir.as<ShRec>());
+        count_launch();
+        CKL();
+        density_diff_kernel<<<div_up(N, 256), 256, 0, st>>>(ctx->ntiles.as<uint32_t>(), ctx->rec.as<SplatRec>(), N, W,
+                                                           H, diff);
+        count_launch();
+        CKL();
+    }
+    density_rows_kernel<<<div_up(H + 1, 8), 256, 0, st>>>(diff, W, H);
+    count_launch();
+    CKL();
+    density_cols_kernel<<<div_up(W, 256), 256, 0, st>>>(diff, W, H, out);
+    count_launch();
+    CKL();
+    CK(cudaMemcpyAsync(counts_host, out, npx * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hc, dc, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return check_flags(ctx, hc->flags);
+}
+
 hgs_status hgs_scene_counts(hgs_ctx* ctx, int64_t* n4, int64_t* n3, int32_t* deg) {
     if (!ctx) return HGS_ERR_INVALID_ARGUMENT;
     if (n4) *n4 = ctx->n4;

@@ -140,6 +140,7 @@ struct hgs_ctx {
     hgs::DBuf loss_ws;   // loss scratch (SSIM maps)
     hgs::DBuf scratch;   // small device scalars (loss sums, skip counts, leakage)
     hgs::DBuf stage;     // upload / download staging
+    hgs::DBuf dmap;      // density_map difference array ((W+1)*(H+1) ints) and counts
     hgs::HostPinned pinned;      // Scratch read-back (training / loss)
     hgs::HostPinned pinned_ctr;  // Counters read-back (render)
     hgs::HostPinned pinned_pipe; // per-slot loss sums of pipelined iterations

@@ -87,6 +87,14 @@ void set_ssim_window();
 void set_srgb_lut();
 void launch_loss(cudaStream_t st, const float* img, const void* gt, bool gt_u8, int W, int H, float* maps,
                  float lambda, bool with_ssim, float* grad, double* sums);
+void launch_metrics(cudaStream_t st, const float* img, const void* gt, bool gt_u8, int W, int H, float* maps,
+                    double* sums);
+// density_map (raster.cpp:268-287): +1 over every projected splat's box via a
+// 2D difference array and row / column prefix sums
+__global__ void density_diff_kernel(const uint32_t* __restrict__ ntiles, const SplatRec* __restrict__ rec, int n,
+                                    int W, int H, int* __restrict__ diff);
+__global__ void density_rows_kernel(int* __restrict__ diff, int W, int H);
+__global__ void density_cols_kernel(const int* __restrict__ diff, int W, int H, uint32_t* __restrict__ out);
 // adam.cu (K8)
 struct AdamArgs {
     float b1, b2, one_m_b1, one_m_b2;

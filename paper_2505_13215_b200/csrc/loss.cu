@@ -13,6 +13,8 @@
 //             dSSIM/da(p) = [W*A](p) + 2 a_p [W*B](p) + b_p [W*C](p),  / n_valid.
 // The L1 term, the (1-l) / -l weights and the loss reduction are fused into
 // the backward pass.  Bound: HBM (about 44 B per pixel and channel).
+#include <algorithm>
+
 #include "kernels.cuh"
 
 namespace hgs {
@@ -300,6 +302,46 @@ void launch_loss(cudaStream_t st, const float* img, const void* gt, bool gt_u8, 
         const GtF32 b{static_cast<const float*>(gt)};
         if (with_ssim) ssim_fwd_kernel<GtF32><<<g, 256, 0, st>>>(img, b, W, H, maps, &sums[0]);
         ssim_bwd_kernel<GtF32><<<gb, 256, 0, st>>>(img, b, W, H, maps, lambda, with_ssim ? 1 : 0, grad, &sums[1]);
+    }
+}
+
+// Sum of squared differences (for PSNR, metrics.cpp:91-101), FP64 per block.
+template <typename Gt>
+__global__ void __launch_bounds__(256) sqdiff_kernel(const float* __restrict__ a, const Gt b, int64_t n,
+                                                     double* __restrict__ sum) {
+    double acc = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const double d = (double)a[i] - (double)b[i];
+        acc += d * d;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    __shared__ double red[8];
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < 8; ++w) t += red[w];
+        atomicAdd(sum, t);
+    }
+}
+
+// metrics of img against gt: sums[0] = SSIM sum over the valid positions and
+// channels, sums[1] = sum of squared differences
+void launch_metrics(cudaStream_t st, const float* img, const void* gt, bool gt_u8, int W, int H, float* maps,
+                    double* sums) {
+    const int vw = W - kWin + 1, vh = H - kWin + 1;
+    dim3 g((vw + 31) / 32, (vh + 31) / 32, 3);
+    const int64_t n = (int64_t)W * H * 3;
+    const unsigned blocks = (unsigned)std::min<int64_t>((n + 255) / 256, 1184);
+    if (gt_u8) {
+        const GtU8 b{static_cast<const uint8_t*>(gt)};
+        if (vw > 0 && vh > 0) ssim_fwd_kernel<GtU8><<<g, 256, 0, st>>>(img, b, W, H, maps, &sums[0]);
+        sqdiff_kernel<GtU8><<<blocks, 256, 0, st>>>(img, b, n, &sums[1]);
+    } else {
+        const GtF32 b{static_cast<const float*>(gt)};
+        if (vw > 0 && vh > 0) ssim_fwd_kernel<GtF32><<<g, 256, 0, st>>>(img, b, W, H, maps, &sums[0]);
+        sqdiff_kernel<GtF32><<<blocks, 256, 0, st>>>(img, b, n, &sums[1]);
     }
 }
 

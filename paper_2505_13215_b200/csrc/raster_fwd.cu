@@ -561,4 +561,49 @@ __global__ void __launch_bounds__(128) raster_fixup_kernel(
     }
 }
 
+// ---- density_map (raster.cpp:268-287)
+__global__ void __launch_bounds__(256) density_diff_kernel(const uint32_t* __restrict__ ntiles,
+                                                           const SplatRec* __restrict__ rec, int n, int W, int H,
+                                                           int* __restrict__ diff) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n || ntiles[i] == 0u) return;  // culled (not projected)
+    const SplatRec& e = rec[i];
+    const int x0 = e.x0, x1 = e.x1, y0 = e.y0, y1 = e.y1;
+    atomicAdd(&diff[y0 * (W + 1) + x0], 1);
+    atomicAdd(&diff[y0 * (W + 1) + x1 + 1], -1);
+    atomicAdd(&diff[(y1 + 1) * (W + 1) + x0], -1);
+    atomicAdd(&diff[(y1 + 1) * (W + 1) + x1 + 1], 1);
+}
+
+// inclusive prefix along each row (one warp per row)
+__global__ void __launch_bounds__(256) density_rows_kernel(int* __restrict__ diff, int W, int H) {
+    const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (row > H) return;
+    int* r = diff + (size_t)row * (W + 1);
+    int carry = 0;
+    for (int x0 = 0; x0 <= W; x0 += 32) {
+        const int x = x0 + lane;
+        int v = x <= W ? r[x] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int u = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += u;
+        }
+        if (x <= W) r[x] = v + carry;
+        carry += __shfl_sync(0xffffffffu, v, 31);
+    }
+}
+
+// inclusive prefix down each column (one thread per column)
+__global__ void __launch_bounds__(256) density_cols_kernel(const int* __restrict__ diff, int W, int H,
+                                                           uint32_t* __restrict__ out) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    if (x >= W) return;
+    int acc = 0;
+    for (int y = 0; y < H; ++y) {
+        acc += diff[(size_t)y * (W + 1) + x];
+        out[(size_t)y * W + x] = (uint32_t)acc;
+    }
+}
+
 }  // namespace hgs

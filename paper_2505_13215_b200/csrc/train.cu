@@ -392,6 +392,70 @@ hgs_status hgs_loss_with_grad(hgs_ctx* ctx, const void* gt, int dtype, int on_de
     return HGS_OK;
 }
 
+// PSNR / SSIM of ctx->img (W x H) against a device frame (metrics.cpp:91-101)
+hgs_status metrics_impl(hgs_ctx* ctx, const void* g, bool gt_u8, double* psnr_out, double* ssim_out) {
+    const int W = ctx->W, H = ctx->H;
+    static bool tables_set = false;
+    if (!tables_set) {
+        set_ssim_window();
+        set_srgb_lut();
+        tables_set = true;
+    }
+    const int64_t n = (int64_t)W * H * 3;
+    Scratch* sc = scratch(ctx);
+    CK(cudaMemsetAsync(sc, 0, 2 * sizeof(double), ctx->stream));
+    if (W >= 11 && H >= 11) CK(ctx->loss_ws.ensure((size_t)(W - 10) * (H - 10) * 9 * 4));
+    launch_metrics(ctx->stream, ctx->img.as<float>(), g, gt_u8, W, H, ctx->loss_ws.as<float>(), &sc->ssim_sum);
+    count_launch(2);
+    CKL();
+    Scratch* h = static_cast<Scratch*>(ctx->pinned.p);
+    CK(cudaMemcpyAsync(h, sc, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    const double mse = h->l1_sum / (double)n;  // the squared-difference sum
+    if (psnr_out) *psnr_out = mse == 0.0 ? INFINITY : 10.0 * std::log10(1.0 / mse);
+    if (ssim_out) *ssim_out = h->ssim_sum / ((double)(W - 10) * (H - 10) * 3);
+    return HGS_OK;
+}
+
+hgs_status hgs_image_metrics(hgs_ctx* ctx, const void* gt, int dtype, int on_device, double* psnr_out,
+                             double* ssim_out) {
+    if (!ctx || !gt) return HGS_ERR_INVALID_ARGUMENT;
+    if (!ctx->have_tape) return fail(ctx, HGS_ERR_STATE, "metrics: render an image first");
+    CK(cudaSetDevice(ctx->device));
+    hgs_status r = ensure_scratch(ctx);
+    if (r != HGS_OK) return r;
+    if (ssim_out && (ctx->W < 11 || ctx->H < 11))  // metrics.cpp:38-39
+        return fail(ctx, HGS_ERR_INVALID_ARGUMENT, "ssim: images smaller than the 11x11 window");
+    const void* g = gt;
+    if (!on_device) {
+        r = upload_image(ctx, gt, dtype, (int64_t)ctx->W * ctx->H * 3, ctx->gt_stage);
+        if (r != HGS_OK) return r;
+        g = ctx->gt_stage.p;
+    } else if (dtype == HGS_F64) {
+        return fail(ctx, HGS_ERR_INVALID_ARGUMENT, "metrics: device frames are HGS_F32 or HGS_U8");
+    }
+    return metrics_impl(ctx, g, dtype == HGS_U8, psnr_out, ssim_out);
+}
+
+hgs_status hgs_metrics(hgs_ctx* ctx, const void* a, const void* b, int dtype, int width, int height,
+                       double* psnr_out, double* ssim_out) {
+    if (!ctx || !a || !b || width <= 0 || height <= 0 || dtype == HGS_U8) return HGS_ERR_INVALID_ARGUMENT;
+    CK(cudaSetDevice(ctx->device));
+    if (ssim_out && (width < 11 || height < 11))
+        return fail(ctx, HGS_ERR_INVALID_ARGUMENT, "ssim: images smaller than the 11x11 window");
+    hgs_status r = ensure_scratch(ctx);
+    if (r != HGS_OK) return r;
+    const int64_t n = (int64_t)width * height * 3;
+    r = upload_image(ctx, a, dtype, n, ctx->img);
+    if (r != HGS_OK) return r;
+    r = upload_image(ctx, b, dtype, n, ctx->gt_stage);
+    if (r != HGS_OK) return r;
+    ctx->W = width;
+    ctx->H = height;
+    ctx->have_tape = false;  // img no longer belongs to a render
+    return metrics_impl(ctx, ctx->gt_stage.p, false, psnr_out, ssim_out);
+}
+
 hgs_status hgs_photometric_loss_with_grad(hgs_ctx* ctx, const void* rendered, const void* gt, int dtype, int width,
                                           int height, double lambda, double* loss_out, void* grad_out) {
     if (!ctx || !rendered || !gt || width <= 0 || height <= 0) return HGS_ERR_INVALID_ARGUMENT;

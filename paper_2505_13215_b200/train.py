@@ -318,10 +318,44 @@ class TrainResult:  # train.hpp:80-84 (state = Adam moments m, v and the step)
     state: tuple
 
 
-def psnr(a: np.ndarray, b: np.ndarray) -> float:
-    """metrics.cpp:91-101: 10 log10(1 / MSE) over all channels (inf if equal)."""
-    mse = float(np.mean((np.asarray(a, np.float64) - np.asarray(b, np.float64)) ** 2))
-    return math.inf if mse == 0.0 else 10.0 * math.log10(1.0 / mse)
+from .api import psnr, ssim  # noqa: E402,F401  (device metrics, metrics.cpp:91-101)
+
+
+@dataclass
+class MetricReport:  # metrics.hpp:21-29
+    frame_psnr: list = field(default_factory=list)
+    frame_ssim: list = field(default_factory=list)
+    mean_psnr: float = 0.0
+    mean_ssim: float = 0.0
+    frames: int = 0
+
+    def add(self, p: float, s: float) -> None:  # metrics.cpp:109-120
+        self.frame_psnr.append(p)
+        self.frame_ssim.append(s)
+        self.frames = len(self.frame_psnr)
+        sp = ss = 0.0
+        for i in range(self.frames):
+            sp += self.frame_psnr[i]
+            ss += self.frame_ssim[i]
+        self.mean_psnr = sp / self.frames
+        self.mean_ssim = ss / self.frames
+
+
+def evaluate_views(scene: HybridScene | None, dataset: MultiViewDataset, weight_cutoff: float = 0.05,
+                   ctx: Context | None = None) -> MetricReport:
+    """eval.cpp:12-23 on the device: renders every (camera, frame) of the
+    dataset and scores it (PSNR + SSIM) without downloading the image.
+    ``scene`` is uploaded into ``ctx`` first unless None (score the resident
+    scene).  Frames may be float (linear) or uint8 (sRGB) arrays."""
+    ctx = ctx or Context(0)
+    if scene is not None:
+        ctx.upload(scene)
+    report = MetricReport()
+    for ci, cam in enumerate(dataset.cameras):
+        for fr in dataset.frames[ci]:
+            ctx.render_device(cam, fr.time, dataset.background, weight_cutoff=weight_cutoff)
+            report.add(*ctx.image_metrics(fr.image))
+    return report
 
 
 def train_scene(scene: HybridScene, dataset: MultiViewDataset, cfg: TrainConfig, ctx: Context | None = None,
@@ -380,9 +414,9 @@ def train_scene(scene: HybridScene, dataset: MultiViewDataset, cfg: TrainConfig,
                 row.conversions = len(moved)
         if cfg.probe_interval > 0 and (it % cfg.probe_interval == 0 or it == cfg.iterations):
             pf = dataset.frames[probe[0]][probe[1]]
-            img = ctx.render(dataset.cameras[probe[0]], pf.time, dataset.background,
-                             weight_cutoff=cfg.weight_cutoff)["rgb"]
-            row.probe_psnr = psnr(img, pf.image)
+            ctx.render_device(dataset.cameras[probe[0]], pf.time, dataset.background,
+                              weight_cutoff=cfg.weight_cutoff)
+            row.probe_psnr = ctx.image_metrics(pf.image, want_ssim=False)[0]
         row.n_dynamic, row.n_static = ctx.counts()
         row.wall_seconds = _time.perf_counter() - t0
         log.append(row)

@@ -119,6 +119,42 @@ def test_bit_identical_across_threads():
     assert (a == b).all() and (a == c).all()
 
 
+def single_static_scene(opacity_logit=1.0):
+    """One default Gaussian3D (scene.hpp:16-24) with the given opacity logit."""
+    return HybridScene(mean3=np.zeros((1, 3)), quat3=np.array([[1.0, 0, 0, 0]]), log_s3=np.zeros((1, 3)),
+                       op3=np.array([opacity_logit]))
+
+
+def _boxes_expect(splats, w, h):
+    expect = np.zeros((h, w), dtype=np.uint32)
+    for sp in splats:
+        expect[sp["y0"]:sp["y1"] + 1, sp["x0"]:sp["x1"] + 1] += 1
+    return expect
+
+
+def test_density_map_covers_exactly_the_boxes():
+    """test_raster.cpp:185-201"""
+    rng = O.Rng(45)
+    scene = rng.random_scene(5, 5)
+    cam = rng.random_camera(48, 48)
+    counts = O.density_map(scene, cam, 0.5)
+    assert counts.shape == (48, 48)
+    assert (counts == _boxes_expect(O.project_scene(scene, cam, 0.5)[0], 48, 48)).all()
+    dyn = O.density_map(scene, cam, 0.5, dynamics_only=True)
+    assert (dyn <= counts).all()
+
+
+def test_density_map_single_static():
+    """tests/python/test_smoke.py:84-96"""
+    scene = single_static_scene()
+    cam = O.look_at([0, 0, -3], [0, 0, 0], [0, -1, 0], 40.0, 24, 16)
+    total = O.density_map(scene, cam, 0.5)
+    dyn = O.density_map(scene, cam, 0.5, dynamics_only=True)
+    assert total.shape == (16, 24)
+    assert total.sum() > 0
+    assert (dyn <= total).all() and dyn.sum() == 0
+
+
 def test_range_and_finite():
     """test_raster.cpp:203-215"""
     rng = O.Rng(46)
