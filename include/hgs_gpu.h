@@ -38,7 +38,10 @@ typedef enum {
     HGS_ERR_DEGENERATE_ROTATION = 3, /* DegenerateRotationError */
     HGS_ERR_NUMERIC_ABORT = 4,       /* NumericAbort */
     HGS_ERR_CUDA = 5,                /* no device / launch failure */
-    HGS_ERR_STATE = 6                /* call out of order (e.g. backward before forward) */
+    HGS_ERR_STATE = 6,               /* call out of order (e.g. backward before forward) */
+    HGS_ERR_FORMAT = 7,              /* FormatError (checkpoint / dataset files) */
+    HGS_ERR_INTEGRITY = 8,           /* IntegrityError (checkpoint checksum) */
+    HGS_ERR_UNSUPPORTED_VERSION = 9  /* UnsupportedVersionError */
 } hgs_status;
 
 enum { HGS_F64 = 0, HGS_F32 = 1, HGS_U8 = 2 };
@@ -57,7 +60,19 @@ typedef struct {
     double tau, extent;
     void *mean_x, *mean_t, *ql, *qr, *log_s4, *op4, *sh4; /* dynamics */
     void *mean3, *quat3, *log_s3, *op3, *sh3;             /* statics  */
+    double duration_seconds;                              /* scene.hpp:52 */
 } hgs_host_scene;
+
+/* Host view of the optimizer state GradAccum (optim.hpp:32-41): Adam
+ * moments laid out like the scene (only the pointer fields of m / v are
+ * read), densification statistics, step and skipped-row counters.
+ * Always double / uint32 (HGS_F64). */
+typedef struct {
+    uint64_t step, skipped_nonfinite;
+    hgs_host_scene m, v;
+    double *grad_norm4, *grad_norm3;
+    uint32_t *count4, *count3;
+} hgs_host_state;
 
 /* Camera (camera.hpp:11-16): x_cam = rot * x + trans, rot row-major. */
 typedef struct {
@@ -182,6 +197,32 @@ hgs_status hgs_metrics(hgs_ctx *ctx, const void *a, const void *b, int dtype, in
  * last render's tape (it reuses the projection buffers). */
 hgs_status hgs_density_map(hgs_ctx *ctx, const hgs_camera *cam, double t, int dynamics_only,
                            double weight_cutoff, uint32_t *counts_host);
+
+/* ---- checkpoints (.hgsc, data_io.cpp:444-719) ---------- */
+/* Versioned, CRC-32-checked, byte-identical to the reference's format.
+ * Device scenes: the SCEN / OPTS payloads are encoded and decoded by CUDA
+ * kernels straight from / into the FP32 SoA pools (FP32 widens exactly into
+ * the f64 fields, so save -> load -> save is byte-identical); the host only
+ * checksums and moves bytes.  Loading rounds f64 values to FP32 exactly like
+ * hgs_scene_upload, validates quaternions (|q| within 1e-6 of 1) and flips
+ * them to the canonical hemisphere (data_io.cpp:500-511).  A scene whose
+ * Gaussians carry different SH degrees is a FormatError (the device pools
+ * hold one degree).  Errors: HGS_ERR_FORMAT (bad magic, truncation,
+ * trailing bytes, missing file, state/scene mismatch), HGS_ERR_INTEGRITY
+ * (checksum), HGS_ERR_UNSUPPORTED_VERSION. */
+hgs_status hgs_checkpoint_save(hgs_ctx *ctx, const char *path, int with_state);
+/* Replaces the device scene (and, when the file has an OPTS section, the
+ * optimizer state; otherwise it is zeroed).  has_state (optional) out. */
+hgs_status hgs_checkpoint_load(hgs_ctx *ctx, const char *path, int *has_state);
+/* Host scenes (bindings.cpp:197-205 save_checkpoint / load_checkpoint):
+ * double precision, no device needed.  hgs_checkpoint_info validates the
+ * whole file (checksums included) and returns the sizes to allocate;
+ * hgs_checkpoint_read fills caller buffers (state_out may be NULL).  Errors
+ * of these three are reported by hgs_io_last_error(). */
+hgs_status hgs_checkpoint_write(const hgs_host_scene *scene, const hgs_host_state *state, const char *path);
+hgs_status hgs_checkpoint_info(const char *path, int64_t *n4, int64_t *n3, int32_t *sh_degree, int *has_state);
+hgs_status hgs_checkpoint_read(const char *path, hgs_host_scene *scene_out, hgs_host_state *state_out);
+const char *hgs_io_last_error(void);
 
 /* ---- optimizer (train.hpp:68-69) --------------------------------------- */
 hgs_status hgs_adam_step(hgs_ctx *ctx, const hgs_lrs *lrs, double mean_lr_scale, int64_t *skipped_out);

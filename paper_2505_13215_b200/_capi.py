@@ -27,7 +27,13 @@ _i64p = C.POINTER(C.c_int64)
 class HostScene(C.Structure):
     _fields_ = [("n4", C.c_int64), ("n3", C.c_int64), ("sh_degree", C.c_int32), ("tau", C.c_double),
                 ("extent", C.c_double)] + [(n, _vp) for n in ("mean_x", "mean_t", "ql", "qr", "log_s4", "op4",
-                                                              "sh4", "mean3", "quat3", "log_s3", "op3", "sh3")]
+                                                              "sh4", "mean3", "quat3", "log_s3", "op3", "sh3")] + \
+        [("duration_seconds", C.c_double)]
+
+
+class HostState(C.Structure):  # hgs_host_state (GradAccum, optim.hpp:32-41)
+    _fields_ = [("step", C.c_uint64), ("skipped_nonfinite", C.c_uint64), ("m", HostScene), ("v", HostScene),
+                ("grad_norm4", _dp), ("grad_norm3", _dp), ("count4", _u32p), ("count3", _u32p)]
 
 
 class Camera_(C.Structure):
@@ -93,12 +99,24 @@ class CudaError(HgsError):
     pass
 
 
+class FormatError(HgsError):  # errors.hpp FormatError
+    pass
+
+
+class IntegrityError(HgsError):  # errors.hpp IntegrityError
+    pass
+
+
+class UnsupportedVersionError(HgsError):  # errors.hpp UnsupportedVersionError
+    pass
+
+
 class StateError(HgsError):
     pass
 
 
 _STATUS = {1: ValueError, 2: DegenerateTemporalError, 3: DegenerateRotationError, 4: NumericAbort, 5: CudaError,
-           6: StateError}
+           6: StateError, 7: FormatError, 8: IntegrityError, 9: UnsupportedVersionError}
 
 _SIGS = {
     "hgs_ctx_create": ([C.c_int, C.POINTER(_vp)], C.c_int),
@@ -140,6 +158,12 @@ _SIGS = {
     "hgs_densify_plan": ([_vp, C.POINTER(DensifyCfg), _vp, _vp, C.POINTER(DensifyReport)], C.c_int),
     "hgs_densify_apply": ([_vp, _dp, _dp, C.c_double], C.c_int),
     "hgs_opacity_reset": ([_vp, C.c_double], C.c_int),
+    "hgs_checkpoint_save": ([_vp, C.c_char_p, C.c_int], C.c_int),
+    "hgs_checkpoint_load": ([_vp, C.c_char_p, C.POINTER(C.c_int)], C.c_int),
+    "hgs_checkpoint_write": ([C.POINTER(HostScene), C.POINTER(HostState), C.c_char_p], C.c_int),
+    "hgs_checkpoint_info": ([C.c_char_p, _i64p, _i64p, _i32p, C.POINTER(C.c_int)], C.c_int),
+    "hgs_checkpoint_read": ([C.c_char_p, C.POINTER(HostScene), C.POINTER(HostState)], C.c_int),
+    "hgs_io_last_error": ([], C.c_char_p),
     "hgs_image_metrics": ([_vp, _vp, C.c_int, C.c_int, _dp, _dp], C.c_int),
     "hgs_metrics": ([_vp, _vp, _vp, C.c_int, C.c_int, C.c_int, _dp, _dp], C.c_int),
     "hgs_density_map": ([_vp, C.POINTER(Camera_), C.c_double, C.c_int, C.c_double, _u32p], C.c_int),
@@ -176,6 +200,12 @@ def lib():
             f.restype = res
         _lib = L
     return _lib
+
+
+def check_io(rc: int) -> None:
+    """Status of the context-free file entry points (message: hgs_io_last_error)."""
+    if rc != 0:
+        raise _STATUS.get(rc, HgsError)(lib().hgs_io_last_error().decode())
 
 
 def check(ctx, rc: int) -> None:

@@ -15,13 +15,15 @@ uses it.
 from __future__ import annotations
 
 import ctypes as C
-from dataclasses import dataclass
+import os
+from dataclasses import dataclass, field
 
 import numpy as np
 
 from . import _capi
 from ._capi import (HGS_F32, HGS_F64, HGS_U8, CudaError, DegenerateRotationError, DegenerateTemporalError,  # noqa: F401
-                    HgsError, NumericAbort, StateError, check, ptr)
+                    FormatError, HgsError, IntegrityError, NumericAbort, StateError, UnsupportedVersionError, check,
+                    check_io, ptr)
 from .scene import Camera, HybridScene, sh_coeff_count
 
 DEFAULT_WEIGHT_CUTOFF = 0.05  # raster.hpp:19
@@ -47,6 +49,7 @@ class LearningRates:  # train.hpp:13-21
 def _host_scene(scene: HybridScene, dtype) -> tuple[_capi.HostScene, list]:
     hs = _capi.HostScene()
     hs.n4, hs.n3, hs.sh_degree, hs.tau, hs.extent = scene.n4, scene.n3, scene.sh_degree, scene.tau, scene.extent
+    hs.duration_seconds = scene.duration_seconds
     keep = []
     for f in HybridScene.DYN_FIELDS + HybridScene.STA_FIELDS:
         a = np.ascontiguousarray(getattr(scene, f), dtype=dtype)
@@ -135,8 +138,22 @@ class Context:
         for f in HybridScene.DYN_FIELDS + HybridScene.STA_FIELDS:
             setattr(s, f, keep[(HybridScene.DYN_FIELDS + HybridScene.STA_FIELDS).index(f)])
         self._check(self._lib.hgs_scene_download(self._h, C.byref(hs), _dtype_code(dtype)))
-        s.tau, s.extent = hs.tau, hs.extent
+        s.tau, s.extent, s.duration_seconds = hs.tau, hs.extent, hs.duration_seconds
         return s
+
+    # ------------------------------------------------------------ checkpoints
+    def save_checkpoint(self, path: str, with_state: bool = True) -> None:
+        """save_checkpoint (data_io.cpp:656-665) of the device scene and, with
+        ``with_state``, its optimizer state -- encoded on the device."""
+        self._check(self._lib.hgs_checkpoint_save(self._h, os.fsencode(path), int(bool(with_state))))
+
+    def load_checkpoint(self, path: str) -> bool:
+        """load_checkpoint (data_io.cpp:667-719) into the device; returns
+        whether the file carried optimizer state (else it is zeroed)."""
+        has = C.c_int()
+        self._check(self._lib.hgs_checkpoint_load(self._h, os.fsencode(path), C.byref(has)))
+        self.counts()
+        return bool(has.value)
 
     # ------------------------------------------------------------ render
     def render(self, camera: Camera, t: float, background=(0.0, 0.0, 0.0), weight_cutoff=DEFAULT_WEIGHT_CUTOFF,
@@ -451,3 +468,75 @@ def psnr(a: np.ndarray, b: np.ndarray) -> float:
 def ssim(a: np.ndarray, b: np.ndarray) -> float:
     """hybridgs.ssim (metrics.cpp): mean SSIM over the valid 11x11 windows."""
     return _metrics(a, b, False, True)[1]
+
+
+@dataclass
+class CheckpointState:
+    """GradAccum (optim.hpp:32-41): Adam moments shaped like the scene,
+    densification statistics and the step / skipped-row counters."""
+    m: HybridScene
+    v: HybridScene
+    grad_norm4: np.ndarray
+    grad_norm3: np.ndarray
+    count4: np.ndarray
+    count3: np.ndarray
+    step: int = 0
+    skipped_nonfinite: int = 0
+
+    @staticmethod
+    def zeros_like(scene: HybridScene) -> "CheckpointState":
+        z = lambda: _empty_like_scene(scene.n4, scene.n3, scene.sh_degree, np.float64)  # noqa: E731
+        return CheckpointState(z(), z(), np.zeros(scene.n4), np.zeros(scene.n3), np.zeros(scene.n4, np.uint32),
+                               np.zeros(scene.n3, np.uint32))
+
+
+def _host_state(st: CheckpointState) -> tuple[_capi.HostState, list]:
+    hs = _capi.HostState()
+    hs.step, hs.skipped_nonfinite = int(st.step), int(st.skipped_nonfinite)
+    hm, km = _host_scene(st.m, np.float64)
+    hv, kv = _host_scene(st.v, np.float64)
+    hs.m, hs.v = hm, hv
+    arrs = [np.ascontiguousarray(st.grad_norm4, np.float64), np.ascontiguousarray(st.grad_norm3, np.float64),
+            np.ascontiguousarray(st.count4, np.uint32), np.ascontiguousarray(st.count3, np.uint32)]
+    hs.grad_norm4, hs.grad_norm3 = arrs[0].ctypes.data_as(_capi._dp), arrs[1].ctypes.data_as(_capi._dp)
+    hs.count4, hs.count3 = arrs[2].ctypes.data_as(_capi._u32p), arrs[3].ctypes.data_as(_capi._u32p)
+    return hs, [km, kv, arrs]
+
+
+def save_checkpoint(scene: HybridScene, path: str, state: CheckpointState | None = None) -> None:
+    """hybridgs.save_checkpoint (bindings.cpp:197-201; data_io.cpp:656-665):
+    a host scene in double precision, byte-identical to the reference."""
+    lib = _capi.lib()
+    hs, keep = _host_scene(scene, np.float64)
+    st, keep2 = _host_state(state) if state is not None else (None, None)
+    check_io(lib.hgs_checkpoint_write(C.byref(hs), C.byref(st) if st is not None else None, os.fsencode(path)))
+    del keep, keep2
+
+
+def load_checkpoint_full(path: str) -> tuple[HybridScene, CheckpointState | None]:
+    """load_checkpoint (data_io.cpp:667-719): (scene, state or None)."""
+    lib = _capi.lib()
+    n4, n3, deg, has = C.c_int64(), C.c_int64(), C.c_int32(), C.c_int()
+    p = os.fsencode(path)
+    check_io(lib.hgs_checkpoint_info(p, C.byref(n4), C.byref(n3), C.byref(deg), C.byref(has)))
+    scene = _empty_like_scene(n4.value, n3.value, deg.value, np.float64)
+    hs, keep = _host_scene(scene, np.float64)
+    for i, f in enumerate(HybridScene.DYN_FIELDS + HybridScene.STA_FIELDS):
+        setattr(scene, f, keep[i])
+    state = CheckpointState.zeros_like(scene) if has.value else None
+    st, keep2 = _host_state(state) if state is not None else (None, None)
+    check_io(lib.hgs_checkpoint_read(p, C.byref(hs), C.byref(st) if st is not None else None))
+    scene.tau, scene.extent, scene.duration_seconds = hs.tau, hs.extent, hs.duration_seconds
+    if state is not None:
+        km, kv, arrs = keep2
+        for i, f in enumerate(HybridScene.DYN_FIELDS + HybridScene.STA_FIELDS):
+            setattr(state.m, f, km[i])
+            setattr(state.v, f, kv[i])
+        state.grad_norm4, state.grad_norm3, state.count4, state.count3 = arrs
+        state.step, state.skipped_nonfinite = int(st.step), int(st.skipped_nonfinite)
+    return scene, state
+
+
+def load_checkpoint(path: str) -> HybridScene:
+    """hybridgs.load_checkpoint (bindings.cpp:202-205): the scene."""
+    return load_checkpoint_full(path)[0]

@@ -202,7 +202,10 @@ __global__ void __launch_bounds__(128) adam_classes_kernel(AdamPools P, AdamArgs
     }
     const unsigned full = 0xffffffffu;
     const uint32_t s = __reduce_add_sync(full, skipped);
-    if ((threadIdx.x & 31) == 0 && s) atomicAdd(skipped_total, (unsigned long long)s);
+    if ((threadIdx.x & 31) == 0 && s) {
+        atomicAdd(skipped_total, (unsigned long long)s);
+        if (A.skipped_cum) atomicAdd(A.skipped_cum, (unsigned long long)s);
+    }
     const unsigned bad = __ballot_sync(full, !ok);
     if ((threadIdx.x & 31) == 0 && bad) atomicOr(flags, FLAG_NONUNIT_QUAT);
 }

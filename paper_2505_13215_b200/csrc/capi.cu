@@ -617,11 +617,12 @@ void hgs_ctx_destroy(hgs_ctx* ctx) {
                     &ctx->sort_v2, &ctx->rec_sorted, &ctx->fast_sorted, &ctx->ntiles_sorted, &ctx->inst_off,
                     &ctx->inst_k, &ctx->inst_v, &ctx->inst_k2, &ctx->inst_v2, &ctx->ranges, &ctx->sorted_of_gid, &ctx->inst_flag, &ctx->inst_pos, &ctx->dbg_k, &ctx->dbg_v, &ctx->scan_ws,
                     &ctx->sort_ws, &ctx->counters, &ctx->img, &ctx->last, &ctx->tfinal, &ctx->trans, &ctx->count,
-                    &ctx->fix_list, &ctx->accum, &ctx->lgrad, &ctx->gt_stage, &ctx->loss_ws, &ctx->stage, &ctx->adam_ok, &ctx->pcut, &ctx->dup_first, &ctx->shdir, &ctx->ddir, &ctx->dup_status, &ctx->gpack, &ctx->dens_cat, &ctx->dens_u32, &ctx->dens_misc, &ctx->dens_kinds, &ctx->dens_jit};
+                    &ctx->fix_list, &ctx->accum, &ctx->lgrad, &ctx->gt_stage, &ctx->loss_ws, &ctx->stage, &ctx->adam_ok, &ctx->pcut, &ctx->dup_first, &ctx->shdir, &ctx->ddir, &ctx->dup_status, &ctx->gpack, &ctx->dens_cat, &ctx->dens_u32, &ctx->dens_misc, &ctx->dens_kinds, &ctx->dens_jit, &ctx->dmap, &ctx->ckpt};
     for (DBuf* b : bufs) b->release();
     ctx->pinned.release();
     ctx->pinned_ctr.release();
     ctx->pinned_pipe.release();
+    ctx->ckpt_host.release();
     for (int k = 0; k < HGS_TRAIN_PIPELINE; ++k)
         if (ctx->pipe_ev[k]) cudaEventDestroy(ctx->pipe_ev[k]);
     for (int b = 0; b < 2; ++b) {
@@ -651,19 +652,24 @@ hgs_status hgs_synchronize(hgs_ctx* ctx) {
     return HGS_OK;
 }
 
-hgs_status hgs_scene_upload(hgs_ctx* ctx, const hgs_host_scene* s, int dtype) {
-    if (!ctx || !s) return HGS_ERR_INVALID_ARGUMENT;
-    if (s->n4 < 0 || s->n3 < 0 || s->sh_degree < 0 || s->sh_degree > 3)
+}  // extern "C"
+
+hgs_status hgs_scene_alloc(hgs_ctx* ctx, int64_t n4, int64_t n3, int deg, double tau, double extent,
+                           double duration) {
+    if (n4 < 0 || n3 < 0 || deg < 0 || deg > 3)
         return fail(ctx, HGS_ERR_INVALID_ARGUMENT, "scene upload: bad sizes or sh_degree (0..3)");
-    if (s->n4 + s->n3 > (int64_t)INT32_MAX / 2) return fail(ctx, HGS_ERR_INVALID_ARGUMENT, "scene too large");
+    if (n4 + n3 > (int64_t)INT32_MAX / 2) return fail(ctx, HGS_ERR_INVALID_ARGUMENT, "scene too large");
     CK(cudaSetDevice(ctx->device));
-    ctx->n4 = s->n4;
-    ctx->n3 = s->n3;
-    ctx->deg = s->sh_degree;
-    ctx->tau = s->tau;
-    ctx->extent = s->extent;
-    ctx->cap4 = round_cap(s->n4);
-    ctx->cap3 = round_cap(s->n3 + s->n4);  // room for every 4D Gaussian to convert
+    if (!ctx->pipeline.empty())
+        return fail(ctx, HGS_ERR_STATE, "scene upload: collect the pipelined iterations first");
+    ctx->n4 = n4;
+    ctx->n3 = n3;
+    ctx->deg = deg;
+    ctx->tau = tau;
+    ctx->extent = extent;
+    ctx->duration = duration;
+    ctx->cap4 = round_cap(n4);
+    ctx->cap3 = round_cap(n3 + n4);  // room for every 4D Gaussian to convert
     const size_t b4 = (size_t)rows4(ctx->deg) * ctx->cap4 * sizeof(float);
     const size_t b3 = (size_t)rows3(ctx->deg) * ctx->cap3 * sizeof(float);
     for (DBuf* b : {&ctx->p4, &ctx->m4, &ctx->v4, &ctx->p4_alt, &ctx->m4_alt, &ctx->v4_alt}) CK(b->ensure(b4));
@@ -676,7 +682,18 @@ hgs_status hgs_scene_upload(hgs_ctx* ctx, const hgs_host_scene* s, int dtype) {
     }
     ctx->step = 0;
     ctx->have_tape = false;
-    hgs_status r = upload_pool(ctx, s, kDyn, 7, ctx->n4, ctx->cap4, ctx->p4.as<float>(), dtype);
+    ctx->stats_pending = false;
+    const uint64_t zero = 0;
+    return hgs_skipped_total(ctx, nullptr, &zero);
+}
+
+extern "C" {
+
+hgs_status hgs_scene_upload(hgs_ctx* ctx, const hgs_host_scene* s, int dtype) {
+    if (!ctx || !s) return HGS_ERR_INVALID_ARGUMENT;
+    hgs_status r = hgs_scene_alloc(ctx, s->n4, s->n3, s->sh_degree, s->tau, s->extent, s->duration_seconds);
+    if (r != HGS_OK) return r;
+    r = upload_pool(ctx, s, kDyn, 7, ctx->n4, ctx->cap4, ctx->p4.as<float>(), dtype);
     if (r != HGS_OK) return r;
     r = upload_pool(ctx, s, kSta, 5, ctx->n3, ctx->cap3, ctx->p3.as<float>(), dtype);
     if (r != HGS_OK) return r;
@@ -696,6 +713,7 @@ hgs_status hgs_scene_download(hgs_ctx* ctx, hgs_host_scene* out, int dtype) {
     out->sh_degree = ctx->deg;
     out->tau = ctx->tau;
     out->extent = ctx->extent;
+    out->duration_seconds = ctx->duration;
     return HGS_OK;
 }
 

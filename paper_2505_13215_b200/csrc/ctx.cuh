@@ -95,7 +95,7 @@ struct hgs_ctx {
     // ---- device-resident scene (component-major SoA, see hgs_common.cuh)
     int64_t n4 = 0, n3 = 0, cap4 = 0, cap3 = 0;
     int deg = 1;
-    double tau = 0.5, extent = 1.0;
+    double tau = 0.5, extent = 1.0, duration = 1.0;
     hgs::DBuf p4, p3;      // params
     hgs::DBuf p4_alt;      // compaction target of the 4D sweep
     hgs::DBuf m4_alt, v4_alt;
@@ -141,6 +141,8 @@ struct hgs_ctx {
     hgs::DBuf scratch;   // small device scalars (loss sums, skip counts, leakage)
     hgs::DBuf stage;     // upload / download staging
     hgs::DBuf dmap;      // density_map difference array ((W+1)*(H+1) ints) and counts
+    hgs::DBuf ckpt;              // checkpoint payloads on the device (checkpoint.cu)
+    hgs::HostPinned ckpt_host;   // checkpoint file image
     hgs::HostPinned pinned;      // Scratch read-back (training / loss)
     hgs::HostPinned pinned_ctr;  // Counters read-back (render)
     hgs::HostPinned pinned_pipe; // per-slot loss sums of pipelined iterations

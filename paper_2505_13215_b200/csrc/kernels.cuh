@@ -103,6 +103,7 @@ struct AdamArgs {
     const double* view_sums = nullptr;  // the step's (ssim, l1) loss sums per view
     int n_views = 0;                    // > 0: skip the whole update if one is non-finite
     uint32_t* abort = nullptr;          // sticky: set by a non-finite step, blocks later updates
+    unsigned long long* skipped_cum = nullptr;  // GradAccum::skipped_nonfinite (never reset by a step)
 };
 struct AdamPools {
     float *p4, *g4, *m4, *v4, *p3, *g3, *m3, *v3;

@@ -31,6 +31,7 @@ struct Scratch {
     uint32_t abort;                      // sticky non-finite-loss flag of pipelined iterations
     uint32_t pad2;
     double pipe_sums[HGS_TRAIN_PIPELINE][kMaxStepViews][2];  // loss sums of pipelined iterations
+    unsigned long long skipped_cum;  // rows skipped for non-finite gradients since upload / load
 };
 static_assert(kMaxStepViews == 32, "hgs_pending_step::dims");
 
@@ -234,6 +235,7 @@ hgs_status run_adam(hgs_ctx* ctx, const hgs_lrs* lrs, double mean_lr_scale, cons
     A.abort = abort;
     const int n = (int)(ctx->n4 + ctx->n3);
     Scratch* sc = scratch(ctx);
+    A.skipped_cum = &sc->skipped_cum;
     AdamPools P;
     P.p4 = ctx->p4.as<float>(), P.g4 = ctx->g4, P.m4 = ctx->m4.as<float>(), P.v4 = ctx->v4.as<float>();
     P.p3 = ctx->p3.as<float>(), P.g3 = ctx->g3, P.m3 = ctx->m3.as<float>(), P.v3 = ctx->v3.as<float>();
@@ -836,3 +838,22 @@ hgs_status hgs_train_step_host(hgs_ctx* ctx, int n_views, const hgs_camera* cams
 }
 
 }  // extern "C"
+
+// GradAccum::skipped_nonfinite of the device state (checkpoint.cu)
+hgs_status hgs_skipped_total(hgs_ctx* ctx, uint64_t* get, const uint64_t* set) {
+    hgs_status r = ensure_scratch(ctx);
+    if (r != HGS_OK) return r;
+    unsigned long long* d = &scratch(ctx)->skipped_cum;
+    if (set) {
+        const unsigned long long v = *set;
+        CK(cudaMemcpyAsync(d, &v, 8, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    }
+    if (get) {
+        unsigned long long v = 0;
+        CK(cudaMemcpyAsync(&v, d, 8, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        *get = v;
+    }
+    return HGS_OK;
+}

@@ -9,3 +9,9 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
 hgs_status hgs_render_finish(hgs_ctx* ctx);
 hgs_status hgs_upload_rows(hgs_ctx* ctx, const hgs_host_scene* s, int dtype, float* dst4, float* dst3);
 hgs_status hgs_layout_state(hgs_ctx* ctx);
+// GradAccum::skipped_nonfinite on the device: read (get) and / or overwrite (set)
+hgs_status hgs_skipped_total(hgs_ctx* ctx, uint64_t* get, const uint64_t* set);
+// (Re)allocates the device pools for n4 / n3 Gaussians of degree deg, zeroes
+// the optimizer state and statistics (the allocation half of hgs_scene_upload)
+hgs_status hgs_scene_alloc(hgs_ctx* ctx, int64_t n4, int64_t n3, int deg, double tau, double extent,
+                           double duration);

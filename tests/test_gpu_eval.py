@@ -119,7 +119,7 @@ def test_image_metrics_u8_and_device_frames(ctx):
     torch.cuda.synchronize()
     p8, s8 = ctx.image_metrics(gt_device_ptr=d8.data_ptr(), gt_u8=True)
     p32, s32 = ctx.image_metrics(gt_device_ptr=d32.data_ptr())
-    assert p8 == p and abs(s8 - s) <= 1e-12
+    assert abs(p8 - p) <= 1e-9 and abs(s8 - s) <= 1e-9  # FP64 atomics: order-dependent last ulp
     assert abs(p32 - p) <= PSNR_TOL and abs(s32 - s) <= SSIM_TOL
 
 
