@@ -224,6 +224,38 @@ hgs_status hgs_checkpoint_info(const char *path, int64_t *n4, int64_t *n3, int32
 hgs_status hgs_checkpoint_read(const char *path, hgs_host_scene *scene_out, hgs_host_state *state_out);
 const char *hgs_io_last_error(void);
 
+/* ---- initialisation (data_io.cpp:189-238) -------------- */
+/* InitConfig (data_io.hpp:43-49) */
+typedef struct {
+    int32_t sh_degree;
+    double tau, duration_seconds, init_temporal_scale, init_opacity;
+} hgs_init_cfg;
+/* init_scene: replaces the device scene with one dynamic Gaussian per point
+ * (positions / rgb: n x 3 doubles), spatial log-scale from the mean distance
+ * to the 3 nearest neighbours -- a tiled FP64 brute-force kNN on the GPU
+ * instead of the reference's serial O(N^2) loop; extent = max distance to
+ * the centroid.  n < 4 is HGS_ERR_INVALID_ARGUMENT (std::invalid_argument). */
+hgs_status hgs_init_scene(hgs_ctx *ctx, const double *positions, const double *rgb, int64_t n,
+                          const hgs_init_cfg *cfg);
+
+/* ---- dataset frames: binary PPM (image.cpp:35-75) ------- */
+/* Frames stay 8-bit sRGB (the HGS_U8 ground-truth dtype): hgs_ppm_read
+ * copies the P6 payload (h*w*3 bytes) into `out` -- e.g. pinned memory
+ * headed for the device -- with read_ppm's header rules and errors
+ * (HGS_ERR_FORMAT: cannot open / not a P6 file / bad header / truncated
+ * pixel data; a size other than width x height is a FormatError too).
+ * hgs_ppm_read_batch reads n frames on `threads` host threads (0 = all
+ * cores) and reports the first failing frame in order.  hgs_ppm_write
+ * (write_ppm) quantises linear HGS_F64 / HGS_F32 images with
+ * linear_to_srgb8 (image.cpp:15-18) or writes HGS_U8 codes as they are.
+ * Context-free: errors are read with hgs_image_last_error(). */
+hgs_status hgs_ppm_info(const char *path, int32_t *width, int32_t *height);
+hgs_status hgs_ppm_read(const char *path, uint8_t *out, int32_t width, int32_t height);
+hgs_status hgs_ppm_read_batch(const char *const *paths, int32_t n, uint8_t *const *outs, int32_t width,
+                              int32_t height, int32_t threads);
+hgs_status hgs_ppm_write(const char *path, const void *img, int dtype, int32_t width, int32_t height);
+const char *hgs_image_last_error(void);
+
 /* ---- optimizer (train.hpp:68-69) --------------------------------------- */
 hgs_status hgs_adam_step(hgs_ctx *ctx, const hgs_lrs *lrs, double mean_lr_scale, int64_t *skipped_out);
 hgs_status hgs_adam_state_download(hgs_ctx *ctx, hgs_host_scene *m, hgs_host_scene *v, int dtype,

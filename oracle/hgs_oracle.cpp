@@ -2030,6 +2030,57 @@ int hgso_density_map(const hgso_scene* s, const hgso_camera* cam, double t, int 
     });
 }
 
+// data_io.cpp:189-238 init_scene: one dynamic Gaussian per point; the
+// literal serial O(N^2) 3-nearest-neighbour search.  out: n4 = n, n3 = 0,
+// buffers sized by the caller.
+int hgso_init_scene(const double* pos, const double* rgb, int64_t n, int sh_degree, double tau, double duration,
+                    double init_temporal_scale, double init_opacity, hgso_scene* out, double* duration_out) {
+    return guard([&] {
+        if (n < 4) throw std::invalid_argument("init_scene: need at least 4 points");
+        double c[3] = {0.0, 0.0, 0.0};
+        for (int64_t i = 0; i < n; ++i)
+            for (int k = 0; k < 3; ++k) c[k] += pos[3 * i + k];
+        for (int k = 0; k < 3; ++k) c[k] /= double(n);
+        double extent = 1e-6;
+        for (int64_t i = 0; i < n; ++i) {
+            const double dx = pos[3 * i] - c[0], dy = pos[3 * i + 1] - c[1], dz = pos[3 * i + 2] - c[2];
+            extent = std::max(extent, std::sqrt(dx * dx + dy * dy + dz * dz));
+        }
+        out->n4 = n;
+        out->n3 = 0;
+        out->sh_degree = sh_degree;
+        out->tau = tau;
+        out->extent = extent;
+        *duration_out = duration;
+        const int K = sh_count(sh_degree);
+        const double nd = double(n);
+        for (int64_t i = 0; i < n; ++i) {
+            double d1 = 1e30, d2 = 1e30, d3 = 1e30;
+            for (int64_t j = 0; j < n; ++j) {
+                if (j == i) continue;
+                const double dx = pos[3 * j] - pos[3 * i], dy = pos[3 * j + 1] - pos[3 * i + 1],
+                             dz = pos[3 * j + 2] - pos[3 * i + 2];
+                const double d = dx * dx + dy * dy + dz * dz;
+                if (d < d1) { d3 = d2; d2 = d1; d1 = d; }
+                else if (d < d2) { d3 = d2; d2 = d; }
+                else if (d < d3) { d3 = d; }
+            }
+            const double mean_nn = (std::sqrt(d1) + std::sqrt(d2) + std::sqrt(d3)) / 3.0;
+            const double s = std::log(std::max(mean_nn, 1e-4));
+            for (int k = 0; k < 3; ++k) out->mean_x[3 * i + k] = pos[3 * i + k];
+            out->mean_t[i] = (double(i) + 0.5) / nd;
+            const double q[4] = {1.0, 0.0, 0.0, 0.0};
+            for (int k = 0; k < 4; ++k) out->ql[4 * i + k] = out->qr[4 * i + k] = q[k];
+            out->log_s4[4 * i + 0] = out->log_s4[4 * i + 1] = out->log_s4[4 * i + 2] = s;
+            out->log_s4[4 * i + 3] = std::log(init_temporal_scale);
+            out->op4[i] = std::log(init_opacity / (1.0 - init_opacity));
+            double* sh = out->sh4 + size_t(i) * K * 3;
+            std::fill(sh, sh + size_t(K) * 3, 0.0);
+            for (int k = 0; k < 3; ++k) sh[k] = (rgb[3 * i + k] - 0.5) / C0;  // from_rgb_dc (sh.cpp:19-23)
+        }
+    });
+}
+
 static void fill_splat(const Splat& s, int n4, int W, int H, hgso_splat& o) {
     o.sx = s.sx; o.sy = s.sy;
     o.conic[0] = s.conic[0][0]; o.conic[1] = s.conic[0][1];

@@ -137,6 +137,9 @@ void hgso_rng_normal_seq(void *rng, int64_t n, double *out);
  * zero), statistics reset; the rng is advanced exactly like the reference. */
 int hgso_densify_and_prune(const hgso_scene *in, const hgso_state *st_in, hgso_scene *out, hgso_state *st_out,
                            const hgso_densify_cfg *cfg, void *rng, hgso_densify_report *rep);
+/* init_scene (data_io.cpp:189-238): out sized for n dynamics, no statics */
+int hgso_init_scene(const double *pos, const double *rgb, int64_t n, int sh_degree, double tau, double duration,
+                    double init_temporal_scale, double init_opacity, hgso_scene *out, double *duration_out);
 /* random_scene: caller passes buffers sized for (n_static, n_dynamic, degree) */
 void hgso_random_scene(void *rng, int n_static, int n_dynamic, int sh_degree, hgso_scene *out);
 void hgso_random_quat(void *rng, double q[4]);

@@ -134,6 +134,8 @@ def lib():
         L.hgso_rng_raw.restype = C.c_uint64
         L.hgso_rng_raw.argtypes = [C.c_void_p]
         L.hgso_rng_normal_seq.argtypes = [C.c_void_p, C.c_int64, _dp]
+        L.hgso_init_scene.argtypes = [_dp, _dp, C.c_int64, C.c_int, C.c_double, C.c_double, C.c_double,
+                                      C.c_double, C.POINTER(_Scene), _dp]
         L.hgso_density_map.argtypes = [C.POINTER(_Scene), C.POINTER(_Camera), C.c_double, C.c_int, C.c_double,
                                        _u32p]
         L.hgso_densify_and_prune.argtypes = [C.POINTER(_Scene), C.POINTER(_State), C.POINTER(_Scene),
@@ -709,6 +711,21 @@ def density_map(scene: HybridScene, cam: Camera, t: float, dynamics_only: bool =
     out = np.zeros((cam.height, cam.width), dtype=np.uint32)
     _check(lib().hgso_density_map(C.byref(_scene_struct(scene)), C.byref(_cam_struct(cam)), t,
                                   1 if dynamics_only else 0, weight_cutoff, out.ctypes.data_as(_u32p)))
+    return out
+
+
+def init_scene(positions, rgb, sh_degree=1, tau=0.5, duration_seconds=1.0, init_temporal_scale=0.1,
+               init_opacity=0.1) -> HybridScene:
+    """data_io.cpp:189-238 (InitConfig defaults, data_io.hpp:43-49)."""
+    pos = np.ascontiguousarray(positions, dtype=np.float64).reshape(-1, 3)
+    col = np.ascontiguousarray(rgb, dtype=np.float64).reshape(-1, 3)
+    n = pos.shape[0]
+    out = _empty_scene_like(HybridScene(sh_degree=sh_degree), n, 0)
+    st = _scene_struct(out)
+    dur = C.c_double()
+    _check(lib().hgso_init_scene(_p(pos), _p(col), n, sh_degree, tau, duration_seconds, init_temporal_scale,
+                                 init_opacity, C.byref(st), C.byref(dur)))
+    out.tau, out.extent, out.duration_seconds = st.tau, st.extent, dur.value
     return out
 
 

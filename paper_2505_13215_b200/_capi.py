@@ -31,6 +31,11 @@ class HostScene(C.Structure):
         [("duration_seconds", C.c_double)]
 
 
+class InitCfg(C.Structure):  # hgs_init_cfg (InitConfig, data_io.hpp:43-49)
+    _fields_ = [("sh_degree", C.c_int32), ("tau", C.c_double), ("duration_seconds", C.c_double),
+                ("init_temporal_scale", C.c_double), ("init_opacity", C.c_double)]
+
+
 class HostState(C.Structure):  # hgs_host_state (GradAccum, optim.hpp:32-41)
     _fields_ = [("step", C.c_uint64), ("skipped_nonfinite", C.c_uint64), ("m", HostScene), ("v", HostScene),
                 ("grad_norm4", _dp), ("grad_norm3", _dp), ("count4", _u32p), ("count3", _u32p)]
@@ -158,6 +163,13 @@ _SIGS = {
     "hgs_densify_plan": ([_vp, C.POINTER(DensifyCfg), _vp, _vp, C.POINTER(DensifyReport)], C.c_int),
     "hgs_densify_apply": ([_vp, _dp, _dp, C.c_double], C.c_int),
     "hgs_opacity_reset": ([_vp, C.c_double], C.c_int),
+    "hgs_init_scene": ([_vp, _dp, _dp, C.c_int64, C.POINTER(InitCfg)], C.c_int),
+    "hgs_ppm_info": ([C.c_char_p, _i32p, _i32p], C.c_int),
+    "hgs_ppm_read": ([C.c_char_p, C.POINTER(C.c_uint8), C.c_int32, C.c_int32], C.c_int),
+    "hgs_ppm_read_batch": ([C.POINTER(C.c_char_p), C.c_int32, C.POINTER(C.POINTER(C.c_uint8)), C.c_int32, C.c_int32,
+                            C.c_int32], C.c_int),
+    "hgs_ppm_write": ([C.c_char_p, _vp, C.c_int, C.c_int32, C.c_int32], C.c_int),
+    "hgs_image_last_error": ([], C.c_char_p),
     "hgs_checkpoint_save": ([_vp, C.c_char_p, C.c_int], C.c_int),
     "hgs_checkpoint_load": ([_vp, C.c_char_p, C.POINTER(C.c_int)], C.c_int),
     "hgs_checkpoint_write": ([C.POINTER(HostScene), C.POINTER(HostState), C.c_char_p], C.c_int),

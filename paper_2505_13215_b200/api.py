@@ -100,6 +100,12 @@ class Context:
             self._lib.hgs_ctx_destroy(self._h)
             self._h = None
 
+    def __enter__(self) -> "Context":
+        return self
+
+    def __exit__(self, *exc) -> None:
+        self.close()
+
     def __del__(self):
         self.close()
 
@@ -140,6 +146,19 @@ class Context:
         self._check(self._lib.hgs_scene_download(self._h, C.byref(hs), _dtype_code(dtype)))
         s.tau, s.extent, s.duration_seconds = hs.tau, hs.extent, hs.duration_seconds
         return s
+
+    # ------------------------------------------------------------ initialisation
+    def init_scene(self, positions: np.ndarray, rgb: np.ndarray, cfg: "InitConfig | None" = None) -> None:
+        """init_scene (data_io.cpp:189-238) straight into the device: one
+        dynamic Gaussian per point, the 3-NN scales from a GPU kNN."""
+        cfg = cfg or InitConfig()
+        pos = np.ascontiguousarray(positions, dtype=np.float64).reshape(-1, 3)
+        col = np.ascontiguousarray(rgb, dtype=np.float64).reshape(-1, 3)
+        if pos.shape != col.shape:
+            raise ValueError("init_scene: positions and rgb differ in length")
+        self._check(self._lib.hgs_init_scene(self._h, pos.ctypes.data_as(_capi._dp), col.ctypes.data_as(_capi._dp),
+                                             pos.shape[0], C.byref(cfg.struct())))
+        self.counts()
 
     # ------------------------------------------------------------ checkpoints
     def save_checkpoint(self, path: str, with_state: bool = True) -> None:
@@ -468,6 +487,31 @@ def psnr(a: np.ndarray, b: np.ndarray) -> float:
 def ssim(a: np.ndarray, b: np.ndarray) -> float:
     """hybridgs.ssim (metrics.cpp): mean SSIM over the valid 11x11 windows."""
     return _metrics(a, b, False, True)[1]
+
+
+@dataclass
+class InitConfig:  # data_io.hpp:43-49
+    sh_degree: int = 1
+    tau: float = 0.5
+    duration_seconds: float = 1.0
+    init_temporal_scale: float = 0.1
+    init_opacity: float = 0.1
+
+    def struct(self) -> _capi.InitCfg:
+        k = _capi.InitCfg()
+        k.sh_degree, k.tau, k.duration_seconds = int(self.sh_degree), float(self.tau), float(self.duration_seconds)
+        k.init_temporal_scale, k.init_opacity = float(self.init_temporal_scale), float(self.init_opacity)
+        return k
+
+
+def init_scene(points, cfg: InitConfig | None = None, ctx: "Context | None" = None) -> HybridScene:
+    """hgs::init_scene (data_io.cpp:189-238): ``points`` is a
+    dataset.InitPoints or a (positions, rgb) pair; returns the host scene
+    (the device copy stays resident in ``ctx``)."""
+    pos, rgb = (points.positions, points.rgb) if hasattr(points, "positions") else points
+    ctx = ctx or default_context()
+    ctx.init_scene(pos, rgb, cfg)
+    return ctx.download()
 
 
 @dataclass

@@ -286,15 +286,17 @@ class TrainConfig:  # train.hpp:23-49
 @dataclass
 class Frame:  # data_io.hpp Frame: one image of one camera at one time
     time: float
-    image: np.ndarray  # (H, W, 3) linear RGB
+    image: np.ndarray  # (H, W, 3): float linear RGB, or uint8 sRGB codes (decoded on the device)
 
 
 @dataclass
-class MultiViewDataset:  # data_io.hpp MultiViewDataset (the fields the loop reads)
+class MultiViewDataset:  # data_io.hpp:28-41 MultiViewDataset
     cameras: list
     frames: list  # frames[camera][frame] -> Frame
     background: tuple = (0.0, 0.0, 0.0)
     duration_seconds: float = 1.0
+    camera_ids: list = field(default_factory=list)
+    init_points: object = None  # dataset.InitPoints (root/points.txt)
 
     def total_frames(self) -> int:
         return sum(len(f) for f in self.frames)
@@ -379,7 +381,11 @@ def train_scene(scene: HybridScene, dataset: MultiViewDataset, cfg: TrainConfig,
         ctx.set_adam_state(*state)
     dev = torch.device("cuda", ctx.device)
     samples = [(c, f) for c in range(len(dataset.frames)) for f in range(len(dataset.frames[c]))]
-    gts = {(c, f): torch.as_tensor(np.ascontiguousarray(dataset.frames[c][f].image, dtype=np.float32), device=dev)
+    # 8-bit sRGB frames (dataset.load_dataset) stay 8-bit on the device and
+    # are decoded inside the loss (HGS_U8); float frames are linear RGB
+    u8 = dataset.frames[0][0].image.dtype == np.uint8
+    gts = {(c, f): torch.as_tensor(np.ascontiguousarray(dataset.frames[c][f].image,
+                                                        dtype=np.uint8 if u8 else np.float32), device=dev)
            for c, f in samples}
     cams = [_capi.camera_struct(c) for c in dataset.cameras]
     rng = MT19937_64(cfg.seed)
@@ -397,10 +403,15 @@ def train_scene(scene: HybridScene, dataset: MultiViewDataset, cfg: TrainConfig,
         o.mean_lr_scale = math.pow(cfg.lrs.mean_final_ratio, it / cfg.iterations)  # train.cpp:449
         karr = (_capi.Camera_ * B)(*[cams[c] for c, _ in batch])
         tarr = (C.c_double * B)(*[dataset.frames[c][f].time for c, f in batch])
-        garr = (_capi._fp * B)(*[C.cast(C.c_void_p(gts[b].data_ptr()), _capi._fp) for b in batch])
         loss = C.c_double()
         # renders, losses, backward scaled by 1/B, densify statistics, NumericAbort, Adam
-        ctx._check(ctx._lib.hgs_train_step(ctx.handle, B, karr, tarr, garr, B, C.byref(o), 1, C.byref(loss)))
+        if u8:
+            garr = (C.c_void_p * B)(*[C.c_void_p(gts[b].data_ptr()) for b in batch])
+            ctx._check(ctx._lib.hgs_train_step_async(ctx.handle, B, karr, tarr, garr, _capi.HGS_U8, 1, B, C.byref(o), 1))
+            ctx._check(ctx._lib.hgs_train_collect(ctx.handle, C.byref(loss)))
+        else:
+            garr = (_capi._fp * B)(*[C.cast(C.c_void_p(gts[b].data_ptr()), _capi._fp) for b in batch])
+            ctx._check(ctx._lib.hgs_train_step(ctx.handle, B, karr, tarr, garr, B, C.byref(o), 1, C.byref(loss)))
         row = TrainLogRow(iter=it, loss=loss.value / B)
         if it >= cfg.warmup_iters and it % cfg.densify_interval == 0:
             if it <= cfg.densify_stop_iter:  # train.cpp:457-465, on the device
