@@ -360,6 +360,8 @@ def run_ours(args) -> None:
     rl = roofline(phase_ms, counts, args.steps, peak, peak_kind)
 
     extra = run_extras(args, ctx, lib, timed, world, rank) if not args.no_extras else None
+    if extra is not None and world == 1:
+        extra["rows_8f"] = run_rows(ctx)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -446,6 +448,91 @@ def run_extras(args, ctx, lib, timed, world, rank) -> dict:
                        "ms_per_step": round(ms / k, 4), "views_per_step_per_gpu": per,
                        "config": "1600k 4D + 400k 3D, SH 3, 1352x1014, 8 views/GPU/step"}
     torch.cuda.synchronize()
+    return out
+
+
+def run_rows(ctx) -> dict:
+    """The SURVEY.md 8f rows, each through its public API call at c2 scale
+    (host-synchronous calls: wall time around the call, synchronised on both
+    sides -- these are end-to-end numbers including their host work)."""
+    import tempfile
+
+    import torch
+
+    from paper_2505_13215_b200 import api as A
+    from paper_2505_13215_b200 import dataset as D
+    from paper_2505_13215_b200.rng import MT19937_64
+    from paper_2505_13215_b200.scene import CONFIGS, ring_camera, synthetic_scene
+    from paper_2505_13215_b200.train import DeviceTrainer
+
+    def wall(fn):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = fn()
+        torch.cuda.synchronize()
+        return (time.perf_counter() - t0) * 1e3, r
+
+    out = {}
+    c = CONFIGS["c2"]
+    scene = synthetic_scene(c["n4"], c["n3"], 3, seed=c["seed"], tau=0.5)
+    target = synthetic_scene(c["n4"], c["n3"], 3, seed=c["seed"] + 1000, tau=0.5)
+    cams = [ring_camera(c["seed"], c["width"], c["height"], index=i, n_ring=16) for i in range(16)]
+    times = [i / 15.0 for i in range(16)]
+    tr = DeviceTrainer(ctx, scene, cams, times, target=target, bg=(0.2, 0.2, 0.2), iterations=1000, gt_format="u8")
+    del target
+    for i in range(8):
+        tr.step([(2 * i) % 16, (2 * i + 1) % 16])
+    n_before = sum(ctx.counts())
+    gn4, c4, gn3, c3 = ctx.densify_stats()
+    avg = np.concatenate([gn4 / np.maximum(c4, 1), gn3 / np.maximum(c3, 1)])
+    thr = float(np.quantile(avg[avg > 0], 0.98)) if (avg > 0).any() else 0.02  # ~2% of the observed densify
+    ms, rep = wall(lambda: ctx.densify_and_prune(MT19937_64(7), grad_threshold=thr, max_gaussians=1_000_000))
+    out["densify_and_prune"] = {"ms": round(ms, 3), "gaussians_before": n_before, "gaussians_after": sum(ctx.counts()),
+                                "report": rep, "grad_threshold": thr,
+                                "what": "hgs_densify_plan + host normal replay + hgs_densify_apply"}
+    frames = [t.cpu().numpy() for t in tr.gt]  # host u8 sRGB frames
+    for v in range(2):
+        ctx.render_device(cams[v], times[v], (0.2, 0.2, 0.2))
+        ctx.image_metrics(frames[v])
+
+    def evaluate():
+        for v in range(16):
+            ctx.render_device(cams[v], times[v], (0.2, 0.2, 0.2))
+            ctx.image_metrics(frames[v])
+
+    ms, _ = wall(evaluate)
+    out["evaluate_views"] = {"value": round(16 / (ms / 1e3), 2), "unit": "views/s", "ms_per_view": round(ms / 16, 4),
+                             "what": "render (no download) + PSNR + SSIM vs a host u8 frame, c2 scene 1352x1014"}
+    ctx.density_map(cams[0], 0.5)
+    ms, _ = wall(lambda: [ctx.density_map(cams[v], times[v]) for v in range(8)])
+    out["density_map"] = {"ms_per_map": round(ms / 8, 4), "what": "c2 scene, 1352x1014 counts downloaded"}
+    with tempfile.TemporaryDirectory() as d:
+        p = os.path.join(d, "c2.hgsc")
+        ctx.save_checkpoint(p)
+        ms_s, _ = wall(lambda: ctx.save_checkpoint(p))
+        size = os.path.getsize(p)
+        ms_l, _ = wall(lambda: ctx.load_checkpoint(p))
+        out["checkpoint"] = {"bytes": size, "save_ms": round(ms_s, 2), "load_ms": round(ms_l, 2),
+                             "save_GBps": round(size / ms_s / 1e6, 2), "load_GBps": round(size / ms_l / 1e6, 2),
+                             "what": "device scene + optimizer state <-> .hgsc file (page cache), CRC-32 included"}
+        w, h = c["width"], c["height"]
+        rng = np.random.default_rng(0)
+        paths = []
+        for i in range(32):
+            paths.append(os.path.join(d, f"f{i}.ppm"))
+            D.write_ppm(rng.integers(0, 256, (h, w, 3), dtype=np.uint8), paths[-1])
+        buf = torch.empty((32, h, w, 3), dtype=torch.uint8).pin_memory().numpy()
+        D.read_ppm_batch(paths, w, h, out=buf)
+        ms, _ = wall(lambda: D.read_ppm_batch(paths, w, h, out=buf))
+        out["ppm_read_batch"] = {"value": round(32 / (ms / 1e3), 1), "unit": "frames/s",
+                                 "GBps": round(32 * w * h * 3 / ms / 1e6, 2),
+                                 "what": "32 P6 frames 1352x1014 (page cache) -> pinned u8 array, all host threads"}
+    rng = np.random.default_rng(1)
+    pos, col = rng.uniform(-3, 3, (100_000, 3)), rng.uniform(0, 1, (100_000, 3))
+    ctx.init_scene(pos[:1000], col[:1000])
+    ms, _ = wall(lambda: ctx.init_scene(pos, col, A.InitConfig(sh_degree=3)))
+    out["init_scene"] = {"ms": round(ms, 2), "points": 100_000, "pairs_per_s": round(1e5 * 1e5 / (ms / 1e3), 1),
+                         "what": "FP64 brute-force 3-NN over 100k points + field init (data_io.cpp:189-238)"}
     return out
 
 

@@ -10,12 +10,18 @@
 // The SoA row order of both pools equals the field order of a checkpoint
 // record (hgs_common.cuh R3_* / R4_*): a record is rows [0, pre) as f64, the
 // u32 SH degree, rows [pre, rows) as f64 (pre = R3_SH / R4_SH).
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
 #include <zlib.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "kernels.cuh"
@@ -183,6 +189,45 @@ __global__ void decode_stats_kernel(const double* __restrict__ gn_in, const uint
     dcnt[i] = 0.f;
 }
 
+// CRC-32 (zlib / IEEE 802.3, reflected 0xEDB88320) of every kCrcChunk-byte
+// chunk of [data, data+n), slicing-by-8 from shared-memory tables; the host
+// folds the chunk CRCs with zlib's crc32_combine_op.  data is 8-byte aligned.
+constexpr uint32_t kCrcChunk = 16384;
+
+__global__ void __launch_bounds__(256) crc32_chunks_kernel(const uint8_t* __restrict__ data, uint64_t n,
+                                                           const uint32_t* __restrict__ tables,
+                                                           uint32_t* __restrict__ out, uint64_t nchunks) {
+    __shared__ uint32_t T[8][256];
+    for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) T[i >> 8][i & 255] = tables[i];
+    __syncthreads();
+    const uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= nchunks) return;
+    const uint64_t b0 = c * kCrcChunk, b1 = min(n, b0 + kCrcChunk);
+    uint32_t crc = 0xFFFFFFFFu;
+    uint64_t p = b0;
+    for (; p + 8 <= b1; p += 8) {
+        const uint2 w = *reinterpret_cast<const uint2*>(data + p);
+        const uint32_t lo = w.x ^ crc, hi = w.y;
+        crc = T[7][lo & 255] ^ T[6][(lo >> 8) & 255] ^ T[5][(lo >> 16) & 255] ^ T[4][lo >> 24] ^ T[3][hi & 255] ^
+              T[2][(hi >> 8) & 255] ^ T[1][(hi >> 16) & 255] ^ T[0][hi >> 24];
+    }
+    for (; p < b1; ++p) crc = T[0][(crc ^ data[p]) & 255] ^ (crc >> 8);
+    out[c] = crc ^ 0xFFFFFFFFu;
+}
+
+// header scalars of a payload (4- or 8-byte values at 4-aligned offsets)
+struct Patch {
+    uint64_t off, val;
+    uint32_t bytes, pad;
+};
+__global__ void patch_kernel(uint8_t* __restrict__ base, const Patch* __restrict__ p, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uint32_t* w = reinterpret_cast<uint32_t*>(base + p[i].off);
+    w[0] = (uint32_t)p[i].val;
+    if (p[i].bytes == 8) w[1] = (uint32_t)(p[i].val >> 32);
+}
+
 // ------------------------------------------------------------ host layout
 
 struct PoolDesc {
@@ -293,6 +338,118 @@ bool write_file(const char* path, const uint8_t* p, size_t n, IoError& e) {
     return ok;
 }
 
+const uint32_t* crc_tables_host() {
+    static uint32_t T[8][256];
+    static bool init = false;
+    if (!init) {
+        for (uint32_t i = 0; i < 256; ++i) {
+            uint32_t c = i;
+            for (int k = 0; k < 8; ++k) c = (c & 1) ? 0xEDB88320u ^ (c >> 1) : c >> 1;
+            T[0][i] = c;
+        }
+        for (int t = 1; t < 8; ++t)
+            for (int i = 0; i < 256; ++i) T[t][i] = (T[t - 1][i] >> 8) ^ T[0][T[t - 1][i] & 255];
+        init = true;
+    }
+    return &T[0][0];
+}
+
+uint64_t crc_chunks(uint64_t n) { return (n + kCrcChunk - 1) / kCrcChunk; }
+
+uint32_t crc_combine_chunks(const uint32_t* c, uint64_t n) {
+    const uint64_t nch = crc_chunks(n);
+    if (nch == 0) return 0u;  // crc32 of the empty string
+    const uLong op = crc32_combine_gen((z_off_t)kCrcChunk);
+    uLong crc = c[0];
+    for (uint64_t i = 1; i < nch; ++i) {
+        const uint64_t len = std::min<uint64_t>(kCrcChunk, n - i * kCrcChunk);
+        crc = len == kCrcChunk ? crc32_combine_op(crc, c[i], op) : crc32_combine(crc, c[i], (z_off_t)len);
+    }
+    return (uint32_t)crc;
+}
+
+void scen_patches(std::vector<Patch>& v, uint32_t deg, double tau, double dur, double ext, uint64_t n3, uint64_t n4) {
+    auto bits = [](double x) {
+        uint64_t b;
+        std::memcpy(&b, &x, 8);
+        return b;
+    };
+    v.push_back({0, deg, 4, 0});
+    v.push_back({4, bits(tau), 8, 0});
+    v.push_back({12, bits(dur), 8, 0});
+    v.push_back({20, bits(ext), 8, 0});
+    v.push_back({28, n3, 8, 0});
+    v.push_back({36, n4, 8, 0});
+}
+
+void opts_patches(std::vector<Patch>& v, uint64_t base, const OptsLayout& L, uint64_t step, uint64_t skipped) {
+    v.push_back({base, step, 8, 0});
+    v.push_back({base + 8, skipped, 8, 0});
+    for (int c = 0; c < 12; ++c) {
+        v.push_back({base + L.m[c] - 8, L.n[c], 8, 0});
+        v.push_back({base + L.v[c] - 8, L.n[c], 8, 0});
+    }
+    v.push_back({base + L.gn3 - 8, L.n3, 8, 0});
+    v.push_back({base + L.gn4 - 8, L.n4, 8, 0});
+    v.push_back({base + L.c3 - 8, L.n3, 8, 0});
+    v.push_back({base + L.c4 - 8, L.n4, 8, 0});
+}
+
+int io_threads(uint64_t n) {
+    if (n < (16ull << 20)) return 1;
+    const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
+    return std::min(8, hw);
+}
+
+// the file through a shared mapping filled by `io_threads` threads (buffered
+// write() calls to one file serialise on its inode lock; page faults on a
+// mapping do not), else concurrent pwrite ranges
+bool pwrite_file(const char* path, const uint8_t* p, uint64_t n, IoError& e) {
+    const int fd = ::open(path, O_RDWR | O_CREAT | O_TRUNC, 0644);
+    if (fd < 0) {
+        e = {HGS_ERR_FORMAT, std::string("save_checkpoint: cannot open ") + path};
+        return false;
+    }
+    const int T = io_threads(n);
+    if (T > 1 && ::ftruncate(fd, (off_t)n) == 0) {
+        void* m = ::mmap(nullptr, (size_t)n, PROT_WRITE, MAP_SHARED, fd, 0);
+        if (m != MAP_FAILED) {
+            const uint64_t part = ((n / T) + 4095) & ~4095ull;
+            auto copy = [&](int t) {
+                const uint64_t a = std::min(n, (uint64_t)t * part), b = std::min(n, a + part);
+                std::memcpy(static_cast<uint8_t*>(m) + a, p + a, (size_t)(b - a));
+            };
+            std::vector<std::thread> th;
+            for (int t = 1; t < T; ++t) th.emplace_back(copy, t);
+            copy(0);
+            for (auto& x : th) x.join();
+            const bool good = ::munmap(m, (size_t)n) == 0 && ::close(fd) == 0;
+            if (!good) e = {HGS_ERR_FORMAT, std::string("save_checkpoint: write failed for ") + path};
+            return good;
+        }
+    }
+    const uint64_t part = ((n / T) + 4095) & ~4095ull;
+    std::vector<char> ok((size_t)T, 1);
+    auto work = [&](int t) {
+        uint64_t a = (uint64_t)t * part, b = std::min(n, a + part);
+        while (a < b) {
+            const ssize_t w = ::pwrite(fd, p + a, (size_t)std::min<uint64_t>(b - a, 1ull << 30), (off_t)a);
+            if (w <= 0) {
+                ok[(size_t)t] = 0;
+                return;
+            }
+            a += (uint64_t)w;
+        }
+    };
+    std::vector<std::thread> th;
+    for (int t = 1; t < T; ++t) th.emplace_back(work, t);
+    work(0);
+    for (auto& x : th) x.join();
+    const bool good = ::close(fd) == 0 && std::all_of(ok.begin(), ok.end(), [](char c) { return c != 0; });
+    if (!good) e = {HGS_ERR_FORMAT, std::string("save_checkpoint: write failed for ") + path};
+    return good;
+}
+
 // ---------------------------------------------------------------- parsing
 
 struct Parsed {
@@ -310,8 +467,18 @@ struct Parsed {
     OptsLayout L;
 };
 
-bool parse_file(const uint8_t* b, uint64_t n, const std::string& path, Parsed& P, IoError& e) {
-    // data_io.cpp:667-704
+struct Sec {
+    const uint8_t* tag;
+    const uint8_t* p;
+    uint64_t len;
+    uint32_t crc;
+};
+
+// data_io.cpp:667-704, structure only: magic, version and every complete
+// section header + payload in order.  Returns false (e set) at the first
+// structural error; `secs` then holds the complete sections before it (the
+// reference checks their checksums before it reaches the error).
+bool walk_sections(const uint8_t* b, uint64_t n, const std::string& path, std::vector<Sec>& secs, IoError& e) {
     if (n < 4 || std::memcmp(b, "HGSC", 4) != 0) {
         e = {HGS_ERR_FORMAT, "load_checkpoint: bad magic in " + path};
         return false;
@@ -331,24 +498,28 @@ bool parse_file(const uint8_t* b, uint64_t n, const std::string& path, Parsed& P
             e = {HGS_ERR_FORMAT, "load_checkpoint: truncated section header in " + path};
             return false;
         }
-        const uint8_t* tag = b + off;
-        const uint64_t len = get<uint64_t>(b + off + 4);
-        const uint32_t crc = get<uint32_t>(b + off + 12);
+        Sec s{b + off, nullptr, get<uint64_t>(b + off + 4), get<uint32_t>(b + off + 12)};
         off += 16;
-        if (len > n - off) {
+        if (s.len > n - off) {
             e = {HGS_ERR_FORMAT, "load_checkpoint: truncated section payload in " + path};
             return false;
         }
-        if (crc_of(b + off, len) != crc) {
-            e = {HGS_ERR_INTEGRITY, "load_checkpoint: checksum mismatch in " + path};
-            return false;
+        s.p = b + off;
+        secs.push_back(s);
+        off += s.len;
+    }
+    return true;
+}
+
+// the scene / state sections (the last of each tag wins; unknown tags are
+// skipped) and their contents
+bool parse_sections(const std::vector<Sec>& secs, const std::string& path, Parsed& P, IoError& e) {
+    for (const Sec& s : secs) {
+        if (std::memcmp(s.tag, "SCEN", 4) == 0) {
+            P.scen = s.p, P.scen_len = s.len, P.has_scen = true;
+        } else if (std::memcmp(s.tag, "OPTS", 4) == 0) {
+            P.opts = s.p, P.opts_len = s.len, P.has_opts = true;
         }
-        if (std::memcmp(tag, "SCEN", 4) == 0) {
-            P.scen = b + off, P.scen_len = len, P.has_scen = true;
-        } else if (std::memcmp(tag, "OPTS", 4) == 0) {
-            P.opts = b + off, P.opts_len = len, P.has_opts = true;
-        }  // unknown tags with valid checksums are skipped
-        off += len;
     }
     if (!P.has_scen) {
         e = {HGS_ERR_FORMAT, "load_checkpoint: no scene section in " + path};
@@ -439,6 +610,23 @@ bool parse_file(const uint8_t* b, uint64_t n, const std::string& path, Parsed& P
     return true;
 }
 
+// the whole load check with host checksums (zlib), in the reference's order
+bool parse_file(const uint8_t* b, uint64_t n, const std::string& path, Parsed& P, IoError& e) {
+    std::vector<Sec> secs;
+    IoError walk_err;
+    const bool walked = walk_sections(b, n, path, secs, walk_err);
+    for (const Sec& s : secs)
+        if (crc_of(s.p, s.len) != s.crc) {
+            e = {HGS_ERR_INTEGRITY, "load_checkpoint: checksum mismatch in " + path};
+            return false;
+        }
+    if (!walked) {
+        e = walk_err;
+        return false;
+    }
+    return parse_sections(secs, path, P, e);
+}
+
 bool read_whole(const char* path, std::vector<uint8_t>& buf, IoError& e) {
     FILE* f = path ? std::fopen(path, "rb") : nullptr;
     if (!f) {
@@ -496,6 +684,21 @@ void host_fields(const hgs_host_scene* s, bool dyn, int K3, HostPool& P) {
 
 }  // namespace
 
+// chunk CRCs of [p, p+n) on the context stream (tables uploaded once)
+hgs_status crc_launch(hgs_ctx* ctx, const uint8_t* p, uint64_t n, uint32_t* out) {
+    const uint64_t nch = crc_chunks(n);
+    if (!nch) return HGS_OK;
+    if (!ctx->crc_tab.p) {
+        CKC(ctx->crc_tab.ensure(8 * 256 * 4));
+        CKC(cudaMemcpy(ctx->crc_tab.p, crc_tables_host(), 8 * 256 * 4, cudaMemcpyHostToDevice));
+    }
+    crc32_chunks_kernel<<<(unsigned)((nch + 255) / 256), 256, 0, ctx->stream>>>(p, n, ctx->crc_tab.as<uint32_t>(), out,
+                                                                              nch);
+    count_launch();
+    CKL();
+    return HGS_OK;
+}
+
 extern "C" {
 
 const char* hgs_io_last_error(void) { return g_io_err.c_str(); }
@@ -522,7 +725,11 @@ hgs_status hgs_checkpoint_save(hgs_ctx* ctx, const char* path, int with_state) {
         hgs_status r = hgs_skipped_total(ctx, &skipped, nullptr);
         if (r != HGS_OK) return r;
     }
-    CKC(ctx->ckpt.ensure(dev_opts + opts_len + 256));
+    const uint64_t nch_s = crc_chunks(scen_len), nch_o = crc_chunks(opts_len);
+    const uint64_t dev_crc = (dev_opts + opts_len + 255) & ~255ull;
+    const uint64_t dev_patch = (dev_crc + 4 * (nch_s + nch_o) + 255) & ~255ull;
+    constexpr int kMaxPatches = 64;
+    CKC(ctx->ckpt.ensure(dev_patch + kMaxPatches * sizeof(Patch)));
     uint8_t* d = ctx->ckpt.as<uint8_t>();
     const int nthr = 256;
     auto launch_records = [&](const float* src, int64_t cap, uint64_t n, const PoolDesc& p, uint64_t off) {
@@ -567,23 +774,38 @@ hgs_status hgs_checkpoint_save(hgs_ctx* ctx, const char* path, int with_state) {
         }
         CKL();
     }
-    CKC(ctx->ckpt_host.ensure(file_len));
+    // header scalars written into the device payloads, then the CRC-32 of
+    // both sections on the device (chunk CRCs, folded on the host)
+    const uint64_t h_crc = (file_len + 255) & ~255ull;
+    const uint64_t h_patch = (h_crc + 4 * (nch_s + nch_o) + 255) & ~255ull;
+    CKC(ctx->ckpt_host.ensure(h_patch + kMaxPatches * sizeof(Patch)));
     uint8_t* h = static_cast<uint8_t*>(ctx->ckpt_host.p);
+    std::vector<Patch> patches;
+    scen_patches(patches, (uint32_t)deg, ctx->tau, ctx->duration, ctx->extent, n3, n4);
+    if (with_state) opts_patches(patches, dev_opts, L, ctx->step, skipped);
+    std::memcpy(h + h_patch, patches.data(), patches.size() * sizeof(Patch));
+    CKC(cudaMemcpyAsync(d + dev_patch, h + h_patch, patches.size() * sizeof(Patch), cudaMemcpyHostToDevice, st));
+    patch_kernel<<<1, kMaxPatches, 0, st>>>(d, reinterpret_cast<const Patch*>(d + dev_patch), (int)patches.size());
+    count_launch();
+    hgs_status r = crc_launch(ctx, d, scen_len, reinterpret_cast<uint32_t*>(d + dev_crc));
+    if (r != HGS_OK) return r;
+    if (with_state) {
+        r = crc_launch(ctx, d + dev_opts, opts_len, reinterpret_cast<uint32_t*>(d + dev_crc) + nch_s);
+        if (r != HGS_OK) return r;
+    }
     uint8_t* hs = h + 24;
     uint8_t* ho = hs + scen_len + 16;
     CKC(cudaMemcpyAsync(hs, d, scen_len, cudaMemcpyDeviceToHost, st));
     if (with_state && opts_len) CKC(cudaMemcpyAsync(ho, d + dev_opts, opts_len, cudaMemcpyDeviceToHost, st));
+    CKC(cudaMemcpyAsync(h + h_crc, d + dev_crc, 4 * (nch_s + nch_o), cudaMemcpyDeviceToHost, st));
     CKC(cudaStreamSynchronize(st));
+    const uint32_t* hc = reinterpret_cast<const uint32_t*>(h + h_crc);
     std::memcpy(h, "HGSC", 4);
     put<uint32_t>(h + 4, kVersion);
-    put_scen_header(hs, (uint32_t)deg, ctx->tau, ctx->duration, ctx->extent, n3, n4);
-    put_section_header(h + 8, "SCEN", scen_len, crc_of(hs, scen_len));
-    if (with_state) {
-        put_opts_header(ho, L, ctx->step, skipped);
-        put_section_header(ho - 16, "OPTS", opts_len, crc_of(ho, opts_len));
-    }
+    put_section_header(h + 8, "SCEN", scen_len, crc_combine_chunks(hc, scen_len));
+    if (with_state) put_section_header(ho - 16, "OPTS", opts_len, crc_combine_chunks(hc + nch_s, opts_len));
     IoError e;
-    if (!write_file(path, h, file_len, e)) return ctx_fail(ctx, e);
+    if (!pwrite_file(path, h, file_len, e)) return ctx_fail(ctx, e);
     return HGS_OK;
 }
 
@@ -592,35 +814,83 @@ hgs_status hgs_checkpoint_load(hgs_ctx* ctx, const char* path, int* has_state) {
     if (!ctx || !path) return HGS_ERR_INVALID_ARGUMENT;
     CKC(cudaSetDevice(ctx->device));
     IoError e;
-    FILE* f = std::fopen(path, "rb");
-    if (!f) return ctx_fail(ctx, {HGS_ERR_FORMAT, std::string("load_checkpoint: cannot open ") + path});
-    std::fseek(f, 0, SEEK_END);
-    const long sz = std::ftell(f);
-    std::fseek(f, 0, SEEK_SET);
-    const uint64_t n = sz > 0 ? (uint64_t)sz : 0;
-    if (cudaError_t ce = ctx->ckpt_host.ensure(n + 16); ce != cudaSuccess) {
-        std::fclose(f);
+    // the file into pinned memory (concurrent pread ranges)
+    const int fd = ::open(path, O_RDONLY);
+    if (fd < 0) return ctx_fail(ctx, {HGS_ERR_FORMAT, std::string("load_checkpoint: cannot open ") + path});
+    struct stat sb;
+    const uint64_t n = ::fstat(fd, &sb) == 0 && sb.st_size > 0 ? (uint64_t)sb.st_size : 0;
+    const uint64_t nch_max = 2 * crc_chunks(n) + 2;
+    const uint64_t h_crc = (n + 255) & ~255ull;
+    if (cudaError_t ce = ctx->ckpt_host.ensure(h_crc + 4 * nch_max); ce != cudaSuccess) {
+        ::close(fd);
         CKC(ce);
     }
     uint8_t* h = static_cast<uint8_t*>(ctx->ckpt_host.p);
-    const size_t got = n ? std::fread(h, 1, n, f) : 0;
-    std::fclose(f);
-    if (got != n) return ctx_fail(ctx, {HGS_ERR_FORMAT, std::string("load_checkpoint: read failed for ") + path});
-    Parsed P;
-    if (!parse_file(h, n, path, P, e)) return ctx_fail(ctx, e);
-    // replace the device scene (zeroed optimizer state and statistics)
-    hgs_status r = hgs_scene_alloc(ctx, (int64_t)P.n4, (int64_t)P.n3, (int)P.deg, P.tau, P.ext, P.dur);
-    if (r != HGS_OK) return r;
+    {
+        const int T = io_threads(n);
+        const uint64_t part = ((n / T) + 4095) & ~4095ull;
+        std::vector<char> ok((size_t)T, 1);
+        auto work = [&](int t) {
+            uint64_t a = (uint64_t)t * part, b = std::min(n, a + part);
+            while (a < b) {
+                const ssize_t got = ::pread(fd, h + a, (size_t)std::min<uint64_t>(b - a, 1ull << 30), (off_t)a);
+                if (got <= 0) {
+                    ok[(size_t)t] = 0;
+                    return;
+                }
+                a += (uint64_t)got;
+            }
+        };
+        std::vector<std::thread> th;
+        for (int t = 1; t < T; ++t) th.emplace_back(work, t);
+        work(0);
+        for (auto& x : th) x.join();
+        ::close(fd);
+        if (!std::all_of(ok.begin(), ok.end(), [](char c) { return c != 0; }))
+            return ctx_fail(ctx, {HGS_ERR_FORMAT, std::string("load_checkpoint: read failed for ") + path});
+    }
+    std::vector<Sec> secs;
+    IoError walk_err;
+    const bool walked = walk_sections(h, n, path, secs, walk_err);
+    // the sections the device decodes (the last of each tag) are checksummed
+    // on the device after their upload, every other one on the host
+    int is = -1, io = -1;
+    for (int i = 0; i < (int)secs.size(); ++i) {
+        if (std::memcmp(secs[i].tag, "SCEN", 4) == 0) is = i;
+        if (std::memcmp(secs[i].tag, "OPTS", 4) == 0) io = i;
+    }
     cudaStream_t st = ctx->stream;
-    const uint64_t dev_opts = (P.scen_len + 255) & ~255ull;
-    const uint64_t opts_len = P.has_opts ? P.opts_len : 0;
-    CKC(ctx->ckpt.ensure(dev_opts + opts_len + 256));
+    const uint64_t scen_len = is >= 0 ? secs[is].len : 0, opts_len = io >= 0 ? secs[io].len : 0;
+    const uint64_t dev_opts = (scen_len + 255) & ~255ull;
+    const uint64_t nch_s = crc_chunks(scen_len), nch_o = crc_chunks(opts_len);
+    const uint64_t dev_crc = (dev_opts + opts_len + 255) & ~255ull;
+    CKC(ctx->ckpt.ensure(dev_crc + 4 * (nch_s + nch_o) + 256));
+    uint8_t* d = ctx->ckpt.as<uint8_t>();
+    if (scen_len) CKC(cudaMemcpyAsync(d, secs[is].p, scen_len, cudaMemcpyHostToDevice, st));
+    if (opts_len) CKC(cudaMemcpyAsync(d + dev_opts, secs[io].p, opts_len, cudaMemcpyHostToDevice, st));
+    hgs_status r = crc_launch(ctx, d, scen_len, reinterpret_cast<uint32_t*>(d + dev_crc));
+    if (r != HGS_OK) return r;
+    r = crc_launch(ctx, d + dev_opts, opts_len, reinterpret_cast<uint32_t*>(d + dev_crc) + nch_s);
+    if (r != HGS_OK) return r;
+    uint32_t* hc = reinterpret_cast<uint32_t*>(h + h_crc);
+    if (nch_s + nch_o) CKC(cudaMemcpyAsync(hc, d + dev_crc, 4 * (nch_s + nch_o), cudaMemcpyDeviceToHost, st));
+    CKC(cudaStreamSynchronize(st));
+    for (int i = 0; i < (int)secs.size(); ++i) {  // in file order, like the reference
+        const uint32_t crc = i == is   ? crc_combine_chunks(hc, scen_len)
+                             : i == io ? crc_combine_chunks(hc + nch_s, opts_len)
+                                       : crc_of(secs[i].p, secs[i].len);
+        if (crc != secs[i].crc)
+            return ctx_fail(ctx, {HGS_ERR_INTEGRITY, std::string("load_checkpoint: checksum mismatch in ") + path});
+    }
+    if (!walked) return ctx_fail(ctx, walk_err);
+    Parsed P;
+    if (!parse_sections(secs, path, P, e)) return ctx_fail(ctx, e);
+    // replace the device scene (zeroed optimizer state and statistics)
+    r = hgs_scene_alloc(ctx, (int64_t)P.n4, (int64_t)P.n3, (int)P.deg, P.tau, P.ext, P.dur);
+    if (r != HGS_OK) return r;
     CKC(ctx->counters.ensure(sizeof(Counters)));
     uint32_t* dflags = &ctx->counters.as<Counters>()->flags;
     CKC(cudaMemsetAsync(dflags, 0, 4, st));
-    uint8_t* d = ctx->ckpt.as<uint8_t>();
-    CKC(cudaMemcpyAsync(d, P.scen, P.scen_len, cudaMemcpyHostToDevice, st));
-    if (opts_len) CKC(cudaMemcpyAsync(d + dev_opts, P.opts, opts_len, cudaMemcpyHostToDevice, st));
     const int deg = (int)P.deg, K3 = 3 * sh_count(deg);
     const PoolDesc P3 = pool3(deg), P4 = pool4(deg);
     auto launch_records = [&](float* dst, int64_t cap, uint64_t cnt, const PoolDesc& p, uint64_t off, int nq, int q0,

@@ -142,6 +142,7 @@ struct hgs_ctx {
     hgs::DBuf stage;     // upload / download staging
     hgs::DBuf dmap;      // density_map difference array ((W+1)*(H+1) ints) and counts
     hgs::DBuf ckpt;              // checkpoint payloads on the device (checkpoint.cu)
+    hgs::DBuf crc_tab;           // CRC-32 slicing tables (checkpoint.cu)
     hgs::HostPinned ckpt_host;   // checkpoint file image
     hgs::HostPinned pinned;      // Scratch read-back (training / loss)
     hgs::HostPinned pinned_ctr;  // Counters read-back (render)
