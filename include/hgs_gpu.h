@@ -170,6 +170,35 @@ hgs_status hgs_grads_device(hgs_ctx *ctx, float **ptr, int64_t *count);
  * buffer (reduced in place by the caller, e.g. ncclAllReduce) back. */
 hgs_status hgs_grads_packed(hgs_ctx *ctx, int unpack, float **ptr, int64_t *count);
 
+/* ---- multi-GPU exchange -------------------------------- */
+/* View-parallel data parallelism: each rank renders its views with
+ * apply_adam = 0, hgs_allreduce_grads sums the packed payload (gradient rows
+ * + densify-statistic deltas) over the ranks with ncclAllReduce on the
+ * context stream, then every rank runs the same hgs_adam_step.  NCCL is
+ * loaded at run time (libnccl.so.2; an already-loaded copy is shared).
+ *   hgs_comm_unique_id  -- on one rank; ship the 128 bytes out of band
+ *   hgs_comm_init       -- one process per GPU (ncclCommInitRank)
+ *   hgs_comm_init_all   -- one process driving n contexts (ncclCommInitAll)
+ *   hgs_allreduce_f64   -- sum of n host doubles over the ranks (the batch
+ *                          loss: every rank raises NumericAbort together)
+ *   hgs_param_checksum  -- order-independent 64-bit checksum of the
+ *                          parameters (replica-consistency check)
+ *   hgs_broadcast_params -- parameters, Adam moments and statistics from
+ *                          `root` (repairs diverged replicas) */
+typedef struct {
+    char internal[128];
+} hgs_comm_id;
+hgs_status hgs_comm_unique_id(hgs_comm_id *out);
+hgs_status hgs_comm_init(hgs_ctx *ctx, int nranks, int rank, const hgs_comm_id *id);
+hgs_status hgs_comm_init_all(hgs_ctx *const *ctxs, int n);
+hgs_status hgs_comm_destroy(hgs_ctx *ctx);
+int hgs_comm_size(hgs_ctx *ctx);
+int hgs_comm_rank(hgs_ctx *ctx);
+hgs_status hgs_allreduce_grads(hgs_ctx *ctx);
+hgs_status hgs_allreduce_f64(hgs_ctx *ctx, double *vals, int n);
+hgs_status hgs_param_checksum(hgs_ctx *ctx, uint64_t *out);
+hgs_status hgs_broadcast_params(hgs_ctx *ctx, int root);
+
 /* ---- loss (loss.hpp:12-13) --------------------------------------------- */
 /* (1-l)*L1 + l*(1-SSIM) of the last rendered image against gt (h*w*3, host
  * dtype or device float); dL/dimage stays on the device for hgs_backward. */

@@ -31,6 +31,10 @@ class HostScene(C.Structure):
         [("duration_seconds", C.c_double)]
 
 
+class CommId(C.Structure):  # hgs_comm_id (ncclUniqueId)
+    _fields_ = [("internal", C.c_char * 128)]
+
+
 class InitCfg(C.Structure):  # hgs_init_cfg (InitConfig, data_io.hpp:43-49)
     _fields_ = [("sh_degree", C.c_int32), ("tau", C.c_double), ("duration_seconds", C.c_double),
                 ("init_temporal_scale", C.c_double), ("init_opacity", C.c_double)]
@@ -163,6 +167,16 @@ _SIGS = {
     "hgs_densify_plan": ([_vp, C.POINTER(DensifyCfg), _vp, _vp, C.POINTER(DensifyReport)], C.c_int),
     "hgs_densify_apply": ([_vp, _dp, _dp, C.c_double], C.c_int),
     "hgs_opacity_reset": ([_vp, C.c_double], C.c_int),
+    "hgs_comm_unique_id": ([C.POINTER(CommId)], C.c_int),
+    "hgs_comm_init": ([_vp, C.c_int, C.c_int, C.POINTER(CommId)], C.c_int),
+    "hgs_comm_init_all": ([C.POINTER(_vp), C.c_int], C.c_int),
+    "hgs_comm_destroy": ([_vp], C.c_int),
+    "hgs_comm_size": ([_vp], C.c_int),
+    "hgs_comm_rank": ([_vp], C.c_int),
+    "hgs_allreduce_grads": ([_vp], C.c_int),
+    "hgs_allreduce_f64": ([_vp, _dp, C.c_int], C.c_int),
+    "hgs_param_checksum": ([_vp, C.POINTER(C.c_uint64)], C.c_int),
+    "hgs_broadcast_params": ([_vp, C.c_int], C.c_int),
     "hgs_init_scene": ([_vp, _dp, _dp, C.c_int64, C.POINTER(InitCfg)], C.c_int),
     "hgs_ppm_info": ([C.c_char_p, _i32p, _i32p], C.c_int),
     "hgs_ppm_read": ([C.c_char_p, C.POINTER(C.c_uint8), C.c_int32, C.c_int32], C.c_int),

@@ -147,6 +147,42 @@ class Context:
         s.tau, s.extent, s.duration_seconds = hs.tau, hs.extent, hs.duration_seconds
         return s
 
+    # ------------------------------------------------------------ multi-GPU exchange
+    @staticmethod
+    def comm_unique_id() -> bytes:
+        """ncclGetUniqueId (128 bytes) -- on one rank, shipped out of band."""
+        k = _capi.CommId()
+        rc = _capi.lib().hgs_comm_unique_id(C.byref(k))
+        if rc != 0:
+            raise _capi.CudaError("comm: NCCL unavailable")
+        return bytes(C.string_at(C.addressof(k), 128))
+
+    def comm_init(self, nranks: int, rank: int, uid: bytes) -> None:
+        k = _capi.CommId()
+        C.memmove(C.addressof(k), uid, 128)
+        self._check(self._lib.hgs_comm_init(self._h, int(nranks), int(rank), C.byref(k)))
+
+    def comm_destroy(self) -> None:
+        self._check(self._lib.hgs_comm_destroy(self._h))
+
+    def allreduce_grads(self) -> None:
+        """Sum the packed gradient payload over the ranks (stream-ordered)."""
+        self._check(self._lib.hgs_allreduce_grads(self._h))
+
+    def allreduce_f64(self, vals) -> np.ndarray:
+        a = np.ascontiguousarray(vals, dtype=np.float64).copy()
+        self._check(self._lib.hgs_allreduce_f64(self._h, a.ctypes.data_as(_capi._dp), a.size))
+        return a
+
+    def param_checksum(self) -> int:
+        """Order-independent 64-bit checksum of the parameters."""
+        v = C.c_uint64()
+        self._check(self._lib.hgs_param_checksum(self._h, C.byref(v)))
+        return v.value
+
+    def broadcast_params(self, root: int = 0) -> None:
+        self._check(self._lib.hgs_broadcast_params(self._h, int(root)))
+
     # ------------------------------------------------------------ initialisation
     def init_scene(self, positions: np.ndarray, rgb: np.ndarray, cfg: "InitConfig | None" = None) -> None:
         """init_scene (data_io.cpp:189-238) straight into the device: one

@@ -611,13 +611,14 @@ void hgs_ctx_destroy(hgs_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
+    hgs_comm_destroy(ctx);
     DBuf* bufs[] = {&ctx->p4, &ctx->p3, &ctx->p4_alt, &ctx->m4_alt, &ctx->v4_alt, &ctx->gbuf, &ctx->scratch, &ctx->m4, &ctx->v4, &ctx->m3, &ctx->v3, &ctx->gn4,
                     &ctx->gn3, &ctx->cnt4, &ctx->cnt3, &ctx->sn4, &ctx->sn3, &ctx->rec, &ctx->depth_key,
                     &ctx->ntiles, &ctx->visflag, &ctx->vispos, &ctx->sort_k, &ctx->sort_v, &ctx->sort_k2,
                     &ctx->sort_v2, &ctx->rec_sorted, &ctx->fast_sorted, &ctx->ntiles_sorted, &ctx->inst_off,
                     &ctx->inst_k, &ctx->inst_v, &ctx->inst_k2, &ctx->inst_v2, &ctx->ranges, &ctx->sorted_of_gid, &ctx->inst_flag, &ctx->inst_pos, &ctx->dbg_k, &ctx->dbg_v, &ctx->scan_ws,
                     &ctx->sort_ws, &ctx->counters, &ctx->img, &ctx->last, &ctx->tfinal, &ctx->trans, &ctx->count,
-                    &ctx->fix_list, &ctx->accum, &ctx->lgrad, &ctx->gt_stage, &ctx->loss_ws, &ctx->stage, &ctx->adam_ok, &ctx->pcut, &ctx->dup_first, &ctx->shdir, &ctx->ddir, &ctx->dup_status, &ctx->gpack, &ctx->dens_cat, &ctx->dens_u32, &ctx->dens_misc, &ctx->dens_kinds, &ctx->dens_jit, &ctx->dmap, &ctx->ckpt, &ctx->crc_tab};
+                    &ctx->fix_list, &ctx->accum, &ctx->lgrad, &ctx->gt_stage, &ctx->loss_ws, &ctx->stage, &ctx->adam_ok, &ctx->pcut, &ctx->dup_first, &ctx->shdir, &ctx->ddir, &ctx->dup_status, &ctx->gpack, &ctx->dens_cat, &ctx->dens_u32, &ctx->dens_misc, &ctx->dens_kinds, &ctx->dens_jit, &ctx->dmap, &ctx->ckpt, &ctx->crc_tab, &ctx->comm_buf};
     for (DBuf* b : bufs) b->release();
     ctx->pinned.release();
     ctx->pinned_ctr.release();

@@ -1,0 +1,257 @@
+// comm.cu -- the multi-GPU exchange of SURVEY.md 8e behind the C ABI.
+//
+// View-parallel data parallelism: every rank holds a replica of the scene and
+// renders its share of the batch; the one exchange per optimizer step is an
+// all-reduce (sum) of the packed gradient payload (valid gradient rows +
+// densify-statistic deltas, hgs_grads_packed), then every rank applies the
+// same Adam step.  Replica consistency is checked with an order-independent
+// 64-bit checksum of the parameters (hgs_param_checksum) and repaired with a
+// broadcast from a root (hgs_broadcast_params).
+//
+// NCCL is resolved at run time (dlopen of libnccl.so.2): a process that
+// already loaded torch's NCCL shares that copy, a plain C++ caller gets the
+// system one; nothing links NCCL into libhgs_gpu.so.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+#include "train_api.cuh"
+
+using namespace hgs;
+
+namespace {
+
+struct NcclApi {
+    bool loaded = false;
+    std::string err;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommInitAll)(ncclComm_t*, int, const int*) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+    static NcclApi api = [] {
+        NcclApi a;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            a.err = std::string("NCCL not found: ") + dlerror();
+            return a;
+        }
+#define SYM(f)                                                             \
+    a.f = reinterpret_cast<decltype(a.f)>(dlsym(h, "nccl" #f));            \
+    if (!a.f) {                                                            \
+        a.err = "NCCL symbol missing: nccl" #f;                            \
+        return a;                                                          \
+    }
+        SYM(GetUniqueId) SYM(CommInitRank) SYM(CommInitAll) SYM(CommDestroy) SYM(AllReduce) SYM(Broadcast)
+        SYM(GroupStart) SYM(GroupEnd) SYM(GetErrorString)
+#undef SYM
+        a.loaded = true;
+        return a;
+    }();
+    return api;
+}
+
+hgs_status fail(hgs_ctx* ctx, hgs_status s, const std::string& m) {
+    if (ctx) ctx->err = m;
+    return s;
+}
+
+#define CKC(x)                                                                                    \
+    do {                                                                                          \
+        cudaError_t e_ = (x);                                                                     \
+        if (e_ != cudaSuccess) return fail(ctx, HGS_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+#define CKN(x)                                                                                            \
+    do {                                                                                                  \
+        ncclResult_t r_ = (x);                                                                            \
+        if (r_ != ncclSuccess) return fail(ctx, HGS_ERR_CUDA, std::string("NCCL: ") + nccl().GetErrorString(r_)); \
+    } while (0)
+
+hgs_status need_nccl(hgs_ctx* ctx) {
+    if (!nccl().loaded) return fail(ctx, HGS_ERR_CUDA, nccl().err);
+    return HGS_OK;
+}
+
+hgs_status need_comm(hgs_ctx* ctx) {
+    if (!ctx->comm) return fail(ctx, HGS_ERR_STATE, "comm: call hgs_comm_init / hgs_comm_init_all first");
+    return HGS_OK;
+}
+
+__device__ __forceinline__ unsigned long long mix64(unsigned long long z) {  // splitmix64 finaliser
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+// order-independent checksum: sum over valid elements of mix64(bits, position)
+__global__ void checksum_kernel(const float* __restrict__ p, int64_t cap, int64_t n, int rows, unsigned long long salt,
+                                unsigned long long* __restrict__ out) {
+    unsigned long long acc = 0;
+    const int64_t total = n * rows;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = e / n, i = e - r * n;
+        const unsigned long long bits = __float_as_uint(p[r * cap + i]);
+        acc += mix64(bits ^ ((unsigned long long)e << 32) ^ salt);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
+}
+
+}  // namespace
+
+extern "C" {
+
+hgs_status hgs_comm_unique_id(hgs_comm_id* out) {
+    if (!out) return HGS_ERR_INVALID_ARGUMENT;
+    if (!nccl().loaded) return HGS_ERR_CUDA;
+    ncclUniqueId id;
+    if (nccl().GetUniqueId(&id) != ncclSuccess) return HGS_ERR_CUDA;
+    static_assert(sizeof(id.internal) == sizeof(out->internal), "hgs_comm_id size");
+    std::memcpy(out->internal, id.internal, sizeof(id.internal));
+    return HGS_OK;
+}
+
+hgs_status hgs_comm_init(hgs_ctx* ctx, int nranks, int rank, const hgs_comm_id* id) {
+    if (!ctx || !id || nranks < 1 || rank < 0 || rank >= nranks) return HGS_ERR_INVALID_ARGUMENT;
+    hgs_status r = need_nccl(ctx);
+    if (r != HGS_OK) return r;
+    if (ctx->comm) return fail(ctx, HGS_ERR_STATE, "comm: already initialised");
+    CKC(cudaSetDevice(ctx->device));
+    ncclUniqueId uid;
+    std::memcpy(uid.internal, id->internal, sizeof(uid.internal));
+    ncclComm_t c = nullptr;
+    CKN(nccl().CommInitRank(&c, nranks, uid, rank));
+    ctx->comm = c;
+    ctx->comm_rank = rank;
+    ctx->comm_size = nranks;
+    return HGS_OK;
+}
+
+hgs_status hgs_comm_init_all(hgs_ctx* const* ctxs, int n) {
+    if (!ctxs || n < 1) return HGS_ERR_INVALID_ARGUMENT;
+    hgs_ctx* ctx = ctxs[0];
+    if (!ctx) return HGS_ERR_INVALID_ARGUMENT;
+    hgs_status r = need_nccl(ctx);
+    if (r != HGS_OK) return r;
+    std::vector<int> devs((size_t)n);
+    for (int i = 0; i < n; ++i) {
+        if (!ctxs[i]) return HGS_ERR_INVALID_ARGUMENT;
+        if (ctxs[i]->comm) return fail(ctx, HGS_ERR_STATE, "comm: already initialised");
+        devs[(size_t)i] = ctxs[i]->device;
+    }
+    std::vector<ncclComm_t> comms((size_t)n);
+    CKN(nccl().CommInitAll(comms.data(), n, devs.data()));
+    for (int i = 0; i < n; ++i) {
+        ctxs[i]->comm = comms[(size_t)i];
+        ctxs[i]->comm_rank = i;
+        ctxs[i]->comm_size = n;
+    }
+    return HGS_OK;
+}
+
+hgs_status hgs_comm_destroy(hgs_ctx* ctx) {
+    if (!ctx) return HGS_ERR_INVALID_ARGUMENT;
+    if (ctx->comm && nccl().loaded) {
+        cudaSetDevice(ctx->device);
+        cudaStreamSynchronize(ctx->stream);
+        nccl().CommDestroy(static_cast<ncclComm_t>(ctx->comm));
+    }
+    ctx->comm = nullptr;
+    ctx->comm_rank = 0;
+    ctx->comm_size = 1;
+    return HGS_OK;
+}
+
+hgs_status hgs_allreduce_grads(hgs_ctx* ctx) {
+    if (!ctx) return HGS_ERR_INVALID_ARGUMENT;
+    hgs_status r = need_comm(ctx);
+    if (r != HGS_OK) return r;
+    CKC(cudaSetDevice(ctx->device));
+    float* p = nullptr;
+    int64_t n = 0;
+    r = hgs_grads_packed(ctx, 0, &p, &n);
+    if (r != HGS_OK) return r;
+    if (n > 0)
+        CKN(nccl().AllReduce(p, p, (size_t)n, ncclFloat32, ncclSum, static_cast<ncclComm_t>(ctx->comm), ctx->stream));
+    return hgs_grads_packed(ctx, 1, nullptr, nullptr);
+}
+
+hgs_status hgs_allreduce_f64(hgs_ctx* ctx, double* vals, int n) {
+    if (!ctx || (n > 0 && !vals) || n < 0) return HGS_ERR_INVALID_ARGUMENT;
+    hgs_status r = need_comm(ctx);
+    if (r != HGS_OK) return r;
+    if (n == 0) return HGS_OK;
+    CKC(cudaSetDevice(ctx->device));
+    CKC(ctx->comm_buf.ensure((size_t)n * 8));
+    CKC(cudaMemcpyAsync(ctx->comm_buf.p, vals, (size_t)n * 8, cudaMemcpyHostToDevice, ctx->stream));
+    CKN(nccl().AllReduce(ctx->comm_buf.p, ctx->comm_buf.p, (size_t)n, ncclFloat64, ncclSum,
+                         static_cast<ncclComm_t>(ctx->comm), ctx->stream));
+    CKC(cudaMemcpyAsync(vals, ctx->comm_buf.p, (size_t)n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CKC(cudaStreamSynchronize(ctx->stream));
+    return HGS_OK;
+}
+
+hgs_status hgs_param_checksum(hgs_ctx* ctx, uint64_t* out) {
+    if (!ctx || !out) return HGS_ERR_INVALID_ARGUMENT;
+    CKC(cudaSetDevice(ctx->device));
+    CKC(ctx->comm_buf.ensure(64));
+    unsigned long long* d = ctx->comm_buf.as<unsigned long long>();
+    CKC(cudaMemsetAsync(d, 0, 8, ctx->stream));
+    const int blocks = ctx->sms * 4;
+    if (ctx->n4)
+        checksum_kernel<<<blocks, 256, 0, ctx->stream>>>(ctx->p4.as<float>(), ctx->cap4, ctx->n4, rows4(ctx->deg),
+                                                         0x4444ull, d);
+    if (ctx->n3)
+        checksum_kernel<<<blocks, 256, 0, ctx->stream>>>(ctx->p3.as<float>(), ctx->cap3, ctx->n3, rows3(ctx->deg),
+                                                         0x3333ull << 40, d);
+    count_launch((ctx->n4 ? 1 : 0) + (ctx->n3 ? 1 : 0));
+    CKC(cudaGetLastError());
+    unsigned long long h = 0;
+    CKC(cudaMemcpyAsync(&h, d, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CKC(cudaStreamSynchronize(ctx->stream));
+    *out = (uint64_t)(h ^ ((uint64_t)ctx->n4 << 1) ^ ((uint64_t)ctx->n3 << 33));
+    return HGS_OK;
+}
+
+hgs_status hgs_broadcast_params(hgs_ctx* ctx, int root) {
+    if (!ctx) return HGS_ERR_INVALID_ARGUMENT;
+    hgs_status r = need_comm(ctx);
+    if (r != HGS_OK) return r;
+    if (root < 0 || root >= ctx->comm_size) return HGS_ERR_INVALID_ARGUMENT;
+    CKC(cudaSetDevice(ctx->device));
+    // every rank must hold the same pool sizes (the replicas diverged in
+    // values, not in structure)
+    const size_t b4 = (size_t)rows4(ctx->deg) * ctx->cap4, b3 = (size_t)rows3(ctx->deg) * ctx->cap3;
+    ncclComm_t c = static_cast<ncclComm_t>(ctx->comm);
+    CKN(nccl().GroupStart());
+    for (DBuf* b : {&ctx->p4, &ctx->m4, &ctx->v4})
+        CKN(nccl().Broadcast(b->p, b->p, b4, ncclFloat32, root, c, ctx->stream));
+    for (DBuf* b : {&ctx->p3, &ctx->m3, &ctx->v3})
+        CKN(nccl().Broadcast(b->p, b->p, b3, ncclFloat32, root, c, ctx->stream));
+    for (DBuf* b : {&ctx->gn4, &ctx->cnt4})
+        CKN(nccl().Broadcast(b->p, b->p, (size_t)ctx->cap4, ncclFloat32, root, c, ctx->stream));
+    for (DBuf* b : {&ctx->gn3, &ctx->cnt3})
+        CKN(nccl().Broadcast(b->p, b->p, (size_t)ctx->cap3, ncclFloat32, root, c, ctx->stream));
+    CKN(nccl().GroupEnd());
+    CKC(cudaStreamSynchronize(ctx->stream));
+    return HGS_OK;
+}
+
+int hgs_comm_size(hgs_ctx* ctx) { return ctx ? ctx->comm_size : 0; }
+int hgs_comm_rank(hgs_ctx* ctx) { return ctx ? ctx->comm_rank : 0; }
+
+}  // extern "C"

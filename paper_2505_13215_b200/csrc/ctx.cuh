@@ -143,6 +143,9 @@ struct hgs_ctx {
     hgs::DBuf dmap;      // density_map difference array ((W+1)*(H+1) ints) and counts
     hgs::DBuf ckpt;              // checkpoint payloads on the device (checkpoint.cu)
     hgs::DBuf crc_tab;           // CRC-32 slicing tables (checkpoint.cu)
+    void* comm = nullptr;        // ncclComm_t of the view-parallel exchange (comm.cu)
+    int comm_rank = 0, comm_size = 1;
+    hgs::DBuf comm_buf;          // small staging for collectives / checksums
     hgs::HostPinned ckpt_host;   // checkpoint file image
     hgs::HostPinned pinned;      // Scratch read-back (training / loss)
     hgs::HostPinned pinned_ctr;  // Counters read-back (render)

@@ -166,7 +166,12 @@ class ViewParallelTrainer(DeviceTrainer):
     """One rank of the view-parallel trainer (torch.distributed, NCCL on GPUs,
     gloo on CPU for the host-logic tests)."""
 
-    def __init__(self, *args, group=None, **kw):
+    def __init__(self, *args, group=None, exchange: str = "torch", verify_every: int = 0, **kw):
+        """exchange: "torch" -- torch.distributed all-reduce of the packed
+        payload; "capi" -- the library's own NCCL communicator
+        (hgs_allreduce_grads).  verify_every > 0: every that many steps the
+        ranks compare parameter checksums and, on a mismatch, reload rank 0's
+        state (SURVEY.md 8e replica consistency)."""
         super().__init__(*args, **kw)
         import torch.distributed as dist
 
@@ -174,6 +179,15 @@ class ViewParallelTrainer(DeviceTrainer):
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
+        if exchange not in ("torch", "capi"):
+            raise ValueError("exchange: 'torch' or 'capi'")
+        self.exchange = exchange
+        self.verify_every = verify_every
+        self.repairs = 0
+        if exchange == "capi":
+            uid = [Context.comm_unique_id() if self.rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0, group=group)
+            self.ctx.comm_init(self.world, self.rank, uid[0])
 
     def grads_tensor(self):
         ptr, n = self.ctx.grads_device()
@@ -195,11 +209,53 @@ class ViewParallelTrainer(DeviceTrainer):
         except _capi.NumericAbort:
             self.ctx.zero_grads()
             raise
-        g = self.packed_grads_tensor()
-        self.dist.all_reduce(g, group=self.group)          # sum of dense grads + stat deltas
-        self.ctx.grads_unpack()
+        if self.exchange == "capi":
+            self.ctx.allreduce_grads()                     # pack -> ncclAllReduce -> unpack, one stream
+        else:
+            g = self.packed_grads_tensor()
+            self.dist.all_reduce(g, group=self.group)      # sum of dense grads + stat deltas
+            self.ctx.grads_unpack()
         self.ctx.adam_step(self.lrs, self.decay())
+        if self.verify_every and self.iter % self.verify_every == 0:
+            self.verify_replicas()
         return total / len(batch)
+
+    def verify_replicas(self) -> bool:
+        """True when every rank's parameters hash equal; otherwise rank 0's
+        scene, optimizer state and statistics are shipped to every rank
+        (as a checkpoint image) and False is returned."""
+        ok = replicas_agree(self.dist, self.group, self.ctx.param_checksum())
+        if not ok:
+            repair_from_root(self.dist, self.group, self.rank, self.ctx)
+            self.repairs += 1
+        return ok
+
+
+def replicas_agree(dist, group, checksum: int) -> bool:
+    """All ranks hold the same 64-bit parameter checksum."""
+    allv = [None] * dist.get_world_size(group)
+    dist.all_gather_object(allv, int(checksum), group=group)
+    return all(v == allv[0] for v in allv)
+
+
+def repair_from_root(dist, group, rank: int, ctx, root: int = 0) -> None:
+    """Every rank takes the root's device state (parameters, Adam moments,
+    statistics, step) through the checkpoint encoder / decoder."""
+    import os
+    import tempfile
+
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, f"replica{rank}.hgsc")
+        blob = [None]
+        if rank == root:
+            ctx.save_checkpoint(path)
+            with open(path, "rb") as f:
+                blob[0] = f.read()
+        dist.broadcast_object_list(blob, src=root, group=group)
+        if rank != root:
+            with open(path, "wb") as f:
+                f.write(blob[0])
+            ctx.load_checkpoint(path)
 
 
 def reduce_batch_loss(dist, group, local_loss: float, device: str = "cpu") -> float:

@@ -165,3 +165,61 @@ def test_numeric_abort_is_a_collective_decision():
         p.join(timeout=60)
     for r in (0, 1):
         assert res[r] == [1.5, "abort", 2.0], res
+
+
+class _FakeReplica:
+    """Stands in for a Context: a byte-string 'device state' that
+    save_checkpoint / load_checkpoint move through files (as the real one)."""
+
+    def __init__(self, state: bytes):
+        self.state = state
+
+    def param_checksum(self) -> int:
+        import zlib
+
+        return zlib.crc32(self.state)
+
+    def save_checkpoint(self, path):
+        with open(path, "wb") as f:
+            f.write(self.state)
+
+    def load_checkpoint(self, path):
+        with open(path, "rb") as f:
+            self.state = f.read()
+        return True
+
+
+def _replica_worker(rank, world, port, q):
+    from paper_2505_13215_b200.train import repair_from_root, replicas_agree
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    ctx = _FakeReplica(b"scene-v1")
+    out = [replicas_agree(dist, None, ctx.param_checksum())]          # identical replicas
+    if rank == 1:
+        ctx.state = b"scene-v1-diverged"
+    ok = replicas_agree(dist, None, ctx.param_checksum())
+    out.append(ok)
+    if not ok:                                                        # every rank takes the same branch
+        repair_from_root(dist, None, rank, ctx)
+    out.append(ctx.state)
+    out.append(replicas_agree(dist, None, ctx.param_checksum()))
+    dist.destroy_process_group()
+    q.put((rank, out))
+
+
+def test_replica_check_and_repair():
+    """ranks compare parameter checksums; a diverged replica is
+    repaired from rank 0's checkpoint image, and all ranks decide together."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_replica_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    for r in (0, 1):
+        assert res[r] == [True, False, b"scene-v1", True], res

@@ -1,0 +1,96 @@
+"""The C-ABI multi-GPU exchange (hgs_comm_*, hgs_allreduce_grads,
+hgs_param_checksum, hgs_broadcast_params) on one B200: a one-rank NCCL
+communicator exercises the whole plumbing (pack -> ncclAllReduce -> unpack on
+the context stream) with the identity reduction; the multi-rank host logic is
+covered by tests/test_dist_cpu.py (gloo, world size 2)."""
+import numpy as np
+import pytest
+
+from paper_2505_13215_b200 import api as A
+from paper_2505_13215_b200.scene import ring_camera, synthetic_scene
+
+pytestmark = pytest.mark.gpu
+
+
+def _trainer(ctx, exchange=None):
+    from paper_2505_13215_b200.train import DeviceTrainer
+
+    target = synthetic_scene(3000, 2000, sh_degree=2, seed=31)
+    scene = synthetic_scene(3000, 2000, sh_degree=2, seed=32).as_float32_exact()
+    cams = [ring_camera(i, 96, 72) for i in range(4)]
+    return DeviceTrainer(ctx, scene, cams, [0.1, 0.4, 0.6, 0.9], target=target, iterations=50)
+
+
+def test_one_rank_allreduce_is_identity():
+    with A.Context(0) as ctx:
+        tr = _trainer(ctx)
+        uid = A.Context.comm_unique_id()
+        assert len(uid) == 128
+        ctx.comm_init(1, 0, uid)
+        assert ctx._lib.hgs_comm_size(ctx.handle) == 1
+        tr.step([0, 1], apply_adam=False)
+        before = ctx.grads()
+        ctx.allreduce_grads()
+        after = ctx.grads()
+        for k in before:
+            assert np.array_equal(np.asarray(before[k]), np.asarray(after[k])), k
+        assert np.array_equal(ctx.allreduce_f64([1.5, -2.0, np.inf]), [1.5, -2.0, np.inf])
+        s0 = ctx.param_checksum()
+        ctx.broadcast_params(0)
+        assert ctx.param_checksum() == s0
+        ctx.adam_step(tr.lrs, tr.decay())
+        assert ctx.param_checksum() != s0
+        ctx.comm_destroy()
+        with pytest.raises(A.StateError):
+            ctx.allreduce_grads()
+
+
+def test_param_checksum_detects_one_flipped_value():
+    scene = synthetic_scene(5000, 3000, sh_degree=3, seed=3).as_float32_exact()
+    with A.Context(0) as a, A.Context(0) as b:
+        a.upload(scene)
+        b.upload(scene)
+        assert a.param_checksum() == b.param_checksum()
+        s2 = scene.copy()
+        s2.sh3[1234, 7, 2] = np.nextafter(np.float32(s2.sh3[1234, 7, 2]), np.float32(1)).astype(np.float64)
+        b.upload(s2)
+        assert a.param_checksum() != b.param_checksum()
+        s3 = scene.copy()  # the same multiset of values in another order is another scene
+        s3.op4[[0, 1]] = s3.op4[[1, 0]]
+        b.upload(s3)
+        assert (s3.op4[0] == s3.op4[1]) or a.param_checksum() != b.param_checksum()
+
+
+def test_view_parallel_trainer_capi_exchange_single_rank(tmp_path):
+    """ViewParallelTrainer(exchange='capi') in a one-rank process group: the
+    same iteration as the plain trainer (FP32 tolerance: atomics)."""
+    import os
+
+    import torch.distributed as dist
+
+    from paper_2505_13215_b200.train import ViewParallelTrainer
+
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29617")
+    dist.init_process_group("gloo", rank=0, world_size=1, init_method=f"file://{tmp_path}/pg")
+    try:
+        target = synthetic_scene(3000, 2000, sh_degree=2, seed=31)
+        scene = synthetic_scene(3000, 2000, sh_degree=2, seed=32).as_float32_exact()
+        cams = [ring_camera(i, 96, 72) for i in range(4)]
+        times = [0.1, 0.4, 0.6, 0.9]
+        with A.Context(0) as c1, A.Context(0) as c2:
+            from paper_2505_13215_b200.train import DeviceTrainer
+
+            ref = DeviceTrainer(c1, scene, cams, times, target=target, iterations=50)
+            vp = ViewParallelTrainer(c2, scene, cams, times, target=target, iterations=50, exchange="capi",
+                                     verify_every=1)
+            for it in range(3):
+                l1 = ref.step([it % 4, (it + 1) % 4])
+                l2 = vp.step([it % 4, (it + 1) % 4])
+                assert l2 == pytest.approx(l1, rel=1e-5)
+            assert vp.repairs == 0
+            s1, s2 = c1.download(), c2.download()
+            for f in ("mean_x", "log_s4", "sh4", "mean3", "op3"):
+                np.testing.assert_allclose(getattr(s2, f), getattr(s1, f), rtol=1e-4, atol=1e-6)
+    finally:
+        dist.destroy_process_group()
