@@ -361,6 +361,7 @@ def run_ours(args) -> None:
 
     extra = run_extras(args, ctx, lib, timed, world, rank) if not args.no_extras else None
     if extra is not None and world == 1:
+        extra["c3_train"] = run_c3(ctx, timed)
         extra["rows_8f"] = run_rows(ctx)
 
     cpu = None
@@ -449,6 +450,64 @@ def run_extras(args, ctx, lib, timed, world, rank) -> dict:
                        "config": "1600k 4D + 400k 3D, SH 3, 1352x1014, 8 views/GPU/step"}
     torch.cuda.synchronize()
     return out
+
+
+def run_c3(ctx, timed) -> dict:
+    """configs[2], N3V-shaped: 300k Gaussians (all 4D at start), 18 cameras,
+    1352x1014, batch 2, the periodic 4D->3D conversion sweep every 100
+    iterations (train.cpp:466-472) inside the timed region.  Frames: 4 per
+    camera (72 8-bit GT renders of a second scene, device resident) instead
+    of 300 (the per-iteration work does not depend on the frame count)."""
+    import torch
+
+    from paper_2505_13215_b200.rng import MT19937_64, uniform_index
+    from paper_2505_13215_b200.scene import CONFIGS, ring_camera, synthetic_scene
+    from paper_2505_13215_b200.train import DeviceTrainer
+
+    c = CONFIGS["c3"]
+    scene = synthetic_scene(c["n4"], c["n3"], 3, seed=c["seed"], tau=0.5)
+    target = synthetic_scene(c["n4"], c["n3"], 3, seed=c["seed"] + 1000, tau=0.5)
+    cams, times = [], []
+    for ci in range(18):
+        cam = ring_camera(c["seed"], c["width"], c["height"], index=ci, n_ring=18)
+        for j in range(4):
+            cams.append(cam)
+            times.append(j / 3.0)
+    tr = DeviceTrainer(ctx, scene, cams, times, target=target, bg=(0.2, 0.2, 0.2), iterations=400, gt_format="u8")
+    del target
+    rng = MT19937_64(3)
+    n = len(cams)
+    state = {"it": 0, "moved": 0, "sweeps": 0}
+
+    def iteration(_):
+        state["it"] += 1
+        tr.step_async([uniform_index(rng, 0, n - 1) for _ in range(2)])
+        if ctx._lib.hgs_train_pending(ctx.handle) > 1:
+            tr.collect()
+        if state["it"] % 100 == 0:  # drain, then the sweep (train.cpp:466-472)
+            while ctx._lib.hgs_train_pending(ctx.handle):
+                tr.collect()
+            moved, _ = ctx.sweep_convert()
+            state["moved"] += len(moved)
+            state["sweeps"] += 1
+
+    def drain():
+        while ctx._lib.hgs_train_pending(ctx.handle):
+            tr.collect()
+
+    for i in range(20):  # warm-up (no sweep)
+        tr.step_async([uniform_index(rng, 0, n - 1) for _ in range(2)])
+        tr.collect()
+    state["it"] = 0
+    k = 200
+    ms = timed(iteration, k, drain)
+    n4, n3 = ctx.counts()
+    torch.cuda.synchronize()
+    return {"value": round(2 * k / (ms / 1e3), 2), "unit": "views/s", "iters_per_s": round(k / (ms / 1e3), 2),
+            "ms_per_iter": round(ms / k, 4), "sweeps": state["sweeps"], "converted": state["moved"],
+            "final_n4": n4, "final_n3": n3,
+            "config": "300k 4D (+ converted 3D), SH 3, 1352x1014, 18 cameras x 4 frames, batch 2, "
+                      "4D->3D sweep every 100 iterations (timed)"}
 
 
 def run_rows(ctx) -> dict:

@@ -323,6 +323,26 @@ typedef struct {
 hgs_status hgs_densify_plan(hgs_ctx *ctx, const hgs_densify_cfg *cfg, uint8_t *kinds3, uint8_t *kinds4,
                             hgs_densify_report *report);
 hgs_status hgs_densify_apply(hgs_ctx *ctx, const double *normals3, const double *normals4, double split_factor);
+/* The training loop's random stream (train.cpp:68-72, 245-275, 387-404):
+ * libstdc++'s std::mt19937_64 with the reference's distributions, so batch
+ * schedules and densification jitter match the reference bit for bit.
+ *   hgs_rng_index       -- std::uniform_int_distribution<size_t>(lo, hi)
+ *   hgs_rng_batch       -- `count` picks over [0, n_samples - 1] (one batch)
+ *   hgs_densify_normals -- the normals for hgs_densify_apply given the kinds
+ *                          hgs_densify_plan returned, drawn in the
+ *                          reference's order
+ *   hgs_densify_and_prune -- plan + draws + apply in one call (the
+ *                          reference's densify_and_prune(scene, accum, cfg, rng)) */
+typedef struct hgs_rng hgs_rng;
+hgs_status hgs_rng_create(uint64_t seed, hgs_rng **out);
+void hgs_rng_destroy(hgs_rng *rng);
+uint64_t hgs_rng_raw(hgs_rng *rng);
+uint64_t hgs_rng_index(hgs_rng *rng, uint64_t lo, uint64_t hi);
+hgs_status hgs_rng_batch(hgs_rng *rng, uint64_t n_samples, int32_t count, uint64_t *out);
+hgs_status hgs_densify_normals(hgs_rng *rng, const uint8_t *kinds3, int64_t d3, const uint8_t *kinds4, int64_t d4,
+                               double *normals3, double *normals4);
+hgs_status hgs_densify_and_prune(hgs_ctx *ctx, const hgs_densify_cfg *cfg, hgs_rng *rng,
+                                 hgs_densify_report *report);
 /* train.cpp:459-465: every opacity logit capped at floor_logit (logit(0.01)). */
 hgs_status hgs_opacity_reset(hgs_ctx *ctx, double floor_logit);
 

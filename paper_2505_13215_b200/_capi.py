@@ -167,6 +167,13 @@ _SIGS = {
     "hgs_densify_plan": ([_vp, C.POINTER(DensifyCfg), _vp, _vp, C.POINTER(DensifyReport)], C.c_int),
     "hgs_densify_apply": ([_vp, _dp, _dp, C.c_double], C.c_int),
     "hgs_opacity_reset": ([_vp, C.c_double], C.c_int),
+    "hgs_rng_create": ([C.c_uint64, C.POINTER(_vp)], C.c_int),
+    "hgs_rng_destroy": ([_vp], None),
+    "hgs_rng_raw": ([_vp], C.c_uint64),
+    "hgs_rng_index": ([_vp, C.c_uint64, C.c_uint64], C.c_uint64),
+    "hgs_rng_batch": ([_vp, C.c_uint64, C.c_int32, C.POINTER(C.c_uint64)], C.c_int),
+    "hgs_densify_normals": ([_vp, _vp, C.c_int64, _vp, C.c_int64, _dp, _dp], C.c_int),
+    "hgs_densify_and_prune": ([_vp, C.POINTER(DensifyCfg), _vp, C.POINTER(DensifyReport)], C.c_int),
     "hgs_comm_unique_id": ([C.POINTER(CommId)], C.c_int),
     "hgs_comm_init": ([_vp, C.c_int, C.c_int, C.POINTER(CommId)], C.c_int),
     "hgs_comm_init_all": ([C.POINTER(_vp), C.c_int], C.c_int),

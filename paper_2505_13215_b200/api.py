@@ -422,10 +422,15 @@ class Context:
                           max_gaussians: int = 20000) -> dict:
         """densify_and_prune (train.cpp:182-299) on the device; ``rng`` is the
         loop's rng.MT19937_64, advanced exactly like the reference's."""
+        cfg = _capi.DensifyCfg(grad_threshold, opacity_prune_eps, clone_size_frac, split_factor, max_gaussians)
+        if isinstance(rng, Rng):  # native stream: one C call (plan, draws, apply)
+            rep = _capi.DensifyReport()
+            self._check(self._lib.hgs_densify_and_prune(self._h, C.byref(cfg), rng.handle, C.byref(rep)))
+            self.counts()
+            return {n: int(getattr(rep, n)) for n, _ in _capi.DensifyReport._fields_}
         from .rng import densify_normals
 
         n4, n3 = self.counts()
-        cfg = _capi.DensifyCfg(grad_threshold, opacity_prune_eps, clone_size_frac, split_factor, max_gaussians)
         k3, k4 = np.zeros(max(n3, 1), np.uint8), np.zeros(max(n4, 1), np.uint8)
         rep = _capi.DensifyReport()
         self._check(self._lib.hgs_densify_plan(self._h, C.byref(cfg), k3.ctypes.data_as(C.c_void_p),
@@ -453,6 +458,53 @@ class Context:
         self.counts()
         return moved[: rep.count].copy(), {"count": int(rep.count), "max_leakage": rep.max_leakage,
                                            "mean_leakage": rep.mean_leakage}
+
+
+class Rng:
+    """The training loop's random stream (hgs_rng: libstdc++ std::mt19937_64
+    with the reference's distributions, train.cpp:68-72, 245-275, 387-404)."""
+
+    def __init__(self, seed: int = 5489):
+        self._lib = _capi.lib()
+        h = _capi._vp()
+        if self._lib.hgs_rng_create(C.c_uint64(seed), C.byref(h)) != 0:
+            raise MemoryError("hgs_rng_create")
+        self._h = h
+
+    @property
+    def handle(self):
+        return self._h
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            self._lib.hgs_rng_destroy(self._h)
+            self._h = None
+
+    def raw(self) -> int:
+        return int(self._lib.hgs_rng_raw(self._h))
+
+    def index(self, lo: int, hi: int) -> int:
+        """std::uniform_int_distribution<size_t>(lo, hi)"""
+        return int(self._lib.hgs_rng_index(self._h, lo, hi))
+
+    def batch(self, n_samples: int, count: int) -> list[int]:
+        """`count` picks over [0, n_samples - 1] (train.cpp:403-404)."""
+        out = (C.c_uint64 * max(1, count))()
+        if self._lib.hgs_rng_batch(self._h, n_samples, count, out) != 0:
+            raise ValueError("rng batch: bad arguments")
+        return [int(v) for v in out[:count]]
+
+    def densify_normals(self, kinds3, kinds4):
+        """The normals densify_and_prune draws (hgs_densify_normals)."""
+        k3 = np.ascontiguousarray(kinds3, dtype=np.uint8)
+        k4 = np.ascontiguousarray(kinds4, dtype=np.uint8)
+        n3, n4 = np.zeros(6 * max(1, k3.size)), np.zeros(8 * max(1, k4.size))
+        rc = self._lib.hgs_densify_normals(self._h, k3.ctypes.data_as(C.c_void_p), k3.size,
+                                           k4.ctypes.data_as(C.c_void_p), k4.size, n3.ctypes.data_as(_capi._dp),
+                                           n4.ctypes.data_as(_capi._dp))
+        if rc != 0:
+            raise ValueError("densify_normals: bad arguments")
+        return n3, n4
 
 
 _default_ctx: Context | None = None

@@ -279,8 +279,10 @@ def shard_batch(batch: list[int], rank: int, world: int) -> list[int]:
 def sample_batches(n_samples: int, batch_size: int, iterations: int, seed: int) -> list[list[int]]:
     """Deterministic batch schedule shared by all ranks (train.cpp:387-404
     samples (camera, frame) pairs uniformly; every rank draws the same list)."""
-    rng = np.random.default_rng(seed)
-    return [list(rng.integers(0, n_samples, batch_size)) for _ in range(iterations)]
+    from .api import Rng
+
+    r = Rng(seed)
+    return [r.batch(n_samples, batch_size) for _ in range(iterations)]
 
 
 # --------------------------------------------------------------------------
@@ -291,7 +293,6 @@ def sample_batches(n_samples: int, batch_size: int, iterations: int, seed: int) 
 
 from dataclasses import dataclass, field  # noqa: E402
 
-from .rng import MT19937_64, uniform_index  # noqa: E402
 
 
 @dataclass
@@ -444,7 +445,9 @@ def train_scene(scene: HybridScene, dataset: MultiViewDataset, cfg: TrainConfig,
                                                         dtype=np.uint8 if u8 else np.float32), device=dev)
            for c, f in samples}
     cams = [_capi.camera_struct(c) for c in dataset.cameras]
-    rng = MT19937_64(cfg.seed)
+    from .api import Rng
+
+    rng = Rng(cfg.seed)  # libstdc++ mt19937_64 stream shared by batches and densification (train.cpp:387)
     probe = (0, len(dataset.frames[0]) // 2)
     o = _capi.TrainOpts()
     o.ssim_lambda, o.weight_cutoff = cfg.ssim_lambda, cfg.weight_cutoff
@@ -455,7 +458,7 @@ def train_scene(scene: HybridScene, dataset: MultiViewDataset, cfg: TrainConfig,
     log = []
     t0 = _time.perf_counter()
     for it in range(1, cfg.iterations + 1):
-        batch = [samples[uniform_index(rng, 0, len(samples) - 1)] for _ in range(B)]
+        batch = [samples[i] for i in rng.batch(len(samples), B)]  # train.cpp:403-404
         o.mean_lr_scale = math.pow(cfg.lrs.mean_final_ratio, it / cfg.iterations)  # train.cpp:449
         karr = (_capi.Camera_ * B)(*[cams[c] for c, _ in batch])
         tarr = (C.c_double * B)(*[dataset.frames[c][f].time for c, f in batch])

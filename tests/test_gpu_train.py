@@ -393,7 +393,8 @@ def test_nonfinite_loss_without_update_is_returned(ctx):
     assert np.isfinite(tr.step([0, 1]))
 
 
-def _densify_case(ctx, max_gaussians):
+def _densify_case(ctx, max_gaussians, native=True):
+    from paper_2505_13215_b200.api import Rng
     from paper_2505_13215_b200.rng import MT19937_64
     from paper_2505_13215_b200.train import DeviceTrainer
 
@@ -413,17 +414,19 @@ def _densify_case(ctx, max_gaussians):
     cfg = dict(grad_threshold=float(np.quantile(avg[avg > 0], 0.5)), opacity_prune_eps=0.3,
                clone_size_frac=0.05, split_factor=1.6, max_gaussians=max_gaussians)
     ref_scene, ref_st, ref_rep = O.densify_and_prune(cur, st, O.Rng(17), **cfg)
-    rep = ctx.densify_and_prune(MT19937_64(17), **cfg)
+    # native: hgs_densify_and_prune with the library's libstdc++ stream;
+    # python: plan / rng.py draws / apply
+    rep = ctx.densify_and_prune(Rng(17) if native else MT19937_64(17), **cfg)
     return cur, ref_scene, ref_st, ref_rep, rep
 
 
-@pytest.mark.parametrize("max_gaussians", [20000, 1300])
-def test_densify_matches_oracle(ctx, max_gaussians):
+@pytest.mark.parametrize("max_gaussians,native", [(20000, True), (1300, True), (1300, False)])
+def test_densify_matches_oracle(ctx, max_gaussians, native):
     """densify_and_prune (train.cpp:182-299) on the device against the oracle
     on the same pools, statistics, Adam state and seed: identical decisions
     (counts, pool sizes, row order), the reference's normal variates (same
     mt19937_64 sequence), Adam rows remapped with fresh rows zero."""
-    cur, ref, ref_st, ref_rep, rep = _densify_case(ctx, max_gaussians)
+    cur, ref, ref_st, ref_rep, rep = _densify_case(ctx, max_gaussians, native)
     for k in ("cloned3", "split3", "pruned3", "cloned4", "split4", "pruned4"):
         assert rep[k] == ref_rep[k], (k, rep, ref_rep)
     assert rep["cloned4"] + rep["split4"] > 0 and rep["pruned4"] > 0
