@@ -147,51 +147,6 @@ __device__ __noinline__ bool clamp_psd_slow(M3& m) {
     return true;
 }
 
-// SH colour in FP32 (sh.cpp:25-47, 73-83); coefficient k channel c at row
-// base + 3k + c.
-// Returns the bit mask of the channels clamped to [0, 1] (raster.cpp:86 / sh.cpp:81).
-__device__ inline uint32_t eval_sh_f32(const float* __restrict__ p, int64_t cap, int i, int base, int deg,
-                                       float dx, float dy, float dz, float rgb[3]) {
-    float basis[16];
-    basis[0] = 0.28209479177387814f;
-    if (deg >= 1) {
-        basis[1] = -0.4886025119029199f * dy;
-        basis[2] = 0.4886025119029199f * dz;
-        basis[3] = -0.4886025119029199f * dx;
-    }
-    if (deg >= 2) {
-        float xx = dx * dx, yy = dy * dy, zz = dz * dz;
-        basis[4] = 1.0925484305920792f * dx * dy;
-        basis[5] = -1.0925484305920792f * dy * dz;
-        basis[6] = 0.31539156525252005f * (2.0f * zz - xx - yy);
-        basis[7] = -1.0925484305920792f * dx * dz;
-        basis[8] = 0.5462742152960396f * (xx - yy);
-        if (deg >= 3) {
-            basis[9] = -0.5900435899266435f * dy * (3.0f * xx - yy);
-            basis[10] = 2.890611442640554f * dx * dy * dz;
-            basis[11] = -0.4570457994644658f * dy * (4.0f * zz - xx - yy);
-            basis[12] = 0.3731763325901154f * dz * (2.0f * zz - 3.0f * xx - 3.0f * yy);
-            basis[13] = -0.4570457994644658f * dx * (4.0f * zz - xx - yy);
-            basis[14] = 1.445305721320277f * dz * (xx - yy);
-            basis[15] = -0.5900435899266435f * dx * (xx - 3.0f * yy);
-        }
-    }
-    const int K = sh_count(deg);
-    float acc[3] = {0.f, 0.f, 0.f};
-    for (int k = 0; k < K; ++k) {
-#pragma unroll
-        for (int c = 0; c < 3; ++c) acc[c] = fmaf(basis[k], __ldg(&p[(int64_t)(base + 3 * k + c) * cap + i]), acc[c]);
-    }
-    uint32_t clamped = 0;
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-        const float raw = acc[c] + 0.5f;
-        clamped |= (raw < 0.0f || raw > 1.0f) ? (1u << c) : 0u;
-        rgb[c] = fminf(fmaxf(raw, 0.0f), 1.0f);
-    }
-    return clamped;
-}
-
 __device__ inline uint32_t f32_bits(double d) { return __float_as_uint(__double2float_rn(d)); }
 
 // project_3d (raster.cpp:26-64).  Returns the cull reason (CULL_NONE when
@@ -367,36 +322,43 @@ __global__ void __launch_bounds__(256, 3) preprocess_kernel(
                 d[1] = v[1] / nrm;
                 d[2] = v[2] / nrm;
             }
+            // SH colour (sh.cpp:73-83, FP32) and, for the SH backward (K7b: it
+            // then needs no SH coefficient), the view direction, the
+            // clamped-channel mask and d rgb / d direction -- one channel at a
+            // time, each coefficient loaded once
             float rgb[3];
             const float fd[3] = {(float)d[0], (float)d[1], (float)d[2]};
-            const uint32_t clamped =
-                gid < n4 ? eval_sh_f32(p4, cap4, gid, R4_SH, deg, fd[0], fd[1], fd[2], rgb)
-                         : eval_sh_f32(p3, cap3, gid - n4, R3_SH, deg, fd[0], fd[1], fd[2], rgb);
-            // view direction, clamped-channel mask and d rgb / d direction for
-            // the SH backward (K7b): it then needs no SH coefficient
-            {
-                const float* P = gid < n4 ? p4 : p3;
-                const int64_t cap = gid < n4 ? cap4 : cap3;
-                const int i = gid < n4 ? gid : gid - n4;
-                const int shrow = gid < n4 ? R4_SH : R3_SH;
-                const int K = sh_count(deg);
-                ShRec sr;
-                sr.dir = make_float4(fd[0], fd[1], fd[2], __uint_as_float(clamped));
-                float* jr[3] = {&sr.j[0].x, &sr.j[1].x, &sr.j[2].x};
+            const float* P = gid < n4 ? p4 : p3;
+            const int64_t cap = gid < n4 ? cap4 : cap3;
+            const int i = gid < n4 ? gid : gid - n4;
+            const int shrow = gid < n4 ? R4_SH : R3_SH;
+            const int K = sh_count(deg);
+            float basis[16];
+            sh_basis_f(fd, deg, basis);
+            ShRec sr;
+            float* jr[3] = {&sr.j[0].x, &sr.j[1].x, &sr.j[2].x};
+            uint32_t clamped = 0;
 #pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    float w[16];
+            for (int c = 0; c < 3; ++c) {
+                float w[16];
 #pragma unroll
-                    for (int k = 0; k < 16; ++k) w[k] = k < K ? __ldg(&P[(int64_t)(shrow + 3 * k + c) * cap + i]) : 0.f;
-                    float g[3];
-                    sh_dir_grad_f(fd, deg, w, g);
-                    jr[c][0] = g[0];
-                    jr[c][1] = g[1];
-                    jr[c][2] = g[2];
-                    jr[c][3] = 0.f;
-                }
-                shrec[gid] = sr;
+                for (int k = 0; k < 16; ++k) w[k] = k < K ? __ldg(&P[(int64_t)(shrow + 3 * k + c) * cap + i]) : 0.f;
+                float acc = 0.f;
+#pragma unroll
+                for (int k = 0; k < 16; ++k)
+                    if (k < K) acc = fmaf(basis[k], w[k], acc);
+                const float raw = acc + 0.5f;  // raster.cpp:86 / sh.cpp:81
+                clamped |= (raw < 0.0f || raw > 1.0f) ? (1u << c) : 0u;
+                rgb[c] = fminf(fmaxf(raw, 0.0f), 1.0f);
+                float g[3];
+                sh_dir_grad_f(fd, deg, w, g);
+                jr[c][0] = g[0];
+                jr[c][1] = g[1];
+                jr[c][2] = g[2];
+                jr[c][3] = 0.f;
             }
+            sr.dir = make_float4(fd[0], fd[1], fd[2], __uint_as_float(clamped));
+            shrec[gid] = sr;
             s.alpha = alpha;
             s.alpha_f = (float)alpha;
             s.r = rgb[0];
