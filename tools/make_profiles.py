@@ -57,7 +57,7 @@ def summarize(rep):
     d = {}
     for r in det[1:]:
         d.setdefault(r[mi], r[vi])
-    kname = name.split("(")[0].replace("void ", "").split("::")[-1].split("<")[0].strip()
+    kname = name.split("(")[0].replace("void ", "").split("<")[0].split("::")[-1].strip()
     return {
         "kernel": kname,
         "duration_us": round(dur_ns * scale, 2) if dur_ns else None,
@@ -93,8 +93,8 @@ def main():
         summ[s["kernel"]] = s
         short = s["kernel"].split("::")[-1]
         with open(os.path.join(out_dir, f"{rnd}_{short}.txt"), "w") as f:
-            f.write(f"# ncu --set full --clock-control none --import-source on -k regex:{short} -s 1 -c 1\n")
-            f.write("#   python tools/prof_step.py   (c2 workload, 3rd training iteration)\n")
+            f.write(f"# ncu --set full --clock-control none --import-source on -k regex:{short} -s 2 -c 1\n")
+            f.write("#   python tools/prof_step.py   (c2 workload, 3rd training iteration; tools/prof_full.sh)\n")
             for k, val in s.items():
                 f.write(f"{k}: {val}\n")
     path = os.path.join(out_dir, "ncu_summary.json")
