@@ -115,6 +115,7 @@ typedef struct {
  * exact tile-ellipse culling, and pixels recomposited by the FP64 fix-up. */
 typedef struct {
     int64_t visible, instances, fixup_pixels, kept_instances;
+    int64_t sweep_redone_frames; /* hgs_render_sweep frames re-rendered after a capacity overflow (total) */
 } hgs_render_info;
 
 /* ---- lifecycle -------------------------------------------------------- */
@@ -143,6 +144,16 @@ hgs_status hgs_rasterize(hgs_ctx *ctx, const hgs_host_scene *scene, int dtype, c
 hgs_status hgs_render(hgs_ctx *ctx, const hgs_camera *cam, double t, const double bg[3],
                       const hgs_raster_opts *opts, float *rgb_host, uint32_t *count_host,
                       float *trans_host, hgs_render_stats *stats);
+/* Render sweep (config c5): n frames (cams[f], ts[f]) of the resident scene
+ * with no host round trip between them and one synchronisation at the end;
+ * out (optional; n * h * w * 3 floats, all cameras the same size) is a
+ * device pointer when out_on_device, else host memory; stats (optional) has
+ * n entries.  Identical images to n hgs_render calls: the instance buffers
+ * are sized from a capacity learned on the context, and a frame that
+ * exceeded it is re-rendered exactly before the call returns. */
+hgs_status hgs_render_sweep(hgs_ctx *ctx, int n, const hgs_camera *cams, const double *ts, const double bg[3],
+                            const hgs_raster_opts *opts, float *out, int out_on_device,
+                            hgs_render_stats *stats);
 /* Device pointer of the last rendered image (float, h*w*3), valid until the
  * next render on this context. */
 const float *hgs_last_image_device(hgs_ctx *ctx);

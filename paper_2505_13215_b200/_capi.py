@@ -70,7 +70,8 @@ class ConversionReport(C.Structure):
 
 
 class RenderInfo(C.Structure):
-    _fields_ = [(n, C.c_int64) for n in ("visible", "instances", "fixup_pixels", "kept_instances")]
+    _fields_ = [(n, C.c_int64) for n in ("visible", "instances", "fixup_pixels", "kept_instances",
+                                         "sweep_redone_frames")]
 
 
 class TrainOpts(C.Structure):
@@ -167,6 +168,8 @@ _SIGS = {
     "hgs_densify_plan": ([_vp, C.POINTER(DensifyCfg), _vp, _vp, C.POINTER(DensifyReport)], C.c_int),
     "hgs_densify_apply": ([_vp, _dp, _dp, C.c_double], C.c_int),
     "hgs_opacity_reset": ([_vp, C.c_double], C.c_int),
+    "hgs_render_sweep": ([_vp, C.c_int, C.POINTER(Camera_), _dp, _dp, C.POINTER(RasterOpts), _fp, C.c_int,
+                          C.POINTER(RenderStats)], C.c_int),
     "hgs_rng_create": ([C.c_uint64, C.POINTER(_vp)], C.c_int),
     "hgs_rng_destroy": ([_vp], None),
     "hgs_rng_raw": ([_vp], C.c_uint64),

@@ -230,6 +230,35 @@ class Context:
         return {"rgb": rgb, "counts": counts, "transmittance": trans,
                 "stats": {n: int(getattr(st, n)) for n, _ in _capi.RenderStats._fields_}}
 
+    def render_sweep(self, cameras: list, times: list, background=(0.0, 0.0, 0.0),
+                     weight_cutoff=DEFAULT_WEIGHT_CUTOFF, out=None, with_stats: bool = False):
+        """Render n frames (cameras[f], times[f]) with one synchronisation
+        (hgs_render_sweep; the c5 render sweep).  out: None (no image
+        output, e.g. timing), "host" (returns an (n, h, w, 3) float32
+        array) or a CUDA tensor / device pointer of n*h*w*3 floats."""
+        n = len(cameras)
+        cams = (_capi.Camera_ * max(1, n))(*[_capi.camera_struct(c) for c in cameras])
+        ts = (C.c_double * max(1, n))(*[float(t) for t in times])
+        bg = np.ascontiguousarray(background, dtype=np.float64)
+        o = _opts(weight_cutoff)
+        st = (_capi.RenderStats * max(1, n))() if with_stats else None
+        host = None
+        ptr_out, on_dev = None, 0
+        if isinstance(out, str) and out == "host":
+            h, w = cameras[0].height, cameras[0].width
+            host = np.empty((n, h, w, 3), dtype=np.float32)
+            ptr_out = host.ctypes.data_as(_capi._fp)
+        elif out is not None:
+            addr = out.data_ptr() if hasattr(out, "data_ptr") else int(out)
+            ptr_out, on_dev = C.cast(C.c_void_p(addr), _capi._fp), 1
+        self._check(self._lib.hgs_render_sweep(self._h, n, cams, ts, bg.ctypes.data_as(_capi._dp), C.byref(o),
+                                               ptr_out, on_dev, st))
+        if n:
+            self._last_shape = (cameras[-1].height, cameras[-1].width)
+        stats = [{k: int(getattr(x, k)) for k, _ in _capi.RenderStats._fields_} for x in st[:n]] if with_stats else None
+        res = host if host is not None else out
+        return (res, stats) if with_stats else res
+
     def render_device(self, camera: Camera, t: float, background=(0.0, 0.0, 0.0),
                       weight_cutoff=DEFAULT_WEIGHT_CUTOFF) -> None:
         """Render into the context's device image only (no host copy); read

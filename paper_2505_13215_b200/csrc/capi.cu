@@ -259,7 +259,7 @@ void prof_collect(hgs_ctx* ctx) {
 // ====================================================================== render
 // The full K1 -> sort -> K2 -> sort -> K4 pipeline; leaves the tape in ctx.
 hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, const double bg[3],
-                               const hgs_raster_opts* opts, int deferred) {
+                               const hgs_raster_opts* opts, int deferred, uint32_t icap, void* counters_slot) {
     std::string why;
     if (!camera_valid(cam, why)) return fail(ctx, HGS_ERR_INVALID_ARGUMENT, why);
     const double cutoff = opts ? opts->weight_cutoff : 0.05;
@@ -283,9 +283,13 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
     const size_t npx = (size_t)W * H;
     CK(ctx->counters.ensure(sizeof(Counters)));
     CK(ctx->pinned_ctr.ensure(sizeof(Counters) + 64));
-    Counters* dc = ctx->counters.as<Counters>();
+    Counters* dc = counters_slot ? static_cast<Counters*>(counters_slot) : ctx->counters.as<Counters>();
     Counters* hc = static_cast<Counters*>(ctx->pinned_ctr.p);
     CK(cudaMemsetAsync(dc, 0, sizeof(Counters), st));
+    // capacity mode (icap > 0): no host round trip -- the duplication runs on
+    // buffers for icap instances and flags FLAG_CAPACITY if that was too few
+    // (the caller re-renders); only the production (culled) path supports it
+    if (want_count || ctx->debug_full_list) icap = 0;
     CK(ctx->img.ensure(npx * 3 * sizeof(float)));
     CK(ctx->last.ensure(npx * sizeof(uint32_t)));
     CK(ctx->tfinal.ensure(npx * sizeof(float)));
@@ -355,15 +359,20 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
                            ctx->scan_ws.as<uint32_t>(), st, &dc->V);
         CKL();
         prof_end(ctx);
-        // the one host round trip of a render: the instance count sizes the
-        // duplication buffers; the preprocess error flags are reported here,
-        // before anything downstream runs (the reference throws in K1)
-        CK(cudaMemcpyAsync(hc, dc, sizeof(Counters), cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-        V = hc->V;
-        I = V ? hc->I : 0;
-        hgs_status fs = check_flags(ctx, hc->flags);
-        if (fs != HGS_OK) return fs;
+        if (icap) {
+            V = N;  // bounds only; the kernels read the true counts on the device
+            I = icap;
+        } else {
+            // the one host round trip of a render: the instance count sizes the
+            // duplication buffers; the preprocess error flags are reported here,
+            // before anything downstream runs (the reference throws in K1)
+            CK(cudaMemcpyAsync(hc, dc, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            V = hc->V;
+            I = V ? hc->I : 0;
+            hgs_status fs = check_flags(ctx, hc->flags);
+            if (fs != HGS_OK) return fs;
+        }
     }
     ctx->V = V;
     ctx->I = I;
@@ -375,7 +384,7 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
         CK(ctx->inst_v2.ensure((size_t)I * 4));
         const int cull = want_count ? 0 : 1;  // count_map counts every box-covered splat
         const uint32_t dup_blocks = div_up((uint32_t)I, kDupPerCtaHost);
-        CK(ctx->dup_first.ensure((size_t)dup_blocks * 4));
+        CK(ctx->dup_first.ensure((size_t)(dup_blocks + 1) * 4));
         if (cull && !ctx->debug_full_list) {
             // production path: duplication + exact culling + order-preserving
             // compaction in one kernel, then the stable tile sort of the kept
@@ -385,12 +394,14 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
             uint32_t* counter = reinterpret_cast<uint32_t*>(status + dup_blocks);
             CK(cudaMemsetAsync(status, 0, (size_t)dup_blocks * 8 + 4, st));
             dup_bounds_kernel<<<div_up((uint32_t)V, 256), 256, 0, st>>>(
-                ctx->inst_off.as<uint32_t>(), ctx->ntiles_sorted.as<uint32_t>(), (int)V, ctx->dup_first.as<uint32_t>());
+                ctx->inst_off.as<uint32_t>(), ctx->ntiles_sorted.as<uint32_t>(), (int)V, ctx->dup_first.as<uint32_t>(),
+                icap ? &dc->V : nullptr, dup_blocks);
             count_launch();
             duplicate_compact_kernel<<<dup_blocks, 256, 0, st>>>(
                 ctx->fast_sorted.as<SplatFast>(), (int)V, ctx->inst_off.as<uint32_t>(), tiles_x,
                 ctx->pcut.as<CullRec>(), ctx->dup_first.as<uint32_t>(), (int)I, ctx->inst_k2.as<uint32_t>(),
-                ctx->inst_v2.as<uint32_t>(), &dc->I_kept, status, counter);
+                ctx->inst_v2.as<uint32_t>(), &dc->I_kept, status, counter, icap ? &dc->V : nullptr,
+                icap ? &dc->I : nullptr, &dc->flags);
             count_launch();
             CKL();
             prof_end(ctx);
@@ -417,7 +428,8 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
             CK(ctx->inst_pos.ensure((size_t)I * 4));
         }
         dup_bounds_kernel<<<div_up((uint32_t)V, 256), 256, 0, st>>>(
-            ctx->inst_off.as<uint32_t>(), ctx->ntiles_sorted.as<uint32_t>(), (int)V, ctx->dup_first.as<uint32_t>());
+            ctx->inst_off.as<uint32_t>(), ctx->ntiles_sorted.as<uint32_t>(), (int)V, ctx->dup_first.as<uint32_t>(),
+            nullptr, dup_blocks);
         count_launch();
         duplicate_kernel<<<dup_blocks, 256, 0, st>>>(
             ctx->fast_sorted.as<SplatFast>(), ctx->rec_sorted.as<SplatRec>(), (int)V, ctx->inst_off.as<uint32_t>(),
@@ -618,12 +630,13 @@ void hgs_ctx_destroy(hgs_ctx* ctx) {
                     &ctx->sort_v2, &ctx->rec_sorted, &ctx->fast_sorted, &ctx->ntiles_sorted, &ctx->inst_off,
                     &ctx->inst_k, &ctx->inst_v, &ctx->inst_k2, &ctx->inst_v2, &ctx->ranges, &ctx->sorted_of_gid, &ctx->inst_flag, &ctx->inst_pos, &ctx->dbg_k, &ctx->dbg_v, &ctx->scan_ws,
                     &ctx->sort_ws, &ctx->counters, &ctx->img, &ctx->last, &ctx->tfinal, &ctx->trans, &ctx->count,
-                    &ctx->fix_list, &ctx->accum, &ctx->lgrad, &ctx->gt_stage, &ctx->loss_ws, &ctx->stage, &ctx->adam_ok, &ctx->pcut, &ctx->dup_first, &ctx->shdir, &ctx->ddir, &ctx->dup_status, &ctx->gpack, &ctx->dens_cat, &ctx->dens_u32, &ctx->dens_misc, &ctx->dens_kinds, &ctx->dens_jit, &ctx->dmap, &ctx->ckpt, &ctx->crc_tab, &ctx->comm_buf};
+                    &ctx->fix_list, &ctx->accum, &ctx->lgrad, &ctx->gt_stage, &ctx->loss_ws, &ctx->stage, &ctx->adam_ok, &ctx->pcut, &ctx->dup_first, &ctx->shdir, &ctx->ddir, &ctx->dup_status, &ctx->gpack, &ctx->dens_cat, &ctx->dens_u32, &ctx->dens_misc, &ctx->dens_kinds, &ctx->dens_jit, &ctx->dmap, &ctx->ckpt, &ctx->crc_tab, &ctx->comm_buf, &ctx->sweep_ctr};
     for (DBuf* b : bufs) b->release();
     ctx->pinned.release();
     ctx->pinned_ctr.release();
     ctx->pinned_pipe.release();
     ctx->ckpt_host.release();
+    ctx->sweep_host.release();
     for (int k = 0; k < HGS_TRAIN_PIPELINE; ++k)
         if (ctx->pipe_ev[k]) cudaEventDestroy(ctx->pipe_ev[k]);
     for (int b = 0; b < 2; ++b) {
@@ -684,6 +697,7 @@ hgs_status hgs_scene_alloc(hgs_ctx* ctx, int64_t n4, int64_t n3, int deg, double
     ctx->step = 0;
     ctx->have_tape = false;
     ctx->stats_pending = false;
+    ctx->icap = 0;
     const uint64_t zero = 0;
     return hgs_skipped_total(ctx, nullptr, &zero);
 }
@@ -781,6 +795,105 @@ hgs_status hgs_scene_counts(hgs_ctx* ctx, int64_t* n4, int64_t* n3, int32_t* deg
     return HGS_OK;
 }
 
+// Render sweep (config c5: one scene, many (camera, t) frames): every frame in
+// capacity mode -- no host round trip inside the sweep, one synchronisation
+// at its end.  The instance capacity is learned from a synchronous first
+// frame (and kept on the context); a frame that overflowed it is redone
+// synchronously at the end with the exact size, so the outputs are always
+// those of hgs_render.
+hgs_status hgs_render_sweep(hgs_ctx* ctx, int n, const hgs_camera* cams, const double* ts, const double bg[3],
+                            const hgs_raster_opts* opts, float* out, int out_on_device, hgs_render_stats* stats) {
+    if (!ctx || n < 0 || (n > 0 && (!cams || !ts)) || !bg) return HGS_ERR_INVALID_ARGUMENT;
+    CK(cudaSetDevice(ctx->device));
+    hgs_status r = hgs_render_finish(ctx);
+    if (r != HGS_OK) return r;
+    if (n == 0) return HGS_OK;
+    std::string why;
+    for (int f = 0; f < n; ++f) {
+        if (!camera_valid(&cams[f], why)) return fail(ctx, HGS_ERR_INVALID_ARGUMENT, why);
+        if (out && (cams[f].width != cams[0].width || cams[f].height != cams[0].height))
+            return fail(ctx, HGS_ERR_INVALID_ARGUMENT, "render_sweep: frames of one output differ in size");
+    }
+    cudaStream_t st = ctx->stream;
+    const size_t npx = (size_t)cams[0].width * cams[0].height;
+    CK(ctx->sweep_ctr.ensure((size_t)n * sizeof(Counters)));
+    CK(ctx->sweep_host.ensure((size_t)n * sizeof(Counters)));
+    Counters* slots = ctx->sweep_ctr.as<Counters>();
+    Counters* hs = static_cast<Counters*>(ctx->sweep_host.p);
+    auto emit = [&](int f) -> cudaError_t {
+        if (!out) return cudaSuccess;
+        return cudaMemcpyAsync(out + (size_t)f * npx * 3, ctx->img.p, npx * 3 * 4,
+                               out_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st);
+    };
+    int f0 = 0;
+    if (ctx->icap == 0) {  // learn the capacity from a synchronous first frame
+        r = hgs_render_pipeline(ctx, &cams[0], ts[0], bg, opts, 1, 0, &slots[0]);
+        if (r != HGS_OK) return r;
+        ctx->icap = (uint32_t)std::min<int64_t>(INT32_MAX / 2, std::max<int64_t>(4096, ctx->I + ctx->I / 4 + 4096));
+        CK(emit(0));
+        f0 = 1;
+    }
+    for (int f = f0; f < n; ++f) {
+        r = hgs_render_pipeline(ctx, &cams[f], ts[f], bg, opts, 1, ctx->icap, &slots[f]);
+        if (r != HGS_OK) return r;
+        CK(emit(f));
+    }
+    CK(cudaMemcpyAsync(hs, slots, (size_t)n * sizeof(Counters), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    prof_collect(ctx);
+    ctx->stats_pending = false;
+    uint32_t need = 0;
+    for (int f = 0; f < n; ++f)
+        if (hs[f].flags & FLAG_CAPACITY) need = std::max(need, hs[f].I);
+    if (need) {  // redo the overflowed frames exactly, keep the larger capacity
+        ctx->icap = (uint32_t)std::min<int64_t>(INT32_MAX / 2, (int64_t)need + need / 4 + 4096);
+        for (int f = 0; f < n; ++f) {
+            if (!(hs[f].flags & FLAG_CAPACITY)) continue;
+            r = hgs_render_pipeline(ctx, &cams[f], ts[f], bg, opts, 1, 0, &slots[f]);
+            if (r != HGS_OK) return r;
+            CK(emit(f));
+            CK(cudaMemcpyAsync(&hs[f], &slots[f], sizeof(Counters), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            ctx->redone_frames++;
+        }
+        // the context's tape is the last frame's: render it again if it was not redone
+        if (!(hs[n - 1].flags & FLAG_CAPACITY) && n > 1) {
+            r = hgs_render_pipeline(ctx, &cams[n - 1], ts[n - 1], bg, opts, 1, 0, &slots[n - 1]);
+            if (r != HGS_OK) return r;
+            CK(cudaMemcpyAsync(&hs[n - 1], &slots[n - 1], sizeof(Counters), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+        }
+    }
+    for (int f = 0; f < n; ++f) {
+        r = check_flags(ctx, hs[f].flags);
+        if (r != HGS_OK) {
+            ctx->have_tape = false;
+            return r;
+        }
+        if (stats) {
+            hgs_render_stats& o = stats[f];
+            o.culled_depth = (int64_t)hs[f].stats[0];
+            o.culled_offscreen = (int64_t)hs[f].stats[1];
+            o.culled_degenerate = (int64_t)hs[f].stats[2];
+            o.culled_temporal = (int64_t)hs[f].stats[3];
+            o.degenerate_temporal = (int64_t)hs[f].stats[4];
+            o.projected = (int64_t)hs[f].stats[5];
+        }
+    }
+    const Counters& last = hs[n - 1];
+    ctx->stats.culled_depth = (int64_t)last.stats[0];
+    ctx->stats.culled_offscreen = (int64_t)last.stats[1];
+    ctx->stats.culled_degenerate = (int64_t)last.stats[2];
+    ctx->stats.culled_temporal = (int64_t)last.stats[3];
+    ctx->stats.degenerate_temporal = (int64_t)last.stats[4];
+    ctx->stats.projected = (int64_t)last.stats[5];
+    ctx->fixups = last.fix_count;
+    ctx->kept = last.I_kept;
+    ctx->V = last.V;
+    ctx->I = last.I;
+    return HGS_OK;
+}
+
 hgs_status hgs_render(hgs_ctx* ctx, const hgs_camera* cam, double t, const double bg[3], const hgs_raster_opts* opts,
                       float* rgb_host, uint32_t* count_host, float* trans_host, hgs_render_stats* stats) {
     if (!ctx || !cam || !bg) return HGS_ERR_INVALID_ARGUMENT;
@@ -835,6 +948,7 @@ hgs_status hgs_render_info_get(hgs_ctx* ctx, hgs_render_info* info) {
     info->instances = ctx->I;
     info->fixup_pixels = ctx->fixups;
     info->kept_instances = ctx->kept;
+    info->sweep_redone_frames = ctx->redone_frames;
     return HGS_OK;
 }
 

@@ -146,6 +146,10 @@ struct hgs_ctx {
     void* comm = nullptr;        // ncclComm_t of the view-parallel exchange (comm.cu)
     int comm_rank = 0, comm_size = 1;
     hgs::DBuf comm_buf;          // small staging for collectives / checksums
+    uint32_t icap = 0;           // instance capacity of capacity-mode renders (hgs_render_sweep)
+    int64_t redone_frames = 0;   // sweep frames re-rendered after a capacity overflow
+    hgs::DBuf sweep_ctr;         // per-frame Counters of a sweep
+    hgs::HostPinned sweep_host;
     hgs::HostPinned ckpt_host;   // checkpoint file image
     hgs::HostPinned pinned;      // Scratch read-back (training / loss)
     hgs::HostPinned pinned_ctr;  // Counters read-back (render)

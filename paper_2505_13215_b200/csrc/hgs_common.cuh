@@ -74,6 +74,7 @@ enum : uint32_t {
     FLAG_NONUNIT_DIR = 4u,      // eval_sh would throw (sh.cpp:74-75)
     FLAG_DEGENERATE_ROT = 8u,   // extract_spatial_rot would throw (gauss_math.cpp:191-192)
     FLAG_NOT_ROTATION = 16u,    // rot3_to_quat would throw (gauss_math.cpp:71-72)
+    FLAG_CAPACITY = 32u,        // a capacity-mode render had more instances than its buffers
 };
 
 inline __host__ __device__ uint32_t div_up(uint32_t a, uint32_t b) { return (a + b - 1) / b; }

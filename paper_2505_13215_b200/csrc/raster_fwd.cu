@@ -139,13 +139,18 @@ __device__ __forceinline__ int last_le(const uint32_t* __restrict__ off, int lo,
 
 // cta_first[b] = the sorted splat owning instance b * kDupPerCta (each CTA
 // boundary lies in exactly one splat's [offset, offset + ntiles) range).
+// V_dev (optional): the visible count on the device (capacity-mode renders
+// launch for N); nblocks bounds the writes (cta_first has nblocks + 1 entries:
+// the CTAs of the capacity and the first splat past it).
 __global__ void __launch_bounds__(256) dup_bounds_kernel(const uint32_t* __restrict__ offsets,
                                                          const uint32_t* __restrict__ ntiles_sorted, int V,
-                                                         uint32_t* __restrict__ cta_first) {
+                                                         uint32_t* __restrict__ cta_first, const uint32_t* V_dev,
+                                                         uint32_t nblocks) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= V) return;
+    if (j >= (V_dev ? (int)*V_dev : V)) return;
     const uint32_t o = offsets[j], n = ntiles_sorted[j];
-    for (uint32_t b = (o + kDupPerCta - 1) / kDupPerCta; b * kDupPerCta < o + n; ++b) cta_first[b] = (uint32_t)j;
+    for (uint32_t b = (o + kDupPerCta - 1) / kDupPerCta; b * kDupPerCta < o + n && b <= nblocks; ++b)
+        cta_first[b] = (uint32_t)j;
 }
 
 // One instance i of the CTA's range: tile key and value (sorted splat index |
@@ -201,16 +206,30 @@ __global__ void __launch_bounds__(kDupThreads) duplicate_compact_kernel(
     const SplatFast* __restrict__ fast, int V, const uint32_t* __restrict__ offsets, int tiles_x,
     const CullRec* __restrict__ cull_rec, const uint32_t* __restrict__ cta_first, int I,
     uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out, uint32_t* __restrict__ kept_total,
-    unsigned long long* status, uint32_t* __restrict__ counter) {
+    unsigned long long* status, uint32_t* __restrict__ counter, const uint32_t* V_dev, const uint32_t* I_dev,
+    uint32_t* flags) {
     __shared__ uint32_t s_off[kDupPerCta + 1];
     __shared__ uint32_t s_tile, s_excl, s_wt[kDupThreads / 32];
     if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1u);
     __syncthreads();
+    // capacity mode (I_dev set): I is the launch capacity, the true count is on
+    // the device; beyond the capacity the render is flagged (and redone by the host)
+    if (V_dev) V = (int)*V_dev;
+    int I_all = I;  // every instance (capacity mode: may exceed the launch capacity I)
+    if (I_dev) {
+        I_all = (int)*I_dev;
+        if (I_all > I) {
+            if (s_tile == 0 && threadIdx.x == 0) atomicOr(flags, FLAG_CAPACITY);
+        } else {
+            I = I_all;
+        }
+    }
     const int tile = (int)s_tile;
     const int i0 = tile * kDupPerCta;
+    if (i0 >= I) return;  // CTAs of the capacity beyond the instances (nothing looks back at them)
     const int i_end = min(i0 + kDupPerCta, I);
     const int j_lo = (int)cta_first[tile];
-    const int j_hi = i_end < I ? (int)cta_first[tile + 1] : V - 1;
+    const int j_hi = i_end < I_all ? (int)cta_first[tile + 1] : V - 1;
     const int cnt = j_hi - j_lo + 1;
     for (int k = threadIdx.x; k < cnt; k += kDupThreads) s_off[k] = __ldg(&offsets[j_lo + k]);
     __syncthreads();

@@ -1,0 +1,79 @@
+"""hgs_render_sweep (config c5's render sweep over t): capacity-mode renders
+without host round trips give exactly the images and RenderStats of
+per-frame hgs_render calls, including frames that overflow the learned
+instance capacity (re-rendered exactly before the call returns)."""
+import numpy as np
+import pytest
+
+from paper_2505_13215_b200 import api as A
+from paper_2505_13215_b200.scene import Camera, ring_camera, synthetic_scene
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = A.Context(0)
+    yield c
+    c.close()
+
+
+def per_frame(ctx, cams, ts, bg):
+    imgs, stats = [], []
+    for c, t in zip(cams, ts):
+        o = ctx.render(c, t, bg)
+        imgs.append(o["rgb"])
+        stats.append(o["stats"])
+    return np.stack(imgs), stats
+
+
+def test_sweep_equals_per_frame_renders(ctx):
+    scene = synthetic_scene(40000, 20000, sh_degree=3, seed=8).as_float32_exact()
+    ctx.upload(scene)
+    cams = [ring_camera(8, 320, 240, index=i % 6, n_ring=6) for i in range(12)]
+    ts = [j / 11.0 for j in range(12)]
+    bg = (0.2, 0.3, 0.4)
+    ref, ref_stats = per_frame(ctx, cams, ts, bg)
+    got, stats = ctx.render_sweep(cams, ts, bg, out="host", with_stats=True)
+    assert np.array_equal(got, ref)
+    assert stats == ref_stats
+    got2 = ctx.render_sweep(cams, ts, bg, out="host")  # learned capacity, no first synchronous frame
+    assert np.array_equal(got2, ref)
+
+
+def test_sweep_capacity_overflow_is_redone(ctx):
+    scene = synthetic_scene(40000, 20000, sh_degree=2, seed=9).as_float32_exact()
+    ctx.upload(scene)  # resets the learned capacity
+    away = Camera.look_at([0, 0, -40], [0, 0, -80], [0, -1, 0], 300.0, 320, 240)  # sees (almost) nothing
+    cams = [away] + [ring_camera(9, 320, 240, index=i, n_ring=5) for i in range(5)]
+    ts = [0.5] * 6
+    before = ctx.render_info()["sweep_redone_frames"]
+    ref, _ = per_frame(ctx, cams, ts, (0, 0, 0))
+    got = ctx.render_sweep(cams, ts, (0, 0, 0), out="host")
+    assert np.array_equal(got, ref)
+    assert ctx.render_info()["sweep_redone_frames"] > before
+    # the grown capacity holds now
+    mid = ctx.render_info()["sweep_redone_frames"]
+    got = ctx.render_sweep(cams[1:], ts[1:], (0, 0, 0), out="host")
+    assert np.array_equal(got, ref[1:])
+    assert ctx.render_info()["sweep_redone_frames"] == mid
+
+
+def test_sweep_device_output_and_errors(ctx):
+    import torch
+
+    scene = synthetic_scene(20000, 10000, sh_degree=1, seed=10).as_float32_exact()
+    ctx.upload(scene)
+    cams = [ring_camera(10, 160, 120, index=i, n_ring=4) for i in range(4)]
+    ts = [0.1, 0.4, 0.6, 0.9]
+    ref, _ = per_frame(ctx, cams, ts, (0, 0, 0))
+    out = torch.zeros((4, 120, 160, 3), dtype=torch.float32, device="cuda")
+    ctx.render_sweep(cams, ts, (0, 0, 0), out=out)
+    assert np.array_equal(out.cpu().numpy(), ref)
+    with pytest.raises(ValueError):
+        ctx.render_sweep(cams + [ring_camera(10, 80, 60)], ts + [0.5], (0, 0, 0), out="host")
+    bad = scene.copy()
+    bad.quat3[5] = [2.0, 0.0, 0.0, 0.0]
+    ctx.upload(bad)
+    with pytest.raises(ValueError, match="quaternion"):
+        ctx.render_sweep(cams, ts, (0, 0, 0))
