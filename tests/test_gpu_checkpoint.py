@@ -179,3 +179,21 @@ def test_checkpoint_of_larger_scene_renders_identically(ctx, tmp_path):
     ctx.upload(HybridScene())
     ctx.load_checkpoint(p)
     assert np.array_equal(ctx.render(cam, 0.3)["rgb"], img)
+
+
+def test_device_load_of_golden_file(ctx, tmp_path):
+    """tests/golden/ckpt_small.hgsc (frozen bytes) through the CUDA decoder."""
+    import os
+
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "ckpt_small.hgsc")
+    ref_scene, ref_state = CK.decode_checkpoint(open(path, "rb").read())
+    assert ctx.load_checkpoint(path) is True
+    got, st = ctx.download(), device_state(ctx)
+    for f in FIELDS:
+        assert np.array_equal(getattr(got, f), getattr(ref_scene, f).astype(np.float32).astype(np.float64)), f
+        assert np.array_equal(getattr(st.m, f), getattr(ref_state.m, f).astype(np.float32).astype(np.float64)), f
+    assert st.step == 321
+    q = tmp_path / "re.hgsc"
+    ctx.save_checkpoint(str(q))
+    _, st2 = CK.load_checkpoint(str(q))
+    assert st2.skipped_nonfinite == 4 and np.array_equal(st2.count3, ref_state.count3)
