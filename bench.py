@@ -212,17 +212,23 @@ def run_ours(args) -> None:
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dist = None
-    if world > 1:
+    vp = world > 1 or args.view_parallel  # the view-parallel code path (also at N=1 with --view-parallel)
+    if vp:
         import torch.distributed as dist
 
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29631")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     scene, target, cams, times, desc = workload(args.config)
     ctx = Context(local)
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream.cuda_stream)
     kw = dict(target=target, bg=(0.2, 0.2, 0.2), iterations=max(1000, args.steps * 10))
-    tr = ViewParallelTrainer(ctx, scene, cams, times, **kw) if world > 1 else DeviceTrainer(ctx, scene, cams, times,
-                                                                                             **kw)
+    tr = (ViewParallelTrainer(ctx, scene, cams, times, exchange="capi", **kw) if vp
+          else DeviceTrainer(ctx, scene, cams, times, **kw))
 
     def batch(step):
         return [(step * world + r) % len(cams) for r in range(world)]
@@ -256,10 +262,11 @@ def run_ours(args) -> None:
         barrier()
         return ms
 
-    # 1 GPU: pipelined iterations (hgs_train_step_async): iteration i is
-    # enqueued before iteration i-1's loss is read back (hgs_train_collect),
-    # every loss is read inside the timed region.  N GPUs: synchronous steps
-    # around the NCCL all-reduce.
+    # Pipelined iterations (hgs_train_step_async): iteration i is enqueued
+    # before iteration i-1's loss is read back (hgs_train_collect), every loss
+    # is read inside the timed region.  N GPUs: the same, each rank's view
+    # followed by hgs_train_exchange_async (NCCL all-reduce of the loss gate
+    # and the packed gradients, gated Adam) -- no host synchronisation.
     def pending():
         return lib.hgs_train_pending(ctx.handle)
 
@@ -273,18 +280,23 @@ def run_ours(args) -> None:
         if pending() > 1:
             tr.collect()
 
+    def step_ngpu(i, gt_host=None):
+        b = batch(i)
+        tr.step_async(b, gt_host=None if gt_host is None else [gt_host[b[rank]]])
+        if pending() > 1:
+            tr.collect()
+
     lib = _capi.lib()
-    step_fn = (lambda i: tr.step(batch(i))) if world > 1 else step_1gpu
+    step_fn = step_ngpu if vp else step_1gpu
     for i in range(args.warmup):
         step_fn(i)
-    if world == 1:
-        drain()
+    drain()
     # ---- device-resident timed region (the headline; no instrumentation)
     l0 = _capi.lib().hgs_launch_count()
     with ClockSampler(local) as clk:
         # NVTX range "timed": `ncu --nvtx --nvtx-include timed/` lists exactly these launches
         torch.cuda.nvtx.range_push("timed")
-        ms = timed(lambda i: step_fn(args.warmup + i), args.steps, drain if world == 1 else None)
+        ms = timed(lambda i: step_fn(args.warmup + i), args.steps, drain)
         torch.cuda.nvtx.range_pop()
     launches = _capi.lib().hgs_launch_count() - l0
     import ctypes as C
@@ -295,7 +307,7 @@ def run_ours(args) -> None:
     if not args.no_phase_profile:
         _capi.lib().hgs_profile(ctx.handle, 1)
         _capi.lib().hgs_profile_read(ctx.handle, None, None, 1)
-        timed(lambda i: step_fn(args.warmup + args.steps + i), args.steps, drain if world == 1 else None)
+        timed(lambda i: step_fn(args.warmup + args.steps + i), args.steps, drain)
         ph = (C.c_double * 16)()
         _capi.lib().hgs_profile_read(ctx.handle, ph, None, 1)
         _capi.lib().hgs_profile(ctx.handle, 0)
@@ -314,31 +326,13 @@ def run_ours(args) -> None:
         g.copy_(torch.as_tensor(linear_to_srgb8(tr.gt[i].cpu().numpy().astype(np.float64))))
     lib = _capi.lib()
 
-    def e2e_step(i):
-        views = batch(args.warmup + args.steps + i)
-        mine = [views[rank]] if world > 1 else [views[0]]
-        n = len(mine)
-        karr = (_capi.Camera_ * n)(*[tr._cams[v] for v in mine])
-        tarr = (C.c_double * n)(*[times[v] for v in mine])
-        garr = (C.c_void_p * n)(*[C.c_void_p(gts_host[v].data_ptr()) for v in mine])
-        loss = C.c_double()
-        tr.iter += 1
-        ctx._check(lib.hgs_train_step_host(ctx.handle, n, karr, tarr, garr, _capi.HGS_U8, world,
-                                           C.byref(tr._opts(tr.decay())), 0 if world > 1 else 1, C.byref(loss)))
-        if world > 1:
-            g = tr.packed_grads_tensor()
-            dist.all_reduce(g)
-            ctx.grads_unpack()
-            ctx.adam_step(tr.lrs, tr.decay())
+    def e2e_step(i):  # pipelined like the device loop, host GT frames
+        step_fn(args.warmup + args.steps + i, gt_host=gts_host)
 
-    if world == 1:
-        def e2e_step(i):  # noqa: F811 -- pipelined like the device loop, host GT frames
-            step_1gpu(args.warmup + args.steps + i, gt_host=gts_host)
     for i in range(args.warmup):  # untimed: the copy stream and GT buffers are created on first use
         e2e_step(-1 - i)
-    if world == 1:
-        drain()
-    e2e_ms = timed(e2e_step, args.steps, drain if world == 1 else None)
+    drain()
+    e2e_ms = timed(e2e_step, args.steps, drain)
     e2e_value = world * args.steps / (e2e_ms / 1e3)
 
     # ---- forward-only render throughput (Mpix/s), device resident: one
@@ -375,10 +369,11 @@ def run_ours(args) -> None:
                "config": dict(desc, parallelism=f"view-parallel dp{world}", views_per_iteration=world),
                "e2e": {"value": round(e2e_value, 3), "unit": UNIT,
                        "h2d_bytes_per_step": int(W * H * 3),  # one 8-bit sRGB frame
-                       "d2h_bytes_per_step": 16 if world == 1 else 96,  # loss sums (+ counters when synchronous)
+                       "d2h_bytes_per_step": 16 if not vp else 24,  # loss sums (+ the all-reduced gate)
                        "path": ("hgs_train_step_async with a host 8-bit sRGB GT frame + hgs_train_collect "
-                                "(pinned host frame in, loss out, every iteration)") if world == 1 else
-                               "hgs_train_step_host (pinned host 8-bit GT frame in, loss out)"},
+                                "(pinned host frame in, loss out, every iteration)") if not vp else
+                               ("hgs_train_step_async (pinned host 8-bit GT frame) + hgs_train_exchange_async "
+                                "(NCCL all-reduce, gated Adam) + hgs_train_collect")},
                "render": {"value": round(render_mpix, 2), "unit": "Mpix/s",
                           "what": "forward render of the device-resident c2 scene, 1352x1014 (hgs_render_sweep "
                                   "of K frames, one synchronisation)"},
@@ -676,6 +671,8 @@ def main():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip the c1/c5 render and c4 training lines")
+    ap.add_argument("--view-parallel", action="store_true",
+                    help="use the N-GPU code path (NCCL exchange) even on one GPU (a one-rank communicator)")
     ap.add_argument("--no-phase-profile", action="store_true",
                     help="no per-phase CUDA events in the timed region (roofline.kernels then empty)")
     args = ap.parse_args()

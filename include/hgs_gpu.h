@@ -398,6 +398,14 @@ hgs_status hgs_train_step_async(hgs_ctx *ctx, int n_views, const hgs_camera *cam
                                 const void *const *gt, int dtype, int gt_on_device, int batch_total,
                                 const hgs_train_opts *opts, int apply_adam);
 hgs_status hgs_train_collect(hgs_ctx *ctx, double *loss_out);
+
+/* Pipelined view-parallel iteration: after hgs_train_step_async(...,
+ * apply_adam = 0) for this rank's views, hgs_train_exchange_async all-reduces
+ * the loss-sum gate and the packed gradients and enqueues the Adam step gated
+ * on the all-reduced loss (every rank skips a non-finite batch together) --
+ * no host synchronisation; hgs_train_collect later returns this rank's loss
+ * and raises NumericAbort on every rank for the same iteration. */
+hgs_status hgs_train_exchange_async(hgs_ctx *ctx, const hgs_train_opts *opts);
 /* Number of enqueued iterations not collected yet. */
 int hgs_train_pending(hgs_ctx *ctx);
 

@@ -206,6 +206,7 @@ _SIGS = {
     "hgs_train_step_async": ([_vp, C.c_int, C.POINTER(Camera_), _dp, C.POINTER(_vp), C.c_int, C.c_int, C.c_int,
                               C.POINTER(TrainOpts), C.c_int], C.c_int),
     "hgs_train_collect": ([_vp, _dp], C.c_int),
+    "hgs_train_exchange_async": ([_vp, C.POINTER(TrainOpts)], C.c_int),
     "hgs_train_pending": ([_vp], C.c_int),
     "hgs_profile": ([_vp, C.c_int], C.c_int),
     "hgs_profile_read": ([_vp, _dp, C.POINTER(C.c_longlong), C.c_int], C.c_int),

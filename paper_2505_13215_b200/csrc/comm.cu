@@ -113,6 +113,15 @@ __global__ void checksum_kernel(const float* __restrict__ p, int64_t cap, int64_
 
 }  // namespace
 
+hgs_status comm_allreduce_f64_dev(hgs_ctx* ctx, double* dev, int n) {
+    hgs_status r = need_comm(ctx);
+    if (r != HGS_OK) return r;
+    if (n > 0)
+        CKN(nccl().AllReduce(dev, dev, (size_t)n, ncclFloat64, ncclSum, static_cast<ncclComm_t>(ctx->comm),
+                             ctx->stream));
+    return HGS_OK;
+}
+
 extern "C" {
 
 hgs_status hgs_comm_unique_id(hgs_comm_id* out) {

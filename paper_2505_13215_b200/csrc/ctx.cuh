@@ -77,6 +77,7 @@ struct hgs_pending_step {
     int dims[32][2] = {};  // per view (W, H)
     double lambda = 0.2;
     bool adam = false;
+    bool dist = false;  // completed by hgs_train_exchange_async (all-reduced abort decision)
     uint64_t step_before = 0;
 };
 

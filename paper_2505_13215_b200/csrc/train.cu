@@ -32,7 +32,20 @@ struct Scratch {
     uint32_t pad2;
     double pipe_sums[HGS_TRAIN_PIPELINE][kMaxStepViews][2];  // loss sums of pipelined iterations
     unsigned long long skipped_cum;  // rows skipped for non-finite gradients since upload / load
+    double pipe_gate[HGS_TRAIN_PIPELINE][2];  // view-parallel: all-reduced sum of every rank's loss sums, 0
 };
+
+// sum of the n loss sums of a step (non-finite iff one of them is) -> gate[0], gate[1] = 0
+__global__ void gate_sum_kernel(const double* __restrict__ sums, int n, double* __restrict__ gate) {
+    double v = 0.0;
+    for (int i = threadIdx.x; i < n; i += 32) v += sums[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) {
+        gate[0] = v;
+        gate[1] = 0.0;
+    }
+}
 static_assert(kMaxStepViews == 32, "hgs_pending_step::dims");
 
 hgs_status fail(hgs_ctx* ctx, hgs_status s, const std::string& m) {
@@ -673,7 +686,7 @@ hgs_status train_step_impl(hgs_ctx* ctx, int n_views, const hgs_camera* cams, co
         if (!ctx->pipe_ev[0])
             for (int k = 0; k < HGS_TRAIN_PIPELINE; ++k)
                 CK(cudaEventCreateWithFlags(&ctx->pipe_ev[k], cudaEventDisableTiming));
-        CK(ctx->pinned_pipe.ensure(sizeof(double) * 2 * kMaxStepViews * HGS_TRAIN_PIPELINE));
+        CK(ctx->pinned_pipe.ensure(sizeof(double) * (2 * kMaxStepViews + 1) * HGS_TRAIN_PIPELINE));
     }
     const int slot = ctx->pipe_next;
     hgs_raster_opts ro{o->weight_cutoff, 1, 0, 0};
@@ -799,6 +812,37 @@ hgs_status hgs_train_step_async(hgs_ctx* ctx, int n_views, const hgs_camera* cam
 
 int hgs_train_pending(hgs_ctx* ctx) { return ctx ? (int)ctx->pipeline.size() : 0; }
 
+// View-parallel completion of the iteration just enqueued with
+// hgs_train_step_async(apply_adam = 0): all-reduce of the loss-sum gate and of
+// the packed gradients over the context's communicator, then the gated Adam
+// step -- all stream-ordered, no host synchronisation.
+hgs_status hgs_train_exchange_async(hgs_ctx* ctx, const hgs_train_opts* o) {
+    if (!ctx || !o) return HGS_ERR_INVALID_ARGUMENT;
+    if (ctx->pipeline.empty() || ctx->pipeline.back().adam || ctx->pipeline.back().dist)
+        return fail(ctx, HGS_ERR_STATE, "train_exchange_async: enqueue an iteration with apply_adam = 0 first");
+    if (!ctx->comm) return fail(ctx, HGS_ERR_STATE, "train_exchange_async: call hgs_comm_init first");
+    CK(cudaSetDevice(ctx->device));
+    hgs_pending_step& ps = ctx->pipeline.back();
+    Scratch* sc = scratch(ctx);
+    double* gate = sc->pipe_gate[ps.slot];
+    gate_sum_kernel<<<1, 32, 0, ctx->stream>>>(&sc->pipe_sums[ps.slot][0][0], 2 * ps.n_views, gate);
+    count_launch();
+    CKL();
+    hgs_status r = comm_allreduce_f64_dev(ctx, gate, 1);
+    if (r != HGS_OK) return r;
+    r = hgs_allreduce_grads(ctx);
+    if (r != HGS_OK) return r;
+    ps.step_before = ctx->step;
+    r = run_adam(ctx, &o->lrs, o->mean_lr_scale, gate, 1, &sc->abort);
+    if (r != HGS_OK) return r;
+    ps.adam = true;
+    ps.dist = true;
+    double* hg = static_cast<double*>(ctx->pinned_pipe.p) + (size_t)HGS_TRAIN_PIPELINE * kMaxStepViews * 2;
+    CK(cudaMemcpyAsync(&hg[ps.slot], gate, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaEventRecord(ctx->pipe_ev[ps.slot], ctx->stream));
+    return HGS_OK;
+}
+
 hgs_status hgs_train_collect(hgs_ctx* ctx, double* loss_out) {
     if (!ctx) return HGS_ERR_INVALID_ARGUMENT;
     if (ctx->pipeline.empty()) return fail(ctx, HGS_ERR_STATE, "train_collect: no pipelined iteration pending");
@@ -811,7 +855,11 @@ hgs_status hgs_train_collect(hgs_ctx* ctx, double* loss_out) {
     for (int v = 0; v < p.n_views; ++v)
         loss += loss_from_sums(hp[2 * v], hp[2 * v + 1], p.dims[v][0], p.dims[v][1], p.lambda);
     if (loss_out) *loss_out = loss;
-    if (!std::isfinite(loss) && p.adam) {
+    // view-parallel steps: the decision is the all-reduced one (every rank's
+    // views), identical on every rank
+    const double* hg = static_cast<const double*>(ctx->pinned_pipe.p) + (size_t)HGS_TRAIN_PIPELINE * kMaxStepViews * 2;
+    const bool bad = p.dist ? !std::isfinite(hg[p.slot]) : !std::isfinite(loss);
+    if (bad && p.adam) {
         // the device skipped this update and every later pending one
         if (p.adam) ctx->step = p.step_before;
         ctx->pipeline.clear();

@@ -18,3 +18,5 @@ hgs_status hgs_skipped_total(hgs_ctx* ctx, uint64_t* get, const uint64_t* set);
 // the optimizer state and statistics (the allocation half of hgs_scene_upload)
 hgs_status hgs_scene_alloc(hgs_ctx* ctx, int64_t n4, int64_t n3, int deg, double tau, double extent,
                            double duration);
+// stream-ordered all-reduce (sum) of n device doubles over the context's communicator (comm.cu)
+hgs_status comm_allreduce_f64_dev(hgs_ctx* ctx, double* dev, int n);

@@ -220,6 +220,20 @@ class ViewParallelTrainer(DeviceTrainer):
             self.verify_replicas()
         return total / len(batch)
 
+    def step_async(self, batch: list[int], batch_total: int | None = None, apply_adam: bool = True,
+                   gt_host: list | None = None) -> None:
+        """Pipelined view-parallel iteration (exchange="capi"): this rank's
+        views, then hgs_train_exchange_async (all-reduced loss gate + packed
+        gradients + gated Adam) -- no host synchronisation; collect() returns
+        this rank's mean view loss later and raises NumericAbort on every rank
+        for the same iteration."""
+        if self.exchange != "capi":
+            raise ValueError("step_async needs exchange='capi'")
+        mine = shard_batch(batch, self.rank, self.world)
+        self.iter += 1
+        DeviceTrainer.step_async(self, mine, batch_total=len(batch), apply_adam=False, gt_host=gt_host)
+        self.ctx._check(self.ctx._lib.hgs_train_exchange_async(self.ctx.handle, C.byref(self._opts(self.decay()))))
+
     def verify_replicas(self) -> bool:
         """True when every rank's parameters hash equal; otherwise rank 0's
         scene, optimizer state and statistics are shipped to every rank

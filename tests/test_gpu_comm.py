@@ -94,3 +94,50 @@ def test_view_parallel_trainer_capi_exchange_single_rank(tmp_path):
                 np.testing.assert_allclose(getattr(s2, f), getattr(s1, f), rtol=1e-4, atol=1e-6)
     finally:
         dist.destroy_process_group()
+
+
+def test_pipelined_exchange_single_rank(tmp_path):
+    """hgs_train_exchange_async (ViewParallelTrainer.step_async): pipelined
+    view-parallel iterations with the all-reduced loss gate -- the same
+    iterations as the plain trainer; a non-finite batch raises NumericAbort
+    at its collect and leaves the parameters untouched."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2505_13215_b200.train import DeviceTrainer, ViewParallelTrainer
+
+    dist.init_process_group("gloo", rank=0, world_size=1, init_method=f"file://{tmp_path}/pg2")
+    try:
+        target = synthetic_scene(3000, 2000, sh_degree=2, seed=41)
+        scene = synthetic_scene(3000, 2000, sh_degree=2, seed=42).as_float32_exact()
+        cams = [ring_camera(i, 96, 72) for i in range(4)]
+        times = [0.1, 0.4, 0.6, 0.9]
+        with A.Context(0) as c1, A.Context(0) as c2:
+            ref = DeviceTrainer(c1, scene, cams, times, target=target, iterations=50)
+            vp = ViewParallelTrainer(c2, scene, cams, times, target=target, iterations=50, exchange="capi")
+            batches = [[it % 4, (it + 1) % 4] for it in range(6)]
+            want = [ref.step(b) for b in batches]
+            got = []
+            for b in batches:
+                vp.step_async(b)
+                if c2._lib.hgs_train_pending(c2.handle) > 2:
+                    got.append(vp.collect())
+            while c2._lib.hgs_train_pending(c2.handle):
+                got.append(vp.collect())
+            assert got == pytest.approx(want, rel=1e-5)
+            s1, s2 = c1.download(), c2.download()
+            for f in ("mean_x", "ql", "log_s4", "sh4", "mean3", "op3"):
+                np.testing.assert_allclose(getattr(s2, f), getattr(s1, f), rtol=1e-4, atol=1e-6)
+            # a non-finite batch: NumericAbort at its collect, parameters untouched
+            before = c2.download()
+            vp.gt[1] = torch.full_like(vp.gt[1], float("nan"))
+            vp.step_async([0, 1])
+            with pytest.raises(A.NumericAbort):
+                vp.collect()
+            after = c2.download()
+            for f in ("mean_x", "sh4", "op3"):
+                assert np.array_equal(getattr(after, f), getattr(before, f)), f
+            vp.step_async([2, 3])  # the gate re-arms
+            assert np.isfinite(vp.collect())
+    finally:
+        dist.destroy_process_group()
