@@ -338,20 +338,22 @@ bool write_file(const char* path, const uint8_t* p, size_t n, IoError& e) {
     return ok;
 }
 
-const uint32_t* crc_tables_host() {
-    static uint32_t T[8][256];
-    static bool init = false;
-    if (!init) {
+struct CrcTables {
+    uint32_t t[8][256];
+    CrcTables() {
         for (uint32_t i = 0; i < 256; ++i) {
             uint32_t c = i;
             for (int k = 0; k < 8; ++k) c = (c & 1) ? 0xEDB88320u ^ (c >> 1) : c >> 1;
-            T[0][i] = c;
+            t[0][i] = c;
         }
-        for (int t = 1; t < 8; ++t)
-            for (int i = 0; i < 256; ++i) T[t][i] = (T[t - 1][i] >> 8) ^ T[0][T[t - 1][i] & 255];
-        init = true;
+        for (int j = 1; j < 8; ++j)
+            for (int i = 0; i < 256; ++i) t[j][i] = (t[j - 1][i] >> 8) ^ t[0][t[j - 1][i] & 255];
     }
-    return &T[0][0];
+};
+
+const uint32_t* crc_tables_host() {
+    static const CrcTables T;  // thread-safe initialisation
+    return &T.t[0][0];
 }
 
 uint64_t crc_chunks(uint64_t n) { return (n + kCrcChunk - 1) / kCrcChunk; }

@@ -2,8 +2,10 @@
 // (backward.hpp:68-74), loss (loss.hpp:12-13), Adam (train.hpp:68-69),
 // conversion sweep (scene.hpp:75 + train.cpp:305-362) and the fused
 // per-iteration step (train.cpp:402-475).  Host code: -ffp-contract=off.
+#include <atomic>
 #include <cmath>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -121,6 +123,20 @@ hgs_status download_floats(hgs_ctx* ctx, const float* dev, int64_t n, void* host
 
 Scratch* scratch(hgs_ctx* ctx) { return ctx->scratch.as<Scratch>(); }
 
+// The SSIM window and the sRGB LUT live in __constant__ memory, one copy per
+// device: set once per device (contexts on several GPUs in one process).
+void ensure_loss_tables(int device) {
+    static std::atomic<uint64_t> done{0};
+    const uint64_t bit = 1ull << (device & 63);
+    if (done.load() & bit) return;
+    static std::mutex m;
+    std::lock_guard<std::mutex> g(m);
+    if (done.load() & bit) return;
+    set_ssim_window();
+    set_srgb_lut();
+    done.fetch_or(bit);
+}
+
 hgs_status ensure_scratch(hgs_ctx* ctx) {
     if (!ctx->scratch.p) {
         CK(ctx->scratch.ensure(sizeof(Scratch)));
@@ -187,12 +203,7 @@ hgs_status run_loss(hgs_ctx* ctx, const void* gt, bool gt_u8, double lambda, dou
     const bool with_ssim = lambda != 0.0;
     if (with_ssim && (W < 11 || H < 11))
         return fail(ctx, HGS_ERR_INVALID_ARGUMENT, "ssim: images smaller than the 11x11 window");
-    static bool tables_set = false;
-    if (!tables_set) {
-        set_ssim_window();
-        set_srgb_lut();
-        tables_set = true;
-    }
+    ensure_loss_tables(ctx->device);
     const size_t npx = (size_t)W * H;
     CK(ctx->lgrad.ensure(npx * 3 * 4));
     Scratch* sc = scratch(ctx);
@@ -410,12 +421,7 @@ hgs_status hgs_loss_with_grad(hgs_ctx* ctx, const void* gt, int dtype, int on_de
 // PSNR / SSIM of ctx->img (W x H) against a device frame (metrics.cpp:91-101)
 hgs_status metrics_impl(hgs_ctx* ctx, const void* g, bool gt_u8, double* psnr_out, double* ssim_out) {
     const int W = ctx->W, H = ctx->H;
-    static bool tables_set = false;
-    if (!tables_set) {
-        set_ssim_window();
-        set_srgb_lut();
-        tables_set = true;
-    }
+    ensure_loss_tables(ctx->device);
     const int64_t n = (int64_t)W * H * 3;
     Scratch* sc = scratch(ctx);
     CK(cudaMemsetAsync(sc, 0, 2 * sizeof(double), ctx->stream));
