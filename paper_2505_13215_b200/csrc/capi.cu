@@ -698,6 +698,7 @@ hgs_status hgs_scene_alloc(hgs_ctx* ctx, int64_t n4, int64_t n3, int deg, double
     ctx->have_tape = false;
     ctx->stats_pending = false;
     ctx->icap = 0;
+    ctx->dens_planned = false;  // a densify plan belongs to the pools it was made for
     const uint64_t zero = 0;
     return hgs_skipped_total(ctx, nullptr, &zero);
 }

@@ -591,6 +591,7 @@ hgs_status hgs_sweep_convert(hgs_ctx* ctx, int64_t* moved_out, hgs_conversion_re
     hgs_status r = ensure_scratch(ctx);
     if (r != HGS_OK) return r;
     cudaStream_t st = ctx->stream;
+    ctx->dens_planned = false;  // the sweep moves rows: a pending densify plan is stale
     const int n4 = (int)ctx->n4, n3 = (int)ctx->n3;
     hgs_conversion_report rep{0, 0.0, 0.0};
     if (n4 == 0) {
