@@ -587,6 +587,7 @@ hgs_status hgs_stats_download(hgs_ctx* ctx, double* gn4, uint32_t* c4, double* g
 hgs_status hgs_sweep_convert(hgs_ctx* ctx, int64_t* moved_out, hgs_conversion_report* report) {
     if (!ctx) return HGS_ERR_INVALID_ARGUMENT;
     if (!(ctx->tau > 0.0)) return fail(ctx, HGS_ERR_INVALID_ARGUMENT, "is_static: tau must be positive");
+    if (!ctx->pipeline.empty()) return fail(ctx, HGS_ERR_STATE, "sweep_convert: pipelined iterations pending");
     CK(cudaSetDevice(ctx->device));
     hgs_status r = ensure_scratch(ctx);
     if (r != HGS_OK) return r;
