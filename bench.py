@@ -408,7 +408,7 @@ def run_extras(args, ctx, lib, timed, world, rank) -> dict:
         ctx.upload(scene)
         ts = [j / 49.0 for j in range(50)] if name == "c5" else [c["t"]]
 
-        k = max(args.steps, 10)
+        k = max(args.steps, 10) * (5 if name == "c1" else 1)  # c1 frames are short: more of them
         cam_objs = [ring_camera(c["seed"], c["width"], c["height"], index=0, n_ring=16)] * k
         sweep_ts = [ts[(i * world + rank) % len(ts)] for i in range(k)]
         ctx.render_sweep(cam_objs, sweep_ts, (0.2, 0.2, 0.2))  # sizes the workspaces and the capacity (untimed)
