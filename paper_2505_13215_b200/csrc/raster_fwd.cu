@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(256) gather_sorted_kernel(const uint32_t* __re
         fp64 = true;
     }
     const double r = fp64 ? 1e30 : fabs(l01) / l11;
-    if (r > 4.0) fp64 = true;
+    if (r > 16.0) fp64 = true;  // FP32 stays certified (e1 grows with r); measured best at 16
     f.l00 = (float)l00;
     f.l01 = (float)l01;
     f.l11 = (float)l11;
