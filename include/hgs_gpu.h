@@ -423,6 +423,9 @@ long long hgs_launch_count(void);
 hgs_status hgs_debug_splats(hgs_ctx *ctx, int32_t *gid, uint32_t *depth_bits, int32_t *box4, double *mean2,
                             double *conic4, double *alpha, float *rgb, int64_t cap, int64_t *n_out);
 hgs_status hgs_debug_instances(hgs_ctx *ctx, uint32_t *tile, uint32_t *gid, int64_t cap, int64_t *n_out);
+/* Parity introspection: the 8x8-quadrant contribution mask of every instance
+ * of the kept full list, in hgs_debug_instances order. */
+hgs_status hgs_debug_instance_masks(hgs_ctx *ctx, uint8_t *masks, int64_t cap, int64_t *n_out);
 /* The rasterizers walk the exactly-culled instance list; keeping the
  * reference's complete list for hgs_debug_instances costs an extra sort. */
 hgs_status hgs_debug_keep_instances(hgs_ctx *ctx, int enable);

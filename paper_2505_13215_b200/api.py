@@ -337,6 +337,16 @@ class Context:
                                                       gid.ctypes.data_as(_capi._u32p), n.value, C.byref(n)))
         return tile, gid
 
+    def debug_instance_masks(self) -> np.ndarray:
+        """Quadrant masks of the kept full instance list (debug_instances order)."""
+        n = C.c_int64()
+        self._check(self._lib.hgs_debug_instance_masks(self._h, None, 0, C.byref(n)))
+        m = np.zeros(n.value, np.uint8)
+        if n.value:
+            self._check(self._lib.hgs_debug_instance_masks(self._h, m.ctypes.data_as(C.POINTER(C.c_uint8)), n.value,
+                                                           C.byref(n)))
+        return m
+
     # ------------------------------------------------------------ training
     def forward_train(self, camera: Camera, t: float, background=(0.0, 0.0, 0.0),
                       weight_cutoff=DEFAULT_WEIGHT_CUTOFF, want_image=True) -> np.ndarray | None:

@@ -1019,4 +1019,19 @@ hgs_status hgs_debug_instances(hgs_ctx* ctx, uint32_t* tile, uint32_t* gid, int6
     return HGS_OK;
 }
 
+// The 8x8-quadrant contribution mask of every instance of the full list
+// (same order as hgs_debug_instances): bit q = quadrant (q & 1, q >> 1).
+hgs_status hgs_debug_instance_masks(hgs_ctx* ctx, uint8_t* masks, int64_t cap, int64_t* n_out) {
+    if (!ctx || !n_out || !ctx->have_tape) return fail(ctx, HGS_ERR_STATE, "no render to inspect");
+    const int64_t I = ctx->I;
+    *n_out = I;
+    if (I > cap || I == 0) return HGS_OK;
+    if (!ctx->inst_vals_all)
+        return fail(ctx, HGS_ERR_STATE, "full instance list not kept: call hgs_debug_keep_instances(ctx, 1) first");
+    std::vector<uint32_t> vals(I);
+    CK(cudaMemcpy(vals.data(), ctx->inst_vals_all, I * 4, cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < I; ++i) masks[i] = (uint8_t)(vals[i] >> hgs::kInstMaskShift);
+    return HGS_OK;
+}
+
 }  // extern "C"

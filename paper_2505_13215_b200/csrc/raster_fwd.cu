@@ -119,6 +119,70 @@ __device__ inline bool tile_may_contribute(const CullRec& e, int xa, int xb, int
     return pmin <= e.pcut + 1e-5f * (1.0f + smag);
 }
 
+// The same question for the four 8x8 quadrants of a tile at once, through
+// the ellipse E = {power <= pcut} itself: for each quadrant row (band of
+// pixel-centre offsets dy in [y1, y2]) the x-range of E over the band is
+// [XL, XR] -- the ellipse's own x-extreme +-X_ext when the extreme point's
+// dy lies in the band, else the boundary at the nearer band edge (the
+// right boundary is concave, the left convex, in dy) -- and a quadrant is
+// reachable iff its x-range overlaps [XL, XR].  Same answer as
+// tile_may_contribute (min of a convex function over a rectangle <= pcut
+// <=> the rectangle meets E), a fraction of its arithmetic.  FP32 with
+// margins covering its rounding: pcut + 1e-5 (1 + 2|pcut|); X_ext / Y_ext and
+// the band clip widened by 1e-3 relative + 1e-3 px; XR / XL widened by
+// 2e-3 (X_ext + |b| max|dy| / a) + 1e-3 px (the sqrt of a cancelling
+// difference loses at most sqrt(8u) of the half-width).  Only for conics
+// with det >= 1e-3 a c (well conditioned); otherwise (and for
+// non-positive-definite or empty cases) returns false = "use the exact
+// per-quadrant test".
+__device__ inline bool quadrant_mask_bands(const CullRec& e, int x0, int x1, int y0, int y1, int tx, int ty,
+                                           uint32_t& mask) {
+    const float a = e.a, b = e.b, c = e.c;
+    if (!(a > 0.0f && c > 0.0f)) return false;
+    const float det = fmaf(a, c, -b * b);
+    if (!(det >= 1e-3f * a * c)) return false;
+    const float P2 = 2.0f * (e.pcut + 1e-5f * (1.0f + 2.0f * fabsf(e.pcut)));
+    if (!(P2 > 0.0f)) return false;
+    const float X_ext = sqrtf(P2 * c / det), Y_ext = sqrtf(P2 * a / det);
+    const float Yc = Y_ext * 1.001f + 1e-3f;  // band clip (wider: conservative)
+    const float dyr = -b * X_ext / c;         // dy of the rightmost point of E (leftmost: -dyr)
+    const float inv_a = 1.0f / a, aP2 = a * P2;
+    mask = 0u;
+#pragma unroll
+    for (int qy = 0; qy < 2; ++qy) {
+        const int ya = max(y0, ty * kTile + qy * 8), yb = min(y1, ty * kTile + qy * 8 + 7);
+        if (ya > yb) continue;
+        const float y1f = fast_dx((float)ya + 0.5f, e.sy_hi, e.sy_lo), y2f = fast_dx((float)yb + 0.5f, e.sy_hi, e.sy_lo);
+        const float lo = fmaxf(y1f, -Yc), hi = fminf(y2f, Yc);
+        if (lo > hi) continue;  // the band misses E
+        const float tol = 1e-3f * Y_ext + 1e-3f;
+        float XR, XL;
+        if (dyr >= lo - tol && dyr <= hi + tol) {
+            XR = X_ext;
+        } else {
+            const float d = fminf(fmaxf(dyr, lo), hi);
+            XR = (-b * d + sqrtf(fmaxf(0.0f, fmaf(-det * d, d, aP2)))) * inv_a;
+        }
+        if (-dyr >= lo - tol && -dyr <= hi + tol) {
+            XL = -X_ext;
+        } else {
+            const float d = fminf(fmaxf(-dyr, lo), hi);
+            XL = (-b * d - sqrtf(fmaxf(0.0f, fmaf(-det * d, d, aP2)))) * inv_a;
+        }
+        const float m = 2e-3f * (X_ext + fabsf(b) * inv_a * fmaxf(fabsf(lo), fabsf(hi))) + 1e-3f;
+        XR += m;
+        XL -= m;
+#pragma unroll
+        for (int qx = 0; qx < 2; ++qx) {
+            const int xa = max(x0, tx * kTile + qx * 8), xb = min(x1, tx * kTile + qx * 8 + 7);
+            if (xa > xb) continue;
+            const float lx = fast_dx((float)xa + 0.5f, e.sx_hi, e.sx_lo), hx = fast_dx((float)xb + 0.5f, e.sx_hi, e.sx_lo);
+            if (hx >= XL && lx <= XR) mask |= 1u << (qy * 2 + qx);
+        }
+    }
+    return true;
+}
+
 // Duplicate each sorted splat into every tile its box overlaps
 // (raster.cpp:182-201), one thread per INSTANCE so splats covering hundreds of
 // tiles do not serialise.  A CTA covers kDupPerCta consecutive instances: two
@@ -173,12 +237,14 @@ __device__ __forceinline__ void dup_instance(int i, const uint32_t* s_off, int c
     uint32_t mask = 0xfu;
     if (cull) {
         const CullRec e = cull_rec[j];
-        mask = 0u;
+        if (!quadrant_mask_bands(e, x0, x1, y0, y1, tx, ty, mask)) {
+            mask = 0u;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int qx0 = tx * kTile + (q & 1) * 8, qy0 = ty * kTile + (q >> 1) * 8;
-            const int xa = max(x0, qx0), xb = min(x1, qx0 + 7), ya = max(y0, qy0), yb = min(y1, qy0 + 7);
-            if (xa <= xb && ya <= yb && tile_may_contribute(e, xa, xb, ya, yb)) mask |= 1u << q;
+            for (int q = 0; q < 4; ++q) {
+                const int qx0 = tx * kTile + (q & 1) * 8, qy0 = ty * kTile + (q >> 1) * 8;
+                const int xa = max(x0, qx0), xb = min(x1, qx0 + 7), ya = max(y0, qy0), yb = min(y1, qy0 + 7);
+                if (xa <= xb && ya <= yb && tile_may_contribute(e, xa, xb, ya, yb)) mask |= 1u << q;
+            }
         }
     }
     key = (uint32_t)(ty * tiles_x + tx);

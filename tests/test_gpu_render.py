@@ -213,3 +213,47 @@ def test_fused_duplication_path_matches_debug_path(ctx, cfg):
         assert ctx.render_info() == prod.render_info()
     finally:
         prod.close()
+
+
+@pytest.mark.parametrize("seed,size,t", [(3, (320, 240), 0.45), (5, (256, 192), 0.8), (7, (200, 150), 0.1)])
+def test_quadrant_masks_are_conservative(ctx, seed, size, t):
+    """The 8x8-quadrant masks (band test / exact rectangle test of the
+    duplication kernels) never clear a quadrant in which some pixel of the
+    splat's box reaches alpha >= 1/255 (raster.cpp:139-140, FP64 truth)."""
+    from paper_2505_13215_b200.scene import synthetic_scene as syn
+
+    scene = syn(15000, 5000, sh_degree=1, seed=seed).as_float32_exact()
+    cam = ring_camera(seed, *size)
+    ctx.upload(scene)
+    ctx.debug_keep_instances(True)  # (the module's context keeps the full list anyway)
+    ctx.render(cam, t)
+    tiles, gids = ctx.debug_instances()
+    masks = ctx.debug_instance_masks()
+    sp = ctx.debug_splats()
+    pos = np.full(int(sp["gid"].max()) + 1, -1, np.int64)
+    pos[sp["gid"]] = np.arange(len(sp["gid"]))
+    k = pos[gids]
+    tiles_x = (cam.width + 15) // 16
+    tx, ty = tiles.astype(np.int64) % tiles_x, tiles.astype(np.int64) // tiles_x
+    box = sp["box"][k]  # x0, x1, y0, y1
+    mx, my = sp["mean"][k, 0], sp["mean"][k, 1]
+    c = sp["conic"][k]
+    lnc = np.log(sp["alpha"][k] * 255.0)  # reachable iff power <= ln(255 alpha)
+    off = np.arange(8)
+    bad = 0
+    for q in range(4):
+        qx0 = tx * 16 + (q & 1) * 8
+        qy0 = ty * 16 + (q >> 1) * 8
+        px = qx0[:, None] + off[None, :]  # (n, 8)
+        py = qy0[:, None] + off[None, :]
+        inx = (px >= box[:, 0:1]) & (px <= box[:, 1:2]) & (px < cam.width)
+        iny = (py >= box[:, 2:3]) & (py <= box[:, 3:4]) & (py < cam.height)
+        dx = (px + 0.5) - mx[:, None]
+        dy = (py + 0.5) - my[:, None]
+        pw = 0.5 * (c[:, 0, None, None] * dx[:, None, :] ** 2 + (c[:, 1] + c[:, 2])[:, None, None] * dx[:, None, :] *
+                    dy[:, :, None] + c[:, 3, None, None] * dy[:, :, None] ** 2)  # (n, y, x)
+        ok = inx[:, None, :] & iny[:, :, None] & (pw <= lnc[:, None, None])
+        reach = ok.any(axis=(1, 2))
+        bad += int((reach & ((masks >> q) & 1 == 0)).sum())
+    assert bad == 0, bad
+    assert masks.any()
