@@ -511,7 +511,6 @@ def run_rows(ctx) -> dict:
 
     from paper_2505_13215_b200 import api as A
     from paper_2505_13215_b200 import dataset as D
-    from paper_2505_13215_b200.rng import MT19937_64
     from paper_2505_13215_b200.scene import CONFIGS, ring_camera, synthetic_scene
     from paper_2505_13215_b200.train import DeviceTrainer
 
@@ -536,10 +535,10 @@ def run_rows(ctx) -> dict:
     gn4, c4, gn3, c3 = ctx.densify_stats()
     avg = np.concatenate([gn4 / np.maximum(c4, 1), gn3 / np.maximum(c3, 1)])
     thr = float(np.quantile(avg[avg > 0], 0.98)) if (avg > 0).any() else 0.02  # ~2% of the observed densify
-    ms, rep = wall(lambda: ctx.densify_and_prune(MT19937_64(7), grad_threshold=thr, max_gaussians=1_000_000))
+    ms, rep = wall(lambda: ctx.densify_and_prune(A.Rng(7), grad_threshold=thr, max_gaussians=1_000_000))
     out["densify_and_prune"] = {"ms": round(ms, 3), "gaussians_before": n_before, "gaussians_after": sum(ctx.counts()),
                                 "report": rep, "grad_threshold": thr,
-                                "what": "hgs_densify_plan + host normal replay + hgs_densify_apply"}
+                                "what": "hgs_densify_and_prune: device plan + libstdc++ normal draws + device apply"}
     frames = [t.cpu().numpy() for t in tr.gt]  # host u8 sRGB frames
     for v in range(2):
         ctx.render_device(cams[v], times[v], (0.2, 0.2, 0.2))
