@@ -153,6 +153,28 @@ class KeyValueFile:
         except ValueError:
             raise FormatError(f"{self.path}: key {key}: not an integer: {v}") from None
 
+    def get_bool(self, key: str, default: bool) -> bool:
+        v = self._find(key)
+        if v is None:
+            return default
+        if v in ("true", "1"):
+            return True
+        if v in ("false", "0"):
+            return False
+        raise FormatError(f"{self.path}: key {key}: expected true/false: {v}")
+
+    def get_uint(self, key: str, default: int) -> int:
+        v = self._find(key)
+        if v is None:
+            return default
+        try:
+            x = int(v)
+            if x < 0 or x >= 1 << 64:
+                raise ValueError
+            return x
+        except ValueError:
+            raise FormatError(f"{self.path}: key {key}: not an unsigned integer: {v}") from None
+
     def finish(self) -> None:
         unknown = [k for k in sorted(self.used) if not self.used[k]]
         if unknown:

@@ -335,6 +335,38 @@ class TrainConfig:  # train.hpp:23-49
     init_temporal_scale: float = 0.1
     init_opacity: float = 0.1
 
+    _FILE_KEYS = ("iterations", "batch_size", "warmup_iters", "densify_interval", "densify_stop_iter",
+                  "grad_threshold", "opacity_prune_eps", "tau", "conversion_enabled", "ssim_lambda",
+                  "opacity_reset_enabled", "opacity_reset_interval", "seed", "sh_degree", "weight_cutoff",
+                  "max_gaussians", "num_threads", "probe_interval", "init_temporal_scale", "init_opacity")
+    _LR_KEYS = (("lr_mean", "mean"), ("lr_mean_final_ratio", "mean_final_ratio"), ("lr_mean_t", "mean_t"),
+                ("lr_quat", "quat"), ("lr_scales", "scales"), ("lr_opacity", "opacity"), ("lr_sh", "sh"))
+
+    @classmethod
+    def from_file(cls, path: str) -> "TrainConfig":
+        """TrainConfig::from_file (train.cpp:87-120): `key = value` lines
+        (config.cpp KeyValueFile rules), unknown keys are a FormatError,
+        then validate()."""
+        from .dataset import KeyValueFile
+
+        kv = KeyValueFile(path)
+        cfg = cls()
+        for k in cls._FILE_KEYS:
+            cur = getattr(cfg, k)
+            if isinstance(cur, bool):
+                setattr(cfg, k, kv.get_bool(k, cur))
+            elif k == "seed":
+                setattr(cfg, k, kv.get_uint(k, cur))
+            elif isinstance(cur, int):
+                setattr(cfg, k, kv.get_int(k, cur))
+            else:
+                setattr(cfg, k, kv.get_float(k, cur))
+        for k, attr in cls._LR_KEYS:
+            setattr(cfg.lrs, attr, kv.get_float(k, getattr(cfg.lrs, attr)))
+        kv.finish()
+        cfg.validate()
+        return cfg
+
     def validate(self) -> None:  # train.cpp:76-85 (TrainConfig::validate)
         if self.warmup_iters > self.iterations and self.iterations > 0:
             raise ValueError("TrainConfig: warmup_iters must be <= iterations")
@@ -382,6 +414,15 @@ class TrainLogRow:  # train.hpp:51-58
     n_dynamic: int = 0
     conversions: int = 0
     wall_seconds: float = 0.0
+
+
+def write_train_log_csv(rows: list, path: str) -> None:
+    """TrainLog::write_csv (train.cpp:122-129)."""
+    with open(path, "w") as f:
+        f.write("iter,loss,probe_psnr,n_static,n_dynamic,conversions,wall_seconds\n")
+        for r in rows:
+            f.write(f"{r.iter},{r.loss:.6g},{r.probe_psnr:.6g},{r.n_static},{r.n_dynamic},{r.conversions},"
+                    f"{r.wall_seconds:.6g}\n")
 
 
 @dataclass
