@@ -548,3 +548,39 @@ def train_scene(scene: HybridScene, dataset: MultiViewDataset, cfg: TrainConfig,
         if on_row:
             on_row(row)
     return TrainResult(scene=ctx.download(), log=log, state=ctx.adam_state())
+
+
+def train(dataset: MultiViewDataset, cfg: TrainConfig, ctx: Context | None = None, on_row=None) -> TrainResult:
+    """hgs::train (train.cpp:366-380): init_scene from the dataset's points
+    (the GPU kNN, api.Context.init_scene), then train_scene."""
+    if not dataset.cameras or dataset.total_frames() == 0:
+        raise ValueError("train: dataset is empty")
+    from .api import InitConfig, default_context
+
+    ctx = ctx or default_context()
+    pts = dataset.init_points
+    if pts is None or len(pts) < 4:
+        raise ValueError("init_scene: need at least 4 points")
+    ctx.init_scene(pts.positions, pts.rgb, InitConfig(sh_degree=cfg.sh_degree, tau=cfg.tau,
+                                                      duration_seconds=dataset.duration_seconds,
+                                                      init_temporal_scale=cfg.init_temporal_scale,
+                                                      init_opacity=cfg.init_opacity))
+    return train_scene(ctx.download(), dataset, cfg, ctx=ctx, on_row=on_row)
+
+
+def train_directory(data_dir: str, held_out: int = -1, config: TrainConfig | None = None,
+                    ctx: Context | None = None):
+    """hybridgs.train (bindings.cpp:221-235): load the dataset directory
+    (8-bit frames), train, and score the held-out camera -> (scene,
+    held_out_psnr); held_out_psnr is -1 without a held-out camera."""
+    from . import dataset as D
+    from .api import default_context
+
+    cfg = config or TrainConfig()
+    split, held = D.load_dataset(data_dir, held_out)
+    ctx = ctx or default_context()
+    result = train(split, cfg, ctx=ctx)
+    held_psnr = -1.0
+    if held.cameras:
+        held_psnr = evaluate_views(None, held, cfg.weight_cutoff, ctx=ctx).mean_psnr
+    return result.scene, held_psnr

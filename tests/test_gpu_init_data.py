@@ -92,3 +92,36 @@ def test_train_from_disk_u8_matches_linear(tmp_path):
     for a, b in zip(*logs):
         assert a.loss == pytest.approx(b.loss, rel=1e-5)
         assert a.probe_psnr == pytest.approx(b.probe_psnr, abs=1e-4)
+
+
+def test_train_directory_end_to_end(tmp_path):
+    """hybridgs.train (bindings.cpp:221-235) on a dataset directory: points ->
+    GPU kNN init -> device training with densification and sweeps ->
+    held-out PSNR; the loss goes down (test_train.cpp:273-307)."""
+    from paper_2505_13215_b200 import dataset as D
+    from paper_2505_13215_b200.train import Frame, MultiViewDataset, TrainConfig, quantize_8bit, train_directory
+
+    target = synthetic_scene(1500, 1500, sh_degree=1, seed=15)
+    cams = [ring_camera(i, 64, 48, index=i, n_ring=4) for i in range(4)]
+    with A.Context(0) as c:
+        c.upload(target)
+        frames = [[Frame(t, quantize_8bit(c.render(cam, t)["rgb"].astype(np.float64))) for t in (0.0, 0.5, 1.0)]
+                  for cam in cams]
+    rng = np.random.default_rng(3)
+    pts = D.InitPoints(target.mean_x[:400].copy(), rng.uniform(0, 1, (400, 3)))
+    ds = MultiViewDataset(cameras=cams, frames=frames, duration_seconds=1.0, camera_ids=[0, 1, 2, 3],
+                          init_points=pts)
+    root = str(tmp_path / "scene")
+    D.save_dataset(ds, root)
+    cfg = TrainConfig(iterations=60, batch_size=2, warmup_iters=20, densify_interval=20, densify_stop_iter=40,
+                      probe_interval=20, sh_degree=1)
+    with A.Context(0) as c:
+        scene, held_psnr = train_directory(root, held_out=3, config=cfg, ctx=c)
+    assert scene.n4 + scene.n3 > 0 and held_psnr > 5.0
+    with A.Context(0) as c:
+        from paper_2505_13215_b200.train import train
+
+        split, _ = D.load_dataset(root, 3)
+        res = train(split, cfg, ctx=c)
+    first, last = res.log[0].loss, res.log[-1].loss
+    assert last < first
