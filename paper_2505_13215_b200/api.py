@@ -594,6 +594,19 @@ def density_map(scene: HybridScene, camera: Camera, t: float, dynamics_only: boo
     return ctx.density_map(camera, t, dynamics_only, weight_cutoff)
 
 
+def sweep_convert(scene: HybridScene) -> tuple[int, float, float]:
+    """hybridgs.sweep_convert (bindings.cpp:135-138; scene.cpp:43-71): converts
+    every dynamic Gaussian with exp(s_t) > tau to a static one IN PLACE (on
+    the device) and returns (count, max_leakage, mean_leakage)."""
+    ctx = default_context()
+    ctx.upload(scene)
+    _, rep = ctx.sweep_convert()
+    out = ctx.download()
+    for f in HybridScene.DYN_FIELDS + HybridScene.STA_FIELDS + ("tau", "extent", "duration_seconds"):
+        setattr(scene, f, getattr(out, f))
+    return rep["count"], rep["max_leakage"], rep["mean_leakage"]
+
+
 def _metrics(a: np.ndarray, b: np.ndarray, want_psnr: bool, want_ssim: bool) -> tuple[float, float]:
     a = np.ascontiguousarray(a, dtype=np.float64)
     b = np.ascontiguousarray(b, dtype=np.float64)

@@ -212,6 +212,22 @@ def test_sweep_matches_oracle(ctx):
     assert rep2["count"] == 0
 
 
+def test_module_sweep_convert_in_place():
+    """hybridgs.sweep_convert(scene) (bindings.cpp:135-138): the host scene
+    is converted in place; (count, max_leakage, mean_leakage) as the oracle."""
+    from paper_2505_13215_b200.api import sweep_convert
+
+    scene = O.Rng(34).random_scene(9, 150, 1).as_float32_exact()
+    scene.tau = 0.3
+    ref = scene.copy()
+    _, rrep = O.sweep_convert(ref, None)
+    count, maxl, meanl = sweep_convert(scene)
+    assert count == rrep["count"] and (scene.n4, scene.n3) == (ref.n4, ref.n3)
+    assert maxl == pytest.approx(rrep["max_leakage"], rel=1e-6)
+    assert meanl == pytest.approx(rrep["mean_leakage"], rel=1e-6)
+    assert np.array_equal(scene.mean_x, ref.mean_x.astype(np.float32).astype(np.float64))
+
+
 def test_sweep_threshold_bit_exact(ctx):
     """exp(s_t) > tau decided exactly at the boundary (test_scene.cpp:12-21)."""
     tau = 0.7
