@@ -74,7 +74,7 @@ __device__ __forceinline__ float warp_sum(float v) {
 // d_conic = -alpha/2 * ([6] [7]; [7] [8]) (backward.cpp:212-221).
 constexpr int kAccStride = 12;
 #ifndef HGS_DIRECT_LANES
-#define HGS_DIRECT_LANES 4
+#define HGS_DIRECT_LANES 8
 #endif
 constexpr int kDirectLanes = HGS_DIRECT_LANES;  // contributing lanes up to which atomics replace the reduction
 constexpr int kThreadsB = 128;  // two pixels per thread
