@@ -89,30 +89,40 @@ __device__ __forceinline__ float rcp_approx(float x) {
     return y;
 }
 
-// Reverse-sweep state of one pixel.
-struct PixBwd {
-    float gr, gg, gb;  // dL/dC
-    float T;           // transmittance after the current splat
-    float GS;          // g . suffix colour (incl. T_final * bg)
-    uint32_t last;
+// Reverse-sweep state of a lane's two pixels, packed (lo = row y, hi = row
+// y + 4): dL/dC, the transmittance after the current splat, g . suffix colour
+// (incl. T_final * bg); last contributor per pixel.
+struct PixBwd2 {
+    f2 gr, gg, gb;
+    f2 T;
+    f2 GS;
+    uint32_t last0, last1;
 };
 
-// One pair of backward.cpp:204-221 given its alpha (p = the pair
-// contributes): returns w = a T_i and h = g dL/da (both 0 when !p) and steps
-// the pixel's state to the front of the splat.
-__device__ __forceinline__ void backprop_pair(PixBwd& s, bool p, float g, float alpha_f, const float4 col,
-                                              float& w_out, float& h_out) {
-    const float a = alpha_f * g;
-    const float inv = rcp_approx(1.0f - a);
-    const float Ti = s.T * inv;  // transmittance before this splat
-    const float gc = fmaf(s.gr, col.x, fmaf(s.gg, col.y, s.gb * col.z));
-    // dL/da = g . (rgb * T_i - S / (1 - a))
-    const float d_a = fmaf(Ti, gc, -inv * s.GS);
-    const float w = p ? a * Ti : 0.0f;
-    h_out = p ? g * d_a : 0.0f;
-    w_out = w;
-    s.GS = fmaf(w, gc, s.GS);
-    s.T = p ? Ti : s.T;
+// One pair of backward.cpp:204-221 for both pixels given the pair alphas
+// (p0 / p1 = the pixel's pair contributes): w = a T_i and h = g dL/da (0 when
+// the pixel's pair does not contribute), and the state stepped to the front
+// of the splat.  Per pixel exactly the scalar sequence
+//   a = alpha g; inv = rcp(1 - a); T_i = T inv; gc = g . rgb;
+//   dL/da = T_i gc - inv S;  w = a T_i;  h = g dL/da;  S += w gc
+__device__ __forceinline__ void backprop_pairs(PixBwd2& s, bool p0, bool p1, f2 G, float alpha_f, const float4 col,
+                                               float& w0, float& w1, float& h0, float& h1, f2& W) {
+    const f2 A = f2_mul(f2_bc(alpha_f), G);
+    const f2 OM = f2_sub(f2_bc(1.0f), A);
+    const f2 INV = f2_pk(rcp_approx(f2_lo(OM)), rcp_approx(f2_hi(OM)));
+    const f2 TI = f2_mul(s.T, INV);
+    const f2 GC = f2_fma(s.gr, f2_bc(col.x), f2_fma(s.gg, f2_bc(col.y), f2_mul(s.gb, f2_bc(col.z))));
+    const f2 NS = f2_mul(f2_mul(f2_bc(-1.0f), INV), s.GS);  // (-inv) S, exact negation
+    const f2 DA = f2_fma(TI, GC, NS);
+    const f2 AT = f2_mul(A, TI);
+    const f2 GDA = f2_mul(G, DA);
+    w0 = p0 ? f2_lo(AT) : 0.0f;
+    w1 = p1 ? f2_hi(AT) : 0.0f;
+    h0 = p0 ? f2_lo(GDA) : 0.0f;
+    h1 = p1 ? f2_hi(GDA) : 0.0f;
+    W = f2_pk(w0, w1);
+    s.GS = f2_fma(W, GC, s.GS);
+    s.T = f2_pk(p0 ? f2_lo(TI) : f2_lo(s.T), p1 ? f2_hi(TI) : f2_hi(s.T));
 }
 
 __global__ void __launch_bounds__(kThreadsB, 7) raster_bwd_kernel(
@@ -132,8 +142,12 @@ __global__ void __launch_bounds__(kThreadsB, 7) raster_bwd_kernel(
     const float pxc = (float)px + 0.5f, pyc0 = (float)py0 + 0.5f, pyc1 = (float)py1 + 0.5f;
     const double pcx = (double)px + 0.5, pcy0 = (double)py0 + 0.5, pcy1 = (double)py1 + 0.5;
 
-    auto init = [&](int py, PixBwd& s) {
-        s = PixBwd{0.f, 0.f, 0.f, 1.f, 0.f, rg.x};
+    struct Pix1 {
+        float gr, gg, gb, T, GS;
+        uint32_t last;
+    };
+    auto init = [&](int py, Pix1& s) {
+        s = Pix1{0.f, 0.f, 0.f, 1.f, 0.f, rg.x};
         if (px >= W || py >= H) return;
         const int pix = py * W + px;
         const uint32_t l = last_arr[pix];
@@ -146,12 +160,23 @@ __global__ void __launch_bounds__(kThreadsB, 7) raster_bwd_kernel(
         if (!(l & 0x80000000u) && (s.gr != 0.f || s.gg != 0.f || s.gb != 0.f)) s.last = l;
     };
     const int cshift = px - tx * kTile, rshift0 = 16 + py0 - ty * kTile, rshift1 = rshift0 + 4;
-    PixBwd s0, s1;
-    init(py0, s0);
-    init(py1, s1);
+    PixBwd2 s;
+    {
+        Pix1 a0, a1;
+        init(py0, a0);
+        init(py1, a1);
+        s.gr = f2_pk(a0.gr, a1.gr);
+        s.gg = f2_pk(a0.gg, a1.gg);
+        s.gb = f2_pk(a0.gb, a1.gb);
+        s.T = f2_pk(a0.T, a1.T);
+        s.GS = f2_pk(a0.GS, a1.GS);
+        s.last0 = a0.last;
+        s.last1 = a1.last;
+    }
+    const f2 PYC = f2_pk(pyc0, pyc1);
     if (threadIdx.x == 0) s_maxlast = rg.x;
     __syncthreads();
-    const uint32_t ml = max(s0.last, s1.last);
+    const uint32_t ml = max(s.last0, s.last1);
     if (ml > rg.x) atomicMax(&s_maxlast, ml);
     __syncthreads();
     const uint32_t end = s_maxlast;
@@ -177,8 +202,8 @@ __global__ void __launch_bounds__(kThreadsB, 7) raster_bwd_kernel(
             // box test from the staged tile-relative column/row masks
             const uint32_t bm = lds_u32(a_bm + 4 * k);
             const bool colin = (bm >> cshift) & 1u;
-            const bool b0 = colin & (idx < s0.last) & ((bm >> rshift0) & 1u);
-            const bool b1 = colin & (idx < s1.last) & ((bm >> rshift1) & 1u);
+            const bool b0 = colin & (idx < s.last0) & ((bm >> rshift0) & 1u);
+            const bool b1 = colin & (idx < s.last1) & ((bm >> rshift1) & 1u);
             if (!__any_sync(0xffffffffu, b0 || b1)) continue;
             const float4 L = lds_f4(a_chol + 16 * k), col = lds_f4(a_col + 16 * k);
             const uint32_t sj = lds_u32(a_j + 4 * k);
@@ -199,13 +224,18 @@ __global__ void __launch_bounds__(kThreadsB, 7) raster_bwd_kernel(
                     dx1 = d.x;
                     dy1 = d.y;
                 }
-            } else {
+            } else {  // both pixels in one packed sequence (= fast_x per pixel)
                 const float4 m = lds_f4(a_mean + 16 * k);
-                x0 = fast_x(m, L, pxc, pyc0, dx0, dy0);
+                dx0 = __fsub_rn(__fsub_rn(pxc, m.x), m.z);
                 dx1 = dx0;
-                dy1 = __fsub_rn(__fsub_rn(pyc1, m.y), m.w);
-                const float u1 = fmaf(L.x, dx1, L.y * dy1), u2 = L.z * dy1;
-                x1 = fmaf(u1, u1, u2 * u2);
+                const f2 DY = f2_sub(f2_sub(PYC, f2_bc(m.y)), f2_bc(m.w));
+                const f2 U1 = f2_fma(f2_bc(L.x), f2_bc(dx0), f2_mul(f2_bc(L.y), DY));
+                const f2 U2 = f2_mul(f2_bc(L.z), DY);
+                const f2 X = f2_fma(U1, U1, f2_mul(U2, U2));
+                x0 = f2_lo(X);
+                x1 = f2_hi(X);
+                dy0 = f2_lo(DY);
+                dy1 = f2_hi(DY);
             }
             // the oracle's a >= 1/255 test (exact: FP64 inside the guard band)
             const float x_skip = __int_as_float(hdr.z), x_keep = col.w;
@@ -220,13 +250,13 @@ __global__ void __launch_bounds__(kThreadsB, 7) raster_bwd_kernel(
             if (!__any_sync(0xffffffffu, p0 || p1)) continue;
             const float g0 = fast_exp2_neg(p0 ? x0 : 128.0f), g1 = fast_exp2_neg(p1 ? x1 : 128.0f);
             float w0, h0, w1, h1;
-            backprop_pair(s0, p0, g0, L.w, col, w0, h0);
-            backprop_pair(s1, p1, g1, L.w, col, w1, h1);
+            f2 Wp;
+            backprop_pairs(s, p0, p1, f2_pk(g0, g1), L.w, col, w0, w1, h0, h1, Wp);
             const float hx0 = h0 * dx0, hx1 = h1 * dx1, hy0 = h0 * dy0, hy1 = h1 * dy1;
             float v[9];
-            v[0] = fmaf(w0, s0.gr, w1 * s1.gr);
-            v[1] = fmaf(w0, s0.gg, w1 * s1.gg);
-            v[2] = fmaf(w0, s0.gb, w1 * s1.gb);
+            v[0] = fmaf(w0, f2_lo(s.gr), w1 * f2_hi(s.gr));
+            v[1] = fmaf(w0, f2_lo(s.gg), w1 * f2_hi(s.gg));
+            v[2] = fmaf(w0, f2_lo(s.gb), w1 * f2_hi(s.gb));
             v[3] = h0 + h1;
             v[4] = hx0 + hx1;
             v[5] = hy0 + hy1;
