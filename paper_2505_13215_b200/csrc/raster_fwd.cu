@@ -446,24 +446,45 @@ struct PixFwd {
     bool done, flagged;
 };
 
-// One pair of raster.cpp:132-143 given its alpha (p = the pair passes the
-// 1/255 test; a no-op otherwise).  err tracks the certified relative error
-// bound of T; a pixel whose T lands inside the band around the oracle's
-// T < 1e-4 decision is flagged for the FP64 fix-up.
-__device__ __forceinline__ void composite_pair(PixFwd& s, bool p, float a, float eps, const float4 c, uint32_t idx) {
-    const float w = p ? a * s.T : 0.0f;
-    s.r = fmaf(c.x, w, s.r);
-    s.g = fmaf(c.y, w, s.g);
-    s.b = fmaf(c.z, w, s.b);
-    const float om = 1.0f - a;
-    s.err = p ? fmaf(a * eps, rcp_approx(om), s.err + 2.5e-7f) : s.err;
-    s.T = p ? s.T * om : s.T;
-    s.last = p ? idx + 1 : s.last;
+// The two pixels of a lane, packed (lo = row y, hi = row y + 4).
+struct PixFwd2 {
+    f2 T, r, g, b, err;
+    uint32_t last0, last1, count0, count1;
+    bool done0, done1, flagged0, flagged1;
+};
+
+// One pair of raster.cpp:132-143 for both pixels given their alphas (p0 / p1
+// = the pixel's pair passes the 1/255 test; a no-op for that pixel
+// otherwise).  err tracks the certified relative error bound of T; a pixel
+// whose T lands inside the band around the oracle's T < 1e-4 decision is
+// flagged for the FP64 fix-up.  Per pixel exactly the scalar sequence
+//   w = a T; rgb += c w; err += a eps / (1 - a) + 2.5e-7; T *= 1 - a
+__device__ __forceinline__ void composite_pairs(PixFwd2& s, bool p0, bool p1, f2 A, f2 EPS, const float4 c,
+                                                uint32_t idx) {
+    const f2 AT = f2_mul(A, s.T);
+    const f2 W = f2_pk(p0 ? f2_lo(AT) : 0.0f, p1 ? f2_hi(AT) : 0.0f);
+    s.r = f2_fma(f2_bc(c.x), W, s.r);
+    s.g = f2_fma(f2_bc(c.y), W, s.g);
+    s.b = f2_fma(f2_bc(c.z), W, s.b);
+    const f2 OM = f2_sub(f2_bc(1.0f), A);
+    const f2 RC = f2_pk(rcp_approx(f2_lo(OM)), rcp_approx(f2_hi(OM)));
+    const f2 EN = f2_fma(f2_mul(A, EPS), RC, f2_add(s.err, f2_bc(2.5e-7f)));
+    s.err = f2_pk(p0 ? f2_lo(EN) : f2_lo(s.err), p1 ? f2_hi(EN) : f2_hi(s.err));
+    const f2 TN = f2_mul(s.T, OM);
+    s.T = f2_pk(p0 ? f2_lo(TN) : f2_lo(s.T), p1 ? f2_hi(TN) : f2_hi(s.T));
+    s.last0 = p0 ? idx + 1 : s.last0;
+    s.last1 = p1 ? idx + 1 : s.last1;
     // T and err only change with p, so re-testing an unchanged pixel is a no-op
-    if (s.T < fmaf(2.0e-4f, s.err, 1.0e-4f)) {
+    const f2 LIM = f2_fma(f2_bc(2.0e-4f), s.err, f2_bc(1.0e-4f));
+    const f2 LOW = f2_fma(f2_bc(-2.0e-4f), s.err, f2_bc(1.0e-4f));
+    if (f2_lo(s.T) < f2_lo(LIM)) {
         // inside the certified error band of the oracle's T < 1e-4 decision?
-        if (s.T > fmaf(-2.0e-4f, s.err, 1.0e-4f)) s.flagged = true;
-        s.done = true;
+        if (f2_lo(s.T) > f2_lo(LOW)) s.flagged0 = true;
+        s.done0 = true;
+    }
+    if (f2_hi(s.T) < f2_hi(LIM)) {
+        if (f2_hi(s.T) > f2_hi(LOW)) s.flagged1 = true;
+        s.done1 = true;
     }
 }
 
@@ -512,11 +533,18 @@ __global__ void __launch_bounds__(kThreads, 6) raster_fwd_kernel(
     const double pcx = (double)px + 0.5, pcy0 = (double)py0 + 0.5, pcy1 = (double)py1 + 0.5;
 
     const int cshift = px - tx * kTile, rshift0 = 16 + py0 - ty * kTile, rshift1 = rshift0 + 4;
-    PixFwd s0{1.0f, 0.f, 0.f, 0.f, 0.f, rg.x, 0u, !in0, false};
-    PixFwd s1{1.0f, 0.f, 0.f, 0.f, 0.f, rg.x, 0u, !in1, false};
+    PixFwd2 s;
+    s.T = f2_bc(1.0f);
+    s.r = s.g = s.b = s.err = f2_bc(0.0f);
+    s.last0 = s.last1 = rg.x;
+    s.count0 = s.count1 = 0u;
+    s.done0 = !in0;
+    s.done1 = !in1;
+    s.flagged0 = s.flagged1 = false;
+    const f2 PYC = f2_pk(pyc0, pyc1);
 
     for (uint32_t base = rg.x; base < rg.y; base += kBatch) {
-        if (__syncthreads_count(!(s0.done && s1.done)) == 0) break;
+        if (__syncthreads_count(!(s.done0 && s.done1)) == 0) break;
         for (int t = threadIdx.x; t < kBatch; t += kThreads) {
             const uint32_t idx = base + t;
             if (idx < rg.y) sb.load(t, fast, inst_val[idx], tx * kTile, ty * kTile);
@@ -524,18 +552,18 @@ __global__ void __launch_bounds__(kThreads, 6) raster_fwd_kernel(
         __syncthreads();
         const int nb = min((uint32_t)kBatch, rg.y - base);
         for (int k = 0; k < nb; ++k) {
-            if (s0.done && s1.done) break;
+            if (s.done0 && s.done1) break;
             if (!((sb.qm[k] >> warp) & 1u)) continue;  // exact: no pixel of this quadrant reaches 1/255
             const int4 hdr = sb.hdr[k];
             // box test from the staged tile-relative column/row masks
             const uint32_t bm = sb.bm[k];
             const bool colin = (bm >> cshift) & 1u;
-            const bool b0 = colin & !s0.done & ((bm >> rshift0) & 1u);
-            const bool b1 = colin & !s1.done & ((bm >> rshift1) & 1u);
+            const bool b0 = colin & !s.done0 & ((bm >> rshift0) & 1u);
+            const bool b1 = colin & !s.done1 & ((bm >> rshift1) & 1u);
             if (!(b0 || b1)) continue;
             if (kCount) {
-                s0.count += b0;
-                s1.count += b1;
+                s.count0 += b0;
+                s.count1 += b1;
             }
             const float4 L = sb.chol[k], c = sb.col[k];
             const SplatRec* e = exact + sb.j[k];
@@ -544,13 +572,15 @@ __global__ void __launch_bounds__(kThreads, 6) raster_fwd_kernel(
             if (eps_s < 0.0f) {  // FP64 exponent path (uniform per splat)
                 if (b0) x0 = exact_x(e, pcx, pcy0);
                 if (b1) x1 = exact_x(e, pcx, pcy1);
-            } else {  // both pixels share the column: one dx (same rounding as fast_x)
+            } else {  // both pixels share the column: one dx, the rest packed (= fast_x per pixel)
                 const float4 m = sb.mean[k];
-                float dx, dy0;
-                x0 = fast_x(m, L, pxc, pyc0, dx, dy0);
-                const float dy1 = __fsub_rn(__fsub_rn(pyc1, m.y), m.w);
-                const float u1 = fmaf(L.x, dx, L.y * dy1), u2 = L.z * dy1;
-                x1 = fmaf(u1, u1, u2 * u2);
+                const float dx = __fsub_rn(__fsub_rn(pxc, m.x), m.z);
+                const f2 DY = f2_sub(f2_sub(PYC, f2_bc(m.y)), f2_bc(m.w));
+                const f2 U1 = f2_fma(f2_bc(L.x), f2_bc(dx), f2_mul(f2_bc(L.y), DY));
+                const f2 U2 = f2_mul(f2_bc(L.z), DY);
+                const f2 X = f2_fma(U1, U1, f2_mul(U2, U2));
+                x0 = f2_lo(X);
+                x1 = f2_hi(X);
             }
             // the oracle's a >= 1/255 test (exact: FP64 inside the guard band)
             const float x_skip = __int_as_float(hdr.z), x_keep = c.w;
@@ -561,18 +591,24 @@ __global__ void __launch_bounds__(kThreads, 6) raster_fwd_kernel(
                 if (band1) p1 = exact_alpha_passes(e, pcx, pcy1);
             }
             if (!(p0 || p1)) continue;
-            const float a0 = L.w * fast_exp2_neg(p0 ? x0 : 128.0f), a1 = L.w * fast_exp2_neg(p1 ? x1 : 128.0f);
-            const float e1 = fabsf(eps_s);
-            composite_pair(s0, p0, a0, fmaf(e1, x0, kAlphaErr0), c, base + k);
-            composite_pair(s1, p1, a1, fmaf(e1, x1, kAlphaErr0), c, base + k);
+            const f2 X2 = f2_pk(x0, x1);
+            const f2 A = f2_mul(f2_bc(L.w), f2_pk(fast_exp2_neg(p0 ? x0 : 128.0f), fast_exp2_neg(p1 ? x1 : 128.0f)));
+            const f2 EPS = f2_fma(f2_bc(fabsf(eps_s)), X2, f2_bc(kAlphaErr0));
+            composite_pairs(s, p0, p1, A, EPS, c, base + k);
         }
     }
-    if (in0)
+    if (in0) {
+        const PixFwd s0{f2_lo(s.T), f2_lo(s.r), f2_lo(s.g), f2_lo(s.b), f2_lo(s.err), s.last0, s.count0, s.done0,
+                        s.flagged0};
         write_pixel(s0, py0 * W + px, bg_r, bg_g, bg_b, out_rgb, out_last, out_tfinal, out_trans, out_count, fix_list,
                     fix_count);
-    if (in1)
+    }
+    if (in1) {
+        const PixFwd s1{f2_hi(s.T), f2_hi(s.r), f2_hi(s.g), f2_hi(s.b), f2_hi(s.err), s.last1, s.count1, s.done1,
+                        s.flagged1};
         write_pixel(s1, py1 * W + px, bg_r, bg_g, bg_b, out_rgb, out_last, out_tfinal, out_trans, out_count, fix_list,
                     fix_count);
+    }
 }
 
 // Host launcher (keeps the template instantiations in this translation unit).
