@@ -92,8 +92,12 @@ constexpr int kSpan = kB + kWin - 1;  // inputs per blocked output group (14)
 template <typename Gt>
 __global__ void __launch_bounds__(256) ssim_fwd_kernel(const float* __restrict__ a, const Gt b, int W, int H,
                                                        float* __restrict__ maps, double* __restrict__ ssim_sum) {
-    __shared__ float sa[kS][kS + 1], sb[kS][kS + 1];
-    __shared__ float h[5][kS][kT + 1];
+    // a / b staged interleaved and the five window sums as (mu_a, mu_b),
+    // (E[a^2], E[b^2]) pairs + E[ab]: each FMA pair is one FFMA2 (same
+    // rounding per element as the scalar code)
+    __shared__ float2 sab[kS][kS + 1];
+    __shared__ float2 h01[kS][kT + 1], h23[kS][kT + 1];
+    __shared__ float h4[kS][kT + 1];
     __shared__ float red[8];
     const int c = blockIdx.z;
     const int vw = W - kWin + 1, vh = H - kWin + 1;
@@ -106,63 +110,78 @@ __global__ void __launch_bounds__(256) ssim_fwd_kernel(const float* __restrict__
             va = a[((size_t)y * W + x) * 3 + c];
             vb = b[((size_t)y * W + x) * 3 + c];
         }
-        sa[ly][lx] = va;
-        sb[ly][lx] = vb;
+        sab[ly][lx] = make_float2(va, vb);
     }
     __syncthreads();
     // horizontal: (row, group of 4 output columns)
     for (int e = threadIdx.x; e < kS * (kT / kB); e += blockDim.x) {
         const int g = e % (kT / kB), ly = e / (kT / kB);
         const int x0 = g * kB;
-        float m[kB][5];
+        f2 m01[kB], m23[kB];
+        float m4[kB];
 #pragma unroll
-        for (int o = 0; o < kB; ++o)
-#pragma unroll
-            for (int q = 0; q < 5; ++q) m[o][q] = 0.f;
+        for (int o = 0; o < kB; ++o) {
+            m01[o] = m23[o] = f2_bc(0.f);
+            m4[o] = 0.f;
+        }
 #pragma unroll
         for (int j = 0; j < kSpan; ++j) {
-            const float va = sa[ly][x0 + j], vb = sb[ly][x0 + j];
-            const float aa = va * va, bb = vb * vb, ab = va * vb;
+            const float2 v = sab[ly][x0 + j];
+            const f2 VAB = f2_pk(v.x, v.y);
+            const f2 SQ = f2_mul(VAB, VAB);  // (a^2, b^2)
+            const float ab = v.x * v.y;
 #pragma unroll
             for (int o = 0; o < kB; ++o) {
                 const int t = j - o;
                 if (t < 0 || t >= kWin) continue;
                 const float w = c_win[t];
-                m[o][0] = fmaf(w, va, m[o][0]);
-                m[o][1] = fmaf(w, vb, m[o][1]);
-                m[o][2] = fmaf(w, aa, m[o][2]);
-                m[o][3] = fmaf(w, bb, m[o][3]);
-                m[o][4] = fmaf(w, ab, m[o][4]);
+                m01[o] = f2_fma(f2_bc(w), VAB, m01[o]);
+                m23[o] = f2_fma(f2_bc(w), SQ, m23[o]);
+                m4[o] = fmaf(w, ab, m4[o]);
             }
         }
 #pragma unroll
-        for (int o = 0; o < kB; ++o)
-#pragma unroll
-            for (int q = 0; q < 5; ++q) h[q][ly][x0 + o] = m[o][q];
+        for (int o = 0; o < kB; ++o) {
+            h01[ly][x0 + o] = make_float2(f2_lo(m01[o]), f2_hi(m01[o]));
+            h23[ly][x0 + o] = make_float2(f2_lo(m23[o]), f2_hi(m23[o]));
+            h4[ly][x0 + o] = m4[o];
+        }
     }
     __syncthreads();
     // vertical: (column, group of 4 output rows) -> SSIM and its gradient maps
     float local = 0.f;
     {
         const int lx = threadIdx.x % kT, y0 = (threadIdx.x / kT) * kB;
-        float m[kB][5];
+        f2 m01[kB], m23[kB];
+        float m4[kB];
 #pragma unroll
-        for (int o = 0; o < kB; ++o)
-#pragma unroll
-            for (int q = 0; q < 5; ++q) m[o][q] = 0.f;
+        for (int o = 0; o < kB; ++o) {
+            m01[o] = m23[o] = f2_bc(0.f);
+            m4[o] = 0.f;
+        }
 #pragma unroll
         for (int i = 0; i < kSpan; ++i) {
-            float v[5];
-#pragma unroll
-            for (int q = 0; q < 5; ++q) v[q] = h[q][y0 + i][lx];
+            const float2 v01 = h01[y0 + i][lx], v23 = h23[y0 + i][lx];
+            const f2 V01 = f2_pk(v01.x, v01.y), V23 = f2_pk(v23.x, v23.y);
+            const float v4 = h4[y0 + i][lx];
 #pragma unroll
             for (int o = 0; o < kB; ++o) {
                 const int t = i - o;
                 if (t < 0 || t >= kWin) continue;
                 const float w = c_win[t];
-#pragma unroll
-                for (int q = 0; q < 5; ++q) m[o][q] = fmaf(w, v[q], m[o][q]);
+                m01[o] = f2_fma(f2_bc(w), V01, m01[o]);
+                m23[o] = f2_fma(f2_bc(w), V23, m23[o]);
+                m4[o] = fmaf(w, v4, m4[o]);
             }
+        }
+        float m[kB][5];
+#pragma unroll
+        for (int o = 0; o < kB; ++o) {
+            m[o][0] = f2_lo(m01[o]);
+            m[o][1] = f2_hi(m01[o]);
+            m[o][2] = f2_lo(m23[o]);
+            m[o][3] = f2_hi(m23[o]);
+            m[o][4] = m4[o];
         }
         const int vx = ox + lx;
         const size_t plane = (size_t)vw * vh;
@@ -196,8 +215,11 @@ template <typename Gt>
 __global__ void __launch_bounds__(256) ssim_bwd_kernel(const float* __restrict__ a, const Gt b, int W, int H,
                                                        const float* __restrict__ maps, float lambda, int with_ssim,
                                                        float* __restrict__ grad, double* __restrict__ l1_sum) {
-    __shared__ float sm[3][kS][kS + 1];
-    __shared__ float h[3][kS][kT + 1];
+    // maps 0 / 1 staged as pairs (one FFMA2 per window tap), map 2 alone
+    __shared__ float2 sm01[kS][kS + 1];
+    __shared__ float sm2[kS][kS + 1];
+    __shared__ float2 h01[kS][kT + 1];
+    __shared__ float h2[kS][kT + 1];
     __shared__ float red[8];
     const int c = blockIdx.z;
     const int vw = W - kWin + 1, vh = H - kWin + 1;
@@ -215,36 +237,39 @@ __global__ void __launch_bounds__(256) ssim_bwd_kernel(const float* __restrict__
                 m1 = maps[o + plane];
                 m2 = maps[o + 2 * plane];
             }
-            sm[0][ly][lx] = m0;
-            sm[1][ly][lx] = m1;
-            sm[2][ly][lx] = m2;
+            sm01[ly][lx] = make_float2(m0, m1);
+            sm2[ly][lx] = m2;
         }
         __syncthreads();
         for (int e = threadIdx.x; e < kS * (kT / kB); e += blockDim.x) {
             const int g = e % (kT / kB), ly = e / (kT / kB);
             const int x0 = g * kB;
-            float s3[kB][3];
+            f2 s01[kB];
+            float s2[kB];
 #pragma unroll
-            for (int o = 0; o < kB; ++o) s3[o][0] = s3[o][1] = s3[o][2] = 0.f;
+            for (int o = 0; o < kB; ++o) {
+                s01[o] = f2_bc(0.f);
+                s2[o] = 0.f;
+            }
 #pragma unroll
             for (int j = 0; j < kSpan; ++j) {
-                const float v0 = sm[0][ly][x0 + j], v1 = sm[1][ly][x0 + j], v2 = sm[2][ly][x0 + j];
+                const float2 v = sm01[ly][x0 + j];
+                const f2 V01 = f2_pk(v.x, v.y);
+                const float v2 = sm2[ly][x0 + j];
 #pragma unroll
                 for (int o = 0; o < kB; ++o) {
                     const int t = j - o;
                     if (t < 0 || t >= kWin) continue;
                     // pixel x gets window weight w[x - vx] from the map at vx
                     const float w = c_win[kWin - 1 - t];
-                    s3[o][0] = fmaf(w, v0, s3[o][0]);
-                    s3[o][1] = fmaf(w, v1, s3[o][1]);
-                    s3[o][2] = fmaf(w, v2, s3[o][2]);
+                    s01[o] = f2_fma(f2_bc(w), V01, s01[o]);
+                    s2[o] = fmaf(w, v2, s2[o]);
                 }
             }
 #pragma unroll
             for (int o = 0; o < kB; ++o) {
-                h[0][ly][x0 + o] = s3[o][0];
-                h[1][ly][x0 + o] = s3[o][1];
-                h[2][ly][x0 + o] = s3[o][2];
+                h01[ly][x0 + o] = make_float2(f2_lo(s01[o]), f2_hi(s01[o]));
+                h2[ly][x0 + o] = s2[o];
             }
         }
         __syncthreads();
@@ -257,18 +282,27 @@ __global__ void __launch_bounds__(256) ssim_bwd_kernel(const float* __restrict__
 #pragma unroll
     for (int o = 0; o < kB; ++o) g3[o][0] = g3[o][1] = g3[o][2] = 0.f;
     if (with_ssim) {
+        f2 g01[kB];
+#pragma unroll
+        for (int o = 0; o < kB; ++o) g01[o] = f2_bc(0.f);
 #pragma unroll
         for (int i = 0; i < kSpan; ++i) {
-            const float v0 = h[0][y0 + i][lx], v1 = h[1][y0 + i][lx], v2 = h[2][y0 + i][lx];
+            const float2 v = h01[y0 + i][lx];
+            const f2 V01 = f2_pk(v.x, v.y);
+            const float v2 = h2[y0 + i][lx];
 #pragma unroll
             for (int o = 0; o < kB; ++o) {
                 const int t = i - o;
                 if (t < 0 || t >= kWin) continue;
                 const float w = c_win[kWin - 1 - t];
-                g3[o][0] = fmaf(w, v0, g3[o][0]);
-                g3[o][1] = fmaf(w, v1, g3[o][1]);
+                g01[o] = f2_fma(f2_bc(w), V01, g01[o]);
                 g3[o][2] = fmaf(w, v2, g3[o][2]);
             }
+        }
+#pragma unroll
+        for (int o = 0; o < kB; ++o) {
+            g3[o][0] = f2_lo(g01[o]);
+            g3[o][1] = f2_hi(g01[o]);
         }
     }
     const int x = ox + lx;
