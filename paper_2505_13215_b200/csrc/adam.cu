@@ -214,6 +214,7 @@ __global__ void __launch_bounds__(128) adam_classes_kernel(AdamPools P, AdamArgs
 __global__ void __launch_bounds__(256) adam_rows_kernel(AdamPools P, AdamArgs A, const uint8_t* __restrict__ cls_ok3,
                                                         const uint8_t* __restrict__ cls_ok4, int blocks_per_row3,
                                                         int blocks_per_row4) {
+    pdl_wait();  // launched with launch_pdl
     if (!update_allowed(A)) return;
     const int R3 = R3_SH + P.K3 - 4, R4 = R4_SH + P.K3 - 8;  // rows without the quaternions
     int b = blockIdx.x;

@@ -502,11 +502,10 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
         ctx->fix_list.as<uint32_t>(), &dc->fix_count);
     count_launch();
     CKL();
-    raster_fixup_kernel<<<ctx->sms * 2, 128, 0, st>>>(
-        ctx->fix_list.as<uint32_t>(), &dc->fix_count, ctx->ranges.as<uint2>(), inst_vals,
-        ctx->rec_sorted.as<SplatRec>(), W, tiles_x, bg[0], bg[1], bg[2], ctx->img.as<float>(),
-        ctx->last.as<uint32_t>(), ctx->tfinal.as<float>(), want_trans ? ctx->trans.as<float>() : nullptr,
-        want_count ? ctx->count.as<uint32_t>() : nullptr);
+    CK(launch_pdl(raster_fixup_kernel, dim3(ctx->sms * 2), dim3(128), 0, st, ctx->fix_list.as<uint32_t>(),
+                  &dc->fix_count, ctx->ranges.as<uint2>(), inst_vals, ctx->rec_sorted.as<SplatRec>(), W, tiles_x,
+                  bg[0], bg[1], bg[2], ctx->img.as<float>(), ctx->last.as<uint32_t>(), ctx->tfinal.as<float>(),
+                  want_trans ? ctx->trans.as<float>() : nullptr, want_count ? ctx->count.as<uint32_t>() : nullptr));
     count_launch();
     CKL();
     prof_end(ctx);
@@ -1035,3 +1034,11 @@ hgs_status hgs_debug_instance_masks(hgs_ctx* ctx, uint8_t* masks, int64_t cap, i
 }
 
 }  // extern "C"
+
+namespace hgs {
+// programmatic dependent launches (raster_common.cuh launch_pdl): on unless HGS_NO_PDL is set
+bool pdl_enabled() {
+    static const bool on = getenv("HGS_NO_PDL") == nullptr;
+    return on;
+}
+}  // namespace hgs

@@ -40,6 +40,7 @@ __global__ void __launch_bounds__(128, 4) gaussian_bwd_kernel(
     float* __restrict__ sn3, float* __restrict__ gn4, float* __restrict__ gn3, float* __restrict__ cnt4,
     float* __restrict__ cnt3, const double* __restrict__ conic_src, int conic_stride,
     const float4* __restrict__ ddir, int first) {
+    pdl_wait();  // launched with launch_pdl
     // one thread per Gaussian in pool order (coalesced SoA parameter and
     // gradient rows); the splat's accumulators are found through the
     // gid -> depth-sorted index map written by the gather kernel
@@ -329,6 +330,7 @@ __global__ void __launch_bounds__(128) sh_bwd_kernel(int N, const uint32_t* __re
                                                      float* __restrict__ g4, float* __restrict__ g3,
                                                      const ShRec* __restrict__ shrec, float4* __restrict__ ddir,
                                                      int first) {
+    pdl_wait();  // launched with launch_pdl
     const int gid = blockIdx.x * blockDim.x + threadIdx.x;
     if (gid >= N) return;
     const uint32_t j = sorted_of_gid[gid];

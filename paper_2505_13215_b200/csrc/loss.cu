@@ -215,6 +215,7 @@ template <typename Gt>
 __global__ void __launch_bounds__(256) ssim_bwd_kernel(const float* __restrict__ a, const Gt b, int W, int H,
                                                        const float* __restrict__ maps, float lambda, int with_ssim,
                                                        float* __restrict__ grad, double* __restrict__ l1_sum) {
+    pdl_wait();  // launched with launch_pdl
     // maps 0 / 1 staged as pairs (one FFMA2 per window tap), map 2 alone
     __shared__ float2 sm01[kS][kS + 1];
     __shared__ float sm2[kS][kS + 1];
@@ -331,11 +332,17 @@ void launch_loss(cudaStream_t st, const float* img, const void* gt, bool gt_u8, 
     if (gt_u8) {
         const GtU8 b{static_cast<const uint8_t*>(gt)};
         if (with_ssim) ssim_fwd_kernel<GtU8><<<g, 256, 0, st>>>(img, b, W, H, maps, &sums[0]);
-        ssim_bwd_kernel<GtU8><<<gb, 256, 0, st>>>(img, b, W, H, maps, lambda, with_ssim ? 1 : 0, grad, &sums[1]);
+        if (with_ssim)  // PDL after the forward kernel (not after the memset of the sums)
+            launch_pdl(ssim_bwd_kernel<GtU8>, gb, dim3(256), 0, st, img, b, W, H, maps, lambda, 1, grad, &sums[1]);
+        else
+            ssim_bwd_kernel<GtU8><<<gb, 256, 0, st>>>(img, b, W, H, maps, lambda, 0, grad, &sums[1]);
     } else {
         const GtF32 b{static_cast<const float*>(gt)};
         if (with_ssim) ssim_fwd_kernel<GtF32><<<g, 256, 0, st>>>(img, b, W, H, maps, &sums[0]);
-        ssim_bwd_kernel<GtF32><<<gb, 256, 0, st>>>(img, b, W, H, maps, lambda, with_ssim ? 1 : 0, grad, &sums[1]);
+        if (with_ssim)
+            launch_pdl(ssim_bwd_kernel<GtF32>, gb, dim3(256), 0, st, img, b, W, H, maps, lambda, 1, grad, &sums[1]);
+        else
+            ssim_bwd_kernel<GtF32><<<gb, 256, 0, st>>>(img, b, W, H, maps, lambda, 0, grad, &sums[1]);
     }
 }
 

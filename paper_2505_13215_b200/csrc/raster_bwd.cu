@@ -291,6 +291,7 @@ __global__ void __launch_bounds__(128) raster_bwd_exact_kernel(
     const uint32_t* __restrict__ inst_val, const SplatRec* __restrict__ exact, int W, int tiles_x, double bg_r,
     double bg_g, double bg_b, const uint32_t* __restrict__ last_arr, const float* __restrict__ dL_dimg,
     float* __restrict__ accum) {
+    pdl_wait();  // launched with launch_pdl
     __shared__ double s_om[4][32 * kExactSub];
     const uint32_t n = *fix_count;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;

@@ -90,6 +90,31 @@ static __device__ __noinline__ float2 exact_delta(const SplatRec* e, double pcx,
     return make_float2((float)__dsub_rn(pcx, e->sx), (float)__dsub_rn(pcy, e->sy));
 }
 
+// ---- programmatic dependent launch (sm_90+): a kernel launched with
+// launch_pdl may be scheduled while its predecessor in the stream drains;
+// pdl_wait() (first statement of such a kernel) blocks until the
+// predecessor grid has completed and its writes are visible.  A no-op for a
+// normally launched kernel.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+bool pdl_enabled();  // capi.cu: HGS_NO_PDL unset
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 // ---- packed FP32 pairs (sm_100 FADD2 / FMUL2 / FFMA2): the two pixels of a
 // rasterizer lane in one instruction.  Each half rounds exactly like the
 // scalar IEEE op (no ftz), so packed and scalar code give identical bits.

@@ -165,27 +165,28 @@ hgs_status run_backward(hgs_ctx* ctx, const float* lg, double scale) {
                                                (float)ctx->bg[2], ctx->accum.as<float>());
     count_launch();
     CKL();
-    raster_bwd_exact_kernel<<<ctx->sms * 2, 128, 0, st>>>(
-        ctx->fix_list.as<uint32_t>(), fix_count, ctx->ranges.as<uint2>(), ctx->inst_vals_final,
-        ctx->rec_sorted.as<SplatRec>(), ctx->W, ctx->tiles_x, ctx->bg[0], ctx->bg[1], ctx->bg[2],
-        ctx->last.as<uint32_t>(), lg, ctx->accum.as<float>());
+    CK(launch_pdl(raster_bwd_exact_kernel, dim3(ctx->sms * 2), dim3(128), 0, st, ctx->fix_list.as<uint32_t>(),
+                  fix_count, ctx->ranges.as<uint2>(), ctx->inst_vals_final, ctx->rec_sorted.as<SplatRec>(), ctx->W,
+                  ctx->tiles_x, ctx->bg[0], ctx->bg[1], ctx->bg[2], ctx->last.as<uint32_t>(), lg,
+                  ctx->accum.as<float>()));
     count_launch();
     CKL();
     prof_end(ctx);
     prof_begin(ctx, PH_GAUSS_BWD);
     const int N = (int)(ctx->n4 + ctx->n3);
     CK(ctx->ddir.ensure((size_t)N * sizeof(float4)));
-    sh_bwd_kernel<<<div_up((uint32_t)N, 128), 128, 0, st>>>(
-        N, ctx->sorted_of_gid.as<uint32_t>(), ctx->accum.as<float>(), kAccStrideHost, (int)ctx->n4,
-        ctx->p4.as<float>(), ctx->cap4, ctx->p3.as<float>(), ctx->cap3, ctx->deg, (float)scale, ctx->g4, ctx->g3,
-        ctx->shdir.as<ShRec>(), ctx->ddir.as<float4>(), ctx->grads_zero ? 1 : 0);
+    CK(launch_pdl(sh_bwd_kernel, dim3(div_up((uint32_t)N, 128)), dim3(128), 0, st, N,
+                  ctx->sorted_of_gid.as<uint32_t>(), ctx->accum.as<float>(), kAccStrideHost, (int)ctx->n4,
+                  ctx->p4.as<float>(), ctx->cap4, ctx->p3.as<float>(), ctx->cap3, ctx->deg, (float)scale, ctx->g4,
+                  ctx->g3, ctx->shdir.as<ShRec>(), ctx->ddir.as<float4>(), ctx->grads_zero ? 1 : 0));
     count_launch();
     CKL();
-    gaussian_bwd_kernel<<<div_up((uint32_t)N, 128), 128, 0, st>>>(
-        N, ctx->sorted_of_gid.as<uint32_t>(), ctx->accum.as<float>(), kAccStrideHost, (int)ctx->n4, ctx->p4.as<float>(), ctx->cap4,
-        ctx->p3.as<float>(), ctx->cap3, ctx->deg, ctx->cam, ctx->t, scale, ctx->g4, ctx->g3, ctx->sn4.as<float>(),
-        ctx->sn3.as<float>(), ctx->dgn4, ctx->dgn3, ctx->dcnt4, ctx->dcnt3, &ctx->rec_sorted.as<SplatRec>()->c00,
-        (int)(sizeof(SplatRec) / sizeof(double)), ctx->ddir.as<float4>(), ctx->grads_zero ? 1 : 0);
+    CK(launch_pdl(gaussian_bwd_kernel, dim3(div_up((uint32_t)N, 128)), dim3(128), 0, st, N,
+                  ctx->sorted_of_gid.as<uint32_t>(), ctx->accum.as<float>(), kAccStrideHost, (int)ctx->n4,
+                  ctx->p4.as<float>(), ctx->cap4, ctx->p3.as<float>(), ctx->cap3, ctx->deg, ctx->cam, ctx->t, scale,
+                  ctx->g4, ctx->g3, ctx->sn4.as<float>(), ctx->sn3.as<float>(), ctx->dgn4, ctx->dgn3, ctx->dcnt4,
+                  ctx->dcnt3, &ctx->rec_sorted.as<SplatRec>()->c00, (int)(sizeof(SplatRec) / sizeof(double)),
+                  ctx->ddir.as<float4>(), ctx->grads_zero ? 1 : 0));
     count_launch();
     CKL();
     ctx->grads_zero = false;
@@ -279,7 +280,7 @@ hgs_status run_adam(hgs_ctx* ctx, const hgs_lrs* lrs, double mean_lr_scale, cons
         const int R3 = R3_SH + P.K3 - 4, R4 = R4_SH + P.K3 - 8;
         const int blocks = R3 * bpr3 + R4 * bpr4;
         if (blocks > 0) {
-            adam_rows_kernel<<<blocks, 256, 0, st>>>(P, A, ok3, ok4, bpr3, bpr4);
+            CK(launch_pdl(adam_rows_kernel, dim3(blocks), dim3(256), 0, st, P, A, ok3, ok4, bpr3, bpr4));
             count_launch();
             CKL();
         }
