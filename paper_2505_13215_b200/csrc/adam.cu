@@ -114,6 +114,7 @@ __global__ void __launch_bounds__(128) adam_classes_kernel(AdamPools P, AdamArgs
                                                            uint8_t* __restrict__ cls_ok4,
                                                            unsigned long long* __restrict__ skipped_total,
                                                            uint32_t* __restrict__ flags) {
+    pdl_wait();  // launched with launch_pdl
     // one thread per (parameter class, 4 consecutive Gaussians); 3D units first
     if (!update_allowed(A)) return;
     const int t = blockIdx.x * blockDim.x + threadIdx.x;

@@ -177,6 +177,7 @@ DevCamera to_dev(const hgs_camera* c) {
 }
 
 __global__ void visflag_kernel(const uint32_t* __restrict__ ntiles, int n, uint32_t* __restrict__ flag) {
+    pdl_wait();  // launched with launch_pdl
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) flag[i] = ntiles[i] > 0u ? 1u : 0u;
 }
@@ -184,6 +185,7 @@ __global__ void visflag_kernel(const uint32_t* __restrict__ ntiles, int n, uint3
 __global__ void compact_kernel(const uint32_t* __restrict__ ntiles, const uint32_t* __restrict__ pos,
                                const uint32_t* __restrict__ depth_key, int n, uint32_t* __restrict__ keys,
                                uint32_t* __restrict__ vals) {
+    pdl_wait();  // launched with launch_pdl
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n && ntiles[i] > 0u) {
         const uint32_t p = pos[i];
@@ -308,6 +310,9 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
         CK(ctx->vispos.ensure((size_t)N * 4));
         CK(ctx->shdir.ensure((size_t)N * sizeof(ShRec)));
         CK(ctx->scan_ws.ensure(scan_workspace_bytes(N) + 4096));
+        CK(ctx->sorted_of_gid.ensure((size_t)N * 4));
+        // zeroed here, ahead of the kernel chain (gather writes it)
+        CK(cudaMemsetAsync(ctx->sorted_of_gid.p, 0xff, (size_t)N * 4, st));
         prof_begin(ctx, PH_PREPROCESS);
         preprocess_kernel<<<div_up(N, 256), 256, 0, st>>>(
             ctx->p4.as<float>(), ctx->cap4, n4, ctx->p3.as<float>(), ctx->cap3, n3, ctx->deg, ctx->cam, t, cutoff,
@@ -315,7 +320,8 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
             &dc->flags, ctx->shdir.as<ShRec>());
         count_launch();
         CKL();
-        visflag_kernel<<<div_up(N, 256), 256, 0, st>>>(ctx->ntiles.as<uint32_t>(), N, ctx->visflag.as<uint32_t>());
+        CK(launch_pdl(visflag_kernel, dim3(div_up(N, 256)), dim3(256), 0, st, ctx->ntiles.as<uint32_t>(), N,
+                      ctx->visflag.as<uint32_t>()));
         count_launch();
         exclusive_scan_u32(ctx->visflag.as<uint32_t>(), ctx->vispos.as<uint32_t>(), N, &dc->V,
                            ctx->scan_ws.as<uint32_t>(), st);
@@ -328,9 +334,9 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
         CK(ctx->sort_k2.ensure((size_t)N * 4));
         CK(ctx->sort_v2.ensure((size_t)N * 4));
         prof_begin(ctx, PH_DEPTH_SORT);
-        compact_kernel<<<div_up(N, 256), 256, 0, st>>>(ctx->ntiles.as<uint32_t>(), ctx->vispos.as<uint32_t>(),
-                                                        ctx->depth_key.as<uint32_t>(), N, ctx->sort_k.as<uint32_t>(),
-                                                        ctx->sort_v.as<uint32_t>());
+        CK(launch_pdl(compact_kernel, dim3(div_up(N, 256)), dim3(256), 0, st, ctx->ntiles.as<uint32_t>(),
+                      ctx->vispos.as<uint32_t>(), ctx->depth_key.as<uint32_t>(), N, ctx->sort_k.as<uint32_t>(),
+                      ctx->sort_v.as<uint32_t>()));
         count_launch();
         CKL();
         CK(ctx->sort_ws.ensure(radix_workspace_bytes(N) + 4096));
@@ -348,11 +354,10 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
         CK(ctx->sorted_of_gid.ensure((size_t)N * 4));
         CK(ctx->pcut.ensure((size_t)N * sizeof(CullRec)));
         prof_begin(ctx, PH_DUPLICATE);
-        CK(cudaMemsetAsync(ctx->sorted_of_gid.p, 0xff, (size_t)N * 4, st));
-        gather_sorted_kernel<<<div_up((uint32_t)N, 256), 256, 0, st>>>(
+        CK(launch_pdl(gather_sorted_kernel, dim3(div_up((uint32_t)N, 256)), dim3(256), 0, st,
             sorted_gid, &dc->V, ctx->rec.as<SplatRec>(), ctx->ntiles.as<uint32_t>(), ctx->rec_sorted.as<SplatRec>(),
             ctx->fast_sorted.as<SplatFast>(), ctx->ntiles_sorted.as<uint32_t>(), ctx->sorted_of_gid.as<uint32_t>(),
-            ctx->pcut.as<CullRec>());
+            ctx->pcut.as<CullRec>()));
         count_launch();
         CKL();
         exclusive_scan_u32(ctx->ntiles_sorted.as<uint32_t>(), ctx->inst_off.as<uint32_t>(), N, &dc->I,
@@ -397,11 +402,11 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
                 ctx->inst_off.as<uint32_t>(), ctx->ntiles_sorted.as<uint32_t>(), (int)V, ctx->dup_first.as<uint32_t>(),
                 icap ? &dc->V : nullptr, dup_blocks);
             count_launch();
-            duplicate_compact_kernel<<<dup_blocks, 256, 0, st>>>(
-                ctx->fast_sorted.as<SplatFast>(), (int)V, ctx->inst_off.as<uint32_t>(), tiles_x,
-                ctx->pcut.as<CullRec>(), ctx->dup_first.as<uint32_t>(), (int)I, ctx->inst_k2.as<uint32_t>(),
-                ctx->inst_v2.as<uint32_t>(), &dc->I_kept, status, counter, icap ? &dc->V : nullptr,
-                icap ? &dc->I : nullptr, &dc->flags);
+            CK(launch_pdl(duplicate_compact_kernel, dim3(dup_blocks), dim3(256), 0, st, ctx->fast_sorted.as<SplatFast>(),
+                          (int)V, ctx->inst_off.as<uint32_t>(), tiles_x, ctx->pcut.as<CullRec>(),
+                          ctx->dup_first.as<uint32_t>(), (int)I, ctx->inst_k2.as<uint32_t>(), ctx->inst_v2.as<uint32_t>(),
+                          &dc->I_kept, status, counter, icap ? &dc->V : nullptr, icap ? &dc->I : nullptr,
+                          &dc->flags));
             count_launch();
             CKL();
             prof_end(ctx);
@@ -417,7 +422,9 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
             CKL();
             uint32_t* keys = which ? ctx->inst_k.as<uint32_t>() : ctx->inst_k2.as<uint32_t>();
             inst_vals = which ? ctx->inst_v.as<uint32_t>() : ctx->inst_v2.as<uint32_t>();
-            tile_ranges_dev_kernel<<<div_up((uint32_t)I, 256), 256, 0, st>>>(keys, &dc->I_kept, ctx->ranges.as<uint2>());
+            CK(launch_pdl(tile_ranges_dev_kernel, dim3(div_up((uint32_t)I, 256)), dim3(256), 0, st,
+                          static_cast<const uint32_t*>(keys), static_cast<const uint32_t*>(&dc->I_kept),
+                          ctx->ranges.as<uint2>()));
             count_launch();
             CKL();
             prof_end(ctx);
@@ -481,7 +488,9 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
             CKL();
             keys = which ? ctx->inst_k.as<uint32_t>() : ctx->inst_k2.as<uint32_t>();
             inst_vals = which ? ctx->inst_v.as<uint32_t>() : ctx->inst_v2.as<uint32_t>();
-            tile_ranges_dev_kernel<<<div_up((uint32_t)I, 256), 256, 0, st>>>(keys, &dc->I_kept, ctx->ranges.as<uint2>());
+            CK(launch_pdl(tile_ranges_dev_kernel, dim3(div_up((uint32_t)I, 256)), dim3(256), 0, st,
+                          static_cast<const uint32_t*>(keys), static_cast<const uint32_t*>(&dc->I_kept),
+                          ctx->ranges.as<uint2>()));
             count_launch();
         } else {
             keys = ctx->inst_keys_all;

@@ -130,6 +130,7 @@ __global__ void __launch_bounds__(kThreadsB, 7) raster_bwd_kernel(
     const SplatRec* __restrict__ exact, int W, int H, int tiles_x, const float* __restrict__ tfinal,
     const uint32_t* __restrict__ last_arr, const float* __restrict__ dL_dimg, float bg_r, float bg_g, float bg_b,
     float* __restrict__ accum) {
+    pdl_wait();  // launched with launch_pdl
     __shared__ SplatBatch<kBatchB> sb;
     __shared__ uint32_t s_maxlast;
     const int tile = blockIdx.x;

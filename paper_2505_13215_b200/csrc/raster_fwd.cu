@@ -19,6 +19,7 @@ __global__ void __launch_bounds__(256) gather_sorted_kernel(const uint32_t* __re
                                                             uint32_t* __restrict__ ntiles_sorted,
                                                             uint32_t* __restrict__ sorted_of_gid,
                                                             CullRec* __restrict__ cull_rec) {
+    pdl_wait();  // launched with launch_pdl
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= (int)*V_dev) return;
     const uint32_t gid = sorted_gid[j];
@@ -274,6 +275,7 @@ __global__ void __launch_bounds__(kDupThreads) duplicate_compact_kernel(
     uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out, uint32_t* __restrict__ kept_total,
     unsigned long long* status, uint32_t* __restrict__ counter, const uint32_t* V_dev, const uint32_t* I_dev,
     uint32_t* flags) {
+    pdl_wait();  // launched with launch_pdl
     __shared__ uint32_t s_off[kDupPerCta + 1];
     __shared__ uint32_t s_tile, s_excl, s_wt[kDupThreads / 32];
     if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1u);
@@ -422,6 +424,7 @@ __global__ void __launch_bounds__(256) tile_ranges_kernel(const uint32_t* __rest
 __global__ void __launch_bounds__(256) tile_ranges_dev_kernel(const uint32_t* __restrict__ keys,
                                                               const uint32_t* __restrict__ n_dev,
                                                               uint2* __restrict__ ranges) {
+    pdl_wait();  // launched with launch_pdl
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const int n = (int)*n_dev;
     if (i >= n) return;
@@ -520,6 +523,7 @@ __global__ void __launch_bounds__(kThreads, 6) raster_fwd_kernel(
     float* __restrict__ out_rgb, uint32_t* __restrict__ out_last, float* __restrict__ out_tfinal,
     float* __restrict__ out_trans, uint32_t* __restrict__ out_count, uint32_t* __restrict__ fix_list,
     uint32_t* __restrict__ fix_count) {
+    pdl_wait();  // launched with launch_pdl
     __shared__ SplatBatch<kBatch> sb;
     const int tile = blockIdx.x;
     const int tx = tile % tiles_x, ty = tile / tiles_x;
@@ -617,13 +621,13 @@ void launch_raster_fwd(bool count_map, int n_tiles, cudaStream_t st, const uint2
                        float bg_b, float* out_rgb, uint32_t* out_last, float* out_tfinal, float* out_trans,
                        uint32_t* out_count, uint32_t* fix_list, uint32_t* fix_count) {
     if (count_map)
-        raster_fwd_kernel<true><<<n_tiles, kThreads, 0, st>>>(ranges, inst_val, fast, exact, W, H, tiles_x, bg_r, bg_g,
-                                                              bg_b, out_rgb, out_last, out_tfinal, out_trans,
-                                                              out_count, fix_list, fix_count);
+        launch_pdl(raster_fwd_kernel<true>, dim3(n_tiles), dim3(kThreads), 0, st, ranges, inst_val, fast, exact, W, H,
+                   tiles_x, bg_r, bg_g, bg_b, out_rgb, out_last, out_tfinal, out_trans, out_count, fix_list,
+                   fix_count);
     else
-        raster_fwd_kernel<false><<<n_tiles, kThreads, 0, st>>>(ranges, inst_val, fast, exact, W, H, tiles_x, bg_r,
-                                                               bg_g, bg_b, out_rgb, out_last, out_tfinal, out_trans,
-                                                               out_count, fix_list, fix_count);
+        launch_pdl(raster_fwd_kernel<false>, dim3(n_tiles), dim3(kThreads), 0, st, ranges, inst_val, fast, exact, W,
+                   H, tiles_x, bg_r, bg_g, bg_b, out_rgb, out_last, out_tfinal, out_trans, out_count, fix_list,
+                   fix_count);
 }
 
 // Exact FP64 recomposite of the flagged pixels (raster.cpp:123-148), one warp

@@ -147,7 +147,10 @@ hgs_status ensure_scratch(hgs_ctx* ctx) {
 }
 
 // K6 + exact pixels + K7 for the current tape; dL/dimage in device `lg`.
-hgs_status run_backward(hgs_ctx* ctx, const float* lg, double scale) {
+// The zeroing of the backward's outputs (screen norms, per-splat
+// accumulators); the training step issues it before the loss so that the
+// kernel chain loss -> K6 -> K7 has no memset in it (programmatic launches).
+hgs_status zero_backward(hgs_ctx* ctx) {
     cudaStream_t st = ctx->stream;
     const int64_t V = ctx->V;
     CK(cudaMemsetAsync(ctx->sn4.p, 0, (size_t)ctx->cap4 * 4, st));
@@ -155,14 +158,25 @@ hgs_status run_backward(hgs_ctx* ctx, const float* lg, double scale) {
     if (V == 0 || ctx->I == 0) return HGS_OK;
     CK(ctx->accum.ensure((size_t)V * kAccStrideHost * 4));
     CK(cudaMemsetAsync(ctx->accum.p, 0, (size_t)V * kAccStrideHost * 4, st));
+    return HGS_OK;
+}
+
+hgs_status run_backward(hgs_ctx* ctx, const float* lg, double scale, bool zeroed = false) {
+    cudaStream_t st = ctx->stream;
+    const int64_t V = ctx->V;
+    if (!zeroed) {
+        hgs_status r = zero_backward(ctx);
+        if (r != HGS_OK) return r;
+    }
+    if (V == 0 || ctx->I == 0) return HGS_OK;
     const int n_tiles = ctx->tiles_x * ctx->tiles_y;
     const uint32_t* fix_count = &ctx->counters.as<Counters>()->fix_count;
     prof_begin(ctx, PH_RASTER_BWD);
-    raster_bwd_kernel<<<n_tiles, 128, 0, st>>>(ctx->ranges.as<uint2>(), ctx->inst_vals_final,
-                                               ctx->fast_sorted.as<SplatFast>(), ctx->rec_sorted.as<SplatRec>(),
-                                               ctx->W, ctx->H, ctx->tiles_x, ctx->tfinal.as<float>(),
-                                               ctx->last.as<uint32_t>(), lg, (float)ctx->bg[0], (float)ctx->bg[1],
-                                               (float)ctx->bg[2], ctx->accum.as<float>());
+    CK(launch_pdl(raster_bwd_kernel, dim3(n_tiles), dim3(128), 0, st, ctx->ranges.as<uint2>(),
+                  static_cast<const uint32_t*>(ctx->inst_vals_final), ctx->fast_sorted.as<SplatFast>(),
+                  ctx->rec_sorted.as<SplatRec>(), ctx->W, ctx->H, ctx->tiles_x, ctx->tfinal.as<float>(),
+                  ctx->last.as<uint32_t>(), lg, (float)ctx->bg[0], (float)ctx->bg[1], (float)ctx->bg[2],
+                  ctx->accum.as<float>()));
     count_launch();
     CKL();
     CK(launch_pdl(raster_bwd_exact_kernel, dim3(ctx->sms * 2), dim3(128), 0, st, ctx->fix_list.as<uint32_t>(),
@@ -273,7 +287,8 @@ hgs_status run_adam(hgs_ctx* ctx, const hgs_lrs* lrs, double mean_lr_scale, cons
         uint8_t* ok3 = ctx->adam_ok.as<uint8_t>();
         uint8_t* ok4 = ok3 + 5 * ctx->cap3;
         const uint32_t units = 5 * div_up((uint32_t)ctx->n3, 4) + 7 * div_up((uint32_t)ctx->n4, 4);
-        adam_classes_kernel<<<div_up(units, 128), 128, 0, st>>>(P, A, ok3, ok4, &sc->skipped, &sc->flags);
+        CK(launch_pdl(adam_classes_kernel, dim3(div_up(units, 128)), dim3(128), 0, st, P, A, ok3, ok4, &sc->skipped,
+                      &sc->flags));
         count_launch();
         CKL();
         const int bpr3 = (int)div_up(div_up((uint32_t)ctx->n3, 4), 256), bpr4 = (int)div_up(div_up((uint32_t)ctx->n4, 4), 256);
@@ -719,6 +734,8 @@ hgs_status train_step_impl(hgs_ctx* ctx, int n_views, const hgs_camera* cams, co
         r = ensure_copy_stream(ctx);
         if (r != HGS_OK) return r;
     }
+    if (apply_adam)  // here, not between the last backward kernel and Adam (programmatic launches)
+        CK(cudaMemsetAsync(&sc->skipped, 0, sizeof(unsigned long long) + 8, ctx->stream));
     for (int v = 0; v < n_views; ++v) {
         const void* g = nullptr;
         const int b = v & 1;
@@ -738,13 +755,15 @@ hgs_status train_step_impl(hgs_ctx* ctx, int n_views, const hgs_camera* cams, co
         }
         r = hgs_render_pipeline(ctx, &cams[v], times[v], o->bg, &ro, 1);
         if (r != HGS_OK) return r;
+        r = zero_backward(ctx);
+        if (r != HGS_OK) return r;
         if (!gt_on_device) CK(cudaStreamWaitEvent(ctx->stream, ctx->gt_ready[b], 0));
         r = run_loss(ctx, g, gt_dtype == HGS_U8, o->ssim_lambda,
                      pipelined ? sc->pipe_sums[slot][v] : sc->view_sums[pending]);
         if (r != HGS_OK) return r;
         if (!gt_on_device) CK(cudaEventRecord(ctx->gt_free[b], ctx->stream));
         ++pending;
-        r = run_backward(ctx, ctx->lgrad.as<float>(), 1.0 / (double)batch_total);  // train.cpp:430-432
+        r = run_backward(ctx, ctx->lgrad.as<float>(), 1.0 / (double)batch_total, true);  // train.cpp:430-432
         if (r != HGS_OK) return r;
         if (!pipelined && pending == kMaxStepViews && v + 1 < n_views) {
             r = flush();
@@ -757,8 +776,7 @@ hgs_status train_step_impl(hgs_ctx* ctx, int n_views, const hgs_camera* cams, co
     }
     const int gate = pending;
     const uint64_t step_before = ctx->step;
-    if (apply_adam) {
-        CK(cudaMemsetAsync(&sc->skipped, 0, sizeof(unsigned long long) + 8, ctx->stream));
+    if (apply_adam) {  // (the skipped counter was zeroed before the views)
         r = run_adam(ctx, &o->lrs, o->mean_lr_scale, pipelined ? &sc->pipe_sums[slot][0][0] : &sc->view_sums[0][0],
                      gate, pipelined ? &sc->abort : nullptr);
         if (r != HGS_OK) return r;
