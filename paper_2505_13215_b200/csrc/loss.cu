@@ -92,6 +92,7 @@ constexpr int kSpan = kB + kWin - 1;  // inputs per blocked output group (14)
 template <typename Gt>
 __global__ void __launch_bounds__(256) ssim_fwd_kernel(const float* __restrict__ a, const Gt b, int W, int H,
                                                        float* __restrict__ maps, double* __restrict__ ssim_sum) {
+    pdl_wait();  // launched with launch_pdl
     // a / b staged interleaved and the five window sums as (mu_a, mu_b),
     // (E[a^2], E[b^2]) pairs + E[ab]: each FMA pair is one FFMA2 (same
     // rounding per element as the scalar code)
@@ -331,14 +332,14 @@ void launch_loss(cudaStream_t st, const float* img, const void* gt, bool gt_u8, 
     dim3 g((vw + 31) / 32, (vh + 31) / 32, 3), gb((W + 31) / 32, (H + 31) / 32, 3);
     if (gt_u8) {
         const GtU8 b{static_cast<const uint8_t*>(gt)};
-        if (with_ssim) ssim_fwd_kernel<GtU8><<<g, 256, 0, st>>>(img, b, W, H, maps, &sums[0]);
-        if (with_ssim)  // PDL after the forward kernel (not after the memset of the sums)
+        if (with_ssim) launch_pdl(ssim_fwd_kernel<GtU8>, g, dim3(256), 0, st, img, b, W, H, maps, &sums[0]);
+        if (with_ssim)
             launch_pdl(ssim_bwd_kernel<GtU8>, gb, dim3(256), 0, st, img, b, W, H, maps, lambda, 1, grad, &sums[1]);
         else
             ssim_bwd_kernel<GtU8><<<gb, 256, 0, st>>>(img, b, W, H, maps, lambda, 0, grad, &sums[1]);
     } else {
         const GtF32 b{static_cast<const float*>(gt)};
-        if (with_ssim) ssim_fwd_kernel<GtF32><<<g, 256, 0, st>>>(img, b, W, H, maps, &sums[0]);
+        if (with_ssim) launch_pdl(ssim_fwd_kernel<GtF32>, g, dim3(256), 0, st, img, b, W, H, maps, &sums[0]);
         if (with_ssim)
             launch_pdl(ssim_bwd_kernel<GtF32>, gb, dim3(256), 0, st, img, b, W, H, maps, lambda, 1, grad, &sums[1]);
         else

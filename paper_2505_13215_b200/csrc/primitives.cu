@@ -77,6 +77,7 @@ __global__ void __launch_bounds__(kCoopThreads) scan_coop_kernel(const uint32_t*
                                                                  const uint32_t* __restrict__ n_dev,
                                                                  uint32_t* __restrict__ total,
                                                                  uint32_t* __restrict__ bsum) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // launched as a programmatic dependent (coop_launch)
     cg::grid_group grid = cg::this_grid();
     const int G = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
     if (n_dev) n = (int)*n_dev;
@@ -119,6 +120,7 @@ struct CoopSort {
 };
 
 __global__ void __launch_bounds__(kCoopThreads) radix_sort_coop_kernel(CoopSort a) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // launched as a programmatic dependent (coop_launch)
     cg::grid_group grid = cg::this_grid();
     __shared__ uint32_t h[256];
     __shared__ uint32_t cnt[kWarps][256];
@@ -236,6 +238,26 @@ constexpr int kMaxCoopGrid = 4 * 256;  // workspace bound (<= 4 blocks/SM on <= 
 
 size_t scan_workspace_bytes(int) { return (size_t)(kMaxCoopGrid + 32) * sizeof(uint32_t); }
 
+bool pdl_enabled();  // capi.cu
+
+// Cooperative launch (grid-wide barriers) that may also be scheduled while
+// its predecessor drains (programmatic dependent launch; the kernels start
+// with griddepcontrol.wait).
+cudaError_t coop_launch(const void* kernel, int grid, void** args, cudaStream_t st) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kCoopThreads);
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    return cudaLaunchKernelExC(&cfg, kernel, args);
+}
+
 void exclusive_scan_u32(const uint32_t* in, uint32_t* out, int n, uint32_t* total, uint32_t* ws, cudaStream_t st,
                         const uint32_t* n_dev) {
     if (n <= 0 && !n_dev) {
@@ -244,7 +266,7 @@ void exclusive_scan_u32(const uint32_t* in, uint32_t* out, int n, uint32_t* tota
     }
     const int G = std::min(coop_grid(scan_coop_kernel, n), kMaxCoopGrid);
     void* args[] = {(void*)&in, (void*)&out, (void*)&n, (void*)&n_dev, (void*)&total, (void*)&ws};
-    cudaLaunchCooperativeKernel((void*)scan_coop_kernel, G, kCoopThreads, args, 0, st);
+    coop_launch((const void*)scan_coop_kernel, G, args, st);
     count_launch();
 }
 
@@ -271,7 +293,7 @@ int radix_sort_pairs(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_
     a.rowsum = ws + 256 * kMaxCoopGrid;
     const int G = std::min(coop_grid(radix_sort_coop_kernel, n), kMaxCoopGrid);
     void* args[] = {(void*)&a};
-    cudaLaunchCooperativeKernel((void*)radix_sort_coop_kernel, G, kCoopThreads, args, 0, st);
+    coop_launch((const void*)radix_sort_coop_kernel, G, args, st);
     count_launch();
     return npasses & 1;
 }

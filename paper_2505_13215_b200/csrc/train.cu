@@ -150,14 +150,14 @@ hgs_status ensure_scratch(hgs_ctx* ctx) {
 // The zeroing of the backward's outputs (screen norms, per-splat
 // accumulators); the training step issues it before the loss so that the
 // kernel chain loss -> K6 -> K7 has no memset in it (programmatic launches).
-hgs_status zero_backward(hgs_ctx* ctx) {
+// V_bound: an upper bound of the render's visible count (N before the render).
+hgs_status zero_backward(hgs_ctx* ctx, int64_t V_bound) {
     cudaStream_t st = ctx->stream;
-    const int64_t V = ctx->V;
     CK(cudaMemsetAsync(ctx->sn4.p, 0, (size_t)ctx->cap4 * 4, st));
     CK(cudaMemsetAsync(ctx->sn3.p, 0, (size_t)ctx->cap3 * 4, st));
-    if (V == 0 || ctx->I == 0) return HGS_OK;
-    CK(ctx->accum.ensure((size_t)V * kAccStrideHost * 4));
-    CK(cudaMemsetAsync(ctx->accum.p, 0, (size_t)V * kAccStrideHost * 4, st));
+    if (V_bound == 0) return HGS_OK;
+    CK(ctx->accum.ensure((size_t)V_bound * kAccStrideHost * 4));
+    CK(cudaMemsetAsync(ctx->accum.p, 0, (size_t)V_bound * kAccStrideHost * 4, st));
     return HGS_OK;
 }
 
@@ -165,7 +165,7 @@ hgs_status run_backward(hgs_ctx* ctx, const float* lg, double scale, bool zeroed
     cudaStream_t st = ctx->stream;
     const int64_t V = ctx->V;
     if (!zeroed) {
-        hgs_status r = zero_backward(ctx);
+        hgs_status r = zero_backward(ctx, (ctx->V == 0 || ctx->I == 0) ? 0 : ctx->V);
         if (r != HGS_OK) return r;
     }
     if (V == 0 || ctx->I == 0) return HGS_OK;
@@ -212,7 +212,8 @@ hgs_status run_backward(hgs_ctx* ctx, const float* lg, double scale, bool zeroed
 // accumulates the loss into scratch->loss_acc (device) -- no host sync.
 // sums (device, optional): where to accumulate (ssim_sum, l1_sum); default
 // the scratch pair read by the loss API
-hgs_status run_loss(hgs_ctx* ctx, const void* gt, bool gt_u8, double lambda, double* sums = nullptr) {
+hgs_status run_loss(hgs_ctx* ctx, const void* gt, bool gt_u8, double lambda, double* sums = nullptr,
+                    bool sums_zeroed = false) {
     cudaStream_t st = ctx->stream;
     const int W = ctx->W, H = ctx->H;
     const bool with_ssim = lambda != 0.0;
@@ -223,7 +224,7 @@ hgs_status run_loss(hgs_ctx* ctx, const void* gt, bool gt_u8, double lambda, dou
     CK(ctx->lgrad.ensure(npx * 3 * 4));
     Scratch* sc = scratch(ctx);
     if (!sums) sums = &sc->ssim_sum;
-    CK(cudaMemsetAsync(sums, 0, 2 * sizeof(double), st));  // ssim_sum, l1_sum
+    if (!sums_zeroed) CK(cudaMemsetAsync(sums, 0, 2 * sizeof(double), st));  // ssim_sum, l1_sum
     const int vw = W - 10, vh = H - 10;
     prof_begin(ctx, PH_LOSS);
     if (with_ssim) CK(ctx->loss_ws.ensure((size_t)vw * vh * 9 * 4));
@@ -753,13 +754,17 @@ hgs_status train_step_impl(hgs_ctx* ctx, int n_views, const hgs_camera* cams, co
         } else {
             g = gt[v];
         }
+        // the zeroing of this view's loss sums and backward outputs goes
+        // ahead of its render, so render -> loss -> backward is one chain of
+        // adjacent kernels (programmatic launches)
+        double* vsums = pipelined ? sc->pipe_sums[slot][v] : sc->view_sums[pending];
+        CK(cudaMemsetAsync(vsums, 0, 2 * sizeof(double), ctx->stream));
+        r = zero_backward(ctx, ctx->n4 + ctx->n3);
+        if (r != HGS_OK) return r;
         r = hgs_render_pipeline(ctx, &cams[v], times[v], o->bg, &ro, 1);
         if (r != HGS_OK) return r;
-        r = zero_backward(ctx);
-        if (r != HGS_OK) return r;
         if (!gt_on_device) CK(cudaStreamWaitEvent(ctx->stream, ctx->gt_ready[b], 0));
-        r = run_loss(ctx, g, gt_dtype == HGS_U8, o->ssim_lambda,
-                     pipelined ? sc->pipe_sums[slot][v] : sc->view_sums[pending]);
+        r = run_loss(ctx, g, gt_dtype == HGS_U8, o->ssim_lambda, vsums, true);
         if (r != HGS_OK) return r;
         if (!gt_on_device) CK(cudaEventRecord(ctx->gt_free[b], ctx->stream));
         ++pending;
