@@ -176,6 +176,17 @@ DevCamera to_dev(const hgs_camera* c) {
     return d;
 }
 
+__global__ void __launch_bounds__(256) zero_jobs_kernel(ZeroJobs J) {
+    pdl_wait();  // launched with launch_pdl
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (int k = 0; k < J.n; ++k) {
+        uint32_t* p = static_cast<uint32_t*>(J.j[k].p);
+        const uint64_t n = J.j[k].words;
+        const uint32_t v = J.j[k].value;
+        for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) p[i] = v;
+    }
+}
+
 __global__ void visflag_kernel(const uint32_t* __restrict__ ntiles, int n, uint32_t* __restrict__ flag) {
     pdl_wait();  // launched with launch_pdl
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -261,7 +272,8 @@ void prof_collect(hgs_ctx* ctx) {
 // ====================================================================== render
 // The full K1 -> sort -> K2 -> sort -> K4 pipeline; leaves the tape in ctx.
 hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, const double bg[3],
-                               const hgs_raster_opts* opts, int deferred, uint32_t icap, void* counters_slot) {
+                               const hgs_raster_opts* opts, int deferred, uint32_t icap, void* counters_slot,
+                               const ZeroJobs* extra) {
     std::string why;
     if (!camera_valid(cam, why)) return fail(ctx, HGS_ERR_INVALID_ARGUMENT, why);
     const double cutoff = opts ? opts->weight_cutoff : 0.05;
@@ -287,7 +299,9 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
     CK(ctx->pinned_ctr.ensure(sizeof(Counters) + 64));
     Counters* dc = counters_slot ? static_cast<Counters*>(counters_slot) : ctx->counters.as<Counters>();
     Counters* hc = static_cast<Counters*>(ctx->pinned_ctr.p);
-    CK(cudaMemsetAsync(dc, 0, sizeof(Counters), st));
+    ZeroJobs zj;
+    if (extra) zj = *extra;
+    zj.add(dc, sizeof(Counters));
     // capacity mode (icap > 0): no host round trip -- the duplication runs on
     // buffers for icap instances and flags FLAG_CAPACITY if that was too few
     // (the caller re-renders); only the production (culled) path supports it
@@ -299,7 +313,18 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
     if (want_trans) CK(ctx->trans.ensure(npx * sizeof(float)));
     if (want_count) CK(ctx->count.ensure(npx * sizeof(uint32_t)));
     CK(ctx->ranges.ensure((size_t)n_tiles * sizeof(uint2)));
-    CK(cudaMemsetAsync(ctx->ranges.p, 0, (size_t)n_tiles * sizeof(uint2), st));
+    zj.add(ctx->ranges.p, (size_t)n_tiles * sizeof(uint2));
+    if (N > 0) {
+        CK(ctx->sorted_of_gid.ensure((size_t)N * 4));
+        zj.add(ctx->sorted_of_gid.p, (size_t)N * 4, 0xffffffffu);  // gather writes the visible ones
+    }
+    {
+        uint64_t words = 0;
+        for (int k = 0; k < zj.n; ++k) words += zj.j[k].words;
+        const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((words + 255) / 256, ctx->sms * 8));
+        CK(launch_pdl(zero_jobs_kernel, dim3(blocks), dim3(256), 0, st, zj));
+        count_launch();
+    }
 
     int64_t V = 0, I = 0;
     if (N > 0) {
@@ -310,14 +335,12 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
         CK(ctx->vispos.ensure((size_t)N * 4));
         CK(ctx->shdir.ensure((size_t)N * sizeof(ShRec)));
         CK(ctx->scan_ws.ensure(scan_workspace_bytes(N) + 4096));
-        CK(ctx->sorted_of_gid.ensure((size_t)N * 4));
-        // zeroed here, ahead of the kernel chain (gather writes it)
-        CK(cudaMemsetAsync(ctx->sorted_of_gid.p, 0xff, (size_t)N * 4, st));
         prof_begin(ctx, PH_PREPROCESS);
-        preprocess_kernel<<<div_up(N, 256), 256, 0, st>>>(
-            ctx->p4.as<float>(), ctx->cap4, n4, ctx->p3.as<float>(), ctx->cap3, n3, ctx->deg, ctx->cam, t, cutoff,
-            tiles_x, ctx->rec.as<SplatRec>(), ctx->depth_key.as<uint32_t>(), ctx->ntiles.as<uint32_t>(), dc->stats,
-            &dc->flags, ctx->shdir.as<ShRec>());
+        CK(launch_pdl(preprocess_kernel, dim3(div_up(N, 256)), dim3(256), 0, st,
+                      static_cast<const float*>(ctx->p4.as<float>()), ctx->cap4, n4,
+                      static_cast<const float*>(ctx->p3.as<float>()), ctx->cap3, n3, ctx->deg, ctx->cam, t, cutoff,
+                      tiles_x, ctx->rec.as<SplatRec>(), ctx->depth_key.as<uint32_t>(), ctx->ntiles.as<uint32_t>(),
+                      dc->stats, &dc->flags, ctx->shdir.as<ShRec>()));
         count_launch();
         CKL();
         CK(launch_pdl(visflag_kernel, dim3(div_up(N, 256)), dim3(256), 0, st, ctx->ntiles.as<uint32_t>(), N,

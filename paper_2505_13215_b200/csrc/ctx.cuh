@@ -57,6 +57,22 @@ struct HostPinned {
     }
 };
 
+// Buffers a render (and the training step around it) zeroes / fills before
+// its kernels: one programmatic launch instead of a chain of memsets.
+struct ZeroJob {
+    void* p;
+    uint64_t words;  // 32-bit words
+    uint32_t value;
+};
+constexpr int kMaxZeroJobs = 8;
+struct ZeroJobs {
+    ZeroJob j[kMaxZeroJobs];
+    int n = 0;
+    void add(void* p, uint64_t bytes, uint32_t value = 0u) {
+        if (bytes) j[n++] = ZeroJob{p, bytes / 4, value};
+    }
+};
+
 // Per-render device counters (RenderStats, flags, totals).
 struct Counters {
     unsigned long long stats[kNumStats];

@@ -240,6 +240,7 @@ __global__ void __launch_bounds__(256, 3) preprocess_kernel(
     int n3, int deg, DevCamera cam, double t, double cutoff, int tiles_x, SplatRec* __restrict__ rec,
     uint32_t* __restrict__ depth_key, uint32_t* __restrict__ ntiles_out,
     unsigned long long* __restrict__ stats, uint32_t* __restrict__ flags, ShRec* __restrict__ shrec) {
+    pdl_wait();  // launched with launch_pdl
     const int gid = blockIdx.x * blockDim.x + threadIdx.x;
     const int n = n4 + n3;
     uint32_t reason = CULL_DEPTH + 100;  // sentinel: inactive lane

@@ -758,10 +758,16 @@ hgs_status train_step_impl(hgs_ctx* ctx, int n_views, const hgs_camera* cams, co
         // ahead of its render, so render -> loss -> backward is one chain of
         // adjacent kernels (programmatic launches)
         double* vsums = pipelined ? sc->pipe_sums[slot][v] : sc->view_sums[pending];
-        CK(cudaMemsetAsync(vsums, 0, 2 * sizeof(double), ctx->stream));
-        r = zero_backward(ctx, ctx->n4 + ctx->n3);
-        if (r != HGS_OK) return r;
-        r = hgs_render_pipeline(ctx, &cams[v], times[v], o->bg, &ro, 1);
+        ZeroJobs zj;  // filled by the render's own fill launch
+        zj.add(vsums, 2 * sizeof(double));
+        zj.add(ctx->sn4.p, (size_t)ctx->cap4 * 4);
+        zj.add(ctx->sn3.p, (size_t)ctx->cap3 * 4);
+        {
+            const int64_t Nv = ctx->n4 + ctx->n3;  // bound of the visible count
+            CK(ctx->accum.ensure((size_t)std::max<int64_t>(Nv, 1) * kAccStrideHost * 4));
+            zj.add(ctx->accum.p, (size_t)Nv * kAccStrideHost * 4);
+        }
+        r = hgs_render_pipeline(ctx, &cams[v], times[v], o->bg, &ro, 1, 0, nullptr, &zj);
         if (r != HGS_OK) return r;
         if (!gt_on_device) CK(cudaStreamWaitEvent(ctx->stream, ctx->gt_ready[b], 0));
         r = run_loss(ctx, g, gt_dtype == HGS_U8, o->ssim_lambda, vsums, true);

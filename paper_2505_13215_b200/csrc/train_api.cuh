@@ -6,9 +6,10 @@
 // hgs_render_finish (the training step does it once at its end)
 // icap > 0: capacity mode (no host round trip, see capi.cu); counters_slot:
 // a device Counters record to use instead of the context's
+// extra: buffers to fill in the render's own fill launch (training step)
 hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, const double bg[3],
                                const hgs_raster_opts* opts, int deferred = 0, uint32_t icap = 0,
-                               void* counters_slot = nullptr);
+                               void* counters_slot = nullptr, const hgs::ZeroJobs* extra = nullptr);
 hgs_status hgs_render_finish(hgs_ctx* ctx);
 hgs_status hgs_upload_rows(hgs_ctx* ctx, const hgs_host_scene* s, int dtype, float* dst4, float* dst3);
 hgs_status hgs_layout_state(hgs_ctx* ctx);
