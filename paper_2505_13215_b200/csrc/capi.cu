@@ -420,10 +420,11 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
             CK(ctx->dup_status.ensure((size_t)dup_blocks * 8 + 64));
             unsigned long long* status = ctx->dup_status.as<unsigned long long>();
             uint32_t* counter = reinterpret_cast<uint32_t*>(status + dup_blocks);
-            CK(cudaMemsetAsync(status, 0, (size_t)dup_blocks * 8 + 4, st));
-            dup_bounds_kernel<<<div_up((uint32_t)V, 256), 256, 0, st>>>(
-                ctx->inst_off.as<uint32_t>(), ctx->ntiles_sorted.as<uint32_t>(), (int)V, ctx->dup_first.as<uint32_t>(),
-                icap ? &dc->V : nullptr, dup_blocks);
+            CK(launch_pdl(dup_bounds_kernel, dim3(div_up((uint32_t)V, 256)), dim3(256), 0, st,
+                          static_cast<const uint32_t*>(ctx->inst_off.as<uint32_t>()),
+                          static_cast<const uint32_t*>(ctx->ntiles_sorted.as<uint32_t>()), (int)V,
+                          ctx->dup_first.as<uint32_t>(), static_cast<const uint32_t*>(icap ? &dc->V : nullptr),
+                          dup_blocks, reinterpret_cast<uint32_t*>(status), dup_blocks * 2 + 1));
             count_launch();
             CK(launch_pdl(duplicate_compact_kernel, dim3(dup_blocks), dim3(256), 0, st, ctx->fast_sorted.as<SplatFast>(),
                           (int)V, ctx->inst_off.as<uint32_t>(), tiles_x, ctx->pcut.as<CullRec>(),
@@ -459,7 +460,7 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
         }
         dup_bounds_kernel<<<div_up((uint32_t)V, 256), 256, 0, st>>>(
             ctx->inst_off.as<uint32_t>(), ctx->ntiles_sorted.as<uint32_t>(), (int)V, ctx->dup_first.as<uint32_t>(),
-            nullptr, dup_blocks);
+            nullptr, dup_blocks, nullptr, 0u);
         count_launch();
         duplicate_kernel<<<dup_blocks, 256, 0, st>>>(
             ctx->fast_sorted.as<SplatFast>(), ctx->rec_sorted.as<SplatRec>(), (int)V, ctx->inst_off.as<uint32_t>(),

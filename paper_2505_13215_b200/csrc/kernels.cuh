@@ -31,7 +31,8 @@ __global__ void duplicate_compact_kernel(const SplatFast* __restrict__ fast, int
                                          unsigned long long* status, uint32_t* __restrict__ counter,
                                          const uint32_t* V_dev, const uint32_t* I_dev, uint32_t* flags);
 __global__ void dup_bounds_kernel(const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ ntiles_sorted,
-                                  int V, uint32_t* __restrict__ cta_first, const uint32_t* V_dev, uint32_t nblocks);
+                                  int V, uint32_t* __restrict__ cta_first, const uint32_t* V_dev, uint32_t nblocks,
+                                  uint32_t* __restrict__ zero_words, uint32_t n_zero);
 __global__ void compact_instances_kernel(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals, int n,
                                          const uint32_t* __restrict__ pos, uint32_t* __restrict__ keys_out,
                                          uint32_t* __restrict__ vals_out);

@@ -210,7 +210,12 @@ __device__ __forceinline__ int last_le(const uint32_t* __restrict__ off, int lo,
 __global__ void __launch_bounds__(256) dup_bounds_kernel(const uint32_t* __restrict__ offsets,
                                                          const uint32_t* __restrict__ ntiles_sorted, int V,
                                                          uint32_t* __restrict__ cta_first, const uint32_t* V_dev,
-                                                         uint32_t nblocks) {
+                                                         uint32_t nblocks, uint32_t* __restrict__ zero_words,
+                                                         uint32_t n_zero) {
+    pdl_wait();  // launched with launch_pdl
+    // the look-back status words (+ tile counter) of duplicate_compact_kernel
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_zero; i += gridDim.x * blockDim.x)
+        zero_words[i] = 0u;
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= (V_dev ? (int)*V_dev : V)) return;
     const uint32_t o = offsets[j], n = ntiles_sorted[j];
