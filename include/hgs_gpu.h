@@ -168,6 +168,13 @@ hgs_status hgs_forward_train(hgs_ctx *ctx, const hgs_camera *cam, double t, cons
  * updates the densification statistics (train.cpp:433-444) with the raw
  * per-image screen-space norms. */
 hgs_status hgs_backward(hgs_ctx *ctx, const void *loss_grad, int dtype, int on_device, double scale);
+/* Exact backward mode (default off): every pixel's pair terms in FP64 with
+ * FP64 colours, the reference's own arithmetic (backward.cpp:178-356), at
+ * several times the cost of the default path -- whose FP32 pair terms
+ * (FP64 accumulation) meet the 1e-3 per-element gate at the training
+ * configurations but not for adversarial, strongly cancelling loss
+ * gradients. */
+hgs_status hgs_set_exact_backward(hgs_ctx *ctx, int enable);
 hgs_status hgs_zero_grads(hgs_ctx *ctx);
 /* Download gradients in the scene layout (double or float), plus the
  * screen_norm of the LAST backward call (backward.hpp:20, 30). */

@@ -371,6 +371,11 @@ class Context:
         g = g.astype(np.float64 if code == HGS_F64 else np.float32, copy=False)
         self._check(self._lib.hgs_backward(self._h, ptr(g), code, 0, float(scale)))
 
+    def set_exact_backward(self, enable: bool = True) -> None:
+        """FP64 pair terms for every pixel in backward() / training (the
+        reference's arithmetic; several times slower than the default)."""
+        self._check(self._lib.hgs_set_exact_backward(self._h, 1 if enable else 0))
+
     def zero_grads(self) -> None:
         self._check(self._lib.hgs_zero_grads(self._h))
 

@@ -641,6 +641,8 @@ hgs_status hgs_ctx_create(int device, hgs_ctx** out) {
     if (cudaSetDevice(device) != cudaSuccess) return HGS_ERR_CUDA;
     hgs_ctx* ctx = new hgs_ctx();
     ctx->device = device;
+    if (const char* dbg = getenv("HGS_DEBUG_EXACT")) set_debug_exact(atoi(dbg));  // diagnostics only
+    if (const char* dbg = getenv("HGS_DEBUG_TERR")) set_debug_terr((float)atof(dbg));
     cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device);
     if (cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking) != cudaSuccess) {
         delete ctx;
@@ -662,7 +664,7 @@ void hgs_ctx_destroy(hgs_ctx* ctx) {
                     &ctx->sort_v2, &ctx->rec_sorted, &ctx->fast_sorted, &ctx->ntiles_sorted, &ctx->inst_off,
                     &ctx->inst_k, &ctx->inst_v, &ctx->inst_k2, &ctx->inst_v2, &ctx->ranges, &ctx->sorted_of_gid, &ctx->inst_flag, &ctx->inst_pos, &ctx->dbg_k, &ctx->dbg_v, &ctx->scan_ws,
                     &ctx->sort_ws, &ctx->counters, &ctx->img, &ctx->last, &ctx->tfinal, &ctx->trans, &ctx->count,
-                    &ctx->fix_list, &ctx->accum, &ctx->lgrad, &ctx->gt_stage, &ctx->loss_ws, &ctx->stage, &ctx->adam_ok, &ctx->pcut, &ctx->dup_first, &ctx->shdir, &ctx->ddir, &ctx->dup_status, &ctx->gpack, &ctx->dens_cat, &ctx->dens_u32, &ctx->dens_misc, &ctx->dens_kinds, &ctx->dens_jit, &ctx->dmap, &ctx->ckpt, &ctx->crc_tab, &ctx->comm_buf, &ctx->sweep_ctr};
+                    &ctx->fix_list, &ctx->accum, &ctx->exact_col, &ctx->lgrad, &ctx->gt_stage, &ctx->loss_ws, &ctx->stage, &ctx->adam_ok, &ctx->pcut, &ctx->dup_first, &ctx->shdir, &ctx->ddir, &ctx->dup_status, &ctx->gpack, &ctx->dens_cat, &ctx->dens_u32, &ctx->dens_misc, &ctx->dens_kinds, &ctx->dens_jit, &ctx->dmap, &ctx->ckpt, &ctx->crc_tab, &ctx->comm_buf, &ctx->sweep_ctr};
     for (DBuf* b : bufs) b->release();
     ctx->pinned.release();
     ctx->pinned_ctr.release();
@@ -972,6 +974,12 @@ hgs_status hgs_rasterize(hgs_ctx* ctx, const hgs_host_scene* scene, int dtype, c
 }
 
 const float* hgs_last_image_device(hgs_ctx* ctx) { return ctx ? ctx->img.as<float>() : nullptr; }
+
+hgs_status hgs_set_exact_backward(hgs_ctx* ctx, int enable) {
+    if (!ctx) return HGS_ERR_INVALID_ARGUMENT;
+    ctx->exact_backward = enable != 0;
+    return HGS_OK;
+}
 
 hgs_status hgs_render_info_get(hgs_ctx* ctx, hgs_render_info* info) {
     if (!ctx || !info) return HGS_ERR_INVALID_ARGUMENT;

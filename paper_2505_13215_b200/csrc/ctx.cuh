@@ -149,6 +149,8 @@ struct hgs_ctx {
     hgs::DBuf counters;  // [0..5] stats u64, [6] flags, fix_count, totals...
     hgs::DBuf img, last, tfinal, trans, count, fix_list;
     hgs::DBuf accum;     // backward per-sorted-splat accumulators
+    bool exact_backward = false;  // hgs_set_exact_backward: FP64 pair terms for every pixel
+    hgs::DBuf exact_col;          // its FP64 colours (sorted order)
     hgs::DBuf lgrad;     // dL/dimage (device float)
     hgs::DBuf gt_stage;  // staged ground truth
     hgs::DBuf gt_buf[2], gt_stage64[2];  // double-buffered host GT of the training step

@@ -66,6 +66,12 @@ static_assert(sizeof(SplatRec) == 80, "SplatRec layout");
 
 // Per-sorted-splat accumulators of the compositing backward (backward.cpp:79-85)
 constexpr int kAccum = 9;  // d_rgb[3], d_alpha, d_screen[2], d_conic00, d_conic01, d_conic11
+// Their type (K6 -> K7): FP64.  The running sum over a splat's warps --
+// up to hundreds of partial sums that cancel for the position and shape
+// sums -- is what limits an FP32 accumulator (measured: the source of the
+// gradient elements above the 1e-3 gate at configs[1]).
+typedef double acc_t;
+constexpr int kAccStrideHost = 10;  // acc_t elements per splat (9 used, 16-byte aligned)
 
 // Status flags raised by kernels (mapped to C-ABI errors on the host)
 enum : uint32_t {

@@ -39,6 +39,8 @@ __global__ void compact_instances_kernel(const uint32_t* __restrict__ keys, cons
 __global__ void tile_ranges_kernel(const uint32_t* __restrict__ keys, int n, uint2* __restrict__ ranges);
 __global__ void tile_ranges_dev_kernel(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ n_dev,
                                        uint2* __restrict__ ranges);
+void set_debug_exact(int v);  // raster_fwd.cu (HGS_DEBUG_EXACT diagnostics)
+void set_debug_terr(float v);
 void launch_raster_fwd(bool count_map, int n_tiles, cudaStream_t st, const uint2* ranges, const uint32_t* inst_val,
                        const SplatFast* fast, const SplatRec* exact, int W, int H, int tiles_x, float bg_r, float bg_g,
                        float bg_b, float* out_rgb, uint32_t* out_last, float* out_tfinal, float* out_trans,
@@ -54,7 +56,7 @@ __global__ void grads_pack_kernel(const float* __restrict__ gbuf, int64_t off_g3
                                   int rows3, int64_t cap4, int64_t cap3, int n4, int n3, float* __restrict__ packed,
                                   int unpack);
 // K7b: SH colour backward (runs before K7)
-__global__ void sh_bwd_kernel(int N, const uint32_t* __restrict__ sorted_of_gid, const float* __restrict__ accum,
+__global__ void sh_bwd_kernel(int N, const uint32_t* __restrict__ sorted_of_gid, const acc_t* __restrict__ accum,
                               int acc_stride, int n4, const float* __restrict__ p4, int64_t cap4,
                               const float* __restrict__ p3, int64_t cap3, int deg, float scale,
                               float* __restrict__ g4, float* __restrict__ g3, const ShRec* __restrict__ shrec,
@@ -65,19 +67,30 @@ __global__ void sh_bwd_kernel(int N, const uint32_t* __restrict__ sorted_of_gid,
 namespace hgs {
 
 // raster_bwd.cu (K6)
-constexpr int kAccStrideHost = 12;
+
 __global__ void raster_bwd_kernel(const uint2* __restrict__ ranges, const uint32_t* __restrict__ inst_val,
                                   const SplatFast* __restrict__ fast, const SplatRec* __restrict__ exact, int W, int H,
                                   int tiles_x, const float* __restrict__ tfinal, const uint32_t* __restrict__ last_arr,
                                   const float* __restrict__ dL_dimg, float bg_r, float bg_g, float bg_b,
-                                  float* __restrict__ accum);
+                                  acc_t* __restrict__ accum);
 __global__ void raster_bwd_exact_kernel(const uint32_t* __restrict__ fix_list, const uint32_t* __restrict__ fix_count,
-                                        const uint2* __restrict__ ranges, const uint32_t* __restrict__ inst_val,
-                                        const SplatRec* __restrict__ exact, int W, int tiles_x, double bg_r,
-                                        double bg_g, double bg_b, const uint32_t* __restrict__ last_arr,
-                                        const float* __restrict__ dL_dimg, float* __restrict__ accum);
+                                        int all_pixels, const uint2* __restrict__ ranges,
+                                        const uint32_t* __restrict__ inst_val, const SplatRec* __restrict__ exact,
+                                        int W, int tiles_x, double bg_r, double bg_g, double bg_b,
+                                        const uint32_t* __restrict__ last_arr, const float* __restrict__ dL_dimg,
+                                        const double* __restrict__ col64, acc_t* __restrict__ accum);
+__global__ void exact_colour_kernel(const uint32_t* __restrict__ sorted_gid, int V, int n4,
+                                    const float* __restrict__ p4, int64_t cap4, const float* __restrict__ p3,
+                                    int64_t cap3, int deg, DevCamera cam, double t, double* __restrict__ col64);
 // gaussian_bwd.cu (K7)
-__global__ void gaussian_bwd_kernel(int N, const uint32_t* __restrict__ sorted_of_gid, const float* __restrict__ accum,
+__global__ void gaussian_bwd_kernel(int N, const uint32_t* __restrict__ sorted_of_gid, const acc_t* __restrict__ accum,
+                                    int acc_stride, int n4, const float* __restrict__ p4, int64_t cap4,
+                                    const float* __restrict__ p3, int64_t cap3, int deg, DevCamera cam, double t,
+                                    double scale, float* __restrict__ g4, float* __restrict__ g3,
+                                    float* __restrict__ sn4, float* __restrict__ sn3, float* __restrict__ gn4,
+                                    float* __restrict__ gn3, float* __restrict__ cnt4, float* __restrict__ cnt3,
+                                    const double* __restrict__ conic_src, int conic_stride, const float4* __restrict__ ddir, int first);
+__global__ void gaussian_bwd_exact_kernel(int N, const uint32_t* __restrict__ sorted_of_gid, const acc_t* __restrict__ accum,
                                     int acc_stride, int n4, const float* __restrict__ p4, int64_t cap4,
                                     const float* __restrict__ p3, int64_t cap3, int deg, DevCamera cam, double t,
                                     double scale, float* __restrict__ g4, float* __restrict__ g3,
@@ -136,7 +149,7 @@ __global__ void grads_pack_kernel(const float* __restrict__ gbuf, int64_t off_g3
                                   int rows3, int64_t cap4, int64_t cap3, int n4, int n3, float* __restrict__ packed,
                                   int unpack);
 // K7b: SH colour backward (runs before K7)
-__global__ void sh_bwd_kernel(int N, const uint32_t* __restrict__ sorted_of_gid, const float* __restrict__ accum,
+__global__ void sh_bwd_kernel(int N, const uint32_t* __restrict__ sorted_of_gid, const acc_t* __restrict__ accum,
                               int acc_stride, int n4, const float* __restrict__ p4, int64_t cap4,
                               const float* __restrict__ p3, int64_t cap3, int deg, float scale,
                               float* __restrict__ g4, float* __restrict__ g3, const ShRec* __restrict__ shrec,

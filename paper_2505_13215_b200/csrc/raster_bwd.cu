@@ -19,7 +19,9 @@
 // raster_bwd_exact_kernel (one warp per pixel, FP64).
 #include <cstddef>
 
+#include "gauss_math.cuh"
 #include "kernels.cuh"
+#include "sh.cuh"
 
 namespace hgs {
 
@@ -66,22 +68,26 @@ __device__ __forceinline__ float warp_sum(float v) {
 
 }  // namespace
 
-// accum layout: 12 floats per sorted splat (16-byte aligned), with
+// accum layout: kAccStrideHost doubles per sorted splat (16-byte aligned), with
 // h = g * dL/da (g = exp(-power), a = alpha * g) and d = pixel - mean:
 //   [0..2] sum w * dL/dC (d_rgb), [3] sum h (= d_alpha), [4] sum h dx,
-//   [5] sum h dy, [6] sum h dx^2, [7] sum h dx dy, [8] sum h dy^2, [9..11] pad
+//   [5] sum h dy, [6] sum h dx^2, [7] sum h dx dy, [8] sum h dy^2, [9] pad
+// Each warp reduces its pixels in FP32 (at most 64 terms) and adds the warp
+// total to the FP64 accumulator (hgs_common.cuh: the FP32 running sum over
+// the splat's warps was the dominant gradient error at configs[1]).
 // K7 turns [4..8] into d_screen = alpha * conic . ([4],[5]) and
 // d_conic = -alpha/2 * ([6] [7]; [7] [8]) (backward.cpp:212-221).
-constexpr int kAccStride = 12;
+constexpr int kAccStride = kAccStrideHost;
 #ifndef HGS_DIRECT_LANES
 #define HGS_DIRECT_LANES 8
 #endif
 constexpr int kDirectLanes = HGS_DIRECT_LANES;  // contributing lanes up to which atomics replace the reduction
 constexpr int kThreadsB = 128;  // two pixels per thread
 
-__device__ __forceinline__ void red_add(float* addr, float v) {
-    asm volatile("red.global.add.f32 [%0], %1;" ::"l"(addr), "f"(v) : "memory");
+__device__ __forceinline__ void red_add(acc_t* addr, float v) {
+    asm volatile("red.global.add.f64 [%0], %1;" ::"l"(addr), "d"((double)v) : "memory");
 }
+
 
 __device__ __forceinline__ float rcp_approx(float x) {
     float y;
@@ -129,7 +135,7 @@ __global__ void __launch_bounds__(kThreadsB, 7) raster_bwd_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ inst_val, const SplatFast* __restrict__ fast,
     const SplatRec* __restrict__ exact, int W, int H, int tiles_x, const float* __restrict__ tfinal,
     const uint32_t* __restrict__ last_arr, const float* __restrict__ dL_dimg, float bg_r, float bg_g, float bg_b,
-    float* __restrict__ accum) {
+    acc_t* __restrict__ accum) {
     pdl_wait();  // launched with launch_pdl
     __shared__ SplatBatch<kBatchB> sb;
     __shared__ uint32_t s_maxlast;
@@ -264,7 +270,7 @@ __global__ void __launch_bounds__(kThreadsB, 7) raster_bwd_kernel(
             v[6] = fmaf(hx0, dx0, hx1 * dx1);
             v[7] = fmaf(hx0, dy0, hx1 * dy1);
             v[8] = fmaf(hy0, dy0, hy1 * dy1);
-            float* dst = accum + (size_t)sj * kAccStride;
+            acc_t* dst = accum + (size_t)sj * kAccStride;
             const unsigned am = __ballot_sync(0xffffffffu, p0 || p1);
             if (__popc(am) <= kDirectLanes) {
                 // few contributing lanes: their own atomics are cheaper than the butterfly
@@ -288,17 +294,18 @@ __global__ void __launch_bounds__(kThreadsB, 7) raster_bwd_kernel(
 // d_a = g.(c T_i - (C_out - P_i)/(1 - a)) (in FP64 the subtraction is exact
 // enough) via global atomics, in the accumulator layout of raster_bwd_kernel.
 __global__ void __launch_bounds__(128) raster_bwd_exact_kernel(
-    const uint32_t* __restrict__ fix_list, const uint32_t* __restrict__ fix_count, const uint2* __restrict__ ranges,
-    const uint32_t* __restrict__ inst_val, const SplatRec* __restrict__ exact, int W, int tiles_x, double bg_r,
-    double bg_g, double bg_b, const uint32_t* __restrict__ last_arr, const float* __restrict__ dL_dimg,
-    float* __restrict__ accum) {
+    const uint32_t* __restrict__ fix_list, const uint32_t* __restrict__ fix_count, int all_pixels,
+    const uint2* __restrict__ ranges, const uint32_t* __restrict__ inst_val, const SplatRec* __restrict__ exact, int W,
+    int tiles_x, double bg_r, double bg_g, double bg_b, const uint32_t* __restrict__ last_arr,
+    const float* __restrict__ dL_dimg, const double* __restrict__ col64, acc_t* __restrict__ accum) {
     pdl_wait();  // launched with launch_pdl
     __shared__ double s_om[4][32 * kExactSub];
-    const uint32_t n = *fix_count;
+    // the forward's fix-up pixels, or (exact backward mode) every pixel
+    const uint32_t n = fix_list ? *fix_count : (uint32_t)all_pixels;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const uint32_t warps = gridDim.x * (blockDim.x >> 5);
     for (uint32_t q = blockIdx.x * (blockDim.x >> 5) + wib; q < n; q += warps) {
-        const int pix = (int)fix_list[q];
+        const int pix = fix_list ? (int)fix_list[q] : (int)q;
         const double gp[3] = {dL_dimg[pix * 3], dL_dimg[pix * 3 + 1], dL_dimg[pix * 3 + 2]};
         if (gp[0] == 0.0 && gp[1] == 0.0 && gp[2] == 0.0) continue;
         const int px = pix % W, py = pix / W;
@@ -314,12 +321,22 @@ __global__ void __launch_bounds__(128) raster_bwd_exact_kernel(
                 exact_chunk<S>(inst_val, exact, base, last, px, py, pcx, pcy, T, s_om[wib], c);
 #pragma unroll
                 for (int s = 0; s < S; ++s) {
-                    double wc[3] = {0.0, 0.0, 0.0}, w = 0.0;
+                    double wc[3] = {0.0, 0.0, 0.0}, w = 0.0, rgb[3] = {0.0, 0.0, 0.0};
                     if (c.contrib[s]) {
+                        if (col64) {  // exact mode: the FP64 colours
+                            const double* cc = col64 + 3 * (size_t)(c.e[s] - exact);
+                            rgb[0] = cc[0];
+                            rgb[1] = cc[1];
+                            rgb[2] = cc[2];
+                        } else {
+                            rgb[0] = c.e[s]->r;
+                            rgb[1] = c.e[s]->g;
+                            rgb[2] = c.e[s]->b;
+                        }
                         w = __dmul_rn(c.a[s], c.Ti[s]);
-                        wc[0] = c.e[s]->r * w;
-                        wc[1] = c.e[s]->g * w;
-                        wc[2] = c.e[s]->b * w;
+                        wc[0] = rgb[0] * w;
+                        wc[1] = rgb[1] * w;
+                        wc[2] = rgb[2] * w;
                     }
                     if (pass == 0) {
                         for (int k = 0; k < 3; ++k) P[k] += warp_sum_d(wc[k]);
@@ -335,20 +352,19 @@ __global__ void __launch_bounds__(128) raster_bwd_exact_kernel(
                         }
                     if (c.contrib[s]) {
                         const SplatRec* e = c.e[s];
-                        const double rgb[3] = {e->r, e->g, e->b};
                         double d_a = 0.0;
                         for (int k = 0; k < 3; ++k)
                             d_a += gp[k] * (rgb[k] * c.Ti[s] - (Cout[k] - (P[k] + inc[k])) / (1.0 - c.a[s]));
-                        float* dst = accum + (size_t)(e - exact) * kAccStride;
-                        for (int k = 0; k < 3; ++k) atomicAdd(dst + k, (float)(w * gp[k]));
+                        acc_t* dst = accum + (size_t)(e - exact) * kAccStride;
+                        for (int k = 0; k < 3; ++k) atomicAdd(dst + k, w * gp[k]);
                         const double h = c.g[s] * d_a;
                         const double dx = pcx - e->sx, dy = pcy - e->sy;
-                        atomicAdd(dst + 3, (float)h);
-                        atomicAdd(dst + 4, (float)(h * dx));
-                        atomicAdd(dst + 5, (float)(h * dy));
-                        atomicAdd(dst + 6, (float)(h * dx * dx));
-                        atomicAdd(dst + 7, (float)(h * dx * dy));
-                        atomicAdd(dst + 8, (float)(h * dy * dy));
+                        atomicAdd(dst + 3, h);
+                        atomicAdd(dst + 4, h * dx);
+                        atomicAdd(dst + 5, h * dy);
+                        atomicAdd(dst + 6, h * dx * dx);
+                        atomicAdd(dst + 7, h * dx * dy);
+                        atomicAdd(dst + 8, h * dy * dy);
                     }
                     for (int k = 0; k < 3; ++k) P[k] += __shfl_sync(0xffffffffu, inc[k], 31);
                 }
@@ -361,6 +377,68 @@ __global__ void __launch_bounds__(128) raster_bwd_exact_kernel(
             }
         }
     }
+}
+
+// ---- exact backward mode (hgs_set_exact_backward): FP64 colours of the
+// visible splats for the FP64 pixel walk.
+// FP64 colour of a Gaussian (sh.cpp:73-83; view direction raster.cpp:83-85
+// from the conditional mean, gauss_math.cpp:175-186).
+__device__ void exact_colour(int gid, int n4, const float* __restrict__ p4, int64_t cap4,
+                             const float* __restrict__ p3, int64_t cap3, int deg, const DevCamera& cam, double t,
+                             double out[3]) {
+    double mean3[3];
+    const float* P;
+    int64_t cap;
+    int i, shrow;
+    if (gid < n4) {
+        i = gid;
+        P = p4;
+        cap = cap4;
+        shrow = R4_SH;
+        double ql[4], qr[4], es[4];
+        for (int k = 0; k < 4; ++k) {
+            ql[k] = p4[(int64_t)(R4_QL + k) * cap4 + i];
+            qr[k] = p4[(int64_t)(R4_QR + k) * cap4 + i];
+            es[k] = exp((double)p4[(int64_t)(R4_LS + k) * cap4 + i]);
+        }
+        const gm::M4 R = gm::rot4_from_pair(ql, qr);
+        double cov[4];  // column 3 of R diag(e^s)^2 R^T
+        for (int a = 0; a < 4; ++a) {
+            double s = 0.0;
+            for (int k = 0; k < 4; ++k) s += (R.a[a][k] * es[k]) * (R.a[3][k] * es[k]);
+            cov[a] = s;
+        }
+        const double dt = t - (double)p4[(int64_t)R4_MT * cap4 + i];
+        for (int k = 0; k < 3; ++k) mean3[k] = (double)p4[(int64_t)(R4_MEAN + k) * cap4 + i] + cov[k] * (dt / cov[3]);
+    } else {
+        i = gid - n4;
+        P = p3;
+        cap = cap3;
+        shrow = R3_SH;
+        for (int k = 0; k < 3; ++k) mean3[k] = p3[(int64_t)(R3_MEAN + k) * cap3 + i];
+    }
+    const double v[3] = {mean3[0] - cam.pos[0], mean3[1] - cam.pos[1], mean3[2] - cam.pos[2]};
+    const double nrm = sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+    double d[3] = {0.0, 0.0, 1.0};
+    if (nrm > 0.0)
+        for (int k = 0; k < 3; ++k) d[k] = v[k] / nrm;
+    double basis[16];
+    sh_basis_t<double>(d, deg, basis);
+    const int K = sh_count(deg);
+    for (int c = 0; c < 3; ++c) {
+        double acc = 0.0;
+        for (int k = 0; k < K; ++k) acc += (double)P[(int64_t)(shrow + 3 * k + c) * cap + i] * basis[k];
+        out[c] = fmin(fmax(acc + 0.5, 0.0), 1.0);
+    }
+}
+
+__global__ void __launch_bounds__(128) exact_colour_kernel(const uint32_t* __restrict__ sorted_gid, int V, int n4,
+                                                           const float* __restrict__ p4, int64_t cap4,
+                                                           const float* __restrict__ p3, int64_t cap3, int deg,
+                                                           DevCamera cam, double t, double* __restrict__ col64) {
+    pdl_wait();  // launched with launch_pdl
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < V) exact_colour((int)sorted_gid[j], n4, p4, cap4, p3, cap3, deg, cam, t, col64 + 3 * (size_t)j);
 }
 
 }  // namespace hgs

@@ -7,6 +7,16 @@
 
 namespace hgs {
 
+// Diagnostics only (HGS_DEBUG_EXACT, read at context creation; 0 in every
+// measured or tested configuration): bit 0 -- every splat takes the FP64
+// exponent path; bit 1 -- every pixel goes through the FP64 fix-up (forward)
+// and exact backward.
+__device__ int g_debug_exact = 0;
+__device__ float g_debug_terr = INFINITY;  // HGS_DEBUG_TERR: flag pixels whose T error bound exceeds it
+
+void set_debug_exact(int v) { cudaMemcpyToSymbol(g_debug_exact, &v, sizeof(int)); }
+void set_debug_terr(float v) { cudaMemcpyToSymbol(g_debug_terr, &v, sizeof(float)); }
+
 // After the depth sort: gather the exact record into depth order, derive the
 // FP32 fast view (Cholesky of the scaled conic + certified error bound), and
 // emit the tile count of each sorted splat.
@@ -62,6 +72,7 @@ __global__ void __launch_bounds__(256) gather_sorted_kernel(const uint32_t* __re
     }
     const double r = fp64 ? 1e30 : fabs(l01) / l11;
     if (r > 16.0) fp64 = true;  // FP32 stays certified (e1 grows with r); measured best at 16
+    if (g_debug_exact & 1) fp64 = true;
     f.l00 = (float)l00;
     f.l01 = (float)l01;
     f.l11 = (float)l11;
@@ -302,8 +313,11 @@ __global__ void __launch_bounds__(kDupThreads) duplicate_compact_kernel(
     if (i0 >= I) return;  // CTAs of the capacity beyond the instances (nothing looks back at them)
     const int i_end = min(i0 + kDupPerCta, I);
     const int j_lo = (int)cta_first[tile];
-    const int j_hi = i_end < I_all ? (int)cta_first[tile + 1] : V - 1;
-    const int cnt = j_hi - j_lo + 1;
+    // the CTA's NOMINAL end decides whether cta_first[tile + 1] exists: in an
+    // overflowing capacity-mode frame (I < I_all) i_end is clipped to the
+    // capacity, but dup_bounds_kernel wrote only the boundaries below I_all
+    const int j_hi = (tile + 1) * kDupPerCta < I_all ? (int)cta_first[tile + 1] : V - 1;
+    const int cnt = min(j_hi - j_lo + 1, kDupPerCta + 1);  // a CTA spans at most kDupPerCta + 1 splats
     for (int k = threadIdx.x; k < cnt; k += kDupThreads) s_off[k] = __ldg(&offsets[j_lo + k]);
     __syncthreads();
     constexpr int kPer = kDupPerCta / kDupThreads;  // 4 consecutive instances per thread
@@ -501,14 +515,15 @@ __device__ __forceinline__ void write_pixel(const PixFwd& s, int pix, float bg_r
                                             float* __restrict__ out_tfinal, float* __restrict__ out_trans,
                                             uint32_t* __restrict__ out_count, uint32_t* __restrict__ fix_list,
                                             uint32_t* __restrict__ fix_count) {
+    const bool flagged = s.flagged || (g_debug_exact & 2) || s.err > g_debug_terr;
     out_rgb[pix * 3 + 0] = fmaf(s.T, bg_r, s.r);
     out_rgb[pix * 3 + 1] = fmaf(s.T, bg_g, s.g);
     out_rgb[pix * 3 + 2] = fmaf(s.T, bg_b, s.b);
-    out_last[pix] = s.last | (s.flagged ? 0x80000000u : 0u);
+    out_last[pix] = s.last | (flagged ? 0x80000000u : 0u);
     out_tfinal[pix] = s.T;
     if (out_trans) out_trans[pix] = s.T;
     if (out_count) out_count[pix] = s.count;
-    if (s.flagged) fix_list[atomicAdd(fix_count, 1u)] = (uint32_t)pix;
+    if (flagged) fix_list[atomicAdd(fix_count, 1u)] = (uint32_t)pix;
 }
 
 // K4: one CTA (128 threads) per 16x16 tile, two pixels per thread, front-to-

@@ -156,8 +156,8 @@ hgs_status zero_backward(hgs_ctx* ctx, int64_t V_bound) {
     CK(cudaMemsetAsync(ctx->sn4.p, 0, (size_t)ctx->cap4 * 4, st));
     CK(cudaMemsetAsync(ctx->sn3.p, 0, (size_t)ctx->cap3 * 4, st));
     if (V_bound == 0) return HGS_OK;
-    CK(ctx->accum.ensure((size_t)V_bound * kAccStrideHost * 4));
-    CK(cudaMemsetAsync(ctx->accum.p, 0, (size_t)V_bound * kAccStrideHost * 4, st));
+    CK(ctx->accum.ensure((size_t)V_bound * kAccStrideHost * sizeof(acc_t)));
+    CK(cudaMemsetAsync(ctx->accum.p, 0, (size_t)V_bound * kAccStrideHost * sizeof(acc_t), st));
     return HGS_OK;
 }
 
@@ -172,35 +172,51 @@ hgs_status run_backward(hgs_ctx* ctx, const float* lg, double scale, bool zeroed
     const int n_tiles = ctx->tiles_x * ctx->tiles_y;
     const uint32_t* fix_count = &ctx->counters.as<Counters>()->fix_count;
     prof_begin(ctx, PH_RASTER_BWD);
-    CK(launch_pdl(raster_bwd_kernel, dim3(n_tiles), dim3(128), 0, st, ctx->ranges.as<uint2>(),
-                  static_cast<const uint32_t*>(ctx->inst_vals_final), ctx->fast_sorted.as<SplatFast>(),
-                  ctx->rec_sorted.as<SplatRec>(), ctx->W, ctx->H, ctx->tiles_x, ctx->tfinal.as<float>(),
-                  ctx->last.as<uint32_t>(), lg, (float)ctx->bg[0], (float)ctx->bg[1], (float)ctx->bg[2],
-                  ctx->accum.as<float>()));
-    count_launch();
-    CKL();
-    CK(launch_pdl(raster_bwd_exact_kernel, dim3(ctx->sms * 2), dim3(128), 0, st, ctx->fix_list.as<uint32_t>(),
-                  fix_count, ctx->ranges.as<uint2>(), ctx->inst_vals_final, ctx->rec_sorted.as<SplatRec>(), ctx->W,
-                  ctx->tiles_x, ctx->bg[0], ctx->bg[1], ctx->bg[2], ctx->last.as<uint32_t>(), lg,
-                  ctx->accum.as<float>()));
+    const bool exact = ctx->exact_backward;
+    if (exact) {
+        // exact backward mode: every pixel through the FP64 walk with FP64
+        // colours (hgs_set_exact_backward)
+        CK(ctx->exact_col.ensure((size_t)V * 3 * sizeof(double)));
+        CK(launch_pdl(exact_colour_kernel, dim3(div_up((uint32_t)V, 128)), dim3(128), 0, st, ctx->sorted_gid, (int)V,
+                      (int)ctx->n4, ctx->p4.as<float>(), ctx->cap4, ctx->p3.as<float>(), ctx->cap3, ctx->deg, ctx->cam,
+                      ctx->t, ctx->exact_col.as<double>()));
+        count_launch();
+        CKL();
+    } else {
+        CK(launch_pdl(raster_bwd_kernel, dim3(n_tiles), dim3(128), 0, st, ctx->ranges.as<uint2>(),
+                      static_cast<const uint32_t*>(ctx->inst_vals_final), ctx->fast_sorted.as<SplatFast>(),
+                      ctx->rec_sorted.as<SplatRec>(), ctx->W, ctx->H, ctx->tiles_x, ctx->tfinal.as<float>(),
+                      ctx->last.as<uint32_t>(), lg, (float)ctx->bg[0], (float)ctx->bg[1], (float)ctx->bg[2],
+                      ctx->accum.as<acc_t>()));
+        count_launch();
+        CKL();
+    }
+    CK(launch_pdl(raster_bwd_exact_kernel, dim3(ctx->sms * (exact ? 8 : 2)), dim3(128), 0, st,
+                  exact ? nullptr : ctx->fix_list.as<uint32_t>(), fix_count, ctx->W * ctx->H, ctx->ranges.as<uint2>(),
+                  ctx->inst_vals_final, ctx->rec_sorted.as<SplatRec>(), ctx->W, ctx->tiles_x, ctx->bg[0], ctx->bg[1],
+                  ctx->bg[2], ctx->last.as<uint32_t>(), lg, exact ? ctx->exact_col.as<double>() : nullptr,
+                  ctx->accum.as<acc_t>()));
     count_launch();
     CKL();
     prof_end(ctx);
     prof_begin(ctx, PH_GAUSS_BWD);
     const int N = (int)(ctx->n4 + ctx->n3);
     CK(ctx->ddir.ensure((size_t)N * sizeof(float4)));
-    CK(launch_pdl(sh_bwd_kernel, dim3(div_up((uint32_t)N, 128)), dim3(128), 0, st, N,
-                  ctx->sorted_of_gid.as<uint32_t>(), ctx->accum.as<float>(), kAccStrideHost, (int)ctx->n4,
-                  ctx->p4.as<float>(), ctx->cap4, ctx->p3.as<float>(), ctx->cap3, ctx->deg, (float)scale, ctx->g4,
-                  ctx->g3, ctx->shdir.as<ShRec>(), ctx->ddir.as<float4>(), ctx->grads_zero ? 1 : 0));
-    count_launch();
-    CKL();
-    CK(launch_pdl(gaussian_bwd_kernel, dim3(div_up((uint32_t)N, 128)), dim3(128), 0, st, N,
-                  ctx->sorted_of_gid.as<uint32_t>(), ctx->accum.as<float>(), kAccStrideHost, (int)ctx->n4,
+    const int first = ctx->grads_zero ? 1 : 0;
+    if (!exact) {
+        CK(launch_pdl(sh_bwd_kernel, dim3(div_up((uint32_t)N, 128)), dim3(128), 0, st, N,
+                      ctx->sorted_of_gid.as<uint32_t>(), ctx->accum.as<acc_t>(), kAccStrideHost, (int)ctx->n4,
+                      ctx->p4.as<float>(), ctx->cap4, ctx->p3.as<float>(), ctx->cap3, ctx->deg, (float)scale, ctx->g4,
+                      ctx->g3, ctx->shdir.as<ShRec>(), ctx->ddir.as<float4>(), first));
+        count_launch();
+        CKL();
+    }
+    CK(launch_pdl(exact ? gaussian_bwd_exact_kernel : gaussian_bwd_kernel, dim3(div_up((uint32_t)N, 128)), dim3(128),
+                  0, st, N, ctx->sorted_of_gid.as<uint32_t>(), ctx->accum.as<acc_t>(), kAccStrideHost, (int)ctx->n4,
                   ctx->p4.as<float>(), ctx->cap4, ctx->p3.as<float>(), ctx->cap3, ctx->deg, ctx->cam, ctx->t, scale,
                   ctx->g4, ctx->g3, ctx->sn4.as<float>(), ctx->sn3.as<float>(), ctx->dgn4, ctx->dgn3, ctx->dcnt4,
                   ctx->dcnt3, &ctx->rec_sorted.as<SplatRec>()->c00, (int)(sizeof(SplatRec) / sizeof(double)),
-                  ctx->ddir.as<float4>(), ctx->grads_zero ? 1 : 0));
+                  ctx->ddir.as<float4>(), first));
     count_launch();
     CKL();
     ctx->grads_zero = false;
@@ -706,8 +722,12 @@ hgs_status train_step_impl(hgs_ctx* ctx, int n_views, const hgs_camera* cams, co
     if (pipelined) {
         if ((int)ctx->pipeline.size() >= HGS_TRAIN_PIPELINE)
             return fail(ctx, HGS_ERR_STATE, "train_step_async: pipeline full (hgs_train_collect first)");
-        if (n_views > kMaxStepViews)
-            return fail(ctx, HGS_ERR_INVALID_ARGUMENT, "train_step_async: at most 32 views per iteration");
+        // more than kMaxStepViews views: view v adds its loss sums into slot
+        // v % kMaxStepViews (the loss is linear in the sums of equal-size views)
+        for (int v = kMaxStepViews; v < n_views; ++v)
+            if (cams[v].width != cams[v % kMaxStepViews].width || cams[v].height != cams[v % kMaxStepViews].height)
+                return fail(ctx, HGS_ERR_INVALID_ARGUMENT,
+                            "train_step_async: more than 32 views per iteration need equal image sizes");
         if (!ctx->pipe_ev[0])
             for (int k = 0; k < HGS_TRAIN_PIPELINE; ++k)
                 CK(cudaEventCreateWithFlags(&ctx->pipe_ev[k], cudaEventDisableTiming));
@@ -757,15 +777,15 @@ hgs_status train_step_impl(hgs_ctx* ctx, int n_views, const hgs_camera* cams, co
         // the zeroing of this view's loss sums and backward outputs goes
         // ahead of its render, so render -> loss -> backward is one chain of
         // adjacent kernels (programmatic launches)
-        double* vsums = pipelined ? sc->pipe_sums[slot][v] : sc->view_sums[pending];
+        double* vsums = pipelined ? sc->pipe_sums[slot][v % kMaxStepViews] : sc->view_sums[pending];
         ZeroJobs zj;  // filled by the render's own fill launch
-        zj.add(vsums, 2 * sizeof(double));
+        if (!pipelined || v < kMaxStepViews) zj.add(vsums, 2 * sizeof(double));
         zj.add(ctx->sn4.p, (size_t)ctx->cap4 * 4);
         zj.add(ctx->sn3.p, (size_t)ctx->cap3 * 4);
         {
             const int64_t Nv = ctx->n4 + ctx->n3;  // bound of the visible count
-            CK(ctx->accum.ensure((size_t)std::max<int64_t>(Nv, 1) * kAccStrideHost * 4));
-            zj.add(ctx->accum.p, (size_t)Nv * kAccStrideHost * 4);
+            CK(ctx->accum.ensure((size_t)std::max<int64_t>(Nv, 1) * kAccStrideHost * sizeof(acc_t)));
+            zj.add(ctx->accum.p, (size_t)Nv * kAccStrideHost * sizeof(acc_t));
         }
         r = hgs_render_pipeline(ctx, &cams[v], times[v], o->bg, &ro, 1, 0, nullptr, &zj);
         if (r != HGS_OK) return r;
@@ -783,9 +803,15 @@ hgs_status train_step_impl(hgs_ctx* ctx, int n_views, const hgs_camera* cams, co
     }
     if (!std::isfinite(loss) && apply_adam) {  // an earlier group of views already failed
         if (loss_out) *loss_out = loss;
+        // drop the aborted step's gradients and statistic deltas (no Adam ran,
+        // so the step counter is unchanged), as the abort path below does
+        CK(cudaMemsetAsync(ctx->gbuf.p, 0, (size_t)ctx->gbuf_floats * 4, ctx->stream));
+        ctx->grads_zero = true;
+        r = hgs_render_finish(ctx);
+        if (r != HGS_OK) return r;
         return fail(ctx, HGS_ERR_NUMERIC_ABORT, "train: non-finite loss");  // train.cpp:445-447
     }
-    const int gate = pending;
+    const int gate = std::min(pending, kMaxStepViews);
     const uint64_t step_before = ctx->step;
     if (apply_adam) {  // (the skipped counter was zeroed before the views)
         r = run_adam(ctx, &o->lrs, o->mean_lr_scale, pipelined ? &sc->pipe_sums[slot][0][0] : &sc->view_sums[0][0],
@@ -796,7 +822,7 @@ hgs_status train_step_impl(hgs_ctx* ctx, int n_views, const hgs_camera* cams, co
         hgs_pending_step ps;
         ps.slot = slot;
         ps.n_views = n_views;
-        for (int v = 0; v < n_views; ++v) {
+        for (int v = 0; v < std::min(n_views, kMaxStepViews); ++v) {
             ps.dims[v][0] = cams[v].width;
             ps.dims[v][1] = cams[v].height;
         }
@@ -804,7 +830,8 @@ hgs_status train_step_impl(hgs_ctx* ctx, int n_views, const hgs_camera* cams, co
         ps.adam = apply_adam != 0;
         ps.step_before = step_before;
         double* hp = static_cast<double*>(ctx->pinned_pipe.p) + (size_t)slot * kMaxStepViews * 2;
-        CK(cudaMemcpyAsync(hp, sc->pipe_sums[slot], sizeof(double) * 2 * n_views, cudaMemcpyDeviceToHost,
+        CK(cudaMemcpyAsync(hp, sc->pipe_sums[slot], sizeof(double) * 2 * std::min(n_views, kMaxStepViews),
+                           cudaMemcpyDeviceToHost,
                            ctx->stream));
         CK(cudaEventRecord(ctx->pipe_ev[slot], ctx->stream));
         ctx->pipeline.push_back(ps);
@@ -863,7 +890,8 @@ hgs_status hgs_train_exchange_async(hgs_ctx* ctx, const hgs_train_opts* o) {
     hgs_pending_step& ps = ctx->pipeline.back();
     Scratch* sc = scratch(ctx);
     double* gate = sc->pipe_gate[ps.slot];
-    gate_sum_kernel<<<1, 32, 0, ctx->stream>>>(&sc->pipe_sums[ps.slot][0][0], 2 * ps.n_views, gate);
+    gate_sum_kernel<<<1, 32, 0, ctx->stream>>>(&sc->pipe_sums[ps.slot][0][0], 2 * std::min(ps.n_views, kMaxStepViews),
+                                               gate);
     count_launch();
     CKL();
     hgs_status r = comm_allreduce_f64_dev(ctx, gate, 1);
@@ -890,8 +918,13 @@ hgs_status hgs_train_collect(hgs_ctx* ctx, double* loss_out) {
     CK(cudaEventSynchronize(ctx->pipe_ev[p.slot]));
     const double* hp = static_cast<const double*>(ctx->pinned_pipe.p) + (size_t)p.slot * kMaxStepViews * 2;
     double loss = 0.0;
-    for (int v = 0; v < p.n_views; ++v)
-        loss += loss_from_sums(hp[2 * v], hp[2 * v + 1], p.dims[v][0], p.dims[v][1], p.lambda);
+    for (int v = 0; v < std::min(p.n_views, kMaxStepViews); ++v) {
+        // slot v holds the sums of views v, v + 32, ... (equal sizes): the
+        // constant lambda * 1 of loss.cpp:26-32 once per view
+        const int nv = (p.n_views - v + kMaxStepViews - 1) / kMaxStepViews;
+        loss += loss_from_sums(hp[2 * v], hp[2 * v + 1], p.dims[v][0], p.dims[v][1], p.lambda) +
+                (p.lambda != 0.0 ? p.lambda * (nv - 1) : 0.0);
+    }
     if (loss_out) *loss_out = loss;
     // view-parallel steps: the decision is the all-reduced one (every rank's
     // views), identical on every rank

@@ -7,7 +7,9 @@ Gates (north_star / SURVEY.md 8d):
   * Adam: identical (param, grad, m, v) -> params/moments within FP32 rounding;
   * conversion: moved list and post-sweep pool order bit-exact.
 """
+import json
 import math
+import os
 
 import numpy as np
 import pytest
@@ -49,23 +51,45 @@ def grad_report(g, r, scene):
     return out
 
 
-def check_grads(ctx, scene, cam, t, bg, w, tol=GRAD_TOL, frac=0.0):
+def save_report(name, rep):
+    """Per-class gradient report of a parity test (HGS_REPORT_DIR: where the
+    B200 runs keep it; the committed copies are under profiles/)."""
+    d = os.environ.get("HGS_REPORT_DIR")
+    if d:
+        os.makedirs(d, exist_ok=True)
+        with open(os.path.join(d, f"grad_report_{name}.json"), "w") as f:
+            json.dump(rep, f, indent=1)
+
+
+def f32_input(w):
+    """The device backward takes dL/dimage in FP32: the oracle gets the same
+    (identical inputs -- an FP64-only perturbation of 6e-8 is amplified by the
+    strongly cancelling elements)."""
+    return np.asarray(w, np.float64).astype(np.float32).astype(np.float64)
+
+
+def check_grads(ctx, scene, cam, t, bg, w, exact=False, name=None):
+    """Every gradient element within 1e-3 (floor 1e-6) of the oracle's."""
     scene = scene.as_float32_exact()
+    w = f32_input(w)
     ctx.upload(scene)
-    img = ctx.forward_train(cam, t, bg)
-    ref_img, tape = O.forward_train(scene, cam, t, bg, num_threads=8)
-    assert np.abs(img - ref_img).max() <= 1e-4
-    ctx.backward(w)
-    g = ctx.grads()
+    ctx.set_exact_backward(exact)
+    try:
+        img = ctx.forward_train(cam, t, bg)
+        ref_img, tape = O.forward_train(scene, cam, t, bg, num_threads=8)
+        assert np.abs(img - ref_img).max() <= 1e-4
+        ctx.backward(w)
+        g = ctx.grads()
+    finally:
+        ctx.set_exact_backward(False)
     r = O.backward(scene, cam, tape, w)
     rep = grad_report(g, r, scene)
-    n_el = sum(v["n"] for v in rep.values())
-    n_bad = sum(v["n_bad"] for v in rep.values())
-    assert n_bad <= frac * n_el, (n_bad, n_el, rep)
+    if name:
+        save_report(name, rep)
     for k, v in rep.items():
-        assert v["max_rel"] <= (0.1 if frac > 0 else GRAD_TOL), (k, v)
+        assert v["n_bad"] == 0 and v["max_rel"] <= GRAD_TOL, (k, v)
         assert abs(v["norm_ratio"] - 1.0) < 1e-3, (k, v)
-    return rep
+    return rep, g, r
 
 
 @pytest.mark.parametrize("seed", [61, 62, 71, 72])
@@ -87,18 +111,51 @@ def test_gradients_match_oracle_mixed(ctx, deg):
     check_grads(ctx, scene, cam, 0.5, (0.2, 0.2, 0.2), w)
 
 
-def test_gradients_dense_scene(ctx):
-    """Crowded tiles: long per-pixel lists, saturation, fix-up pixels.
-
-    Stress case (4000 large overlapping splats, >100 layers per pixel, O(1)
-    loss gradients): FP32 compositing leaves a handful of elements of nearly
-    occluded splats just above 1e-3, so the gate here is <= 1e-4 of the
-    elements above 1e-3 (reference metric, absolute floor 1e-6)."""
+def _dense_case():
     scene = synthetic_scene(3000, 1000, 3, seed=11, density_n=100)
     cam = ring_camera(11, 160, 120)
     w = np.random.default_rng(5).uniform(-1, 1, (120, 160, 3))
-    rep = check_grads(ctx, scene, cam, 0.5, (0.2, 0.2, 0.2), w, frac=1e-4)
-    print(rep)
+    return scene, cam, w
+
+
+def test_gradients_dense_scene_exact_mode(ctx):
+    """Crowded tiles (4000 large overlapping splats, >100 layers per pixel,
+    random-sign O(1) loss gradients): with the exact backward mode (FP64 pair
+    terms, hgs_set_exact_backward) every element meets the gate."""
+    scene, cam, w = _dense_case()
+    check_grads(ctx, scene, cam, 0.5, (0.2, 0.2, 0.2), w, exact=True, name="dense_exact")
+
+
+def test_gradients_dense_scene(ctx):
+    """The same adversarial scene on the default path (FP32 pair terms, FP64
+    accumulation).  Random-sign loss gradients make a handful of elements
+    sums that cancel by 1e3-1e5: FP32 pair arithmetic (~1e-7 per term)
+    cannot give them 1e-3 (the exact mode above does).  Gate: every element
+    but <= 3e-5 of them within 1e-3 (measured on B200: 6 of 258000, in
+    mean_t, q_right and the SH rows of one Gaussian), and each of those off
+    by at most 3e-7 of its class's gradient scale -- the FP32 resolution of
+    that scale."""
+    scene, cam, w = _dense_case()
+    scene = scene.as_float32_exact()
+    w = f32_input(w)
+    ctx.upload(scene)
+    ctx.forward_train(cam, 0.5, (0.2, 0.2, 0.2))
+    _, tape = O.forward_train(scene, cam, 0.5, (0.2, 0.2, 0.2), num_threads=8)
+    ctx.backward(w)
+    g = ctx.grads()
+    r = O.backward(scene, cam, tape, w)
+    rep = grad_report(g, r, scene)
+    save_report("dense_default", rep)
+    n_el = sum(v["n"] for v in rep.values())
+    n_bad = sum(v["n_bad"] for v in rep.values())
+    assert n_bad <= 3e-5 * n_el, (n_bad, n_el, rep)
+    for k in rep:
+        a = np.asarray(g[k], np.float64).ravel()
+        b = np.asarray(r[k], np.float64).ravel()
+        scale = np.abs(b).max()
+        bad = rel_err(a, b) > GRAD_TOL
+        assert (np.abs(a - b)[bad] <= 3e-7 * scale).all(), (k, a[bad], b[bad], scale)
+        assert abs(rep[k]["norm_ratio"] - 1.0) < 1e-3, (k, rep[k])
 
 
 def test_loss_matches_oracle(ctx):
@@ -137,7 +194,7 @@ def test_loss_on_render_and_backward(ctx):
     r = O.backward(scene, cam, tape, lg.astype(np.float64))
     rep = grad_report(g, r, scene)
     for k, v in rep.items():
-        assert v["frac_bad"] <= 1e-3, (k, v)
+        assert v["n_bad"] == 0, (k, v)
 
 
 def test_adam_matches_oracle(ctx):
@@ -349,17 +406,17 @@ def test_gradients_c2_full_size(ctx):
     ctx.upload(scene)
     img = ctx.forward_train(cam, 0.0, bg)
     loss, w = O.photometric_loss_with_grad(img.astype(np.float64), gt, 0.2)  # the oracle's dL/dimage
+    w = f32_input(w)
     ref_img, tape = O.forward_train(scene, cam, 0.0, bg, num_threads=O.hardware_threads())
     assert np.abs(img - ref_img).max() <= 1e-4
     ctx.backward(w)
     g = ctx.grads()
     r = O.backward(scene, cam, tape, w)
     rep = grad_report(g, r, scene)
-    n_el = sum(v["n"] for v in rep.values())
-    n_bad = sum(v["n_bad"] for v in rep.values())
+    save_report("c2", rep)
     print({k: (v["max_rel"], v["n_bad"], v["norm_ratio"]) for k, v in rep.items()})
-    assert n_bad <= 1e-4 * n_el, (n_bad, n_el)
     for k, v in rep.items():
+        assert v["n_bad"] == 0 and v["max_rel"] <= GRAD_TOL, (k, v)
         assert abs(v["norm_ratio"] - 1.0) < 1e-3, (k, v)
 
 
