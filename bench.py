@@ -140,8 +140,8 @@ def algorithmic_bytes(phase: str, n: dict) -> float | None:
     """Per-step algorithmic bytes of each kernel phase (SURVEY.md 8d table,
     adapted to this implementation's passes)."""
     N4, N3, V, I, K, px, P = n["n4"], n["n3"], n["V"], n["I"], n["K"], n["px"], n["rows_avg"]
-    if phase == "preprocess":   # params in (68/44 B geometry + 192 B SH of visible) + 80 B record out + flags
-        return 68 * N4 + 44 * N3 + (192 + 80) * V + 4 * (N4 + N3) * 3
+    if phase == "preprocess":   # params in (68/44 B geometry + 192 B SH of visible), 80 B record + 64 B
+        return 68 * N4 + 44 * N3 + (192 + 80 + 64) * V + 4 * (N4 + N3) * 3  # colour record out, flags
     if phase == "depth_sort":   # global LSD over V keys+values: (8 + 24*passes) * n
         return (8 + 24 * 4) * V
     if phase == "duplicate":    # gather (80 B in, 80+64+8 B out) + offsets scan; 12 B per instance out
@@ -418,27 +418,47 @@ def run_extras(args, ctx, lib, timed, world, rank) -> dict:
                                  "config": f"{c['n4'] // 1000}k 4D + {c['n3'] // 1000}k 3D, "
                                            f"{c['width']}x{c['height']}" + (", t=j/49" if name == "c5" else "")}
         del scene
+    # c4: 8 views per optimizer step in TOTAL (BASELINE configs[3]), split
+    # over the ranks (strong scaling of the step); at N > 1 the packed
+    # gradient all-reduce + gated Adam are inside the timed region
+    # (ViewParallelTrainer, hgs_train_exchange_async)
+    import torch.distributed as tdist
+
+    from paper_2505_13215_b200.train import ViewParallelTrainer
+
     c = CONFIGS["c4"]
     scene = synthetic_scene(c["n4"], c["n3"], 3, seed=c["seed"], tau=0.5)
     target = synthetic_scene(c["n4"], c["n3"], 3, seed=c["seed"] + 1000, tau=0.5)
     cams = [ring_camera(c["seed"], c["width"], c["height"], index=i, n_ring=16) for i in range(16)]
     times = [i / 15.0 for i in range(16)]
-    tr = DeviceTrainer(ctx, scene, cams, times, target=target, bg=(0.2, 0.2, 0.2), iterations=1000)
+    vp = tdist.is_available() and tdist.is_initialized()
+    kw = dict(target=target, bg=(0.2, 0.2, 0.2), iterations=1000)
+    tr = (ViewParallelTrainer(ctx, scene, cams, times, exchange="capi", **kw) if vp
+          else DeviceTrainer(ctx, scene, cams, times, **kw))
     del target
     for v in range(16):
         ctx.render(cams[v], times[v], (0.2, 0.2, 0.2))
-    per = 8
+    per_step = 8
 
     def step(i):
-        tr.step([(i * per * world + rank * per + j) % 16 for j in range(per)])
+        tr.step_async([(i * per_step + j) % 16 for j in range(per_step)])
+        if ctx._lib.hgs_train_pending(ctx.handle) > 1:
+            tr.collect()
+
+    def drain():
+        while ctx._lib.hgs_train_pending(ctx.handle):
+            tr.collect()
 
     for i in range(args.warmup):
         step(i)
+    drain()
     k = max(2, args.steps // 2)
-    ms = timed(step, k)
-    out["c4_train"] = {"value": round(world * k * per / (ms / 1e3), 3), "unit": "views/s",
-                       "ms_per_step": round(ms / k, 4), "views_per_step_per_gpu": per,
-                       "config": "1600k 4D + 400k 3D, SH 3, 1352x1014, 8 views/GPU/step"}
+    ms = timed(step, k, drain)
+    out["c4_train"] = {"value": round(k * per_step / (ms / 1e3), 3), "unit": "views/s",
+                       "ms_per_step": round(ms / k, 4), "views_per_step": per_step,
+                       "views_per_gpu_per_step": per_step / world, "scaling": "strong",
+                       "exchange": "NCCL all-reduce of the packed gradients + gated Adam (timed)" if vp else "none (1 GPU)",
+                       "config": "1600k 4D + 400k 3D, SH 3, 1352x1014, 8 views per optimizer step over all GPUs"}
     torch.cuda.synchronize()
     return out
 
@@ -599,66 +619,104 @@ def cpu_baseline(scene, cam, t, gt) -> dict:
     dt = time.perf_counter() - t0
     return {"value": round(1.0 / dt, 5), "unit": UNIT, "cores": cores, "kind": "port",
             "sample": f"one full {cam.width}x{cam.height} training iteration of the c2 scene "
-                      f"({dt:.2f} s): tiled forward w/ tape on {cores} threads, L1+SSIM, backward 1 thread, Adam"}
+                      f"({dt:.2f} s): tiled forward w/ tape on {cores} threads, L1+SSIM, backward 1 thread, Adam",
+            "literal_forward_train": literal_forward_train(scene, cam, t)}
+
+
+def literal_forward_train(scene, cam, t) -> dict:
+    """The reference's own forward_train is UNTILED (backward.cpp:142-175:
+    every projected splat tested at every pixel).  Timed on one thread, as the
+    reference, at 1/256 of c2's pixels x Gaussians (N/4 Gaussians, W/8 x H/8
+    pixels) and extrapolated x256 (the cost is linear in both)."""
+    import oracle as O
+    from paper_2505_13215_b200.scene import Camera
+
+    sub = scene.subset(scene.n4 // 4, scene.n3 // 4) if hasattr(scene, "subset") else None
+    if sub is None:
+        return {"note": "scene subset unavailable"}
+    small = Camera(fx=cam.fx / 8, fy=cam.fy / 8, cx=cam.cx / 8, cy=cam.cy / 8, rot=cam.rot, trans=cam.trans,
+                   width=cam.width // 8, height=cam.height // 8, near=cam.near, far=cam.far)
+    t0 = time.perf_counter()
+    O.forward_train(sub, small, t, (0.2, 0.2, 0.2), untiled=True)
+    dt = time.perf_counter() - t0
+    return {"seconds_at_1_256": round(dt, 3), "extrapolated_s_per_c2_view": round(256 * dt, 1),
+            "views_per_s": round(1.0 / (256 * dt), 6), "cores": 1,
+            "sample": f"{sub.n4 + sub.n3} Gaussians, {small.width}x{small.height}, untiled taped forward only"}
 
 
 # ------------------------------------------------------------------ reference arm
 def run_reference(args) -> None:
-    """The reference's own CPU path (FP64 oracle port of proj/src; the C++
-    reference needs Eigen3 and cannot be compiled in this image).  Batch-image
-    parallel like train_scene (one std::thread per view, train.cpp:419-422),
-    all host threads used; each step is a bounded sample: B views cropped to a
-    horizontal band so the whole --steps/--warmup run stays within minutes."""
+    """The reference's own CPU path for the same workload (config c2, one
+    full 1352x1014 view per training iteration = the GPU arm's iteration at
+    N=1): the FP64 oracle port of proj/src (the C++ reference needs Eigen3,
+    absent here), forward tiled with its tape on all host threads
+    (RasterOpts::num_threads, raster.cpp:150-163), L1 + D-SSIM, backward on
+    one thread as the reference, Adam.  Under torchrun only rank 0 runs."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     import oracle as O
-    from paper_2505_13215_b200.scene import Camera
     from paper_2505_13215_b200.train import quantize_8bit
 
     scene, target, cams, times, desc = workload(args.config)
     cores = O.hardware_threads()
-    B = max(1, min(cores, 8))
-    full_step_s = 30.0  # measured: B=8 concurrent full-view iterations, one thread each (8-core host)
-    frac = float(np.clip(150.0 / ((args.steps + args.warmup) * full_step_s), 0.1, 1.0))
-    H, W = cams[0].height, cams[0].width
-    hb = max(16, int(round(H * frac)))
-    y0 = (H - hb) // 2
+    gts = {}
 
-    def band(c: Camera) -> Camera:
-        return Camera(fx=c.fx, fy=c.fy, cx=c.cx, cy=c.cy - y0, rot=c.rot, trans=c.trans, width=W, height=hb,
-                      near=c.near, far=c.far)
+    def gt(v):
+        if v not in gts:
+            gts[v] = quantize_8bit(O.rasterize(target, cams[v], times[v], (0.2, 0.2, 0.2), num_threads=cores)["rgb"])
+        return gts[v]
 
-    bcams = [band(c) for c in cams]
-    gts = []
-    for i in range(len(cams)):
-        img = O.rasterize(target, bcams[i], times[i], (0.2, 0.2, 0.2), num_threads=cores)["rgb"]
-        gts.append(quantize_8bit(img))
     s = scene.copy()
     st = O.AdamState(s)
 
     def step(i):
-        vs = [(i * B + b) % len(cams) for b in range(B)]
-        O.train_step(s, st, [bcams[v] for v in vs], [times[v] for v in vs], [gts[v] for v in vs],
-                     (0.2, 0.2, 0.2), num_threads=B, tile_threads=1)
+        v = i % len(cams)
+        O.train_step(s, st, [cams[v]], [times[v]], [gt(v)], (0.2, 0.2, 0.2), num_threads=1, tile_threads=cores)
 
+    for v in range(min(len(cams), args.warmup + args.steps)):
+        gt(v)  # ground truth rendered outside the timed steps
     for i in range(args.warmup):
         step(i)
     t0 = time.perf_counter()
     for i in range(args.steps):
         step(args.warmup + i)
     dt = time.perf_counter() - t0
-    views = B * args.steps * hb / H
-    value = views / dt
-    sample = (f"each step: {B} views x {W}x{hb} band ({hb / H:.2f} of a view), one thread per view "
-              f"(train.cpp:419-422), FP64 oracle port of the reference")
+    value = args.steps / dt
+    sample = (f"each step: one full {cams[0].width}x{cams[0].height} c2 training iteration, forward tiled on "
+              f"{cores} threads, backward 1 thread; FP64 oracle port of the reference")
     out = {"impl": "reference", "metric": METRIC, "value": round(value, 5), "unit": UNIT, "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 2),
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": dict(desc, parallelism=f"batch-image threads x{B}"),
-           "cpu_baseline": {"value": round(value, 5), "unit": UNIT, "cores": B, "kind": "port", "sample": sample},
+           "config": dict(desc, parallelism="tile threads (RasterOpts::num_threads)"),
+           "cpu_baseline": {"value": round(value, 5), "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
            "e2e": {"value": round(value, 5), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
+
+
+def self_launch(args) -> int | None:
+    """`bench.py --gpus N` outside torchrun: start N ranks with
+    torch.distributed.run on 127.0.0.1 and return their exit code; under
+    torchrun, insist that WORLD_SIZE == --gpus."""
+    world = os.environ.get("WORLD_SIZE")
+    if world is not None:
+        if int(world) != args.gpus:
+            raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+        return None
+    if args.gpus <= 1:
+        return None
+    import socket
+
+    import torch
+
+    if torch.cuda.device_count() < args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but only {torch.cuda.device_count()} CUDA devices")
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -678,8 +736,11 @@ def main():
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     if args.impl == "reference":
         run_reference(args)
-    else:
-        run_ours(args)
+        return
+    rc = self_launch(args)
+    if rc is not None:
+        sys.exit(rc)
+    run_ours(args)
 
 
 if __name__ == "__main__":

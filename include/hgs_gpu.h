@@ -190,9 +190,10 @@ hgs_status hgs_grads_packed(hgs_ctx *ctx, int unpack, float **ptr, int64_t *coun
 
 /* ---- multi-GPU exchange -------------------------------- */
 /* View-parallel data parallelism: each rank renders its views with
- * apply_adam = 0, hgs_allreduce_grads sums the packed payload (gradient rows
- * + densify-statistic deltas) over the ranks with ncclAllReduce on the
- * context stream, then every rank runs the same hgs_adam_step.  NCCL is
+ * apply_adam = 0, hgs_allreduce_grads sums the gradient rows + the
+ * densify-statistic deltas over the ranks in place (one NCCL group of
+ * all-reduces over the valid prefix of every row, on the context stream; no
+ * packing), then every rank runs the same hgs_adam_step.  NCCL is
  * loaded at run time (libnccl.so.2; an already-loaded copy is shared).
  *   hgs_comm_unique_id  -- on one rank; ship the 128 bytes out of band
  *   hgs_comm_init       -- one process per GPU (ncclCommInitRank)

@@ -2,9 +2,8 @@
 //
 // View-parallel data parallelism: every rank holds a replica of the scene and
 // renders its share of the batch; the one exchange per optimizer step is an
-// all-reduce (sum) of the packed gradient payload (valid gradient rows +
-// densify-statistic deltas, hgs_grads_packed), then every rank applies the
-// same Adam step.  Replica consistency is checked with an order-independent
+// all-reduce (sum) of the valid gradient rows + densify-statistic deltas,
+// in place (one NCCL group), then every rank applies the same Adam step.  Replica consistency is checked with an order-independent
 // 64-bit checksum of the parameters (hgs_param_checksum) and repaired with a
 // broadcast from a root (hgs_broadcast_params).
 //
@@ -185,18 +184,32 @@ hgs_status hgs_comm_destroy(hgs_ctx* ctx) {
     return HGS_OK;
 }
 
+// In place, no packing: one NCCL group of sum all-reduces over the valid
+// prefix [0, n) of every gradient row (the rows are strided by the pool
+// capacity, whose tail is padding) and of the densification-statistic
+// deltas.  NCCL runs the group as one aggregated launch (with a one-rank
+// communicator: the identity, still issued through NCCL).
 hgs_status hgs_allreduce_grads(hgs_ctx* ctx) {
     if (!ctx) return HGS_ERR_INVALID_ARGUMENT;
     hgs_status r = need_comm(ctx);
     if (r != HGS_OK) return r;
+    if (!ctx->gbuf.p) return fail(ctx, HGS_ERR_STATE, "allreduce_grads: no scene uploaded");
     CKC(cudaSetDevice(ctx->device));
-    float* p = nullptr;
-    int64_t n = 0;
-    r = hgs_grads_packed(ctx, 0, &p, &n);
-    if (r != HGS_OK) return r;
-    if (n > 0)
-        CKN(nccl().AllReduce(p, p, (size_t)n, ncclFloat32, ncclSum, static_cast<ncclComm_t>(ctx->comm), ctx->stream));
-    return hgs_grads_packed(ctx, 1, nullptr, nullptr);
+    ctx->grads_zero = false;
+    ncclComm_t c = static_cast<ncclComm_t>(ctx->comm);
+    const int r4 = rows4(ctx->deg), r3 = rows3(ctx->deg);
+    auto ar = [&](float* p, int64_t n) -> ncclResult_t {
+        return n > 0 ? nccl().AllReduce(p, p, (size_t)n, ncclFloat32, ncclSum, c, ctx->stream) : ncclSuccess;
+    };
+    CKN(nccl().GroupStart());
+    for (int k = 0; k < r4; ++k) CKN(ar(ctx->g4 + (int64_t)k * ctx->cap4, ctx->n4));
+    for (int k = 0; k < r3; ++k) CKN(ar(ctx->g3 + (int64_t)k * ctx->cap3, ctx->n3));
+    CKN(ar(ctx->dgn4, ctx->n4));
+    CKN(ar(ctx->dgn3, ctx->n3));
+    CKN(ar(ctx->dcnt4, ctx->n4));
+    CKN(ar(ctx->dcnt3, ctx->n3));
+    CKN(nccl().GroupEnd());
+    return HGS_OK;
 }
 
 hgs_status hgs_allreduce_f64(hgs_ctx* ctx, double* vals, int n) {

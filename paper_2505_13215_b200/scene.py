@@ -78,6 +78,15 @@ class HybridScene:
     def copy(self) -> "HybridScene":
         return copy.deepcopy(self)
 
+    def subset(self, n4: int, n3: int) -> "HybridScene":
+        """The first n4 dynamic and n3 static Gaussians (a bounded sample)."""
+        out = self.copy()
+        for f in self.DYN_FIELDS:
+            setattr(out, f, np.ascontiguousarray(getattr(self, f)[:n4]))
+        for f in self.STA_FIELDS:
+            setattr(out, f, np.ascontiguousarray(getattr(self, f)[:n3]))
+        return out
+
     def as_float32_exact(self) -> "HybridScene":
         """Round every parameter to float32 and widen back.
 

@@ -184,7 +184,9 @@ class ViewParallelTrainer(DeviceTrainer):
         self.exchange = exchange
         self.verify_every = verify_every
         self.repairs = 0
-        if exchange == "capi":
+        if exchange == "capi" and self.ctx._lib.hgs_comm_size(self.ctx.handle) != self.world:
+            # one communicator per context: a second trainer on the same
+            # context (another scene) reuses it
             uid = [Context.comm_unique_id() if self.rank == 0 else None]
             dist.broadcast_object_list(uid, src=0, group=group)
             self.ctx.comm_init(self.world, self.rank, uid[0])

@@ -20,3 +20,21 @@ def test_reference_arm_json_contract():
     assert line["e2e"]["value"] == line["value"] and line["e2e"]["h2d_bytes_per_step"] == 0
     assert line["cpu_baseline"]["cores"] >= 1 and line["cpu_baseline"]["kind"] in ("port", "reference")
     assert "workload" in line["config"]
+
+
+def test_gpus_flag_must_match_world_size():
+    """--gpus N under torchrun with another WORLD_SIZE fails loudly (no silent
+    one-GPU measurement)."""
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "1"],
+                         capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert out.returncode != 0 and "WORLD_SIZE=1" in out.stderr
+
+
+def test_gpus_flag_without_enough_devices_fails():
+    """--gpus N outside torchrun self-launches N ranks; with fewer CUDA devices
+    than N (this container has none) it refuses instead of measuring fewer."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "1"],
+                         capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert out.returncode != 0 and "CUDA devices" in out.stderr

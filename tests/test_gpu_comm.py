@@ -1,8 +1,10 @@
 """The C-ABI multi-GPU exchange (hgs_comm_*, hgs_allreduce_grads,
 hgs_param_checksum, hgs_broadcast_params) on one B200: a one-rank NCCL
-communicator exercises the whole plumbing (pack -> ncclAllReduce -> unpack on
-the context stream) with the identity reduction; the multi-rank host logic is
-covered by tests/test_dist_cpu.py (gloo, world size 2)."""
+communicator exercises the whole plumbing (the grouped in-place
+ncclAllReduce of every gradient row on the context stream) with the identity
+reduction; two processes sharing the GPU exchange through gloo in
+tests/test_gpu_dist_product.py (NCCL refuses two ranks on one device), and the
+multi-rank host logic is covered by tests/test_dist_cpu.py."""
 import numpy as np
 import pytest
 
