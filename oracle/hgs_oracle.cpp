@@ -1096,7 +1096,9 @@ void backward(const View& v, const Cam& cam, const Tape& tape, const double* lg,
             const auto& list = tape.contribs[pix];
             if (list.empty()) continue;
             double gp[3] = {lg[pix * 3], lg[pix * 3 + 1], lg[pix * 3 + 2]};
-            if (gp[0] == 0.0 && gp[1] == 0.0 && gp[2] == 0.0) continue;
+            // gpix.isZero() (backward.cpp:189): Eigen's isZero is every
+            // |component| <= dummy_precision = 1e-12, not == 0
+            if (std::abs(gp[0]) <= 1e-12 && std::abs(gp[1]) <= 1e-12 && std::abs(gp[2]) <= 1e-12) continue;
             double pc[2] = {px + 0.5, py + 0.5};
             const size_t n = list.size();
             std::vector<double> av(n), tv(n), gv(n);

@@ -161,9 +161,11 @@ class Context:
         k = _capi.CommId()
         C.memmove(C.addressof(k), uid, 128)
         self._check(self._lib.hgs_comm_init(self._h, int(nranks), int(rank), C.byref(k)))
+        self._comm_world = int(nranks)
 
     def comm_destroy(self) -> None:
         self._check(self._lib.hgs_comm_destroy(self._h))
+        self._comm_world = None
 
     def allreduce_grads(self) -> None:
         """Sum the packed gradient payload over the ranks (stream-ordered)."""

@@ -163,8 +163,11 @@ __global__ void __launch_bounds__(kThreadsB, 7) raster_bwd_kernel(
         s.gb = dL_dimg[pix * 3 + 2];
         s.T = tfinal[pix];
         s.GS = s.T * fmaf(s.gr, bg_r, fmaf(s.gg, bg_g, s.gb * bg_b));
-        // flagged pixels go through the exact kernel; zero gradient = untouched (backward.cpp:188)
-        if (!(l & 0x80000000u) && (s.gr != 0.f || s.gg != 0.f || s.gb != 0.f)) s.last = l;
+        // flagged pixels go through the exact kernel; a gradient that is
+        // zero by Eigen's isZero (every |component| <= 1e-12, backward.cpp:189;
+        // for floats <= 1e-12f is the same test) leaves the pixel untouched
+        const bool zero = fabsf(s.gr) <= 1e-12f && fabsf(s.gg) <= 1e-12f && fabsf(s.gb) <= 1e-12f;
+        if (!(l & 0x80000000u) && !zero) s.last = l;
     };
     const int cshift = px - tx * kTile, rshift0 = 16 + py0 - ty * kTile, rshift1 = rshift0 + 4;
     PixBwd2 s;
@@ -307,7 +310,7 @@ __global__ void __launch_bounds__(128) raster_bwd_exact_kernel(
     for (uint32_t q = blockIdx.x * (blockDim.x >> 5) + wib; q < n; q += warps) {
         const int pix = fix_list ? (int)fix_list[q] : (int)q;
         const double gp[3] = {dL_dimg[pix * 3], dL_dimg[pix * 3 + 1], dL_dimg[pix * 3 + 2]};
-        if (gp[0] == 0.0 && gp[1] == 0.0 && gp[2] == 0.0) continue;
+        if (fabs(gp[0]) <= 1e-12 && fabs(gp[1]) <= 1e-12 && fabs(gp[2]) <= 1e-12) continue;  // isZero, backward.cpp:189
         const int px = pix % W, py = pix / W;
         const uint2 rg = ranges[(py / kTile) * tiles_x + px / kTile];
         const uint32_t last = last_arr[pix] & 0x7fffffffu;

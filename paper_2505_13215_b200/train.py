@@ -184,7 +184,7 @@ class ViewParallelTrainer(DeviceTrainer):
         self.exchange = exchange
         self.verify_every = verify_every
         self.repairs = 0
-        if exchange == "capi" and self.ctx._lib.hgs_comm_size(self.ctx.handle) != self.world:
+        if exchange == "capi" and getattr(self.ctx, "_comm_world", None) != self.world:
             # one communicator per context: a second trainer on the same
             # context (another scene) reuses it
             uid = [Context.comm_unique_id() if self.rank == 0 else None]
