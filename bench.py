@@ -636,12 +636,23 @@ def literal_forward_train(scene, cam, t) -> dict:
         return {"note": "scene subset unavailable"}
     small = Camera(fx=cam.fx / 8, fy=cam.fy / 8, cx=cam.cx / 8, cy=cam.cy / 8, rot=cam.rot, trans=cam.trans,
                    width=cam.width // 8, height=cam.height // 8, near=cam.near, far=cam.far)
+    try:  # the reference's own forward_train (oracle/_ref, compiled from its sources) when built
+        from oracle import ref as R
+
+        use_ref = R.available()
+    except Exception:
+        use_ref = False
     t0 = time.perf_counter()
-    O.forward_train(sub, small, t, (0.2, 0.2, 0.2), untiled=True)
+    if use_ref:
+        R.forward_backward(sub, small, t, (0.2, 0.2, 0.2), None)
+    else:
+        O.forward_train(sub, small, t, (0.2, 0.2, 0.2), untiled=True)
     dt = time.perf_counter() - t0
     return {"seconds_at_1_256": round(dt, 3), "extrapolated_s_per_c2_view": round(256 * dt, 1),
             "views_per_s": round(1.0 / (256 * dt), 6), "cores": 1,
-            "sample": f"{sub.n4 + sub.n3} Gaussians, {small.width}x{small.height}, untiled taped forward only"}
+            "kind": "reference" if use_ref else "port",
+            "sample": f"{sub.n4 + sub.n3} Gaussians, {small.width}x{small.height}, untiled taped forward only "
+                      f"({'hgs::forward_train of the reference compiled from its sources' if use_ref else 'oracle restatement'})"}
 
 
 # ------------------------------------------------------------------ reference arm

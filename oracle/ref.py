@@ -92,6 +92,10 @@ def forward_backward(scene: HybridScene, cam: Camera, t: float, background, loss
     """hgs::forward_train + hgs::backward (backward.hpp:68-74): image, grads."""
     st = O._scene_struct(scene)
     rgb = np.zeros((cam.height, cam.width, 3))
+    if loss_grad is None:  # the taped forward only
+        _check(lib().hgsr_forward_backward(C.byref(st), C.byref(O._cam_struct(cam)), t,
+                                           O._p(O._arr(background, 3)), weight_cutoff, None, O._p(rgb), None))
+        return rgb, None
     g = O.zero_grads(scene)
     lg = O._arr(loss_grad)
     _check(lib().hgsr_forward_backward(C.byref(st), C.byref(O._cam_struct(cam)), t, O._p(O._arr(background, 3)),
