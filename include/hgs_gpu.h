@@ -312,6 +312,18 @@ hgs_status hgs_adam_state_upload(hgs_ctx *ctx, const hgs_host_scene *m, const hg
                                  uint64_t step);
 hgs_status hgs_stats_download(hgs_ctx *ctx, double *grad_norm4, uint32_t *count4, double *grad_norm3,
                               uint32_t *count3);
+/* Inverse of hgs_stats_download: GradAccum::grad_norm* / count*
+ * (optim.hpp:32-41) into the device, pending deltas cleared. */
+hgs_status hgs_stats_upload(hgs_ctx *ctx, const double *grad_norm4, const uint32_t *count4, const double *grad_norm3,
+                            const uint32_t *count3);
+/* Host gradients into the device gradient rows (layout of hgs_grads_download;
+ * statistic deltas cleared), so a reference-signature optimizer_step(scene,
+ * const SceneGrads&, ...) (train.hpp:68-69) runs hgs_adam_step on them. */
+hgs_status hgs_grads_upload(hgs_ctx *ctx, const hgs_host_scene *grads, int dtype);
+/* GradAccum::skipped_nonfinite (optim.hpp:39) of the device state: rows x
+ * classes skipped for non-finite gradients since the upload; read (get)
+ * and / or set it (set, e.g. when resuming from a checkpoint). */
+hgs_status hgs_skipped_nonfinite(hgs_ctx *ctx, uint64_t *get, const uint64_t *set);
 
 /* ---- conversion (scene.hpp:75 + train.cpp:305-362) --------------------- */
 /* Moves every dynamic Gaussian with exp(s_t) > tau into the static pool

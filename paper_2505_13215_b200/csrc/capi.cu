@@ -664,7 +664,7 @@ void hgs_ctx_destroy(hgs_ctx* ctx) {
                     &ctx->sort_v2, &ctx->rec_sorted, &ctx->fast_sorted, &ctx->ntiles_sorted, &ctx->inst_off,
                     &ctx->inst_k, &ctx->inst_v, &ctx->inst_k2, &ctx->inst_v2, &ctx->ranges, &ctx->sorted_of_gid, &ctx->inst_flag, &ctx->inst_pos, &ctx->dbg_k, &ctx->dbg_v, &ctx->scan_ws,
                     &ctx->sort_ws, &ctx->counters, &ctx->img, &ctx->last, &ctx->tfinal, &ctx->trans, &ctx->count,
-                    &ctx->fix_list, &ctx->accum, &ctx->exact_col, &ctx->lgrad, &ctx->gt_stage, &ctx->loss_ws, &ctx->stage, &ctx->adam_ok, &ctx->pcut, &ctx->dup_first, &ctx->shdir, &ctx->ddir, &ctx->dup_status, &ctx->gpack, &ctx->dens_cat, &ctx->dens_u32, &ctx->dens_misc, &ctx->dens_kinds, &ctx->dens_jit, &ctx->dmap, &ctx->ckpt, &ctx->crc_tab, &ctx->comm_buf, &ctx->sweep_ctr};
+                    &ctx->fix_list, &ctx->accum, &ctx->exact_col, &ctx->loss_img, &ctx->lgrad, &ctx->gt_stage, &ctx->loss_ws, &ctx->stage, &ctx->adam_ok, &ctx->pcut, &ctx->dup_first, &ctx->shdir, &ctx->ddir, &ctx->dup_status, &ctx->gpack, &ctx->dens_cat, &ctx->dens_u32, &ctx->dens_misc, &ctx->dens_kinds, &ctx->dens_jit, &ctx->dmap, &ctx->ckpt, &ctx->crc_tab, &ctx->comm_buf, &ctx->sweep_ctr};
     for (DBuf* b : bufs) b->release();
     ctx->pinned.release();
     ctx->pinned_ctr.release();

@@ -152,6 +152,7 @@ struct hgs_ctx {
     bool exact_backward = false;  // hgs_set_exact_backward: FP64 pair terms for every pixel
     hgs::DBuf exact_col;          // its FP64 colours (sorted order)
     hgs::DBuf lgrad;     // dL/dimage (device float)
+    hgs::DBuf loss_img;  // the image of a standalone hgs_photometric_loss_with_grad
     hgs::DBuf gt_stage;  // staged ground truth
     hgs::DBuf gt_buf[2], gt_stage64[2];  // double-buffered host GT of the training step
     cudaStream_t copy_stream = nullptr;  // host -> device GT copies, overlapped with the render

@@ -228,10 +228,13 @@ hgs_status run_backward(hgs_ctx* ctx, const float* lg, double scale, bool zeroed
 // accumulates the loss into scratch->loss_acc (device) -- no host sync.
 // sums (device, optional): where to accumulate (ssim_sum, l1_sum); default
 // the scratch pair read by the loss API
+// img / W / H: the rendered image (default: the context's last render)
 hgs_status run_loss(hgs_ctx* ctx, const void* gt, bool gt_u8, double lambda, double* sums = nullptr,
-                    bool sums_zeroed = false) {
+                    bool sums_zeroed = false, const float* img = nullptr, int W = -1, int H = -1) {
     cudaStream_t st = ctx->stream;
-    const int W = ctx->W, H = ctx->H;
+    if (!img) img = ctx->img.as<float>();
+    if (W < 0) W = ctx->W;
+    if (H < 0) H = ctx->H;
     const bool with_ssim = lambda != 0.0;
     if (with_ssim && (W < 11 || H < 11))
         return fail(ctx, HGS_ERR_INVALID_ARGUMENT, "ssim: images smaller than the 11x11 window");
@@ -244,7 +247,7 @@ hgs_status run_loss(hgs_ctx* ctx, const void* gt, bool gt_u8, double lambda, dou
     const int vw = W - 10, vh = H - 10;
     prof_begin(ctx, PH_LOSS);
     if (with_ssim) CK(ctx->loss_ws.ensure((size_t)vw * vh * 9 * 4));
-    launch_loss(st, ctx->img.as<float>(), gt, gt_u8, W, H, ctx->loss_ws.as<float>(), (float)lambda, with_ssim,
+    launch_loss(st, img, gt, gt_u8, W, H, ctx->loss_ws.as<float>(), (float)lambda, with_ssim,
                 ctx->lgrad.as<float>(), sums);
     count_launch(with_ssim ? 2 : 1);
     CKL();
@@ -517,14 +520,14 @@ hgs_status hgs_photometric_loss_with_grad(hgs_ctx* ctx, const void* rendered, co
     hgs_status r = ensure_scratch(ctx);
     if (r != HGS_OK) return r;
     const int64_t n = (int64_t)width * height * 3;
-    r = upload_image(ctx, rendered, dtype, n, ctx->img);
+    // its own image buffer: the last render (the tape of a pending backward)
+    // stays valid, as the reference's pure loss function leaves it
+    r = upload_image(ctx, rendered, dtype, n, ctx->loss_img);
     if (r != HGS_OK) return r;
     r = upload_image(ctx, gt, dtype, n, ctx->gt_stage);
     if (r != HGS_OK) return r;
-    ctx->W = width;
-    ctx->H = height;
-    ctx->have_tape = false;  // img no longer belongs to a render
-    r = run_loss(ctx, ctx->gt_stage.as<float>(), false, lambda);
+    r = run_loss(ctx, ctx->gt_stage.as<float>(), false, lambda, nullptr, false, ctx->loss_img.as<float>(), width,
+                 height);
     if (r != HGS_OK) return r;
     Scratch* h = static_cast<Scratch*>(ctx->pinned.p);
     CK(cudaMemcpyAsync(h, ctx->scratch.p, sizeof(Scratch), cudaMemcpyDeviceToHost, ctx->stream));
@@ -586,6 +589,54 @@ hgs_status hgs_adam_state_upload(hgs_ctx* ctx, const hgs_host_scene* m, const hg
     r = hgs_upload_rows(ctx, v, dtype, ctx->v4.as<float>(), ctx->v3.as<float>());
     if (r != HGS_OK) return r;
     ctx->step = step;
+    return HGS_OK;
+}
+
+// Host gradients (the SceneGrads of optimizer_step(scene, grads, ...),
+// train.hpp:68-69) into the device gradient rows; the densification-
+// statistic deltas are cleared (an uploaded gradient carries none).
+hgs_status hgs_grads_upload(hgs_ctx* ctx, const hgs_host_scene* g, int dtype) {
+    if (!ctx || !g) return HGS_ERR_INVALID_ARGUMENT;
+    if (!ctx->gbuf.p) return fail(ctx, HGS_ERR_STATE, "grads_upload: no scene uploaded");
+    if (g->n4 != ctx->n4 || g->n3 != ctx->n3 || g->sh_degree != ctx->deg)
+        return fail(ctx, HGS_ERR_INVALID_ARGUMENT, "grads_upload: pool sizes / SH degree differ from the scene");
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaMemsetAsync(ctx->gbuf.p, 0, (size_t)ctx->gbuf_floats * 4, ctx->stream));
+    hgs_status r = hgs_upload_rows(ctx, g, dtype, ctx->g4, ctx->g3);
+    if (r != HGS_OK) return r;
+    ctx->grads_zero = false;
+    return HGS_OK;
+}
+
+// Densification statistics (GradAccum::grad_norm* / count*, optim.hpp:32-41)
+// into the device (e.g. when training resumes from a checkpoint state).
+hgs_status hgs_stats_upload(hgs_ctx* ctx, const double* gn4, const uint32_t* c4, const double* gn3,
+                            const uint32_t* c3) {
+    if (!ctx) return HGS_ERR_INVALID_ARGUMENT;
+    if (!ctx->gbuf.p) return fail(ctx, HGS_ERR_STATE, "stats_upload: no scene uploaded");
+    CK(cudaSetDevice(ctx->device));
+    const int64_t n4 = ctx->n4, n3 = ctx->n3;
+    std::vector<float> a(n4, 0.f), b(n4, 0.f), c(n3, 0.f), d(n3, 0.f);
+    for (int64_t i = 0; i < n4; ++i) {
+        if (gn4) a[i] = (float)gn4[i];
+        if (c4) b[i] = (float)c4[i];
+    }
+    for (int64_t i = 0; i < n3; ++i) {
+        if (gn3) c[i] = (float)gn3[i];
+        if (c3) d[i] = (float)c3[i];
+    }
+    if (n4) {
+        CK(cudaMemcpy(ctx->gn4.p, a.data(), n4 * 4, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(ctx->cnt4.p, b.data(), n4 * 4, cudaMemcpyHostToDevice));
+        CK(cudaMemset(ctx->dgn4, 0, n4 * 4));
+        CK(cudaMemset(ctx->dcnt4, 0, n4 * 4));
+    }
+    if (n3) {
+        CK(cudaMemcpy(ctx->gn3.p, c.data(), n3 * 4, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(ctx->cnt3.p, d.data(), n3 * 4, cudaMemcpyHostToDevice));
+        CK(cudaMemset(ctx->dgn3, 0, n3 * 4));
+        CK(cudaMemset(ctx->dcnt3, 0, n3 * 4));
+    }
     return HGS_OK;
 }
 
@@ -958,7 +1009,8 @@ hgs_status hgs_train_step_host(hgs_ctx* ctx, int n_views, const hgs_camera* cams
 
 }  // extern "C"
 
-// GradAccum::skipped_nonfinite of the device state (checkpoint.cu)
+// GradAccum::skipped_nonfinite of the device state (checkpoint.cu, and the
+// C ABI's hgs_skipped_nonfinite)
 hgs_status hgs_skipped_total(hgs_ctx* ctx, uint64_t* get, const uint64_t* set) {
     hgs_status r = ensure_scratch(ctx);
     if (r != HGS_OK) return r;
@@ -975,4 +1027,9 @@ hgs_status hgs_skipped_total(hgs_ctx* ctx, uint64_t* get, const uint64_t* set) {
         *get = v;
     }
     return HGS_OK;
+}
+
+extern "C" hgs_status hgs_skipped_nonfinite(hgs_ctx* ctx, uint64_t* get, const uint64_t* set) {
+    if (!ctx) return HGS_ERR_INVALID_ARGUMENT;
+    return hgs_skipped_total(ctx, get, set);
 }
