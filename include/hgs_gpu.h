@@ -449,6 +449,8 @@ hgs_status hgs_debug_instance_masks(hgs_ctx *ctx, uint8_t *masks, int64_t cap, i
 /* The rasterizers walk the exactly-culled instance list; keeping the
  * reference's complete list for hgs_debug_instances costs an extra sort. */
 hgs_status hgs_debug_keep_instances(hgs_ctx *ctx, int enable);
+/* Test hook: instance capacity of the next hgs_render_sweep frames. */
+hgs_status hgs_debug_set_sweep_capacity(hgs_ctx *ctx, int64_t capacity);
 
 #ifdef __cplusplus
 }

@@ -1037,6 +1037,14 @@ hgs_status hgs_debug_splats(hgs_ctx* ctx, int32_t* gid, uint32_t* depth_bits, in
 
 // Keep the reference's complete tile-sorted instance list on subsequent
 // renders (an extra sort of every instance; parity tests only).
+// Test hook: the instance capacity the next hgs_render_sweep frames are
+// launched with (0 = learn it from a synchronous first frame).
+hgs_status hgs_debug_set_sweep_capacity(hgs_ctx* ctx, int64_t capacity) {
+    if (!ctx || capacity < 0 || capacity > INT32_MAX / 2) return HGS_ERR_INVALID_ARGUMENT;
+    ctx->icap = (uint32_t)capacity;
+    return HGS_OK;
+}
+
 hgs_status hgs_debug_keep_instances(hgs_ctx* ctx, int enable) {
     if (!ctx) return HGS_ERR_INVALID_ARGUMENT;
     ctx->debug_full_list = enable != 0;

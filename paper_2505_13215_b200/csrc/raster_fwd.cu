@@ -278,6 +278,15 @@ __device__ __forceinline__ uint32_t dup_warp_incl_scan(uint32_t v) {
     return v;
 }
 
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
 // Duplication fused with the exact culling compaction: each CTA claims the
 // next 1024-instance tile in order (atomic counter), evaluates its instances
 // (4 consecutive per thread), block-scans the keep flags, obtains the number
@@ -345,19 +354,25 @@ __global__ void __launch_bounds__(kDupThreads) duplicate_compact_kernel(
     }
     const uint32_t ex = wbase + incl - nk;
     if (threadIdx.x < 32) {
-        // warp 0: publish the aggregate, look back 32 predecessors at a time
-        volatile unsigned long long* st = status;
+        // warp 0: publish the aggregate, look back 32 predecessors at a time.
+        // Memory model: each status word carries its own payload (flag << 32 |
+        // count) in one aligned 64-bit relaxed gpu-scope access -- single-copy
+        // atomic, so a reader sees either 0 or a complete (flag, count); no
+        // other data is published through it, so no acquire / release pairing
+        // is needed.  Progress: tiles are claimed in launch order by the
+        // atomic counter, so every predecessor is resident or finished.
+        unsigned long long* st = status;
         uint32_t excl = 0;
         if (tile > 0) {
-            if (lane == 0) st[tile] = (1ull << 32) | tot;
+            if (lane == 0) st_relaxed_u64(st + tile, (1ull << 32) | tot);
             int hi = tile - 1;
             while (true) {
                 const int p = hi - lane;
-                unsigned long long w = p >= 0 ? st[p] : (2ull << 32);
+                unsigned long long w = p >= 0 ? ld_relaxed_u64(st + p) : (2ull << 32);
                 uint32_t flag = (uint32_t)(w >> 32);
                 while (__any_sync(0xffffffffu, flag == 0u)) {
                     if (flag == 0u) {
-                        w = st[p];
+                        w = ld_relaxed_u64(st + p);
                         flag = (uint32_t)(w >> 32);
                     }
                 }
@@ -372,8 +387,7 @@ __global__ void __launch_bounds__(kDupThreads) duplicate_compact_kernel(
             }
         }
         if (lane == 0) {
-            __threadfence();
-            st[tile] = (2ull << 32) | (excl + tot);
+            st_relaxed_u64(st + tile, (2ull << 32) | (excl + tot));
             s_excl = excl;
             if (i_end >= I) *kept_total = excl + tot;
         }

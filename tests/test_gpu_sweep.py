@@ -77,3 +77,40 @@ def test_sweep_device_output_and_errors(ctx):
     ctx.upload(bad)
     with pytest.raises(ValueError, match="quaternion"):
         ctx.render_sweep(cams, ts, (0, 0, 0))
+
+
+def test_sweep_overflow_inside_the_last_duplication_block(ctx):
+    """A capacity that is not a multiple of the 1024-instance duplication
+    block, overflowed by a frame whose instances still fit in that last block
+    (capacity < I <= blocks * 1024): the last block must bound its splat range
+    by its nominal end -- the frame is flagged, redone exactly."""
+    scene = synthetic_scene(30000, 10000, sh_degree=1, seed=12).as_float32_exact()
+    ctx.upload(scene)
+    cam = ring_camera(12, 320, 240, index=2, n_ring=6)
+    ref, _ = per_frame(ctx, [cam], [0.5], (0, 0, 0))
+    ctx.render(cam, 0.5, (0, 0, 0))
+    n_inst = ctx.render_info()["instances"]
+    cap = n_inst - 1
+    if cap % 1024 == 0:
+        cap -= 1
+    assert cap % 1024 != 0 and -(-cap // 1024) * 1024 >= n_inst > cap
+    before = ctx.render_info()["sweep_redone_frames"]
+    for _ in range(3):
+        ctx._check(ctx._lib.hgs_debug_set_sweep_capacity(ctx.handle, cap))
+        got = ctx.render_sweep([cam, cam], [0.5, 0.5], (0, 0, 0), out="host")
+        assert np.array_equal(got[0], ref[0]) and np.array_equal(got[1], ref[0])
+    assert ctx.render_info()["sweep_redone_frames"] >= before + 3
+
+
+def test_repeated_sweeps_are_bit_identical(ctx):
+    """The fused duplication (decoupled look-back across CTAs) and the
+    atomics-free forward give the same bits on every run: 40 frames of one
+    view in one sweep, twice, against one per-frame render."""
+    scene = synthetic_scene(100000, 0, sh_degree=3, seed=1).as_float32_exact()
+    ctx.upload(scene)
+    cam = ring_camera(1, 640, 480, index=0, n_ring=16)
+    ref, ref_stats = per_frame(ctx, [cam], [0.5], (0.2, 0.2, 0.2))
+    for _ in range(2):
+        got, stats = ctx.render_sweep([cam] * 40, [0.5] * 40, (0.2, 0.2, 0.2), out="host", with_stats=True)
+        assert all(np.array_equal(g, ref[0]) for g in got)
+        assert all(s == ref_stats[0] for s in stats)
