@@ -146,6 +146,7 @@ _SIGS = {
     "hgs_render_info_get": ([_vp, C.POINTER(RenderInfo)], C.c_int),
     "hgs_set_exact_backward": ([_vp, C.c_int], C.c_int),
     "hgs_debug_set_sweep_capacity": ([_vp, C.c_int64], C.c_int),
+    "hgs_skipped_nonfinite": ([_vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)], C.c_int),
     "hgs_grads_upload": ([_vp, C.POINTER(HostScene), C.c_int], C.c_int),
     "hgs_stats_upload": ([_vp, _dp, _u32p, _dp, _u32p], C.c_int),
     "hgs_debug_splats": ([_vp, _i32p, _u32p, _i32p, _dp, _dp, _dp, _fp, C.c_int64, _i64p], C.c_int),
