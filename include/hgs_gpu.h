@@ -211,6 +211,9 @@ hgs_status hgs_comm_unique_id(hgs_comm_id *out);
 hgs_status hgs_comm_init(hgs_ctx *ctx, int nranks, int rank, const hgs_comm_id *id);
 hgs_status hgs_comm_init_all(hgs_ctx *const *ctxs, int n);
 hgs_status hgs_comm_destroy(hgs_ctx *ctx);
+/* The NCCL the exchange binds (the copy already mapped into the process --
+ * e.g. torch's -- else libnccl.so.2): version code and library path. */
+hgs_status hgs_comm_nccl_info(int *version, char *path, int path_len);
 int hgs_comm_size(hgs_ctx *ctx);
 int hgs_comm_rank(hgs_ctx *ctx);
 hgs_status hgs_allreduce_grads(hgs_ctx *ctx);

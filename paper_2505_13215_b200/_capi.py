@@ -187,6 +187,7 @@ _SIGS = {
     "hgs_comm_init": ([_vp, C.c_int, C.c_int, C.POINTER(CommId)], C.c_int),
     "hgs_comm_init_all": ([C.POINTER(_vp), C.c_int], C.c_int),
     "hgs_comm_destroy": ([_vp], C.c_int),
+    "hgs_comm_nccl_info": ([C.POINTER(C.c_int), C.c_char_p, C.c_int], C.c_int),
     "hgs_comm_size": ([_vp], C.c_int),
     "hgs_comm_rank": ([_vp], C.c_int),
     "hgs_allreduce_grads": ([_vp], C.c_int),

@@ -11,6 +11,7 @@
 // already loaded torch's NCCL shares that copy, a plain C++ caller gets the
 // system one; nothing links NCCL into libhgs_gpu.so.
 #include <dlfcn.h>
+#include <link.h>
 #include <nccl.h>
 
 #include <cstring>
@@ -37,13 +38,36 @@ struct NcclApi {
     ncclResult_t (*GroupStart)() = nullptr;
     ncclResult_t (*GroupEnd)() = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
+    ncclResult_t (*GetVersion)(int*) = nullptr;
+    std::string path;  // the library the symbols came from
 };
+
+// The NCCL already mapped into the process (e.g. torch's bundled copy), so a
+// process holds one NCCL; else the first libnccl.so.2 on the search path.
+int find_loaded_nccl(struct dl_phdr_info* info, size_t, void* out) {
+    const char* n = info->dlpi_name;
+    if (n && std::strstr(n, "libnccl.so")) {
+        *static_cast<std::string*>(out) = n;
+        return 1;
+    }
+    return 0;
+}
 
 NcclApi& nccl() {
     static NcclApi api = [] {
         NcclApi a;
-        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        std::string loaded;
+        dl_iterate_phdr(find_loaded_nccl, &loaded);
+        void* h = loaded.empty() ? nullptr : dlopen(loaded.c_str(), RTLD_NOW | RTLD_NOLOAD);
+        a.path = loaded;
+        if (!h) {
+            h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+            a.path = "libnccl.so.2";
+        }
+        if (!h) {
+            h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+            a.path = "libnccl.so";
+        }
         if (!h) {
             a.err = std::string("NCCL not found: ") + dlerror();
             return a;
@@ -55,7 +79,7 @@ NcclApi& nccl() {
         return a;                                                          \
     }
         SYM(GetUniqueId) SYM(CommInitRank) SYM(CommInitAll) SYM(CommDestroy) SYM(AllReduce) SYM(Broadcast)
-        SYM(GroupStart) SYM(GroupEnd) SYM(GetErrorString)
+        SYM(GroupStart) SYM(GroupEnd) SYM(GetErrorString) SYM(GetVersion)
 #undef SYM
         a.loaded = true;
         return a;
@@ -270,6 +294,17 @@ hgs_status hgs_broadcast_params(hgs_ctx* ctx, int root) {
         CKN(nccl().Broadcast(b->p, b->p, (size_t)ctx->cap3, ncclFloat32, root, c, ctx->stream));
     CKN(nccl().GroupEnd());
     CKC(cudaStreamSynchronize(ctx->stream));
+    return HGS_OK;
+}
+
+// The NCCL the exchange uses: its version code (ncclGetVersion) and path.
+hgs_status hgs_comm_nccl_info(int* version, char* path, int path_len) {
+    if (!nccl().loaded) return HGS_ERR_CUDA;
+    if (version && nccl().GetVersion(version) != ncclSuccess) return HGS_ERR_CUDA;
+    if (path && path_len > 0) {
+        std::strncpy(path, nccl().path.c_str(), (size_t)path_len - 1);
+        path[path_len - 1] = 0;
+    }
     return HGS_OK;
 }
 

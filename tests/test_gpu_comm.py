@@ -143,3 +143,23 @@ def test_pipelined_exchange_single_rank(tmp_path):
             assert np.isfinite(vp.collect())
     finally:
         dist.destroy_process_group()
+
+
+def test_exchange_binds_the_process_nccl():
+    """In a process where torch.distributed already mapped its NCCL, the
+    library's exchange binds that same copy (one NCCL per process)."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2505_13215_b200 import _capi
+
+    torch.cuda.init()
+    import torch.distributed  # noqa: F401  (maps torch's libnccl)
+
+    ver = C.c_int()
+    buf = C.create_string_buffer(512)
+    assert _capi.lib().hgs_comm_nccl_info(C.byref(ver), buf, 512) == 0
+    tv = torch.cuda.nccl.version()
+    tcode = tv[0] * 10000 + tv[1] * 100 + tv[2] if isinstance(tv, tuple) else int(tv)
+    assert ver.value == tcode, (ver.value, tcode, buf.value)
