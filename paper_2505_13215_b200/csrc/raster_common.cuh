@@ -195,6 +195,36 @@ struct SplatBatch {
     }
 };
 
+// The staged batch's splats that warp `warp` (8x8 quadrant (warp & 1,
+// warp >> 1) of the tile) has to walk: quadrant-mask bit set, in batch order,
+// each entry k | (the pixel box covers the whole quadrant) << 8 -- for those
+// the per-pixel box test is known true.  Built by the warp itself from the
+// staged masks (one ballot per 32 splats), so the hot loops run only over
+// their warp's splats without per-splat mask and box bit tests.
+template <int B>
+__device__ __forceinline__ int build_warp_list(const uint32_t* __restrict__ qm, const uint32_t* __restrict__ bm,
+                                               int nb, int warp, uint16_t* __restrict__ list) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t colm = 0xffu << ((warp & 1) * 8), rowm = 0xffu << (16 + (warp >> 1) * 8);
+    const uint32_t lt = (1u << lane) - 1u;
+    int cnt = 0;
+    for (int b = 0; b < nb; b += 32) {
+        const int k = b + lane;
+        bool in = false;
+        uint32_t full = 0u;
+        if (k < nb) {
+            in = (qm[k] >> warp) & 1u;
+            const uint32_t m = bm[k];
+            full = ((m & colm) == colm && (m & rowm) == rowm) ? 1u : 0u;
+        }
+        const uint32_t bal = __ballot_sync(0xffffffffu, in);
+        if (in) list[cnt + __popc(bal & lt)] = (uint16_t)(k | (full << 8));
+        cnt += __popc(bal);
+    }
+    __syncwarp();
+    return cnt;
+}
+
 __device__ __forceinline__ float fast_dx(float pc, float hi, float lo) { return __fsub_rn(__fsub_rn(pc, hi), lo); }
 
 // Shared-memory loads through an explicit 32-bit shared-window address held
@@ -208,6 +238,11 @@ __device__ __forceinline__ uint32_t opaque_u32(uint32_t x) {
 __device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
     uint32_t v;
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
+    unsigned short v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
     return v;
 }
 __device__ __forceinline__ float4 lds_f4(uint32_t a) {

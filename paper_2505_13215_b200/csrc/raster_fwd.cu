@@ -3,6 +3,8 @@
 //
 // Reference: raster.cpp:167-235 (rasterize), 123-148 (composite_pixel),
 // backward.cpp:142-175 (the taped forward, which must match bitwise).
+#include <cstddef>
+
 #include "kernels.cuh"
 
 namespace hgs {
@@ -482,12 +484,18 @@ struct PixFwd {
     bool done, flagged;
 };
 
-// The two pixels of a lane, packed (lo = row y, hi = row y + 4).
+// The two pixels of a lane, packed (lo = row y, hi = row y + 4).  A pixel is
+// finished exactly when T < 1e-4 + 2e-4 err (the certified band's upper edge):
+// T and err change only on contributing pairs, so the test recomputed from
+// the state equals the reference's break (raster.cpp:141-143); the pixel is
+// flagged for the FP64 fix-up when its final T also lies above the band's
+// lower edge.
 struct PixFwd2 {
     f2 T, r, g, b, err;
     uint32_t last0, last1, count0, count1;
-    bool done0, done1, flagged0, flagged1;
 };
+
+__device__ __forceinline__ f2 term_limit(const PixFwd2& s) { return f2_fma(f2_bc(2.0e-4f), s.err, f2_bc(1.0e-4f)); }
 
 // One pair of raster.cpp:132-143 for both pixels given their alphas (p0 / p1
 // = the pixel's pair passes the 1/255 test; a no-op for that pixel
@@ -495,33 +503,23 @@ struct PixFwd2 {
 // whose T lands inside the band around the oracle's T < 1e-4 decision is
 // flagged for the FP64 fix-up.  Per pixel exactly the scalar sequence
 //   w = a T; rgb += c w; err += a eps / (1 - a) + 2.5e-7; T *= 1 - a
+// A is exactly 0 for a pixel whose pair does not contribute (its exponent
+// argument is replaced by 128: ex2.approx.ftz(-128) flushes to +0), so every
+// update below is then exactly the identity (T * 1, err + 0, rgb + c * 0) and
+// no per-pixel selects are needed.
 __device__ __forceinline__ void composite_pairs(PixFwd2& s, bool p0, bool p1, f2 A, f2 EPS, const float4 c,
                                                 uint32_t idx) {
     const f2 AT = f2_mul(A, s.T);
-    const f2 W = f2_pk(p0 ? f2_lo(AT) : 0.0f, p1 ? f2_hi(AT) : 0.0f);
-    s.r = f2_fma(f2_bc(c.x), W, s.r);
-    s.g = f2_fma(f2_bc(c.y), W, s.g);
-    s.b = f2_fma(f2_bc(c.z), W, s.b);
+    s.r = f2_fma(f2_bc(c.x), AT, s.r);
+    s.g = f2_fma(f2_bc(c.y), AT, s.g);
+    s.b = f2_fma(f2_bc(c.z), AT, s.b);
     const f2 OM = f2_sub(f2_bc(1.0f), A);
     const f2 RC = f2_pk(rcp_approx(f2_lo(OM)), rcp_approx(f2_hi(OM)));
-    const f2 EN = f2_fma(f2_mul(A, EPS), RC, f2_add(s.err, f2_bc(2.5e-7f)));
-    s.err = f2_pk(p0 ? f2_lo(EN) : f2_lo(s.err), p1 ? f2_hi(EN) : f2_hi(s.err));
-    const f2 TN = f2_mul(s.T, OM);
-    s.T = f2_pk(p0 ? f2_lo(TN) : f2_lo(s.T), p1 ? f2_hi(TN) : f2_hi(s.T));
+    const f2 P = f2_pk(p0 ? 2.5e-7f : 0.0f, p1 ? 2.5e-7f : 0.0f);
+    s.err = f2_fma(f2_mul(A, EPS), RC, f2_add(s.err, P));
+    s.T = f2_mul(s.T, OM);
     s.last0 = p0 ? idx + 1 : s.last0;
     s.last1 = p1 ? idx + 1 : s.last1;
-    // T and err only change with p, so re-testing an unchanged pixel is a no-op
-    const f2 LIM = f2_fma(f2_bc(2.0e-4f), s.err, f2_bc(1.0e-4f));
-    const f2 LOW = f2_fma(f2_bc(-2.0e-4f), s.err, f2_bc(1.0e-4f));
-    if (f2_lo(s.T) < f2_lo(LIM)) {
-        // inside the certified error band of the oracle's T < 1e-4 decision?
-        if (f2_lo(s.T) > f2_lo(LOW)) s.flagged0 = true;
-        s.done0 = true;
-    }
-    if (f2_hi(s.T) < f2_hi(LIM)) {
-        if (f2_hi(s.T) > f2_hi(LOW)) s.flagged1 = true;
-        s.done1 = true;
-    }
 }
 
 __device__ __forceinline__ void write_pixel(const PixFwd& s, int pix, float bg_r, float bg_g, float bg_b,
@@ -559,6 +557,7 @@ __global__ void __launch_bounds__(kThreads, 6) raster_fwd_kernel(
     uint32_t* __restrict__ fix_count) {
     pdl_wait();  // launched with launch_pdl
     __shared__ SplatBatch<kBatch> sb;
+    __shared__ uint16_t s_list[kThreads / 32][kBatch];  // per-warp splat lists (build_warp_list)
     const int tile = blockIdx.x;
     const int tx = tile % tiles_x, ty = tile / tiles_x;
     // warp w owns the 8x8 quadrant (w & 1, w >> 1); a lane owns rows y, y+4
@@ -576,42 +575,61 @@ __global__ void __launch_bounds__(kThreads, 6) raster_fwd_kernel(
     s.r = s.g = s.b = s.err = f2_bc(0.0f);
     s.last0 = s.last1 = rg.x;
     s.count0 = s.count1 = 0u;
-    s.done0 = !in0;
-    s.done1 = !in1;
-    s.flagged0 = s.flagged1 = false;
     const f2 PYC = f2_pk(pyc0, pyc1);
+    using SB = SplatBatch<kBatch>;
+    const uint32_t sbase = opaque_u32((uint32_t)__cvta_generic_to_shared(&sb));
+    const uint32_t a_bm = sbase + offsetof(SB, bm), a_hdr = sbase + offsetof(SB, hdr),
+                   a_chol = sbase + offsetof(SB, chol), a_col = sbase + offsetof(SB, col),
+                   a_mean = sbase + offsetof(SB, mean), a_j = sbase + offsetof(SB, j);
 
     for (uint32_t base = rg.x; base < rg.y; base += kBatch) {
-        if (__syncthreads_count(!(s.done0 && s.done1)) == 0) break;
+        {
+            const f2 LIM = term_limit(s);
+            const bool act = (in0 && f2_lo(s.T) >= f2_lo(LIM)) || (in1 && f2_hi(s.T) >= f2_hi(LIM));
+            if (__syncthreads_count(act) == 0) break;
+        }
         for (int t = threadIdx.x; t < kBatch; t += kThreads) {
             const uint32_t idx = base + t;
             if (idx < rg.y) sb.load(t, fast, inst_val[idx], tx * kTile, ty * kTile);
         }
         __syncthreads();
         const int nb = min((uint32_t)kBatch, rg.y - base);
-        for (int k = 0; k < nb; ++k) {
-            if (s.done0 && s.done1) break;
-            if (!((sb.qm[k] >> warp) & 1u)) continue;  // exact: no pixel of this quadrant reaches 1/255
-            const int4 hdr = sb.hdr[k];
-            // box test from the staged tile-relative column/row masks
-            const uint32_t bm = sb.bm[k];
-            const bool colin = (bm >> cshift) & 1u;
-            const bool b0 = colin & !s.done0 & ((bm >> rshift0) & 1u);
-            const bool b1 = colin & !s.done1 & ((bm >> rshift1) & 1u);
-            if (!(b0 || b1)) continue;
+        // the splats whose quadrant-mask bit is set for this warp (exact: no
+        // pixel of the quadrant reaches 1/255 otherwise)
+        const int cnt = build_warp_list<kBatch>(sb.qm, sb.bm, nb, warp, s_list[warp]);
+        const uint32_t a_list = opaque_u32((uint32_t)__cvta_generic_to_shared(&s_list[warp][0]));
+        for (int q = 0; q < cnt; ++q) {
+            const f2 LIM = term_limit(s);
+            bool b0 = in0 && f2_lo(s.T) >= f2_lo(LIM), b1 = in1 && f2_hi(s.T) >= f2_hi(LIM);
+            if (!(b0 || b1)) break;  // both pixels finished
+            const uint32_t le = lds_u16(a_list + 2 * q);
+            const int k = (int)(le & 0xffu);
+            const uint32_t o16 = (uint32_t)k << 4, o4 = (uint32_t)k << 2;
+            const int4 hdr = lds_i4(a_hdr + o16);
+            // box test: known true when the box covers the quadrant, else from
+            // the staged tile-relative column/row masks
+            if (!(le >> 8)) {
+                const uint32_t bm = lds_u32(a_bm + o4);
+                const bool colin = (bm >> cshift) & 1u;
+                b0 = b0 & colin & ((bm >> rshift0) & 1u);
+                b1 = b1 & colin & ((bm >> rshift1) & 1u);
+                if (!(b0 || b1)) continue;
+            }
             if (kCount) {
                 s.count0 += b0;
                 s.count1 += b1;
             }
-            const float4 L = sb.chol[k], c = sb.col[k];
-            const SplatRec* e = exact + sb.j[k];
+            const float4 L = lds_f4(a_chol + o16), c = lds_f4(a_col + o16);
+            const SplatRec* e = exact + lds_u32(a_j + o4);
             const float eps_s = __int_as_float(hdr.w);
-            float x0 = INFINITY, x1 = INFINITY;
+            // a pixel outside the box keeps x = 128: finite, so its EPS (and A * EPS
+            // = 0 in composite_pairs) stays finite, and above every x_skip
+            float x0 = 128.0f, x1 = 128.0f;
             if (eps_s < 0.0f) {  // FP64 exponent path (uniform per splat)
                 if (b0) x0 = exact_x(e, pcx, pcy0);
                 if (b1) x1 = exact_x(e, pcx, pcy1);
             } else {  // both pixels share the column: one dx, the rest packed (= fast_x per pixel)
-                const float4 m = sb.mean[k];
+                const float4 m = lds_f4(a_mean + o16);
                 const float dx = __fsub_rn(__fsub_rn(pxc, m.x), m.z);
                 const f2 DY = f2_sub(f2_sub(PYC, f2_bc(m.y)), f2_bc(m.w));
                 const f2 U1 = f2_fma(f2_bc(L.x), f2_bc(dx), f2_mul(f2_bc(L.y), DY));
@@ -635,15 +653,19 @@ __global__ void __launch_bounds__(kThreads, 6) raster_fwd_kernel(
             composite_pairs(s, p0, p1, A, EPS, c, base + k);
         }
     }
+    // flagged: finished inside the certified error band of the T < 1e-4 decision
+    const f2 LIM = term_limit(s), LOW = f2_fma(f2_bc(-2.0e-4f), s.err, f2_bc(1.0e-4f));
+    const bool flag0 = f2_lo(s.T) < f2_lo(LIM) && f2_lo(s.T) > f2_lo(LOW);
+    const bool flag1 = f2_hi(s.T) < f2_hi(LIM) && f2_hi(s.T) > f2_hi(LOW);
     if (in0) {
-        const PixFwd s0{f2_lo(s.T), f2_lo(s.r), f2_lo(s.g), f2_lo(s.b), f2_lo(s.err), s.last0, s.count0, s.done0,
-                        s.flagged0};
+        const PixFwd s0{f2_lo(s.T), f2_lo(s.r), f2_lo(s.g), f2_lo(s.b), f2_lo(s.err), s.last0, s.count0, true,
+                        flag0};
         write_pixel(s0, py0 * W + px, bg_r, bg_g, bg_b, out_rgb, out_last, out_tfinal, out_trans, out_count, fix_list,
                     fix_count);
     }
     if (in1) {
-        const PixFwd s1{f2_hi(s.T), f2_hi(s.r), f2_hi(s.g), f2_hi(s.b), f2_hi(s.err), s.last1, s.count1, s.done1,
-                        s.flagged1};
+        const PixFwd s1{f2_hi(s.T), f2_hi(s.r), f2_hi(s.g), f2_hi(s.b), f2_hi(s.err), s.last1, s.count1, true,
+                        flag1};
         write_pixel(s1, py1 * W + px, bg_r, bg_g, bg_b, out_rgb, out_last, out_tfinal, out_trans, out_count, fix_list,
                     fix_count);
     }
