@@ -120,13 +120,17 @@ __device__ __forceinline__ void backprop_pairs(PixBwd2& s, bool p0, bool p1, f2 
     const f2 GC = f2_fma(s.gr, f2_bc(col.x), f2_fma(s.gg, f2_bc(col.y), f2_mul(s.gb, f2_bc(col.z))));
     const f2 NS = f2_mul(f2_mul(f2_bc(-1.0f), INV), s.GS);  // (-inv) S, exact negation
     const f2 DA = f2_fma(TI, GC, NS);
+    // g (hence a) is exactly 0 for a pixel whose pair does not contribute
+    // (exponent 128: ex2.approx.ftz(-128) flushes to +0), so its w and h are
+    // 0 and its suffix unchanged without selects; only T needs one (T * rcp(1)
+    // is not guaranteed to be T)
     const f2 AT = f2_mul(A, TI);
     const f2 GDA = f2_mul(G, DA);
-    w0 = p0 ? f2_lo(AT) : 0.0f;
-    w1 = p1 ? f2_hi(AT) : 0.0f;
-    h0 = p0 ? f2_lo(GDA) : 0.0f;
-    h1 = p1 ? f2_hi(GDA) : 0.0f;
-    W = f2_pk(w0, w1);
+    w0 = f2_lo(AT);
+    w1 = f2_hi(AT);
+    h0 = f2_lo(GDA);
+    h1 = f2_hi(GDA);
+    W = AT;
     s.GS = f2_fma(W, GC, s.GS);
     s.T = f2_pk(p0 ? f2_lo(TI) : f2_lo(s.T), p1 ? f2_hi(TI) : f2_hi(s.T));
 }
@@ -138,6 +142,7 @@ __global__ void __launch_bounds__(kThreadsB, 7) raster_bwd_kernel(
     acc_t* __restrict__ accum) {
     pdl_wait();  // launched with launch_pdl
     __shared__ SplatBatch<kBatchB> sb;
+    __shared__ uint16_t s_list[kThreadsB / 32][kBatchB];  // per-warp splat lists (build_warp_list)
     __shared__ uint32_t s_maxlast;
     const int tile = blockIdx.x;
     const int tx = tile % tiles_x, ty = tile / tiles_x;
@@ -194,7 +199,7 @@ __global__ void __launch_bounds__(kThreadsB, 7) raster_bwd_kernel(
 
     using SB = SplatBatch<kBatchB>;
     const uint32_t sbase = opaque_u32((uint32_t)__cvta_generic_to_shared(&sb));
-    const uint32_t a_qm = sbase + offsetof(SB, qm), a_bm = sbase + offsetof(SB, bm), a_hdr = sbase + offsetof(SB, hdr),
+    const uint32_t a_bm = sbase + offsetof(SB, bm), a_hdr = sbase + offsetof(SB, hdr),
                    a_chol = sbase + offsetof(SB, chol), a_col = sbase + offsetof(SB, col),
                    a_mean = sbase + offsetof(SB, mean), a_j = sbase + offsetof(SB, j);
     const int nbatch = (int)((end - rg.x + kBatchB - 1) / kBatchB);
@@ -205,18 +210,29 @@ __global__ void __launch_bounds__(kThreadsB, 7) raster_bwd_kernel(
         for (int t = threadIdx.x; t < nb; t += kThreadsB) sb.load(t, fast, inst_val[base + t], tx * kTile, ty * kTile);
         __syncthreads();
         const int kmax = (int)min((uint32_t)nb, warp_end > base ? warp_end - base : 0u);
-        for (int k = kmax - 1; k >= 0; --k) {
-            if (!((lds_u32(a_qm + 4 * k) >> warp) & 1u)) continue;  // exact: no pixel of this quadrant reaches 1/255
-            const int4 hdr = lds_i4(a_hdr + 16 * k);
+        if (kmax == 0) continue;  // (warp-uniform; the next batch's barriers are reached by every warp)
+        // this warp's splats (quadrant-mask bit set: exact, no pixel of the
+        // quadrant reaches 1/255 otherwise), walked back to front below kmax
+        const int cnt = build_warp_list<kBatchB>(sb.qm, sb.bm, kmax, warp, s_list[warp]);
+        const uint32_t a_list = opaque_u32((uint32_t)__cvta_generic_to_shared(&s_list[warp][0]));
+        for (int q = cnt - 1; q >= 0; --q) {
+            const uint32_t le = lds_u16(a_list + 2 * q);
+            const int k = (int)(le & 0xffu);
+            const uint32_t o16 = (uint32_t)k << 4, o4 = (uint32_t)k << 2;
+            const int4 hdr = lds_i4(a_hdr + o16);
             const uint32_t idx = base + k;
-            // box test from the staged tile-relative column/row masks
-            const uint32_t bm = lds_u32(a_bm + 4 * k);
-            const bool colin = (bm >> cshift) & 1u;
-            const bool b0 = colin & (idx < s.last0) & ((bm >> rshift0) & 1u);
-            const bool b1 = colin & (idx < s.last1) & ((bm >> rshift1) & 1u);
+            // box test: known true when the box covers the quadrant, else from
+            // the staged tile-relative column/row masks
+            bool b0 = idx < s.last0, b1 = idx < s.last1;
+            if (!(le >> 8)) {
+                const uint32_t bm = lds_u32(a_bm + o4);
+                const bool colin = (bm >> cshift) & 1u;
+                b0 = b0 & colin & ((bm >> rshift0) & 1u);
+                b1 = b1 & colin & ((bm >> rshift1) & 1u);
+            }
             if (!__any_sync(0xffffffffu, b0 || b1)) continue;
-            const float4 L = lds_f4(a_chol + 16 * k), col = lds_f4(a_col + 16 * k);
-            const uint32_t sj = lds_u32(a_j + 4 * k);
+            const float4 L = lds_f4(a_chol + o16), col = lds_f4(a_col + o16);
+            const uint32_t sj = lds_u32(a_j + o4);
             const SplatRec* e = exact + sj;
             // exponent argument and offset of both pixels (same column: one dx
             // on the fast path, the same rounding sequence as K4's fast_x)
@@ -235,7 +251,7 @@ __global__ void __launch_bounds__(kThreadsB, 7) raster_bwd_kernel(
                     dy1 = d.y;
                 }
             } else {  // both pixels in one packed sequence (= fast_x per pixel)
-                const float4 m = lds_f4(a_mean + 16 * k);
+                const float4 m = lds_f4(a_mean + o16);
                 dx0 = __fsub_rn(__fsub_rn(pxc, m.x), m.z);
                 dx1 = dx0;
                 const f2 DY = f2_sub(f2_sub(PYC, f2_bc(m.y)), f2_bc(m.w));
