@@ -454,6 +454,12 @@ hgs_status hgs_debug_instance_masks(hgs_ctx *ctx, uint8_t *masks, int64_t cap, i
 hgs_status hgs_debug_keep_instances(hgs_ctx *ctx, int enable);
 /* Test hook: instance capacity of the next hgs_render_sweep frames. */
 hgs_status hgs_debug_set_sweep_capacity(hgs_ctx *ctx, int64_t capacity);
+/* Pixel-splat pair counters of the tile rasterizers (checked build
+ * libhgs_gpu_checked.so only; HGS_ERR_STATE in the production library):
+ * out[0..3] = K4 lane-iterations, box-covered pairs (exponent evaluated),
+ * alpha-passing (composited) pairs, warp-iterations; out[4..7] the same for
+ * K6.  reset != 0 zeroes them after the read. */
+hgs_status hgs_debug_pair_counters(hgs_ctx *ctx, unsigned long long out[8], int reset);
 
 #ifdef __cplusplus
 }

@@ -271,6 +271,32 @@ void prof_collect(hgs_ctx* ctx) {
 
 // ====================================================================== render
 // The full K1 -> sort -> K2 -> sort -> K4 pipeline; leaves the tape in ctx.
+namespace hgs {
+#ifdef HGS_CHECKED
+__device__ CheckCaps g_chk;
+__device__ unsigned long long g_pairs[8];
+void set_check_caps(const CheckCaps& caps, cudaStream_t st) {
+    cudaMemcpyToSymbolAsync(g_chk, &caps, sizeof(CheckCaps), 0, cudaMemcpyHostToDevice, st);
+    cudaStreamSynchronize(st);  // (checked builds only) caps is a host temporary
+}
+#else
+void set_check_caps(const CheckCaps&, cudaStream_t) {}
+#endif
+}  // namespace hgs
+
+namespace {
+// Capacities (elements) of the render workspace for the checked build.
+CheckCaps render_caps(const hgs_ctx* ctx, size_t npx, int n_tiles) {
+    CheckCaps c;
+    c.splats = std::min(ctx->rec_sorted.cap / sizeof(SplatRec), ctx->fast_sorted.cap / sizeof(SplatFast));
+    if (ctx->accum.cap) c.splats = std::min<unsigned long long>(c.splats, ctx->accum.cap / (kAccStrideHost * sizeof(acc_t)));
+    c.inst = std::min(std::min(ctx->inst_k.cap, ctx->inst_v.cap), std::min(ctx->inst_k2.cap, ctx->inst_v2.cap)) / 4;
+    c.pixels = npx;
+    c.tiles = (unsigned long long)n_tiles;
+    return c;
+}
+}  // namespace
+
 hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, const double bg[3],
                                const hgs_raster_opts* opts, int deferred, uint32_t icap, void* counters_slot,
                                const ZeroJobs* extra) {
@@ -410,6 +436,9 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
         CK(ctx->inst_v.ensure((size_t)I * 4));
         CK(ctx->inst_k2.ensure((size_t)I * 4));
         CK(ctx->inst_v2.ensure((size_t)I * 4));
+#ifdef HGS_CHECKED
+        set_check_caps(render_caps(ctx, npx, n_tiles), st);
+#endif
         const int cull = want_count ? 0 : 1;  // count_map counts every box-covered splat
         const uint32_t dup_blocks = div_up((uint32_t)I, kDupPerCtaHost);
         CK(ctx->dup_first.ensure((size_t)(dup_blocks + 1) * 4));
@@ -527,6 +556,9 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
         }
     }
     ctx->inst_vals_final = inst_vals;
+#ifdef HGS_CHECKED
+    set_check_caps(render_caps(ctx, npx, n_tiles), st);
+#endif
     prof_begin(ctx, PH_RASTER_FWD);
     launch_raster_fwd(
         want_count, n_tiles, st, ctx->ranges.as<uint2>(), inst_vals, ctx->fast_sorted.as<SplatFast>(), ctx->rec_sorted.as<SplatRec>(), W, H,
@@ -1043,6 +1075,21 @@ hgs_status hgs_debug_set_sweep_capacity(hgs_ctx* ctx, int64_t capacity) {
     if (!ctx || capacity < 0 || capacity > INT32_MAX / 2) return HGS_ERR_INVALID_ARGUMENT;
     ctx->icap = (uint32_t)capacity;
     return HGS_OK;
+}
+
+hgs_status hgs_debug_pair_counters(hgs_ctx* ctx, unsigned long long out[8], int reset) {
+    if (!ctx || !out) return HGS_ERR_INVALID_ARGUMENT;
+#ifdef HGS_CHECKED
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaMemcpyFromSymbol(out, g_pairs, 8 * sizeof(unsigned long long)));
+    if (reset) {
+        const unsigned long long z[8] = {};
+        CK(cudaMemcpyToSymbol(g_pairs, z, sizeof(z)));
+    }
+    return HGS_OK;
+#else
+    return fail(ctx, HGS_ERR_STATE, "pair counters exist in the checked build only (libhgs_gpu_checked.so)");
+#endif
 }
 
 hgs_status hgs_debug_keep_instances(hgs_ctx* ctx, int enable) {

@@ -335,6 +335,7 @@ __device__ __forceinline__ void gaussian_bwd_body(
     if (gid >= N) return;
     const uint32_t j = sorted_of_gid[gid];
     if (j == 0xffffffffu) return;  // not visible in this view
+    HGS_DCHECK(j < g_chk.splats);
     const acc_t* acc = accum + (size_t)j * acc_stride;
     double av[9];
 #pragma unroll
@@ -462,6 +463,7 @@ __global__ void __launch_bounds__(128) sh_bwd_kernel(int N, const uint32_t* __re
     if (gid >= N) return;
     const uint32_t j = sorted_of_gid[gid];
     if (j == 0xffffffffu) return;  // not visible in this view
+    HGS_DCHECK(j < g_chk.splats);
     const acc_t* acc = accum + (size_t)j * acc_stride;
     const double2 a01 = *reinterpret_cast<const double2*>(acc), a23 = *reinterpret_cast<const double2*>(acc + 2),
                   a45 = *reinterpret_cast<const double2*>(acc + 4), a67 = *reinterpret_cast<const double2*>(acc + 6);

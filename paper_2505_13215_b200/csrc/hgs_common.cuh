@@ -11,6 +11,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
 
 namespace hgs {
@@ -84,6 +85,38 @@ enum : uint32_t {
 };
 
 inline __host__ __device__ uint32_t div_up(uint32_t a, uint32_t b) { return (a + b - 1) / b; }
+
+// ---- checked build (make CHECKED=1 -> libhgs_gpu_checked.so, -rdc): device-side
+// bounds asserts on the indices of the hot kernels against the capacities of
+// the current render's buffers (set by the host before each render chain).
+// The substitute for compute-sanitizer, which this GPU pool does not allow.
+struct CheckCaps {
+    unsigned long long splats;  // sorted-splat / per-Gaussian record buffers (elements)
+    unsigned long long inst;    // instance key/value buffers (elements)
+    unsigned long long pixels;  // image-sized buffers (pixels)
+    unsigned long long tiles;   // tile ranges
+};
+#ifdef HGS_CHECKED
+extern __device__ CheckCaps g_chk;
+extern __device__ unsigned long long g_pairs[8];  // hgs_debug_pair_counters
+#define HGS_COUNT_PAIRS(slot, v) atomicAdd(&g_pairs[slot], (unsigned long long)(v))
+#define HGS_DCHECK(c)                                                                                 \
+    do {                                                                                              \
+        if (!(c)) {                                                                                   \
+            printf("HGS_CHECKED %s:%d block %d thread %d: %s\n", __FILE__, __LINE__, (int)blockIdx.x, \
+                   (int)threadIdx.x, #c);                                                             \
+            __trap();                                                                                 \
+        }                                                                                             \
+    } while (0)
+#else
+#define HGS_COUNT_PAIRS(slot, v) \
+    do {                         \
+    } while (0)
+#define HGS_DCHECK(c) \
+    do {              \
+    } while (0)
+#endif
+void set_check_caps(const CheckCaps& caps, cudaStream_t st);  // capi.cu (no-op unless HGS_CHECKED)
 
 }  // namespace hgs
 

@@ -127,6 +127,7 @@ __global__ void __launch_bounds__(kCoopThreads) radix_sort_coop_kernel(CoopSort 
     __shared__ uint32_t goff[256];
     const int G = gridDim.x, b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n = a.n_dev ? (int)*a.n_dev : a.n;
+    HGS_DCHECK(!a.n_dev || n <= a.n);
     const int C = ((n + G - 1) / G + 31) & ~31;
     const int lo = min(b * C, n), hi = min(lo + C, n);
     const unsigned lt_mask = (1u << lane) - 1u;
@@ -161,13 +162,18 @@ __global__ void __launch_bounds__(kCoopThreads) radix_sort_coop_kernel(CoopSort 
             const uint32_t base = block_excl_scan(a.rowsum[tid], tot);
             goff[tid] = base + a.hist[tid * G + b];
         }
-        for (int t0 = lo; t0 < hi; t0 += kTileItems) {
+        // rounds per warp: a chunk smaller than a full 4096-item tile is spread
+        // over all 8 warps (R rounds of 32 consecutive items each) instead of
+        // 16 serial rounds on the first warps
+        const int R = min(kItems, max(1, (hi - lo + kCoopThreads - 1) / kCoopThreads));
+        for (int t0 = lo; t0 < hi; t0 += R * kCoopThreads) {
             for (int i = tid; i < kWarps * 256; i += kCoopThreads) (&cnt[0][0])[i] = 0u;
             __syncthreads();
-            const int wbase = t0 + warp * (kItems * 32);
+            const int wbase = t0 + warp * (R * 32);
             uint32_t k[kItems], v[kItems], rank[kItems];
 #pragma unroll
             for (int r = 0; r < kItems; ++r) {
+                if (r >= R) break;
                 const int idx = wbase + r * 32 + lane;
                 const bool valid = idx < hi;
                 k[r] = valid ? ki[idx] : 0u;
@@ -191,10 +197,12 @@ __global__ void __launch_bounds__(kCoopThreads) radix_sort_coop_kernel(CoopSort 
             __syncthreads();
 #pragma unroll
             for (int r = 0; r < kItems; ++r) {
+                if (r >= R) break;
                 const int idx = wbase + r * 32 + lane;
                 if (idx < hi) {
                     const uint32_t d = (k[r] >> shift) & 255u;
                     const uint32_t pos = goff[d] + cnt[warp][d] + rank[r];
+                    HGS_DCHECK(pos < (uint32_t)n);
                     ko[pos] = k[r];
                     vo[pos] = v[r];
                 }

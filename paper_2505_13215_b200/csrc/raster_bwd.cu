@@ -150,7 +150,9 @@ __global__ void __launch_bounds__(kThreadsB, 7) raster_bwd_kernel(
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int px = tx * kTile + (warp & 1) * 8 + (lane & 7);
     const int py0 = ty * kTile + (warp >> 1) * 8 + (lane >> 3), py1 = py0 + 4;
+    HGS_DCHECK((unsigned long long)tile < g_chk.tiles);
     const uint2 rg = ranges[tile];
+    HGS_DCHECK(rg.x <= rg.y && rg.y <= g_chk.inst);
     const float pxc = (float)px + 0.5f, pyc0 = (float)py0 + 0.5f, pyc1 = (float)py1 + 0.5f;
     const double pcx = (double)px + 0.5, pcy0 = (double)py0 + 0.5, pcy1 = (double)py1 + 0.5;
 
@@ -195,6 +197,7 @@ __global__ void __launch_bounds__(kThreadsB, 7) raster_bwd_kernel(
     if (ml > rg.x) atomicMax(&s_maxlast, ml);
     __syncthreads();
     const uint32_t end = s_maxlast;
+    HGS_DCHECK(end >= rg.x && end <= rg.y);
     const uint32_t warp_end = __reduce_max_sync(0xffffffffu, ml);  // nothing past it in this warp
 
     using SB = SplatBatch<kBatchB>;
@@ -203,6 +206,9 @@ __global__ void __launch_bounds__(kThreadsB, 7) raster_bwd_kernel(
                    a_chol = sbase + offsetof(SB, chol), a_col = sbase + offsetof(SB, col),
                    a_mean = sbase + offsetof(SB, mean), a_j = sbase + offsetof(SB, j);
     const int nbatch = (int)((end - rg.x + kBatchB - 1) / kBatchB);
+#ifdef HGS_CHECKED
+    unsigned long long n_it = 0, n_box = 0, n_pass = 0, n_wit = 0;
+#endif
     for (int bi = nbatch - 1; bi >= 0; --bi) {
         const uint32_t base = rg.x + (uint32_t)bi * kBatchB;
         const int nb = (int)min((uint32_t)kBatchB, end - base);
@@ -231,8 +237,14 @@ __global__ void __launch_bounds__(kThreadsB, 7) raster_bwd_kernel(
                 b1 = b1 & colin & ((bm >> rshift1) & 1u);
             }
             if (!__any_sync(0xffffffffu, b0 || b1)) continue;
+#ifdef HGS_CHECKED
+            ++n_it;
+            n_box += (int)b0 + (int)b1;
+            if (lane == 0) ++n_wit;
+#endif
             const float4 L = lds_f4(a_chol + o16), col = lds_f4(a_col + o16);
             const uint32_t sj = lds_u32(a_j + o4);
+            HGS_DCHECK(sj < g_chk.splats);
             const SplatRec* e = exact + sj;
             // exponent argument and offset of both pixels (same column: one dx
             // on the fast path, the same rounding sequence as K4's fast_x)
@@ -274,6 +286,9 @@ __global__ void __launch_bounds__(kThreadsB, 7) raster_bwd_kernel(
             // lanes without a contributing pixel hold zeros; skip the
             // reduction when the whole warp is empty
             if (!__any_sync(0xffffffffu, p0 || p1)) continue;
+#ifdef HGS_CHECKED
+            n_pass += (int)p0 + (int)p1;
+#endif
             const float g0 = fast_exp2_neg(p0 ? x0 : 128.0f), g1 = fast_exp2_neg(p1 ? x1 : 128.0f);
             float w0, h0, w1, h1;
             f2 Wp;
@@ -304,6 +319,12 @@ __global__ void __launch_bounds__(kThreadsB, 7) raster_bwd_kernel(
             }
         }
     }
+#ifdef HGS_CHECKED
+    HGS_COUNT_PAIRS(4, n_it);
+    HGS_COUNT_PAIRS(5, n_box);
+    HGS_COUNT_PAIRS(6, n_pass);
+    HGS_COUNT_PAIRS(7, n_wit);
+#endif
 }
 
 // FP64 backward of the fix-up pixels (backward.cpp:182-221), one warp per
@@ -325,11 +346,13 @@ __global__ void __launch_bounds__(128) raster_bwd_exact_kernel(
     const uint32_t warps = gridDim.x * (blockDim.x >> 5);
     for (uint32_t q = blockIdx.x * (blockDim.x >> 5) + wib; q < n; q += warps) {
         const int pix = fix_list ? (int)fix_list[q] : (int)q;
+        HGS_DCHECK(pix >= 0 && (unsigned long long)pix < g_chk.pixels);
         const double gp[3] = {dL_dimg[pix * 3], dL_dimg[pix * 3 + 1], dL_dimg[pix * 3 + 2]};
         if (fabs(gp[0]) <= 1e-12 && fabs(gp[1]) <= 1e-12 && fabs(gp[2]) <= 1e-12) continue;  // isZero, backward.cpp:189
         const int px = pix % W, py = pix / W;
         const uint2 rg = ranges[(py / kTile) * tiles_x + px / kTile];
         const uint32_t last = last_arr[pix] & 0x7fffffffu;
+        HGS_DCHECK(rg.x <= rg.y && rg.y <= g_chk.inst && last <= rg.y);
         const double pcx = px + 0.5, pcy = py + 0.5;
         double Cout[3];
         for (int pass = 0; pass < 2; ++pass) {

@@ -176,6 +176,7 @@ struct SplatBatch {
     // (ox, oy): the tile's first pixel
     __device__ __forceinline__ void load(int t, const SplatFast* __restrict__ fast, uint32_t v, int ox, int oy) {
         const uint32_t jj = v & kInstIndexMask;
+        HGS_DCHECK(t < B && jj < g_chk.splats);
         qm[t] = v >> kInstMaskShift;
         const float4* src = reinterpret_cast<const float4*>(fast + jj);
         const float4 a = __ldg(src + 0), b = __ldg(src + 1), c = __ldg(src + 2), d = __ldg(src + 3);
@@ -222,6 +223,7 @@ __device__ __forceinline__ int build_warp_list(const uint32_t* __restrict__ qm, 
         cnt += __popc(bal);
     }
     __syncwarp();
+    HGS_DCHECK(cnt <= nb && nb <= B);
     return cnt;
 }
 
@@ -326,12 +328,14 @@ __device__ __forceinline__ void exact_chunk(const uint32_t* __restrict__ inst_va
 #pragma unroll
     for (int s = 0; s < S; ++s) {
         const uint32_t i = base + 32 * s + lane;
+        HGS_DCHECK(i >= end || i < g_chk.inst);
         v[s] = i < end ? inst_val[i] : 0xffffffffu;
     }
     double om[S];
     bool ok[S];
 #pragma unroll
     for (int s = 0; s < S; ++s) {
+        HGS_DCHECK(v[s] == 0xffffffffu || (v[s] & kInstIndexMask) < g_chk.splats);
         c.e[s] = v[s] != 0xffffffffu ? exact + (v[s] & kInstIndexMask) : nullptr;
         c.a[s] = -1.0;
         c.g[s] = 0.0;

@@ -243,6 +243,7 @@ __device__ __forceinline__ void dup_instance(int i, const uint32_t* s_off, int c
                                              const CullRec* __restrict__ cull_rec, int tiles_x, uint32_t& key,
                                              uint32_t& val) {
     const int jl = last_le(s_off, 0, cnt - 1, (uint32_t)i);
+    HGS_DCHECK(jl >= 0 && jl < cnt);
     const int j = j_lo + jl;
     const int32_t xr = __ldg(&fast[j].xr), yr = __ldg(&fast[j].yr);
     const int x0 = box_x0(xr), x1 = x0 + box_w(xr), y0 = box_x0(yr), y1 = y0 + box_w(yr);
@@ -329,6 +330,7 @@ __global__ void __launch_bounds__(kDupThreads) duplicate_compact_kernel(
     // capacity, but dup_bounds_kernel wrote only the boundaries below I_all
     const int j_hi = (tile + 1) * kDupPerCta < I_all ? (int)cta_first[tile + 1] : V - 1;
     const int cnt = min(j_hi - j_lo + 1, kDupPerCta + 1);  // a CTA spans at most kDupPerCta + 1 splats
+    HGS_DCHECK(j_lo >= 0 && cnt >= 1 && j_lo + cnt <= V && (unsigned long long)V <= g_chk.splats);
     for (int k = threadIdx.x; k < cnt; k += kDupThreads) s_off[k] = __ldg(&offsets[j_lo + k]);
     __syncthreads();
     constexpr int kPer = kDupPerCta / kDupThreads;  // 4 consecutive instances per thread
@@ -399,6 +401,7 @@ __global__ void __launch_bounds__(kDupThreads) duplicate_compact_kernel(
 #pragma unroll
     for (int k = 0; k < kPer; ++k)
         if (val[k] >> kInstMaskShift) {
+            HGS_DCHECK(pos < (uint32_t)I && (unsigned long long)I <= g_chk.inst);
             keys_out[pos] = key[k];
             vals_out[pos] = val[k];
             ++pos;
@@ -484,29 +487,33 @@ struct PixFwd {
     bool done, flagged;
 };
 
-// The two pixels of a lane, packed (lo = row y, hi = row y + 4).  A pixel is
-// finished exactly when T < 1e-4 + 2e-4 err (the certified band's upper edge):
-// T and err change only on contributing pairs, so the test recomputed from
-// the state equals the reference's break (raster.cpp:141-143); the pixel is
+// The two pixels of a lane, packed (lo = row y, hi = row y + 4).  E is the
+// certified ABSOLUTE error bound of T (|T_fp32 - T_oracle| <= E).  A pixel is
+// finished exactly when T < 1e-4 + 2E (the certified band's upper edge): T
+// and E change only on contributing pairs, so the test recomputed from the
+// state equals the reference's break (raster.cpp:141-143); the pixel is
 // flagged for the FP64 fix-up when its final T also lies above the band's
-// lower edge.
+// lower edge 1e-4 - 2E.
 struct PixFwd2 {
-    f2 T, r, g, b, err;
+    f2 T, r, g, b, E;
     uint32_t last0, last1, count0, count1;
 };
 
-__device__ __forceinline__ f2 term_limit(const PixFwd2& s) { return f2_fma(f2_bc(2.0e-4f), s.err, f2_bc(1.0e-4f)); }
+__device__ __forceinline__ f2 term_limit(const PixFwd2& s) { return f2_fma(f2_bc(2.0f), s.E, f2_bc(1.0e-4f)); }
 
 // One pair of raster.cpp:132-143 for both pixels given their alphas (p0 / p1
 // = the pixel's pair passes the 1/255 test; a no-op for that pixel
-// otherwise).  err tracks the certified relative error bound of T; a pixel
-// whose T lands inside the band around the oracle's T < 1e-4 decision is
-// flagged for the FP64 fix-up.  Per pixel exactly the scalar sequence
-//   w = a T; rgb += c w; err += a eps / (1 - a) + 2.5e-7; T *= 1 - a
-// A is exactly 0 for a pixel whose pair does not contribute (its exponent
-// argument is replaced by 128: ex2.approx.ftz(-128) flushes to +0), so every
-// update below is then exactly the identity (T * 1, err + 0, rgb + c * 0) and
-// no per-pixel selects are needed.
+// otherwise).  Per pixel exactly the scalar sequence
+//   w = a T; rgb += c w; T' = T (1 - a); E' = E (1 - a) + w eps + 2.5e-7 T'
+// The error bound: with a_f = a (1 + d), |d| <= eps, and two roundings in
+// fl(T fl(1 - a_f)),  T' - T'_oracle = (T - T_oracle)(1 - a) - T a d + 2u T',
+// so E' above bounds it (2.5e-7 > 2u (1 + u) with u = 2^-24; the (1 - a_f)
+// vs (1 - a) factor on E and E's own FP32 rounding are second order, inside
+// that margin) -- the relative bound err of the earlier form times T, without
+// its division by 1 - a.  A is exactly 0 for a pixel whose pair does not
+// contribute (its exponent argument is replaced by 128: ex2.approx.ftz(-128)
+// flushes to +0), so the updates are then exactly the identity (T * 1,
+// E * 1 + 0 + 0, rgb + c * 0); only the rounding term needs the pass flag.
 __device__ __forceinline__ void composite_pairs(PixFwd2& s, bool p0, bool p1, f2 A, f2 EPS, const float4 c,
                                                 uint32_t idx) {
     const f2 AT = f2_mul(A, s.T);
@@ -514,10 +521,10 @@ __device__ __forceinline__ void composite_pairs(PixFwd2& s, bool p0, bool p1, f2
     s.g = f2_fma(f2_bc(c.y), AT, s.g);
     s.b = f2_fma(f2_bc(c.z), AT, s.b);
     const f2 OM = f2_sub(f2_bc(1.0f), A);
-    const f2 RC = f2_pk(rcp_approx(f2_lo(OM)), rcp_approx(f2_hi(OM)));
-    const f2 P = f2_pk(p0 ? 2.5e-7f : 0.0f, p1 ? 2.5e-7f : 0.0f);
-    s.err = f2_fma(f2_mul(A, EPS), RC, f2_add(s.err, P));
-    s.T = f2_mul(s.T, OM);
+    const f2 TN = f2_mul(s.T, OM);
+    const f2 U = f2_pk(p0 ? 2.5e-7f : 0.0f, p1 ? 2.5e-7f : 0.0f);
+    s.E = f2_fma(s.E, OM, f2_fma(AT, EPS, f2_mul(TN, U)));
+    s.T = TN;
     s.last0 = p0 ? idx + 1 : s.last0;
     s.last1 = p1 ? idx + 1 : s.last1;
 }
@@ -527,7 +534,7 @@ __device__ __forceinline__ void write_pixel(const PixFwd& s, int pix, float bg_r
                                             float* __restrict__ out_tfinal, float* __restrict__ out_trans,
                                             uint32_t* __restrict__ out_count, uint32_t* __restrict__ fix_list,
                                             uint32_t* __restrict__ fix_count) {
-    const bool flagged = s.flagged || (g_debug_exact & 2) || s.err > g_debug_terr;
+    const bool flagged = s.flagged || (g_debug_exact & 2) || s.err > g_debug_terr * s.T;
     out_rgb[pix * 3 + 0] = fmaf(s.T, bg_r, s.r);
     out_rgb[pix * 3 + 1] = fmaf(s.T, bg_g, s.g);
     out_rgb[pix * 3 + 2] = fmaf(s.T, bg_b, s.b);
@@ -565,17 +572,22 @@ __global__ void __launch_bounds__(kThreads, 6) raster_fwd_kernel(
     const int px = tx * kTile + (warp & 1) * 8 + (lane & 7);
     const int py0 = ty * kTile + (warp >> 1) * 8 + (lane >> 3), py1 = py0 + 4;
     const bool in0 = px < W && py0 < H, in1 = px < W && py1 < H;
+    HGS_DCHECK((unsigned long long)tile < g_chk.tiles);
     const uint2 rg = ranges[tile];
+    HGS_DCHECK(rg.x <= rg.y && rg.y <= g_chk.inst);
     const float pxc = (float)px + 0.5f, pyc0 = (float)py0 + 0.5f, pyc1 = (float)py1 + 0.5f;
     const double pcx = (double)px + 0.5, pcy0 = (double)py0 + 0.5, pcy1 = (double)py1 + 0.5;
 
     const int cshift = px - tx * kTile, rshift0 = 16 + py0 - ty * kTile, rshift1 = rshift0 + 4;
     PixFwd2 s;
     s.T = f2_bc(1.0f);
-    s.r = s.g = s.b = s.err = f2_bc(0.0f);
+    s.r = s.g = s.b = s.E = f2_bc(0.0f);
     s.last0 = s.last1 = rg.x;
     s.count0 = s.count1 = 0u;
     const f2 PYC = f2_pk(pyc0, pyc1);
+#ifdef HGS_CHECKED
+    unsigned long long n_it = 0, n_box = 0, n_pass = 0, n_wit = 0;
+#endif
     using SB = SplatBatch<kBatch>;
     const uint32_t sbase = opaque_u32((uint32_t)__cvta_generic_to_shared(&sb));
     const uint32_t a_bm = sbase + offsetof(SB, bm), a_hdr = sbase + offsetof(SB, hdr),
@@ -598,10 +610,18 @@ __global__ void __launch_bounds__(kThreads, 6) raster_fwd_kernel(
         // pixel of the quadrant reaches 1/255 otherwise)
         const int cnt = build_warp_list<kBatch>(sb.qm, sb.bm, nb, warp, s_list[warp]);
         const uint32_t a_list = opaque_u32((uint32_t)__cvta_generic_to_shared(&s_list[warp][0]));
+#ifdef HGS_CHECKED
+        n_wit += cnt;  // upper bound: the warp's list (lanes may finish earlier)
+#endif
+        // control flow is warp-uniform (votes): a lane whose pixels finished
+        // keeps walking with b0 = b1 = false (A = 0: no state change)
         for (int q = 0; q < cnt; ++q) {
             const f2 LIM = term_limit(s);
             bool b0 = in0 && f2_lo(s.T) >= f2_lo(LIM), b1 = in1 && f2_hi(s.T) >= f2_hi(LIM);
             if (!(b0 || b1)) break;  // both pixels finished
+#ifdef HGS_CHECKED
+            if (b0 || b1) ++n_it;
+#endif
             const uint32_t le = lds_u16(a_list + 2 * q);
             const int k = (int)(le & 0xffu);
             const uint32_t o16 = (uint32_t)k << 4, o4 = (uint32_t)k << 2;
@@ -619,6 +639,9 @@ __global__ void __launch_bounds__(kThreads, 6) raster_fwd_kernel(
                 s.count0 += b0;
                 s.count1 += b1;
             }
+#ifdef HGS_CHECKED
+            n_box += (int)b0 + (int)b1;
+#endif
             const float4 L = lds_f4(a_chol + o16), c = lds_f4(a_col + o16);
             const SplatRec* e = exact + lds_u32(a_j + o4);
             const float eps_s = __int_as_float(hdr.w);
@@ -647,24 +670,33 @@ __global__ void __launch_bounds__(kThreads, 6) raster_fwd_kernel(
                 if (band1) p1 = exact_alpha_passes(e, pcx, pcy1);
             }
             if (!(p0 || p1)) continue;
+#ifdef HGS_CHECKED
+            n_pass += (int)p0 + (int)p1;
+#endif
             const f2 X2 = f2_pk(x0, x1);
             const f2 A = f2_mul(f2_bc(L.w), f2_pk(fast_exp2_neg(p0 ? x0 : 128.0f), fast_exp2_neg(p1 ? x1 : 128.0f)));
             const f2 EPS = f2_fma(f2_bc(fabsf(eps_s)), X2, f2_bc(kAlphaErr0));
             composite_pairs(s, p0, p1, A, EPS, c, base + k);
         }
     }
+#ifdef HGS_CHECKED
+    HGS_COUNT_PAIRS(0, n_it);
+    HGS_COUNT_PAIRS(1, n_box);
+    HGS_COUNT_PAIRS(2, n_pass);
+    if (lane == 0) HGS_COUNT_PAIRS(3, n_wit);
+#endif
     // flagged: finished inside the certified error band of the T < 1e-4 decision
-    const f2 LIM = term_limit(s), LOW = f2_fma(f2_bc(-2.0e-4f), s.err, f2_bc(1.0e-4f));
+    const f2 LIM = term_limit(s), LOW = f2_fma(f2_bc(-2.0f), s.E, f2_bc(1.0e-4f));
     const bool flag0 = f2_lo(s.T) < f2_lo(LIM) && f2_lo(s.T) > f2_lo(LOW);
     const bool flag1 = f2_hi(s.T) < f2_hi(LIM) && f2_hi(s.T) > f2_hi(LOW);
     if (in0) {
-        const PixFwd s0{f2_lo(s.T), f2_lo(s.r), f2_lo(s.g), f2_lo(s.b), f2_lo(s.err), s.last0, s.count0, true,
+        const PixFwd s0{f2_lo(s.T), f2_lo(s.r), f2_lo(s.g), f2_lo(s.b), f2_lo(s.E), s.last0, s.count0, true,
                         flag0};
         write_pixel(s0, py0 * W + px, bg_r, bg_g, bg_b, out_rgb, out_last, out_tfinal, out_trans, out_count, fix_list,
                     fix_count);
     }
     if (in1) {
-        const PixFwd s1{f2_hi(s.T), f2_hi(s.r), f2_hi(s.g), f2_hi(s.b), f2_hi(s.err), s.last1, s.count1, true,
+        const PixFwd s1{f2_hi(s.T), f2_hi(s.r), f2_hi(s.g), f2_hi(s.b), f2_hi(s.E), s.last1, s.count1, true,
                         flag1};
         write_pixel(s1, py1 * W + px, bg_r, bg_g, bg_b, out_rgb, out_last, out_tfinal, out_trans, out_count, fix_list,
                     fix_count);
@@ -697,12 +729,15 @@ __global__ void __launch_bounds__(128) raster_fixup_kernel(
     pdl_wait();  // launched with launch_pdl
     __shared__ double s_om[4][32 * kExactSub];
     const uint32_t n = *fix_count;
+    HGS_DCHECK(n <= g_chk.pixels);
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const uint32_t warps = gridDim.x * (blockDim.x >> 5);
     for (uint32_t q = blockIdx.x * (blockDim.x >> 5) + wib; q < n; q += warps) {
         const int pix = (int)fix_list[q];
+        HGS_DCHECK(pix >= 0 && (unsigned long long)pix < g_chk.pixels);
         const int px = pix % W, py = pix / W;
         const uint2 rg = ranges[(py / kTile) * tiles_x + px / kTile];
+        HGS_DCHECK(rg.x <= rg.y && rg.y <= g_chk.inst);
         const double pcx = px + 0.5, pcy = py + 0.5;
         double T = 1.0, ar = 0.0, ag = 0.0, ab = 0.0;
         uint32_t count = 0, last = rg.x;

@@ -1,4 +1,4 @@
-"""A small end-to-end run of every kernel family for compute-sanitizer
+"""A small end-to-end run (the checked-build workload, tests/test_gpu_checked.py) of every kernel family for compute-sanitizer
 (memcheck / racecheck / synccheck / initcheck): render (full instance list
 and the fused production path), render sweep with a forced capacity overflow,
 forward_train / loss / backward (default and exact mode), Adam, train steps
@@ -14,10 +14,12 @@ from paper_2505_13215_b200.api import Context, Rng
 from paper_2505_13215_b200.scene import ring_camera, synthetic_scene
 from paper_2505_13215_b200.train import DeviceTrainer
 
+# HGS_RUN_SCALE=k: k times the Gaussians and k times the image side (checked-build test)
+k = int(os.environ.get("HGS_RUN_SCALE", "1"))
 ctx = Context(0)
-scene = synthetic_scene(1500, 800, 2, seed=5, density_n=1500)
-target = synthetic_scene(1500, 800, 2, seed=6, density_n=1500)
-cams = [ring_camera(5, 96, 72, index=i, n_ring=4) for i in range(4)]
+scene = synthetic_scene(1500 * k, 800 * k, 2, seed=5, density_n=1500 * k)
+target = synthetic_scene(1500 * k, 800 * k, 2, seed=6, density_n=1500 * k)
+cams = [ring_camera(5, 96 * k, 72 * k, index=i, n_ring=4) for i in range(4)]
 bg = (0.2, 0.2, 0.2)
 ctx.upload(scene)
 ctx.render(cams[0], 0.5, bg)
@@ -25,7 +27,7 @@ ctx._lib.hgs_debug_keep_instances(ctx.handle, 1)
 ctx.render(cams[1], 0.3, bg, count_map=True, transmittance_map=True)
 ctx._lib.hgs_debug_keep_instances(ctx.handle, 0)
 ctx.render_sweep([cams[2]] * 6, [j / 5 for j in range(6)], bg)
-w = np.random.default_rng(0).uniform(-1, 1, (72, 96, 3))
+w = np.random.default_rng(0).uniform(-1, 1, (72 * k, 96 * k, 3))
 for exact in (False, True):
     ctx.set_exact_backward(exact)
     ctx.forward_train(cams[0], 0.5, bg)
