@@ -362,7 +362,8 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
         CK(ctx->shdir.ensure((size_t)N * sizeof(ShRec)));
         CK(ctx->scan_ws.ensure(scan_workspace_bytes(N) + 4096));
         prof_begin(ctx, PH_PREPROCESS);
-        CK(launch_pdl(preprocess_kernel, dim3(div_up(N, 256)), dim3(256), 0, st,
+        CK(preprocess_setup());
+        CK(launch_pdl(preprocess_kernel, dim3(div_up(N, 256)), dim3(256), preprocess_smem_bytes(ctx->deg), st,
                       static_cast<const float*>(ctx->p4.as<float>()), ctx->cap4, n4,
                       static_cast<const float*>(ctx->p3.as<float>()), ctx->cap3, n3, ctx->deg, ctx->cam, t, cutoff,
                       tiles_x, ctx->rec.as<SplatRec>(), ctx->depth_key.as<uint32_t>(), ctx->ntiles.as<uint32_t>(),
@@ -590,12 +591,12 @@ hgs_status hgs_render_finish(hgs_ctx* ctx) {
     Counters* hc = static_cast<Counters*>(ctx->pinned_ctr.p);
     CK(cudaMemcpyAsync(hc, dc, sizeof(Counters), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
-    ctx->stats.culled_depth = (int64_t)hc->stats[0];
-    ctx->stats.culled_offscreen = (int64_t)hc->stats[1];
-    ctx->stats.culled_degenerate = (int64_t)hc->stats[2];
-    ctx->stats.culled_temporal = (int64_t)hc->stats[3];
-    ctx->stats.degenerate_temporal = (int64_t)hc->stats[4];
-    ctx->stats.projected = (int64_t)hc->stats[5];
+    ctx->stats.culled_depth = (int64_t)hc->stat(0);
+    ctx->stats.culled_offscreen = (int64_t)hc->stat(1);
+    ctx->stats.culled_degenerate = (int64_t)hc->stat(2);
+    ctx->stats.culled_temporal = (int64_t)hc->stat(3);
+    ctx->stats.degenerate_temporal = (int64_t)hc->stat(4);
+    ctx->stats.projected = (int64_t)hc->stat(5);
     ctx->fixups = hc->fix_count;
     ctx->kept = ctx->I ? (int64_t)hc->I_kept : 0;
     hgs_status s = check_flags(ctx, hc->flags);
@@ -831,7 +832,8 @@ hgs_status hgs_density_map(hgs_ctx* ctx, const hgs_camera* cam, double t, int dy
         CK(ctx->depth_key.ensure((size_t)N * 4));
         CK(ctx->ntiles.ensure((size_t)N * 4));
         CK(ctx->shdir.ensure((size_t)N * sizeof(ShRec)));
-        preprocess_kernel<<<div_up(N, 256), 256, 0, st>>>(
+        CK(preprocess_setup());
+        preprocess_kernel<<<div_up(N, 256), 256, preprocess_smem_bytes(ctx->deg), st>>>(
             ctx->p4.as<float>(), ctx->cap4, n4, ctx->p3.as<float>(), ctx->cap3, n3, ctx->deg, to_dev(cam), t,
             weight_cutoff, tiles_x, ctx->rec.as<SplatRec>(), ctx->depth_key.as<uint32_t>(), ctx->ntiles.as<uint32_t>(),
             dc->stats, &dc->flags, ctx->shdir.as<ShRec>());
@@ -939,21 +941,21 @@ hgs_status hgs_render_sweep(hgs_ctx* ctx, int n, const hgs_camera* cams, const d
         }
         if (stats) {
             hgs_render_stats& o = stats[f];
-            o.culled_depth = (int64_t)hs[f].stats[0];
-            o.culled_offscreen = (int64_t)hs[f].stats[1];
-            o.culled_degenerate = (int64_t)hs[f].stats[2];
-            o.culled_temporal = (int64_t)hs[f].stats[3];
-            o.degenerate_temporal = (int64_t)hs[f].stats[4];
-            o.projected = (int64_t)hs[f].stats[5];
+            o.culled_depth = (int64_t)hs[f].stat(0);
+            o.culled_offscreen = (int64_t)hs[f].stat(1);
+            o.culled_degenerate = (int64_t)hs[f].stat(2);
+            o.culled_temporal = (int64_t)hs[f].stat(3);
+            o.degenerate_temporal = (int64_t)hs[f].stat(4);
+            o.projected = (int64_t)hs[f].stat(5);
         }
     }
     const Counters& last = hs[n - 1];
-    ctx->stats.culled_depth = (int64_t)last.stats[0];
-    ctx->stats.culled_offscreen = (int64_t)last.stats[1];
-    ctx->stats.culled_degenerate = (int64_t)last.stats[2];
-    ctx->stats.culled_temporal = (int64_t)last.stats[3];
-    ctx->stats.degenerate_temporal = (int64_t)last.stats[4];
-    ctx->stats.projected = (int64_t)last.stats[5];
+    ctx->stats.culled_depth = (int64_t)last.stat(0);
+    ctx->stats.culled_offscreen = (int64_t)last.stat(1);
+    ctx->stats.culled_degenerate = (int64_t)last.stat(2);
+    ctx->stats.culled_temporal = (int64_t)last.stat(3);
+    ctx->stats.degenerate_temporal = (int64_t)last.stat(4);
+    ctx->stats.projected = (int64_t)last.stat(5);
     ctx->fixups = last.fix_count;
     ctx->kept = last.I_kept;
     ctx->V = last.V;

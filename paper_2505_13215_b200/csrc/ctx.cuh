@@ -74,15 +74,21 @@ struct ZeroJobs {
 };
 
 // Per-render device counters (RenderStats, flags, totals).
-struct Counters {
-    unsigned long long stats[kNumStats];
+struct __align__(128) Counters {
     uint32_t flags;
     uint32_t V;
     uint32_t I;
     uint32_t fix_count;
     uint32_t skipped;
     uint32_t I_kept;
-    uint32_t pad[2];
+    uint32_t pad[26];
+    unsigned long long stats[kStatStripes * kStatStride];  // striped RenderStats (K1)
+    // RenderStats counter k summed over the stripes (host side)
+    unsigned long long stat(int k) const {
+        unsigned long long s = 0;
+        for (int r = 0; r < kStatStripes; ++r) s += stats[r * kStatStride + k];
+        return s;
+    }
 };
 
 }  // namespace hgs

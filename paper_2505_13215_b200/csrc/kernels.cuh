@@ -12,6 +12,9 @@ __global__ void preprocess_kernel(const float* __restrict__ p4, int64_t cap4, in
                                   uint32_t* __restrict__ ntiles_out, unsigned long long* __restrict__ stats,
                                   uint32_t* __restrict__ flags, ShRec* __restrict__ shrec);
 
+size_t preprocess_smem_bytes(int deg);  // dynamic shared memory of a preprocess_kernel launch
+cudaError_t preprocess_setup();         // opt-in to > 48 KB dynamic shared memory (once per process)
+
 // raster_fwd.cu (K2 + K4)
 __global__ void gather_sorted_kernel(const uint32_t* __restrict__ sorted_gid, const uint32_t* __restrict__ V_dev,
                                      const SplatRec* __restrict__ rec,

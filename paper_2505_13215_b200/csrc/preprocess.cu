@@ -15,6 +15,7 @@
 #include "raster_common.cuh"
 #include "sh.cuh"
 #include "gauss_math.cuh"
+#include "tma.cuh"
 
 namespace hgs {
 
@@ -24,30 +25,6 @@ using gm::M3;
 using gm::M4;
 using gm::rot4_from_pair;
 using gm::quat_to_rot3;
-
-// gauss_math.cpp:159-162
-__device__ inline M4 build_cov4(const M4& rot, const double ls[4]) {
-    double e[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) e[j] = exp(ls[j]);
-    double m[4][4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) m[i][j] = rot.a[i][j] * e[j];
-    M4 r;
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            double s = m[i][0] * m[j][0];
-            s = s + m[i][1] * m[j][1];
-            s = s + m[i][2] * m[j][2];
-            s = s + m[i][3] * m[j][3];
-            r.a[i][j] = s;
-        }
-    return r;
-}
 
 // gauss_math.cpp:154-157
 __device__ inline M3 build_cov3(const M3& rot, const double ls[3]) {
@@ -164,15 +141,17 @@ __device__ inline uint32_t project_3d(const double m[3], const M3& cov, const De
     const double z = p[2];
     if (z < cam.near_ || z > cam.far_) return CULL_DEPTH;
     depth = z;
-    const double sx = cam.fx * p[0] / z + cam.cx;
-    const double sy = cam.fy * p[1] / z + cam.cy;
+    // the six divisions by z and z*z through two reciprocals (gm::Rcp: bit-identical quotients)
+    const gm::Rcp rz(z), rzz(z * z);
+    const double sx = rz.div(cam.fx * p[0]) + cam.cx;
+    const double sy = rz.div(cam.fy * p[1]) + cam.cy;
     double J[2][3];
-    J[0][0] = cam.fx / z;
+    J[0][0] = rz.div(cam.fx);
     J[0][1] = 0.0;
-    J[0][2] = -cam.fx * p[0] / (z * z);
+    J[0][2] = rzz.div(-cam.fx * p[0]);
     J[1][0] = 0.0;
-    J[1][1] = cam.fy / z;
-    J[1][2] = -cam.fy * p[1] / (z * z);
+    J[1][1] = rz.div(cam.fy);
+    J[1][2] = rzz.div(-cam.fy * p[1]);
     double T[2][3];
 #pragma unroll
     for (int i = 0; i < 2; ++i)
@@ -207,10 +186,11 @@ __device__ inline uint32_t project_3d(const double m[3], const M3& cov, const De
     c2[1][1] += kLowPass;
     const double det = c2[0][0] * c2[1][1] - c2[0][1] * c2[1][0];
     if (det <= 1e-12) return CULL_DEGENERATE;
-    s.c00 = c2[1][1] / det;
-    s.c01 = -c2[0][1] / det;
-    s.c10 = -c2[1][0] / det;
-    s.c11 = c2[0][0] / det;
+    const gm::Rcp rdet(det);
+    s.c00 = rdet.div(c2[1][1]);
+    s.c01 = rdet.div(-c2[0][1]);
+    s.c10 = rdet.div(-c2[1][0]);
+    s.c11 = rdet.div(c2[0][0]);
     const double mid = 0.5 * (c2[0][0] + c2[1][1]);
     const double max_ev = mid + sqrt(fmax(0.0, mid * mid - det));
     const int radius = (int)ceil(3.0 * sqrt(max_ev));
@@ -233,16 +213,69 @@ __device__ inline double sigmoid(double x) { return 1.0 / (1.0 + exp(-x)); }
 
 }  // namespace
 
+// Shared-memory staging of a block's parameter columns: one 1D bulk copy
+// (TMA) per parameter row of the block's 256 Gaussians, all issued at block
+// start by one thread and completed on an mbarrier, so the block's whole
+// 17-65 row working set is in flight at once (the per-thread loads of the
+// FP64 slice and of the 48 SH rows used to be exposed one latency after the
+// other).  Row stride 260 floats: the 3D pool's columns start at any
+// Gaussian index, so a row is copied from the 16-byte-aligned index below
+// and read at offset (0..3).
+constexpr int kPreThreads = 256;
+constexpr int kPreStride = kPreThreads + 4;
+size_t preprocess_smem_bytes(int deg) { return (size_t)rows4(deg) * kPreStride * sizeof(float); }
+__global__ void preprocess_kernel(const float* __restrict__ p4, int64_t cap4, int n4, const float* __restrict__ p3,
+                                  int64_t cap3, int n3, int deg, DevCamera cam, double t, double cutoff, int tiles_x,
+                                  SplatRec* __restrict__ rec, uint32_t* __restrict__ depth_key,
+                                  uint32_t* __restrict__ ntiles_out, unsigned long long* __restrict__ stats,
+                                  uint32_t* __restrict__ flags, ShRec* __restrict__ shrec);
+cudaError_t preprocess_setup() {
+    static cudaError_t e = cudaFuncSetAttribute(preprocess_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)preprocess_smem_bytes(3));
+    return e;
+}
+
 // K1.  stats[0..5] = culled_depth, culled_offscreen, culled_degenerate,
 // culled_temporal, degenerate_temporal, projected.
-__global__ void __launch_bounds__(256, 3) preprocess_kernel(
+__global__ void __launch_bounds__(kPreThreads, 3) preprocess_kernel(
     const float* __restrict__ p4, int64_t cap4, int n4, const float* __restrict__ p3, int64_t cap3,
     int n3, int deg, DevCamera cam, double t, double cutoff, int tiles_x, SplatRec* __restrict__ rec,
     uint32_t* __restrict__ depth_key, uint32_t* __restrict__ ntiles_out,
     unsigned long long* __restrict__ stats, uint32_t* __restrict__ flags, ShRec* __restrict__ shrec) {
     pdl_wait();  // launched with launch_pdl
+    extern __shared__ __align__(128) float s_cols[];  // [row][kPreStride]
+    __shared__ __align__(8) uint64_t s_bar;
+    __shared__ uint32_t s_stat[kNumStats];
+    if (threadIdx.x < kNumStats) s_stat[threadIdx.x] = 0u;
     const int gid = blockIdx.x * blockDim.x + threadIdx.x;
     const int n = n4 + n3;
+    // the block's rows: one pool only (a block straddling the 4D/3D boundary
+    // reads global memory directly)
+    const int g0 = blockIdx.x * kPreThreads, g1 = min(g0 + kPreThreads, n);
+    const bool staged = g1 <= n4 || g0 >= n4;
+    int soff = 0;
+    __syncthreads();  // s_stat zeroed
+    if (staged) {
+        const bool dyn = g1 <= n4;
+        const int i0 = dyn ? g0 : g0 - n4;
+        const int a0 = i0 & ~3;  // 16-byte aligned start
+        soff = i0 - a0;
+        if (threadIdx.x == 0) {
+            mbar_init(&s_bar, 1);
+            const int nrows = dyn ? rows4(deg) : rows3(deg);
+            const uint32_t bytes = (uint32_t)(((g1 - g0 + soff + 3) & ~3) * sizeof(float));
+            mbar_arrive_expect_tx(&s_bar, bytes * (uint32_t)nrows);
+            const float* src = (dyn ? p4 : p3) + a0;
+            const int64_t cap = dyn ? cap4 : cap3;
+            for (int r = 0; r < nrows; ++r) bulk_g2s(s_cols + r * kPreStride, src + r * cap, bytes, &s_bar);
+        }
+        __syncthreads();  // the barrier is initialised before anyone waits on it
+        mbar_wait_parity(&s_bar, 0);
+    }
+    // parameter row `row` of this thread's Gaussian (pool P, index i)
+    auto ld = [&](const float* __restrict__ P, int64_t cap, int row, int i) -> float {
+        return staged ? s_cols[row * kPreStride + soff + (int)threadIdx.x] : __ldg(&P[(int64_t)row * cap + i]);
+    };
     uint32_t reason = CULL_DEPTH + 100;  // sentinel: inactive lane
     uint32_t flag = 0;
     if (gid < n) {
@@ -257,61 +290,92 @@ __global__ void __launch_bounds__(256, 3) preprocess_kernel(
             double ql[4], qr[4], ls[4], mean4[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                ql[k] = __ldg(&p4[(int64_t)(R4_QL + k) * cap4 + i]);
-                qr[k] = __ldg(&p4[(int64_t)(R4_QR + k) * cap4 + i]);
-                ls[k] = __ldg(&p4[(int64_t)(R4_LS + k) * cap4 + i]);
+                ql[k] = ld(p4, cap4, R4_QL + k, i);
+                qr[k] = ld(p4, cap4, R4_QR + k, i);
+                ls[k] = ld(p4, cap4, R4_LS + k, i);
             }
 #pragma unroll
-            for (int k = 0; k < 3; ++k) mean4[k] = __ldg(&p4[(int64_t)(R4_MEAN + k) * cap4 + i]);
-            mean4[3] = __ldg(&p4[(int64_t)R4_MT * cap4 + i]);
-            const M4 cov4 = build_cov4(rot4_from_pair(ql, qr), ls);
+            for (int k = 0; k < 3; ++k) mean4[k] = ld(p4, cap4, R4_MEAN + k, i);
+            mean4[3] = ld(p4, cap4, R4_MT, i);
+            // cov4 = M M^T with M = rot4 diag(exp(s)) (gauss_math.cpp:159-162);
+            // its entries are formed on demand below with build_cov4's
+            // operation order (entry (i, j) and (j, i) round identically)
+            const M4 rot = rot4_from_pair(ql, qr);
+            double e4[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) e4[j] = exp(ls[j]);
+            double m[4][4];
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) m[a][j] = rot.a[a][j] * e4[j];
+            auto cov4 = [&](int a, int b) {
+                double sum = m[a][0] * m[b][0];
+                sum = sum + m[a][1] * m[b][1];
+                sum = sum + m[a][2] * m[b][2];
+                sum = sum + m[a][3] * m[b][3];
+                return sum;
+            };
             // condition_at_time (gauss_math.cpp:175-186)
-            const double s44 = cov4.a[3][3];
+            const double s44 = cov4(3, 3);
             if (s44 < 1e-12) {
                 reason = CULL_DEGEN_TEMPORAL;
             } else {
-                const double cross[3] = {cov4.a[0][3], cov4.a[1][3], cov4.a[2][3]};
                 const double dt = t - mean4[3];
-                const double f = dt / s44;
+                const gm::Rcp r44(s44);  // the 11 divisions by s44 through one reciprocal
+                const double w = exp(r44.div(-0.5 * dt * dt));
+                // clamp_psd: lambda_min(Schur complement) >= lambda_min(cov4) = exp(2 min s);
+                // the eigen-solve can only change the result when that bound is near 1e-12.
+                // Sufficient without exp: 2 smin >= -27 and 2 (smax - smin) <= 27 give
+                // lam_lo - 1e-13 scale >= (1 - 0.054) e^-27 > 1e-12.
+                const double smin = fmin(fmin(ls[0], ls[1]), fmin(ls[2], ls[3]));
+                const double smax = fmax(fmax(ls[0], ls[1]), fmax(ls[2], ls[3]));
+                bool psd_fast = 2.0 * smin >= -27.0 && 2.0 * (smax - smin) <= 27.0;
+                if (!psd_fast) psd_fast = exp(2.0 * smin) - 1e-13 * exp(2.0 * smax) >= 1e-12;
+                if (w < cutoff && psd_fast) {
+                    // temporally culled, and clamp_psd provably neither throws nor
+                    // changes anything: the slice itself is never needed
+                    reason = CULL_TEMPORAL;
+                } else {
+                const double cross[3] = {cov4(0, 3), cov4(1, 3), cov4(2, 3)};
+                const double f = r44.div(dt);
 #pragma unroll
                 for (int k = 0; k < 3; ++k) mean3[k] = mean4[k] + cross[k] * f;
                 M3 c;
 #pragma unroll
                 for (int a = 0; a < 3; ++a)
 #pragma unroll
-                    for (int b = 0; b < 3; ++b) c.a[a][b] = cov4.a[a][b] - (cross[a] * cross[b]) / s44;
-                // clamp_psd: lambda_min(Schur complement) >= lambda_min(cov4) = exp(2 min s);
-                // the eigen-solve can only change the result when that bound is near 1e-12.
-                double smin = fmin(fmin(ls[0], ls[1]), fmin(ls[2], ls[3]));
-                double smax = fmax(fmax(ls[0], ls[1]), fmax(ls[2], ls[3]));
-                double lam_lo = exp(2.0 * smin), scale = exp(2.0 * smax);
-                if (!(lam_lo - 1e-13 * scale >= 1e-12)) ok = clamp_psd_slow(c);
+                    for (int b = a; b < 3; ++b) {
+                        c.a[a][b] = cov4(a, b) - r44.div(cross[a] * cross[b]);
+                        c.a[b][a] = c.a[a][b];
+                    }
+                if (!psd_fast) ok = clamp_psd_slow(c);
                 if (!ok) flag |= FLAG_INDEFINITE;
-                const double w = exp(-0.5 * dt * dt / s44);
                 if (w < cutoff) {
                     reason = CULL_TEMPORAL;
                 } else {
                     reason = project_3d(mean3, c, cam, s, depth, ntiles, tiles_x);
                     if (reason == CULL_NONE)
-                        alpha = fmin(sigmoid((double)__ldg(&p4[(int64_t)R4_OP * cap4 + i])) * w, kAlphaClamp);
+                        alpha = fmin(sigmoid((double)ld(p4, cap4, R4_OP, i)) * w, kAlphaClamp);
+                }
                 }
             }
         } else {
             const int i = gid - n4;
             double q[4], ls[3];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) q[k] = __ldg(&p3[(int64_t)(R3_Q + k) * cap3 + i]);
+            for (int k = 0; k < 4; ++k) q[k] = ld(p3, cap3, R3_Q + k, i);
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
-                ls[k] = __ldg(&p3[(int64_t)(R3_LS + k) * cap3 + i]);
-                mean3[k] = __ldg(&p3[(int64_t)(R3_MEAN + k) * cap3 + i]);
+                ls[k] = ld(p3, cap3, R3_LS + k, i);
+                mean3[k] = ld(p3, cap3, R3_MEAN + k, i);
             }
             M3 rot;
             if (!quat_to_rot3(q, rot)) flag |= FLAG_NONUNIT_QUAT;
             const M3 cov3 = build_cov3(rot, ls);
             reason = project_3d(mean3, cov3, cam, s, depth, ntiles, tiles_x);
             if (reason == CULL_NONE)
-                alpha = fmin(sigmoid((double)__ldg(&p3[(int64_t)R3_OP * cap3 + i])), kAlphaClamp);
+                alpha = fmin(sigmoid((double)ld(p3, cap3, R3_OP, i)), kAlphaClamp);
         }
         if (reason == CULL_NONE) {
             // view direction (raster.cpp:83-85) and SH colour
@@ -319,9 +383,10 @@ __global__ void __launch_bounds__(256, 3) preprocess_kernel(
             double nrm = sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
             double d[3] = {0.0, 0.0, 1.0};
             if (nrm > 0.0) {
-                d[0] = v[0] / nrm;
-                d[1] = v[1] / nrm;
-                d[2] = v[2] / nrm;
+                const gm::Rcp rn(nrm);
+                d[0] = rn.div(v[0]);
+                d[1] = rn.div(v[1]);
+                d[2] = rn.div(v[2]);
             }
             // SH colour (sh.cpp:73-83, FP32) and, for the SH backward (K7b: it
             // then needs no SH coefficient), the view direction, the
@@ -336,27 +401,43 @@ __global__ void __launch_bounds__(256, 3) preprocess_kernel(
             const int K = sh_count(deg);
             float basis[16];
             sh_basis_f(fd, deg, basis);
+            // coefficient-major: the 3 channel values of 4 coefficients in flight
+            // at a time, each folded into the 3 colour sums (the same per-channel
+            // FMA order as sh.cpp:78-80) and, through the direction factors of
+            // that coefficient (dY_k / d(dir), explicit FMAs), into the Jacobian
+            float acc[3] = {0.f, 0.f, 0.f}, jg[3][3] = {{0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}};
+            const float x = fd[0], y = fd[1], z = fd[2];
+#pragma unroll
+            for (int k0 = 0; k0 < 16; k0 += 4) {
+                float w[4][3];
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+                    for (int c = 0; c < 3; ++c)
+                        w[kk][c] = k0 + kk < K ? ld(P, cap, shrow + 3 * (k0 + kk) + c, i) : 0.f;
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) {
+                    const int k = k0 + kk;
+                    if (k >= K) continue;
+                    float f[3];
+                    sh_dir_factor(k, x, y, z, f);
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        acc[c] = fmaf(basis[k], w[kk][c], acc[c]);
+#pragma unroll
+                        for (int j = 0; j < 3; ++j)
+                            if (sh_dir_nonzero(k, j)) jg[c][j] = __fmaf_rn(f[j], w[kk][c], jg[c][j]);
+                    }
+                }
+            }
             ShRec sr;
-            float* jr[3] = {&sr.j[0].x, &sr.j[1].x, &sr.j[2].x};
             uint32_t clamped = 0;
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
-                float w[16];
-#pragma unroll
-                for (int k = 0; k < 16; ++k) w[k] = k < K ? __ldg(&P[(int64_t)(shrow + 3 * k + c) * cap + i]) : 0.f;
-                float acc = 0.f;
-#pragma unroll
-                for (int k = 0; k < 16; ++k)
-                    if (k < K) acc = fmaf(basis[k], w[k], acc);
-                const float raw = acc + 0.5f;  // raster.cpp:86 / sh.cpp:81
+                const float raw = acc[c] + 0.5f;  // raster.cpp:86 / sh.cpp:81
                 clamped |= (raw < 0.0f || raw > 1.0f) ? (1u << c) : 0u;
                 rgb[c] = fminf(fmaxf(raw, 0.0f), 1.0f);
-                float g[3];
-                sh_dir_grad_f(fd, deg, w, g);
-                jr[c][0] = g[0];
-                jr[c][1] = g[1];
-                jr[c][2] = g[2];
-                jr[c][3] = 0.f;
+                sr.j[c] = make_float4(jg[c][0], jg[c][1], jg[c][2], 0.f);
             }
             sr.dir = make_float4(fd[0], fd[1], fd[2], __uint_as_float(clamped));
             shrec[gid] = sr;
@@ -372,15 +453,19 @@ __global__ void __launch_bounds__(256, 3) preprocess_kernel(
             ntiles_out[gid] = 0u;
         }
     }
-    // warp-aggregated RenderStats counters
+    // RenderStats counters: warp ballots -> block totals in shared memory ->
+    // one global atomic per statistic and block, on the block's stripe
     const unsigned full = 0xffffffffu;
 #pragma unroll
     for (int k = 0; k < kNumStats; ++k) {
         const uint32_t want = k == 0 ? CULL_DEPTH : k == 1 ? CULL_OFFSCREEN : k == 2 ? CULL_DEGENERATE
                              : k == 3 ? CULL_TEMPORAL : k == 4 ? CULL_DEGEN_TEMPORAL : CULL_NONE;
         const unsigned b = __ballot_sync(full, reason == want);
-        if ((threadIdx.x & 31) == 0 && b) atomicAdd(&stats[k], (unsigned long long)__popc(b));
+        if ((threadIdx.x & 31) == 0 && b) atomicAdd(&s_stat[k], (uint32_t)__popc(b));
     }
+    __syncthreads();
+    if (threadIdx.x < kNumStats && s_stat[threadIdx.x])
+        atomicAdd(&stats[(blockIdx.x % kStatStripes) * kStatStride + threadIdx.x], (unsigned long long)s_stat[threadIdx.x]);
     const unsigned fb = __reduce_or_sync(full, flag);
     if ((threadIdx.x & 31) == 0 && fb) atomicOr(flags, fb);
 }

@@ -85,4 +85,38 @@ __device__ __forceinline__ void sh_dir_grad_f(const float d[3], int deg, const f
     sh_dir_grad_t<float>(d, deg, w, g);
 }
 
+// dY_k / d(x, y, z) of one basis function (k a compile-time constant after
+// unrolling), FP32 with explicit products for K1 (sh.cpp:49-71); entries
+// outside sh_dir_nonzero are 0 and left unset.
+__host__ __device__ constexpr bool sh_dir_nonzero(int k, int j) {
+    // x / y / z dependence of Y_k
+    return k == 0 ? false
+         : k == 1 ? j == 1 : k == 2 ? j == 2 : k == 3 ? j == 0
+         : k == 4 ? j != 2 : k == 5 ? j != 0 : k == 6 ? true : k == 7 ? j != 1 : k == 8 ? j != 2
+         : k == 9 ? j != 2 : k == 15 ? j != 2 : true;
+}
+__device__ __forceinline__ void sh_dir_factor(int k, float x, float y, float z, float f[3]) {
+    const float C1 = 0.4886025119029199f, A = 1.0925484305920792f, B = 0.31539156525252005f,
+                Cc = 0.5462742152960396f, D0 = -0.5900435899266435f, D1 = 2.890611442640554f,
+                D2 = -0.4570457994644658f, D3 = 0.3731763325901154f, D5 = 1.445305721320277f;
+    switch (k) {
+        case 1: f[1] = -C1; break;
+        case 2: f[2] = C1; break;
+        case 3: f[0] = -C1; break;
+        case 4: f[0] = A * y; f[1] = A * x; break;
+        case 5: f[1] = -A * z; f[2] = -A * y; break;
+        case 6: f[0] = B * (-2.0f * x); f[1] = B * (-2.0f * y); f[2] = B * (4.0f * z); break;
+        case 7: f[0] = -A * z; f[2] = -A * x; break;
+        case 8: f[0] = Cc * (2.0f * x); f[1] = Cc * (-2.0f * y); break;
+        case 9: f[0] = D0 * (6.0f * x * y); f[1] = D0 * (3.0f * x * x - 3.0f * y * y); break;
+        case 10: f[0] = D1 * (y * z); f[1] = D1 * (x * z); f[2] = D1 * (x * y); break;
+        case 11: f[0] = D2 * (-2.0f * x * y); f[1] = D2 * (4.0f * z * z - x * x - 3.0f * y * y); f[2] = D2 * (8.0f * y * z); break;
+        case 12: f[0] = D3 * (-6.0f * x * z); f[1] = D3 * (-6.0f * y * z); f[2] = D3 * (6.0f * z * z - 3.0f * x * x - 3.0f * y * y); break;
+        case 13: f[0] = D2 * (4.0f * z * z - 3.0f * x * x - y * y); f[1] = D2 * (-2.0f * x * y); f[2] = D2 * (8.0f * x * z); break;
+        case 14: f[0] = D5 * (2.0f * x * z); f[1] = D5 * (-2.0f * y * z); f[2] = D5 * (x * x - y * y); break;
+        case 15: f[0] = D0 * (3.0f * x * x - 3.0f * y * y); f[1] = D0 * (-6.0f * x * y); break;
+        default: break;
+    }
+}
+
 }  // namespace hgs

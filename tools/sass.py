@@ -13,7 +13,7 @@ for line in out.splitlines():
     if m:
         cur = m.group(1)
         body[cur] = []
-    elif cur and re.match(r"\s+/\*[0-9a-f]{4}\*/", line):
+    elif cur and re.match(r"\s+/\*[0-9a-f]{4,6}\*/", line):
         body[cur].append(line.split(";")[0].split("*/", 1)[1].strip())
 for name, ins in body.items():
     if pat.search(name):
