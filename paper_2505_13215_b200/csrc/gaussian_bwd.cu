@@ -41,6 +41,7 @@ struct Geo {
     double R4[4][4], es[4];                // 4D rotation (3D: rotation in [0..2][0..2]), exp(scales)
     double q[4], ql[4], qr[4];
     double cross[3], s44, dt, weight, sg;
+    double i44, iz, ivd;  // 1/s44, 1/z, 1/|v| (K7 is toleranced: one reciprocal per divisor)
 };
 
 __device__ __forceinline__ void geometry(Geo& g, const float pg[R4_SH], const double* cn, const DevCamera& cam,
@@ -55,6 +56,7 @@ __device__ __forceinline__ void geometry(Geo& g, const float pg[R4_SH], const do
     double mean3[3], opl;
     g.weight = 1.0;
     g.s44 = 1.0;
+    g.i44 = 1.0;
     g.dt = 0.0;
     if (dyn) {
         for (int k = 0; k < 4; ++k) {
@@ -83,10 +85,15 @@ __device__ __forceinline__ void geometry(Geo& g, const float pg[R4_SH], const do
         g.s44 = S4[3][3];
         for (int k = 0; k < 3; ++k) g.cross[k] = S4[k][3];
         g.dt = t - prm(R4_MT);
-        for (int k = 0; k < 3; ++k) mean3[k] = prm(R4_MEAN + k) + g.cross[k] * (g.dt / g.s44);
+        g.i44 = 1.0 / g.s44;
+        const double f = g.dt * g.i44;
+        for (int k = 0; k < 3; ++k) mean3[k] = prm(R4_MEAN + k) + g.cross[k] * f;
         for (int a = 0; a < 3; ++a)
-            for (int b = 0; b < 3; ++b) g.cov3[a][b] = S4[a][b] - g.cross[a] * g.cross[b] / g.s44;
-        g.weight = exp(-0.5 * g.dt * g.dt / g.s44);
+            for (int b = a; b < 3; ++b) {
+                g.cov3[a][b] = S4[a][b] - g.cross[a] * g.cross[b] * g.i44;
+                g.cov3[b][a] = g.cov3[a][b];
+            }
+        g.weight = exp(-0.5 * g.dt * g.dt * g.i44);
         opl = prm(R4_OP);
         g.clamped = sigmoid(opl) * g.weight >= kAlphaClamp;
     } else {
@@ -117,13 +124,14 @@ __device__ __forceinline__ void geometry(Geo& g, const float pg[R4_SH], const do
     g.z = cp[2];
     g.xq = cp[0];
     g.yq = cp[1];
-    const double z = g.z;
-    g.J[0][0] = cam.fx / z;
+    g.iz = 1.0 / g.z;
+    const double iz = g.iz, iz2 = iz * iz;
+    g.J[0][0] = cam.fx * iz;
     g.J[0][1] = 0.0;
-    g.J[0][2] = -cam.fx * g.xq / (z * z);
+    g.J[0][2] = -cam.fx * g.xq * iz2;
     g.J[1][0] = 0.0;
-    g.J[1][1] = cam.fy / z;
-    g.J[1][2] = -cam.fy * g.yq / (z * z);
+    g.J[1][1] = cam.fy * iz;
+    g.J[1][2] = -cam.fy * g.yq * iz2;
     for (int a = 0; a < 2; ++a)
         for (int k = 0; k < 3; ++k)
             g.Tm[a][k] = g.J[a][0] * cam.R[k] + g.J[a][1] * cam.R[3 + k] + g.J[a][2] * cam.R[6 + k];
@@ -132,8 +140,11 @@ __device__ __forceinline__ void geometry(Geo& g, const float pg[R4_SH], const do
     g.dir[0] = 0.0;
     g.dir[1] = 0.0;
     g.dir[2] = 1.0;
-    if (g.vd > 0.0)
-        for (int k = 0; k < 3; ++k) g.dir[k] = v[k] / g.vd;
+    g.ivd = 0.0;
+    if (g.vd > 0.0) {
+        g.ivd = 1.0 / g.vd;
+        for (int k = 0; k < 3; ++k) g.dir[k] = v[k] * g.ivd;
+    }
 }
 
 // The accumulator-dependent part of backward.cpp:224-354: K6's conic-free
@@ -174,18 +185,19 @@ __device__ __forceinline__ void chain(const Geo& g, const DevCamera& cam, const 
             d_jac[a][k] = d_tmat[a][0] * cam.R[k * 3] + d_tmat[a][1] * cam.R[k * 3 + 1] + d_tmat[a][2] * cam.R[k * 3 + 2];
     T d_cp[3];
     for (int k = 0; k < 3; ++k) d_cp[k] = g.J[0][k] * d_screen[0] + g.J[1][k] * d_screen[1];
-    const double fx = cam.fx, fy = cam.fy, z = g.z, xq = g.xq, yq = g.yq;
-    d_cp[0] += d_jac[0][2] * (-fx / (z * z));
-    d_cp[1] += d_jac[1][2] * (-fy / (z * z));
-    d_cp[2] += d_jac[0][0] * (-fx / (z * z)) + d_jac[1][1] * (-fy / (z * z)) + d_jac[0][2] * (2.0 * fx * xq / (z * z * z)) +
-               d_jac[1][2] * (2.0 * fy * yq / (z * z * z));
+    const double fx = cam.fx, fy = cam.fy, iz = g.iz, xq = g.xq, yq = g.yq;
+    const double iz2 = iz * iz, iz3 = iz2 * iz;
+    d_cp[0] += d_jac[0][2] * (-fx * iz2);
+    d_cp[1] += d_jac[1][2] * (-fy * iz2);
+    d_cp[2] += d_jac[0][0] * (-fx * iz2) + d_jac[1][1] * (-fy * iz2) + d_jac[0][2] * (2.0 * fx * xq * iz3) +
+               d_jac[1][2] * (2.0 * fy * yq * iz3);
     T d_mean3[3];
     for (int k = 0; k < 3; ++k) d_mean3[k] = cam.R[k] * d_cp[0] + cam.R[3 + k] * d_cp[1] + cam.R[6 + k] * d_cp[2];
     // ---- colour path (backward.cpp:252-273): d loss / d view direction
     if (g.vd > 0.0)
         for (int a = 0; a < 3; ++a) {
             T s = T(0.0);
-            for (int b = 0; b < 3; ++b) s += ((a == b ? 1.0 : 0.0) - g.dir[a] * g.dir[b]) / g.vd * d_dir[b];
+            for (int b = 0; b < 3; ++b) s += ((a == b ? 1.0 : 0.0) - g.dir[a] * g.dir[b]) * g.ivd * d_dir[b];
             d_mean3[a] += s;
         }
     T dS[3][3];
@@ -229,16 +241,16 @@ __device__ __forceinline__ void chain(const Geo& g, const DevCamera& cam, const 
         d_weight += d_alpha * sg;
     }
     for (int k = 0; k < 3; ++k) out[R4_MEAN + k] = d_mean3[k];
-    const double s44 = g.s44, dt = g.dt, weight = g.weight;
+    const double i44 = g.i44, dt = g.dt, weight = g.weight, i44s = i44 * i44;
     const double(&cross)[3] = g.cross;
     const T dmc = d_mean3[0] * cross[0] + d_mean3[1] * cross[1] + d_mean3[2] * cross[2];
-    out[R4_MT] = -dmc / s44 + d_weight * weight * dt / s44;
+    out[R4_MT] = -dmc * i44 + d_weight * weight * dt * i44;
     T sc[3];
     for (int a = 0; a < 3; ++a) sc[a] = dS[a][0] * cross[0] + dS[a][1] * cross[1] + dS[a][2] * cross[2];
     T d_cross[3];
-    for (int a = 0; a < 3; ++a) d_cross[a] = d_mean3[a] * (dt / s44) - 2.0 * sc[a] / s44;
+    for (int a = 0; a < 3; ++a) d_cross[a] = d_mean3[a] * (dt * i44) - 2.0 * sc[a] * i44;
     const T csc = cross[0] * sc[0] + cross[1] * sc[1] + cross[2] * sc[2];
-    const T d_s44 = -dmc * dt / (s44 * s44) + csc / (s44 * s44) + d_weight * weight * 0.5 * dt * dt / (s44 * s44);
+    const T d_s44 = -dmc * dt * i44s + csc * i44s + d_weight * weight * 0.5 * dt * dt * i44s;
     T d4[4][4];
     for (int a = 0; a < 4; ++a)
         for (int b = 0; b < 4; ++b) d4[a][b] = T(0.0);
