@@ -184,19 +184,46 @@ def roofline(phase_ms: dict, counts: dict, steps: int, peak: float, peak_kind: s
     except Exception:
         pass
     main_kernel = {"raster_bwd": "raster_bwd_kernel", "raster_fwd": "raster_fwd_kernel",
-                   "duplicate": "duplicate_kernel", "gaussian_bwd": "gaussian_bwd_kernel",
+                   "duplicate": "duplicate_compact_kernel", "gaussian_bwd": "gaussian_bwd_kernel",
                    "adam": "adam_rows_kernel", "tile_sort": "radix_sort_coop_kernel",
-                   "depth_sort": "radix_sort_coop_kernel"}
+                   "depth_sort": "radix_sort_coop_kernel", "preprocess": "preprocess_kernel",
+                   "loss": "ssim_fwd_kernel"}
     for k in kernels:
         prof = ncu.get(main_kernel.get(k["phase"], ""), {})
         k["ncu"] = {key: prof.get(key) for key in ("kernel", "duration_us", "dram_bytes_per_launch",
-                                                   "issue_slots_busy_pct", "ipc_active")} if prof else None
+                                                   "issue_slots_busy_pct", "ipc_active", "pipes_pct",
+                                                   "report")} if prof else None
+    # the rasterizers' own roofline: instruction issue.  Pixel-splat pairs per
+    # step from the checked build's counters (profiles/*_pairs.json,
+    # tools/count_pairs.py: a property of the workload), pipe utilisation from
+    # the committed ncu capture of the kernel
+    pairs = {}
+    try:
+        pf = sorted(f for f in os.listdir(os.path.join(ROOT, "profiles")) if f.endswith("_pairs.json"))
+        pairs = json.load(open(os.path.join(ROOT, "profiles", pf[-1]))) if pf else {}
+        pairs["file"] = pf[-1] if pf else None
+    except Exception:
+        pairs = {}
+    issue = {}
+    for k in kernels:
+        if k["phase"] in ("raster_fwd", "raster_bwd"):
+            pc = pairs.get(k["phase"]) or {}
+            e = pc.get("box_pairs_evaluated")
+            ip = ((k.get("ncu") or {}).get("pipes_pct") or {})
+            issue[k["phase"]] = {
+                "bound": "instruction issue (FP32 / ALU / shared-memory pipes)",
+                "issue_pct": ip.get("issue"), "fma_pipe_pct": ip.get("fma"), "alu_pipe_pct": ip.get("alu"),
+                "lsu_pipe_pct": ip.get("lsu"), "xu_pipe_pct": ip.get("xu"),
+                "shared_wavefront_pct": ip.get("shared_wavefronts"),
+                "pairs_evaluated_per_step": e, "alpha_passing_pairs_per_step": pc.get("alpha_passing_pairs"),
+                "Gpairs_per_s": round(e / (k["ms_per_step"] * 1e-3) / 1e9, 2) if e else None,
+                "pairs_source": pairs.get("file"), "pipes_source": (k.get("ncu") or {}).get("report")}
     tp = (top.get("ncu") or {})
     return {"bound": "hbm", "kernel": top["phase"], "achieved": top["GB/s"], "peak": peak, "unit": "GB/s",
             "frac": top["frac"], "traffic": tp.get("dram_bytes_per_launch"), "peak_source": peak_kind,
-            "note": "the tile rasterizers are issue-bound (see issue_slots_busy_pct), not HBM-bound: "
-                    "their splat reads hit L2",
-            "kernels": kernels}
+            "note": "the tile rasterizers are issue-bound, not HBM-bound (their splat reads hit L2): "
+                    "their roofline is `issue` (pipe utilisation and pixel-splat pairs per second)",
+            "issue": issue, "kernels": kernels}
 
 
 # ------------------------------------------------------------------ our arm

@@ -125,6 +125,8 @@ __global__ void __launch_bounds__(kCoopThreads) radix_sort_coop_kernel(CoopSort 
     __shared__ uint32_t h[256];
     __shared__ uint32_t cnt[kWarps][256];
     __shared__ uint32_t goff[256];
+    __shared__ uint32_t dstart[256];
+    __shared__ uint32_t s_k[kTileItems], s_v[kTileItems];  // the tile, stably sorted by digit
     const int G = gridDim.x, b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n = a.n_dev ? (int)*a.n_dev : a.n;
     HGS_DCHECK(!a.n_dev || n <= a.n);
@@ -194,18 +196,34 @@ __global__ void __launch_bounds__(kCoopThreads) radix_sort_coop_kernel(CoopSort 
                 cnt[w][tid] = tile_tot;
                 tile_tot += t;
             }
+            {
+                uint32_t all;
+                dstart[tid] = block_excl_scan(tile_tot, all);
+            }
             __syncthreads();
+            // the tile, stably sorted by digit, in shared memory ...
 #pragma unroll
             for (int r = 0; r < kItems; ++r) {
                 if (r >= R) break;
                 const int idx = wbase + r * 32 + lane;
                 if (idx < hi) {
                     const uint32_t d = (k[r] >> shift) & 255u;
-                    const uint32_t pos = goff[d] + cnt[warp][d] + rank[r];
-                    HGS_DCHECK(pos < (uint32_t)n);
-                    ko[pos] = k[r];
-                    vo[pos] = v[r];
+                    const uint32_t lp = dstart[d] + cnt[warp][d] + rank[r];
+                    s_k[lp] = k[r];
+                    s_v[lp] = v[r];
                 }
+            }
+            __syncthreads();
+            // ... written out in order: consecutive threads write consecutive
+            // addresses of each digit's run (coalesced)
+            const int nt = min(R * kCoopThreads, hi - t0);
+            for (int q = tid; q < nt; q += kCoopThreads) {
+                const uint32_t kk = s_k[q];
+                const uint32_t d = (kk >> shift) & 255u;
+                const uint32_t pos = goff[d] + (uint32_t)q - dstart[d];
+                HGS_DCHECK(pos < (uint32_t)n);
+                ko[pos] = kk;
+                vo[pos] = s_v[q];
             }
             __syncthreads();
             goff[tid] += tile_tot;

@@ -67,6 +67,18 @@ def summarize(rep):
         "achieved_occupancy_pct": num(d.get("Achieved Occupancy")),
         "registers": num(d.get("Registers Per Thread")),
         "dram_throughput_pct": num(d.get("DRAM Throughput")),
+        # pipe utilisation (% of peak sustained while the SM is active) and the
+        # shared-memory wavefront share: the issue-bound kernels' roofline
+        "pipes_pct": {k: (round(get(m), 1) if get(m) is not None else None) for k, m in (
+            ("issue", "smsp__issue_active.avg.pct_of_peak_sustained_active"),
+            ("fma", "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
+            ("alu", "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"),
+            ("fp64", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+            ("lsu", "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active"),
+            ("xu", "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active"),
+            ("shared_wavefronts", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"),
+            ("dram", "dram__throughput.avg.pct_of_peak_sustained_elapsed"))},
+        "warp_instructions": get("smsp__inst_executed.sum"),
         "stalls_pct": {k: round(100 * x / tot, 1) for k, x in sorted(stalls.items(), key=lambda t: -t[1])[:8]},
         "report": os.path.basename(rep),
     }
@@ -85,7 +97,7 @@ def main():
         sys.stdout = old
     with open(os.path.join(out_dir, f"{rnd}_launches.txt"), "w") as f:
         f.write("# ncu --nvtx --nvtx-include timed/ --metrics gpu__time_duration.sum --clock-control none\n")
-        f.write("#   python bench.py --steps 5 --warmup 3 --no-cpu-baseline   (timed region only)\n")
+        f.write("#   python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-extras   (timed region only)\n")
         f.write(buf.getvalue())
     summ = {}
     for rep in reps:
