@@ -53,7 +53,7 @@ __global__ void raster_fixup_kernel(const uint32_t* __restrict__ fix_list, const
                                     const SplatRec* __restrict__ exact, int W, int tiles_x, double bg_r, double bg_g,
                                     double bg_b, float* __restrict__ out_rgb, uint32_t* __restrict__ out_last,
                                     float* __restrict__ out_tfinal, float* __restrict__ out_trans,
-                                    uint32_t* __restrict__ out_count);
+                                    uint32_t* __restrict__ out_count, double* __restrict__ out_cout);
 
 __global__ void grads_pack_kernel(const float* __restrict__ gbuf, int64_t off_g3, int64_t off_dgn4, int rows4,
                                   int rows3, int64_t cap4, int64_t cap3, int n4, int n3, float* __restrict__ packed,
@@ -81,7 +81,8 @@ __global__ void raster_bwd_exact_kernel(const uint32_t* __restrict__ fix_list, c
                                         const uint32_t* __restrict__ inst_val, const SplatRec* __restrict__ exact,
                                         int W, int tiles_x, double bg_r, double bg_g, double bg_b,
                                         const uint32_t* __restrict__ last_arr, const float* __restrict__ dL_dimg,
-                                        const double* __restrict__ col64, acc_t* __restrict__ accum);
+                                        const double* __restrict__ col64, acc_t* __restrict__ accum,
+                                        const double* __restrict__ fix_cout);
 __global__ void exact_colour_kernel(const uint32_t* __restrict__ sorted_gid, int V, int n4,
                                     const float* __restrict__ p4, int64_t cap4, const float* __restrict__ p3,
                                     int64_t cap3, int deg, DevCamera cam, double t, double* __restrict__ col64);

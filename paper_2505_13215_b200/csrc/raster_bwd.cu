@@ -337,7 +337,8 @@ __global__ void __launch_bounds__(128) raster_bwd_exact_kernel(
     const uint32_t* __restrict__ fix_list, const uint32_t* __restrict__ fix_count, int all_pixels,
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ inst_val, const SplatRec* __restrict__ exact, int W,
     int tiles_x, double bg_r, double bg_g, double bg_b, const uint32_t* __restrict__ last_arr,
-    const float* __restrict__ dL_dimg, const double* __restrict__ col64, acc_t* __restrict__ accum) {
+    const float* __restrict__ dL_dimg, const double* __restrict__ col64, acc_t* __restrict__ accum,
+    const double* __restrict__ fix_cout) {
     pdl_wait();  // launched with launch_pdl
     __shared__ double s_om[4][32 * kExactSub];
     // the forward's fix-up pixels, or (exact backward mode) every pixel
@@ -355,7 +356,16 @@ __global__ void __launch_bounds__(128) raster_bwd_exact_kernel(
         HGS_DCHECK(rg.x <= rg.y && rg.y <= g_chk.inst && last <= rg.y);
         const double pcx = px + 0.5, pcy = py + 0.5;
         double Cout[3];
-        for (int pass = 0; pass < 2; ++pass) {
+        // the forward fix-up already composited the flagged pixel in FP64:
+        // its colour replaces pass 0 (fix-list mode)
+        int pass0 = 0;
+        if (fix_list && fix_cout) {
+            Cout[0] = fix_cout[3 * q + 0];
+            Cout[1] = fix_cout[3 * q + 1];
+            Cout[2] = fix_cout[3 * q + 2];
+            pass0 = 1;
+        }
+        for (int pass = pass0; pass < 2; ++pass) {
             double T = 1.0, P[3] = {0.0, 0.0, 0.0};
             constexpr int S = kExactSub;
             for (uint32_t base = rg.x; base < last; base += 32 * S) {

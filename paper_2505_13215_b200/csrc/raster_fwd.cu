@@ -725,7 +725,8 @@ __global__ void __launch_bounds__(128) raster_fixup_kernel(
     const uint32_t* __restrict__ fix_list, const uint32_t* __restrict__ fix_count, const uint2* __restrict__ ranges,
     const uint32_t* __restrict__ inst_val, const SplatRec* __restrict__ exact, int W, int tiles_x, double bg_r,
     double bg_g, double bg_b, float* __restrict__ out_rgb, uint32_t* __restrict__ out_last,
-    float* __restrict__ out_tfinal, float* __restrict__ out_trans, uint32_t* __restrict__ out_count) {
+    float* __restrict__ out_tfinal, float* __restrict__ out_trans, uint32_t* __restrict__ out_count,
+    double* __restrict__ out_cout) {
     pdl_wait();  // launched with launch_pdl
     __shared__ double s_om[4][32 * kExactSub];
     const uint32_t n = *fix_count;
@@ -767,9 +768,16 @@ __global__ void __launch_bounds__(128) raster_fixup_kernel(
             if (c.term >= 0) break;
         }
         if (lane == 0) {
-            out_rgb[pix * 3 + 0] = (float)__dadd_rn(ar, __dmul_rn(T, bg_r));
-            out_rgb[pix * 3 + 1] = (float)__dadd_rn(ag, __dmul_rn(T, bg_g));
-            out_rgb[pix * 3 + 2] = (float)__dadd_rn(ab, __dmul_rn(T, bg_b));
+            const double cr = __dadd_rn(ar, __dmul_rn(T, bg_r)), cg = __dadd_rn(ag, __dmul_rn(T, bg_g)),
+                         cb = __dadd_rn(ab, __dmul_rn(T, bg_b));
+            out_rgb[pix * 3 + 0] = (float)cr;
+            out_rgb[pix * 3 + 1] = (float)cg;
+            out_rgb[pix * 3 + 2] = (float)cb;
+            if (out_cout) {  // the FP64 pixel colour for raster_bwd_exact_kernel (fix-list order)
+                out_cout[3 * q + 0] = cr;
+                out_cout[3 * q + 1] = cg;
+                out_cout[3 * q + 2] = cb;
+            }
             out_last[pix] = last | 0x80000000u;
             out_tfinal[pix] = (float)T;
             if (out_trans) out_trans[pix] = (float)T;
