@@ -429,6 +429,22 @@ hgs_status hgs_train_collect(hgs_ctx *ctx, double *loss_out);
  * no host synchronisation; hgs_train_collect later returns this rank's loss
  * and raises NumericAbort on every rank for the same iteration. */
 hgs_status hgs_train_exchange_async(hgs_ctx *ctx, const hgs_train_opts *opts);
+/* Sharded optimizer exchange (enable = 1) for hgs_train_exchange_async:
+ * instead of one all-reduce of the gradients and the full Adam step on every
+ * rank, a reduce-scatter of every gradient row (rank r owns Gaussians
+ * [r c, r c + c) of each pool, c = ceil(n / ranks) rounded up to 4), Adam on
+ * the owned range only, and an all-gather of the updated parameter rows and
+ * densification statistics -- the same bytes on the wire as the all-reduce,
+ * 1/ranks of the Adam work.  The Adam moments then live sharded: before
+ * anything that needs them whole (densification, the 4D->3D sweep,
+ * checkpoints with state, hgs_adam_state_download, hgs_broadcast_params)
+ * every rank calls hgs_gather_state (those calls fail with HGS_ERR_STATE
+ * otherwise).  A one-rank communicator runs the same path (identity
+ * collectives, the whole range). */
+hgs_status hgs_comm_set_sharded(hgs_ctx *ctx, int enable);
+hgs_status hgs_gather_state(hgs_ctx *ctx);
+/* The shard [lo, hi) this rank owns of a pool of n Gaussians. */
+void hgs_shard_range(int64_t n, int ranks, int rank, int64_t *lo, int64_t *hi);
 /* Number of enqueued iterations not collected yet. */
 int hgs_train_pending(hgs_ctx *ctx);
 

@@ -153,6 +153,9 @@ _SIGS = {
     "hgs_debug_instances": ([_vp, _u32p, _u32p, C.c_int64, _i64p], C.c_int),
     "hgs_debug_keep_instances": ([_vp, C.c_int], C.c_int),
     "hgs_debug_pair_counters": ([_vp, C.POINTER(C.c_ulonglong), C.c_int], C.c_int),
+    "hgs_comm_set_sharded": ([_vp, C.c_int], C.c_int),
+    "hgs_gather_state": ([_vp], C.c_int),
+    "hgs_shard_range": ([C.c_int64, C.c_int, C.c_int, _i64p, _i64p], None),
     "hgs_debug_instance_masks": ([_vp, C.POINTER(C.c_uint8), C.c_int64, _i64p], C.c_int),
     "hgs_forward_train": ([_vp, C.POINTER(Camera_), C.c_double, _dp, C.POINTER(RasterOpts), _fp], C.c_int),
     "hgs_backward": ([_vp, _vp, C.c_int, C.c_int, C.c_double], C.c_int),

@@ -185,6 +185,23 @@ class Context:
     def broadcast_params(self, root: int = 0) -> None:
         self._check(self._lib.hgs_broadcast_params(self._h, int(root)))
 
+    def set_sharded(self, enable: bool = True) -> None:
+        """Sharded optimizer exchange for train_exchange_async: reduce-scatter
+        of the gradient rows, Adam on this rank's shard, all-gather of the
+        parameters (hgs_comm_set_sharded)."""
+        self._check(self._lib.hgs_comm_set_sharded(self._h, 1 if enable else 0))
+
+    def gather_state(self) -> None:
+        """Whole Adam moments on every rank (collective; a no-op unless the
+        sharded exchange left them sharded)."""
+        self._check(self._lib.hgs_gather_state(self._h))
+
+    @staticmethod
+    def shard_range(n: int, ranks: int, rank: int) -> tuple[int, int]:
+        lo, hi = C.c_int64(), C.c_int64()
+        _capi.lib().hgs_shard_range(int(n), int(ranks), int(rank), C.byref(lo), C.byref(hi))
+        return lo.value, hi.value
+
     # ------------------------------------------------------------ initialisation
     def init_scene(self, positions: np.ndarray, rgb: np.ndarray, cfg: "InitConfig | None" = None) -> None:
         """init_scene (data_io.cpp:189-238) straight into the device: one

@@ -745,6 +745,7 @@ hgs_status hgs_scene_alloc(hgs_ctx* ctx, int64_t n4, int64_t n3, int deg, double
     if (n4 < 0 || n3 < 0 || deg < 0 || deg > 3)
         return fail(ctx, HGS_ERR_INVALID_ARGUMENT, "scene upload: bad sizes or sh_degree (0..3)");
     if (n4 + n3 > (int64_t)INT32_MAX / 2) return fail(ctx, HGS_ERR_INVALID_ARGUMENT, "scene too large");
+    ctx->state_sharded = false;  // fresh moments
     CK(cudaSetDevice(ctx->device));
     if (!ctx->pipeline.empty())
         return fail(ctx, HGS_ERR_STATE, "scene upload: collect the pipelined iterations first");

@@ -708,6 +708,10 @@ const char* hgs_io_last_error(void) { return g_io_err.c_str(); }
 // ------------------------------------------------------------ device save
 hgs_status hgs_checkpoint_save(hgs_ctx* ctx, const char* path, int with_state) {
     if (!ctx || !path) return HGS_ERR_INVALID_ARGUMENT;
+    if (with_state && ctx->state_sharded) {
+        ctx->err = "save_checkpoint: the Adam moments are sharded (hgs_gather_state on every rank first)";
+        return HGS_ERR_STATE;
+    }
     CKC(cudaSetDevice(ctx->device));
     if (!ctx->pipeline.empty()) {
         ctx->err = "save_checkpoint: collect the pipelined iterations first";
@@ -814,6 +818,7 @@ hgs_status hgs_checkpoint_save(hgs_ctx* ctx, const char* path, int with_state) {
 // ------------------------------------------------------------ device load
 hgs_status hgs_checkpoint_load(hgs_ctx* ctx, const char* path, int* has_state) {
     if (!ctx || !path) return HGS_ERR_INVALID_ARGUMENT;
+    ctx->state_sharded = false;  // the loaded state is whole
     CKC(cudaSetDevice(ctx->device));
     IoError e;
     // the file into pinned memory (concurrent pread ranges)

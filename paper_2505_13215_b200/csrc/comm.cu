@@ -14,7 +14,10 @@
 #include <link.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cstring>
+#include <initializer_list>
+#include <utility>
 #include <string>
 #include <vector>
 
@@ -35,6 +38,9 @@ struct NcclApi {
     ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                               cudaStream_t) = nullptr;
     ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*ReduceScatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                                  cudaStream_t) = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*GroupStart)() = nullptr;
     ncclResult_t (*GroupEnd)() = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
@@ -79,7 +85,7 @@ NcclApi& nccl() {
         return a;                                                          \
     }
         SYM(GetUniqueId) SYM(CommInitRank) SYM(CommInitAll) SYM(CommDestroy) SYM(AllReduce) SYM(Broadcast)
-        SYM(GroupStart) SYM(GroupEnd) SYM(GetErrorString) SYM(GetVersion)
+        SYM(ReduceScatter) SYM(AllGather) SYM(GroupStart) SYM(GroupEnd) SYM(GetErrorString) SYM(GetVersion)
 #undef SYM
         a.loaded = true;
         return a;
@@ -134,6 +140,23 @@ __global__ void checksum_kernel(const float* __restrict__ p, int64_t cap, int64_
     if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
 }
 
+// Zero rows [0, span) of `rows` rows (stride cap) outside [lo, hi): the
+// gradient entries a reduce-scatter left unreduced on this rank.
+__global__ void zero_outside_kernel(float* __restrict__ base, int64_t cap, int rows, int64_t span, int64_t lo,
+                                    int64_t hi) {
+    const int64_t total = span * rows;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = e / span, i = e - r * span;
+        if (i < lo || i >= hi) base[r * cap + i] = 0.0f;
+    }
+}
+
+__global__ void add_u64_kernel(unsigned long long* __restrict__ dst, const unsigned long long* __restrict__ src) {
+    *dst += *src;
+}
+
+int64_t shard_chunk(int64_t n, int ranks) { return ranks > 0 ? ((n + ranks - 1) / ranks + 3) / 4 * 4 : n; }
+
 }  // namespace
 
 hgs_status comm_allreduce_f64_dev(hgs_ctx* ctx, double* dev, int n) {
@@ -142,6 +165,103 @@ hgs_status comm_allreduce_f64_dev(hgs_ctx* ctx, double* dev, int n) {
     if (n > 0)
         CKN(nccl().AllReduce(dev, dev, (size_t)n, ncclFloat64, ncclSum, static_cast<ncclComm_t>(ctx->comm),
                              ctx->stream));
+    return HGS_OK;
+}
+
+// Every row of the pools (and the statistic rows) of n Gaussians, chunk c
+// per rank: the in-place collectives need ranks * c <= capacity, which
+// round_cap (n rounded up to 128, + 128) guarantees for <= 32 ranks.
+hgs_status comm_check_chunks(hgs_ctx* ctx, int64_t& c4, int64_t& c3) {
+    c4 = shard_chunk(ctx->n4, ctx->comm_size);
+    c3 = shard_chunk(ctx->n3, ctx->comm_size);
+    if (c4 * ctx->comm_size > ctx->cap4 || c3 * ctx->comm_size > ctx->cap3)
+        return fail(ctx, HGS_ERR_STATE, "sharded exchange: pool capacity below ranks x chunk");
+    return HGS_OK;
+}
+
+// Reduce-scatter of every gradient row and statistic-delta row: rank r
+// receives the sum of [r c, r c + c) in place.
+hgs_status comm_reduce_scatter_grads(hgs_ctx* ctx) {
+    hgs_status r = need_comm(ctx);
+    if (r != HGS_OK) return r;
+    int64_t c4, c3;
+    r = comm_check_chunks(ctx, c4, c3);
+    if (r != HGS_OK) return r;
+    ncclComm_t c = static_cast<ncclComm_t>(ctx->comm);
+    const int rk = ctx->comm_rank;
+    auto rs = [&](float* row, int64_t ch) -> ncclResult_t {
+        return ch > 0 ? nccl().ReduceScatter(row, row + (int64_t)rk * ch, (size_t)ch, ncclFloat32, ncclSum, c,
+                                             ctx->stream)
+                      : ncclSuccess;
+    };
+    ctx->grads_zero = false;
+    CKN(nccl().GroupStart());
+    for (int k = 0; k < rows4(ctx->deg); ++k) CKN(rs(ctx->g4 + (int64_t)k * ctx->cap4, c4));
+    for (int k = 0; k < rows3(ctx->deg); ++k) CKN(rs(ctx->g3 + (int64_t)k * ctx->cap3, c3));
+    CKN(rs(ctx->dgn4, c4));
+    CKN(rs(ctx->dcnt4, c4));
+    CKN(rs(ctx->dgn3, c3));
+    CKN(rs(ctx->dcnt3, c3));
+    CKN(nccl().GroupEnd());
+    return HGS_OK;
+}
+
+// All-gather of row sets: rank r contributes [r c, r c + c) of every row.
+hgs_status comm_allgather_rows(hgs_ctx* ctx, std::initializer_list<std::pair<float*, int>> sets4,
+                               std::initializer_list<std::pair<float*, int>> sets3) {
+    int64_t c4, c3;
+    hgs_status r = comm_check_chunks(ctx, c4, c3);
+    if (r != HGS_OK) return r;
+    ncclComm_t c = static_cast<ncclComm_t>(ctx->comm);
+    const int rk = ctx->comm_rank;
+    auto ag = [&](float* row, int64_t ch) -> ncclResult_t {
+        return ch > 0 ? nccl().AllGather(row + (int64_t)rk * ch, row, (size_t)ch, ncclFloat32, c, ctx->stream)
+                      : ncclSuccess;
+    };
+    CKN(nccl().GroupStart());
+    for (const auto& s : sets4)
+        for (int k = 0; k < s.second; ++k) CKN(ag(s.first + (int64_t)k * ctx->cap4, c4));
+    for (const auto& s : sets3)
+        for (int k = 0; k < s.second; ++k) CKN(ag(s.first + (int64_t)k * ctx->cap3, c3));
+    CKN(nccl().GroupEnd());
+    return HGS_OK;
+}
+
+// After the sharded Adam: this rank's gradients outside its shard were
+// never reduced (zeroed here; the shard itself was zeroed by Adam), the
+// updated parameters and folded statistics are all-gathered, and the step's
+// skipped-class count is summed over the ranks into skipped_nonfinite.
+hgs_status comm_sharded_finish(hgs_ctx* ctx, unsigned long long* skipped, unsigned long long* skipped_cum) {
+    int64_t c4, c3;
+    hgs_status r = comm_check_chunks(ctx, c4, c3);
+    if (r != HGS_OK) return r;
+    int64_t lo4, hi4, lo3, hi3;
+    hgs_shard_range(ctx->n4, ctx->comm_size, ctx->comm_rank, &lo4, &hi4);
+    hgs_shard_range(ctx->n3, ctx->comm_size, ctx->comm_rank, &lo3, &hi3);
+    const int blocks = ctx->sms * 4;
+    const int64_t s4 = c4 * ctx->comm_size, s3 = c3 * ctx->comm_size;
+    if (s4 > 0) {
+        zero_outside_kernel<<<blocks, 256, 0, ctx->stream>>>(ctx->g4, ctx->cap4, rows4(ctx->deg), s4, lo4, hi4);
+        zero_outside_kernel<<<blocks, 256, 0, ctx->stream>>>(ctx->dgn4, ctx->cap4, 1, s4, lo4, hi4);
+        zero_outside_kernel<<<blocks, 256, 0, ctx->stream>>>(ctx->dcnt4, ctx->cap4, 1, s4, lo4, hi4);
+        count_launch(3);
+    }
+    if (s3 > 0) {
+        zero_outside_kernel<<<blocks, 256, 0, ctx->stream>>>(ctx->g3, ctx->cap3, rows3(ctx->deg), s3, lo3, hi3);
+        zero_outside_kernel<<<blocks, 256, 0, ctx->stream>>>(ctx->dgn3, ctx->cap3, 1, s3, lo3, hi3);
+        zero_outside_kernel<<<blocks, 256, 0, ctx->stream>>>(ctx->dcnt3, ctx->cap3, 1, s3, lo3, hi3);
+        count_launch(3);
+    }
+    CKC(cudaGetLastError());
+    r = comm_allgather_rows(ctx, {{ctx->p4.as<float>(), rows4(ctx->deg)}, {ctx->gn4.as<float>(), 1}, {ctx->cnt4.as<float>(), 1}},
+                            {{ctx->p3.as<float>(), rows3(ctx->deg)}, {ctx->gn3.as<float>(), 1}, {ctx->cnt3.as<float>(), 1}});
+    if (r != HGS_OK) return r;
+    CKN(nccl().AllReduce(skipped, skipped, 1, ncclUint64, ncclSum, static_cast<ncclComm_t>(ctx->comm), ctx->stream));
+    add_u64_kernel<<<1, 1, 0, ctx->stream>>>(skipped_cum, skipped);
+    count_launch();
+    CKC(cudaGetLastError());
+    ctx->grads_zero = true;
+    ctx->state_sharded = true;
     return HGS_OK;
 }
 
@@ -236,6 +356,34 @@ hgs_status hgs_allreduce_grads(hgs_ctx* ctx) {
     return HGS_OK;
 }
 
+void hgs_shard_range(int64_t n, int ranks, int rank, int64_t* lo, int64_t* hi) {
+    const int64_t c = shard_chunk(n, ranks);
+    const int64_t l = std::min<int64_t>(n, (int64_t)rank * c);
+    if (lo) *lo = l;
+    if (hi) *hi = std::min<int64_t>(n, l + c);
+}
+
+hgs_status hgs_comm_set_sharded(hgs_ctx* ctx, int enable) {
+    if (!ctx) return HGS_ERR_INVALID_ARGUMENT;
+    if (enable && ctx->comm_size > 32) return fail(ctx, HGS_ERR_INVALID_ARGUMENT, "sharded exchange: at most 32 ranks");
+    ctx->sharded = enable != 0;
+    return HGS_OK;
+}
+
+hgs_status hgs_gather_state(hgs_ctx* ctx) {
+    if (!ctx) return HGS_ERR_INVALID_ARGUMENT;
+    if (!ctx->state_sharded) return HGS_OK;
+    hgs_status r = need_comm(ctx);
+    if (r != HGS_OK) return r;
+    CKC(cudaSetDevice(ctx->device));
+    r = comm_allgather_rows(ctx, {{ctx->m4.as<float>(), rows4(ctx->deg)}, {ctx->v4.as<float>(), rows4(ctx->deg)}},
+                            {{ctx->m3.as<float>(), rows3(ctx->deg)}, {ctx->v3.as<float>(), rows3(ctx->deg)}});
+    if (r != HGS_OK) return r;
+    CKC(cudaStreamSynchronize(ctx->stream));
+    ctx->state_sharded = false;
+    return HGS_OK;
+}
+
 hgs_status hgs_allreduce_f64(hgs_ctx* ctx, double* vals, int n) {
     if (!ctx || (n > 0 && !vals) || n < 0) return HGS_ERR_INVALID_ARGUMENT;
     hgs_status r = need_comm(ctx);
@@ -276,6 +424,8 @@ hgs_status hgs_param_checksum(hgs_ctx* ctx, uint64_t* out) {
 hgs_status hgs_broadcast_params(hgs_ctx* ctx, int root) {
     if (!ctx) return HGS_ERR_INVALID_ARGUMENT;
     hgs_status r = need_comm(ctx);
+    if (r != HGS_OK) return r;
+    r = hgs_gather_state(ctx);  // the moments whole on every rank before root's are broadcast
     if (r != HGS_OK) return r;
     if (root < 0 || root >= ctx->comm_size) return HGS_ERR_INVALID_ARGUMENT;
     CKC(cudaSetDevice(ctx->device));

@@ -174,6 +174,8 @@ struct hgs_ctx {
     hgs::DBuf crc_tab;           // CRC-32 slicing tables (checkpoint.cu)
     void* comm = nullptr;        // ncclComm_t of the view-parallel exchange (comm.cu)
     int comm_rank = 0, comm_size = 1;
+    bool sharded = false;      // hgs_comm_set_sharded: reduce-scatter / sharded Adam / all-gather
+    bool state_sharded = false;  // Adam moments valid only on this rank's shard (hgs_gather_state)
     hgs::DBuf comm_buf;          // small staging for collectives / checksums
     uint32_t icap = 0;           // instance capacity of capacity-mode renders (hgs_render_sweep)
     int64_t redone_frames = 0;   // sweep frames re-rendered after a capacity overflow

@@ -211,6 +211,8 @@ hgs_status hgs_densify_plan(hgs_ctx* ctx, const hgs_densify_cfg* cfg, uint8_t* k
                             hgs_densify_report* rep) {
     if (!ctx || !cfg || !rep) return HGS_ERR_INVALID_ARGUMENT;
     if (!ctx->pipeline.empty()) return fail(ctx, HGS_ERR_STATE, "densify: pipelined iterations pending");
+    if (ctx->state_sharded) return fail(ctx, HGS_ERR_STATE, "densify: the Adam moments are sharded (hgs_gather_state on every rank first)");
+
     if (!(cfg->split_factor > 0.0) || cfg->max_gaussians < 0)
         return fail(ctx, HGS_ERR_INVALID_ARGUMENT, "densify: bad configuration");
     CK(cudaSetDevice(ctx->device));

@@ -301,8 +301,16 @@ double loss_from_sums(const Scratch& h, int W, int H, double lambda) {
 // kernels leave every parameter untouched when one is non-finite (the step
 // then fails with NumericAbort, train.cpp:445-447, without a host round trip
 // before the update).
+// Adam over the Gaussians [lo, hi) of each pool (hi < 0: to the end; lo a
+// multiple of 4): the kernels see row pointers offset by lo and n = hi - lo
+// (the row stride stays the capacity).  cumulative = false: the step's
+// skipped count is not added to GradAccum::skipped_nonfinite here (the
+// sharded exchange adds the all-reduced count).
 hgs_status run_adam(hgs_ctx* ctx, const hgs_lrs* lrs, double mean_lr_scale, const double* view_sums = nullptr,
-                    int n_views = 0, uint32_t* abort = nullptr) {
+                    int n_views = 0, uint32_t* abort = nullptr, int64_t lo4 = 0, int64_t hi4 = -1, int64_t lo3 = 0,
+                    int64_t hi3 = -1, bool cumulative = true) {
+    if (hi4 < 0) hi4 = ctx->n4;
+    if (hi3 < 0) hi3 = ctx->n3;
     cudaStream_t st = ctx->stream;
     ctx->step++;
     const double bc1 = 1.0 - std::pow(0.9, (double)ctx->step);
@@ -323,26 +331,31 @@ hgs_status run_adam(hgs_ctx* ctx, const hgs_lrs* lrs, double mean_lr_scale, cons
     A.view_sums = view_sums;
     A.n_views = n_views;
     A.abort = abort;
-    const int n = (int)(ctx->n4 + ctx->n3);
+    const int n4 = (int)std::max<int64_t>(0, hi4 - lo4), n3 = (int)std::max<int64_t>(0, hi3 - lo3);
+    const int n = n4 + n3;
     Scratch* sc = scratch(ctx);
-    A.skipped_cum = &sc->skipped_cum;
+    A.skipped_cum = cumulative ? &sc->skipped_cum : nullptr;
     AdamPools P;
-    P.p4 = ctx->p4.as<float>(), P.g4 = ctx->g4, P.m4 = ctx->m4.as<float>(), P.v4 = ctx->v4.as<float>();
-    P.p3 = ctx->p3.as<float>(), P.g3 = ctx->g3, P.m3 = ctx->m3.as<float>(), P.v3 = ctx->v3.as<float>();
-    P.gn4 = ctx->gn4.as<float>(), P.cnt4 = ctx->cnt4.as<float>(), P.dgn4 = ctx->dgn4, P.dcnt4 = ctx->dcnt4;
-    P.gn3 = ctx->gn3.as<float>(), P.cnt3 = ctx->cnt3.as<float>(), P.dgn3 = ctx->dgn3, P.dcnt3 = ctx->dcnt3;
-    P.cap4 = ctx->cap4, P.cap3 = ctx->cap3, P.n4 = (int)ctx->n4, P.n3 = (int)ctx->n3, P.K3 = 3 * sh_count(ctx->deg);
+    P.p4 = ctx->p4.as<float>() + lo4, P.g4 = ctx->g4 + lo4, P.m4 = ctx->m4.as<float>() + lo4,
+    P.v4 = ctx->v4.as<float>() + lo4;
+    P.p3 = ctx->p3.as<float>() + lo3, P.g3 = ctx->g3 + lo3, P.m3 = ctx->m3.as<float>() + lo3,
+    P.v3 = ctx->v3.as<float>() + lo3;
+    P.gn4 = ctx->gn4.as<float>() + lo4, P.cnt4 = ctx->cnt4.as<float>() + lo4, P.dgn4 = ctx->dgn4 + lo4,
+    P.dcnt4 = ctx->dcnt4 + lo4;
+    P.gn3 = ctx->gn3.as<float>() + lo3, P.cnt3 = ctx->cnt3.as<float>() + lo3, P.dgn3 = ctx->dgn3 + lo3,
+    P.dcnt3 = ctx->dcnt3 + lo3;
+    P.cap4 = ctx->cap4, P.cap3 = ctx->cap3, P.n4 = n4, P.n3 = n3, P.K3 = 3 * sh_count(ctx->deg);
     prof_begin(ctx, PH_ADAM);
     if (n > 0) {
         CK(ctx->adam_ok.ensure((size_t)(5 * ctx->cap3 + 7 * ctx->cap4)));
-        uint8_t* ok3 = ctx->adam_ok.as<uint8_t>();
-        uint8_t* ok4 = ok3 + 5 * ctx->cap3;
-        const uint32_t units = 5 * div_up((uint32_t)ctx->n3, 4) + 7 * div_up((uint32_t)ctx->n4, 4);
+        uint8_t* ok3 = ctx->adam_ok.as<uint8_t>() + lo3;
+        uint8_t* ok4 = ctx->adam_ok.as<uint8_t>() + 5 * ctx->cap3 + lo4;
+        const uint32_t units = 5 * div_up((uint32_t)n3, 4) + 7 * div_up((uint32_t)n4, 4);
         CK(launch_pdl(adam_classes_kernel, dim3(div_up(units, 128)), dim3(128), 0, st, P, A, ok3, ok4, &sc->skipped,
                       &sc->flags));
         count_launch();
         CKL();
-        const int bpr3 = (int)div_up(div_up((uint32_t)ctx->n3, 4), 256), bpr4 = (int)div_up(div_up((uint32_t)ctx->n4, 4), 256);
+        const int bpr3 = (int)div_up(div_up((uint32_t)n3, 4), 256), bpr4 = (int)div_up(div_up((uint32_t)n4, 4), 256);
         const int R3 = R3_SH + P.K3 - 4, R4 = R4_SH + P.K3 - 8;
         const int blocks = R3 * bpr3 + R4 * bpr4;
         if (blocks > 0) {
@@ -588,6 +601,7 @@ hgs_status hgs_adam_step(hgs_ctx* ctx, const hgs_lrs* lrs, double mean_lr_scale,
 
 hgs_status hgs_adam_state_download(hgs_ctx* ctx, hgs_host_scene* m, hgs_host_scene* v, int dtype, uint64_t* step) {
     if (!ctx) return HGS_ERR_INVALID_ARGUMENT;
+    if (ctx->state_sharded) return fail(ctx, HGS_ERR_STATE, "adam_state_download: the Adam moments are sharded (hgs_gather_state on every rank first)");
     DBuf p4 = ctx->p4, p3 = ctx->p3;
     hgs_status r = HGS_OK;
     if (m) {
@@ -615,6 +629,7 @@ hgs_status hgs_adam_state_upload(hgs_ctx* ctx, const hgs_host_scene* m, const hg
     if (!ctx || !m || !v) return HGS_ERR_INVALID_ARGUMENT;
     if (m->n4 != ctx->n4 || m->n3 != ctx->n3 || v->n4 != ctx->n4 || v->n3 != ctx->n3)
         return fail(ctx, HGS_ERR_INVALID_ARGUMENT, "adam state: pool sizes differ from the scene");
+    ctx->state_sharded = false;
     hgs_status r = hgs_upload_rows(ctx, m, dtype, ctx->m4.as<float>(), ctx->m3.as<float>());
     if (r != HGS_OK) return r;
     r = hgs_upload_rows(ctx, v, dtype, ctx->v4.as<float>(), ctx->v3.as<float>());
@@ -703,6 +718,8 @@ hgs_status hgs_sweep_convert(hgs_ctx* ctx, int64_t* moved_out, hgs_conversion_re
     if (!ctx) return HGS_ERR_INVALID_ARGUMENT;
     if (!(ctx->tau > 0.0)) return fail(ctx, HGS_ERR_INVALID_ARGUMENT, "is_static: tau must be positive");
     if (!ctx->pipeline.empty()) return fail(ctx, HGS_ERR_STATE, "sweep_convert: pipelined iterations pending");
+    if (ctx->state_sharded) return fail(ctx, HGS_ERR_STATE, "sweep_convert: the Adam moments are sharded (hgs_gather_state on every rank first)");
+
     CK(cudaSetDevice(ctx->device));
     hgs_status r = ensure_scratch(ctx);
     if (r != HGS_OK) return r;
@@ -978,11 +995,25 @@ hgs_status hgs_train_exchange_async(hgs_ctx* ctx, const hgs_train_opts* o) {
     CKL();
     hgs_status r = comm_allreduce_f64_dev(ctx, gate, 1);
     if (r != HGS_OK) return r;
-    r = hgs_allreduce_grads(ctx);
-    if (r != HGS_OK) return r;
-    ps.step_before = ctx->step;
-    r = run_adam(ctx, &o->lrs, o->mean_lr_scale, gate, 1, &sc->abort);
-    if (r != HGS_OK) return r;
+    if (ctx->sharded) {
+        // reduce-scatter -> Adam on this rank's shard -> all-gather (comm.cu)
+        r = comm_reduce_scatter_grads(ctx);
+        if (r != HGS_OK) return r;
+        ps.step_before = ctx->step;
+        int64_t lo4, hi4, lo3, hi3;
+        hgs_shard_range(ctx->n4, ctx->comm_size, ctx->comm_rank, &lo4, &hi4);
+        hgs_shard_range(ctx->n3, ctx->comm_size, ctx->comm_rank, &lo3, &hi3);
+        r = run_adam(ctx, &o->lrs, o->mean_lr_scale, gate, 1, &sc->abort, lo4, hi4, lo3, hi3, false);
+        if (r != HGS_OK) return r;
+        r = comm_sharded_finish(ctx, &sc->skipped, &sc->skipped_cum);
+        if (r != HGS_OK) return r;
+    } else {
+        r = hgs_allreduce_grads(ctx);
+        if (r != HGS_OK) return r;
+        ps.step_before = ctx->step;
+        r = run_adam(ctx, &o->lrs, o->mean_lr_scale, gate, 1, &sc->abort);
+        if (r != HGS_OK) return r;
+    }
     ps.adam = true;
     ps.dist = true;
     double* hg = static_cast<double*>(ctx->pinned_pipe.p) + (size_t)HGS_TRAIN_PIPELINE * kMaxStepViews * 2;

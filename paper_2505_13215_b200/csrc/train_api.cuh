@@ -21,3 +21,6 @@ hgs_status hgs_scene_alloc(hgs_ctx* ctx, int64_t n4, int64_t n3, int deg, double
                            double duration);
 // stream-ordered all-reduce (sum) of n device doubles over the context's communicator (comm.cu)
 hgs_status comm_allreduce_f64_dev(hgs_ctx* ctx, double* dev, int n);
+// sharded optimizer exchange (comm.cu, hgs_comm_set_sharded)
+hgs_status comm_reduce_scatter_grads(hgs_ctx* ctx);
+hgs_status comm_sharded_finish(hgs_ctx* ctx, unsigned long long* skipped, unsigned long long* skipped_cum);

@@ -51,6 +51,27 @@ class _CudaArray:
         self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f4", "data": (ptr, False), "version": 3}
 
 
+def render_gt_u8_device(ctx: Context, target: HybridScene, cameras: list, times: list, bg=(0.0, 0.0, 0.0),
+                        weight_cutoff: float = 0.05) -> list:
+    """Ground-truth frames as the reference's dataset holds them (8-bit sRGB,
+    image.cpp:15-18), rendered and encoded on the device: one device u8 HWC
+    tensor per (camera, time).  For dataset-sized frame counts (configs[2]:
+    18 cameras x 300 frames) where the host round trip per frame would
+    dominate.  Uploads ``target`` (the caller uploads its own scene after)."""
+    import torch
+
+    ctx.upload(target)
+    out = []
+    for cam, t in zip(cameras, times):
+        ctx.render_device(cam, t, bg, weight_cutoff=weight_cutoff)
+        n = cam.height * cam.width * 3
+        img = torch.as_tensor(_CudaArray(ctx.last_image_device_ptr(), n), device=f"cuda:{ctx.device}")
+        v = img.double().clamp(0.0, 1.0).pow(1.0 / 2.2).mul(255.0).add(0.5).floor()
+        out.append(v.to(torch.uint8).view(cam.height, cam.width, 3).clone())
+        torch.cuda.synchronize(ctx.device)  # the next render reuses the context's image buffer
+    return out
+
+
 class DeviceTrainer:
     """Single-GPU (or one-rank) trainer around a Context.
 
@@ -62,9 +83,11 @@ class DeviceTrainer:
                  target: HybridScene | None = None, gt_images: list[np.ndarray] | None = None,
                  bg=(0.0, 0.0, 0.0), ssim_lambda: float = 0.2, lrs: LearningRates | None = None,
                  iterations: int = 2000, weight_cutoff: float = 0.05, quantize_gt: bool = True,
-                 gt_format: str = "f32"):
+                 gt_format: str = "f32", gt_device: list | None = None):
         """gt_format: "f32" -- linear float frames on the device; "u8" -- the
-        8-bit sRGB codes (4x smaller), decoded inside the loss (HGS_U8)."""
+        8-bit sRGB codes (4x smaller), decoded inside the loss (HGS_U8).
+        gt_device: ready device frames in that format (torch tensors, HWC),
+        e.g. from render_gt_u8_device; then neither target nor gt_images."""
         import torch
 
         self.torch = torch
@@ -78,6 +101,8 @@ class DeviceTrainer:
         self.weight_cutoff = weight_cutoff
         self.iter = 0
         dev = torch.device("cuda", ctx.device)
+        if gt_device is not None:
+            gt_images = []
         if gt_images is None:
             if target is None:
                 raise ValueError("DeviceTrainer: need target or gt_images")
@@ -89,7 +114,9 @@ class DeviceTrainer:
         if gt_format not in ("f32", "u8"):
             raise ValueError("gt_format: 'f32' or 'u8'")
         self.gt_format = gt_format
-        if gt_format == "u8":
+        if gt_device is not None:
+            self.gt = list(gt_device)
+        elif gt_format == "u8":
             self.gt = [torch.as_tensor(np.ascontiguousarray(linear_to_srgb8(g)), device=dev) for g in gt_images]
         else:
             self.gt = [torch.as_tensor(np.ascontiguousarray(g, dtype=np.float32), device=dev) for g in gt_images]
@@ -166,7 +193,8 @@ class ViewParallelTrainer(DeviceTrainer):
     """One rank of the view-parallel trainer (torch.distributed, NCCL on GPUs,
     gloo on CPU for the host-logic tests)."""
 
-    def __init__(self, *args, group=None, exchange: str = "torch", verify_every: int = 0, **kw):
+    def __init__(self, *args, group=None, exchange: str = "torch", verify_every: int = 0, sharded: bool = False,
+                 **kw):
         """exchange: "torch" -- torch.distributed all-reduce of the packed
         payload; "capi" -- the library's own NCCL communicator
         (hgs_allreduce_grads).  verify_every > 0: every that many steps the
@@ -190,6 +218,14 @@ class ViewParallelTrainer(DeviceTrainer):
             uid = [Context.comm_unique_id() if self.rank == 0 else None]
             dist.broadcast_object_list(uid, src=0, group=group)
             self.ctx.comm_init(self.world, self.rank, uid[0])
+        # sharded=True (exchange "capi", pipelined steps): reduce-scatter ->
+        # Adam on this rank's shard -> all-gather; gather_state() before
+        # densification / sweeps / checkpoints with optimizer state
+        if sharded and exchange != "capi":
+            raise ValueError("sharded exchange needs exchange='capi'")
+        self.sharded = sharded
+        if exchange == "capi":
+            self.ctx.set_sharded(sharded)
 
     def grads_tensor(self):
         ptr, n = self.ctx.grads_device()
@@ -235,6 +271,13 @@ class ViewParallelTrainer(DeviceTrainer):
         self.iter += 1
         DeviceTrainer.step_async(self, mine, batch_total=len(batch), apply_adam=False, gt_host=gt_host)
         self.ctx._check(self.ctx._lib.hgs_train_exchange_async(self.ctx.handle, C.byref(self._opts(self.decay()))))
+
+    def gather_state(self) -> None:
+        """Whole Adam moments on every rank (call on every rank after sharded
+        steps, before densify / sweep_convert / save_checkpoint)."""
+        while self.ctx._lib.hgs_train_pending(self.ctx.handle):
+            self.collect()
+        self.ctx.gather_state()
 
     def verify_replicas(self) -> bool:
         """True when every rank's parameters hash equal; otherwise rank 0's

@@ -73,3 +73,19 @@ def test_cpp_consumer_compiles_and_fails_loudly(tmp_path):
     if torch.cuda.is_available():
         pytest.skip("GPU present: covered by tests/test_gpu_render.py::test_cpp_consumer_runs")
     assert subprocess.run([exe], capture_output=True).returncode == 2
+
+
+def test_shard_ranges_partition_the_pool():
+    """hgs_shard_range (sharded optimizer exchange): contiguous, 4-aligned
+    starts, every Gaussian owned once, ranks x chunk within the pool capacity."""
+    from paper_2505_13215_b200.api import Context
+
+    for n in (0, 1, 3, 4, 5, 127, 1000, 240_000, 1_600_001):
+        for ranks in (1, 2, 3, 4, 7, 8, 16, 32):
+            got = [Context.shard_range(n, ranks, r) for r in range(ranks)]
+            assert got[0][0] == 0 and got[-1][1] == n
+            for (lo, hi), (lo2, _) in zip(got, got[1:]):
+                assert hi == lo2 and (lo % 4 == 0 or lo == hi) and lo <= hi
+            chunk = max(hi - lo for lo, hi in got) if n else 0
+            cap = ((n + 127) // 128) * 128 + 128  # round_cap of the device pools
+            assert chunk * ranks <= cap

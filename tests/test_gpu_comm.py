@@ -163,3 +163,43 @@ def test_exchange_binds_the_process_nccl():
     tv = torch.cuda.nccl.version()
     tcode = tv[0] * 10000 + tv[1] * 100 + tv[2] if isinstance(tv, tuple) else int(tv)
     assert ver.value == tcode, (ver.value, tcode, buf.value)
+
+
+def test_sharded_exchange_one_rank_matches_the_allreduce_exchange(tmp_path):
+    """hgs_comm_set_sharded: reduce-scatter -> Adam on the rank's shard ->
+    all-gather.  With a one-rank communicator the shard is the whole pool:
+    three pipelined exchange steps give the parameters and moments of the
+    all-reduce exchange (FP tolerance: K6's atomics order), the moments are
+    flagged sharded until hgs_gather_state, and the state-dependent calls
+    refuse to run on sharded moments."""
+    import ctypes as C
+
+    from paper_2505_13215_b200.train import DeviceTrainer
+
+    with A.Context(0) as a, A.Context(0) as b:
+        ta, tb = _trainer(a), _trainer(b)
+        for ctx in (a, b):
+            ctx.comm_init(1, 0, A.Context.comm_unique_id())
+        b.set_sharded(True)
+        for i in range(3):
+            for ctx, tr in ((a, ta), (b, tb)):
+                DeviceTrainer.step_async(tr, [i % 4], batch_total=1, apply_adam=False)
+                ctx._check(ctx._lib.hgs_train_exchange_async(ctx.handle, C.byref(tr._opts(tr.decay()))))
+                tr.collect()
+        sa, sb = a.download(), b.download()
+        for f in ("mean_x", "ql", "log_s4", "op4", "sh4", "mean3", "quat3", "op3", "sh3"):
+            x, y = np.asarray(getattr(sa, f)), np.asarray(getattr(sb, f))
+            assert np.allclose(x, y, rtol=1e-5, atol=1e-7), f
+        with pytest.raises(A.StateError):
+            b.save_checkpoint(str(tmp_path / "s.hgsc"))
+        with pytest.raises(A.StateError):
+            b.sweep_convert()
+        b.gather_state()
+        ma, va = a.adam_state()[:2]
+        mb, vb = b.adam_state()[:2]
+        for f in ("mean_x", "sh4", "mean3", "sh3"):
+            assert np.allclose(np.asarray(getattr(ma, f)), np.asarray(getattr(mb, f)), rtol=1e-4, atol=1e-9), f
+            assert np.allclose(np.asarray(getattr(va, f)), np.asarray(getattr(vb, f)), rtol=1e-4, atol=1e-12), f
+        b.save_checkpoint(str(tmp_path / "s.hgsc"))
+        assert np.array_equal(a.densify_stats()[0], b.densify_stats()[0]) or np.allclose(
+            a.densify_stats()[0], b.densify_stats()[0], rtol=1e-5)

@@ -107,3 +107,27 @@ def test_train_scene_rejects_bad_config(ctx):
     init = synthetic_scene(100, 50, 1, seed=44)
     with pytest.raises(ValueError):
         train_scene(init, ds, TrainConfig(iterations=10, warmup_iters=20), ctx=ctx)
+
+
+@pytest.mark.gpu
+def test_render_gt_u8_device_matches_the_host_encoding():
+    """render_gt_u8_device (configs[2]'s 5400 device-resident GT frames) encodes
+    the rendered frame like linear_to_srgb8 (image.cpp:15-18) on the host."""
+    import numpy as np
+
+    from paper_2505_13215_b200.api import Context
+    from paper_2505_13215_b200.scene import ring_camera, synthetic_scene
+    from paper_2505_13215_b200.train import linear_to_srgb8, render_gt_u8_device
+
+    ctx = Context(0)
+    try:
+        target = synthetic_scene(3000, 1000, 2, seed=11)
+        cams = [ring_camera(3, 160, 120, index=i, n_ring=3) for i in range(3)]
+        times = [0.1, 0.5, 0.9]
+        dev = render_gt_u8_device(ctx, target, cams, times, bg=(0.2, 0.2, 0.2))
+        for cam, t, d in zip(cams, times, dev):
+            host = linear_to_srgb8(ctx.render(cam, t, (0.2, 0.2, 0.2))["rgb"].astype(np.float64))
+            diff = np.abs(d.cpu().numpy().astype(int) - host.astype(int))
+            assert diff.max() <= 1 and (diff == 0).mean() >= 0.999
+    finally:
+        ctx.close()
