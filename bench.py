@@ -254,7 +254,7 @@ def run_ours(args) -> None:
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream.cuda_stream)
     kw = dict(target=target, bg=(0.2, 0.2, 0.2), iterations=max(1000, args.steps * 10))
-    tr = (ViewParallelTrainer(ctx, scene, cams, times, exchange="capi", **kw) if vp
+    tr = (ViewParallelTrainer(ctx, scene, cams, times, exchange="capi", sharded=args.sharded, **kw) if vp
           else DeviceTrainer(ctx, scene, cams, times, **kw))
 
     def batch(step):
@@ -769,6 +769,9 @@ def main():
     ap.add_argument("--no-extras", action="store_true", help="skip the c1/c5 render and c4 training lines")
     ap.add_argument("--view-parallel", action="store_true",
                     help="use the N-GPU code path (NCCL exchange) even on one GPU (a one-rank communicator)")
+    ap.add_argument("--sharded", action="store_true",
+                    help="view-parallel path with the sharded optimizer exchange (reduce-scatter -> Adam on the "
+                         "rank's shard -> all-gather) instead of the gradient all-reduce")
     ap.add_argument("--no-phase-profile", action="store_true",
                     help="no per-phase CUDA events in the timed region (roofline.kernels then empty)")
     args = ap.parse_args()
