@@ -221,16 +221,18 @@ __global__ void __launch_bounds__(kThreadsB, 7) raster_bwd_kernel(
         // quadrant reaches 1/255 otherwise), walked back to front below kmax
         const int cnt = build_warp_list<kBatchB>(sb.qm, sb.bm, kmax, warp, s_list[warp]);
         const uint32_t a_list = opaque_u32((uint32_t)__cvta_generic_to_shared(&s_list[warp][0]));
+        // splat k of the batch precedes a pixel's last contributor iff
+        // 16 k < 16 (last - base) (clamped to [-1, kBatchB]: no overflow)
+        const int l0 = max(-1, min((int)kBatchB, (int)s.last0 - (int)base)) * 16;
+        const int l1 = max(-1, min((int)kBatchB, (int)s.last1 - (int)base)) * 16;
         for (int q = cnt - 1; q >= 0; --q) {
             const uint32_t le = lds_u16(a_list + 2 * q);
-            const int k = (int)(le & 0xffu);
-            const uint32_t o16 = (uint32_t)k << 4, o4 = (uint32_t)k << 2;
+            const uint32_t o16 = le & 0x0ff0u, o4 = o16 >> 2;
             const int4 hdr = lds_i4(a_hdr + o16);
-            const uint32_t idx = base + k;
             // box test: known true when the box covers the quadrant, else from
             // the staged tile-relative column/row masks
-            bool b0 = idx < s.last0, b1 = idx < s.last1;
-            if (!(le >> 8)) {
+            bool b0 = (int)o16 < l0, b1 = (int)o16 < l1;
+            if (!(le & 0x8000u)) {
                 const uint32_t bm = lds_u32(a_bm + o4);
                 const bool colin = (bm >> cshift) & 1u;
                 b0 = b0 & colin & ((bm >> rshift0) & 1u);

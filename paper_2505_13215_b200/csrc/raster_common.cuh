@@ -198,7 +198,8 @@ struct SplatBatch {
 
 // The staged batch's splats that warp `warp` (8x8 quadrant (warp & 1,
 // warp >> 1) of the tile) has to walk: quadrant-mask bit set, in batch order,
-// each entry k | (the pixel box covers the whole quadrant) << 8 -- for those
+// each entry k << 4 (the byte offset of the splat's 16-byte SoA slots) |
+// (the pixel box covers the whole quadrant) << 15 -- for those
 // the per-pixel box test is known true.  Built by the warp itself from the
 // staged masks (one ballot per 32 splats), so the hot loops run only over
 // their warp's splats without per-splat mask and box bit tests.
@@ -219,7 +220,7 @@ __device__ __forceinline__ int build_warp_list(const uint32_t* __restrict__ qm, 
             full = ((m & colm) == colm && (m & rowm) == rowm) ? 1u : 0u;
         }
         const uint32_t bal = __ballot_sync(0xffffffffu, in);
-        if (in) list[cnt + __popc(bal & lt)] = (uint16_t)(k | (full << 8));
+        if (in) list[cnt + __popc(bal & lt)] = (uint16_t)((k << 4) | (full << 15));
         cnt += __popc(bal);
     }
     __syncwarp();

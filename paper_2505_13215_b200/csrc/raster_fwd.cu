@@ -623,12 +623,12 @@ __global__ void __launch_bounds__(kThreads, 6) raster_fwd_kernel(
             if (b0 || b1) ++n_it;
 #endif
             const uint32_t le = lds_u16(a_list + 2 * q);
-            const int k = (int)(le & 0xffu);
-            const uint32_t o16 = (uint32_t)k << 4, o4 = (uint32_t)k << 2;
+            const uint32_t o16 = le & 0x0ff0u, o4 = o16 >> 2;
+            const int k = (int)(o16 >> 4);
             const int4 hdr = lds_i4(a_hdr + o16);
             // box test: known true when the box covers the quadrant, else from
             // the staged tile-relative column/row masks
-            if (!(le >> 8)) {
+            if (!(le & 0x8000u)) {
                 const uint32_t bm = lds_u32(a_bm + o4);
                 const bool colin = (bm >> cshift) & 1u;
                 b0 = b0 & colin & ((bm >> rshift0) & 1u);
