@@ -195,12 +195,13 @@ __global__ void __launch_bounds__(256) ssim_fwd_kernel(const float* __restrict__
             const float var_a = m[o][2] - mu_a * mu_a, var_b = m[o][3] - mu_b * mu_b, cov = m[o][4] - mu_a * mu_b;
             const float a1 = 2.f * mu_a * mu_b + C1, a2 = 2.f * cov + C2;
             const float b1 = mu_a * mu_a + mu_b * mu_b + C1, b2 = var_a + var_b + C2;
-            const float denom = b1 * b2;
-            const float sv = a1 * a2 / denom;
+            // one reciprocal instead of five divisions: 1/b1 = b2/denom, 1/b2 = b1/denom
+            const float inv = __frcp_rn(b1 * b2);
+            const float sv = a1 * a2 * inv;
             local += sv;
-            const float d_mu = (a2 / denom) * 2.f * mu_b - (sv / b1) * 2.f * mu_a;
-            const float d_var = -sv / b2;
-            const float d_cov = 2.f * a1 / denom;
+            const float d_mu = (a2 * inv) * 2.f * mu_b - (sv * (b2 * inv)) * 2.f * mu_a;
+            const float d_var = -sv * (b1 * inv);
+            const float d_cov = 2.f * a1 * inv;
             const size_t off = (size_t)c * 3 * plane + (size_t)vy * vw + vx;
             maps[off] = d_mu - 2.f * d_var * mu_a - d_cov * mu_b;
             maps[off + plane] = d_var;
