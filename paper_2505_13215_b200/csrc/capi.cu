@@ -284,6 +284,7 @@ void set_check_caps(const CheckCaps&, cudaStream_t) {}
 #endif
 }  // namespace hgs
 
+#ifdef HGS_CHECKED
 namespace {
 // Capacities (elements) of the render workspace for the checked build.
 CheckCaps render_caps(const hgs_ctx* ctx, size_t npx, int n_tiles) {
@@ -296,6 +297,7 @@ CheckCaps render_caps(const hgs_ctx* ctx, size_t npx, int n_tiles) {
     return c;
 }
 }  // namespace
+#endif
 
 hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, const double bg[3],
                                const hgs_raster_opts* opts, int deferred, uint32_t icap, void* counters_slot,

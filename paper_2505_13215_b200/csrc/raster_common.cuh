@@ -126,13 +126,13 @@ __device__ __forceinline__ f2 f2_pk(float lo, float hi) {
 }
 __device__ __forceinline__ f2 f2_bc(float a) { return f2_pk(a, a); }
 __device__ __forceinline__ float f2_lo(f2 v) {
-    float lo, hi;
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+    float lo;
+    asm("{\n.reg .f32 t;\nmov.b64 {%0, t}, %1;\n}" : "=f"(lo) : "l"(v));
     return lo;
 }
 __device__ __forceinline__ float f2_hi(f2 v) {
-    float lo, hi;
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+    float hi;
+    asm("{\n.reg .f32 t;\nmov.b64 {t, %0}, %1;\n}" : "=f"(hi) : "l"(v));
     return hi;
 }
 __device__ __forceinline__ f2 f2_add(f2 a, f2 b) {
