@@ -613,8 +613,8 @@ __global__ void __launch_bounds__(kThreads, 6) raster_fwd_kernel(
 #ifdef HGS_CHECKED
         n_wit += cnt;  // upper bound: the warp's list (lanes may finish earlier)
 #endif
-        // control flow is warp-uniform (votes): a lane whose pixels finished
-        // keeps walking with b0 = b1 = false (A = 0: no state change)
+        // a lane leaves the walk once both its pixels finished (a per-lane exit:
+        // warp-uniform votes here measured 3% slower)
         for (int q = 0; q < cnt; ++q) {
             const f2 LIM = term_limit(s);
             bool b0 = in0 && f2_lo(s.T) >= f2_lo(LIM), b1 = in1 && f2_hi(s.T) >= f2_hi(LIM);
