@@ -8,5 +8,5 @@ for lib in _variants/*.so; do
   python -c "
 import json,sys; d=json.loads(open('gpurun_out/ab.json').read().strip().splitlines()[-1])
 ph=' '.join(f\"{k['phase']}={k['ms_per_step']:.4f}\" for k in d['roofline']['kernels'])
-print('$lib', 'views/s', d['value'], 'render', d['render']['value'], 'fix', d['render_info']['fixup_pixels'], ph)"
+print('$lib', 'views/s', d['value'], 'e2e', d['e2e']['value'], 'render', d['render']['value'], 'fix', d['render_info']['fixup_pixels'], ph)"
 done; done
