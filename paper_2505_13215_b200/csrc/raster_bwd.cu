@@ -135,7 +135,7 @@ __device__ __forceinline__ void backprop_pairs(PixBwd2& s, bool p0, bool p1, f2 
     s.T = f2_pk(p0 ? f2_lo(TI) : f2_lo(s.T), p1 ? f2_hi(TI) : f2_hi(s.T));
 }
 
-__global__ void __launch_bounds__(kThreadsB, 7) raster_bwd_kernel(
+__global__ void __launch_bounds__(kThreadsB, 8) raster_bwd_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ inst_val, const SplatFast* __restrict__ fast,
     const SplatRec* __restrict__ exact, int W, int H, int tiles_x, const float* __restrict__ tfinal,
     const uint32_t* __restrict__ last_arr, const float* __restrict__ dL_dimg, float bg_r, float bg_g, float bg_b,

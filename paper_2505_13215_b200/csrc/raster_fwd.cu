@@ -556,7 +556,7 @@ __device__ __forceinline__ void write_pixel(const PixFwd& s, int pix, float bg_r
 // final transmittance (read by the backward) and the optional count /
 // transmittance maps.
 template <bool kCount>  // kCount: per-pixel count of box-covered splats (count_map)
-__global__ void __launch_bounds__(kThreads, 6) raster_fwd_kernel(
+__global__ void __launch_bounds__(kThreads, 8) raster_fwd_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ inst_val, const SplatFast* __restrict__ fast,
     const SplatRec* __restrict__ exact, int W, int H, int tiles_x, float bg_r, float bg_g, float bg_b,
     float* __restrict__ out_rgb, uint32_t* __restrict__ out_last, float* __restrict__ out_tfinal,
