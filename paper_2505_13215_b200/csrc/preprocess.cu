@@ -244,34 +244,37 @@ __global__ void __launch_bounds__(kPreThreads, 3) preprocess_kernel(
     unsigned long long* __restrict__ stats, uint32_t* __restrict__ flags, ShRec* __restrict__ shrec) {
     pdl_wait();  // launched with launch_pdl
     extern __shared__ __align__(128) float s_cols[];  // [row][kPreStride]
-    __shared__ __align__(8) uint64_t s_bar;
-    __shared__ uint32_t s_stat[kNumStats];
-    if (threadIdx.x < kNumStats) s_stat[threadIdx.x] = 0u;
+    // two transaction barriers: the geometry rows, then the SH rows (the FP64
+    // geometry runs while the SH rows are still in flight)
+    __shared__ __align__(8) uint64_t s_bar[2];
+    __shared__ uint32_t s_stat[kNumStats], s_done;
     const int gid = blockIdx.x * blockDim.x + threadIdx.x;
     const int n = n4 + n3;
     // the block's rows: one pool only (a block straddling the 4D/3D boundary
     // reads global memory directly)
     const int g0 = blockIdx.x * kPreThreads, g1 = min(g0 + kPreThreads, n);
     const bool staged = g1 <= n4 || g0 >= n4;
-    int soff = 0;
-    __syncthreads();  // s_stat zeroed
-    if (staged) {
-        const bool dyn = g1 <= n4;
-        const int i0 = dyn ? g0 : g0 - n4;
-        const int a0 = i0 & ~3;  // 16-byte aligned start
-        soff = i0 - a0;
-        if (threadIdx.x == 0) {
-            mbar_init(&s_bar, 1);
-            const int nrows = dyn ? rows4(deg) : rows3(deg);
+    const bool sdyn = g1 <= n4;
+    const int si0 = sdyn ? g0 : g0 - n4;
+    const int soff = staged ? si0 - (si0 & ~3) : 0;  // 16-byte aligned copy start
+    if (threadIdx.x < kNumStats) s_stat[threadIdx.x] = 0u;
+    if (threadIdx.x == 0) {
+        s_done = 0u;
+        if (staged) {
+            mbar_init(&s_bar[0], 1);
+            mbar_init(&s_bar[1], 1);
+            const int ngeo = sdyn ? R4_SH : R3_SH, nrows = sdyn ? rows4(deg) : rows3(deg);
             const uint32_t bytes = (uint32_t)(((g1 - g0 + soff + 3) & ~3) * sizeof(float));
-            mbar_arrive_expect_tx(&s_bar, bytes * (uint32_t)nrows);
-            const float* src = (dyn ? p4 : p3) + a0;
-            const int64_t cap = dyn ? cap4 : cap3;
-            for (int r = 0; r < nrows; ++r) bulk_g2s(s_cols + r * kPreStride, src + r * cap, bytes, &s_bar);
+            mbar_arrive_expect_tx(&s_bar[0], bytes * (uint32_t)ngeo);
+            mbar_arrive_expect_tx(&s_bar[1], bytes * (uint32_t)(nrows - ngeo));
+            const float* src = (sdyn ? p4 : p3) + (si0 - soff);
+            const int64_t cap = sdyn ? cap4 : cap3;
+            for (int r = 0; r < nrows; ++r)
+                bulk_g2s(s_cols + r * kPreStride, src + r * cap, bytes, &s_bar[r < ngeo ? 0 : 1]);
         }
-        __syncthreads();  // the barrier is initialised before anyone waits on it
-        mbar_wait_parity(&s_bar, 0);
     }
+    __syncthreads();  // statistics zeroed, barriers initialised
+    if (staged) mbar_wait_parity(&s_bar[0], 0);
     // parameter row `row` of this thread's Gaussian (pool P, index i)
     auto ld = [&](const float* __restrict__ P, int64_t cap, int row, int i) -> float {
         return staged ? s_cols[row * kPreStride + soff + (int)threadIdx.x] : __ldg(&P[(int64_t)row * cap + i]);
@@ -399,6 +402,7 @@ __global__ void __launch_bounds__(kPreThreads, 3) preprocess_kernel(
             const int i = gid < n4 ? gid : gid - n4;
             const int shrow = gid < n4 ? R4_SH : R3_SH;
             const int K = sh_count(deg);
+            if (staged) mbar_wait_parity(&s_bar[1], 0);  // the SH rows
             float basis[16];
             sh_basis_f(fd, deg, basis);
             // coefficient-major: the 3 channel values of 4 coefficients in flight
@@ -463,9 +467,21 @@ __global__ void __launch_bounds__(kPreThreads, 3) preprocess_kernel(
         const unsigned b = __ballot_sync(full, reason == want);
         if ((threadIdx.x & 31) == 0 && b) atomicAdd(&s_stat[k], (uint32_t)__popc(b));
     }
-    __syncthreads();
-    if (threadIdx.x < kNumStats && s_stat[threadIdx.x])
-        atomicAdd(&stats[(blockIdx.x % kStatStripes) * kStatStride + threadIdx.x], (unsigned long long)s_stat[threadIdx.x]);
+    // the block's last warp to get here flushes the totals (no block barrier:
+    // warps of culled Gaussians leave early instead of waiting for the rest)
+    uint32_t last = 0;
+    if ((threadIdx.x & 31) == 0) {
+        __threadfence_block();
+        last = atomicAdd(&s_done, 1u) == blockDim.x / 32 - 1 ? 1u : 0u;
+    }
+    if (__shfl_sync(full, last, 0)) {
+        __threadfence_block();
+        const int lane = threadIdx.x & 31;
+        if (lane < kNumStats) {
+            const uint32_t v = atomicAdd(&s_stat[lane], 0u);  // (an atomic read: ordered after the others)
+            if (v) atomicAdd(&stats[(blockIdx.x % kStatStripes) * kStatStride + lane], (unsigned long long)v);
+        }
+    }
     const unsigned fb = __reduce_or_sync(full, flag);
     if ((threadIdx.x & 31) == 0 && fb) atomicOr(flags, fb);
 }
