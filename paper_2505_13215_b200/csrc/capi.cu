@@ -342,6 +342,7 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
     if (want_trans) CK(ctx->trans.ensure(npx * sizeof(float)));
     if (want_count) CK(ctx->count.ensure(npx * sizeof(uint32_t)));
     CK(ctx->ranges.ensure((size_t)n_tiles * sizeof(uint2)));
+    CK(ctx->tile_order.ensure((size_t)n_tiles * sizeof(uint32_t)));
     zj.add(ctx->ranges.p, (size_t)n_tiles * sizeof(uint2));
     if (N > 0) {
         CK(ctx->sorted_of_gid.ensure((size_t)N * 4));
@@ -568,7 +569,7 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
         want_count, n_tiles, st, ctx->ranges.as<uint2>(), inst_vals, ctx->fast_sorted.as<SplatFast>(), ctx->rec_sorted.as<SplatRec>(), W, H,
         tiles_x, (float)bg[0], (float)bg[1], (float)bg[2], ctx->img.as<float>(), ctx->last.as<uint32_t>(),
         ctx->tfinal.as<float>(), want_trans ? ctx->trans.as<float>() : nullptr, want_count ? ctx->count.as<uint32_t>() : nullptr,
-        ctx->fix_list.as<uint32_t>(), &dc->fix_count);
+        ctx->fix_list.as<uint32_t>(), &dc->fix_count, tile_order_enabled() ? ctx->tile_order.as<uint32_t>() : nullptr);
     count_launch();
     CKL();
     CK(launch_pdl(raster_fixup_kernel, dim3(ctx->sms * 2), dim3(128), 0, st, ctx->fix_list.as<uint32_t>(),
@@ -1143,6 +1144,11 @@ hgs_status hgs_debug_instance_masks(hgs_ctx* ctx, uint8_t* masks, int64_t cap, i
 
 namespace hgs {
 // programmatic dependent launches (raster_common.cuh launch_pdl): on unless HGS_NO_PDL is set
+bool tile_order_enabled() {  // HGS_NO_TILE_ORDER=1: row-major tile launch order
+    static const bool on = !getenv("HGS_NO_TILE_ORDER");
+    return on;
+}
+
 bool pdl_enabled() {
     static const bool on = getenv("HGS_NO_PDL") == nullptr;
     return on;

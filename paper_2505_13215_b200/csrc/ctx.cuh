@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <deque>
 #include <string>
 #include <vector>
@@ -64,12 +66,17 @@ struct ZeroJob {
     uint64_t words;  // 32-bit words
     uint32_t value;
 };
-constexpr int kMaxZeroJobs = 8;
+constexpr int kMaxZeroJobs = 10;
 struct ZeroJobs {
     ZeroJob j[kMaxZeroJobs];
     int n = 0;
     void add(void* p, uint64_t bytes, uint32_t value = 0u) {
-        if (bytes) j[n++] = ZeroJob{p, bytes / 4, value};
+        if (!bytes) return;
+        if (n >= kMaxZeroJobs) {  // a programming error: more fills than the launch carries
+            fprintf(stderr, "hgs: ZeroJobs overflow\n");
+            abort();
+        }
+        j[n++] = ZeroJob{p, bytes / 4, value};
     }
 };
 
@@ -150,6 +157,7 @@ struct hgs_ctx {
     hgs::DBuf shdir, ddir;  // K1 view direction + clamp mask; K7b dL/d(direction)
     hgs::DBuf inst_k, inst_v, inst_k2, inst_v2;       // tile sort (I)
     hgs::DBuf ranges, scan_ws, sort_ws, inst_flag, inst_pos;
+    hgs::DBuf tile_order;  // the rasterizers' tile launch order (heaviest first; K4 and K6)
     hgs::DBuf dbg_k, dbg_v;         // the reference's full sorted instance list (debug / count_map)
     bool debug_full_list = false;   // hgs_debug_keep_instances
     hgs::DBuf counters;  // [0..5] stats u64, [6] flags, fix_count, totals...

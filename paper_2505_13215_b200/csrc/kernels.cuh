@@ -47,7 +47,7 @@ void set_debug_terr(float v);
 void launch_raster_fwd(bool count_map, int n_tiles, cudaStream_t st, const uint2* ranges, const uint32_t* inst_val,
                        const SplatFast* fast, const SplatRec* exact, int W, int H, int tiles_x, float bg_r, float bg_g,
                        float bg_b, float* out_rgb, uint32_t* out_last, float* out_tfinal, float* out_trans,
-                       uint32_t* out_count, uint32_t* fix_list, uint32_t* fix_count);
+                       uint32_t* out_count, uint32_t* fix_list, uint32_t* fix_count, uint32_t* tile_order);
 __global__ void raster_fixup_kernel(const uint32_t* __restrict__ fix_list, const uint32_t* __restrict__ fix_count,
                                     const uint2* __restrict__ ranges, const uint32_t* __restrict__ inst_val,
                                     const SplatRec* __restrict__ exact, int W, int tiles_x, double bg_r, double bg_g,
@@ -75,7 +75,7 @@ __global__ void raster_bwd_kernel(const uint2* __restrict__ ranges, const uint32
                                   const SplatFast* __restrict__ fast, const SplatRec* __restrict__ exact, int W, int H,
                                   int tiles_x, const float* __restrict__ tfinal, const uint32_t* __restrict__ last_arr,
                                   const float* __restrict__ dL_dimg, float bg_r, float bg_g, float bg_b,
-                                  acc_t* __restrict__ accum);
+                                  acc_t* __restrict__ accum, const uint32_t* __restrict__ tile_order);
 __global__ void raster_bwd_exact_kernel(const uint32_t* __restrict__ fix_list, const uint32_t* __restrict__ fix_count,
                                         int all_pixels, const uint2* __restrict__ ranges,
                                         const uint32_t* __restrict__ inst_val, const SplatRec* __restrict__ exact,

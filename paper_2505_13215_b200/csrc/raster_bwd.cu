@@ -139,12 +139,12 @@ __global__ void __launch_bounds__(kThreadsB, 8) raster_bwd_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ inst_val, const SplatFast* __restrict__ fast,
     const SplatRec* __restrict__ exact, int W, int H, int tiles_x, const float* __restrict__ tfinal,
     const uint32_t* __restrict__ last_arr, const float* __restrict__ dL_dimg, float bg_r, float bg_g, float bg_b,
-    acc_t* __restrict__ accum) {
+    acc_t* __restrict__ accum, const uint32_t* __restrict__ tile_order) {
     pdl_wait();  // launched with launch_pdl
     __shared__ SplatBatch<kBatchB> sb;
     __shared__ uint16_t s_list[kThreadsB / 32][kBatchB];  // per-warp splat lists (build_warp_list)
     __shared__ uint32_t s_maxlast;
-    const int tile = blockIdx.x;
+    const int tile = tile_order ? (int)tile_order[blockIdx.x] : (int)blockIdx.x;  // heaviest tiles first
     const int tx = tile % tiles_x, ty = tile / tiles_x;
     // warp w owns the 8x8 quadrant (w & 1, w >> 1); a lane owns rows y, y+4
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;

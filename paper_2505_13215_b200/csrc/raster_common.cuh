@@ -97,7 +97,8 @@ static __device__ __noinline__ float2 exact_delta(const SplatRec* e, double pcx,
 // normally launched kernel.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
-bool pdl_enabled();  // capi.cu: HGS_NO_PDL unset
+bool pdl_enabled();         // capi.cu: HGS_NO_PDL unset
+bool tile_order_enabled();  // capi.cu: HGS_NO_TILE_ORDER unset
 
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,

@@ -471,6 +471,49 @@ __global__ void __launch_bounds__(256) tile_ranges_dev_kernel(const uint32_t* __
     if (i == n - 1 || keys[i + 1] != t) ranges[t].y = (uint32_t)(i + 1);
 }
 
+// The rasterizers' launch order: tiles by descending instance count
+// (counting sort on len / 8, capped; order within a bucket arbitrary), so the
+// longest tiles start in the first wave and the last wave holds short ones
+// (the tail of a K4 / K6 launch was ~5% of its duration).  One CTA.
+// K6 uses the same order (ordering it by its own walk lengths, written by K4,
+// measured 2% slower: the extra launch and a worse proxy).
+__global__ void __launch_bounds__(1024) tile_order_kernel(const uint2* __restrict__ ranges, int n_tiles,
+                                                          uint32_t* __restrict__ order) {
+    pdl_wait();  // launched with launch_pdl
+    __shared__ uint32_t hist[256];
+    const int tid = threadIdx.x;
+    if (tid < 256) hist[tid] = 0u;
+    __syncthreads();
+    auto bucket = [&](int t) {
+        const uint2 r = ranges[t];
+        return 255u - min((r.y - r.x) >> 3, 255u);  // heaviest first
+    };
+    for (int t = tid; t < n_tiles; t += blockDim.x) atomicAdd(&hist[bucket(t)], 1u);
+    __syncthreads();
+    if (tid < 32) {  // exclusive scan of the 256 buckets, 8 per lane
+        uint32_t v[8], run = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            v[q] = hist[tid * 8 + q];
+            run += v[q];
+        }
+        uint32_t incl = run;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+            if (tid >= o) incl += u;
+        }
+        uint32_t ex = incl - run;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            hist[tid * 8 + q] = ex;
+            ex += v[q];
+        }
+    }
+    __syncthreads();
+    for (int t = tid; t < n_tiles; t += blockDim.x) order[atomicAdd(&hist[bucket(t)], 1u)] = (uint32_t)t;
+}
+
 constexpr int kBatch = 256;
 constexpr int kThreads = 128;  // 16x16 tile, two pixels (rows y and y+8) per thread
 
@@ -561,11 +604,11 @@ __global__ void __launch_bounds__(kThreads, 8) raster_fwd_kernel(
     const SplatRec* __restrict__ exact, int W, int H, int tiles_x, float bg_r, float bg_g, float bg_b,
     float* __restrict__ out_rgb, uint32_t* __restrict__ out_last, float* __restrict__ out_tfinal,
     float* __restrict__ out_trans, uint32_t* __restrict__ out_count, uint32_t* __restrict__ fix_list,
-    uint32_t* __restrict__ fix_count) {
+    uint32_t* __restrict__ fix_count, const uint32_t* __restrict__ tile_order) {
     pdl_wait();  // launched with launch_pdl
     __shared__ SplatBatch<kBatch> sb;
     __shared__ uint16_t s_list[kThreads / 32][kBatch];  // per-warp splat lists (build_warp_list)
-    const int tile = blockIdx.x;
+    const int tile = tile_order ? (int)tile_order[blockIdx.x] : (int)blockIdx.x;
     const int tx = tile % tiles_x, ty = tile / tiles_x;
     // warp w owns the 8x8 quadrant (w & 1, w >> 1); a lane owns rows y, y+4
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -707,15 +750,20 @@ __global__ void __launch_bounds__(kThreads, 8) raster_fwd_kernel(
 void launch_raster_fwd(bool count_map, int n_tiles, cudaStream_t st, const uint2* ranges, const uint32_t* inst_val,
                        const SplatFast* fast, const SplatRec* exact, int W, int H, int tiles_x, float bg_r, float bg_g,
                        float bg_b, float* out_rgb, uint32_t* out_last, float* out_tfinal, float* out_trans,
-                       uint32_t* out_count, uint32_t* fix_list, uint32_t* fix_count) {
+                       uint32_t* out_count, uint32_t* fix_list, uint32_t* fix_count, uint32_t* tile_order) {
+    if (tile_order) {
+        launch_pdl(tile_order_kernel, dim3(1), dim3(1024), 0, st, ranges, n_tiles, tile_order);
+        count_launch();
+    }
+    const uint32_t* order = tile_order;
     if (count_map)
         launch_pdl(raster_fwd_kernel<true>, dim3(n_tiles), dim3(kThreads), 0, st, ranges, inst_val, fast, exact, W, H,
                    tiles_x, bg_r, bg_g, bg_b, out_rgb, out_last, out_tfinal, out_trans, out_count, fix_list,
-                   fix_count);
+                   fix_count, order);
     else
         launch_pdl(raster_fwd_kernel<false>, dim3(n_tiles), dim3(kThreads), 0, st, ranges, inst_val, fast, exact, W,
                    H, tiles_x, bg_r, bg_g, bg_b, out_rgb, out_last, out_tfinal, out_trans, out_count, fix_list,
-                   fix_count);
+                   fix_count, order);
 }
 
 // Exact FP64 recomposite of the flagged pixels (raster.cpp:123-148), one warp

@@ -210,7 +210,8 @@ hgs_status run_backward(hgs_ctx* ctx, const float* lg, double scale, bool zeroed
                       static_cast<const uint32_t*>(ctx->inst_vals_final), ctx->fast_sorted.as<SplatFast>(),
                       ctx->rec_sorted.as<SplatRec>(), ctx->W, ctx->H, ctx->tiles_x, ctx->tfinal.as<float>(),
                       ctx->last.as<uint32_t>(), lg, (float)ctx->bg[0], (float)ctx->bg[1], (float)ctx->bg[2],
-                      ctx->accum.as<acc_t>()));
+                      ctx->accum.as<acc_t>(),
+                      static_cast<const uint32_t*>(tile_order_enabled() ? ctx->tile_order.as<uint32_t>() : nullptr)));
         count_launch();
         CKL();
         if (side) {
