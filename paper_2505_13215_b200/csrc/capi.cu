@@ -569,14 +569,8 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
         want_count, n_tiles, st, ctx->ranges.as<uint2>(), inst_vals, ctx->fast_sorted.as<SplatFast>(), ctx->rec_sorted.as<SplatRec>(), W, H,
         tiles_x, (float)bg[0], (float)bg[1], (float)bg[2], ctx->img.as<float>(), ctx->last.as<uint32_t>(),
         ctx->tfinal.as<float>(), want_trans ? ctx->trans.as<float>() : nullptr, want_count ? ctx->count.as<uint32_t>() : nullptr,
-        ctx->fix_list.as<uint32_t>(), &dc->fix_count, tile_order_enabled() ? ctx->tile_order.as<uint32_t>() : nullptr);
-    count_launch();
-    CKL();
-    CK(launch_pdl(raster_fixup_kernel, dim3(ctx->sms * 2), dim3(128), 0, st, ctx->fix_list.as<uint32_t>(),
-                  &dc->fix_count, ctx->ranges.as<uint2>(), inst_vals, ctx->rec_sorted.as<SplatRec>(), W, tiles_x,
-                  bg[0], bg[1], bg[2], ctx->img.as<float>(), ctx->last.as<uint32_t>(), ctx->tfinal.as<float>(),
-                  want_trans ? ctx->trans.as<float>() : nullptr, want_count ? ctx->count.as<uint32_t>() : nullptr,
-                  ctx->fix_cout.as<double>()));
+        ctx->fix_list.as<uint32_t>(), &dc->fix_count, tile_order_enabled() ? ctx->tile_order.as<uint32_t>() : nullptr,
+        bg[0], bg[1], bg[2], ctx->fix_cout.as<double>());
     count_launch();
     CKL();
     prof_end(ctx);

@@ -47,13 +47,9 @@ void set_debug_terr(float v);
 void launch_raster_fwd(bool count_map, int n_tiles, cudaStream_t st, const uint2* ranges, const uint32_t* inst_val,
                        const SplatFast* fast, const SplatRec* exact, int W, int H, int tiles_x, float bg_r, float bg_g,
                        float bg_b, float* out_rgb, uint32_t* out_last, float* out_tfinal, float* out_trans,
-                       uint32_t* out_count, uint32_t* fix_list, uint32_t* fix_count, uint32_t* tile_order);
-__global__ void raster_fixup_kernel(const uint32_t* __restrict__ fix_list, const uint32_t* __restrict__ fix_count,
-                                    const uint2* __restrict__ ranges, const uint32_t* __restrict__ inst_val,
-                                    const SplatRec* __restrict__ exact, int W, int tiles_x, double bg_r, double bg_g,
-                                    double bg_b, float* __restrict__ out_rgb, uint32_t* __restrict__ out_last,
-                                    float* __restrict__ out_tfinal, float* __restrict__ out_trans,
-                                    uint32_t* __restrict__ out_count, double* __restrict__ out_cout);
+                       uint32_t* out_count, uint32_t* fix_list, uint32_t* fix_count, uint32_t* tile_order,
+                       double bg_rd, double bg_gd, double bg_bd, double* out_cout);
+
 
 __global__ void grads_pack_kernel(const float* __restrict__ gbuf, int64_t off_g3, int64_t off_dgn4, int rows4,
                                   int rows3, int64_t cap4, int64_t cap3, int n4, int n3, float* __restrict__ packed,

@@ -523,6 +523,66 @@ __device__ __forceinline__ float rcp_approx(float x) {
     return y;
 }
 
+// Exact FP64 recomposite of one flagged pixel (raster.cpp:123-148) by one
+// warp over 32-splat chunks (exact_chunk: lane-parallel FP64 alphas, the
+// transmittance chain in list order, colours summed lane-parallel in FP64).
+// q: the pixel's fix-list slot (its FP64 colour goes to out_cout[q] for
+// raster_bwd_exact_kernel).  Out of line: K4 calls it after its main loop.
+static __device__ __noinline__ void fixup_pixel(uint32_t q, int pix, uint2 rg, const uint32_t* __restrict__ inst_val,
+                                               const SplatRec* __restrict__ exact, int W, double bg_r, double bg_g,
+                                               double bg_b, float* __restrict__ out_rgb, uint32_t* __restrict__ out_last,
+                                               float* __restrict__ out_tfinal, float* __restrict__ out_trans,
+                                               uint32_t* __restrict__ out_count, double* __restrict__ out_cout,
+                                               double* s_om) {
+    const int lane = threadIdx.x & 31;
+    HGS_DCHECK(pix >= 0 && (unsigned long long)pix < g_chk.pixels);
+    HGS_DCHECK(rg.x <= rg.y && rg.y <= g_chk.inst);
+    const int px = pix % W, py = pix / W;
+    const double pcx = px + 0.5, pcy = py + 0.5;
+    double T = 1.0, ar = 0.0, ag = 0.0, ab = 0.0;
+    uint32_t count = 0, last = rg.x;
+    constexpr int S = kExactSub;
+    for (uint32_t base = rg.x; base < rg.y; base += 32 * S) {
+        ExactChunk<S> c;
+        exact_chunk<S>(inst_val, exact, base, rg.y, px, py, pcx, pcy, T, s_om, c);
+        double wr = 0.0, wg = 0.0, wb = 0.0;
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            // in-box splats up to (and including) the terminating one
+            const int tl = c.term - 32 * s;
+            const uint32_t upto = (c.term < 0 || tl >= 31) ? 0xffffffffu : tl < 0 ? 0u : ((2u << tl) - 1u);
+            count += __popc(c.inmask[s] & upto);
+            if (c.contrib[s]) {
+                const double w = __dmul_rn(c.a[s], c.Ti[s]);
+                wr += c.e[s]->r * w;
+                wg += c.e[s]->g * w;
+                wb += c.e[s]->b * w;
+            }
+            const uint32_t cb = __ballot_sync(0xffffffffu, c.contrib[s]);
+            if (cb) last = base + 32 * s + (31 - __clz(cb)) + 1;
+        }
+        ar += warp_sum_d(wr);
+        ag += warp_sum_d(wg);
+        ab += warp_sum_d(wb);
+        if (c.term >= 0) break;
+    }
+    if (lane == 0) {
+        const double cr = __dadd_rn(ar, __dmul_rn(T, bg_r)), cg = __dadd_rn(ag, __dmul_rn(T, bg_g)),
+                     cb = __dadd_rn(ab, __dmul_rn(T, bg_b));
+        out_rgb[pix * 3 + 0] = (float)cr;
+        out_rgb[pix * 3 + 1] = (float)cg;
+        out_rgb[pix * 3 + 2] = (float)cb;
+        out_cout[3 * q + 0] = cr;
+        out_cout[3 * q + 1] = cg;
+        out_cout[3 * q + 2] = cb;
+        out_last[pix] = last | 0x80000000u;
+        out_tfinal[pix] = (float)T;
+        if (out_trans) out_trans[pix] = (float)T;
+        if (out_count) out_count[pix] = count;
+    }
+    __syncwarp();
+}
+
 // Per-pixel compositing state of K4.
 struct PixFwd {
     float T, r, g, b, err;
@@ -576,7 +636,7 @@ __device__ __forceinline__ void write_pixel(const PixFwd& s, int pix, float bg_r
                                             float* __restrict__ out_rgb, uint32_t* __restrict__ out_last,
                                             float* __restrict__ out_tfinal, float* __restrict__ out_trans,
                                             uint32_t* __restrict__ out_count, uint32_t* __restrict__ fix_list,
-                                            uint32_t* __restrict__ fix_count) {
+                                            uint32_t* __restrict__ fix_count, uint32_t* s_nfix, uint2* s_fix) {
     const bool flagged = s.flagged || (g_debug_exact & 2) || s.err > g_debug_terr * s.T;
     out_rgb[pix * 3 + 0] = fmaf(s.T, bg_r, s.r);
     out_rgb[pix * 3 + 1] = fmaf(s.T, bg_g, s.g);
@@ -585,7 +645,11 @@ __device__ __forceinline__ void write_pixel(const PixFwd& s, int pix, float bg_r
     out_tfinal[pix] = s.T;
     if (out_trans) out_trans[pix] = s.T;
     if (out_count) out_count[pix] = s.count;
-    if (flagged) fix_list[atomicAdd(fix_count, 1u)] = (uint32_t)pix;
+    if (flagged) {  // the fix-list slot (the backward's exact pixels) and the CTA's own list
+        const uint32_t q = atomicAdd(fix_count, 1u);
+        fix_list[q] = (uint32_t)pix;
+        s_fix[atomicAdd(s_nfix, 1u)] = make_uint2((uint32_t)pix, q);
+    }
 }
 
 // K4: one CTA (128 threads) per 16x16 tile, two pixels per thread, front-to-
@@ -604,9 +668,12 @@ __global__ void __launch_bounds__(kThreads, 8) raster_fwd_kernel(
     const SplatRec* __restrict__ exact, int W, int H, int tiles_x, float bg_r, float bg_g, float bg_b,
     float* __restrict__ out_rgb, uint32_t* __restrict__ out_last, float* __restrict__ out_tfinal,
     float* __restrict__ out_trans, uint32_t* __restrict__ out_count, uint32_t* __restrict__ fix_list,
-    uint32_t* __restrict__ fix_count, const uint32_t* __restrict__ tile_order) {
+    uint32_t* __restrict__ fix_count, const uint32_t* __restrict__ tile_order, double bg_rd, double bg_gd,
+    double bg_bd, double* __restrict__ out_cout) {
     pdl_wait();  // launched with launch_pdl
     __shared__ SplatBatch<kBatch> sb;
+    __shared__ uint32_t s_nfix;  // the CTA's pixels handed to the FP64 fix-up
+    if (threadIdx.x == 0) s_nfix = 0u;
     __shared__ uint16_t s_list[kThreads / 32][kBatch];  // per-warp splat lists (build_warp_list)
     const int tile = tile_order ? (int)tile_order[blockIdx.x] : (int)blockIdx.x;
     const int tx = tile % tiles_x, ty = tile / tiles_x;
@@ -732,17 +799,32 @@ __global__ void __launch_bounds__(kThreads, 8) raster_fwd_kernel(
     const f2 LIM = term_limit(s), LOW = f2_fma(f2_bc(-2.0f), s.E, f2_bc(1.0e-4f));
     const bool flag0 = f2_lo(s.T) < f2_lo(LIM) && f2_lo(s.T) > f2_lo(LOW);
     const bool flag1 = f2_hi(s.T) < f2_hi(LIM) && f2_hi(s.T) > f2_hi(LOW);
+    // after the walk the staged batch is dead: its memory holds the CTA's
+    // fix-up list (hdr) and the fix-up walks' transmittance factors (mean)
+    __syncthreads();
+    uint2* s_fix = reinterpret_cast<uint2*>(&sb.hdr[0]);  // <= 256 entries (pixel, fix-list slot)
     if (in0) {
         const PixFwd s0{f2_lo(s.T), f2_lo(s.r), f2_lo(s.g), f2_lo(s.b), f2_lo(s.E), s.last0, s.count0, true,
                         flag0};
         write_pixel(s0, py0 * W + px, bg_r, bg_g, bg_b, out_rgb, out_last, out_tfinal, out_trans, out_count, fix_list,
-                    fix_count);
+                    fix_count, &s_nfix, s_fix);
     }
     if (in1) {
         const PixFwd s1{f2_hi(s.T), f2_hi(s.r), f2_hi(s.g), f2_hi(s.b), f2_hi(s.E), s.last1, s.count1, true,
                         flag1};
         write_pixel(s1, py1 * W + px, bg_r, bg_g, bg_b, out_rgb, out_last, out_tfinal, out_trans, out_count, fix_list,
-                    fix_count);
+                    fix_count, &s_nfix, s_fix);
+    }
+    // the FP64 fix-up of this tile's flagged pixels (~0.1% of the pixels), one
+    // warp per pixel, inside the CTA: the walks overlap the other CTAs' work
+    // instead of forming a serial tail kernel
+    __syncthreads();
+    const uint32_t nfix = s_nfix;
+    double* s_om = reinterpret_cast<double*>(&sb.mean[0]) + warp * (32 * kExactSub);
+    for (uint32_t k = warp; k < nfix; k += kThreads / 32) {
+        const uint2 f = s_fix[k];
+        fixup_pixel(f.y, (int)f.x, rg, inst_val, exact, W, bg_rd, bg_gd, bg_bd, out_rgb, out_last, out_tfinal,
+                    out_trans, out_count, out_cout, s_om);
     }
 }
 
@@ -750,7 +832,8 @@ __global__ void __launch_bounds__(kThreads, 8) raster_fwd_kernel(
 void launch_raster_fwd(bool count_map, int n_tiles, cudaStream_t st, const uint2* ranges, const uint32_t* inst_val,
                        const SplatFast* fast, const SplatRec* exact, int W, int H, int tiles_x, float bg_r, float bg_g,
                        float bg_b, float* out_rgb, uint32_t* out_last, float* out_tfinal, float* out_trans,
-                       uint32_t* out_count, uint32_t* fix_list, uint32_t* fix_count, uint32_t* tile_order) {
+                       uint32_t* out_count, uint32_t* fix_list, uint32_t* fix_count, uint32_t* tile_order,
+                       double bg_rd, double bg_gd, double bg_bd, double* out_cout) {
     if (tile_order) {
         launch_pdl(tile_order_kernel, dim3(1), dim3(1024), 0, st, ranges, n_tiles, tile_order);
         count_launch();
@@ -759,79 +842,11 @@ void launch_raster_fwd(bool count_map, int n_tiles, cudaStream_t st, const uint2
     if (count_map)
         launch_pdl(raster_fwd_kernel<true>, dim3(n_tiles), dim3(kThreads), 0, st, ranges, inst_val, fast, exact, W, H,
                    tiles_x, bg_r, bg_g, bg_b, out_rgb, out_last, out_tfinal, out_trans, out_count, fix_list,
-                   fix_count, order);
+                   fix_count, order, bg_rd, bg_gd, bg_bd, out_cout);
     else
         launch_pdl(raster_fwd_kernel<false>, dim3(n_tiles), dim3(kThreads), 0, st, ranges, inst_val, fast, exact, W,
                    H, tiles_x, bg_r, bg_g, bg_b, out_rgb, out_last, out_tfinal, out_trans, out_count, fix_list,
-                   fix_count, order);
-}
-
-// Exact FP64 recomposite of the flagged pixels (raster.cpp:123-148), one warp
-// per pixel over 32-splat chunks (exact_chunk: lane-parallel FP64 alphas, the
-// transmittance chain in list order, colours summed lane-parallel in FP64).
-__global__ void __launch_bounds__(128) raster_fixup_kernel(
-    const uint32_t* __restrict__ fix_list, const uint32_t* __restrict__ fix_count, const uint2* __restrict__ ranges,
-    const uint32_t* __restrict__ inst_val, const SplatRec* __restrict__ exact, int W, int tiles_x, double bg_r,
-    double bg_g, double bg_b, float* __restrict__ out_rgb, uint32_t* __restrict__ out_last,
-    float* __restrict__ out_tfinal, float* __restrict__ out_trans, uint32_t* __restrict__ out_count,
-    double* __restrict__ out_cout) {
-    pdl_wait();  // launched with launch_pdl
-    __shared__ double s_om[4][32 * kExactSub];
-    const uint32_t n = *fix_count;
-    HGS_DCHECK(n <= g_chk.pixels);
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const uint32_t warps = gridDim.x * (blockDim.x >> 5);
-    for (uint32_t q = blockIdx.x * (blockDim.x >> 5) + wib; q < n; q += warps) {
-        const int pix = (int)fix_list[q];
-        HGS_DCHECK(pix >= 0 && (unsigned long long)pix < g_chk.pixels);
-        const int px = pix % W, py = pix / W;
-        const uint2 rg = ranges[(py / kTile) * tiles_x + px / kTile];
-        HGS_DCHECK(rg.x <= rg.y && rg.y <= g_chk.inst);
-        const double pcx = px + 0.5, pcy = py + 0.5;
-        double T = 1.0, ar = 0.0, ag = 0.0, ab = 0.0;
-        uint32_t count = 0, last = rg.x;
-        constexpr int S = kExactSub;
-        for (uint32_t base = rg.x; base < rg.y; base += 32 * S) {
-            ExactChunk<S> c;
-            exact_chunk<S>(inst_val, exact, base, rg.y, px, py, pcx, pcy, T, s_om[wib], c);
-            double wr = 0.0, wg = 0.0, wb = 0.0;
-#pragma unroll
-            for (int s = 0; s < S; ++s) {
-                // in-box splats up to (and including) the terminating one
-                const int tl = c.term - 32 * s;
-                const uint32_t upto = (c.term < 0 || tl >= 31) ? 0xffffffffu : tl < 0 ? 0u : ((2u << tl) - 1u);
-                count += __popc(c.inmask[s] & upto);
-                if (c.contrib[s]) {
-                    const double w = __dmul_rn(c.a[s], c.Ti[s]);
-                    wr += c.e[s]->r * w;
-                    wg += c.e[s]->g * w;
-                    wb += c.e[s]->b * w;
-                }
-                const uint32_t cb = __ballot_sync(0xffffffffu, c.contrib[s]);
-                if (cb) last = base + 32 * s + (31 - __clz(cb)) + 1;
-            }
-            ar += warp_sum_d(wr);
-            ag += warp_sum_d(wg);
-            ab += warp_sum_d(wb);
-            if (c.term >= 0) break;
-        }
-        if (lane == 0) {
-            const double cr = __dadd_rn(ar, __dmul_rn(T, bg_r)), cg = __dadd_rn(ag, __dmul_rn(T, bg_g)),
-                         cb = __dadd_rn(ab, __dmul_rn(T, bg_b));
-            out_rgb[pix * 3 + 0] = (float)cr;
-            out_rgb[pix * 3 + 1] = (float)cg;
-            out_rgb[pix * 3 + 2] = (float)cb;
-            if (out_cout) {  // the FP64 pixel colour for raster_bwd_exact_kernel (fix-list order)
-                out_cout[3 * q + 0] = cr;
-                out_cout[3 * q + 1] = cg;
-                out_cout[3 * q + 2] = cb;
-            }
-            out_last[pix] = last | 0x80000000u;
-            out_tfinal[pix] = (float)T;
-            if (out_trans) out_trans[pix] = (float)T;
-            if (out_count) out_count[pix] = count;
-        }
-    }
+                   fix_count, order, bg_rd, bg_gd, bg_bd, out_cout);
 }
 
 // ---- density_map (raster.cpp:268-287)
