@@ -339,6 +339,7 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
     CK(ctx->tfinal.ensure(npx * sizeof(float)));
     CK(ctx->fix_list.ensure(npx * sizeof(uint32_t)));
     CK(ctx->fix_cout.ensure(npx * 3 * sizeof(double)));
+    CK(ctx->fix_slot.ensure(npx * sizeof(uint32_t)));
     if (want_trans) CK(ctx->trans.ensure(npx * sizeof(float)));
     if (want_count) CK(ctx->count.ensure(npx * sizeof(uint32_t)));
     CK(ctx->ranges.ensure((size_t)n_tiles * sizeof(uint2)));
@@ -570,7 +571,7 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
         tiles_x, (float)bg[0], (float)bg[1], (float)bg[2], ctx->img.as<float>(), ctx->last.as<uint32_t>(),
         ctx->tfinal.as<float>(), want_trans ? ctx->trans.as<float>() : nullptr, want_count ? ctx->count.as<uint32_t>() : nullptr,
         ctx->fix_list.as<uint32_t>(), &dc->fix_count, tile_order_enabled() ? ctx->tile_order.as<uint32_t>() : nullptr,
-        bg[0], bg[1], bg[2], ctx->fix_cout.as<double>());
+        bg[0], bg[1], bg[2], ctx->fix_cout.as<double>(), ctx->fix_slot.as<uint32_t>());
     count_launch();
     CKL();
     prof_end(ctx);
@@ -712,9 +713,6 @@ void hgs_ctx_destroy(hgs_ctx* ctx) {
         if (ctx->gt_free[b]) cudaEventDestroy(ctx->gt_free[b]);
     }
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
-    if (ctx->side_stream) cudaStreamDestroy(ctx->side_stream);
-    if (ctx->side_fork) cudaEventDestroy(ctx->side_fork);
-    if (ctx->side_join) cudaEventDestroy(ctx->side_join);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;
 }

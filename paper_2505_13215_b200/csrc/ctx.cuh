@@ -163,6 +163,7 @@ struct hgs_ctx {
     hgs::DBuf counters;  // [0..5] stats u64, [6] flags, fix_count, totals...
     hgs::DBuf img, last, tfinal, trans, count, fix_list;
     hgs::DBuf fix_cout;  // FP64 colours of the fix-up pixels (forward fix-up -> exact backward)
+    hgs::DBuf fix_slot;  // per pixel: its fix-list slot (written for the fix-up pixels only)
     hgs::DBuf accum;     // backward per-sorted-splat accumulators
     bool exact_backward = false;  // hgs_set_exact_backward: FP64 pair terms for every pixel
     hgs::DBuf exact_col;          // its FP64 colours (sorted order)
@@ -171,8 +172,6 @@ struct hgs_ctx {
     hgs::DBuf gt_stage;  // staged ground truth
     hgs::DBuf gt_buf[2], gt_stage64[2];  // double-buffered host GT of the training step
     cudaStream_t copy_stream = nullptr;  // host -> device GT copies, overlapped with the render
-    cudaStream_t side_stream = nullptr;  // the FP64 fix-up backward, concurrent with K6
-    cudaEvent_t side_fork = nullptr, side_join = nullptr;
     cudaEvent_t gt_ready[2] = {nullptr, nullptr}, gt_free[2] = {nullptr, nullptr};
     hgs::DBuf loss_ws;   // loss scratch (SSIM maps)
     hgs::DBuf scratch;   // small device scalars (loss sums, skip counts, leakage)

@@ -48,7 +48,7 @@ void launch_raster_fwd(bool count_map, int n_tiles, cudaStream_t st, const uint2
                        const SplatFast* fast, const SplatRec* exact, int W, int H, int tiles_x, float bg_r, float bg_g,
                        float bg_b, float* out_rgb, uint32_t* out_last, float* out_tfinal, float* out_trans,
                        uint32_t* out_count, uint32_t* fix_list, uint32_t* fix_count, uint32_t* tile_order,
-                       double bg_rd, double bg_gd, double bg_bd, double* out_cout);
+                       double bg_rd, double bg_gd, double bg_bd, double* out_cout, uint32_t* fix_slot);
 
 
 __global__ void grads_pack_kernel(const float* __restrict__ gbuf, int64_t off_g3, int64_t off_dgn4, int rows4,
@@ -71,14 +71,14 @@ __global__ void raster_bwd_kernel(const uint2* __restrict__ ranges, const uint32
                                   const SplatFast* __restrict__ fast, const SplatRec* __restrict__ exact, int W, int H,
                                   int tiles_x, const float* __restrict__ tfinal, const uint32_t* __restrict__ last_arr,
                                   const float* __restrict__ dL_dimg, float bg_r, float bg_g, float bg_b,
-                                  acc_t* __restrict__ accum, const uint32_t* __restrict__ tile_order);
-__global__ void raster_bwd_exact_kernel(const uint32_t* __restrict__ fix_list, const uint32_t* __restrict__ fix_count,
-                                        int all_pixels, const uint2* __restrict__ ranges,
+                                  acc_t* __restrict__ accum, const uint32_t* __restrict__ tile_order,
+                                  const uint32_t* __restrict__ fix_slot, const double* __restrict__ fix_cout,
+                                  double bg_rd, double bg_gd, double bg_bd);
+__global__ void raster_bwd_exact_kernel(int all_pixels, const uint2* __restrict__ ranges,
                                         const uint32_t* __restrict__ inst_val, const SplatRec* __restrict__ exact,
                                         int W, int tiles_x, double bg_r, double bg_g, double bg_b,
                                         const uint32_t* __restrict__ last_arr, const float* __restrict__ dL_dimg,
-                                        const double* __restrict__ col64, acc_t* __restrict__ accum,
-                                        const double* __restrict__ fix_cout);
+                                        const double* __restrict__ col64, acc_t* __restrict__ accum);
 __global__ void exact_colour_kernel(const uint32_t* __restrict__ sorted_gid, int V, int n4,
                                     const float* __restrict__ p4, int64_t cap4, const float* __restrict__ p3,
                                     int64_t cap3, int deg, DevCamera cam, double t, double* __restrict__ col64);

@@ -135,13 +135,131 @@ __device__ __forceinline__ void backprop_pairs(PixBwd2& s, bool p0, bool p1, f2 
     s.T = f2_pk(p0 ? f2_lo(TI) : f2_lo(s.T), p1 ? f2_hi(TI) : f2_hi(s.T));
 }
 
+// FP64 backward of one pixel (backward.cpp:182-221) by one warp over 32-splat
+// chunks (exact_chunk).  Pass 0 recomposites the pixel to get C_out (skipped
+// when the forward fix-up's FP64 colour `cout` is given); pass 1 walks the
+// list again, forms the inclusive colour prefix P_i with a warp scan, and
+// every contributing lane emits its gradient with
+// d_a = g.(c T_i - (C_out - P_i)/(1 - a)) (in FP64 the subtraction is exact
+// enough) via global atomics, in the accumulator layout of raster_bwd_kernel.
+// Out of line: K6 calls it for its tile's fix-up pixels after its walk.
+static __device__ __noinline__ void exact_bwd_pixel(int pix, uint2 rg, const double* __restrict__ cout,
+                                                   const uint32_t* __restrict__ inst_val,
+                                                   const SplatRec* __restrict__ exact, int W, double bg_r,
+                                                   double bg_g, double bg_b, const uint32_t* __restrict__ last_arr,
+                                                   const float* __restrict__ dL_dimg,
+                                                   const double* __restrict__ col64, acc_t* __restrict__ accum,
+                                                   double* s_om) {
+    const int lane = threadIdx.x & 31;
+    HGS_DCHECK(pix >= 0 && (unsigned long long)pix < g_chk.pixels);
+    const double gp[3] = {dL_dimg[pix * 3], dL_dimg[pix * 3 + 1], dL_dimg[pix * 3 + 2]};
+    if (fabs(gp[0]) <= 1e-12 && fabs(gp[1]) <= 1e-12 && fabs(gp[2]) <= 1e-12) return;  // isZero, backward.cpp:189
+    const int px = pix % W, py = pix / W;
+    const uint32_t last = last_arr[pix] & 0x7fffffffu;
+    HGS_DCHECK(rg.x <= rg.y && rg.y <= g_chk.inst && last <= rg.y);
+    const double pcx = px + 0.5, pcy = py + 0.5;
+    double Cout[3];
+    int pass0 = 0;
+    if (cout) {
+        Cout[0] = cout[0];
+        Cout[1] = cout[1];
+        Cout[2] = cout[2];
+        pass0 = 1;
+    }
+    for (int pass = pass0; pass < 2; ++pass) {
+        double T = 1.0, P[3] = {0.0, 0.0, 0.0};
+        constexpr int S = kExactSub;
+        for (uint32_t base = rg.x; base < last; base += 32 * S) {
+            ExactChunk<S> c;
+            exact_chunk<S>(inst_val, exact, base, last, px, py, pcx, pcy, T, s_om, c);
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                double wc[3] = {0.0, 0.0, 0.0}, w = 0.0, rgb[3] = {0.0, 0.0, 0.0};
+                if (c.contrib[s]) {
+                    if (col64) {  // exact mode: the FP64 colours
+                        const double* cc = col64 + 3 * (size_t)(c.e[s] - exact);
+                        rgb[0] = cc[0];
+                        rgb[1] = cc[1];
+                        rgb[2] = cc[2];
+                    } else {
+                        rgb[0] = c.e[s]->r;
+                        rgb[1] = c.e[s]->g;
+                        rgb[2] = c.e[s]->b;
+                    }
+                    w = __dmul_rn(c.a[s], c.Ti[s]);
+                    wc[0] = rgb[0] * w;
+                    wc[1] = rgb[1] * w;
+                    wc[2] = rgb[2] * w;
+                }
+                if (pass == 0) {
+                    for (int k = 0; k < 3; ++k) P[k] += warp_sum_d(wc[k]);
+                    continue;
+                }
+                // inclusive prefix of this 32-splat slice (list order) on top of the running P
+                double inc[3] = {wc[0], wc[1], wc[2]};
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1)
+                    for (int k = 0; k < 3; ++k) {
+                        const double u = __shfl_up_sync(0xffffffffu, inc[k], o);
+                        if (lane >= o) inc[k] += u;
+                    }
+                if (c.contrib[s]) {
+                    const SplatRec* e = c.e[s];
+                    double d_a = 0.0;
+                    for (int k = 0; k < 3; ++k)
+                        d_a += gp[k] * (rgb[k] * c.Ti[s] - (Cout[k] - (P[k] + inc[k])) / (1.0 - c.a[s]));
+                    acc_t* dst = accum + (size_t)(e - exact) * kAccStride;
+                    for (int k = 0; k < 3; ++k) atomicAdd(dst + k, w * gp[k]);
+                    const double h = c.g[s] * d_a;
+                    const double dx = pcx - e->sx, dy = pcy - e->sy;
+                    atomicAdd(dst + 3, h);
+                    atomicAdd(dst + 4, h * dx);
+                    atomicAdd(dst + 5, h * dy);
+                    atomicAdd(dst + 6, h * dx * dx);
+                    atomicAdd(dst + 7, h * dx * dy);
+                    atomicAdd(dst + 8, h * dy * dy);
+                }
+                for (int k = 0; k < 3; ++k) P[k] += __shfl_sync(0xffffffffu, inc[k], 31);
+            }
+            if (c.term >= 0) break;
+        }
+        if (pass == 0) {
+            Cout[0] = P[0] + T * bg_r;
+            Cout[1] = P[1] + T * bg_g;
+            Cout[2] = P[2] + T * bg_b;
+        }
+    }
+    __syncwarp();
+}
+
+// The exact backward mode (hgs_set_exact_backward): every pixel through
+// exact_bwd_pixel with the FP64 colours, one warp per pixel.
+__global__ void __launch_bounds__(128) raster_bwd_exact_kernel(
+    int all_pixels, const uint2* __restrict__ ranges, const uint32_t* __restrict__ inst_val,
+    const SplatRec* __restrict__ exact, int W, int tiles_x, double bg_r, double bg_g, double bg_b,
+    const uint32_t* __restrict__ last_arr, const float* __restrict__ dL_dimg, const double* __restrict__ col64,
+    acc_t* __restrict__ accum) {
+    pdl_wait();  // launched with launch_pdl
+    __shared__ double s_om[4][32 * kExactSub];
+    const int wib = threadIdx.x >> 5;
+    const uint32_t warps = gridDim.x * (blockDim.x >> 5);
+    for (uint32_t q = blockIdx.x * (blockDim.x >> 5) + wib; q < (uint32_t)all_pixels; q += warps) {
+        const int pix = (int)q;
+        const int px = pix % W, py = pix / W;
+        exact_bwd_pixel(pix, ranges[(py / kTile) * tiles_x + px / kTile], nullptr, inst_val, exact, W, bg_r, bg_g,
+                        bg_b, last_arr, dL_dimg, col64, accum, s_om[wib]);
+    }
+}
+
 __global__ void __launch_bounds__(kThreadsB, 8) raster_bwd_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ inst_val, const SplatFast* __restrict__ fast,
     const SplatRec* __restrict__ exact, int W, int H, int tiles_x, const float* __restrict__ tfinal,
     const uint32_t* __restrict__ last_arr, const float* __restrict__ dL_dimg, float bg_r, float bg_g, float bg_b,
-    acc_t* __restrict__ accum, const uint32_t* __restrict__ tile_order) {
+    acc_t* __restrict__ accum, const uint32_t* __restrict__ tile_order, const uint32_t* __restrict__ fix_slot,
+    const double* __restrict__ fix_cout, double bg_rd, double bg_gd, double bg_bd) {
     pdl_wait();  // launched with launch_pdl
     __shared__ SplatBatch<kBatchB> sb;
+    __shared__ uint32_t s_nfix, s_fix[kThreadsB * 2];  // this tile's fix-up pixels (FP64 backward after the walk)
     __shared__ uint16_t s_list[kThreadsB / 32][kBatchB];  // per-warp splat lists (build_warp_list)
     __shared__ uint32_t s_maxlast;
     const int tile = tile_order ? (int)tile_order[blockIdx.x] : (int)blockIdx.x;  // heaviest tiles first
@@ -175,8 +293,11 @@ __global__ void __launch_bounds__(kThreadsB, 8) raster_bwd_kernel(
         // for floats <= 1e-12f is the same test) leaves the pixel untouched
         const bool zero = fabsf(s.gr) <= 1e-12f && fabsf(s.gg) <= 1e-12f && fabsf(s.gb) <= 1e-12f;
         if (!(l & 0x80000000u) && !zero) s.last = l;
+        if ((l & 0x80000000u) && !zero) s_fix[atomicAdd(&s_nfix, 1u)] = (uint32_t)pix;
     };
     const int cshift = px - tx * kTile, rshift0 = 16 + py0 - ty * kTile, rshift1 = rshift0 + 4;
+    if (threadIdx.x == 0) s_nfix = 0u;
+    __syncthreads();
     PixBwd2 s;
     {
         Pix1 a0, a1;
@@ -327,109 +448,16 @@ __global__ void __launch_bounds__(kThreadsB, 8) raster_bwd_kernel(
     HGS_COUNT_PAIRS(6, n_pass);
     HGS_COUNT_PAIRS(7, n_wit);
 #endif
-}
-
-// FP64 backward of the fix-up pixels (backward.cpp:182-221), one warp per
-// pixel over 32-splat chunks (exact_chunk).  Pass 0 recomposites the pixel to
-// get C_out; pass 1 walks the list again, forms the inclusive colour prefix
-// P_i with a warp scan, and every contributing lane emits its gradient with
-// d_a = g.(c T_i - (C_out - P_i)/(1 - a)) (in FP64 the subtraction is exact
-// enough) via global atomics, in the accumulator layout of raster_bwd_kernel.
-__global__ void __launch_bounds__(128) raster_bwd_exact_kernel(
-    const uint32_t* __restrict__ fix_list, const uint32_t* __restrict__ fix_count, int all_pixels,
-    const uint2* __restrict__ ranges, const uint32_t* __restrict__ inst_val, const SplatRec* __restrict__ exact, int W,
-    int tiles_x, double bg_r, double bg_g, double bg_b, const uint32_t* __restrict__ last_arr,
-    const float* __restrict__ dL_dimg, const double* __restrict__ col64, acc_t* __restrict__ accum,
-    const double* __restrict__ fix_cout) {
-    pdl_wait();  // launched with launch_pdl
-    __shared__ double s_om[4][32 * kExactSub];
-    // the forward's fix-up pixels, or (exact backward mode) every pixel
-    const uint32_t n = fix_list ? *fix_count : (uint32_t)all_pixels;
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const uint32_t warps = gridDim.x * (blockDim.x >> 5);
-    for (uint32_t q = blockIdx.x * (blockDim.x >> 5) + wib; q < n; q += warps) {
-        const int pix = fix_list ? (int)fix_list[q] : (int)q;
-        HGS_DCHECK(pix >= 0 && (unsigned long long)pix < g_chk.pixels);
-        const double gp[3] = {dL_dimg[pix * 3], dL_dimg[pix * 3 + 1], dL_dimg[pix * 3 + 2]};
-        if (fabs(gp[0]) <= 1e-12 && fabs(gp[1]) <= 1e-12 && fabs(gp[2]) <= 1e-12) continue;  // isZero, backward.cpp:189
-        const int px = pix % W, py = pix / W;
-        const uint2 rg = ranges[(py / kTile) * tiles_x + px / kTile];
-        const uint32_t last = last_arr[pix] & 0x7fffffffu;
-        HGS_DCHECK(rg.x <= rg.y && rg.y <= g_chk.inst && last <= rg.y);
-        const double pcx = px + 0.5, pcy = py + 0.5;
-        double Cout[3];
-        // the forward fix-up already composited the flagged pixel in FP64:
-        // its colour replaces pass 0 (fix-list mode)
-        int pass0 = 0;
-        if (fix_list && fix_cout) {
-            Cout[0] = fix_cout[3 * q + 0];
-            Cout[1] = fix_cout[3 * q + 1];
-            Cout[2] = fix_cout[3 * q + 2];
-            pass0 = 1;
-        }
-        for (int pass = pass0; pass < 2; ++pass) {
-            double T = 1.0, P[3] = {0.0, 0.0, 0.0};
-            constexpr int S = kExactSub;
-            for (uint32_t base = rg.x; base < last; base += 32 * S) {
-                ExactChunk<S> c;
-                exact_chunk<S>(inst_val, exact, base, last, px, py, pcx, pcy, T, s_om[wib], c);
-#pragma unroll
-                for (int s = 0; s < S; ++s) {
-                    double wc[3] = {0.0, 0.0, 0.0}, w = 0.0, rgb[3] = {0.0, 0.0, 0.0};
-                    if (c.contrib[s]) {
-                        if (col64) {  // exact mode: the FP64 colours
-                            const double* cc = col64 + 3 * (size_t)(c.e[s] - exact);
-                            rgb[0] = cc[0];
-                            rgb[1] = cc[1];
-                            rgb[2] = cc[2];
-                        } else {
-                            rgb[0] = c.e[s]->r;
-                            rgb[1] = c.e[s]->g;
-                            rgb[2] = c.e[s]->b;
-                        }
-                        w = __dmul_rn(c.a[s], c.Ti[s]);
-                        wc[0] = rgb[0] * w;
-                        wc[1] = rgb[1] * w;
-                        wc[2] = rgb[2] * w;
-                    }
-                    if (pass == 0) {
-                        for (int k = 0; k < 3; ++k) P[k] += warp_sum_d(wc[k]);
-                        continue;
-                    }
-                    // inclusive prefix of this 32-splat slice (list order) on top of the running P
-                    double inc[3] = {wc[0], wc[1], wc[2]};
-#pragma unroll
-                    for (int o = 1; o < 32; o <<= 1)
-                        for (int k = 0; k < 3; ++k) {
-                            const double u = __shfl_up_sync(0xffffffffu, inc[k], o);
-                            if (lane >= o) inc[k] += u;
-                        }
-                    if (c.contrib[s]) {
-                        const SplatRec* e = c.e[s];
-                        double d_a = 0.0;
-                        for (int k = 0; k < 3; ++k)
-                            d_a += gp[k] * (rgb[k] * c.Ti[s] - (Cout[k] - (P[k] + inc[k])) / (1.0 - c.a[s]));
-                        acc_t* dst = accum + (size_t)(e - exact) * kAccStride;
-                        for (int k = 0; k < 3; ++k) atomicAdd(dst + k, w * gp[k]);
-                        const double h = c.g[s] * d_a;
-                        const double dx = pcx - e->sx, dy = pcy - e->sy;
-                        atomicAdd(dst + 3, h);
-                        atomicAdd(dst + 4, h * dx);
-                        atomicAdd(dst + 5, h * dy);
-                        atomicAdd(dst + 6, h * dx * dx);
-                        atomicAdd(dst + 7, h * dx * dy);
-                        atomicAdd(dst + 8, h * dy * dy);
-                    }
-                    for (int k = 0; k < 3; ++k) P[k] += __shfl_sync(0xffffffffu, inc[k], 31);
-                }
-                if (c.term >= 0) break;
-            }
-            if (pass == 0) {
-                Cout[0] = P[0] + T * bg_r;
-                Cout[1] = P[1] + T * bg_g;
-                Cout[2] = P[2] + T * bg_b;
-            }
-        }
+    // the FP64 backward of this tile's fix-up pixels, one warp per pixel, with
+    // the forward fix-up's FP64 colour; the staged batch's memory holds the
+    // walks' transmittance factors
+    __syncthreads();
+    const uint32_t nfix = s_nfix;
+    double* s_om = reinterpret_cast<double*>(&sb.mean[0]) + warp * (32 * kExactSub);
+    for (uint32_t k = warp; k < nfix; k += kThreadsB / 32) {
+        const int pix = (int)s_fix[k];
+        exact_bwd_pixel(pix, rg, fix_cout + 3 * (size_t)fix_slot[pix], inst_val, exact, W, bg_rd, bg_gd, bg_bd,
+                        last_arr, dL_dimg, nullptr, accum, s_om);
     }
 }
 

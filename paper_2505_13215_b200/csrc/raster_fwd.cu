@@ -636,7 +636,8 @@ __device__ __forceinline__ void write_pixel(const PixFwd& s, int pix, float bg_r
                                             float* __restrict__ out_rgb, uint32_t* __restrict__ out_last,
                                             float* __restrict__ out_tfinal, float* __restrict__ out_trans,
                                             uint32_t* __restrict__ out_count, uint32_t* __restrict__ fix_list,
-                                            uint32_t* __restrict__ fix_count, uint32_t* s_nfix, uint2* s_fix) {
+                                            uint32_t* __restrict__ fix_count, uint32_t* s_nfix, uint2* s_fix,
+                                            uint32_t* __restrict__ fix_slot) {
     const bool flagged = s.flagged || (g_debug_exact & 2) || s.err > g_debug_terr * s.T;
     out_rgb[pix * 3 + 0] = fmaf(s.T, bg_r, s.r);
     out_rgb[pix * 3 + 1] = fmaf(s.T, bg_g, s.g);
@@ -648,6 +649,7 @@ __device__ __forceinline__ void write_pixel(const PixFwd& s, int pix, float bg_r
     if (flagged) {  // the fix-list slot (the backward's exact pixels) and the CTA's own list
         const uint32_t q = atomicAdd(fix_count, 1u);
         fix_list[q] = (uint32_t)pix;
+        fix_slot[pix] = q;  // K6 finds the pixel's FP64 colour through it
         s_fix[atomicAdd(s_nfix, 1u)] = make_uint2((uint32_t)pix, q);
     }
 }
@@ -669,7 +671,7 @@ __global__ void __launch_bounds__(kThreads, 8) raster_fwd_kernel(
     float* __restrict__ out_rgb, uint32_t* __restrict__ out_last, float* __restrict__ out_tfinal,
     float* __restrict__ out_trans, uint32_t* __restrict__ out_count, uint32_t* __restrict__ fix_list,
     uint32_t* __restrict__ fix_count, const uint32_t* __restrict__ tile_order, double bg_rd, double bg_gd,
-    double bg_bd, double* __restrict__ out_cout) {
+    double bg_bd, double* __restrict__ out_cout, uint32_t* __restrict__ fix_slot) {
     pdl_wait();  // launched with launch_pdl
     __shared__ SplatBatch<kBatch> sb;
     __shared__ uint32_t s_nfix;  // the CTA's pixels handed to the FP64 fix-up
@@ -807,13 +809,13 @@ __global__ void __launch_bounds__(kThreads, 8) raster_fwd_kernel(
         const PixFwd s0{f2_lo(s.T), f2_lo(s.r), f2_lo(s.g), f2_lo(s.b), f2_lo(s.E), s.last0, s.count0, true,
                         flag0};
         write_pixel(s0, py0 * W + px, bg_r, bg_g, bg_b, out_rgb, out_last, out_tfinal, out_trans, out_count, fix_list,
-                    fix_count, &s_nfix, s_fix);
+                    fix_count, &s_nfix, s_fix, fix_slot);
     }
     if (in1) {
         const PixFwd s1{f2_hi(s.T), f2_hi(s.r), f2_hi(s.g), f2_hi(s.b), f2_hi(s.E), s.last1, s.count1, true,
                         flag1};
         write_pixel(s1, py1 * W + px, bg_r, bg_g, bg_b, out_rgb, out_last, out_tfinal, out_trans, out_count, fix_list,
-                    fix_count, &s_nfix, s_fix);
+                    fix_count, &s_nfix, s_fix, fix_slot);
     }
     // the FP64 fix-up of this tile's flagged pixels (~0.1% of the pixels), one
     // warp per pixel, inside the CTA: the walks overlap the other CTAs' work
@@ -833,7 +835,7 @@ void launch_raster_fwd(bool count_map, int n_tiles, cudaStream_t st, const uint2
                        const SplatFast* fast, const SplatRec* exact, int W, int H, int tiles_x, float bg_r, float bg_g,
                        float bg_b, float* out_rgb, uint32_t* out_last, float* out_tfinal, float* out_trans,
                        uint32_t* out_count, uint32_t* fix_list, uint32_t* fix_count, uint32_t* tile_order,
-                       double bg_rd, double bg_gd, double bg_bd, double* out_cout) {
+                       double bg_rd, double bg_gd, double bg_bd, double* out_cout, uint32_t* fix_slot) {
     if (tile_order) {
         launch_pdl(tile_order_kernel, dim3(1), dim3(1024), 0, st, ranges, n_tiles, tile_order);
         count_launch();
@@ -842,11 +844,11 @@ void launch_raster_fwd(bool count_map, int n_tiles, cudaStream_t st, const uint2
     if (count_map)
         launch_pdl(raster_fwd_kernel<true>, dim3(n_tiles), dim3(kThreads), 0, st, ranges, inst_val, fast, exact, W, H,
                    tiles_x, bg_r, bg_g, bg_b, out_rgb, out_last, out_tfinal, out_trans, out_count, fix_list,
-                   fix_count, order, bg_rd, bg_gd, bg_bd, out_cout);
+                   fix_count, order, bg_rd, bg_gd, bg_bd, out_cout, fix_slot);
     else
         launch_pdl(raster_fwd_kernel<false>, dim3(n_tiles), dim3(kThreads), 0, st, ranges, inst_val, fast, exact, W,
                    H, tiles_x, bg_r, bg_g, bg_b, out_rgb, out_last, out_tfinal, out_trans, out_count, fix_list,
-                   fix_count, order, bg_rd, bg_gd, bg_bd, out_cout);
+                   fix_count, order, bg_rd, bg_gd, bg_bd, out_cout, fix_slot);
 }
 
 // ---- density_map (raster.cpp:268-287)

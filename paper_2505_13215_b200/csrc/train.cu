@@ -170,7 +170,6 @@ hgs_status run_backward(hgs_ctx* ctx, const float* lg, double scale, bool zeroed
     }
     if (V == 0 || ctx->I == 0) return HGS_OK;
     const int n_tiles = ctx->tiles_x * ctx->tiles_y;
-    const uint32_t* fix_count = &ctx->counters.as<Counters>()->fix_count;
     prof_begin(ctx, PH_RASTER_BWD);
     const bool exact = ctx->exact_backward;
     if (exact) {
@@ -183,50 +182,25 @@ hgs_status run_backward(hgs_ctx* ctx, const float* lg, double scale, bool zeroed
         count_launch();
         CKL();
     } else {
-        // The FP64 backward of the fix-up pixels is latency bound (one warp per
-        // pixel walking its list) and independent of K6 but for the (commutative)
-        // accumulator atomics: it runs on a side stream, concurrently with K6,
-        // joined before K7.  HGS_NO_SIDE=1 serialises it (diagnostics).
-        static const bool side = !getenv("HGS_NO_SIDE");
-        cudaStream_t xs = st;
-        if (side) {
-            if (!ctx->side_stream) {
-                CK(cudaStreamCreateWithFlags(&ctx->side_stream, cudaStreamNonBlocking));
-                CK(cudaEventCreateWithFlags(&ctx->side_fork, cudaEventDisableTiming));
-                CK(cudaEventCreateWithFlags(&ctx->side_join, cudaEventDisableTiming));
-            }
-            xs = ctx->side_stream;
-            CK(cudaEventRecord(ctx->side_fork, st));
-            CK(cudaStreamWaitEvent(xs, ctx->side_fork, 0));
-            CK(launch_pdl(raster_bwd_exact_kernel, dim3(ctx->sms * 2), dim3(128), 0, xs, ctx->fix_list.as<uint32_t>(),
-                          fix_count, ctx->W * ctx->H, ctx->ranges.as<uint2>(), ctx->inst_vals_final,
-                          ctx->rec_sorted.as<SplatRec>(), ctx->W, ctx->tiles_x, ctx->bg[0], ctx->bg[1], ctx->bg[2],
-                          ctx->last.as<uint32_t>(), lg, static_cast<const double*>(nullptr), ctx->accum.as<acc_t>(),
-                          static_cast<const double*>(ctx->fix_cout.as<double>())));
-            count_launch();
-            CKL();
-        }
+        // K6; the FP64 backward of each tile's fix-up pixels runs inside the
+        // tile's CTA after its walk (exact_bwd_pixel, with the forward
+        // fix-up's FP64 colour)
         CK(launch_pdl(raster_bwd_kernel, dim3(n_tiles), dim3(128), 0, st, ctx->ranges.as<uint2>(),
                       static_cast<const uint32_t*>(ctx->inst_vals_final), ctx->fast_sorted.as<SplatFast>(),
                       ctx->rec_sorted.as<SplatRec>(), ctx->W, ctx->H, ctx->tiles_x, ctx->tfinal.as<float>(),
                       ctx->last.as<uint32_t>(), lg, (float)ctx->bg[0], (float)ctx->bg[1], (float)ctx->bg[2],
                       ctx->accum.as<acc_t>(),
-                      static_cast<const uint32_t*>(tile_order_enabled() ? ctx->tile_order.as<uint32_t>() : nullptr)));
+                      static_cast<const uint32_t*>(tile_order_enabled() ? ctx->tile_order.as<uint32_t>() : nullptr),
+                      static_cast<const uint32_t*>(ctx->fix_slot.as<uint32_t>()),
+                      static_cast<const double*>(ctx->fix_cout.as<double>()), ctx->bg[0], ctx->bg[1], ctx->bg[2]));
         count_launch();
         CKL();
-        if (side) {
-            CK(cudaEventRecord(ctx->side_join, xs));
-            CK(cudaStreamWaitEvent(st, ctx->side_join, 0));
-        }
     }
-    static const bool side_on = !getenv("HGS_NO_SIDE");
-    if (exact || !side_on) {
-        CK(launch_pdl(raster_bwd_exact_kernel, dim3(ctx->sms * (exact ? 8 : 2)), dim3(128), 0, st,
-                      exact ? nullptr : ctx->fix_list.as<uint32_t>(), fix_count, ctx->W * ctx->H,
+    if (exact) {
+        CK(launch_pdl(raster_bwd_exact_kernel, dim3(ctx->sms * 8), dim3(128), 0, st, ctx->W * ctx->H,
                       ctx->ranges.as<uint2>(), ctx->inst_vals_final, ctx->rec_sorted.as<SplatRec>(), ctx->W,
                       ctx->tiles_x, ctx->bg[0], ctx->bg[1], ctx->bg[2], ctx->last.as<uint32_t>(), lg,
-                      exact ? ctx->exact_col.as<double>() : nullptr, ctx->accum.as<acc_t>(),
-                      exact ? nullptr : ctx->fix_cout.as<double>()));
+                      ctx->exact_col.as<double>(), ctx->accum.as<acc_t>()));
         count_launch();
         CKL();
     }
