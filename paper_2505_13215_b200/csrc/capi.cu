@@ -475,17 +475,12 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
             const int end_bit = ((bits + 7) / 8) * 8;
             CK(ctx->sort_ws.ensure(radix_workspace_bytes((int)I) + 4096));
             ctx->inst_keys_all = ctx->inst_vals_all = nullptr;
+            // the sort's last phase also writes the tile ranges
             int which = radix_sort_pairs(ctx->inst_k2.as<uint32_t>(), ctx->inst_v2.as<uint32_t>(),
                                          ctx->inst_k.as<uint32_t>(), ctx->inst_v.as<uint32_t>(), (int)I, 0, end_bit,
-                                         ctx->sort_ws.as<uint32_t>(), st, &dc->I_kept);
+                                         ctx->sort_ws.as<uint32_t>(), st, &dc->I_kept, ctx->ranges.as<uint2>());
             CKL();
-            uint32_t* keys = which ? ctx->inst_k.as<uint32_t>() : ctx->inst_k2.as<uint32_t>();
             inst_vals = which ? ctx->inst_v.as<uint32_t>() : ctx->inst_v2.as<uint32_t>();
-            CK(launch_pdl(tile_ranges_dev_kernel, dim3(div_up((uint32_t)I, 256)), dim3(256), 0, st,
-                          static_cast<const uint32_t*>(keys), static_cast<const uint32_t*>(&dc->I_kept),
-                          ctx->ranges.as<uint2>()));
-            count_launch();
-            CKL();
             prof_end(ctx);
         } else {
         prof_begin(ctx, PH_DUPLICATE);

@@ -114,6 +114,7 @@ __global__ void __launch_bounds__(kCoopThreads) scan_coop_kernel(const uint32_t*
 struct CoopSort {
     uint32_t *k0, *v0, *k1, *v1;
     const uint32_t* n_dev;
+    uint2* ranges;  // optional: [first, end) of every key's run in the sorted keys (the tile ranges)
     int n, shift0, npasses;
     uint32_t* hist;    // [256][G]
     uint32_t* rowsum;  // [256]
@@ -236,6 +237,13 @@ __global__ void __launch_bounds__(kCoopThreads) radix_sort_coop_kernel(CoopSort 
         vi = vo;
         vo = t;
     }
+    if (a.ranges) {  // run boundaries of the sorted keys (after the last barrier)
+        for (int i = lo + tid; i < hi; i += kCoopThreads) {
+            const uint32_t t = ki[i];
+            if (i == 0 || ki[i - 1] != t) a.ranges[t].x = (uint32_t)i;
+            if (i == n - 1 || ki[i + 1] != t) a.ranges[t].y = (uint32_t)(i + 1);
+        }
+    }
 }
 
 // Grid of a cooperative kernel for n items: co-resident (<= 4 blocks per SM
@@ -302,7 +310,8 @@ size_t radix_workspace_bytes(int) { return (size_t)(256 * kMaxCoopGrid + 256 + 6
 // lands in (keys, vals) when the pass count is even, else in (keys_alt,
 // vals_alt); the return value says which (0 = original buffers).
 int radix_sort_pairs(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt, int n,
-                     int begin_bit, int end_bit, uint32_t* ws, cudaStream_t st, const uint32_t* n_dev) {
+                     int begin_bit, int end_bit, uint32_t* ws, cudaStream_t st, const uint32_t* n_dev,
+                     uint2* ranges) {
     if (!n_dev && n <= 1) return 0;
     const int npasses = (end_bit - begin_bit + 7) / 8;
     if (npasses <= 0) return 0;
@@ -312,6 +321,7 @@ int radix_sort_pairs(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_
     a.k1 = keys_alt;
     a.v1 = vals_alt;
     a.n_dev = n_dev;
+    a.ranges = ranges;
     a.n = n;
     a.shift0 = begin_bit;
     a.npasses = npasses;

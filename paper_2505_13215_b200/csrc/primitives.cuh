@@ -15,8 +15,11 @@ void exclusive_scan_u32(const uint32_t* in, uint32_t* out, int n, uint32_t* tota
                         cudaStream_t st, const uint32_t* n_dev = nullptr);
 
 size_t radix_workspace_bytes(int n);
-// n_dev (optional): device-side item count (then n is ignored).
+// n_dev (optional): device-side item count (then n is ignored).  ranges
+// (optional): [first, end) of every key's run in the sorted keys (the tile
+// ranges; entries of absent keys untouched).
 int radix_sort_pairs(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt, int n,
-                     int begin_bit, int end_bit, uint32_t* ws, cudaStream_t st, const uint32_t* n_dev = nullptr);
+                     int begin_bit, int end_bit, uint32_t* ws, cudaStream_t st, const uint32_t* n_dev = nullptr,
+                     uint2* ranges = nullptr);
 
 }  // namespace hgs
