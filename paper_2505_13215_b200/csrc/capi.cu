@@ -187,24 +187,6 @@ __global__ void __launch_bounds__(256) zero_jobs_kernel(ZeroJobs J) {
     }
 }
 
-__global__ void visflag_kernel(const uint32_t* __restrict__ ntiles, int n, uint32_t* __restrict__ flag) {
-    pdl_wait();  // launched with launch_pdl
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) flag[i] = ntiles[i] > 0u ? 1u : 0u;
-}
-
-__global__ void compact_kernel(const uint32_t* __restrict__ ntiles, const uint32_t* __restrict__ pos,
-                               const uint32_t* __restrict__ depth_key, int n, uint32_t* __restrict__ keys,
-                               uint32_t* __restrict__ vals) {
-    pdl_wait();  // launched with launch_pdl
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n && ntiles[i] > 0u) {
-        const uint32_t p = pos[i];
-        keys[p] = depth_key[i];
-        vals[p] = (uint32_t)i;
-    }
-}
-
 hgs_status check_flags(hgs_ctx* ctx, uint32_t flags) {
     if (flags & FLAG_NONUNIT_QUAT) return fail(ctx, HGS_ERR_INVALID_ARGUMENT, "quat_to_rot3: non-unit quaternion");
     if (flags & FLAG_INDEFINITE)
@@ -375,25 +357,18 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
                       dc->stats, &dc->flags, ctx->shdir.as<ShRec>()));
         count_launch();
         CKL();
-        CK(launch_pdl(visflag_kernel, dim3(div_up(N, 256)), dim3(256), 0, st, ctx->ntiles.as<uint32_t>(), N,
-                      ctx->visflag.as<uint32_t>()));
-        count_launch();
-        exclusive_scan_u32(ctx->visflag.as<uint32_t>(), ctx->vispos.as<uint32_t>(), N, &dc->V,
-                           ctx->scan_ws.as<uint32_t>(), st);
-        CKL();
-        prof_end(ctx);
         // the visible count V stays on the device: buffers are sized for N,
         // the sort, gather and offset scan read V from device memory
         CK(ctx->sort_k.ensure((size_t)N * 4));
         CK(ctx->sort_v.ensure((size_t)N * 4));
         CK(ctx->sort_k2.ensure((size_t)N * 4));
         CK(ctx->sort_v2.ensure((size_t)N * 4));
-        prof_begin(ctx, PH_DEPTH_SORT);
-        CK(launch_pdl(compact_kernel, dim3(div_up(N, 256)), dim3(256), 0, st, ctx->ntiles.as<uint32_t>(),
-                      ctx->vispos.as<uint32_t>(), ctx->depth_key.as<uint32_t>(), N, ctx->sort_k.as<uint32_t>(),
-                      ctx->sort_v.as<uint32_t>()));
-        count_launch();
+        // the visible Gaussians' (depth key, index) in index order, V
+        compact_visible(ctx->ntiles.as<uint32_t>(), ctx->depth_key.as<uint32_t>(), N, ctx->sort_k.as<uint32_t>(),
+                        ctx->sort_v.as<uint32_t>(), &dc->V, ctx->scan_ws.as<uint32_t>(), st);
         CKL();
+        prof_end(ctx);
+        prof_begin(ctx, PH_DEPTH_SORT);
         CK(ctx->sort_ws.ensure(radix_workspace_bytes(N) + 4096));
         // stable sort by f32 depth bits; gid (projected order) breaks ties
         int which = radix_sort_pairs(ctx->sort_k.as<uint32_t>(), ctx->sort_v.as<uint32_t>(), ctx->sort_k2.as<uint32_t>(),

@@ -111,6 +111,52 @@ __global__ void __launch_bounds__(kCoopThreads) scan_coop_kernel(const uint32_t*
     }
 }
 
+// Stream compaction of the visible Gaussians (ntiles > 0) into the depth
+// sort's input, in index order: keys[r] = depth_key[i], vals[r] = i, *total =
+// the visible count -- the scan kernel's structure with the flag test and the
+// scatter fused in (one launch instead of flag / scan / scatter).
+__global__ void __launch_bounds__(kCoopThreads) compact_coop_kernel(const uint32_t* __restrict__ ntiles,
+                                                                    const uint32_t* __restrict__ depth_key, int n,
+                                                                    uint32_t* __restrict__ keys,
+                                                                    uint32_t* __restrict__ vals,
+                                                                    uint32_t* __restrict__ total,
+                                                                    uint32_t* __restrict__ bsum) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // launched as a programmatic dependent (coop_launch)
+    cg::grid_group grid = cg::this_grid();
+    const int G = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
+    const int C = ((n + G - 1) / G + 3) & ~3;
+    const int lo = min(b * C, n), hi = min(lo + C, n);
+    uint32_t s = 0;
+    for (int i = lo + tid; i < hi; i += kCoopThreads) s += ntiles[i] > 0u ? 1u : 0u;
+    s = block_sum(s);
+    if (tid == 0) bsum[b] = s;
+    grid.sync();
+    uint32_t part = 0;
+    for (int c = tid; c < b; c += kCoopThreads) part += bsum[c];
+    uint32_t run = block_sum(part);
+    if (b == G - 1 && tid == 0) *total = run + bsum[b];
+    for (int t0 = lo; t0 < hi; t0 += kTileItems) {
+        const int base = t0 + tid * kItems;
+        uint32_t v[kItems], sum = 0;
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
+            v[k] = base + k < hi && ntiles[base + k] > 0u ? 1u : 0u;
+            sum += v[k];
+        }
+        uint32_t tot;
+        uint32_t r = run + block_excl_scan(sum, tot);
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
+            if (v[k]) {
+                keys[r] = depth_key[base + k];
+                vals[r] = (uint32_t)(base + k);
+            }
+            r += v[k];
+        }
+        run += tot;
+    }
+}
+
 struct CoopSort {
     uint32_t *k0, *v0, *k1, *v1;
     const uint32_t* n_dev;
@@ -301,6 +347,18 @@ void exclusive_scan_u32(const uint32_t* in, uint32_t* out, int n, uint32_t* tota
     const int G = std::min(coop_grid(scan_coop_kernel, n), kMaxCoopGrid);
     void* args[] = {(void*)&in, (void*)&out, (void*)&n, (void*)&n_dev, (void*)&total, (void*)&ws};
     coop_launch((const void*)scan_coop_kernel, G, args, st);
+    count_launch();
+}
+
+void compact_visible(const uint32_t* ntiles, const uint32_t* depth_key, int n, uint32_t* keys, uint32_t* vals,
+                     uint32_t* total, uint32_t* ws, cudaStream_t st) {
+    if (n <= 0) {
+        cudaMemsetAsync(total, 0, sizeof(uint32_t), st);
+        return;
+    }
+    const int G = std::min(coop_grid(compact_coop_kernel, n), kMaxCoopGrid);
+    void* args[] = {(void*)&ntiles, (void*)&depth_key, (void*)&n, (void*)&keys, (void*)&vals, (void*)&total, (void*)&ws};
+    coop_launch((const void*)compact_coop_kernel, G, args, st);
     count_launch();
 }
 

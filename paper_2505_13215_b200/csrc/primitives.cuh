@@ -14,6 +14,11 @@ size_t scan_workspace_bytes(int n);
 void exclusive_scan_u32(const uint32_t* in, uint32_t* out, int n, uint32_t* total, uint32_t* ws,
                         cudaStream_t st, const uint32_t* n_dev = nullptr);
 
+// keys[r] = depth_key[i], vals[r] = i for the i with ntiles[i] > 0, in index
+// order; *total (device) = their count.  ws: scan_workspace_bytes(n).
+void compact_visible(const uint32_t* ntiles, const uint32_t* depth_key, int n, uint32_t* keys, uint32_t* vals,
+                     uint32_t* total, uint32_t* ws, cudaStream_t st);
+
 size_t radix_workspace_bytes(int n);
 // n_dev (optional): device-side item count (then n is ignored).  ranges
 // (optional): [first, end) of every key's run in the sorted keys (the tile
