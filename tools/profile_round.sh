@@ -13,4 +13,4 @@ HGS_LIB=paper_2505_13215_b200/libhgs_gpu_checked.so timeout 600 python tools/cou
 echo "pairs rc $?"; cp profiles/${tag}_pairs.json gpurun_out/ 2>/dev/null
 python tools/prof_step.py > /dev/null 2>&1 && bash tools/prof_full.sh $tag raster_bwd_kernel raster_fwd_kernel preprocess_kernel \
   radix_sort_coop_kernel duplicate_compact_kernel gaussian_bwd_kernel adam_rows_kernel ssim_fwd_kernel ssim_bwd_kernel \
-  raster_bwd_exact_kernel sh_bwd_kernel adam_classes_kernel raster_fixup_kernel gather_sorted_kernel
+  sh_bwd_kernel adam_classes_kernel gather_sorted_kernel
