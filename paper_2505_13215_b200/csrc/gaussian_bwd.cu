@@ -219,18 +219,17 @@ __device__ __forceinline__ void chain(const Geo& g, const DevCamera& cam, const 
         for (int a = 0; a < 3; ++a)
             for (int b = 0; b < 3; ++b) dR[a][b] = dm[a][b] * g.es[b];
         const double w = g.q[0], x = g.q[1], y = g.q[2], zz = g.q[3];
-        // drot3_dq (backward.cpp:54-72), contracted with dR
-        const double D[4][3][3] = {{{0, -zz, y}, {zz, 0, -x}, {-y, x, 0}},
-                                   {{0, y, zz}, {y, -2 * x, -w}, {zz, w, -2 * x}},
-                                   {{-2 * y, x, w}, {x, 0, zz}, {-w, zz, -2 * y}},
-                                   {{-2 * zz, -w, x}, {w, -2 * zz, y}, {x, y, 0}}};
-        T dq[4];
-        for (int k = 0; k < 4; ++k) {
-            T s = T(0.0);
-            for (int a = 0; a < 3; ++a)
-                for (int b = 0; b < 3; ++b) s += dR[a][b] * 2.0 * D[k][a][b];
-            dq[k] = s;
-        }
+        // drot3_dq (backward.cpp:54-72) contracted with dR, its zero entries dropped
+        //   D0 = {{0, -z, y}, {z, 0, -x}, {-y, x, 0}}      D1 = {{0, y, z}, {y, -2x, -w}, {z, w, -2x}}
+        //   D2 = {{-2y, x, w}, {x, 0, z}, {-w, z, -2y}}     D3 = {{-2z, -w, x}, {w, -2z, y}, {x, y, 0}}
+        const T dq[4] = {
+            2.0 * (-zz * dR[0][1] + y * dR[0][2] + zz * dR[1][0] - x * dR[1][2] - y * dR[2][0] + x * dR[2][1]),
+            2.0 * (y * dR[0][1] + zz * dR[0][2] + y * dR[1][0] - 2 * x * dR[1][1] - w * dR[1][2] + zz * dR[2][0] +
+                   w * dR[2][1] - 2 * x * dR[2][2]),
+            2.0 * (-2 * y * dR[0][0] + x * dR[0][1] + w * dR[0][2] + x * dR[1][0] + zz * dR[1][2] - w * dR[2][0] +
+                   zz * dR[2][1] - 2 * y * dR[2][2]),
+            2.0 * (-2 * zz * dR[0][0] - w * dR[0][1] + x * dR[0][2] + w * dR[1][0] - 2 * zz * dR[1][1] +
+                   y * dR[1][2] + x * dR[2][0] + y * dR[2][1])};
         const T qd = g.q[0] * dq[0] + g.q[1] * dq[1] + g.q[2] * dq[2] + g.q[3] * dq[3];
         for (int k = 0; k < 4; ++k) out[R3_Q + k] = dq[k] - qd * g.q[k];
         return;
@@ -287,21 +286,14 @@ __device__ __forceinline__ void chain(const Geo& g, const DevCamera& cam, const 
             dL[a][b] = x;
             dR[a][b] = y;
         }
-    T dql[4], dqr[4];
-    for (int k = 0; k < 4; ++k) {
-        double ek[4] = {k == 0 ? 1.0 : 0.0, k == 1 ? 1.0 : 0.0, k == 2 ? 1.0 : 0.0, k == 3 ? 1.0 : 0.0};
-        double le[4][4], re[4][4];
-        isoL(ek, le);
-        isoR(ek, re);
-        T x = T(0.0), y = T(0.0);
-        for (int a = 0; a < 4; ++a)
-            for (int b = 0; b < 4; ++b) {
-                x += dL[a][b] * le[a][b];
-                y += dR[a][b] * re[a][b];
-            }
-        dql[k] = x;
-        dqr[k] = y;
-    }
+    // d/dq_k of the isoclinic factors contracted with dL, dR: isoL(e_k) and
+    // isoR(e_k) are signed permutation matrices (isoL / isoR above), so each
+    // contraction is 4 signed terms (the zero products of the dense form are
+    // not folded by the compiler: 0 * x is not 0 for a NaN x)
+    const T dql[4] = {dL[0][0] + dL[1][1] + dL[2][2] + dL[3][3], -dL[0][1] + dL[1][0] - dL[2][3] + dL[3][2],
+                      -dL[0][2] + dL[1][3] + dL[2][0] - dL[3][1], -dL[0][3] - dL[1][2] + dL[2][1] + dL[3][0]};
+    const T dqr[4] = {dR[0][0] + dR[1][1] + dR[2][2] + dR[3][3], -dR[0][1] + dR[1][0] + dR[2][3] - dR[3][2],
+                      -dR[0][2] - dR[1][3] + dR[2][0] + dR[3][1], -dR[0][3] + dR[1][2] - dR[2][1] + dR[3][0]};
     const double(&ql)[4] = g.ql;
     const double(&qr)[4] = g.qr;
     const T dl = ql[0] * dql[0] + ql[1] * dql[1] + ql[2] * dql[2] + ql[3] * dql[3];
