@@ -257,3 +257,26 @@ def test_quadrant_masks_are_conservative(ctx, seed, size, t):
         bad += int((reach & ((masks >> q) & 1 == 0)).sum())
     assert bad == 0, bad
     assert masks.any()
+
+
+def _replicate3(scene, idx):
+    from dataclasses import replace
+
+    return replace(scene, mean3=scene.mean3[idx], quat3=scene.quat3[idx], log_s3=scene.log_s3[idx],
+                   op3=scene.op3[idx], sh3=scene.sh3[idx])
+
+
+def test_depth_sort_ties_and_clusters(ctx):
+    """Depth-sort corner cases: 6000 copies of 3 Gaussians (equal depth keys:
+    ties broken by the projected index), a narrow depth cluster in front of
+    one far outlier (keys sharing their high digits) and a spread scene --
+    all against the oracle's instance order."""
+    rng = O.Rng(12)
+    base = rng.random_scene(3, 0, 1)
+    cam = rng.random_camera(48, 40)
+    check_render(ctx, _replicate3(base, np.arange(6000) % 3), cam, 0.5)
+    cl = rng.random_scene(3000, 0, 0)
+    cl.mean3[:] = 1e-3 * (cl.mean3 - cl.mean3.mean(0))
+    cl.mean3[0] = [0.0, 0.0, 5.0]  # 8 units away, the cluster at 3
+    check_render(ctx, cl, O.look_at([0, 0, -3], [0, 0, 0], [0, -1, 0], 50.0, 48, 40), 0.5)
+    check_render(ctx, synthetic_scene(20_000, 20_000, 0, seed=13), ring_camera(13, 96, 80), 0.5)

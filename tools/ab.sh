@@ -4,7 +4,8 @@
 steps=${1:-30}; rounds=${2:-2}
 for r in $(seq $rounds); do
 for lib in _variants/*.so; do
-  HGS_LIB=$lib python bench.py --no-extras --no-cpu-baseline --steps $steps --warmup 5 > gpurun_out/ab.json 2>/dev/null
+  envf=${lib%.so}.env; extra=""; [ -f $envf ] && extra=$(cat $envf)  # optional per-variant env (VAR=val ...)
+  env $extra HGS_LIB=$lib python bench.py --no-extras --no-cpu-baseline --steps $steps --warmup 5 > gpurun_out/ab.json 2>/dev/null
   python -c "
 import json,sys; d=json.loads(open('gpurun_out/ab.json').read().strip().splitlines()[-1])
 ph=' '.join(f\"{k['phase']}={k['ms_per_step']:.4f}\" for k in d['roofline']['kernels'])

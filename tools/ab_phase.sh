@@ -3,5 +3,6 @@
 cfg=${1:-c5}; pat=${2:-.}
 for lib in _variants/*.so; do
   echo "== $lib"
-  HGS_LIB=$lib CFG=$cfg VIEWS=1 STEPS=4 python tools/phase_cfg.py 2>&1 | grep -E "$pat"
+  envf=${lib%.so}.env; extra=""; [ -f $envf ] && extra=$(cat $envf)
+  env $extra HGS_LIB=$lib CFG=$cfg VIEWS=1 STEPS=4 python tools/phase_cfg.py 2>&1 | grep -E "$pat"
 done
