@@ -37,7 +37,6 @@ __device__ __forceinline__ float rcp_approx_a(float x) {
 
 __device__ __forceinline__ float4 ld4(const float* p) { return __ldcs(reinterpret_cast<const float4*>(p)); }
 __device__ __forceinline__ void st4(float* p, float4 v) { __stcs(reinterpret_cast<float4*>(p), v); }
-__device__ __forceinline__ float comp(const float4& v, int k) { return k == 0 ? v.x : k == 1 ? v.y : k == 2 ? v.z : v.w; }
 __device__ __forceinline__ bool fin(float x) { return isfinite(x); }
 
 // One Adam element (train.cpp:155-170); ok = the class is finite.
@@ -49,29 +48,28 @@ __device__ __forceinline__ void adam1(float& p, float& m, float& v, float g, boo
     p -= lr * mhat * rcp_approx_a(sqrt_approx(vhat) + 1e-15f);
 }
 
-// Parameter classes of a pool: first row, row count, bit in the class mask.
-struct PoolLayout {
-    int n_cls;
-    int r0[7], d[7];
-    bool quat[7];
-};
-__device__ __forceinline__ PoolLayout layout(bool dyn, int K3) {
-    PoolLayout L;
+// Parameter class c of a pool: first row, row count, quaternion class.
+__device__ __forceinline__ void cls_rows(bool dyn, int c, int K3, int& r0, int& d, bool& quat) {
+    quat = false;
     if (dyn) {
-        L.n_cls = 7;
-        const int r0[7] = {R4_MEAN, R4_MT, R4_QL, R4_QR, R4_LS, R4_OP, R4_SH};
-        const int d[7] = {3, 1, 4, 4, 4, 1, K3};
-        for (int c = 0; c < 7; ++c) L.r0[c] = r0[c], L.d[c] = d[c], L.quat[c] = (c == 2 || c == 3);
+        switch (c) {
+            case 0: r0 = R4_MEAN, d = 3; break;
+            case 1: r0 = R4_MT, d = 1; break;
+            case 2: r0 = R4_QL, d = 4, quat = true; break;
+            case 3: r0 = R4_QR, d = 4, quat = true; break;
+            case 4: r0 = R4_LS, d = 4; break;
+            case 5: r0 = R4_OP, d = 1; break;
+            default: r0 = R4_SH, d = K3; break;
+        }
     } else {
-        L.n_cls = 5;
-        const int r0[5] = {R3_MEAN, R3_Q, R3_LS, R3_OP, R3_SH};
-        const int d[5] = {3, 4, 3, 1, K3};
-        for (int c = 0; c < 5; ++c) L.r0[c] = r0[c], L.d[c] = d[c], L.quat[c] = (c == 1);
-        L.r0[5] = L.r0[6] = 0;
-        L.d[5] = L.d[6] = 0;
-        L.quat[5] = L.quat[6] = false;
+        switch (c) {
+            case 0: r0 = R3_MEAN, d = 3; break;
+            case 1: r0 = R3_Q, d = 4, quat = true; break;
+            case 2: r0 = R3_LS, d = 3; break;
+            case 3: r0 = R3_OP, d = 1; break;
+            default: r0 = R3_SH, d = K3; break;
+        }
     }
-    return L;
 }
 
 // train.cpp:46-53 followed by UnitQuat::normalized (gauss_math.cpp:35-44)
@@ -110,75 +108,117 @@ __device__ __forceinline__ bool update_allowed(const AdamArgs& A) {
 
 }  // namespace
 
-__global__ void __launch_bounds__(128) adam_classes_kernel(AdamPools P, AdamArgs A, uint8_t* __restrict__ cls_ok3,
+__global__ void __launch_bounds__(128, 6) adam_classes_kernel(AdamPools P, AdamArgs A, uint8_t* __restrict__ cls_ok3,
                                                            uint8_t* __restrict__ cls_ok4,
                                                            unsigned long long* __restrict__ skipped_total,
                                                            uint32_t* __restrict__ flags) {
     pdl_wait();  // launched with launch_pdl
-    // one thread per (parameter class, 4 consecutive Gaussians); 3D units first
+    // one thread per (parameter class, 4 consecutive Gaussians); 3D units
+    // first.  The SH class (the bulk of the rows) is checked by adam_sh_slices
+    // threads per 4 Gaussians, each over a slice of its rows (slice fastest:
+    // a load instruction covers 8 groups x 16 B of 4 rows), flags combined
+    // by two shuffles.  Units: 3D classes 0-3 | 3D SH | 4D classes 0-5 |
+    // pad to a multiple of 4 | 4D SH.
     if (!update_allowed(A)) return;
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int S = adam_sh_slices(P.K3);
     const int q3 = (P.n3 + 3) >> 2, q4 = (P.n4 + 3) >> 2;
+    const int a3 = 4 * q3, e3 = a3 + S * q3, b4 = e3 + 6 * q4, a4 = e3 + ((6 * q4 + 3) & ~3), e4 = a4 + S * q4;
+    bool active = true, dyn = false;
+    int c = 0, grp = 0, sl = 0;
+    if (t < a3) {
+        c = t / q3, grp = t - c * q3;
+    } else if (t < e3) {
+        c = 4, grp = (t - a3) / S, sl = (t - a3) - grp * S;
+    } else if (t < b4) {
+        dyn = true, c = (t - e3) / q4, grp = (t - e3) - c * q4;
+    } else if (t >= a4 && t < e4) {
+        dyn = true, c = 6, grp = (t - a4) / S, sl = (t - a4) - grp * S;
+    } else {
+        active = false;
+    }
+    const bool sliced = active && S > 1 && ((!dyn && c == 4) || (dyn && c == 6));
     uint32_t skipped = 0;
     bool ok = true;
-    if (t < 5 * q3 + 7 * q4) {
-        const bool dyn = t >= 5 * q3;
-        const int u = dyn ? t - 5 * q3 : t;
-        const int q = dyn ? q4 : q3;
-        const int c = u / q, i0 = (u % q) * 4;
-        const int n = dyn ? P.n4 : P.n3;
-        const int64_t cap = dyn ? P.cap4 : P.cap3;
-        float* p = dyn ? P.p4 : P.p3;
-        float* g = dyn ? P.g4 : P.g3;
-        float* m = dyn ? P.m4 : P.m3;
-        float* v = dyn ? P.v4 : P.v3;
-        const PoolLayout L = layout(dyn, P.K3);
-        const int nvalid = min(4, n - i0);
-        const int r0 = L.r0[c], d = L.d[c];
-        bool f[4] = {true, true, true, true};
-#pragma unroll 16
-        for (int k = 0; k < d; ++k) {
-            const float4 gv = __ldg(reinterpret_cast<const float4*>(g + (int64_t)(r0 + k) * cap + i0));
-            f[0] &= fin(gv.x);
-            f[1] &= fin(gv.y);
-            f[2] &= fin(gv.z);
-            f[3] &= fin(gv.w);
+    const int i0 = grp * 4;
+    const int n = dyn ? P.n4 : P.n3;
+    const int64_t cap = dyn ? P.cap4 : P.cap3;
+    float* p = dyn ? P.p4 : P.p3;
+    float* g = dyn ? P.g4 : P.g3;
+    float* m = dyn ? P.m4 : P.m3;
+    float* v = dyn ? P.v4 : P.v3;
+    int r0 = 0, d = 0;
+    bool quat = false;
+    cls_rows(dyn, c, P.K3, r0, d, quat);
+    uint32_t fm = 0xfu;  // finite flags of the 4 Gaussians (bit w)
+    if (active) {
+        int k0 = 0, k1 = d;
+        if (sliced) {
+            const int R = (d + S - 1) / S;
+            k0 = min(d, sl * R), k1 = min(d, k0 + R);
         }
-        for (int w = 0; w < nvalid; ++w)
-            if (!f[w]) ++skipped;
+        bool f0 = true, f1 = true, f2 = true, f3 = true;
+#pragma unroll 4
+        for (int k = k0; k < k1; ++k) {
+            const float4 gv = __ldg(reinterpret_cast<const float4*>(g + (int64_t)(r0 + k) * cap + i0));
+            f0 &= fin(gv.x);
+            f1 &= fin(gv.y);
+            f2 &= fin(gv.z);
+            f3 &= fin(gv.w);
+        }
+        fm = (uint32_t)f0 | ((uint32_t)f1 << 1) | ((uint32_t)f2 << 2) | ((uint32_t)f3 << 3);
+    }
+    if (S > 1) {  // (every lane: aligned groups of S lanes are one SH group)
+        uint32_t x = fm & __shfl_xor_sync(0xffffffffu, fm, 1);
+        if (S > 2) x &= __shfl_xor_sync(0xffffffffu, x, 2);
+        if (sliced) fm = x;
+    }
+    if (active && sl == 0) {
+        const int nvalid = min(4, n - i0);
+        skipped = (uint32_t)__popc(~fm & ((1u << nvalid) - 1u));
         uint8_t* out = (dyn ? cls_ok4 : cls_ok3) + (int64_t)c * cap + i0;
-        *reinterpret_cast<uchar4*>(out) = make_uchar4(f[0], f[1], f[2], f[3]);
-        if (L.quat[c]) {
-            // quaternion class: update, renormalise (even if skipped), zero its gradient
-            float4 pr[4], mr[4], vr[4], gr[4];
-            for (int k = 0; k < 4; ++k) {
-                const int64_t o = (int64_t)(r0 + k) * cap + i0;
-                pr[k] = ld4(p + o);
-                mr[k] = ld4(m + o);
-                vr[k] = ld4(v + o);
-                gr[k] = ld4(g + o);
-            }
-            for (int w = 0; w < nvalid; ++w) {
-                float qv[4], mq[4], vq[4];
+        *reinterpret_cast<uchar4*>(out) = make_uchar4(fm & 1u, (fm >> 1) & 1u, (fm >> 2) & 1u, (fm >> 3) & 1u);
+        if (quat) {
+            // quaternion class: update, renormalise (even if skipped), zero its
+            // gradient; two Gaussians (float2 columns) at a time
+#pragma unroll 1
+            for (int h = 0; 2 * h < nvalid; ++h) {
+                float2 pr[4], mr[4], vr[4], gr[4];
+#pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    qv[k] = comp(pr[k], w);
-                    mq[k] = comp(mr[k], w);
-                    vq[k] = comp(vr[k], w);
-                    adam1(qv[k], mq[k], vq[k], comp(gr[k], w), f[w], A.lr_quat, A);
+                    const int64_t o = (int64_t)(r0 + k) * cap + i0 + 2 * h;
+                    pr[k] = __ldcs(reinterpret_cast<const float2*>(p + o));
+                    mr[k] = __ldcs(reinterpret_cast<const float2*>(m + o));
+                    vr[k] = __ldcs(reinterpret_cast<const float2*>(v + o));
+                    gr[k] = __ldcs(reinterpret_cast<const float2*>(g + o));
                 }
-                ok &= renorm_quat(qv, mq);
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int w = 2 * h + e;
+                    if (w >= nvalid) break;
+                    float qv[4], mq[4], vq[4];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        qv[k] = e ? pr[k].y : pr[k].x;
+                        mq[k] = e ? mr[k].y : mr[k].x;
+                        vq[k] = e ? vr[k].y : vr[k].x;
+                        adam1(qv[k], mq[k], vq[k], e ? gr[k].y : gr[k].x, (fm >> w) & 1u, A.lr_quat, A);
+                    }
+                    ok &= renorm_quat(qv, mq);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        if (e) pr[k].y = qv[k], mr[k].y = mq[k], vr[k].y = vq[k];
+                        else pr[k].x = qv[k], mr[k].x = mq[k], vr[k].x = vq[k];
+                    }
+                }
+#pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    (&pr[k].x)[w] = qv[k];
-                    (&mr[k].x)[w] = mq[k];
-                    (&vr[k].x)[w] = vq[k];
+                    const int64_t o = (int64_t)(r0 + k) * cap + i0 + 2 * h;
+                    __stcs(reinterpret_cast<float2*>(p + o), pr[k]);
+                    __stcs(reinterpret_cast<float2*>(m + o), mr[k]);
+                    __stcs(reinterpret_cast<float2*>(v + o), vr[k]);
+                    __stcs(reinterpret_cast<float2*>(g + o), make_float2(0.f, 0.f));
                 }
-            }
-            for (int k = 0; k < 4; ++k) {
-                const int64_t o = (int64_t)(r0 + k) * cap + i0;
-                st4(p + o, pr[k]);
-                st4(m + o, mr[k]);
-                st4(v + o, vr[k]);
-                st4(g + o, make_float4(0.f, 0.f, 0.f, 0.f));
             }
         }
         if (c == 0) {

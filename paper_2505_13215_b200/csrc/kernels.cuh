@@ -126,6 +126,13 @@ struct AdamPools {
     int64_t cap4, cap3;
     int n4, n3, K3;  // K3 = 3 * sh_count(deg)
 };
+// Threads per 4 Gaussians checking the SH class's gradient rows (K3 rows)
+__host__ __device__ inline int adam_sh_slices(int K3) { return K3 >= 16 ? 4 : 1; }
+// adam_classes_kernel's thread count
+inline uint32_t adam_class_units(int n3, int n4, int K3) {
+    const uint32_t q3 = div_up((uint32_t)n3, 4), q4 = div_up((uint32_t)n4, 4), S = adam_sh_slices(K3);
+    return (4 + S) * q3 + ((6 * q4 + 3) & ~3u) + S * q4;
+}
 __global__ void adam_classes_kernel(AdamPools P, AdamArgs A, uint8_t* __restrict__ cls_ok3,
                                     uint8_t* __restrict__ cls_ok4, unsigned long long* __restrict__ skipped_total,
                                     uint32_t* __restrict__ flags);

@@ -11,6 +11,7 @@
 // Reads 68 B (4D) / 44 B (3D) of geometry + 4*3K B of SH per Gaussian, all
 // coalesced from the component-major SoA pools; writes an 80 B SplatRec, a
 // depth key and a tile count.  Bound: HBM.
+#include <atomic>
 #include "hgs_common.cuh"
 #include "raster_common.cuh"
 #include "sh.cuh"
@@ -229,9 +230,15 @@ __global__ void preprocess_kernel(const float* __restrict__ p4, int64_t cap4, in
                                   SplatRec* __restrict__ rec, uint32_t* __restrict__ depth_key,
                                   uint32_t* __restrict__ ntiles_out, unsigned long long* __restrict__ stats,
                                   uint32_t* __restrict__ flags, ShRec* __restrict__ shrec);
-cudaError_t preprocess_setup() {
-    static cudaError_t e = cudaFuncSetAttribute(preprocess_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                (int)preprocess_smem_bytes(3));
+cudaError_t preprocess_setup() {  // the attribute is per device: set it once on each
+    static std::atomic<unsigned long long> done{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (done.load() & bit) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(preprocess_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)preprocess_smem_bytes(3));
+    if (e == cudaSuccess) done.fetch_or(bit);
     return e;
 }
 

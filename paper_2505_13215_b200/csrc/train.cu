@@ -325,7 +325,7 @@ hgs_status run_adam(hgs_ctx* ctx, const hgs_lrs* lrs, double mean_lr_scale, cons
         CK(ctx->adam_ok.ensure((size_t)(5 * ctx->cap3 + 7 * ctx->cap4)));
         uint8_t* ok3 = ctx->adam_ok.as<uint8_t>() + lo3;
         uint8_t* ok4 = ctx->adam_ok.as<uint8_t>() + 5 * ctx->cap3 + lo4;
-        const uint32_t units = 5 * div_up((uint32_t)n3, 4) + 7 * div_up((uint32_t)n4, 4);
+        const uint32_t units = adam_class_units(n3, n4, P.K3);
         CK(launch_pdl(adam_classes_kernel, dim3(div_up(units, 128)), dim3(128), 0, st, P, A, ok3, ok4, &sc->skipped,
                       &sc->flags));
         count_launch();
