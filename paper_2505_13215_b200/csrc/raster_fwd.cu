@@ -238,11 +238,12 @@ __global__ void __launch_bounds__(256) dup_bounds_kernel(const uint32_t* __restr
 
 // One instance i of the CTA's range: tile key and value (sorted splat index |
 // quadrant mask << 28).  s_off: the offsets of splats [j_lo, j_lo + cnt).
-__device__ __forceinline__ void dup_instance(int i, const uint32_t* s_off, int cnt, int j_lo,
-                                             const SplatFast* __restrict__ fast, int cull,
-                                             const CullRec* __restrict__ cull_rec, int tiles_x, uint32_t& key,
-                                             uint32_t& val) {
-    const int jl = last_le(s_off, 0, cnt - 1, (uint32_t)i);
+// instance i of the CTA's splat window; jl: the local index of its splat
+// (the last staged offset <= i)
+__device__ __forceinline__ void dup_instance_at(int i, int jl, const uint32_t* s_off, int cnt, int j_lo,
+                                                const SplatFast* __restrict__ fast, int cull,
+                                                const CullRec* __restrict__ cull_rec, int tiles_x, uint32_t& key,
+                                                uint32_t& val) {
     HGS_DCHECK(jl >= 0 && jl < cnt);
     const int j = j_lo + jl;
     const int32_t xr = __ldg(&fast[j].xr), yr = __ldg(&fast[j].yr);
@@ -269,6 +270,14 @@ __device__ __forceinline__ void dup_instance(int i, const uint32_t* s_off, int c
     }
     key = (uint32_t)(ty * tiles_x + tx);
     val = (uint32_t)j | (mask << kInstMaskShift);
+}
+
+__device__ __forceinline__ void dup_instance(int i, const uint32_t* s_off, int cnt, int j_lo,
+                                             const SplatFast* __restrict__ fast, int cull,
+                                             const CullRec* __restrict__ cull_rec, int tiles_x, uint32_t& key,
+                                             uint32_t& val) {
+    dup_instance_at(i, last_le(s_off, 0, cnt - 1, (uint32_t)i), s_off, cnt, j_lo, fast, cull, cull_rec, tiles_x, key,
+                    val);
 }
 
 __device__ __forceinline__ uint32_t dup_warp_incl_scan(uint32_t v) {
@@ -336,12 +345,18 @@ __global__ void __launch_bounds__(kDupThreads) duplicate_compact_kernel(
     constexpr int kPer = kDupPerCta / kDupThreads;  // 4 consecutive instances per thread
     uint32_t key[kPer], val[kPer];
     uint32_t nk = 0;
+    // one search for the thread's first instance, then forward steps (its
+    // 4 consecutive instances span few splats)
+    int jl = last_le(s_off, 0, cnt - 1, (uint32_t)min(i0 + (int)threadIdx.x * kPer, i_end - 1));
 #pragma unroll
     for (int k = 0; k < kPer; ++k) {
         const int i = i0 + threadIdx.x * kPer + k;
         key[k] = 0u;
         val[k] = 0u;
-        if (i < i_end) dup_instance(i, s_off, cnt, j_lo, fast, 1, cull_rec, tiles_x, key[k], val[k]);
+        if (i < i_end) {
+            while (jl + 1 < cnt && s_off[jl + 1] <= (uint32_t)i) ++jl;
+            dup_instance_at(i, jl, s_off, cnt, j_lo, fast, 1, cull_rec, tiles_x, key[k], val[k]);
+        }
         nk += (val[k] >> kInstMaskShift) ? 1u : 0u;
     }
     // block exclusive scan of the kept counts
