@@ -409,6 +409,21 @@ class Context:
         out["screen_norm4"], out["screen_norm3"] = sn4, sn3
         return out
 
+    def upload_grads(self, grads: dict, dtype=np.float64) -> None:
+        """Host gradients (the fields of grads(), same shapes) into the device
+        gradient rows (hgs_grads_upload) -- the optimizer_step(scene, const
+        SceneGrads&, ...) entry of train.hpp:68-69 with host gradients."""
+        n4, n3 = self.counts()
+        s = _empty_like_scene(n4, n3, self.sh_degree, dtype)
+        for f in HybridScene.DYN_FIELDS + HybridScene.STA_FIELDS:
+            a = np.ascontiguousarray(grads[f], dtype=dtype)
+            if a.shape != getattr(s, f).shape:
+                raise ValueError(f"gradient {f}: shape {a.shape}, expected {getattr(s, f).shape}")
+            setattr(s, f, a)
+        hs, keep = _host_scene(s, dtype)
+        self._check(self._lib.hgs_grads_upload(self._h, C.byref(hs), _dtype_code(dtype)))
+        del keep
+
     def grads_packed(self) -> tuple[int, int]:
         """(device pointer, float count) of the packed gradient payload
         (hgs_grads_packed): valid gradient rows + stat deltas, contiguous."""

@@ -233,6 +233,49 @@ def test_adam_matches_oracle(ctx):
         assert (np.linalg.norm(got.quat3, axis=1) - 1 < 1e-6).all() and (got.quat3[:, 0] >= 0).all()
 
 
+@pytest.mark.parametrize("deg", [0, 1, 2, 3])
+def test_adam_host_gradients_nonfinite_rows(ctx, deg):
+    """optimizer_step with host gradients (hgs_grads_upload): one non-finite
+    element in a single gradient row skips exactly that Gaussian's class --
+    placed in every SH row in turn (the SH class is checked in row slices
+    from degree 2 on), in the quaternions and in the means -- against the
+    oracle's optimizer_step (train.cpp:131-180)."""
+    rng = O.Rng(700 + deg)
+    scene = rng.random_scene(70, 90, deg).as_float32_exact()
+    ctx.upload(scene)
+    st = O.AdamState(scene)
+    ref = scene.copy()
+    K = (deg + 1) ** 2
+    gen = np.random.default_rng(deg)
+    for it in range(2):
+        g = {f: gen.uniform(-1, 1, getattr(scene, f).shape) for f in HybridScene.DYN_FIELDS + HybridScene.STA_FIELDS}
+        for j in range(3 * K):  # Gaussian j (mod n): SH coefficient j // 3, channel j % 3
+            bad = np.inf if j % 2 else np.nan
+            g["sh4"][j % 70, j // 3, j % 3] = bad
+            g["sh3"][(j + it) % 90, j // 3, j % 3] = bad
+        g["ql"][5, 2] = np.nan
+        g["qr"][6, 3] = np.inf
+        g["quat3"][7, 1] = np.nan
+        g["mean_x"][8, 0] = -np.inf
+        g["op3"][9] = np.nan
+        g["screen_norm4"], g["screen_norm3"] = np.zeros(70), np.zeros(90)
+        ctx.upload_grads(g)
+        skipped = ctx.adam_step()
+        before = st.skipped_nonfinite
+        O.optimizer_step(ref, g, st)
+        assert skipped == st.skipped_nonfinite - before
+        got = ctx.download()
+        m, v, _ = ctx.adam_state()
+        for f in HybridScene.DYN_FIELDS + HybridScene.STA_FIELDS:
+            a, b = getattr(got, f), getattr(ref, f)
+            assert np.abs(a - b).max(initial=0) <= 2e-6 * max(1.0, np.abs(b).max(initial=0)), f
+            assert np.allclose(getattr(v, f), getattr(st.v, f), rtol=1e-5, atol=1e-15), f
+        ref = got.copy()
+        for f in HybridScene.DYN_FIELDS + HybridScene.STA_FIELDS:
+            setattr(st.m, f, getattr(m, f).copy())
+            setattr(st.v, f, getattr(v, f).copy())
+
+
 def test_sweep_matches_oracle(ctx):
     rng = O.Rng(33)
     scene = rng.random_scene(7, 200, 2).as_float32_exact()
