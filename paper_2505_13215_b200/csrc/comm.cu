@@ -15,7 +15,11 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <condition_variable>
+#include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <initializer_list>
 #include <utility>
 #include <string>
@@ -59,9 +63,199 @@ int find_loaded_nccl(struct dl_phdr_info* info, size_t, void* out) {
     return 0;
 }
 
+// ---- loopback collectives (HGS_NCCL_LOOPBACK=1): the NCCL entry points
+// replaced by an in-process implementation for ranks that are threads of one
+// process sharing one device -- the test double that runs the N > 1 exchange
+// (all-reduce, reduce-scatter, all-gather, broadcast: every collective this
+// file issues) on a single GPU, where NCCL refuses two ranks per device.
+// Each call is a host barrier over the group; the last rank to arrive makes
+// its stream wait for every rank's inputs, combines them in rank order into
+// a scratch buffer (so in-place calls read before anything is written),
+// copies each rank's result out and records an event every rank's stream
+// waits on.  Group calls are executed one by one (every rank issues the same
+// sequence).
+enum LoopKind { LK_ALLREDUCE, LK_REDUCE_SCATTER, LK_ALLGATHER, LK_BROADCAST };
+constexpr int kLoopMaxRanks = 8;
+
+struct LoopCall {
+    const void* send;
+    void* recv;
+    cudaStream_t st;
+};
+struct LoopGroup {
+    int world = 0, joined = 0;
+    std::mutex mu;
+    std::condition_variable cv;
+    int arrived = 0;
+    unsigned long long gen = 0;
+    LoopCall calls[kLoopMaxRanks];
+    cudaEvent_t ready[kLoopMaxRanks] = {};
+    cudaEvent_t done = nullptr;
+    void* tmp = nullptr;
+    size_t tmp_bytes = 0;
+};
+struct LoopRank {
+    LoopGroup* g;
+    int rank;
+};
+std::mutex g_loop_mu;
+std::map<unsigned long long, LoopGroup*> g_loop_groups;
+unsigned long long g_loop_next = 1;
+
+struct LoopSrc {
+    const void* p[kLoopMaxRanks];
+};
+
+template <typename T>
+__global__ void loop_combine_kernel(LoopSrc src, int world, int kind, int root, size_t count, T* __restrict__ out) {
+    const size_t total = (kind == LK_ALLREDUCE || kind == LK_BROADCAST) ? count : count * (size_t)world;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+        T v;
+        if (kind == LK_ALLGATHER) {
+            v = static_cast<const T*>(src.p[i / count])[i % count];
+        } else if (kind == LK_BROADCAST) {
+            v = static_cast<const T*>(src.p[root])[i];
+        } else {
+            v = static_cast<const T*>(src.p[0])[i];
+            for (int k = 1; k < world; ++k) v += static_cast<const T*>(src.p[k])[i];
+        }
+        out[i] = v;
+    }
+}
+
+size_t loop_type_size(ncclDataType_t t) {
+    return (t == ncclFloat64 || t == ncclUint64 || t == ncclInt64) ? 8 : 4;
+}
+
+ncclResult_t loop_collective(int kind, const void* send, void* recv, size_t count, ncclDataType_t type, int root,
+                             ncclComm_t comm, cudaStream_t st) {
+    LoopRank* me = reinterpret_cast<LoopRank*>(comm);
+    LoopGroup& g = *me->g;
+    if (cudaEventRecord(g.ready[me->rank], st) != cudaSuccess) return ncclUnhandledCudaError;
+    std::unique_lock<std::mutex> lk(g.mu);
+    g.calls[me->rank] = LoopCall{send, recv, st};
+    const unsigned long long gen = g.gen;
+    if (++g.arrived < g.world) {
+        g.cv.wait(lk, [&] { return g.gen != gen; });
+    } else {
+        const size_t es = loop_type_size(type);
+        const size_t total = (kind == LK_ALLREDUCE || kind == LK_BROADCAST) ? count : count * (size_t)g.world;
+        bool ok = true;
+        for (int k = 0; k < g.world; ++k) ok &= cudaStreamWaitEvent(st, g.ready[k], 0) == cudaSuccess;
+        if (total * es > g.tmp_bytes) {
+            ok &= cudaStreamSynchronize(st) == cudaSuccess;
+            if (g.tmp) cudaFree(g.tmp);
+            g.tmp = nullptr;
+            ok &= cudaMalloc(&g.tmp, total * es) == cudaSuccess;
+            g.tmp_bytes = ok ? total * es : 0;
+        }
+        if (ok && total > 0) {
+            LoopSrc src{};
+            for (int k = 0; k < g.world; ++k) src.p[k] = g.calls[k].send;
+            const unsigned blocks = (unsigned)std::min<size_t>((total + 255) / 256, 4096);
+            if (type == ncclFloat32)
+                loop_combine_kernel<float><<<blocks, 256, 0, st>>>(src, g.world, kind, root, count,
+                                                                   static_cast<float*>(g.tmp));
+            else if (type == ncclFloat64)
+                loop_combine_kernel<double><<<blocks, 256, 0, st>>>(src, g.world, kind, root, count,
+                                                                    static_cast<double*>(g.tmp));
+            else if (es == 8)
+                loop_combine_kernel<unsigned long long><<<blocks, 256, 0, st>>>(
+                    src, g.world, kind, root, count, static_cast<unsigned long long*>(g.tmp));
+            else
+                loop_combine_kernel<uint32_t><<<blocks, 256, 0, st>>>(src, g.world, kind, root, count,
+                                                                      static_cast<uint32_t*>(g.tmp));
+            for (int k = 0; k < g.world; ++k) {
+                const char* from = static_cast<const char*>(g.tmp);
+                size_t n = count * es;
+                if (kind == LK_REDUCE_SCATTER) from += (size_t)k * count * es;
+                if (kind == LK_ALLGATHER) n = total * es;
+                ok &= cudaMemcpyAsync(g.calls[k].recv, from, n, cudaMemcpyDeviceToDevice, st) == cudaSuccess;
+            }
+        }
+        ok &= cudaEventRecord(g.done, st) == cudaSuccess;
+        g.arrived = 0;
+        ++g.gen;
+        g.cv.notify_all();
+        if (!ok) return ncclUnhandledCudaError;
+    }
+    lk.unlock();
+    return cudaStreamWaitEvent(st, g.done, 0) == cudaSuccess ? ncclSuccess : ncclUnhandledCudaError;
+}
+
+ncclResult_t loop_get_unique_id(ncclUniqueId* id) {
+    std::lock_guard<std::mutex> lk(g_loop_mu);
+    std::memset(id, 0, sizeof(*id));
+    const unsigned long long key = g_loop_next++;
+    std::memcpy(id->internal, &key, sizeof(key));
+    return ncclSuccess;
+}
+ncclResult_t loop_comm_init_rank(ncclComm_t* comm, int world, ncclUniqueId id, int rank) {
+    if (world < 1 || world > kLoopMaxRanks || rank < 0 || rank >= world) return ncclInvalidArgument;
+    unsigned long long key;
+    std::memcpy(&key, id.internal, sizeof(key));
+    std::lock_guard<std::mutex> lk(g_loop_mu);
+    LoopGroup*& g = g_loop_groups[key];
+    if (!g) {
+        g = new LoopGroup();
+        g->world = world;
+        for (int k = 0; k < world; ++k) cudaEventCreateWithFlags(&g->ready[k], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&g->done, cudaEventDisableTiming);
+    }
+    if (g->world != world) return ncclInvalidArgument;
+    ++g->joined;
+    *comm = reinterpret_cast<ncclComm_t>(new LoopRank{g, rank});
+    return ncclSuccess;
+}
+ncclResult_t loop_comm_init_all(ncclComm_t*, int, const int*) { return ncclInvalidUsage; }
+ncclResult_t loop_comm_destroy(ncclComm_t comm) {
+    LoopRank* me = reinterpret_cast<LoopRank*>(comm);
+    std::lock_guard<std::mutex> lk(g_loop_mu);
+    delete me;  // (the group stays: its events may still be waited on)
+    return ncclSuccess;
+}
+ncclResult_t loop_all_reduce(const void* s, void* r, size_t n, ncclDataType_t t, ncclRedOp_t, ncclComm_t c,
+                             cudaStream_t st) {
+    return loop_collective(LK_ALLREDUCE, s, r, n, t, 0, c, st);
+}
+ncclResult_t loop_broadcast(const void* s, void* r, size_t n, ncclDataType_t t, int root, ncclComm_t c,
+                            cudaStream_t st) {
+    return loop_collective(LK_BROADCAST, s, r, n, t, root, c, st);
+}
+ncclResult_t loop_reduce_scatter(const void* s, void* r, size_t n, ncclDataType_t t, ncclRedOp_t, ncclComm_t c,
+                                 cudaStream_t st) {
+    return loop_collective(LK_REDUCE_SCATTER, s, r, n, t, 0, c, st);
+}
+ncclResult_t loop_all_gather(const void* s, void* r, size_t n, ncclDataType_t t, ncclComm_t c, cudaStream_t st) {
+    return loop_collective(LK_ALLGATHER, s, r, n, t, 0, c, st);
+}
+ncclResult_t loop_group() { return ncclSuccess; }
+const char* loop_error_string(ncclResult_t r) { return r == ncclSuccess ? "success" : "loopback collective failed"; }
+ncclResult_t loop_version(int* v) {
+    *v = 0;
+    return ncclSuccess;
+}
+
 NcclApi& nccl() {
     static NcclApi api = [] {
         NcclApi a;
+        if (getenv("HGS_NCCL_LOOPBACK")) {  // in-process test double (above)
+            a.GetUniqueId = loop_get_unique_id;
+            a.CommInitRank = loop_comm_init_rank;
+            a.CommInitAll = loop_comm_init_all;
+            a.CommDestroy = loop_comm_destroy;
+            a.AllReduce = loop_all_reduce;
+            a.Broadcast = loop_broadcast;
+            a.ReduceScatter = loop_reduce_scatter;
+            a.AllGather = loop_all_gather;
+            a.GroupStart = loop_group;
+            a.GroupEnd = loop_group;
+            a.GetErrorString = loop_error_string;
+            a.GetVersion = loop_version;
+            a.path = "loopback";
+            a.loaded = true;
+            return a;
+        }
         std::string loaded;
         dl_iterate_phdr(find_loaded_nccl, &loaded);
         void* h = loaded.empty() ? nullptr : dlopen(loaded.c_str(), RTLD_NOW | RTLD_NOLOAD);

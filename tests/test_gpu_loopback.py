@@ -1,0 +1,149 @@
+"""The C-ABI exchange with TWO ranks on one B200, through the library's own
+collective path (csrc/comm.cu), NCCL replaced by its in-process loopback
+double (HGS_NCCL_LOOPBACK=1: ranks are threads of one process sharing the
+device; every all-reduce / reduce-scatter / all-gather / broadcast is a host
+barrier + a combine kernel in rank order).  NCCL itself refuses two ranks on
+one device, so this is how the N > 1 product path -- hgs_train_exchange_async
+with the grouped all-reduce, and the sharded reduce-scatter -> Adam on the
+rank's shard -> all-gather -- runs here.  Checked: the two replicas are
+bit-identical after three exchanged iterations in both modes, the sharded
+exchange gives the all-reduce exchange's parameters and (after
+hgs_gather_state) Adam moments, the replicas' summed loss equals one process
+running the 2-view iteration, and a broadcast repairs a diverged replica.
+"""
+import multiprocessing as mp
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+FIELDS = ("mean_x", "mean_t", "ql", "qr", "log_s4", "op4", "sh4", "mean3", "quat3", "log_s3", "op3", "sh3")
+
+
+def _setup():
+    from paper_2505_13215_b200.scene import ring_camera, synthetic_scene
+
+    target = synthetic_scene(3001, 2003, sh_degree=3, seed=81)  # odd counts: ragged shards
+    scene = synthetic_scene(3001, 2003, sh_degree=3, seed=82).as_float32_exact()
+    cams = [ring_camera(8, 96, 72, index=i, n_ring=4) for i in range(4)]
+    return scene, target, cams, [0.1, 0.4, 0.6, 0.9]
+
+
+def _run_ranks(mode, world, out, errs):
+    import ctypes as C
+    import threading
+
+    from paper_2505_13215_b200 import api as A
+    from paper_2505_13215_b200.train import DeviceTrainer, shard_batch
+
+    scene, target, cams, times = _setup()
+    uid = A.Context.comm_unique_id()
+    ctxs = [A.Context(0) for _ in range(world)]
+    trs = [DeviceTrainer(c, scene, cams, times, target=target, bg=(0.2, 0.2, 0.2), iterations=50) for c in ctxs]
+
+    def rank_fn(r):
+        try:
+            ctx, tr = ctxs[r], trs[r]
+            ctx.comm_init(world, r, uid)
+            ctx.set_sharded(mode == "sharded")
+            losses = []
+            for i in range(3):
+                batch = [i % 4, (i + 1) % 4]
+                tr.iter += 1
+                DeviceTrainer.step_async(tr, shard_batch(batch, r, world), batch_total=len(batch),
+                                         apply_adam=False)
+                ctx._check(ctx._lib.hgs_train_exchange_async(ctx.handle, C.byref(tr._opts(tr.decay()))))
+                losses.append(tr.collect())
+            ctx.gather_state()  # collective
+            s = ctx.download()
+            m, v, step = ctx.adam_state()
+            out[(mode, r)] = dict(losses=losses, checksum=ctx.param_checksum(), step=step,
+                                  p={f: np.asarray(getattr(s, f)).copy() for f in FIELDS},
+                                  m={f: np.asarray(getattr(m, f)).copy() for f in FIELDS},
+                                  v={f: np.asarray(getattr(v, f)).copy() for f in FIELDS},
+                                  stats=[np.asarray(a).copy() for a in ctx.densify_stats()])
+            if mode == "allreduce":
+                # a diverged replica is repaired by a broadcast from rank 0
+                if r == 1:
+                    s2 = ctx.download()
+                    s2.op3[:7] += 0.25
+                    ctx.upload(s2)
+                before = ctx.param_checksum()
+                ctx.broadcast_params(0)
+                out[(mode, r, "repair")] = (before, ctx.param_checksum())
+        except BaseException as e:  # reported by the parent
+            errs.append(f"{mode} rank {r}: {type(e).__name__}: {e}")
+
+    ts = [threading.Thread(target=rank_fn, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=600)
+    for c in ctxs:
+        c.close()
+
+
+def _child(path):
+    out, errs = {}, []
+    for mode in ("allreduce", "sharded"):
+        _run_ranks(mode, 2, out, errs)
+        if errs:
+            break
+    # one process, no exchange: the first 2-view iteration's loss
+    from paper_2505_13215_b200.api import Context
+    from paper_2505_13215_b200.train import DeviceTrainer
+
+    ref_loss = None
+    if not errs:
+        scene, target, cams, times = _setup()
+        with Context(0) as ctx:
+            tr = DeviceTrainer(ctx, scene, cams, times, target=target, bg=(0.2, 0.2, 0.2), iterations=50)
+            ref_loss = tr.step([0, 1], apply_adam=False)
+    np.save(path, np.array([dict(out=out, errs=errs, ref_loss=ref_loss)], dtype=object), allow_pickle=True)
+
+
+def test_two_rank_exchange_loopback(tmp_path):
+    path = str(tmp_path / "loop.npy")
+    old = os.environ.get("HGS_NCCL_LOOPBACK")
+    os.environ["HGS_NCCL_LOOPBACK"] = "1"  # read by the child's library at its first collective
+    try:
+        p = mp.get_context("spawn").Process(target=_child, args=(path,))
+        p.start()
+        p.join(900)
+    finally:
+        if old is None:
+            os.environ.pop("HGS_NCCL_LOOPBACK", None)
+        else:
+            os.environ["HGS_NCCL_LOOPBACK"] = old
+    assert p.exitcode == 0, p.exitcode
+    res = np.load(path, allow_pickle=True)[0]
+    assert not res["errs"], res["errs"]
+    out = res["out"]
+    for mode in ("allreduce", "sharded"):
+        a, b = out[(mode, 0)], out[(mode, 1)]
+        # replicas bit-identical (parameters, gathered moments, statistics, step)
+        assert a["checksum"] == b["checksum"], mode
+        assert a["step"] == b["step"] == 3
+        for f in FIELDS:
+            assert np.array_equal(a["p"][f], b["p"][f]), (mode, f)
+            assert np.array_equal(a["m"][f], b["m"][f]), (mode, f)
+            assert np.array_equal(a["v"][f], b["v"][f]), (mode, f)
+        for x, y in zip(a["stats"], b["stats"]):
+            assert np.array_equal(x, y), mode
+        # the first iteration: rank losses (means over the rank's view) sum to
+        # the one-process 2-view loss
+        assert (a["losses"][0] + b["losses"][0]) / 2 == pytest.approx(res["ref_loss"], rel=1e-6)
+    # sharded == all-reduce exchange up to K6's atomic summation order
+    ar, sh = out[("allreduce", 0)], out[("sharded", 0)]
+    for f in FIELDS:
+        assert np.allclose(sh["p"][f], ar["p"][f], rtol=1e-5, atol=1e-7), f
+        assert np.allclose(sh["m"][f], ar["m"][f], rtol=1e-4, atol=1e-9), f
+        assert np.allclose(sh["v"][f], ar["v"][f], rtol=1e-4, atol=1e-12), f
+    for x, y in zip(sh["stats"], ar["stats"]):
+        assert np.allclose(x, y, rtol=1e-5, atol=1e-12)
+    # broadcast repair: rank 1 diverged, both end on rank 0's parameters
+    b0, a0 = out[("allreduce", 0, "repair")]
+    b1, a1 = out[("allreduce", 1, "repair")]
+    assert b1 != b0 and a0 == a1 == b0
