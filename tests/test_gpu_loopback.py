@@ -5,7 +5,8 @@ device; every all-reduce / reduce-scatter / all-gather / broadcast is a host
 barrier + a combine kernel in rank order).  NCCL itself refuses two ranks on
 one device, so this is how the N > 1 product path -- hgs_train_exchange_async
 with the grouped all-reduce, and the sharded reduce-scatter -> Adam on the
-rank's shard -> all-gather -- runs here.  Checked: the two replicas are
+rank's shard -> all-gather -- runs here (2 ranks; the sharded exchange also
+with 3, one of which renders no view).  Checked: the replicas are
 bit-identical after three exchanged iterations in both modes, the sharded
 exchange gives the all-reduce exchange's parameters and (after
 hgs_gather_state) Adam moments, the replicas' summed loss equals one process
@@ -31,7 +32,7 @@ def _setup():
     return scene, target, cams, [0.1, 0.4, 0.6, 0.9]
 
 
-def _run_ranks(mode, world, out, errs):
+def _run_ranks(mode, world, out, errs, tmp):
     import ctypes as C
     import threading
 
@@ -56,10 +57,15 @@ def _run_ranks(mode, world, out, errs):
                                          apply_adam=False)
                 ctx._check(ctx._lib.hgs_train_exchange_async(ctx.handle, C.byref(tr._opts(tr.decay()))))
                 losses.append(tr.collect())
+            refused = False  # sharded moments: the state-dependent calls refuse
+            try:
+                ctx.save_checkpoint(os.path.join(tmp, f"{mode}{world}_{r}.hgsc"))
+            except A.StateError:
+                refused = True
             ctx.gather_state()  # collective
             s = ctx.download()
             m, v, step = ctx.adam_state()
-            out[(mode, r)] = dict(losses=losses, checksum=ctx.param_checksum(), step=step,
+            out[(mode, world, r)] = dict(losses=losses, checksum=ctx.param_checksum(), step=step, refused=refused,
                                   p={f: np.asarray(getattr(s, f)).copy() for f in FIELDS},
                                   m={f: np.asarray(getattr(m, f)).copy() for f in FIELDS},
                                   v={f: np.asarray(getattr(v, f)).copy() for f in FIELDS},
@@ -72,7 +78,7 @@ def _run_ranks(mode, world, out, errs):
                     ctx.upload(s2)
                 before = ctx.param_checksum()
                 ctx.broadcast_params(0)
-                out[(mode, r, "repair")] = (before, ctx.param_checksum())
+                out[(mode, world, r, "repair")] = (before, ctx.param_checksum())
         except BaseException as e:  # reported by the parent
             errs.append(f"{mode} rank {r}: {type(e).__name__}: {e}")
 
@@ -87,8 +93,8 @@ def _run_ranks(mode, world, out, errs):
 
 def _child(path):
     out, errs = {}, []
-    for mode in ("allreduce", "sharded"):
-        _run_ranks(mode, 2, out, errs)
+    for mode, world in (("allreduce", 2), ("sharded", 2), ("sharded", 3)):
+        _run_ranks(mode, world, out, errs, os.path.dirname(path))
         if errs:
             break
     # one process, no exchange: the first 2-view iteration's loss
@@ -121,29 +127,38 @@ def test_two_rank_exchange_loopback(tmp_path):
     res = np.load(path, allow_pickle=True)[0]
     assert not res["errs"], res["errs"]
     out = res["out"]
-    for mode in ("allreduce", "sharded"):
-        a, b = out[(mode, 0)], out[(mode, 1)]
-        # replicas bit-identical (parameters, gathered moments, statistics, step)
-        assert a["checksum"] == b["checksum"], mode
-        assert a["step"] == b["step"] == 3
+    for mode, world in (("allreduce", 2), ("sharded", 2), ("sharded", 3)):
+        a = out[(mode, world, 0)]
+        for r in range(world):
+            assert out[(mode, world, r)]["refused"] == (mode == "sharded"), (mode, world, r)
+        for r in range(1, world):
+            b = out[(mode, world, r)]
+            # replicas bit-identical (parameters, gathered moments, statistics, step)
+            assert a["checksum"] == b["checksum"], (mode, world)
+            assert a["step"] == b["step"] == 3
+            for f in FIELDS:
+                assert np.array_equal(a["p"][f], b["p"][f]), (mode, world, f)
+                assert np.array_equal(a["m"][f], b["m"][f]), (mode, world, f)
+                assert np.array_equal(a["v"][f], b["v"][f]), (mode, world, f)
+            for x, y in zip(a["stats"], b["stats"]):
+                assert np.array_equal(x, y), (mode, world)
+        if world == 2:
+            # the first iteration: the ranks' one-view losses average to the
+            # one-process 2-view loss
+            b = out[(mode, world, 1)]
+            assert (a["losses"][0] + b["losses"][0]) / 2 == pytest.approx(res["ref_loss"], rel=1e-6)
+    # sharded (2 or 3 ranks; with 3, one rank renders no view) == all-reduce
+    # exchange, up to K6's atomic summation order
+    ar = out[("allreduce", 2, 0)]
+    for world in (2, 3):
+        sh = out[("sharded", world, 0)]
         for f in FIELDS:
-            assert np.array_equal(a["p"][f], b["p"][f]), (mode, f)
-            assert np.array_equal(a["m"][f], b["m"][f]), (mode, f)
-            assert np.array_equal(a["v"][f], b["v"][f]), (mode, f)
-        for x, y in zip(a["stats"], b["stats"]):
-            assert np.array_equal(x, y), mode
-        # the first iteration: rank losses (means over the rank's view) sum to
-        # the one-process 2-view loss
-        assert (a["losses"][0] + b["losses"][0]) / 2 == pytest.approx(res["ref_loss"], rel=1e-6)
-    # sharded == all-reduce exchange up to K6's atomic summation order
-    ar, sh = out[("allreduce", 0)], out[("sharded", 0)]
-    for f in FIELDS:
-        assert np.allclose(sh["p"][f], ar["p"][f], rtol=1e-5, atol=1e-7), f
-        assert np.allclose(sh["m"][f], ar["m"][f], rtol=1e-4, atol=1e-9), f
-        assert np.allclose(sh["v"][f], ar["v"][f], rtol=1e-4, atol=1e-12), f
-    for x, y in zip(sh["stats"], ar["stats"]):
-        assert np.allclose(x, y, rtol=1e-5, atol=1e-12)
+            assert np.allclose(sh["p"][f], ar["p"][f], rtol=1e-5, atol=1e-7), (world, f)
+            assert np.allclose(sh["m"][f], ar["m"][f], rtol=1e-4, atol=1e-9), (world, f)
+            assert np.allclose(sh["v"][f], ar["v"][f], rtol=1e-4, atol=1e-12), (world, f)
+        for x, y in zip(sh["stats"], ar["stats"]):
+            assert np.allclose(x, y, rtol=1e-5, atol=1e-12), world
     # broadcast repair: rank 1 diverged, both end on rank 0's parameters
-    b0, a0 = out[("allreduce", 0, "repair")]
-    b1, a1 = out[("allreduce", 1, "repair")]
+    b0, a0 = out[("allreduce", 2, 0, "repair")]
+    b1, a1 = out[("allreduce", 2, 1, "repair")]
     assert b1 != b0 and a0 == a1 == b0
