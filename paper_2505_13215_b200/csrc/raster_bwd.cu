@@ -272,7 +272,10 @@ __global__ void __launch_bounds__(kThreadsB, 8) raster_bwd_kernel(
     const uint2 rg = ranges[tile];
     HGS_DCHECK(rg.x <= rg.y && rg.y <= g_chk.inst);
     const float pxc = (float)px + 0.5f, pyc0 = (float)py0 + 0.5f, pyc1 = (float)py1 + 0.5f;
-    const double pcx = (double)px + 0.5, pcy0 = (double)py0 + 0.5, pcy1 = (double)py1 + 0.5;
+    // FP64 pixel centres for the rare exact paths, rebuilt there (opaque: not
+    // hoisted into 6 loop-carried registers of the 64)
+    auto pcx = [&] { return (double)(int)opaque_u32((uint32_t)px) + 0.5; };
+    auto pcy = [&](int py) { return (double)(int)opaque_u32((uint32_t)py) + 0.5; };
 
     struct Pix1 {
         float gr, gg, gb, T, GS;
@@ -295,7 +298,10 @@ __global__ void __launch_bounds__(kThreadsB, 8) raster_bwd_kernel(
         if (!(l & 0x80000000u) && !zero) s.last = l;
         if ((l & 0x80000000u) && !zero) s_fix[atomicAdd(&s_nfix, 1u)] = (uint32_t)pix;
     };
-    const int cshift = px - tx * kTile, rshift0 = 16 + py0 - ty * kTile, rshift1 = rshift0 + 4;
+    // the box test's bits in a staged tile-relative mask (column bit | row bit):
+    // a pixel is in the box iff both are set
+    const int cshift = px - tx * kTile, rshift0 = 16 + py0 - ty * kTile;
+    const uint32_t bx0 = (1u << cshift) | (1u << rshift0), bx1 = (1u << cshift) | (1u << (rshift0 + 4));
     if (threadIdx.x == 0) s_nfix = 0u;
     __syncthreads();
     PixBwd2 s;
@@ -355,9 +361,8 @@ __global__ void __launch_bounds__(kThreadsB, 8) raster_bwd_kernel(
             bool b0 = (int)o16 < l0, b1 = (int)o16 < l1;
             if (!(le & 0x8000u)) {
                 const uint32_t bm = lds_u32(a_bm + o4);
-                const bool colin = (bm >> cshift) & 1u;
-                b0 = b0 & colin & ((bm >> rshift0) & 1u);
-                b1 = b1 & colin & ((bm >> rshift1) & 1u);
+                b0 = b0 && (bm & bx0) == bx0;
+                b1 = b1 && (bm & bx1) == bx1;
             }
             if (!__any_sync(0xffffffffu, b0 || b1)) continue;
 #ifdef HGS_CHECKED
@@ -374,14 +379,14 @@ __global__ void __launch_bounds__(kThreadsB, 8) raster_bwd_kernel(
             float x0 = INFINITY, x1 = INFINITY, dx0 = 0.f, dx1 = 0.f, dy0 = 0.f, dy1 = 0.f;
             if (__int_as_float(hdr.w) < 0.0f) {  // FP64 exponent path (uniform per splat)
                 if (b0) {
-                    x0 = exact_x(e, pcx, pcy0);
-                    const float2 d = exact_delta(e, pcx, pcy0);
+                    x0 = exact_x(e, pcx(), pcy(py0));
+                    const float2 d = exact_delta(e, pcx(), pcy(py0));
                     dx0 = d.x;
                     dy0 = d.y;
                 }
                 if (b1) {
-                    x1 = exact_x(e, pcx, pcy1);
-                    const float2 d = exact_delta(e, pcx, pcy1);
+                    x1 = exact_x(e, pcx(), pcy(py1));
+                    const float2 d = exact_delta(e, pcx(), pcy(py1));
                     dx1 = d.x;
                     dy1 = d.y;
                 }
@@ -403,8 +408,8 @@ __global__ void __launch_bounds__(kThreadsB, 8) raster_bwd_kernel(
             bool p0 = b0 && x0 < x_skip, p1 = b1 && x1 < x_skip;
             const bool band0 = p0 && x0 >= x_keep, band1 = p1 && x1 >= x_keep;
             if (band0 || band1) {  // rare
-                if (band0) p0 = exact_alpha_passes(e, pcx, pcy0);
-                if (band1) p1 = exact_alpha_passes(e, pcx, pcy1);
+                if (band0) p0 = exact_alpha_passes(e, pcx(), pcy(py0));
+                if (band1) p1 = exact_alpha_passes(e, pcx(), pcy(py1));
             }
             // lanes without a contributing pixel hold zeros; skip the
             // reduction when the whole warp is empty

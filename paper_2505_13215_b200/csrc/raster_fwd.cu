@@ -703,9 +703,15 @@ __global__ void __launch_bounds__(kThreads, 8) raster_fwd_kernel(
     const uint2 rg = ranges[tile];
     HGS_DCHECK(rg.x <= rg.y && rg.y <= g_chk.inst);
     const float pxc = (float)px + 0.5f, pyc0 = (float)py0 + 0.5f, pyc1 = (float)py1 + 0.5f;
-    const double pcx = (double)px + 0.5, pcy0 = (double)py0 + 0.5, pcy1 = (double)py1 + 0.5;
+    // FP64 pixel centres for the rare exact paths, rebuilt there (opaque: not
+    // hoisted into 6 loop-carried registers of the 64)
+    auto pcx = [&] { return (double)(int)opaque_u32((uint32_t)px) + 0.5; };
+    auto pcy = [&](int py) { return (double)(int)opaque_u32((uint32_t)py) + 0.5; };
 
-    const int cshift = px - tx * kTile, rshift0 = 16 + py0 - ty * kTile, rshift1 = rshift0 + 4;
+    // the box test's bits in a staged tile-relative mask (column bit | row bit):
+    // a pixel is in the box iff both are set
+    const int cshift = px - tx * kTile, rshift0 = 16 + py0 - ty * kTile;
+    const uint32_t bx0 = (1u << cshift) | (1u << rshift0), bx1 = (1u << cshift) | (1u << (rshift0 + 4));
     PixFwd2 s;
     s.T = f2_bc(1.0f);
     s.r = s.g = s.b = s.E = f2_bc(0.0f);
@@ -757,9 +763,8 @@ __global__ void __launch_bounds__(kThreads, 8) raster_fwd_kernel(
             // the staged tile-relative column/row masks
             if (!(le & 0x8000u)) {
                 const uint32_t bm = lds_u32(a_bm + o4);
-                const bool colin = (bm >> cshift) & 1u;
-                b0 = b0 & colin & ((bm >> rshift0) & 1u);
-                b1 = b1 & colin & ((bm >> rshift1) & 1u);
+                b0 = b0 && (bm & bx0) == bx0;
+                b1 = b1 && (bm & bx1) == bx1;
                 if (!(b0 || b1)) continue;
             }
             if (kCount) {
@@ -776,8 +781,8 @@ __global__ void __launch_bounds__(kThreads, 8) raster_fwd_kernel(
             // = 0 in composite_pairs) stays finite, and above every x_skip
             float x0 = 128.0f, x1 = 128.0f;
             if (eps_s < 0.0f) {  // FP64 exponent path (uniform per splat)
-                if (b0) x0 = exact_x(e, pcx, pcy0);
-                if (b1) x1 = exact_x(e, pcx, pcy1);
+                if (b0) x0 = exact_x(e, pcx(), pcy(py0));
+                if (b1) x1 = exact_x(e, pcx(), pcy(py1));
             } else {  // both pixels share the column: one dx, the rest packed (= fast_x per pixel)
                 const float4 m = lds_f4(a_mean + o16);
                 const float dx = __fsub_rn(__fsub_rn(pxc, m.x), m.z);
@@ -793,8 +798,8 @@ __global__ void __launch_bounds__(kThreads, 8) raster_fwd_kernel(
             bool p0 = b0 && x0 < x_skip, p1 = b1 && x1 < x_skip;
             const bool band0 = p0 && x0 >= x_keep, band1 = p1 && x1 >= x_keep;
             if (band0 || band1) {  // rare
-                if (band0) p0 = exact_alpha_passes(e, pcx, pcy0);
-                if (band1) p1 = exact_alpha_passes(e, pcx, pcy1);
+                if (band0) p0 = exact_alpha_passes(e, pcx(), pcy(py0));
+                if (band1) p1 = exact_alpha_passes(e, pcx(), pcy(py1));
             }
             if (!(p0 || p1)) continue;
 #ifdef HGS_CHECKED
