@@ -301,7 +301,12 @@ __global__ void __launch_bounds__(kThreadsB, 8) raster_bwd_kernel(
     // the box test's bits in a staged tile-relative mask (column bit | row bit):
     // a pixel is in the box iff both are set
     const int cshift = px - tx * kTile, rshift0 = 16 + py0 - ty * kTile;
-    const uint32_t bx0 = (1u << cshift) | (1u << rshift0), bx1 = (1u << cshift) | (1u << (rshift0 + 4));
+    // per-thread loop constants in shared memory (read back with volatile
+    // loads where needed): the box-test bits and the FP32 pixel-centre column
+    __shared__ uint4 s_pix[kThreadsB];
+    s_pix[threadIdx.x] = make_uint4((1u << cshift) | (1u << rshift0), (1u << cshift) | (1u << (rshift0 + 4)),
+                                    __float_as_uint(pxc), 0u);
+    const uint32_t a_pix = opaque_u32((uint32_t)__cvta_generic_to_shared(&s_pix[threadIdx.x]));
     if (threadIdx.x == 0) s_nfix = 0u;
     __syncthreads();
     PixBwd2 s;
@@ -361,8 +366,9 @@ __global__ void __launch_bounds__(kThreadsB, 8) raster_bwd_kernel(
             bool b0 = (int)o16 < l0, b1 = (int)o16 < l1;
             if (!(le & 0x8000u)) {
                 const uint32_t bm = lds_u32(a_bm + o4);
-                b0 = b0 && (bm & bx0) == bx0;
-                b1 = b1 && (bm & bx1) == bx1;
+                const uint2 bx = ldsv_u2(a_pix);
+                b0 = b0 && (bm & bx.x) == bx.x;
+                b1 = b1 && (bm & bx.y) == bx.y;
             }
             if (!__any_sync(0xffffffffu, b0 || b1)) continue;
 #ifdef HGS_CHECKED
@@ -371,28 +377,29 @@ __global__ void __launch_bounds__(kThreadsB, 8) raster_bwd_kernel(
             if (lane == 0) ++n_wit;
 #endif
             const float4 L = lds_f4(a_chol + o16), col = lds_f4(a_col + o16);
-            const uint32_t sj = lds_u32(a_j + o4);
-            HGS_DCHECK(sj < g_chk.splats);
-            const SplatRec* e = exact + sj;
+            // the splat's index (loaded where used: the rare exact paths and the
+            // accumulator address)
+            auto sjf = [&] { return lds_u32(a_j + o4); };
+            auto rec = [&] { return exact + sjf(); };
             // exponent argument and offset of both pixels (same column: one dx
             // on the fast path, the same rounding sequence as K4's fast_x)
             float x0 = INFINITY, x1 = INFINITY, dx0 = 0.f, dx1 = 0.f, dy0 = 0.f, dy1 = 0.f;
             if (__int_as_float(hdr.w) < 0.0f) {  // FP64 exponent path (uniform per splat)
                 if (b0) {
-                    x0 = exact_x(e, pcx(), pcy(py0));
-                    const float2 d = exact_delta(e, pcx(), pcy(py0));
+                    x0 = exact_x(rec(), pcx(), pcy(py0));
+                    const float2 d = exact_delta(rec(), pcx(), pcy(py0));
                     dx0 = d.x;
                     dy0 = d.y;
                 }
                 if (b1) {
-                    x1 = exact_x(e, pcx(), pcy(py1));
-                    const float2 d = exact_delta(e, pcx(), pcy(py1));
+                    x1 = exact_x(rec(), pcx(), pcy(py1));
+                    const float2 d = exact_delta(rec(), pcx(), pcy(py1));
                     dx1 = d.x;
                     dy1 = d.y;
                 }
             } else {  // both pixels in one packed sequence (= fast_x per pixel)
                 const float4 m = lds_f4(a_mean + o16);
-                dx0 = __fsub_rn(__fsub_rn(pxc, m.x), m.z);
+                dx0 = __fsub_rn(__fsub_rn(ldsv_f(a_pix + 8), m.x), m.z);
                 dx1 = dx0;
                 const f2 DY = f2_sub(f2_sub(PYC, f2_bc(m.y)), f2_bc(m.w));
                 const f2 U1 = f2_fma(f2_bc(L.x), f2_bc(dx0), f2_mul(f2_bc(L.y), DY));
@@ -408,8 +415,8 @@ __global__ void __launch_bounds__(kThreadsB, 8) raster_bwd_kernel(
             bool p0 = b0 && x0 < x_skip, p1 = b1 && x1 < x_skip;
             const bool band0 = p0 && x0 >= x_keep, band1 = p1 && x1 >= x_keep;
             if (band0 || band1) {  // rare
-                if (band0) p0 = exact_alpha_passes(e, pcx(), pcy(py0));
-                if (band1) p1 = exact_alpha_passes(e, pcx(), pcy(py1));
+                if (band0) p0 = exact_alpha_passes(rec(), pcx(), pcy(py0));
+                if (band1) p1 = exact_alpha_passes(rec(), pcx(), pcy(py1));
             }
             // lanes without a contributing pixel hold zeros; skip the
             // reduction when the whole warp is empty
@@ -432,6 +439,8 @@ __global__ void __launch_bounds__(kThreadsB, 8) raster_bwd_kernel(
             v[6] = fmaf(hx0, dx0, hx1 * dx1);
             v[7] = fmaf(hx0, dy0, hx1 * dy1);
             v[8] = fmaf(hy0, dy0, hy1 * dy1);
+            const uint32_t sj = sjf();
+            HGS_DCHECK(sj < g_chk.splats);
             acc_t* dst = accum + (size_t)sj * kAccStride;
             const unsigned am = __ballot_sync(0xffffffffu, p0 || p1);
             if (__popc(am) <= kDirectLanes) {

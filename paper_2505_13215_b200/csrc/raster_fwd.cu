@@ -711,7 +711,12 @@ __global__ void __launch_bounds__(kThreads, 8) raster_fwd_kernel(
     // the box test's bits in a staged tile-relative mask (column bit | row bit):
     // a pixel is in the box iff both are set
     const int cshift = px - tx * kTile, rshift0 = 16 + py0 - ty * kTile;
-    const uint32_t bx0 = (1u << cshift) | (1u << rshift0), bx1 = (1u << cshift) | (1u << (rshift0 + 4));
+    // per-thread loop constants in shared memory (read back with volatile
+    // loads where needed): the box-test bits and the FP32 pixel-centre column
+    __shared__ uint4 s_pix[kThreads];
+    s_pix[threadIdx.x] = make_uint4((1u << cshift) | (1u << rshift0), (1u << cshift) | (1u << (rshift0 + 4)),
+                                    __float_as_uint(pxc), 0u);
+    const uint32_t a_pix = opaque_u32((uint32_t)__cvta_generic_to_shared(&s_pix[threadIdx.x]));
     PixFwd2 s;
     s.T = f2_bc(1.0f);
     s.r = s.g = s.b = s.E = f2_bc(0.0f);
@@ -763,8 +768,9 @@ __global__ void __launch_bounds__(kThreads, 8) raster_fwd_kernel(
             // the staged tile-relative column/row masks
             if (!(le & 0x8000u)) {
                 const uint32_t bm = lds_u32(a_bm + o4);
-                b0 = b0 && (bm & bx0) == bx0;
-                b1 = b1 && (bm & bx1) == bx1;
+                const uint2 bx = ldsv_u2(a_pix);
+                b0 = b0 && (bm & bx.x) == bx.x;
+                b1 = b1 && (bm & bx.y) == bx.y;
                 if (!(b0 || b1)) continue;
             }
             if (kCount) {
@@ -775,17 +781,18 @@ __global__ void __launch_bounds__(kThreads, 8) raster_fwd_kernel(
             n_box += (int)b0 + (int)b1;
 #endif
             const float4 L = lds_f4(a_chol + o16), c = lds_f4(a_col + o16);
-            const SplatRec* e = exact + lds_u32(a_j + o4);
+            // the exact record (rare paths only: loaded there)
+            auto rec = [&] { return exact + lds_u32(a_j + o4); };
             const float eps_s = __int_as_float(hdr.w);
             // a pixel outside the box keeps x = 128: finite, so its EPS (and A * EPS
             // = 0 in composite_pairs) stays finite, and above every x_skip
             float x0 = 128.0f, x1 = 128.0f;
             if (eps_s < 0.0f) {  // FP64 exponent path (uniform per splat)
-                if (b0) x0 = exact_x(e, pcx(), pcy(py0));
-                if (b1) x1 = exact_x(e, pcx(), pcy(py1));
+                if (b0) x0 = exact_x(rec(), pcx(), pcy(py0));
+                if (b1) x1 = exact_x(rec(), pcx(), pcy(py1));
             } else {  // both pixels share the column: one dx, the rest packed (= fast_x per pixel)
                 const float4 m = lds_f4(a_mean + o16);
-                const float dx = __fsub_rn(__fsub_rn(pxc, m.x), m.z);
+                const float dx = __fsub_rn(__fsub_rn(ldsv_f(a_pix + 8), m.x), m.z);
                 const f2 DY = f2_sub(f2_sub(PYC, f2_bc(m.y)), f2_bc(m.w));
                 const f2 U1 = f2_fma(f2_bc(L.x), f2_bc(dx), f2_mul(f2_bc(L.y), DY));
                 const f2 U2 = f2_mul(f2_bc(L.z), DY);
@@ -798,8 +805,8 @@ __global__ void __launch_bounds__(kThreads, 8) raster_fwd_kernel(
             bool p0 = b0 && x0 < x_skip, p1 = b1 && x1 < x_skip;
             const bool band0 = p0 && x0 >= x_keep, band1 = p1 && x1 >= x_keep;
             if (band0 || band1) {  // rare
-                if (band0) p0 = exact_alpha_passes(e, pcx(), pcy(py0));
-                if (band1) p1 = exact_alpha_passes(e, pcx(), pcy(py1));
+                if (band0) p0 = exact_alpha_passes(rec(), pcx(), pcy(py0));
+                if (band1) p1 = exact_alpha_passes(rec(), pcx(), pcy(py1));
             }
             if (!(p0 || p1)) continue;
 #ifdef HGS_CHECKED
