@@ -79,14 +79,16 @@ __device__ __forceinline__ double exact_alpha(const SplatRec& e, double pcx, dou
     return __dmul_rn(e.alpha, exp(-exact_power(e, pcx, pcy)));
 }
 
-// Out-of-line rare paths (keep the FP32 hot loop free of predicated FP64).
-static __device__ __noinline__ float exact_x(const SplatRec* e, double pcx, double pcy) {
+// The rare FP64 paths of the hot loops.  Inlined (in warp-uniform or rare
+// branches): as calls they forced the loop's per-pixel predicates through
+// registers on every iteration (the call ABI keeps no predicate), -1.7% K4.
+static __device__ __forceinline__ float exact_x(const SplatRec* e, double pcx, double pcy) {
     return __double2float_rn(__dmul_rn(exact_power(*e, pcx, pcy), kLog2eD));
 }
-static __device__ __noinline__ bool exact_alpha_passes(const SplatRec* e, double pcx, double pcy) {
+static __device__ __forceinline__ bool exact_alpha_passes(const SplatRec* e, double pcx, double pcy) {
     return !(exact_alpha(*e, pcx, pcy) < kAlphaCutoff);
 }
-static __device__ __noinline__ float2 exact_delta(const SplatRec* e, double pcx, double pcy) {
+static __device__ __forceinline__ float2 exact_delta(const SplatRec* e, double pcx, double pcy) {
     return make_float2((float)__dsub_rn(pcx, e->sx), (float)__dsub_rn(pcy, e->sy));
 }
 
