@@ -359,7 +359,11 @@ __global__ void __launch_bounds__(kPreThreads, 3) preprocess_kernel(
                         c.a[a][b] = cov4(a, b) - r44.div(cross[a] * cross[b]);
                         c.a[b][a] = c.a[a][b];
                     }
-                if (!psd_fast) ok = clamp_psd_slow(c);
+                if (!psd_fast) {  // (a copy: c's address must not escape the hot path,
+                    M3 m = c;      // or it lives in local memory for every Gaussian)
+                    ok = clamp_psd_slow(m);
+                    c = m;
+                }
                 if (!ok) flag |= FLAG_INDEFINITE;
                 if (w < cutoff) {
                     reason = CULL_TEMPORAL;
