@@ -10,7 +10,8 @@ with 3, one of which renders no view).  Checked: the replicas are
 bit-identical after three exchanged iterations in both modes, the sharded
 exchange gives the all-reduce exchange's parameters and (after
 hgs_gather_state) Adam moments, the replicas' summed loss equals one process
-running the 2-view iteration, and a broadcast repairs a diverged replica.
+running the 2-view iteration, a non-finite loss on one rank aborts the same
+iteration on every rank, and a broadcast repairs a diverged replica.
 """
 import multiprocessing as mp
 import os
@@ -91,12 +92,69 @@ def _run_ranks(mode, world, out, errs, tmp):
         c.close()
 
 
+def _run_abort(mode, out, errs):
+    """Rank 1's view of iteration 1 has a NaN ground-truth pixel: the
+    exchanged loss gate makes every rank skip that update and raise
+    NumericAbort for the same iteration (train.cpp:445-447); training then
+    continues in lock step."""
+    import ctypes as C
+    import threading
+
+    from paper_2505_13215_b200 import api as A
+    from paper_2505_13215_b200._capi import NumericAbort
+    from paper_2505_13215_b200.train import DeviceTrainer, shard_batch
+
+    world = 2
+    scene, target, cams, times = _setup()
+    uid = A.Context.comm_unique_id()
+    ctxs = [A.Context(0) for _ in range(world)]
+    trs = [DeviceTrainer(c, scene, cams, times, target=target, bg=(0.2, 0.2, 0.2), iterations=50) for c in ctxs]
+
+    def rank_fn(r):
+        try:
+            ctx, tr = ctxs[r], trs[r]
+            ctx.comm_init(world, r, uid)
+            ctx.set_sharded(mode == "sharded")
+            res = []
+            for i in range(3):
+                batch = [i % 4, (i + 1) % 4]
+                mine = shard_batch(batch, r, world)
+                poison = i == 1 and r == 1
+                if poison:
+                    tr.gt[mine[0]][3, 3, 0] = float("nan")
+                tr.iter += 1
+                DeviceTrainer.step_async(tr, mine, batch_total=len(batch), apply_adam=False)
+                ctx._check(ctx._lib.hgs_train_exchange_async(ctx.handle, C.byref(tr._opts(tr.decay()))))
+                try:
+                    tr.collect()
+                    res.append(("ok", ctx.param_checksum()))
+                except NumericAbort:
+                    tr._pending_n = []
+                    res.append(("abort", ctx.param_checksum()))
+                if poison:
+                    tr.gt[mine[0]][3, 3, 0] = 0.5
+            out[("abort", mode, r)] = res
+        except BaseException as e:
+            errs.append(f"abort {mode} rank {r}: {type(e).__name__}: {e}")
+
+    ts = [threading.Thread(target=rank_fn, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=600)
+    for c in ctxs:
+        c.close()
+
+
 def _child(path):
     out, errs = {}, []
     for mode, world in (("allreduce", 2), ("sharded", 2), ("sharded", 3)):
         _run_ranks(mode, world, out, errs, os.path.dirname(path))
         if errs:
             break
+    for mode in ("allreduce", "sharded"):
+        if not errs:
+            _run_abort(mode, out, errs)
     # one process, no exchange: the first 2-view iteration's loss
     from paper_2505_13215_b200.api import Context
     from paper_2505_13215_b200.train import DeviceTrainer
@@ -158,6 +216,13 @@ def test_two_rank_exchange_loopback(tmp_path):
             assert np.allclose(sh["v"][f], ar["v"][f], rtol=1e-4, atol=1e-12), (world, f)
         for x, y in zip(sh["stats"], ar["stats"]):
             assert np.allclose(x, y, rtol=1e-5, atol=1e-12), world
+    # a non-finite loss on one rank: every rank aborts the same iteration,
+    # keeps the previous parameters, and continues in lock step
+    for mode in ("allreduce", "sharded"):
+        r0, r1 = out[("abort", mode, 0)], out[("abort", mode, 1)]
+        assert r0 == r1, mode
+        assert [k for k, _ in r0] == ["ok", "abort", "ok"], (mode, r0)
+        assert r0[1][1] == r0[0][1] and r0[2][1] != r0[1][1], mode
     # broadcast repair: rank 1 diverged, both end on rank 0's parameters
     b0, a0 = out[("allreduce", 2, 0, "repair")]
     b1, a1 = out[("allreduce", 2, 1, "repair")]
