@@ -46,7 +46,11 @@ static_assert(sizeof(SplatFast) == 64, "SplatFast layout");
 struct __align__(16) CullRec {
     float sx_hi, sy_hi, sx_lo, sy_lo;
     float a, b, c, pcut;
+    // the splat's tile-independent terms of quadrant_mask_bands (gather_sorted)
+    float X_ext, Yc, dyr, inv_a;  // X_ext < 0: the band test does not apply
+    float aP2, det, tol, mB;      // mB = 2e-3 |b| / a (the XR / XL margin's slope)
 };
+static_assert(sizeof(CullRec) == 64, "CullRec layout");
 
 // Per-Gaussian colour record of K1 for the SH backward (K7b): the FP32 view
 // direction, the mask of channels clamped to [0,1] and the Jacobian

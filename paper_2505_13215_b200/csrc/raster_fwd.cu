@@ -22,6 +22,8 @@ void set_debug_terr(float v) { cudaMemcpyToSymbol(g_debug_terr, &v, sizeof(float
 // After the depth sort: gather the exact record into depth order, derive the
 // FP32 fast view (Cholesky of the scaled conic + certified error bound), and
 // emit the tile count of each sorted splat.
+__device__ inline void band_terms(CullRec& e);  // (below, with the band test)
+
 __global__ void __launch_bounds__(256) gather_sorted_kernel(const uint32_t* __restrict__ sorted_gid,
                                                             const uint32_t* __restrict__ V_dev,
                                                             const SplatRec* __restrict__ rec,
@@ -50,6 +52,7 @@ __global__ void __launch_bounds__(256) gather_sorted_kernel(const uint32_t* __re
         cr.b = (float)(0.5 * (e.c01 + e.c10));
         cr.c = (float)e.c11;
         cr.pcut = (float)(log(e.alpha * 255.0) + 1e-5);
+        band_terms(cr);
         cull_rec[j] = cr;
     }
     ntiles_sorted[j] = ntiles[gid];
@@ -149,18 +152,33 @@ __device__ inline bool tile_may_contribute(const CullRec& e, int xa, int xb, int
 // with det >= 1e-3 a c (well conditioned); otherwise (and for
 // non-positive-definite or empty cases) returns false = "use the exact
 // per-quadrant test".
+// The splat's tile-independent terms of the band test (once per splat, in
+// gather_sorted); X_ext < 0 marks conics the test does not apply to
+// (non-positive-definite, ill-conditioned det < 1e-3 a c, empty E).
+__device__ inline void band_terms(CullRec& e) {
+    const float a = e.a, b = e.b, c = e.c;
+    e.X_ext = -1.0f;
+    if (!(a > 0.0f && c > 0.0f)) return;
+    const float det = fmaf(a, c, -b * b);
+    if (!(det >= 1e-3f * a * c)) return;
+    const float P2 = 2.0f * (e.pcut + 1e-5f * (1.0f + 2.0f * fabsf(e.pcut)));
+    if (!(P2 > 0.0f)) return;
+    const float X_ext = sqrtf(P2 * c / det), Y_ext = sqrtf(P2 * a / det);
+    e.X_ext = X_ext;
+    e.Yc = Y_ext * 1.001f + 1e-3f;  // band clip (wider: conservative)
+    e.dyr = -b * X_ext / c;         // dy of the rightmost point of E (leftmost: -dyr)
+    e.inv_a = 1.0f / a;
+    e.aP2 = a * P2;
+    e.det = det;
+    e.tol = 1e-3f * Y_ext + 1e-3f;
+    e.mB = 2e-3f * fabsf(b) * e.inv_a;
+}
+
 __device__ inline bool quadrant_mask_bands(const CullRec& e, int x0, int x1, int y0, int y1, int tx, int ty,
                                            uint32_t& mask) {
-    const float a = e.a, b = e.b, c = e.c;
-    if (!(a > 0.0f && c > 0.0f)) return false;
-    const float det = fmaf(a, c, -b * b);
-    if (!(det >= 1e-3f * a * c)) return false;
-    const float P2 = 2.0f * (e.pcut + 1e-5f * (1.0f + 2.0f * fabsf(e.pcut)));
-    if (!(P2 > 0.0f)) return false;
-    const float X_ext = sqrtf(P2 * c / det), Y_ext = sqrtf(P2 * a / det);
-    const float Yc = Y_ext * 1.001f + 1e-3f;  // band clip (wider: conservative)
-    const float dyr = -b * X_ext / c;         // dy of the rightmost point of E (leftmost: -dyr)
-    const float inv_a = 1.0f / a, aP2 = a * P2;
+    const float X_ext = e.X_ext;
+    if (!(X_ext >= 0.0f)) return false;
+    const float b = e.b, Yc = e.Yc, dyr = e.dyr, inv_a = e.inv_a, aP2 = e.aP2, det = e.det, tol = e.tol;
     mask = 0u;
 #pragma unroll
     for (int qy = 0; qy < 2; ++qy) {
@@ -169,7 +187,6 @@ __device__ inline bool quadrant_mask_bands(const CullRec& e, int x0, int x1, int
         const float y1f = fast_dx((float)ya + 0.5f, e.sy_hi, e.sy_lo), y2f = fast_dx((float)yb + 0.5f, e.sy_hi, e.sy_lo);
         const float lo = fmaxf(y1f, -Yc), hi = fminf(y2f, Yc);
         if (lo > hi) continue;  // the band misses E
-        const float tol = 1e-3f * Y_ext + 1e-3f;
         float XR, XL;
         if (dyr >= lo - tol && dyr <= hi + tol) {
             XR = X_ext;
@@ -183,7 +200,7 @@ __device__ inline bool quadrant_mask_bands(const CullRec& e, int x0, int x1, int
             const float d = fminf(fmaxf(-dyr, lo), hi);
             XL = (-b * d - sqrtf(fmaxf(0.0f, fmaf(-det * d, d, aP2)))) * inv_a;
         }
-        const float m = 2e-3f * (X_ext + fabsf(b) * inv_a * fmaxf(fabsf(lo), fabsf(hi))) + 1e-3f;
+        const float m = fmaf(e.mB, fmaxf(fabsf(lo), fabsf(hi)), 2e-3f * X_ext) + 1e-3f;
         XR += m;
         XL -= m;
 #pragma unroll
