@@ -327,7 +327,7 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
     CK(ctx->ranges.ensure((size_t)n_tiles * sizeof(uint2)));
     CK(ctx->tile_order.ensure((size_t)n_tiles * sizeof(uint32_t)));
     zj.add(ctx->ranges.p, (size_t)n_tiles * sizeof(uint2));
-    if (N > 0) {
+    if (N > 0 && !ctx->skip_gid_map) {  // (the backward's gid -> sorted index map)
         CK(ctx->sorted_of_gid.ensure((size_t)N * 4));
         zj.add(ctx->sorted_of_gid.p, (size_t)N * 4, 0xffffffffu);  // gather writes the visible ones
     }
@@ -386,7 +386,7 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
         prof_begin(ctx, PH_DUPLICATE);
         CK(launch_pdl(gather_sorted_kernel, dim3(div_up((uint32_t)N, 256)), dim3(256), 0, st,
             sorted_gid, &dc->V, ctx->rec.as<SplatRec>(), ctx->ntiles.as<uint32_t>(), ctx->rec_sorted.as<SplatRec>(),
-            ctx->fast_sorted.as<SplatFast>(), ctx->ntiles_sorted.as<uint32_t>(), ctx->sorted_of_gid.as<uint32_t>(),
+            ctx->fast_sorted.as<SplatFast>(), ctx->ntiles_sorted.as<uint32_t>(), ctx->skip_gid_map ? nullptr : ctx->sorted_of_gid.as<uint32_t>(),
             ctx->pcut.as<CullRec>()));
         count_launch();
         CKL();
@@ -867,14 +867,18 @@ hgs_status hgs_render_sweep(hgs_ctx* ctx, int n, const hgs_camera* cams, const d
     };
     int f0 = 0;
     if (ctx->icap == 0) {  // learn the capacity from a synchronous first frame
+        ctx->skip_gid_map = n > 1;
         r = hgs_render_pipeline(ctx, &cams[0], ts[0], bg, opts, 1, 0, &slots[0]);
+        ctx->skip_gid_map = false;
         if (r != HGS_OK) return r;
         ctx->icap = (uint32_t)std::min<int64_t>(INT32_MAX / 2, std::max<int64_t>(4096, ctx->I + ctx->I / 4 + 4096));
         CK(emit(0));
         f0 = 1;
     }
     for (int f = f0; f < n; ++f) {
+        ctx->skip_gid_map = f + 1 < n;  // only the last frame's tape is kept
         r = hgs_render_pipeline(ctx, &cams[f], ts[f], bg, opts, 1, ctx->icap, &slots[f]);
+        ctx->skip_gid_map = false;
         if (r != HGS_OK) return r;
         CK(emit(f));
     }
@@ -889,7 +893,9 @@ hgs_status hgs_render_sweep(hgs_ctx* ctx, int n, const hgs_camera* cams, const d
         ctx->icap = (uint32_t)std::min<int64_t>(INT32_MAX / 2, (int64_t)need + need / 4 + 4096);
         for (int f = 0; f < n; ++f) {
             if (!(hs[f].flags & FLAG_CAPACITY)) continue;
+            ctx->skip_gid_map = f + 1 < n;
             r = hgs_render_pipeline(ctx, &cams[f], ts[f], bg, opts, 1, 0, &slots[f]);
+            ctx->skip_gid_map = false;
             if (r != HGS_OK) return r;
             CK(emit(f));
             CK(cudaMemcpyAsync(&hs[f], &slots[f], sizeof(Counters), cudaMemcpyDeviceToHost, st));

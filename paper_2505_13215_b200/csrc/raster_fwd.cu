@@ -37,7 +37,7 @@ __global__ void __launch_bounds__(256) gather_sorted_kernel(const uint32_t* __re
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= (int)*V_dev) return;
     const uint32_t gid = sorted_gid[j];
-    sorted_of_gid[gid] = (uint32_t)j;
+    if (sorted_of_gid) sorted_of_gid[gid] = (uint32_t)j;  // (null: no backward of this render)
     const SplatRec e = rec[gid];
     rec_sorted[j] = e;
     // tile culling (FP32, conservative): threshold on the power, alpha * exp(-p)
