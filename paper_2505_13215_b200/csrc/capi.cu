@@ -385,7 +385,8 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
         CK(ctx->pcut.ensure((size_t)N * sizeof(CullRec)));
         prof_begin(ctx, PH_DUPLICATE);
         CK(launch_pdl(gather_sorted_kernel, dim3(div_up((uint32_t)N, 256)), dim3(256), 0, st,
-            sorted_gid, &dc->V, ctx->rec.as<SplatRec>(), ctx->ntiles.as<uint32_t>(), ctx->rec_sorted.as<SplatRec>(),
+            sorted_gid, &dc->V, ctx->rec.as<SplatRec>(), ctx->ntiles.as<uint32_t>(),
+            ctx->skip_gid_map ? nullptr : ctx->rec_sorted.as<SplatRec>(),
             ctx->fast_sorted.as<SplatFast>(), ctx->ntiles_sorted.as<uint32_t>(), ctx->skip_gid_map ? nullptr : ctx->sorted_of_gid.as<uint32_t>(),
             ctx->pcut.as<CullRec>()));
         count_launch();
@@ -537,11 +538,13 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
 #endif
     prof_begin(ctx, PH_RASTER_FWD);
     launch_raster_fwd(
-        want_count, n_tiles, st, ctx->ranges.as<uint2>(), inst_vals, ctx->fast_sorted.as<SplatFast>(), ctx->rec_sorted.as<SplatRec>(), W, H,
+        want_count, n_tiles, st, ctx->ranges.as<uint2>(), inst_vals, ctx->fast_sorted.as<SplatFast>(),
+        ctx->skip_gid_map ? ctx->rec.as<SplatRec>() : ctx->rec_sorted.as<SplatRec>(), W, H,
         tiles_x, (float)bg[0], (float)bg[1], (float)bg[2], ctx->img.as<float>(), ctx->last.as<uint32_t>(),
         ctx->tfinal.as<float>(), want_trans ? ctx->trans.as<float>() : nullptr, want_count ? ctx->count.as<uint32_t>() : nullptr,
         ctx->fix_list.as<uint32_t>(), &dc->fix_count, tile_order_enabled() ? ctx->tile_order.as<uint32_t>() : nullptr,
-        bg[0], bg[1], bg[2], ctx->fix_cout.as<double>(), ctx->fix_slot.as<uint32_t>());
+        bg[0], bg[1], bg[2], ctx->fix_cout.as<double>(), ctx->fix_slot.as<uint32_t>(),
+        ctx->skip_gid_map ? ctx->sorted_gid : nullptr);
     count_launch();
     CKL();
     prof_end(ctx);

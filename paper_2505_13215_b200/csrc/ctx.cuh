@@ -160,7 +160,8 @@ struct hgs_ctx {
     hgs::DBuf tile_order;  // the rasterizers' tile launch order (heaviest first; K4 and K6)
     hgs::DBuf dbg_k, dbg_v;         // the reference's full sorted instance list (debug / count_map)
     bool debug_full_list = false;   // hgs_debug_keep_instances
-    bool skip_gid_map = false;  // render sweeps: frames whose tape is not kept need no gid -> sorted map
+    bool skip_gid_map = false;  // render sweeps: a frame whose tape is not kept writes no gid -> sorted
+                                // map and no depth-ordered SplatRec copy (K4 reads rec through the depth order)
     hgs::DBuf counters;  // [0..5] stats u64, [6] flags, fix_count, totals...
     hgs::DBuf img, last, tfinal, trans, count, fix_list;
     hgs::DBuf fix_cout;  // FP64 colours of the fix-up pixels (forward fix-up -> exact backward)

@@ -48,7 +48,8 @@ void launch_raster_fwd(bool count_map, int n_tiles, cudaStream_t st, const uint2
                        const SplatFast* fast, const SplatRec* exact, int W, int H, int tiles_x, float bg_r, float bg_g,
                        float bg_b, float* out_rgb, uint32_t* out_last, float* out_tfinal, float* out_trans,
                        uint32_t* out_count, uint32_t* fix_list, uint32_t* fix_count, uint32_t* tile_order,
-                       double bg_rd, double bg_gd, double bg_bd, double* out_cout, uint32_t* fix_slot);
+                       double bg_rd, double bg_gd, double bg_bd, double* out_cout, uint32_t* fix_slot,
+                       const uint32_t* remap = nullptr);
 
 
 __global__ void grads_pack_kernel(const float* __restrict__ gbuf, int64_t off_g3, int64_t off_dgn4, int rows4,

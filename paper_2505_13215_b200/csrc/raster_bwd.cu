@@ -171,7 +171,7 @@ static __device__ __noinline__ void exact_bwd_pixel(int pix, uint2 rg, const dou
         constexpr int S = kExactSub;
         for (uint32_t base = rg.x; base < last; base += 32 * S) {
             ExactChunk<S> c;
-            exact_chunk<S>(inst_val, exact, base, last, px, py, pcx, pcy, T, s_om, c);
+            exact_chunk<S>(inst_val, exact, nullptr, base, last, px, py, pcx, pcy, T, s_om, c);
 #pragma unroll
             for (int s = 0; s < S; ++s) {
                 double wc[3] = {0.0, 0.0, 0.0}, w = 0.0, rgb[3] = {0.0, 0.0, 0.0};

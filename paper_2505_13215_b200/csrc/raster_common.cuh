@@ -341,7 +341,8 @@ struct ExactChunk {
 
 template <int S>
 __device__ __forceinline__ void exact_chunk(const uint32_t* __restrict__ inst_val, const SplatRec* __restrict__ exact,
-                                            uint32_t base, uint32_t end, int px, int py, double pcx, double pcy,
+                                            const uint32_t* __restrict__ remap, uint32_t base, uint32_t end, int px,
+                                            int py, double pcx, double pcy,
                                             double& T, double* s_om, ExactChunk<S>& c) {
     const int lane = threadIdx.x & 31;
     uint32_t v[S];
@@ -356,7 +357,9 @@ __device__ __forceinline__ void exact_chunk(const uint32_t* __restrict__ inst_va
 #pragma unroll
     for (int s = 0; s < S; ++s) {
         HGS_DCHECK(v[s] == 0xffffffffu || (v[s] & kInstIndexMask) < g_chk.splats);
-        c.e[s] = v[s] != 0xffffffffu ? exact + (v[s] & kInstIndexMask) : nullptr;
+        // remap (render sweeps): the records are indexed by Gaussian, not by sorted splat
+        c.e[s] = v[s] == 0xffffffffu ? nullptr
+                 : exact + (remap ? __ldg(remap + (v[s] & kInstIndexMask)) : (v[s] & kInstIndexMask));
         c.a[s] = -1.0;
         c.g[s] = 0.0;
         c.Ti[s] = 0.0;

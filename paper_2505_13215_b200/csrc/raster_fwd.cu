@@ -39,7 +39,7 @@ __global__ void __launch_bounds__(256) gather_sorted_kernel(const uint32_t* __re
     const uint32_t gid = sorted_gid[j];
     if (sorted_of_gid) sorted_of_gid[gid] = (uint32_t)j;  // (null: no backward of this render)
     const SplatRec e = rec[gid];
-    rec_sorted[j] = e;
+    if (rec_sorted) rec_sorted[j] = e;  // (null: sweep frame without a tape; K4 reads rec via the depth order)
     // tile culling (FP32, conservative): threshold on the power, alpha * exp(-p)
     // >= 1/255 <=> p <= ln(255 alpha) (+1e-5 margin, see tile_may_contribute)
     {
@@ -561,7 +561,8 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // q: the pixel's fix-list slot (its FP64 colour goes to out_cout[q] for
 // raster_bwd_exact_kernel).  Out of line: K4 calls it after its main loop.
 static __device__ __noinline__ void fixup_pixel(uint32_t q, int pix, uint2 rg, const uint32_t* __restrict__ inst_val,
-                                               const SplatRec* __restrict__ exact, int W, double bg_r, double bg_g,
+                                               const SplatRec* __restrict__ exact, const uint32_t* __restrict__ remap,
+                                               int W, double bg_r, double bg_g,
                                                double bg_b, float* __restrict__ out_rgb, uint32_t* __restrict__ out_last,
                                                float* __restrict__ out_tfinal, float* __restrict__ out_trans,
                                                uint32_t* __restrict__ out_count, double* __restrict__ out_cout,
@@ -576,7 +577,7 @@ static __device__ __noinline__ void fixup_pixel(uint32_t q, int pix, uint2 rg, c
     constexpr int S = kExactSub;
     for (uint32_t base = rg.x; base < rg.y; base += 32 * S) {
         ExactChunk<S> c;
-        exact_chunk<S>(inst_val, exact, base, rg.y, px, py, pcx, pcy, T, s_om, c);
+        exact_chunk<S>(inst_val, exact, remap, base, rg.y, px, py, pcx, pcy, T, s_om, c);
         double wr = 0.0, wg = 0.0, wb = 0.0;
 #pragma unroll
         for (int s = 0; s < S; ++s) {
@@ -703,7 +704,7 @@ __global__ void __launch_bounds__(kThreads, 8) raster_fwd_kernel(
     float* __restrict__ out_rgb, uint32_t* __restrict__ out_last, float* __restrict__ out_tfinal,
     float* __restrict__ out_trans, uint32_t* __restrict__ out_count, uint32_t* __restrict__ fix_list,
     uint32_t* __restrict__ fix_count, const uint32_t* __restrict__ tile_order, double bg_rd, double bg_gd,
-    double bg_bd, double* __restrict__ out_cout, uint32_t* __restrict__ fix_slot) {
+    double bg_bd, double* __restrict__ out_cout, uint32_t* __restrict__ fix_slot, const uint32_t* __restrict__ remap) {
     pdl_wait();  // launched with launch_pdl
     __shared__ SplatBatch<kBatch> sb;
     __shared__ uint32_t s_nfix;  // the CTA's pixels handed to the FP64 fix-up
@@ -799,7 +800,10 @@ __global__ void __launch_bounds__(kThreads, 8) raster_fwd_kernel(
 #endif
             const float4 L = lds_f4(a_chol + o16), c = lds_f4(a_col + o16);
             // the exact record (rare paths only: loaded there)
-            auto rec = [&] { return exact + lds_u32(a_j + o4); };
+            auto rec = [&] {
+                const uint32_t j = lds_u32(a_j + o4);
+                return exact + (remap ? __ldg(remap + j) : j);
+            };
             const float eps_s = __int_as_float(hdr.w);
             // a pixel outside the box keeps x = 128: finite, so its EPS (and A * EPS
             // = 0 in composite_pairs) stays finite, and above every x_skip
@@ -869,7 +873,7 @@ __global__ void __launch_bounds__(kThreads, 8) raster_fwd_kernel(
     double* s_om = reinterpret_cast<double*>(&sb.mean[0]) + warp * (32 * kExactSub);
     for (uint32_t k = warp; k < nfix; k += kThreads / 32) {
         const uint2 f = s_fix[k];
-        fixup_pixel(f.y, (int)f.x, rg, inst_val, exact, W, bg_rd, bg_gd, bg_bd, out_rgb, out_last, out_tfinal,
+        fixup_pixel(f.y, (int)f.x, rg, inst_val, exact, remap, W, bg_rd, bg_gd, bg_bd, out_rgb, out_last, out_tfinal,
                     out_trans, out_count, out_cout, s_om);
     }
 }
@@ -879,7 +883,8 @@ void launch_raster_fwd(bool count_map, int n_tiles, cudaStream_t st, const uint2
                        const SplatFast* fast, const SplatRec* exact, int W, int H, int tiles_x, float bg_r, float bg_g,
                        float bg_b, float* out_rgb, uint32_t* out_last, float* out_tfinal, float* out_trans,
                        uint32_t* out_count, uint32_t* fix_list, uint32_t* fix_count, uint32_t* tile_order,
-                       double bg_rd, double bg_gd, double bg_bd, double* out_cout, uint32_t* fix_slot) {
+                       double bg_rd, double bg_gd, double bg_bd, double* out_cout, uint32_t* fix_slot,
+                       const uint32_t* remap) {
     if (tile_order) {
         launch_pdl(tile_order_kernel, dim3(1), dim3(1024), 0, st, ranges, n_tiles, tile_order);
         count_launch();
@@ -888,11 +893,11 @@ void launch_raster_fwd(bool count_map, int n_tiles, cudaStream_t st, const uint2
     if (count_map)
         launch_pdl(raster_fwd_kernel<true>, dim3(n_tiles), dim3(kThreads), 0, st, ranges, inst_val, fast, exact, W, H,
                    tiles_x, bg_r, bg_g, bg_b, out_rgb, out_last, out_tfinal, out_trans, out_count, fix_list,
-                   fix_count, order, bg_rd, bg_gd, bg_bd, out_cout, fix_slot);
+                   fix_count, order, bg_rd, bg_gd, bg_bd, out_cout, fix_slot, remap);
     else
         launch_pdl(raster_fwd_kernel<false>, dim3(n_tiles), dim3(kThreads), 0, st, ranges, inst_val, fast, exact, W,
                    H, tiles_x, bg_r, bg_g, bg_b, out_rgb, out_last, out_tfinal, out_trans, out_count, fix_list,
-                   fix_count, order, bg_rd, bg_gd, bg_bd, out_cout, fix_slot);
+                   fix_count, order, bg_rd, bg_gd, bg_bd, out_cout, fix_slot, remap);
 }
 
 // ---- density_map (raster.cpp:268-287)
