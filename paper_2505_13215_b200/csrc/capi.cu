@@ -350,7 +350,8 @@ hgs_status hgs_render_pipeline(hgs_ctx* ctx, const hgs_camera* cam, double t, co
         CK(ctx->scan_ws.ensure(scan_workspace_bytes(N) + 4096));
         prof_begin(ctx, PH_PREPROCESS);
         CK(preprocess_setup());
-        CK(launch_pdl(preprocess_kernel, dim3(div_up(N, 256)), dim3(256), preprocess_smem_bytes(ctx->deg), st,
+        CK(launch_pdl(ctx->skip_gid_map ? preprocess_render_kernel : preprocess_kernel, dim3(div_up(N, 256)),
+                      dim3(256), preprocess_smem_bytes(ctx->deg), st,
                       static_cast<const float*>(ctx->p4.as<float>()), ctx->cap4, n4,
                       static_cast<const float*>(ctx->p3.as<float>()), ctx->cap3, n3, ctx->deg, ctx->cam, t, cutoff,
                       tiles_x, ctx->rec.as<SplatRec>(), ctx->depth_key.as<uint32_t>(), ctx->ntiles.as<uint32_t>(),
@@ -807,7 +808,7 @@ hgs_status hgs_density_map(hgs_ctx* ctx, const hgs_camera* cam, double t, int dy
         CK(ctx->ntiles.ensure((size_t)N * 4));
         CK(ctx->shdir.ensure((size_t)N * sizeof(ShRec)));
         CK(preprocess_setup());
-        preprocess_kernel<<<div_up(N, 256), 256, preprocess_smem_bytes(ctx->deg), st>>>(
+        preprocess_render_kernel<<<div_up(N, 256), 256, preprocess_smem_bytes(ctx->deg), st>>>(
             ctx->p4.as<float>(), ctx->cap4, n4, ctx->p3.as<float>(), ctx->cap3, n3, ctx->deg, to_dev(cam), t,
             weight_cutoff, tiles_x, ctx->rec.as<SplatRec>(), ctx->depth_key.as<uint32_t>(), ctx->ntiles.as<uint32_t>(),
             dc->stats, &dc->flags, ctx->shdir.as<ShRec>());

@@ -11,6 +11,13 @@ __global__ void preprocess_kernel(const float* __restrict__ p4, int64_t cap4, in
                                   SplatRec* __restrict__ rec, uint32_t* __restrict__ depth_key,
                                   uint32_t* __restrict__ ntiles_out, unsigned long long* __restrict__ stats,
                                   uint32_t* __restrict__ flags, ShRec* __restrict__ shrec);
+// the same without the backward's ShRec (render-only frames)
+__global__ void preprocess_render_kernel(const float* __restrict__ p4, int64_t cap4, int n4,
+                                         const float* __restrict__ p3, int64_t cap3, int n3, int deg, DevCamera cam,
+                                         double t, double cutoff, int tiles_x, SplatRec* __restrict__ rec,
+                                         uint32_t* __restrict__ depth_key, uint32_t* __restrict__ ntiles_out,
+                                         unsigned long long* __restrict__ stats, uint32_t* __restrict__ flags,
+                                         ShRec* __restrict__ shrec);
 
 size_t preprocess_smem_bytes(int deg);  // dynamic shared memory of a preprocess_kernel launch
 cudaError_t preprocess_setup();         // opt-in to > 48 KB dynamic shared memory (once per process)

@@ -230,21 +230,33 @@ __global__ void preprocess_kernel(const float* __restrict__ p4, int64_t cap4, in
                                   SplatRec* __restrict__ rec, uint32_t* __restrict__ depth_key,
                                   uint32_t* __restrict__ ntiles_out, unsigned long long* __restrict__ stats,
                                   uint32_t* __restrict__ flags, ShRec* __restrict__ shrec);
+__global__ void preprocess_render_kernel(const float* __restrict__ p4, int64_t cap4, int n4,
+                                         const float* __restrict__ p3, int64_t cap3, int n3, int deg, DevCamera cam,
+                                         double t, double cutoff, int tiles_x, SplatRec* __restrict__ rec,
+                                         uint32_t* __restrict__ depth_key, uint32_t* __restrict__ ntiles_out,
+                                         unsigned long long* __restrict__ stats, uint32_t* __restrict__ flags,
+                                         ShRec* __restrict__ shrec);
 cudaError_t preprocess_setup() {  // the attribute is per device: set it once on each
     static std::atomic<unsigned long long> done{0};
     int dev = 0;
     cudaGetDevice(&dev);
     const unsigned long long bit = 1ull << (dev & 63);
     if (done.load() & bit) return cudaSuccess;
-    const cudaError_t e = cudaFuncSetAttribute(preprocess_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               (int)preprocess_smem_bytes(3));
+    cudaError_t e = cudaFuncSetAttribute(preprocess_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)preprocess_smem_bytes(3));
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(preprocess_render_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)preprocess_smem_bytes(3));
     if (e == cudaSuccess) done.fetch_or(bit);
     return e;
 }
 
 // K1.  stats[0..5] = culled_depth, culled_offscreen, culled_degenerate,
-// culled_temporal, degenerate_temporal, projected.
-__global__ void __launch_bounds__(kPreThreads, 3) preprocess_kernel(
+// culled_temporal, degenerate_temporal, projected.  kTape: also the SH
+// colour's direction Jacobian and clamp mask for the backward (ShRec);
+// render sweep frames whose tape is not kept skip them.
+template <bool kTape>
+__device__ __forceinline__ void preprocess_body(
     const float* __restrict__ p4, int64_t cap4, int n4, const float* __restrict__ p3, int64_t cap3,
     int n3, int deg, DevCamera cam, double t, double cutoff, int tiles_x, SplatRec* __restrict__ rec,
     uint32_t* __restrict__ depth_key, uint32_t* __restrict__ ntiles_out,
@@ -434,14 +446,14 @@ __global__ void __launch_bounds__(kPreThreads, 3) preprocess_kernel(
                 for (int kk = 0; kk < 4; ++kk) {
                     const int k = k0 + kk;
                     if (k >= K) continue;
-                    float f[3];
-                    sh_dir_factor(k, x, y, z, f);
+                    float f[3] = {0.f, 0.f, 0.f};
+                    if (kTape) sh_dir_factor(k, x, y, z, f);
 #pragma unroll
                     for (int c = 0; c < 3; ++c) {
                         acc[c] = fmaf(basis[k], w[kk][c], acc[c]);
 #pragma unroll
                         for (int j = 0; j < 3; ++j)
-                            if (sh_dir_nonzero(k, j)) jg[c][j] = __fmaf_rn(f[j], w[kk][c], jg[c][j]);
+                            if (kTape && sh_dir_nonzero(k, j)) jg[c][j] = __fmaf_rn(f[j], w[kk][c], jg[c][j]);
                     }
                 }
             }
@@ -455,7 +467,7 @@ __global__ void __launch_bounds__(kPreThreads, 3) preprocess_kernel(
                 sr.j[c] = make_float4(jg[c][0], jg[c][1], jg[c][2], 0.f);
             }
             sr.dir = make_float4(fd[0], fd[1], fd[2], __uint_as_float(clamped));
-            shrec[gid] = sr;
+            if (kTape) shrec[gid] = sr;
             s.alpha = alpha;
             s.alpha_f = (float)alpha;
             s.r = rgb[0];
@@ -495,6 +507,21 @@ __global__ void __launch_bounds__(kPreThreads, 3) preprocess_kernel(
     }
     const unsigned fb = __reduce_or_sync(full, flag);
     if ((threadIdx.x & 31) == 0 && fb) atomicOr(flags, fb);
+}
+
+#define HGS_K1_PARAMS                                                                                         \
+    const float *__restrict__ p4, int64_t cap4, int n4, const float *__restrict__ p3, int64_t cap3, int n3, \
+        int deg, DevCamera cam, double t, double cutoff, int tiles_x, SplatRec *__restrict__ rec,           \
+        uint32_t *__restrict__ depth_key, uint32_t *__restrict__ ntiles_out,                                \
+        unsigned long long *__restrict__ stats, uint32_t *__restrict__ flags, ShRec *__restrict__ shrec
+#define HGS_K1_ARGS p4, cap4, n4, p3, cap3, n3, deg, cam, t, cutoff, tiles_x, rec, depth_key, ntiles_out, stats, flags, shrec
+
+__global__ void __launch_bounds__(kPreThreads, 3) preprocess_kernel(HGS_K1_PARAMS) {
+    preprocess_body<true>(HGS_K1_ARGS);
+}
+// render-only (sweep frames without a kept tape; density maps): no ShRec
+__global__ void __launch_bounds__(kPreThreads, 3) preprocess_render_kernel(HGS_K1_PARAMS) {
+    preprocess_body<false>(HGS_K1_ARGS);
 }
 
 }  // namespace hgs
