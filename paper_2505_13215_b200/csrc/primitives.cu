@@ -166,7 +166,9 @@ struct CoopSort {
     uint32_t* rowsum;  // [256]
 };
 
-__global__ void __launch_bounds__(kCoopThreads) radix_sort_coop_kernel(CoopSort a) {
+// (3 blocks/SM, 80 registers: at configs[4] sizes the passes are latency
+// bound at 2 blocks/SM -- 97 registers -- and 4 (64, spilling) measured slower)
+__global__ void __launch_bounds__(kCoopThreads, 3) radix_sort_coop_kernel(CoopSort a) {
     asm volatile("griddepcontrol.wait;" ::: "memory");  // launched as a programmatic dependent (coop_launch)
     cg::grid_group grid = cg::this_grid();
     __shared__ uint32_t h[256];
