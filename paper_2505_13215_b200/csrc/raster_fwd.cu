@@ -323,7 +323,9 @@ __device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned l
 // and writes only the kept (tile key, value) pairs -- in the reference's
 // order, without materialising the full instance list.  status: one 64-bit
 // (flag << 32 | count) word per tile, zeroed before the launch.
-__global__ void __launch_bounds__(kDupThreads) duplicate_compact_kernel(
+// (8 CTAs/SM, 32 registers: latency-bound on the per-instance loads and the
+// look-back; full occupancy beats the spills -- -2% at c2 and c5 vs 48 registers)
+__global__ void __launch_bounds__(kDupThreads, 8) duplicate_compact_kernel(
     const SplatFast* __restrict__ fast, int V, const uint32_t* __restrict__ offsets, int tiles_x,
     const CullRec* __restrict__ cull_rec, const uint32_t* __restrict__ cta_first, int I,
     uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out, uint32_t* __restrict__ kept_total,
