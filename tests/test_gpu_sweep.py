@@ -114,3 +114,32 @@ def test_repeated_sweeps_are_bit_identical(ctx):
         got, stats = ctx.render_sweep([cam] * 40, [0.5] * 40, (0.2, 0.2, 0.2), out="host", with_stats=True)
         assert all(np.array_equal(g, ref[0]) for g in got)
         assert all(s == ref_stats[0] for s in stats)
+
+
+@pytest.mark.parametrize("overflow", [False, True])
+def test_backward_after_a_sweep_uses_the_last_frame(ctx, overflow):
+    """A sweep keeps only the last frame's tape (the earlier frames skip the
+    backward-only outputs: the gid -> sorted map, the depth-ordered records,
+    K1's SH Jacobian): hgs_backward right after the sweep gives the gradients
+    of a plain render of that frame -- also when capacity overflows made
+    the sweep re-render frames."""
+    scene = synthetic_scene(20000, 10000, sh_degree=2, seed=18).as_float32_exact()
+    ctx.upload(scene)
+    cams = [ring_camera(18, 160, 120, index=i % 5, n_ring=5) for i in range(5)]
+    ts = [0.1, 0.3, 0.5, 0.7, 0.9]
+    bg = (0.2, 0.2, 0.2)
+    w = np.random.default_rng(18).uniform(-1, 1, (120, 160, 3))
+    ctx.forward_train(cams[-1], ts[-1], bg)
+    ctx.zero_grads()
+    ctx.backward(w)
+    ref = ctx.grads()
+    ctx.render(cams[0], ts[0], bg)  # a different frame's tape, so stale state would show
+    if overflow:
+        ctx._check(ctx._lib.hgs_debug_set_sweep_capacity(ctx.handle, 1024))  # every frame overflows: redone
+    ctx.render_sweep(cams, ts, bg)
+    ctx.zero_grads()
+    ctx.backward(w)
+    got = ctx.grads()
+    for f in ("mean_x", "mean_t", "ql", "log_s4", "op4", "sh4", "mean3", "quat3", "op3", "sh3"):
+        a, b = np.asarray(got[f]), np.asarray(ref[f])
+        assert np.allclose(a, b, rtol=1e-5, atol=1e-7 * max(1e-30, np.abs(b).max())), f
